@@ -1,0 +1,189 @@
+/*
+ * terralio_gpu.h — C-ABI of the B200-native RBF terrain hot path.
+ *
+ * This is the drop-in boundary between the reference's C++ class API
+ * (terralio::terrain::TerrainModel & friends, /root/reference/proj/core) and
+ * the sm_100a kernels in paper_2509_26222_b200/csrc. Plain C: opaque
+ * handles, plain pointers + sizes, int status codes; no CUDA, torch or Eigen
+ * types. A C++ shim (include/terralio_b200/*.hpp) and a ctypes binding
+ * (paper_2509_26222_b200/_abi.py) rebuild the reference interface on top of
+ * it; INTEGRATION.md shows the binding a proj/core maintainer adds.
+ *
+ * Conventions
+ *  - Arrays are SoA `double*` (x[], y[], z[] …). Each data entry point takes
+ *    a tlg_mem tag saying whether its pointers are host or device memory;
+ *    host buffers are staged through pinned memory inside the call.
+ *  - Status codes map 1:1 onto the reference's exceptions (see tlg_status);
+ *    tlg_last_error() returns the thread's last message.
+ *  - All device work is enqueued on the context's CUDA stream. Entry points
+ *    that return host-visible results synchronise that stream.
+ *  - There is no CPU fallback: every numeric result comes from a kernel;
+ *    calls fail with TLG_CUDA_ERROR when no sm_100 device is present.
+ *  - Jacobian rows use Eigen's column-major rows x 6 layout
+ *    (CostEval::jacobian, scan_matcher.hpp:75): J[c * n + i].
+ */
+#ifndef TERRALIO_GPU_H_
+#define TERRALIO_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TLG_ABI_VERSION 1
+
+typedef enum tlg_status {
+  TLG_OK = 0,
+  TLG_INVALID_ARGUMENT = 1,     /* std::invalid_argument (kernel.cpp:18-24, center_select.cpp:10-15,22-24) */
+  TLG_DOMAIN_ERROR = 2,         /* std::domain_error (kernel.cpp:29-31, terrain_model.cpp:98) */
+  TLG_NO_SUPPORTED_CENTERS = 3, /* terrain::NoSupportedCenters (center_select.hpp:30-32) */
+  TLG_RUNTIME_ERROR = 4,        /* std::runtime_error (terrain_model.cpp:289-295, snapshot.cpp) */
+  TLG_CUDA_ERROR = 5,
+  TLG_OUT_OF_MEMORY = 6,
+  TLG_BUFFER_TOO_SMALL = 7
+} tlg_status;
+
+typedef enum tlg_mem { TLG_HOST = 0, TLG_DEVICE = 1 } tlg_mem;
+
+/* terrain::KernelParams (kernel.hpp:12-24). */
+typedef struct tlg_kernel_params {
+  double sigma;         /* default 0.04 */
+  double sigma_eps;     /* default 0.1  */
+  double lambda;        /* default 1e-3 */
+  double cutoff_radius; /* 0 = auto: max(cfg, 3 sigma_tilde) after finalize */
+} tlg_kernel_params;
+
+/* terrain::CenterSet minus the centre list (center_select.hpp:22-28). */
+typedef struct tlg_center_params {
+  double mesh_resolution;
+  double accept_radius;
+  int32_t accept_count;
+  int32_t reserved;
+  double roi_min_x, roi_min_y, roi_max_x, roi_max_y;
+} tlg_center_params;
+
+/* terrain::UpdateReport (terrain_model.hpp:21-26) + which solver ran. */
+typedef struct tlg_update_report {
+  uint64_t active_blocks;
+  uint64_t active_centers;
+  uint64_t born_centers;
+  int32_t rejected;     /* inner solve failed; births persist, weights/blocks unchanged */
+  int32_t solver;       /* 1 = one-shot Woodbury (m x m), 2 = information form (n x n) */
+} tlg_update_report;
+
+/* Normal-equation block of the stacked manifold rows
+ * (scan_matcher.cpp:296-299 A = J^T J, g = J^T r; :253 cost = |r|^2). */
+typedef struct tlg_normal_eq {
+  double A[21];   /* upper triangle of J^T J, row-major (i <= j) */
+  double g[6];    /* J^T r */
+  double cost;    /* sum r^2 */
+  double valid;   /* number of supported (valid) rows */
+} tlg_normal_eq;
+
+typedef struct tlg_ctx tlg_ctx;
+typedef struct tlg_model tlg_model;
+
+/* ---- library / context ---------------------------------------------------- */
+int tlg_abi_version(void);
+const char* tlg_last_error(void);
+/* device = CUDA ordinal; stream = cudaStream_t or NULL for a private stream. */
+tlg_status tlg_ctx_create(int device, void* stream, tlg_ctx** out);
+tlg_status tlg_ctx_destroy(tlg_ctx* ctx);
+tlg_status tlg_ctx_set_stream(tlg_ctx* ctx, void* stream);
+tlg_status tlg_ctx_synchronize(tlg_ctx* ctx);
+/* Number of kernels this context has launched (bench launch accounting). */
+uint64_t tlg_ctx_launch_count(const tlg_ctx* ctx);
+
+/* ---- kernel.cpp ------------------------------------------------------------- */
+/* KernelParams::finalize (kernel.cpp:15-25): fills the auto cutoff, validates. */
+tlg_status tlg_kernel_finalize(tlg_kernel_params* p);
+
+/* ---- center_select.cpp ------------------------------------------------------ */
+/* supported_mesh_nodes (center_select.cpp:18-62): lattice nodes of `roi`
+ * (i outer, j inner) with >= accept_count observation points within
+ * accept_radius. Bit-exact node coordinates and order. z is only validated
+ * (TerrainObservation::validate, :9-16). out_* in out_mem; *out_n always set;
+ * TLG_BUFFER_TOO_SMALL when *out_n > cap. */
+tlg_status tlg_supported_mesh_nodes(tlg_ctx* ctx, const double* x, const double* y,
+                                    const double* z, size_t m, size_t z_len, tlg_mem in_mem,
+                                    const tlg_center_params* params, double* out_x,
+                                    double* out_y, size_t cap, size_t* out_n,
+                                    tlg_mem out_mem);
+/* select_centers (center_select.cpp:64-76): as above, TLG_NO_SUPPORTED_CENTERS
+ * when empty. */
+tlg_status tlg_select_centers(tlg_ctx* ctx, const double* x, const double* y, const double* z,
+                              size_t m, size_t z_len, tlg_mem in_mem,
+                              const tlg_center_params* params, double* out_x, double* out_y,
+                              size_t cap, size_t* out_n, tlg_mem out_mem);
+
+/* ---- TerrainModel ------------------------------------------------------------ */
+/* TerrainModel(kernel, centers) (terrain_model.cpp:26-44). */
+tlg_status tlg_model_create(tlg_ctx* ctx, const tlg_kernel_params* kernel,
+                            const tlg_center_params* centers, const double* cx,
+                            const double* cy, size_t n, tlg_mem mem, tlg_model** out);
+tlg_status tlg_model_destroy(tlg_model* model);
+tlg_status tlg_model_counts(const tlg_model* model, size_t* num_centers, size_t* num_blocks);
+tlg_status tlg_model_kernel(const tlg_model* model, tlg_kernel_params* out);
+tlg_status tlg_model_center_params(const tlg_model* model, tlg_center_params* out);
+tlg_status tlg_model_get_centers(tlg_model* model, double* cx, double* cy, tlg_mem mem);
+tlg_status tlg_model_get_weights(tlg_model* model, double* w, tlg_mem mem);
+tlg_status tlg_model_set_weights(tlg_model* model, const double* w, tlg_mem mem);
+tlg_status tlg_model_get_block_index(tlg_model* model, uint32_t* out, tlg_mem mem);
+tlg_status tlg_model_block_size(const tlg_model* model, uint32_t block, size_t* n);
+tlg_status tlg_model_get_block_members(const tlg_model* model, uint32_t block, uint32_t* out);
+/* block_info_inverse(b): bn x bn column-major. */
+tlg_status tlg_model_get_block_info_inverse(tlg_model* model, uint32_t block, double* out,
+                                            tlg_mem mem);
+tlg_status tlg_model_set_block_info_inverse(tlg_model* model, uint32_t block,
+                                            const double* in, tlg_mem mem);
+
+/* predict_height / predict_gradient (terrain_model.cpp:109-143), batched:
+ * z[i] (0 when unsupported), supported[i] (1/0), grad_x/grad_y[i]. Any output
+ * may be NULL. Non-finite queries: TLG_DOMAIN_ERROR (kernel.cpp:29-31). */
+tlg_status tlg_eval(tlg_model* model, const double* x, const double* y, size_t n,
+                    tlg_mem in_mem, double* z, uint8_t* supported, double* grad_x,
+                    double* grad_y, tlg_mem out_mem);
+
+/* moment_feature (terrain_model.cpp:97-107), batched as CSR over queries:
+ * row_ptr[n+1], ids ascending per row, vals = s * kappa_sigma_tilde. */
+tlg_status tlg_moment_features(tlg_model* model, const double* x, const double* y, size_t n,
+                               tlg_mem in_mem, uint32_t* row_ptr, uint32_t* ids, double* vals,
+                               size_t cap, size_t* nnz, tlg_mem out_mem);
+
+/* Manifold soft-constraint rows, batched generalisation of
+ * kin::manifold_residual/jacobian (contact.cpp:7-39) with the total_cost
+ * weighting (scan_matcher.cpp:221-248): for lever arm h_i,
+ *   xi = R h_i + t,  raw_i = xi_z - wheel_radius - f(xi_xy),
+ *   J_i = [-df/dx, -df/dy, 1] [-R hat(h_i), I3],
+ *   w_i = sqrt(huber/|raw|) if huber > 0 and |raw| > huber else 1,
+ *   r_i = sqrt(lambda_M) w_i raw_i,  J row scaled alike; unsupported -> zero row.
+ * R row-major 3x3 and t[3] are host arrays. Outputs r, J (J[c*n+i]), valid,
+ * raw may be NULL; `ne` (host, may be NULL) receives the fused reduction. */
+tlg_status tlg_manifold_rows(tlg_model* model, const double R[9], const double t[3],
+                             const double* hx, const double* hy, const double* hz, size_t n,
+                             tlg_mem in_mem, double wheel_radius, double lambda_M,
+                             double huber_delta, double* r, double* J, uint8_t* valid,
+                             double* raw, tlg_mem out_mem, tlg_normal_eq* ne);
+
+/* recursive_update(obs, allow_birth) (terrain_model.cpp:145-253). */
+tlg_status tlg_recursive_update(tlg_model* model, const double* x, const double* y,
+                                const double* z, size_t m, size_t z_len, tlg_mem in_mem,
+                                int allow_birth, tlg_update_report* report);
+
+/* fit_batch_ridge (terrain_model.cpp:269-308). */
+tlg_status tlg_fit_batch_ridge(tlg_ctx* ctx, const tlg_kernel_params* kernel,
+                               const tlg_center_params* centers, const double* cx,
+                               const double* cy, size_t n, const double* x, const double* y,
+                               const double* z, size_t m, size_t z_len, tlg_mem mem,
+                               tlg_model** out);
+
+/* RBFT v1 snapshot (snapshot.cpp:7-126), byte-identical layout. */
+tlg_status tlg_model_save(tlg_model* model, const char* path);
+tlg_status tlg_model_load(tlg_ctx* ctx, const char* path, tlg_model** out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TERRALIO_GPU_H_ */

@@ -1,0 +1,354 @@
+"""TEST INFRASTRUCTURE — ctypes wrapper of the CPU oracle (liboracle.so).
+
+The oracle is a plain-C++ restatement of the reference hot path (see
+terralio_oracle.hpp). Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this module; it is the
+checker, never the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+ODIR = Path(__file__).resolve().parent
+LIB = ODIR / "_build" / "liboracle.so"
+
+OK, INVALID_ARGUMENT, DOMAIN_ERROR, NO_SUPPORTED_CENTERS, RUNTIME_ERROR = 0, 1, 2, 3, 4
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(msg)
+        self.status = status
+
+
+class KP(C.Structure):
+    _fields_ = [("sigma", C.c_double), ("sigma_eps", C.c_double), ("lambda_", C.c_double),
+                ("cutoff_radius", C.c_double)]
+
+
+class CP(C.Structure):
+    _fields_ = [("mesh_resolution", C.c_double), ("accept_radius", C.c_double),
+                ("accept_count", C.c_int), ("pad", C.c_int), ("roi_min_x", C.c_double),
+                ("roi_min_y", C.c_double), ("roi_max_x", C.c_double), ("roi_max_y", C.c_double)]
+
+
+_lib = None
+
+
+def load():
+    global _lib
+    if _lib is None:
+        if not LIB.exists():
+            subprocess.run(["make", "-C", str(ODIR)], check=True, capture_output=True)
+        _lib = C.CDLL(str(LIB))
+        _lib.orc_last_error.restype = C.c_char_p
+        _lib.orc_rng_new.restype = C.c_void_p
+        _lib.orc_rng_new.argtypes = [C.c_ulonglong]
+        _lib.orc_normal_new.restype = C.c_void_p
+        _lib.orc_normal_new.argtypes = [C.c_double, C.c_double]
+        for f in ("orc_rng_free", "orc_normal_free", "orc_model_free", "orc_grid_free"):
+            getattr(_lib, f).argtypes = [C.c_void_p]
+        _lib.orc_uniform.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_size_t, C.c_void_p]
+        _lib.orc_uniform_int.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        _lib.orc_normal.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+        _lib.orc_grid_new.restype = C.c_void_p
+        _lib.orc_grid_new.argtypes = [C.c_double, C.c_void_p, C.c_void_p, C.c_size_t]
+        _lib.orc_grid_query.restype = C.c_size_t
+        _lib.orc_grid_query.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double,
+                                        C.c_void_p, C.c_size_t]
+        _lib.orc_sigma_tilde.restype = C.c_double
+        _lib.orc_moment_scale.restype = C.c_double
+        for f in ("orc_model_num_centers", "orc_model_num_blocks", "orc_model_block_size",
+                  "orc_model_centers_near"):
+            getattr(_lib, f).restype = C.c_size_t
+        _lib.orc_model_num_centers.argtypes = [C.c_void_p]
+        _lib.orc_model_num_blocks.argtypes = [C.c_void_p]
+        _lib.orc_model_block_size.argtypes = [C.c_void_p, C.c_uint]
+        _lib.orc_model_centers_near.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_void_p,
+                                                C.c_size_t]
+        for f in ("orc_model_weights", "orc_model_set_weights", "orc_model_block_index",
+                  "orc_model_kernel"):
+            getattr(_lib, f).argtypes = [C.c_void_p, C.c_void_p]
+        _lib.orc_model_centers.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.orc_model_block_members.argtypes = [C.c_void_p, C.c_uint, C.c_void_p]
+        _lib.orc_model_block_info_inverse.argtypes = [C.c_void_p, C.c_uint, C.c_void_p]
+        _lib.orc_model_predict.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
+        _lib.orc_model_moment_feature.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_void_p,
+                                                  C.c_void_p, C.c_size_t, C.c_void_p]
+        _lib.orc_model_recursive_update.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p,
+                                                    C.c_void_p, C.c_size_t, C.c_size_t, C.c_int,
+                                                    C.c_void_p]
+        _lib.orc_model_new.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                                       C.c_void_p]
+        _lib.orc_fit_batch_ridge.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.c_size_t, C.c_void_p]
+        _lib.orc_model_save.argtypes = [C.c_void_p, C.c_char_p]
+        _lib.orc_model_load.argtypes = [C.c_char_p, C.c_void_p]
+        _lib.orc_supported_mesh_nodes.argtypes = [
+            C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_double, C.c_double,
+            C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_void_p,
+            C.c_void_p, C.c_size_t, C.c_void_p]
+        _lib.orc_kernel_eval.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double,
+                                         C.c_double, C.c_double, C.c_void_p]
+        _lib.orc_manifold_rows.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_size_t, C.c_double,
+                                           C.c_double, C.c_double, C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
+        _lib.orc_lm_step.argtypes = [C.c_void_p, C.c_double, C.c_void_p]
+        _lib.orc_so3_exp.argtypes = [C.c_void_p, C.c_void_p]
+    return _lib
+
+
+def _chk(st):
+    if st != OK:
+        raise OracleError(st, load().orc_last_error().decode())
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _f64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+# ---- RNG (std::mt19937_64 + libstdc++ distributions) ------------------------
+class Rng:
+    def __init__(self, seed: int):
+        self.h = load().orc_rng_new(seed)
+
+    def uniform(self, lo, hi, n=None):
+        k = 1 if n is None else n
+        out = np.empty(k)
+        load().orc_uniform(self.h, lo, hi, k, _p(out))
+        return float(out[0]) if n is None else out
+
+    def uniform_int(self, lo, hi):
+        return load().orc_uniform_int(self.h, lo, hi)
+
+    def __del__(self):
+        try:
+            load().orc_rng_free(self.h)
+        except Exception:
+            pass
+
+
+class Normal:
+    def __init__(self, mean=0.0, sd=1.0):
+        self.h = load().orc_normal_new(mean, sd)
+
+    def draw(self, rng: Rng, n=None):
+        k = 1 if n is None else n
+        out = np.empty(k)
+        load().orc_normal(self.h, rng.h, k, _p(out))
+        return float(out[0]) if n is None else out
+
+    def __del__(self):
+        try:
+            load().orc_normal_free(self.h)
+        except Exception:
+            pass
+
+
+def kp(kernel) -> KP:
+    return KP(kernel.sigma, kernel.sigma_eps, kernel.lambda_, kernel.cutoff_radius)
+
+
+def cp(centers) -> CP:
+    r = centers.roi
+    return CP(centers.mesh_resolution, centers.accept_radius, int(centers.accept_count), 0,
+              r.min[0], r.min[1], r.max[0], r.max[1])
+
+
+def kernel_finalize(kernel):
+    k = kp(kernel)
+    _chk(load().orc_kernel_finalize(C.byref(k)))
+    return k.cutoff_radius
+
+
+def kernel_eval(kernel, x, c, bw):
+    out = C.c_double()
+    _chk(load().orc_kernel_eval(C.byref(kp(kernel)), x[0], x[1], c[0], c[1], bw, C.byref(out)))
+    return out.value
+
+
+def sigma_tilde(kernel):
+    return load().orc_sigma_tilde(C.byref(kp(kernel)))
+
+
+def moment_scale(kernel):
+    return load().orc_moment_scale(C.byref(kp(kernel)))
+
+
+class Grid:
+    def __init__(self, cell, pts):
+        p = _f64(pts).reshape(-1, 2)
+        x, y = _f64(p[:, 0]), _f64(p[:, 1])
+        self.h = load().orc_grid_new(cell, _p(x), _p(y), len(x))
+
+    def radius_query(self, q, r):
+        out = np.empty(1 << 16, dtype=np.uint32)
+        n = load().orc_grid_query(self.h, q[0], q[1], r, _p(out), len(out))
+        return out[:n].copy()
+
+    def __del__(self):
+        try:
+            load().orc_grid_free(self.h)
+        except Exception:
+            pass
+
+
+def supported_mesh_nodes(xy, z, roi, res, r_a, count, throw_empty=False):
+    p = _f64(xy).reshape(-1, 2)
+    x, y, zz = _f64(p[:, 0]), _f64(p[:, 1]), _f64(z).reshape(-1)
+    cap = max(1024, 4 * len(x) + 1024)
+    ox, oy = np.empty(cap), np.empty(cap)
+    n = C.c_size_t()
+    _chk(load().orc_supported_mesh_nodes(_p(x), _p(y), _p(zz), len(x), len(zz), roi.min[0],
+                                         roi.min[1], roi.max[0], roi.max[1], res, r_a, count,
+                                         1 if throw_empty else 0, _p(ox), _p(oy), cap,
+                                         C.byref(n)))
+    return np.stack([ox[: n.value], oy[: n.value]], 1)
+
+
+class Model:
+    def __init__(self, kernel=None, centers=None, _h=None):
+        if _h is not None:
+            self.h = _h
+            return
+        c = _f64(centers.centers).reshape(-1, 2)
+        cx, cy = _f64(c[:, 0]), _f64(c[:, 1])
+        h = C.c_void_p()
+        _chk(load().orc_model_new(C.byref(kp(kernel)), C.byref(cp(centers)), _p(cx), _p(cy),
+                                  len(cx), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            load().orc_model_free(self.h)
+        except Exception:
+            pass
+
+    def num_centers(self):
+        return load().orc_model_num_centers(self.h)
+
+    def num_blocks(self):
+        return load().orc_model_num_blocks(self.h)
+
+    def kernel_cutoff(self):
+        k = KP()
+        load().orc_model_kernel(self.h, C.byref(k))
+        return k.cutoff_radius
+
+    def centers(self):
+        n = self.num_centers()
+        cx, cy = np.empty(n), np.empty(n)
+        load().orc_model_centers(self.h, _p(cx), _p(cy))
+        return np.stack([cx, cy], 1)
+
+    def weights(self):
+        w = np.empty(self.num_centers())
+        load().orc_model_weights(self.h, _p(w))
+        return w
+
+    def set_weights(self, w):
+        w = _f64(w)
+        load().orc_model_set_weights(self.h, _p(w))
+
+    def block_index(self):
+        out = np.empty(self.num_centers(), dtype=np.uint32)
+        load().orc_model_block_index(self.h, _p(out))
+        return out
+
+    def block_members(self, b):
+        n = load().orc_model_block_size(self.h, b)
+        out = np.empty(n, dtype=np.uint32)
+        load().orc_model_block_members(self.h, b, _p(out))
+        return out
+
+    def block_info_inverse(self, b):
+        n = load().orc_model_block_size(self.h, b)
+        out = np.empty(n * n)
+        load().orc_model_block_info_inverse(self.h, b, _p(out))
+        return out.reshape(n, n, order="F")
+
+    def predict(self, xy, threads=1):
+        p = _f64(xy).reshape(-1, 2)
+        x, y = _f64(p[:, 0]), _f64(p[:, 1])
+        n = len(x)
+        z, s, gx, gy = np.empty(n), np.empty(n, dtype=np.uint8), np.empty(n), np.empty(n)
+        _chk(load().orc_model_predict(self.h, _p(x), _p(y), n, _p(z), _p(s), _p(gx), _p(gy),
+                                      threads))
+        return z, s, gx, gy
+
+    def centers_near(self, q):
+        out = np.empty(1 << 16, dtype=np.uint32)
+        n = load().orc_model_centers_near(self.h, q[0], q[1], _p(out), len(out))
+        return out[:n].copy()
+
+    def moment_feature(self, q):
+        ids, vals = np.empty(1 << 16, dtype=np.uint32), np.empty(1 << 16)
+        n = C.c_size_t()
+        _chk(load().orc_model_moment_feature(self.h, q[0], q[1], _p(ids), _p(vals), len(ids),
+                                             C.byref(n)))
+        return ids[: n.value].copy(), vals[: n.value].copy()
+
+    def recursive_update(self, xy, z, allow_birth=True):
+        p = _f64(xy).reshape(-1, 2)
+        x, y, zz = _f64(p[:, 0]), _f64(p[:, 1]), _f64(z).reshape(-1)
+        rep = (C.c_ulonglong * 4)()
+        _chk(load().orc_model_recursive_update(self.h, _p(x), _p(y), _p(zz), len(x), len(zz),
+                                               1 if allow_birth else 0, rep))
+        return dict(active_blocks=rep[0], active_centers=rep[1], born_centers=rep[2],
+                    rejected=bool(rep[3]))
+
+    def save(self, path):
+        _chk(load().orc_model_save(self.h, str(path).encode()))
+
+    @staticmethod
+    def load_file(path):
+        h = C.c_void_p()
+        _chk(load().orc_model_load(str(path).encode(), C.byref(h)))
+        return Model(_h=h)
+
+    def manifold_rows(self, R, t, h, wheel_radius=0.0, lambda_M=1.0, huber=0.05, threads=1):
+        Rm, tv = _f64(R).reshape(9), _f64(t).reshape(3)
+        ha = _f64(h).reshape(-1, 3)
+        hx, hy, hz = _f64(ha[:, 0]), _f64(ha[:, 1]), _f64(ha[:, 2])
+        n = len(hx)
+        r, J, v, raw, ne = (np.empty(n), np.empty(6 * n), np.empty(n, dtype=np.uint8),
+                            np.empty(n), np.empty(29))
+        _chk(load().orc_manifold_rows(self.h, _p(Rm), _p(tv), _p(hx), _p(hy), _p(hz), n,
+                                      wheel_radius, lambda_M, huber, _p(r), _p(J), _p(v), _p(raw),
+                                      _p(ne), threads))
+        return dict(r=r, J=J.reshape(n, 6), valid=v, raw=raw), ne
+
+
+def fit_batch_ridge(kernel, centers, xy, z):
+    c = _f64(centers.centers).reshape(-1, 2)
+    cx, cy = _f64(c[:, 0]), _f64(c[:, 1])
+    p = _f64(xy).reshape(-1, 2)
+    x, y, zz = _f64(p[:, 0]), _f64(p[:, 1]), _f64(z).reshape(-1)
+    h = C.c_void_p()
+    _chk(load().orc_fit_batch_ridge(C.byref(kp(kernel)), C.byref(cp(centers)), _p(cx), _p(cy),
+                                    len(cx), _p(x), _p(y), _p(zz), len(x), C.byref(h)))
+    return Model(_h=h)
+
+
+def lm_step(ne29, mu):
+    d = np.empty(6)
+    ne = _f64(ne29)
+    st = load().orc_lm_step(_p(ne), mu, _p(d))
+    return d, st == OK
+
+
+def so3_exp(w):
+    R = np.empty(9)
+    load().orc_so3_exp(_p(_f64(w)), _p(R))
+    return R.reshape(3, 3)

@@ -1,0 +1,352 @@
+// TEST INFRASTRUCTURE — C entry points over the CPU oracle, loaded by
+// tests/ (ctypes) and bench.py's cpu_baseline leg only. Status codes mirror
+// include/terralio_gpu.h so tests can compare error behaviour 1:1.
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "terralio_oracle.hpp"
+
+using namespace oracle;
+
+namespace {
+thread_local std::string g_err;
+
+enum {
+  ORC_OK = 0,
+  ORC_INVALID_ARGUMENT = 1,
+  ORC_DOMAIN_ERROR = 2,
+  ORC_NO_SUPPORTED_CENTERS = 3,
+  ORC_RUNTIME_ERROR = 4,
+  ORC_BUFFER_TOO_SMALL = 7,
+};
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return ORC_OK;
+  } catch (const NoSupportedCenters& e) {
+    g_err = e.what();
+    return ORC_NO_SUPPORTED_CENTERS;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return ORC_INVALID_ARGUMENT;
+  } catch (const std::domain_error& e) {
+    g_err = e.what();
+    return ORC_DOMAIN_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return ORC_RUNTIME_ERROR;
+  }
+}
+
+struct KP {
+  double sigma, sigma_eps, lambda, cutoff_radius;
+};
+struct CP {
+  double mesh_resolution, accept_radius;
+  int accept_count;
+  int pad;
+  double roi_min_x, roi_min_y, roi_max_x, roi_max_y;
+};
+
+KernelParams to_kp(const KP* k) {
+  KernelParams p;
+  p.sigma = k->sigma;
+  p.sigma_eps = k->sigma_eps;
+  p.lambda = k->lambda;
+  p.cutoff_radius = k->cutoff_radius;
+  return p;
+}
+CenterSet to_cs(const CP* c, const double* cx, const double* cy, size_t n) {
+  CenterSet s;
+  s.mesh_resolution = c->mesh_resolution;
+  s.accept_radius = c->accept_radius;
+  s.accept_count = c->accept_count;
+  s.roi = {{c->roi_min_x, c->roi_min_y}, {c->roi_max_x, c->roi_max_y}};
+  s.centers.resize(n);
+  for (size_t i = 0; i < n; ++i) s.centers[i] = {cx[i], cy[i]};
+  return s;
+}
+TerrainObservation to_obs(const double* x, const double* y, const double* z, size_t m) {
+  TerrainObservation o;
+  o.xy.resize(m);
+  o.z.assign(z, z + m);
+  for (size_t i = 0; i < m; ++i) o.xy[i] = {x[i], y[i]};
+  return o;
+}
+}  // namespace
+
+extern "C" {
+
+const char* orc_last_error() { return g_err.c_str(); }
+
+// ---- RNG: std::mt19937_64 with libstdc++ distributions ----------------------
+void* orc_rng_new(unsigned long long seed) { return new std::mt19937_64(seed); }
+void orc_rng_free(void* r) { delete static_cast<std::mt19937_64*>(r); }
+void orc_uniform(void* r, double lo, double hi, size_t n, double* out) {
+  std::uniform_real_distribution<double> u(lo, hi);
+  auto& g = *static_cast<std::mt19937_64*>(r);
+  for (size_t i = 0; i < n; ++i) out[i] = u(g);
+}
+int orc_uniform_int(void* r, int lo, int hi) {
+  std::uniform_int_distribution<int> u(lo, hi);
+  return u(*static_cast<std::mt19937_64*>(r));
+}
+void* orc_normal_new(double mean, double sd) { return new std::normal_distribution<double>(mean, sd); }
+void orc_normal_free(void* d) { delete static_cast<std::normal_distribution<double>*>(d); }
+void orc_normal(void* d, void* r, size_t n, double* out) {
+  auto& nd = *static_cast<std::normal_distribution<double>*>(d);
+  auto& g = *static_cast<std::mt19937_64*>(r);
+  for (size_t i = 0; i < n; ++i) out[i] = nd(g);
+}
+
+// ---- kernel.cpp --------------------------------------------------------------
+int orc_kernel_finalize(KP* k) {
+  return guarded([&] {
+    KernelParams p = to_kp(k);
+    p.finalize();
+    k->cutoff_radius = p.cutoff_radius;
+  });
+}
+int orc_kernel_eval(const KP* k, double xx, double xy, double cx, double cy, double bw,
+                    double* out) {
+  return guarded([&] { *out = kernel_eval(to_kp(k), {xx, xy}, {cx, cy}, bw); });
+}
+double orc_sigma_tilde(const KP* k) { return to_kp(k).sigma_tilde(); }
+double orc_moment_scale(const KP* k) { return to_kp(k).moment_scale(); }
+
+// ---- grid_index.hpp ------------------------------------------------------------
+void* orc_grid_new(double cell, const double* x, const double* y, size_t n) {
+  auto* g = new GridIndex2(cell);
+  for (size_t i = 0; i < n; ++i) g->insert({x[i], y[i]});
+  return g;
+}
+void orc_grid_free(void* g) { delete static_cast<GridIndex2*>(g); }
+size_t orc_grid_query(void* g, double qx, double qy, double r, unsigned* out, size_t cap) {
+  const auto ids = static_cast<GridIndex2*>(g)->radius_query({qx, qy}, r);
+  for (size_t i = 0; i < ids.size() && i < cap; ++i) out[i] = ids[i];
+  return ids.size();
+}
+
+// ---- center_select.cpp ---------------------------------------------------------
+int orc_supported_mesh_nodes(const double* x, const double* y, const double* z, size_t m,
+                             size_t zn, double rminx, double rminy, double rmaxx,
+                             double rmaxy, double res, double r_a, int count, int throw_empty,
+                             double* out_x, double* out_y, size_t cap, size_t* out_n) {
+  return guarded([&] {
+    TerrainObservation o;
+    o.xy.resize(m);
+    for (size_t i = 0; i < m; ++i) o.xy[i] = {x[i], y[i]};
+    o.z.assign(z, z + zn);
+    const Rect roi{{rminx, rminy}, {rmaxx, rmaxy}};
+    std::vector<V2> nodes = throw_empty ? select_centers(o, roi, res, r_a, count).centers
+                                        : supported_mesh_nodes(o, roi, res, r_a, count);
+    *out_n = nodes.size();
+    if (nodes.size() > cap) throw std::length_error("buffer too small");
+    for (size_t i = 0; i < nodes.size(); ++i) {
+      out_x[i] = nodes[i].x;
+      out_y[i] = nodes[i].y;
+    }
+  });
+}
+
+// ---- TerrainModel ----------------------------------------------------------------
+int orc_model_new(const KP* k, const CP* c, const double* cx, const double* cy, size_t n,
+                  void** out) {
+  return guarded([&] { *out = new TerrainModel(to_kp(k), to_cs(c, cx, cy, n)); });
+}
+void orc_model_free(void* m) { delete static_cast<TerrainModel*>(m); }
+size_t orc_model_num_centers(void* m) { return static_cast<TerrainModel*>(m)->num_centers(); }
+size_t orc_model_num_blocks(void* m) { return static_cast<TerrainModel*>(m)->num_blocks(); }
+void orc_model_kernel(void* m, KP* k) {
+  const auto& p = static_cast<TerrainModel*>(m)->kernel();
+  *k = {p.sigma, p.sigma_eps, p.lambda, p.cutoff_radius};
+}
+void orc_model_centers(void* m, double* cx, double* cy) {
+  const auto& c = static_cast<TerrainModel*>(m)->centers().centers;
+  for (size_t i = 0; i < c.size(); ++i) {
+    cx[i] = c[i].x;
+    cy[i] = c[i].y;
+  }
+}
+void orc_model_weights(void* m, double* w) {
+  const auto& v = static_cast<TerrainModel*>(m)->weights();
+  std::memcpy(w, v.data(), v.size() * sizeof(double));
+}
+void orc_model_set_weights(void* m, const double* w) {
+  auto* t = static_cast<TerrainModel*>(m);
+  t->set_weights(std::vector<double>(w, w + t->num_centers()));
+}
+void orc_model_block_index(void* m, unsigned* out) {
+  auto* t = static_cast<TerrainModel*>(m);
+  for (size_t i = 0; i < t->num_centers(); ++i) out[i] = t->block_of(static_cast<unsigned>(i));
+}
+size_t orc_model_block_size(void* m, unsigned b) {
+  return static_cast<TerrainModel*>(m)->block_members(b).size();
+}
+void orc_model_block_members(void* m, unsigned b, unsigned* out) {
+  const auto& v = static_cast<TerrainModel*>(m)->block_members(b);
+  for (size_t i = 0; i < v.size(); ++i) out[i] = v[i];
+}
+// column-major bn x bn
+void orc_model_block_info_inverse(void* m, unsigned b, double* out) {
+  const Mat& a = static_cast<TerrainModel*>(m)->block_info_inverse(b);
+  std::memcpy(out, a.a.data(), a.a.size() * sizeof(double));
+}
+
+// Batch predict over points, parallel over points with `threads` workers
+// (concurrent readers are allowed). Any output may be NULL.
+int orc_model_predict(void* m, const double* x, const double* y, size_t n, double* z,
+                      unsigned char* sup, double* gx, double* gy, int threads) {
+  auto* t = static_cast<TerrainModel*>(m);
+  return guarded([&] {
+    auto work = [&](size_t b, size_t e) {
+      for (size_t i = b; i < e; ++i) {
+        if (z || sup) {
+          const HeightQuery q = t->predict_height({x[i], y[i]});
+          if (z) z[i] = q.z;
+          if (sup) sup[i] = q.supported ? 1 : 0;
+        }
+        if (gx || gy) {
+          const V2 g = t->predict_gradient({x[i], y[i]});
+          if (gx) gx[i] = g.x;
+          if (gy) gy[i] = g.y;
+        }
+      }
+    };
+    if (threads <= 1) {
+      work(0, n);
+      return;
+    }
+    std::vector<std::thread> pool;
+    const size_t chunk = (n + threads - 1) / threads;
+    for (int w = 0; w < threads; ++w) {
+      const size_t b = w * chunk, e = std::min(n, b + chunk);
+      if (b < e) pool.emplace_back(work, b, e);
+    }
+    for (auto& th : pool) th.join();
+  });
+}
+
+size_t orc_model_centers_near(void* m, double qx, double qy, unsigned* out, size_t cap) {
+  auto* t = static_cast<TerrainModel*>(m);
+  const auto ids = t->centers_near({qx, qy}, t->kernel().cutoff_radius);
+  for (size_t i = 0; i < ids.size() && i < cap; ++i) out[i] = ids[i];
+  return ids.size();
+}
+
+int orc_model_moment_feature(void* m, double qx, double qy, unsigned* ids, double* vals,
+                             size_t cap, size_t* out_n) {
+  return guarded([&] {
+    const SparseVec f = static_cast<TerrainModel*>(m)->moment_feature({qx, qy});
+    *out_n = f.entries.size();
+    for (size_t i = 0; i < f.entries.size() && i < cap; ++i) {
+      ids[i] = f.entries[i].first;
+      vals[i] = f.entries[i].second;
+    }
+  });
+}
+
+int orc_model_recursive_update(void* m, const double* x, const double* y, const double* z,
+                               size_t mm, size_t zn, int allow_birth, unsigned long long* rep) {
+  return guarded([&] {
+    TerrainObservation o;
+    o.xy.resize(mm);
+    for (size_t i = 0; i < mm; ++i) o.xy[i] = {x[i], y[i]};
+    o.z.assign(z, z + zn);
+    const UpdateReport r = static_cast<TerrainModel*>(m)->recursive_update(o, allow_birth != 0);
+    rep[0] = r.active_blocks;
+    rep[1] = r.active_centers;
+    rep[2] = r.born_centers;
+    rep[3] = r.rejected ? 1 : 0;
+  });
+}
+
+int orc_fit_batch_ridge(const KP* k, const CP* c, const double* cx, const double* cy,
+                        size_t n, const double* x, const double* y, const double* z,
+                        size_t m, void** out) {
+  return guarded([&] {
+    *out = new TerrainModel(fit_batch_ridge(to_kp(k), to_cs(c, cx, cy, n), to_obs(x, y, z, m)));
+  });
+}
+
+int orc_model_save(void* m, const char* path) {
+  return guarded([&] { static_cast<TerrainModel*>(m)->save(path); });
+}
+int orc_model_load(const char* path, void** out) {
+  return guarded([&] { *out = new TerrainModel(TerrainModel::load(path)); });
+}
+
+// ---- manifold rows + normal equations (contact.cpp, scan_matcher.cpp) ----------
+// R row-major 3x3, t[3]; lever arms SoA hx/hy/hz. Outputs (nullable): r[n],
+// J[6*n] (row i at J[6*i..]), valid[n], raw[n]; ne[29] = A upper-tri (21,
+// row-major i<=j), g[6], cost, valid count.
+int orc_manifold_rows(void* m, const double* R, const double* t, const double* hx,
+                      const double* hy, const double* hz, size_t n, double wheel_radius,
+                      double lambda_M, double huber, double* r, double* J,
+                      unsigned char* valid, double* raw, double* ne29, int threads) {
+  auto* tm = static_cast<TerrainModel*>(m);
+  return guarded([&] {
+    M3 RR;
+    for (int i = 0; i < 9; ++i) RR.a[i] = R[i];
+    const V3 tt{t[0], t[1], t[2]};
+    std::vector<ManifoldRow> rows(n);
+    auto work = [&](size_t b, size_t e) {
+      for (size_t i = b; i < e; ++i)
+        rows[i] = manifold_row(*tm, RR, tt, {hx[i], hy[i], hz[i]}, wheel_radius, lambda_M, huber);
+    };
+    if (threads <= 1) {
+      work(0, n);
+    } else {
+      std::vector<std::thread> pool;
+      const size_t chunk = (n + threads - 1) / threads;
+      for (int w = 0; w < threads; ++w) {
+        const size_t b = w * chunk, e = std::min(n, b + chunk);
+        if (b < e) pool.emplace_back(work, b, e);
+      }
+      for (auto& th : pool) th.join();
+    }
+    NormalEq ne;
+    for (size_t i = 0; i < n; ++i) {
+      accumulate(ne, rows[i]);
+      if (r) r[i] = rows[i].r;
+      if (J)
+        for (int c = 0; c < 6; ++c) J[6 * i + c] = rows[i].J[c];
+      if (valid) valid[i] = rows[i].valid ? 1 : 0;
+      if (raw) raw[i] = rows[i].raw;
+    }
+    if (ne29) {
+      int k = 0;
+      for (int i = 0; i < 6; ++i)
+        for (int j = i; j < 6; ++j) ne29[k++] = ne.A[6 * i + j];
+      for (int i = 0; i < 6; ++i) ne29[21 + i] = ne.g[i];
+      ne29[27] = ne.cost;
+      ne29[28] = static_cast<double>(ne.valid);
+    }
+  });
+}
+
+int orc_lm_step(const double* ne29, double mu, double* delta) {
+  NormalEq ne;
+  int k = 0;
+  for (int i = 0; i < 6; ++i)
+    for (int j = i; j < 6; ++j) {
+      ne.A[6 * i + j] = ne29[k];
+      ne.A[6 * j + i] = ne29[k];
+      ++k;
+    }
+  for (int i = 0; i < 6; ++i) ne.g[i] = ne29[21 + i];
+  return lm_step(ne, mu, delta) ? ORC_OK : ORC_RUNTIME_ERROR;
+}
+
+void orc_so3_exp(const double* w, double* R) {
+  const M3 m = so3_exp({w[0], w[1], w[2]});
+  std::memcpy(R, m.a, sizeof(m.a));
+}
+
+}  // extern "C"

@@ -1,0 +1,747 @@
+// TEST INFRASTRUCTURE — CPU restatement of the reference hot path.
+// See terralio_oracle.hpp for the contract. Each function cites the
+// reference file:line (under /root/reference/proj/core) it follows.
+#include "terralio_oracle.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <limits>
+#include <set>
+
+namespace oracle {
+
+// ---------------------------------------------------------------------------
+// grid_index.hpp:20-61
+std::uint32_t GridIndex2::insert(const V2& p) {
+  const auto id = static_cast<std::uint32_t>(points_.size());
+  points_.push_back(p);
+  cells_[pack(coord(p.x), coord(p.y))].push_back(id);
+  return id;
+}
+
+void GridIndex2::build(const std::vector<V2>& pts) {
+  points_.reserve(points_.size() + pts.size());
+  for (const V2& p : pts) insert(p);
+}
+
+int GridIndex2::coord(double v) const { return static_cast<int>(std::floor(v / cell_)); }
+
+std::vector<std::uint32_t> GridIndex2::radius_query(const V2& q, double radius) const {
+  std::vector<std::uint32_t> out;
+  const double r2 = radius * radius;
+  const int span = static_cast<int>(std::ceil(radius / cell_));
+  const int cx = coord(q.x), cy = coord(q.y);
+  for (int ix = cx - span; ix <= cx + span; ++ix)
+    for (int iy = cy - span; iy <= cy + span; ++iy) {
+      auto it = cells_.find(pack(ix, iy));
+      if (it == cells_.end()) continue;
+      for (std::uint32_t id : it->second) {
+        const V2& p = points_[id];
+        if (sqnorm(p.x - q.x, p.y - q.y) <= r2) out.push_back(id);
+      }
+    }
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// kernel.cpp:8-35
+double KernelParams::sigma_tilde() const {
+  return std::sqrt(sigma * sigma + sigma_eps * sigma_eps);
+}
+double KernelParams::moment_scale() const {
+  const double st2 = sigma * sigma + sigma_eps * sigma_eps;
+  return sigma * sigma / st2;
+}
+void KernelParams::finalize() {
+  if (!(sigma > 0.0)) throw std::invalid_argument("kernel sigma must be > 0");
+  if (sigma_eps < 0.0) throw std::invalid_argument("sigma_eps must be >= 0");
+  if (!(lambda > 0.0)) throw std::invalid_argument("lambda must be > 0");
+  cutoff_radius = std::max(cutoff_radius, 3.0 * sigma_tilde());
+  if (!std::isfinite(sigma) || !std::isfinite(sigma_eps) || !std::isfinite(lambda))
+    throw std::invalid_argument("non-finite kernel parameter");
+}
+
+static bool finite2(const V2& v) { return std::isfinite(v.x) && std::isfinite(v.y); }
+
+double kernel_eval(const KernelParams& p, const V2& x, const V2& c, double bw) {
+  if (!finite2(x) || !finite2(c) || !std::isfinite(bw))
+    throw std::domain_error("non-finite kernel input");
+  if (!(bw > 0.0)) throw std::domain_error("bandwidth must be > 0");
+  const double r2 = sqnorm(x.x - c.x, x.y - c.y);
+  if (r2 > p.cutoff_radius * p.cutoff_radius) return 0.0;
+  return std::exp(-r2 / (2.0 * bw * bw));
+}
+
+// ---------------------------------------------------------------------------
+// center_select.cpp:9-76
+void TerrainObservation::validate() const {
+  if (xy.size() != z.size()) throw std::invalid_argument("observation xy/z length mismatch");
+  if (xy.empty()) throw std::invalid_argument("empty observation");
+  for (std::size_t i = 0; i < xy.size(); ++i)
+    if (!finite2(xy[i]) || !std::isfinite(z[i]))
+      throw std::invalid_argument("non-finite observation coordinate");
+}
+
+std::vector<V2> supported_mesh_nodes(const TerrainObservation& pts, const Rect& roi,
+                                     double res, double r_a, int count) {
+  if (!(res > 0.0)) throw std::invalid_argument("mesh_resolution must be > 0");
+  if (count < 1) throw std::invalid_argument("accept_count must be >= 1");
+  pts.validate();
+  GridIndex2 index(std::max(r_a, res));
+  index.build(pts.xy);
+  const int nx = static_cast<int>(std::floor((roi.max.x - roi.min.x) / res + 1e-9));
+  const int ny = static_cast<int>(std::floor((roi.max.y - roi.min.y) / res + 1e-9));
+  Rect bbox{pts.xy.front(), pts.xy.front()};
+  for (const V2& p : pts.xy) {
+    bbox.min.x = std::min(bbox.min.x, p.x);
+    bbox.min.y = std::min(bbox.min.y, p.y);
+    bbox.max.x = std::max(bbox.max.x, p.x);
+    bbox.max.y = std::max(bbox.max.y, p.y);
+  }
+  bbox = bbox.dilated(r_a);
+  auto clamp_idx = [&](double v, double lo, int n) {
+    const int i = static_cast<int>(std::floor((v - lo) / res));
+    return std::min(std::max(i, 0), n);
+  };
+  const int i0 = clamp_idx(bbox.min.x, roi.min.x, nx);
+  const int i1 = clamp_idx(bbox.max.x, roi.min.x, nx);
+  const int j0 = clamp_idx(bbox.min.y, roi.min.y, ny);
+  const int j1 = clamp_idx(bbox.max.y, roi.min.y, ny);
+  std::vector<V2> nodes;
+  for (int i = i0; i <= i1; ++i)
+    for (int j = j0; j <= j1; ++j) {
+      const V2 node{roi.min.x + i * res, roi.min.y + j * res};
+      if (static_cast<int>(index.radius_query(node, r_a).size()) >= count)
+        nodes.push_back(node);
+    }
+  return nodes;
+}
+
+CenterSet select_centers(const TerrainObservation& pts, const Rect& roi, double res,
+                         double r_a, int count) {
+  CenterSet set;
+  set.mesh_resolution = res;
+  set.accept_radius = r_a;
+  set.accept_count = count;
+  set.roi = roi;
+  set.centers = supported_mesh_nodes(pts, roi, res, r_a, count);
+  if (set.centers.empty()) throw NoSupportedCenters();
+  return set;
+}
+
+// ---------------------------------------------------------------------------
+// Pivoted LDL^T — restates the published Eigen::LDLT algorithm (diagonal
+// pivoting on the largest remaining |d|, left-looking column updates, zero
+// pivots tolerated, pseudo-inverse of D in solve).
+Ldlt::Ldlt(const Mat& a) : n(a.rows), lu(a), perm(static_cast<size_t>(a.rows)) {
+  std::vector<double> tmp(static_cast<size_t>(n));
+  bool found_zero = false;
+  int sign = 0;  // 0 zero, 1 psd, 2 nsd, 3 indefinite
+  for (long k = 0; k < n; ++k) {
+    long big = k;
+    double bv = std::abs(lu(k, k));
+    for (long i = k + 1; i < n; ++i)
+      if (std::abs(lu(i, i)) > bv) {
+        bv = std::abs(lu(i, i));
+        big = i;
+      }
+    perm[static_cast<size_t>(k)] = big;
+    if (big != k) {
+      for (long c = 0; c < k; ++c) std::swap(lu(k, c), lu(big, c));
+      for (long r = big + 1; r < n; ++r) std::swap(lu(r, k), lu(r, big));
+      std::swap(lu(k, k), lu(big, big));
+      for (long i = k + 1; i < big; ++i) {
+        const double t = lu(i, k);
+        lu(i, k) = lu(big, i);
+        lu(big, i) = t;
+      }
+    }
+    if (k > 0) {
+      for (long c = 0; c < k; ++c) tmp[static_cast<size_t>(c)] = lu(c, c) * lu(k, c);
+      double s = 0.0;
+      for (long c = 0; c < k; ++c) s += lu(k, c) * tmp[static_cast<size_t>(c)];
+      lu(k, k) -= s;
+      for (long r = k + 1; r < n; ++r) {
+        double acc = 0.0;
+        for (long c = 0; c < k; ++c) acc += lu(r, c) * tmp[static_cast<size_t>(c)];
+        lu(r, k) -= acc;
+      }
+    }
+    const double akk = lu(k, k);
+    const bool valid = std::abs(akk) > 0.0;
+    if (k == 0 && !valid) {
+      sign = 0;
+      for (long j = 0; j < n; ++j) perm[static_cast<size_t>(j)] = j;
+      positive = true;
+      return;
+    }
+    if (k + 1 < n && valid)
+      for (long r = k + 1; r < n; ++r) lu(r, k) /= akk;
+    else if (k + 1 < n)
+      for (long r = k + 1; r < n; ++r) ok = ok && (lu(r, k) == 0.0);
+    if (found_zero && valid)
+      ok = false;
+    else if (!valid)
+      found_zero = true;
+    if (sign == 1) {
+      if (akk < 0.0) sign = 3;
+    } else if (sign == 2) {
+      if (akk > 0.0) sign = 3;
+    } else if (sign == 0) {
+      if (akk > 0.0) sign = 1;
+      else if (akk < 0.0) sign = 2;
+    }
+  }
+  positive = (sign == 1 || sign == 0);
+}
+
+std::vector<double> Ldlt::vectorD() const {
+  std::vector<double> d(static_cast<size_t>(n));
+  for (long i = 0; i < n; ++i) d[static_cast<size_t>(i)] = lu(i, i);
+  return d;
+}
+
+Mat Ldlt::solve(const Mat& b) const {
+  Mat x = b;
+  const double tol = std::numeric_limits<double>::min();
+  for (long c = 0; c < x.cols; ++c) {
+    double* v = &x.a[static_cast<size_t>(c * x.rows)];
+    for (long k = 0; k < n; ++k) std::swap(v[k], v[perm[static_cast<size_t>(k)]]);
+    for (long k = 0; k < n; ++k)
+      for (long r = k + 1; r < n; ++r) v[r] -= lu(r, k) * v[k];
+    for (long k = 0; k < n; ++k) {
+      const double d = lu(k, k);
+      v[k] = (std::abs(d) > tol) ? v[k] / d : 0.0;
+    }
+    for (long k = n - 1; k >= 0; --k) {
+      double s = v[k];
+      for (long r = k + 1; r < n; ++r) s -= lu(r, k) * v[r];
+      v[k] = s;
+    }
+    for (long k = n - 1; k >= 0; --k) std::swap(v[k], v[perm[static_cast<size_t>(k)]]);
+  }
+  return x;
+}
+
+std::vector<double> Ldlt::solve(const std::vector<double>& b) const {
+  Mat m(static_cast<long>(b.size()), 1);
+  m.a = b;
+  return solve(m).a;
+}
+
+// ---------------------------------------------------------------------------
+// terrain_model.cpp:15-22
+namespace {
+std::int64_t pack2(std::int64_t x, std::int64_t y) { return (x << 32) ^ (y & 0xffffffffll); }
+std::int64_t mesh_node_key(const V2& node, const Rect& roi, double res) {
+  return pack2(std::llround((node.x - roi.min.x) / res), std::llround((node.y - roi.min.y) / res));
+}
+}  // namespace
+
+// terrain_model.cpp:26-44
+TerrainModel::TerrainModel(KernelParams kernel, CenterSet centers)
+    : kernel_(kernel), centers_(std::move(centers)) {
+  kernel_.finalize();
+  const auto n = centers_.centers.size();
+  weights_.assign(n, 0.0);
+  block_index_.resize(n);
+  for (std::uint32_t i = 0; i < n; ++i) {
+    const std::uint32_t b = block_for_tile(tile_key(centers_.centers[i]));
+    block_index_[i] = b;
+    blocks_[b].members.push_back(i);
+  }
+  for (auto& blk : blocks_) {
+    const long bn = static_cast<long>(blk.members.size());
+    blk.info_inv = Mat(bn, bn);
+    for (long i = 0; i < bn; ++i) blk.info_inv(i, i) = 1.0 * (1.0 / kernel_.lambda);
+  }
+  rebuild_indexes();
+}
+
+// terrain_model.cpp:46-51
+std::int64_t TerrainModel::tile_key(const V2& c) const {
+  const double side = 2.0 * kernel_.cutoff_radius;
+  if (!(side < 1e12)) return 0;
+  return pack2(static_cast<std::int64_t>(std::floor(c.x / side)),
+               static_cast<std::int64_t>(std::floor(c.y / side)));
+}
+
+// terrain_model.cpp:53-60
+std::uint32_t TerrainModel::block_for_tile(std::int64_t key) {
+  auto it = tile_blocks_.find(key);
+  if (it != tile_blocks_.end()) return it->second;
+  const auto id = static_cast<std::uint32_t>(blocks_.size());
+  tile_blocks_.emplace(key, id);
+  blocks_.emplace_back();
+  return id;
+}
+
+// terrain_model.cpp:62-70
+void TerrainModel::rebuild_indexes() {
+  const double cell = std::min(kernel_.cutoff_radius, 1e6);
+  center_index_ = std::make_unique<GridIndex2>(cell);
+  center_index_->build(centers_.centers);
+  mesh_occupancy_.clear();
+  for (const V2& c : centers_.centers)
+    mesh_occupancy_.emplace(mesh_node_key(c, centers_.roi, centers_.mesh_resolution), 1u);
+}
+
+std::vector<std::uint32_t> TerrainModel::centers_near(const V2& x, double radius) const {
+  return center_index_->radius_query(x, radius);
+}
+
+// terrain_model.cpp:77-95
+std::uint32_t TerrainModel::add_center(const V2& c) {
+  const auto id = static_cast<std::uint32_t>(centers_.centers.size());
+  centers_.centers.push_back(c);
+  const std::uint32_t b = block_for_tile(tile_key(c));
+  block_index_.push_back(b);
+  Block& blk = blocks_[b];
+  blk.members.push_back(id);
+  const long bn = static_cast<long>(blk.members.size());
+  Mat grown(bn, bn);
+  for (long cc = 0; cc + 1 < bn; ++cc)
+    for (long r = 0; r + 1 < bn; ++r) grown(r, cc) = blk.info_inv(r, cc);
+  grown(bn - 1, bn - 1) = 1.0 / kernel_.lambda;
+  blk.info_inv = std::move(grown);
+  weights_.push_back(0.0);
+  center_index_->insert(c);
+  mesh_occupancy_.emplace(mesh_node_key(c, centers_.roi, centers_.mesh_resolution), 1u);
+  return id;
+}
+
+// terrain_model.cpp:97-107
+SparseVec TerrainModel::moment_feature(const V2& x) const {
+  if (!finite2(x)) throw std::domain_error("non-finite query");
+  SparseVec m;
+  const double scale = kernel_.moment_scale();
+  const double st = kernel_.sigma_tilde();
+  for (std::uint32_t id : centers_near(x, kernel_.cutoff_radius)) {
+    const double k = kernel_eval(kernel_, x, centers_.centers[id], st);
+    if (k != 0.0) m.entries.emplace_back(id, scale * k);
+  }
+  return m;
+}
+
+// terrain_model.cpp:109-125 (single 256-chunk of parallel.hpp:31-45: acc = 0 + s)
+HeightQuery TerrainModel::predict_height(const V2& x) const {
+  const auto ids = centers_near(x, kernel_.cutoff_radius);
+  if (ids.empty()) return {0.0, false};
+  double acc = 0.0;
+  for (std::size_t b = 0; b < ids.size(); b += 256) {
+    const std::size_t e = std::min(ids.size(), b + 256);
+    double s = 0.0;
+    for (std::size_t i = b; i < e; ++i)
+      s += weights_[ids[i]] * kernel_eval(kernel_, x, centers_.centers[ids[i]], kernel_.sigma);
+    acc += s;
+  }
+  return {acc, true};
+}
+
+// terrain_model.cpp:127-143; element order (w * ((-(x-c)) * inv_s2)) * k
+V2 TerrainModel::predict_gradient(const V2& x) const {
+  const auto ids = centers_near(x, kernel_.cutoff_radius);
+  const double inv_s2 = 1.0 / (kernel_.sigma * kernel_.sigma);
+  V2 acc{0.0, 0.0};
+  for (std::size_t b = 0; b < ids.size(); b += 256) {
+    const std::size_t e = std::min(ids.size(), b + 256);
+    V2 s{0.0, 0.0};
+    for (std::size_t i = b; i < e; ++i) {
+      const V2& c = centers_.centers[ids[i]];
+      const double k = kernel_eval(kernel_, x, c, kernel_.sigma);
+      const double w = weights_[ids[i]];
+      s.x += (w * ((-(x.x - c.x)) * inv_s2)) * k;
+      s.y += (w * ((-(x.y - c.y)) * inv_s2)) * k;
+    }
+    acc.x += s.x;
+    acc.y += s.y;
+  }
+  return acc;
+}
+
+// terrain_model.cpp:145-253
+UpdateReport TerrainModel::recursive_update(const TerrainObservation& obs, bool allow_birth) {
+  obs.validate();
+  UpdateReport report;
+  if (allow_birth) {
+    const auto nodes = supported_mesh_nodes(obs, centers_.roi, centers_.mesh_resolution,
+                                            centers_.accept_radius, centers_.accept_count);
+    for (const V2& node : nodes) {
+      const auto key = mesh_node_key(node, centers_.roi, centers_.mesh_resolution);
+      if (mesh_occupancy_.count(key)) continue;
+      add_center(node);
+      ++report.born_centers;
+    }
+  }
+  std::vector<char> active(centers_.centers.size(), 0);
+  for (const V2& x : obs.xy)
+    for (std::uint32_t id : centers_near(x, kernel_.cutoff_radius)) active[id] = 1;
+  std::set<std::uint32_t> active_blocks;
+  for (std::uint32_t i = 0; i < active.size(); ++i)
+    if (active[i]) active_blocks.insert(block_index_[i]);
+  report.active_blocks = active_blocks.size();
+  if (active_blocks.empty()) return report;
+
+  std::vector<std::uint32_t> merged;
+  for (std::uint32_t b : active_blocks)
+    merged.insert(merged.end(), blocks_[b].members.begin(), blocks_[b].members.end());
+  report.active_centers = merged.size();
+  const long n = static_cast<long>(merged.size());
+  const long m_total = static_cast<long>(obs.size());
+  std::vector<std::int32_t> row_of(centers_.centers.size(), -1);
+  for (long r = 0; r < n; ++r) row_of[merged[static_cast<size_t>(r)]] = static_cast<std::int32_t>(r);
+
+  Mat Mt(n, m_total);
+  const double scale = kernel_.moment_scale();
+  const double st = kernel_.sigma_tilde();
+  for (long j = 0; j < m_total; ++j) {
+    const V2& x = obs.xy[static_cast<size_t>(j)];
+    for (std::uint32_t id : centers_near(x, kernel_.cutoff_radius)) {
+      const double k = kernel_eval(kernel_, x, centers_.centers[id], st);
+      if (k != 0.0) Mt(row_of[id], j) = scale * k;
+    }
+  }
+  Mat Hinv(n, n);
+  std::vector<double> w(static_cast<size_t>(n));
+  {
+    long off = 0;
+    for (std::uint32_t b : active_blocks) {
+      const long bn = static_cast<long>(blocks_[b].members.size());
+      for (long c = 0; c < bn; ++c)
+        for (long r = 0; r < bn; ++r) Hinv(off + r, off + c) = blocks_[b].info_inv(r, c);
+      for (long i = 0; i < bn; ++i)
+        w[static_cast<size_t>(off + i)] = weights_[blocks_[b].members[static_cast<size_t>(i)]];
+      off += bn;
+    }
+  }
+  constexpr long kChunk = 64;
+  for (long o = 0; o < m_total; o += kChunk) {
+    const long m = std::min(kChunk, m_total - o);
+    // K = Hinv * Mc  (n x m)
+    Mat K(n, m);
+    for (long c = 0; c < m; ++c)
+      for (long k = 0; k < n; ++k) {
+        const double v = Mt(k, o + c);
+        if (v == 0.0) continue;
+        for (long r = 0; r < n; ++r) K(r, c) += Hinv(r, k) * v;
+      }
+    // S = Mc^T K + I, symmetrised
+    Mat S(m, m);
+    for (long c = 0; c < m; ++c)
+      for (long r = 0; r < m; ++r) {
+        double s = 0.0;
+        for (long k = 0; k < n; ++k) s += Mt(k, o + r) * K(k, c);
+        S(r, c) = s;
+      }
+    for (long i = 0; i < m; ++i) S(i, i) += 1.0;
+    Mat Ss(m, m);
+    for (long c = 0; c < m; ++c)
+      for (long r = 0; r < m; ++r) Ss(r, c) = 0.5 * (S(r, c) + S(c, r));
+    Ldlt ldlt(Ss);
+    if (!ldlt.ok || !ldlt.positive) {
+      report.rejected = true;
+      return report;
+    }
+    Mat Kt(m, n);
+    for (long c = 0; c < n; ++c)
+      for (long r = 0; r < m; ++r) Kt(r, c) = K(c, r);
+    const Mat KS = ldlt.solve(Kt);  // m x n
+    for (double v : KS.a)
+      if (!std::isfinite(v)) {
+        report.rejected = true;
+        return report;
+      }
+    // Hinv -= K * KS
+    for (long c = 0; c < n; ++c)
+      for (long k = 0; k < m; ++k) {
+        const double v = KS(k, c);
+        for (long r = 0; r < n; ++r) Hinv(r, c) -= K(r, k) * v;
+      }
+    for (long c = 0; c < n; ++c)
+      for (long r = c + 1; r < n; ++r) {
+        const double s = 0.5 * (Hinv(r, c) + Hinv(c, r));
+        Hinv(r, c) = s;
+        Hinv(c, r) = s;
+      }
+    // resid = z_c - Mc^T w ; w += Hinv * (Mc * resid)
+    std::vector<double> resid(static_cast<size_t>(m));
+    for (long r = 0; r < m; ++r) {
+      double s = 0.0;
+      for (long k = 0; k < n; ++k) s += Mt(k, o + r) * w[static_cast<size_t>(k)];
+      resid[static_cast<size_t>(r)] = obs.z[static_cast<size_t>(o + r)] - s;
+    }
+    std::vector<double> mr(static_cast<size_t>(n), 0.0);
+    for (long c = 0; c < m; ++c)
+      for (long k = 0; k < n; ++k) mr[static_cast<size_t>(k)] += Mt(k, o + c) * resid[static_cast<size_t>(c)];
+    std::vector<double> dw(static_cast<size_t>(n), 0.0);
+    for (long c = 0; c < n; ++c) {
+      const double v = mr[static_cast<size_t>(c)];
+      for (long r = 0; r < n; ++r) dw[static_cast<size_t>(r)] += Hinv(r, c) * v;
+    }
+    for (long r = 0; r < n; ++r) w[static_cast<size_t>(r)] += dw[static_cast<size_t>(r)];
+  }
+  {
+    long off = 0;
+    for (std::uint32_t b : active_blocks) {
+      const long bn = static_cast<long>(blocks_[b].members.size());
+      Mat blk(bn, bn);
+      for (long c = 0; c < bn; ++c)
+        for (long r = 0; r < bn; ++r) blk(r, c) = Hinv(off + r, off + c);
+      Mat sym(bn, bn);
+      for (long c = 0; c < bn; ++c)
+        for (long r = 0; r < bn; ++r) sym(r, c) = 0.5 * (blk(r, c) + blk(c, r));
+      blocks_[b].info_inv = std::move(sym);
+      for (long i = 0; i < bn; ++i)
+        weights_[blocks_[b].members[static_cast<size_t>(i)]] = w[static_cast<size_t>(off + i)];
+      off += bn;
+    }
+  }
+  return report;
+}
+
+// terrain_model.cpp:269-308
+TerrainModel fit_batch_ridge(const KernelParams& params, const CenterSet& centers,
+                             const TerrainObservation& obs) {
+  obs.validate();
+  TerrainModel model(params, centers);
+  const long n = static_cast<long>(model.num_centers());
+  Mat H(n, n);
+  for (long i = 0; i < n; ++i) H(i, i) = 1.0 * model.kernel().lambda;
+  std::vector<double> b(static_cast<size_t>(n), 0.0);
+  for (std::size_t j = 0; j < obs.size(); ++j) {
+    const SparseVec m = model.moment_feature(obs.xy[j]);
+    for (const auto& [i1, v1] : m.entries) {
+      b[i1] += v1 * obs.z[j];
+      for (const auto& [i2, v2] : m.entries) H(i1, i2) += v1 * v2;
+    }
+  }
+  Ldlt ldlt(H);
+  std::vector<double> w = ldlt.solve(b);
+  bool finite = true;
+  for (double v : w) finite = finite && std::isfinite(v);
+  if (!ldlt.ok || !finite) {
+    const auto d = ldlt.vectorD();
+    double mx = 0.0, mn = std::numeric_limits<double>::infinity();
+    for (double v : d) {
+      mx = std::max(mx, std::abs(v));
+      mn = std::min(mn, std::abs(v));
+    }
+    throw std::runtime_error("ridge solve failed; condition estimate " +
+                             std::to_string(mx / std::max(mn, 1e-300)));
+  }
+  model.weights_ = w;
+  for (auto& blk : model.blocks_) {
+    const long bn = static_cast<long>(blk.members.size());
+    Mat Hb(bn, bn), I(bn, bn);
+    for (long r = 0; r < bn; ++r) {
+      I(r, r) = 1.0;
+      for (long c = 0; c < bn; ++c) Hb(r, c) = H(blk.members[static_cast<size_t>(r)], blk.members[static_cast<size_t>(c)]);
+    }
+    const Mat inv = Ldlt(Hb).solve(I);
+    Mat sym(bn, bn);
+    for (long c = 0; c < bn; ++c)
+      for (long r = 0; r < bn; ++r) sym(r, c) = 0.5 * (inv(r, c) + inv(c, r));
+    blk.info_inv = std::move(sym);
+  }
+  return model;
+}
+
+// ---------------------------------------------------------------------------
+// snapshot.cpp:7-126 ("RBFT" v1, little-endian)
+namespace {
+template <typename T>
+void put(std::ostream& out, const T& v) {
+  out.write(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+template <typename T>
+T get(std::istream& in) {
+  T v;
+  in.read(reinterpret_cast<char*>(&v), sizeof(T));
+  if (!in) throw std::runtime_error("truncated terrain snapshot");
+  return v;
+}
+}  // namespace
+
+void TerrainModel::save(const std::string& path) const {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw std::runtime_error("cannot open " + path);
+  out.write("RBFT", 4);
+  put<std::uint32_t>(out, 1u);
+  put<std::uint32_t>(out, static_cast<std::uint32_t>(num_centers()));
+  put<std::uint32_t>(out, static_cast<std::uint32_t>(blocks_.size()));
+  for (const V2& c : centers_.centers) {
+    put<double>(out, c.x);
+    put<double>(out, c.y);
+  }
+  for (double w : weights_) put<double>(out, w);
+  for (std::uint32_t b : block_index_) put<std::uint32_t>(out, b);
+  for (const Block& blk : blocks_)
+    for (long r = 0; r < blk.info_inv.rows; ++r)
+      for (long c = 0; c <= r; ++c) put<double>(out, blk.info_inv(r, c));
+  put<double>(out, kernel_.sigma);
+  put<double>(out, kernel_.sigma_eps);
+  put<double>(out, kernel_.lambda);
+  put<double>(out, kernel_.cutoff_radius);
+  put<double>(out, centers_.mesh_resolution);
+  put<double>(out, centers_.accept_radius);
+  put<std::uint32_t>(out, static_cast<std::uint32_t>(centers_.accept_count));
+  put<double>(out, centers_.roi.min.x);
+  put<double>(out, centers_.roi.min.y);
+  put<double>(out, centers_.roi.max.x);
+  put<double>(out, centers_.roi.max.y);
+}
+
+TerrainModel TerrainModel::load(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("cannot open " + path);
+  char magic[4];
+  in.read(magic, 4);
+  if (!in || std::memcmp(magic, "RBFT", 4) != 0)
+    throw std::runtime_error("not a terrain snapshot: " + path);
+  if (get<std::uint32_t>(in) != 1u) throw std::runtime_error("unsupported snapshot version");
+  const auto n = get<std::uint32_t>(in);
+  const auto nb = get<std::uint32_t>(in);
+  TerrainModel model;
+  model.centers_.centers.resize(n);
+  for (auto& c : model.centers_.centers) {
+    c.x = get<double>(in);
+    c.y = get<double>(in);
+  }
+  model.weights_.resize(n);
+  for (std::uint32_t i = 0; i < n; ++i) model.weights_[i] = get<double>(in);
+  model.block_index_.resize(n);
+  model.blocks_.resize(nb);
+  for (std::uint32_t i = 0; i < n; ++i) {
+    const auto b = get<std::uint32_t>(in);
+    if (b >= nb) throw std::runtime_error("corrupt block index");
+    model.block_index_[i] = b;
+    model.blocks_[b].members.push_back(i);
+  }
+  for (auto& blk : model.blocks_) {
+    const long bn = static_cast<long>(blk.members.size());
+    blk.info_inv = Mat(bn, bn);
+    for (long r = 0; r < bn; ++r)
+      for (long c = 0; c <= r; ++c) {
+        const double v = get<double>(in);
+        blk.info_inv(r, c) = v;
+        blk.info_inv(c, r) = v;
+      }
+  }
+  model.kernel_.sigma = get<double>(in);
+  model.kernel_.sigma_eps = get<double>(in);
+  model.kernel_.lambda = get<double>(in);
+  model.kernel_.cutoff_radius = get<double>(in);
+  model.centers_.mesh_resolution = get<double>(in);
+  model.centers_.accept_radius = get<double>(in);
+  model.centers_.accept_count = static_cast<int>(get<std::uint32_t>(in));
+  model.centers_.roi.min.x = get<double>(in);
+  model.centers_.roi.min.y = get<double>(in);
+  model.centers_.roi.max.x = get<double>(in);
+  model.centers_.roi.max.y = get<double>(in);
+  model.kernel_.finalize();
+  for (std::uint32_t i = 0; i < n; ++i)
+    model.tile_blocks_.emplace(model.tile_key(model.centers_.centers[i]), model.block_index_[i]);
+  model.rebuild_indexes();
+  return model;
+}
+
+// ---------------------------------------------------------------------------
+// so3.cpp:8-27
+M3 hat(const V3& v) {
+  M3 m;
+  m.a[0] = 0.0;  m.a[1] = -v.z; m.a[2] = v.y;
+  m.a[3] = v.z;  m.a[4] = 0.0;  m.a[5] = -v.x;
+  m.a[6] = -v.y; m.a[7] = v.x;  m.a[8] = 0.0;
+  return m;
+}
+
+M3 mul(const M3& a, const M3& b) {
+  M3 r;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) r(i, j) = (a(i, 0) * b(0, j) + a(i, 1) * b(1, j)) + a(i, 2) * b(2, j);
+  return r;
+}
+
+V3 mul(const M3& a, const V3& v) {
+  return {(a(0, 0) * v.x + a(0, 1) * v.y) + a(0, 2) * v.z,
+          (a(1, 0) * v.x + a(1, 1) * v.y) + a(1, 2) * v.z,
+          (a(2, 0) * v.x + a(2, 1) * v.y) + a(2, 2) * v.z};
+}
+
+M3 so3_exp(const V3& w) {
+  const double theta2 = (w.x * w.x + w.y * w.y) + w.z * w.z;
+  const M3 W = hat(w);
+  const M3 W2 = mul(W, W);
+  M3 R;
+  if (theta2 < 1e-16) {
+    for (int i = 0; i < 9; ++i) R.a[i] = ((i % 4 == 0) ? 1.0 : 0.0) + W.a[i] + 0.5 * W2.a[i];
+    return R;
+  }
+  const double theta = std::sqrt(theta2);
+  const double a = std::sin(theta) / theta;
+  const double b = (1.0 - std::cos(theta)) / theta2;
+  for (int i = 0; i < 9; ++i) R.a[i] = ((i % 4 == 0) ? 1.0 : 0.0) + a * W.a[i] + b * W2.a[i];
+  return R;
+}
+
+// ---------------------------------------------------------------------------
+// contact.cpp:7-39 (residual + 1x6 Jacobian) with the scan_matcher.cpp:
+// 221-248 weighting: sqrt(lambda_M) * w_Huber, invalid rows stay zero.
+ManifoldRow manifold_row(const TerrainModel& terrain, const M3& R, const V3& t, const V3& h,
+                         double wheel_radius, double lambda_M, double huber_delta) {
+  ManifoldRow row;
+  const V3 Rh = mul(R, h);
+  const V3 xi{Rh.x + t.x, Rh.y + t.y, Rh.z + t.z};
+  const HeightQuery q = terrain.predict_height({xi.x, xi.y});
+  if (!q.supported) return row;
+  row.valid = true;
+  row.raw = xi.z - wheel_radius - q.z;
+  const V2 grad = terrain.predict_gradient({xi.x, xi.y});
+  const double dr[3] = {-grad.x, -grad.y, 1.0};
+  // dxi/dtheta = (-R) * hat(h)
+  M3 negR;
+  for (int i = 0; i < 9; ++i) negR.a[i] = -R.a[i];
+  const M3 D = mul(negR, hat(h));
+  double J[6];
+  for (int c = 0; c < 3; ++c) J[c] = (dr[0] * D(0, c) + dr[1] * D(1, c)) + dr[2] * D(2, c);
+  J[3] = dr[0];
+  J[4] = dr[1];
+  J[5] = dr[2];
+  const double sl = std::sqrt(lambda_M);
+  double w = 1.0;
+  if (huber_delta > 0.0 && std::abs(row.raw) > huber_delta)
+    w = std::sqrt(huber_delta / std::abs(row.raw));
+  row.r = sl * w * row.raw;
+  for (int c = 0; c < 6; ++c) row.J[c] = sl * w * J[c];
+  return row;
+}
+
+void accumulate(NormalEq& ne, const ManifoldRow& row) {
+  for (int i = 0; i < 6; ++i) {
+    for (int j = 0; j < 6; ++j) ne.A[6 * i + j] += row.J[i] * row.J[j];
+    ne.g[i] += row.J[i] * row.r;
+  }
+  ne.cost += row.r * row.r;
+  ne.valid += row.valid ? 1 : 0;
+}
+
+bool lm_step(const NormalEq& ne, double mu, double delta[6]) {
+  Mat damped(6, 6);
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 6; ++j) damped(i, j) = ne.A[6 * i + j];
+  for (int i = 0; i < 6; ++i) damped(i, i) += mu * std::max(ne.A[6 * i + i], 1e-12);
+  for (int i = 0; i < 6; ++i) damped(i, i) += 1e-3;
+  std::vector<double> g(ne.g, ne.g + 6);
+  const auto x = Ldlt(damped).solve(g);
+  bool finite = true;
+  for (int i = 0; i < 6; ++i) {
+    delta[i] = -x[static_cast<size_t>(i)];
+    finite = finite && std::isfinite(delta[i]);
+  }
+  return finite;
+}
+
+}  // namespace oracle

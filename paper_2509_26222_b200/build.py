@@ -1,0 +1,88 @@
+"""Builds libterralio_gpu.so (sm_100a) in-tree, and the CPU oracle.
+
+Usage: python -m paper_2509_26222_b200.build [--force]
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB_DIR = PKG / "lib"
+LIB = LIB_DIR / "libterralio_gpu.so"
+OBJ_DIR = ROOT / "build" / "obj"
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = [
+    "-O3", "-std=c++17", "-lineinfo", *ARCH,
+    "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
+    "--expt-relaxed-constexpr",
+    "-I", str(ROOT / "include"),
+]
+
+SOURCES = ["model.cu", "grid.cu", "eval.cu", "select.cu", "dense.cu", "update.cu", "abi.cu"]
+
+
+def _stale(target: Path, deps: list[Path]) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def _run(cmd: list[str]) -> None:
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("command failed: " + " ".join(cmd))
+    if r.stderr.strip():
+        sys.stderr.write(r.stderr)
+
+
+def build_gpu(force: bool = False, verbose: bool = False) -> Path:
+    OBJ_DIR.mkdir(parents=True, exist_ok=True)
+    LIB_DIR.mkdir(parents=True, exist_ok=True)
+    headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "terralio_gpu.h"]
+    jobs = []
+    objs = []
+    for src in SOURCES:
+        s = CSRC / src
+        o = OBJ_DIR / (src + ".o")
+        objs.append(o)
+        if force or _stale(o, [s, *headers]):
+            cmd = [NVCC, *NVCC_FLAGS, "-c", str(s), "-o", str(o)]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            jobs.append(cmd)
+    if jobs:
+        with ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
+            list(ex.map(_run, jobs))
+    if force or jobs or _stale(LIB, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart_static",
+              "-lrt", "-lpthread", "-ldl"])
+    return LIB
+
+
+def build_oracle(force: bool = False) -> Path:
+    odir = ROOT / "oracle"
+    args = ["make", "-C", str(odir)]
+    if force:
+        _run(["make", "-C", str(odir), "clean"])
+    _run(args)
+    return odir / "_build" / "liboracle.so"
+
+
+def main() -> None:
+    force = "--force" in sys.argv
+    print(build_oracle(force))
+    print(build_gpu(force, verbose="-v" in sys.argv))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,635 @@
+// extern "C" entry points of include/terralio_gpu.h. Each one converts
+// internal exceptions into the status enum + a thread-local message.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstdio>
+#include <fstream>
+
+#include "internal.cuh"
+
+using namespace tlg;
+
+tlg_model* model_create_impl(tlg_ctx* ctx, const tlg_kernel_params& k0,
+                             const tlg_center_params& cp, const double* hx, const double* hy,
+                             size_t n);
+namespace tlg {
+void block_resize(tlg_model* m, uint32_t b, int old_n, int new_n);
+void upload_new_centres(tlg_model* m, size_t first);
+uint32_t add_center_host(tlg_model* m, double x, double y);
+void moment_device(tlg_model* m, const double* x, const double* y, size_t n, uint32_t* rowp,
+                   uint32_t** ids, double** vals, size_t* nnz);
+}  // namespace tlg
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+tlg_status guard(F&& f) {
+  try {
+    f();
+    return TLG_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return TLG_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return TLG_RUNTIME_ERROR;
+  }
+}
+
+void check_ptr(const void* p, const char* what) {
+  if (!p) throw Error(TLG_INVALID_ARGUMENT, std::string("null argument: ") + what);
+}
+}  // namespace
+
+// Pinned staging buffer; the stream is drained first so a previous async
+// copy out of the buffer can never be overwritten.
+void* tlg_ctx::host_stage(size_t bytes) {
+  TLG_CUDA(cudaStreamSynchronize(stream));
+  if (bytes > pinned_bytes) {
+    if (pinned) cudaFreeHost(pinned);
+    pinned = nullptr;
+    pinned_bytes = 0;
+    TLG_CUDA(cudaMallocHost(&pinned, bytes));
+    pinned_bytes = bytes;
+  }
+  return pinned;
+}
+
+void tlg_ctx::sync() { TLG_CUDA(cudaStreamSynchronize(stream)); }
+
+namespace tlg {
+void copy_in(tlg_ctx* ctx, void* dst, const void* src, size_t bytes, tlg_mem mem) {
+  if (!bytes) return;
+  TLG_CUDA(cudaMemcpyAsync(dst, src, bytes,
+                           mem == TLG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                           ctx->stream));
+}
+void copy_out(tlg_ctx* ctx, void* dst, const void* src, size_t bytes, tlg_mem mem) {
+  if (!bytes) return;
+  TLG_CUDA(cudaMemcpyAsync(dst, src, bytes,
+                           mem == TLG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                           ctx->stream));
+}
+}  // namespace tlg
+
+extern "C" {
+
+int tlg_abi_version(void) { return TLG_ABI_VERSION; }
+const char* tlg_last_error(void) { return g_err.c_str(); }
+
+tlg_status tlg_ctx_create(int device, void* stream, tlg_ctx** out) {
+  return guard([&] {
+    check_ptr(out, "out");
+    int ndev = 0;
+    TLG_CUDA(cudaGetDeviceCount(&ndev));
+    require(device >= 0 && device < ndev, TLG_INVALID_ARGUMENT, "bad device ordinal");
+    cudaDeviceProp prop;
+    TLG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      throw Error(TLG_CUDA_ERROR, "terralio_gpu is built for sm_100a (B200); device is sm_" +
+                                      std::to_string(prop.major) + std::to_string(prop.minor));
+    TLG_CUDA(cudaSetDevice(device));
+    auto* c = new tlg_ctx();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+      if (e != cudaSuccess) {
+        delete c;
+        throw_cuda(e, "cudaStreamCreate", __FILE__, __LINE__);
+      }
+      c->own_stream = true;
+    }
+    *out = c;
+  });
+}
+
+tlg_status tlg_ctx_destroy(tlg_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+tlg_status tlg_ctx_set_stream(tlg_ctx* ctx, void* stream) {
+  return guard([&] {
+    check_ptr(ctx, "ctx");
+    ctx->sync();
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    ctx->own_stream = false;
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+tlg_status tlg_ctx_synchronize(tlg_ctx* ctx) {
+  return guard([&] {
+    check_ptr(ctx, "ctx");
+    ctx->sync();
+  });
+}
+
+uint64_t tlg_ctx_launch_count(const tlg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+tlg_status tlg_kernel_finalize(tlg_kernel_params* p) {
+  return guard([&] {
+    check_ptr(p, "params");
+    finalize_kernel(*p);
+  });
+}
+
+// ---- center selection ------------------------------------------------------
+static tlg_status select_impl(tlg_ctx* ctx, const double* x, const double* y, const double* z,
+                              size_t m, size_t zn, tlg_mem in_mem, const tlg_center_params* p,
+                              double* out_x, double* out_y, size_t cap, size_t* out_n,
+                              tlg_mem out_mem, bool throw_empty) {
+  return guard([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(p, "params");
+    check_ptr(out_n, "out_n");
+    *out_n = 0;
+    // center_select.cpp:22-24 then :25 (validate)
+    if (!(p->mesh_resolution > 0.0))
+      throw Error(TLG_INVALID_ARGUMENT, "mesh_resolution must be > 0");
+    if (p->accept_count < 1) throw Error(TLG_INVALID_ARGUMENT, "accept_count must be >= 1");
+    const double* dx = as_device(ctx, S_IN_X, x, m, in_mem);
+    const double* dy = as_device(ctx, S_IN_Y, y, m, in_mem);
+    const double* dz = as_device(ctx, S_IN_Z, z, zn, in_mem);
+    validate_obs_device(ctx, dx, dy, dz, m, zn);
+    const double *nx = nullptr, *ny = nullptr;
+    const size_t n = supported_nodes_device(ctx, dx, dy, m, *p, &nx, &ny);
+    *out_n = n;
+    if (throw_empty && n == 0) throw NoSupported();
+    if (n > cap) throw Error(TLG_BUFFER_TOO_SMALL, "output buffer too small");
+    if (n) {
+      check_ptr(out_x, "out_x");
+      check_ptr(out_y, "out_y");
+      copy_out(ctx, out_x, nx, n * 8, out_mem);
+      copy_out(ctx, out_y, ny, n * 8, out_mem);
+    }
+    ctx->sync();
+  });
+}
+
+tlg_status tlg_supported_mesh_nodes(tlg_ctx* ctx, const double* x, const double* y,
+                                    const double* z, size_t m, size_t z_len, tlg_mem in_mem,
+                                    const tlg_center_params* params, double* out_x,
+                                    double* out_y, size_t cap, size_t* out_n, tlg_mem out_mem) {
+  return select_impl(ctx, x, y, z, m, z_len, in_mem, params, out_x, out_y, cap, out_n, out_mem,
+                     false);
+}
+
+tlg_status tlg_select_centers(tlg_ctx* ctx, const double* x, const double* y, const double* z,
+                              size_t m, size_t z_len, tlg_mem in_mem,
+                              const tlg_center_params* params, double* out_x, double* out_y,
+                              size_t cap, size_t* out_n, tlg_mem out_mem) {
+  return select_impl(ctx, x, y, z, m, z_len, in_mem, params, out_x, out_y, cap, out_n, out_mem,
+                     true);
+}
+
+// ---- model -------------------------------------------------------------------
+tlg_status tlg_model_create(tlg_ctx* ctx, const tlg_kernel_params* kernel,
+                            const tlg_center_params* centers, const double* cx,
+                            const double* cy, size_t n, tlg_mem mem, tlg_model** out) {
+  return guard([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(kernel, "kernel");
+    check_ptr(centers, "centers");
+    check_ptr(out, "out");
+    std::vector<double> hx(n), hy(n);
+    if (n) {
+      check_ptr(cx, "cx");
+      check_ptr(cy, "cy");
+      if (mem == TLG_DEVICE) {
+        TLG_CUDA(cudaMemcpy(hx.data(), cx, n * 8, cudaMemcpyDeviceToHost));
+        TLG_CUDA(cudaMemcpy(hy.data(), cy, n * 8, cudaMemcpyDeviceToHost));
+      } else {
+        std::memcpy(hx.data(), cx, n * 8);
+        std::memcpy(hy.data(), cy, n * 8);
+      }
+    }
+    *out = model_create_impl(ctx, *kernel, *centers, hx.data(), hy.data(), n);
+  });
+}
+
+tlg_status tlg_model_destroy(tlg_model* m) {
+  return guard([&] {
+    if (!m) return;
+    cudaStreamSynchronize(m->ctx->stream);
+    delete m;
+  });
+}
+
+tlg_status tlg_model_counts(const tlg_model* m, size_t* nc, size_t* nb) {
+  return guard([&] {
+    check_ptr(m, "model");
+    if (nc) *nc = m->hcx.size();
+    if (nb) *nb = m->members.size();
+  });
+}
+
+tlg_status tlg_model_kernel(const tlg_model* m, tlg_kernel_params* out) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(out, "out");
+    *out = m->kernel;
+  });
+}
+
+tlg_status tlg_model_center_params(const tlg_model* m, tlg_center_params* out) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(out, "out");
+    *out = m->cparams;
+  });
+}
+
+tlg_status tlg_model_get_centers(tlg_model* m, double* cx, double* cy, tlg_mem mem) {
+  return guard([&] {
+    check_ptr(m, "model");
+    const size_t n = m->hcx.size();
+    if (cx) copy_out(m->ctx, cx, m->cx.p, n * 8, mem);
+    if (cy) copy_out(m->ctx, cy, m->cy.p, n * 8, mem);
+    m->ctx->sync();
+  });
+}
+
+tlg_status tlg_model_get_weights(tlg_model* m, double* w, tlg_mem mem) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(w, "w");
+    copy_out(m->ctx, w, m->w.p, m->hcx.size() * 8, mem);
+    m->ctx->sync();
+  });
+}
+
+tlg_status tlg_model_set_weights(tlg_model* m, const double* w, tlg_mem mem) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(w, "w");
+    copy_in(m->ctx, m->w.p, w, m->hcx.size() * 8, mem);
+    sync_weights_to_grid(m);
+    m->ctx->sync();
+  });
+}
+
+tlg_status tlg_model_get_block_index(tlg_model* m, uint32_t* out, tlg_mem mem) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(out, "out");
+    copy_out(m->ctx, out, m->d_block_index.p, m->hcx.size() * 4, mem);
+    m->ctx->sync();
+  });
+}
+
+tlg_status tlg_model_block_size(const tlg_model* m, uint32_t b, size_t* n) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(n, "n");
+    require(b < m->members.size(), TLG_INVALID_ARGUMENT, "block id out of range");
+    *n = m->members[b].size();
+  });
+}
+
+tlg_status tlg_model_get_block_members(const tlg_model* m, uint32_t b, uint32_t* out) {
+  return guard([&] {
+    check_ptr(m, "model");
+    require(b < m->members.size(), TLG_INVALID_ARGUMENT, "block id out of range");
+    if (!m->members[b].empty()) {
+      check_ptr(out, "out");
+      std::memcpy(out, m->members[b].data(), m->members[b].size() * 4);
+    }
+  });
+}
+
+tlg_status tlg_model_get_block_info_inverse(tlg_model* m, uint32_t b, double* out, tlg_mem mem) {
+  return guard([&] {
+    check_ptr(m, "model");
+    require(b < m->members.size(), TLG_INVALID_ARGUMENT, "block id out of range");
+    const size_t bn = m->members[b].size();
+    if (!bn) return;
+    check_ptr(out, "out");
+    TLG_CUDA(cudaMemcpy2DAsync(out, bn * 8, m->pool.p + m->blk_off[b], m->blk_ld[b] * 8, bn * 8,
+                               bn, mem == TLG_DEVICE ? cudaMemcpyDeviceToDevice
+                                                     : cudaMemcpyDeviceToHost,
+                               m->ctx->stream));
+    m->ctx->sync();
+  });
+}
+
+tlg_status tlg_model_set_block_info_inverse(tlg_model* m, uint32_t b, const double* in,
+                                            tlg_mem mem) {
+  return guard([&] {
+    check_ptr(m, "model");
+    require(b < m->members.size(), TLG_INVALID_ARGUMENT, "block id out of range");
+    const size_t bn = m->members[b].size();
+    if (!bn) return;
+    check_ptr(in, "in");
+    TLG_CUDA(cudaMemcpy2DAsync(m->pool.p + m->blk_off[b], m->blk_ld[b] * 8, in, bn * 8, bn * 8,
+                               bn, mem == TLG_DEVICE ? cudaMemcpyDeviceToDevice
+                                                     : cudaMemcpyHostToDevice,
+                               m->ctx->stream));
+    m->ctx->sync();
+  });
+}
+
+tlg_status tlg_eval(tlg_model* m, const double* x, const double* y, size_t n, tlg_mem in_mem,
+                    double* z, uint8_t* supported, double* gx, double* gy, tlg_mem out_mem) {
+  return guard([&] {
+    check_ptr(m, "model");
+    if (n == 0) return;
+    check_ptr(x, "x");
+    check_ptr(y, "y");
+    tlg_ctx* ctx = m->ctx;
+    const double* dx = as_device(ctx, S_IN_X, x, n, in_mem);
+    const double* dy = as_device(ctx, S_IN_Y, y, n, in_mem);
+    const bool dev = out_mem == TLG_DEVICE;
+    double* dz = z ? (dev ? z : ctx->ws<double>(S_OUT_Z, n)) : nullptr;
+    uint8_t* ds = supported ? (dev ? supported : ctx->ws<uint8_t>(S_OUT_SUP, n)) : nullptr;
+    double* dgx = gx ? (dev ? gx : ctx->ws<double>(S_OUT_GX, n)) : nullptr;
+    double* dgy = gy ? (dev ? gy : ctx->ws<double>(S_OUT_GY, n)) : nullptr;
+    eval_device(m, dx, dy, n, dz, ds, dgx, dgy);
+    if (!dev) {
+      if (z) copy_out(ctx, z, dz, n * 8, TLG_HOST);
+      if (supported) copy_out(ctx, supported, ds, n, TLG_HOST);
+      if (gx) copy_out(ctx, gx, dgx, n * 8, TLG_HOST);
+      if (gy) copy_out(ctx, gy, dgy, n * 8, TLG_HOST);
+      ctx->sync();
+    }
+  });
+}
+
+tlg_status tlg_moment_features(tlg_model* m, const double* x, const double* y, size_t n,
+                               tlg_mem in_mem, uint32_t* row_ptr, uint32_t* ids, double* vals,
+                               size_t cap, size_t* nnz, tlg_mem out_mem) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(nnz, "nnz");
+    *nnz = 0;
+    if (n == 0) return;
+    tlg_ctx* ctx = m->ctx;
+    const double* dx = as_device(ctx, S_IN_X, x, n, in_mem);
+    const double* dy = as_device(ctx, S_IN_Y, y, n, in_mem);
+    uint32_t* drow = ctx->ws<uint32_t>(S_MOMENT_ROW, n + 1);
+    uint32_t* dids = nullptr;
+    double* dvals = nullptr;
+    moment_device(m, dx, dy, n, drow, &dids, &dvals, nnz);
+    if (*nnz > cap) throw Error(TLG_BUFFER_TOO_SMALL, "output buffer too small");
+    if (row_ptr) copy_out(ctx, row_ptr, drow, (n + 1) * 4, out_mem);
+    if (ids) copy_out(ctx, ids, dids, *nnz * 4, out_mem);
+    if (vals) copy_out(ctx, vals, dvals, *nnz * 8, out_mem);
+    ctx->sync();
+  });
+}
+
+tlg_status tlg_manifold_rows(tlg_model* m, const double R[9], const double t[3], const double* hx,
+                             const double* hy, const double* hz, size_t n, tlg_mem in_mem,
+                             double wheel_radius, double lambda_M, double huber_delta, double* r,
+                             double* J, uint8_t* valid, double* raw, tlg_mem out_mem,
+                             tlg_normal_eq* ne) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(R, "R");
+    check_ptr(t, "t");
+    require(lambda_M >= 0.0, TLG_INVALID_ARGUMENT, "lambda_M must be >= 0");
+    if (n == 0) {
+      if (ne) *ne = tlg_normal_eq{};
+      return;
+    }
+    tlg_ctx* ctx = m->ctx;
+    const double* dhx = as_device(ctx, S_IN_HX, hx, n, in_mem);
+    const double* dhy = as_device(ctx, S_IN_HY, hy, n, in_mem);
+    const double* dhz = as_device(ctx, S_IN_HZ, hz, n, in_mem);
+    const bool dev = out_mem == TLG_DEVICE;
+    double* dr = r ? (dev ? r : ctx->ws<double>(S_OUT_R, n)) : nullptr;
+    double* dJ = J ? (dev ? J : ctx->ws<double>(S_OUT_J, 6 * n)) : nullptr;
+    uint8_t* dv = valid ? (dev ? valid : ctx->ws<uint8_t>(S_OUT_SUP, n)) : nullptr;
+    double* draw = raw ? (dev ? raw : ctx->ws<double>(S_OUT_RAW, n)) : nullptr;
+    manifold_device(m, R, t, dhx, dhy, dhz, n, wheel_radius, lambda_M, huber_delta, dr, dJ, dv,
+                    draw, ne);
+    if (!dev) {
+      if (r) copy_out(ctx, r, dr, n * 8, TLG_HOST);
+      if (J) copy_out(ctx, J, dJ, 6 * n * 8, TLG_HOST);
+      if (valid) copy_out(ctx, valid, dv, n, TLG_HOST);
+      if (raw) copy_out(ctx, raw, draw, n * 8, TLG_HOST);
+      ctx->sync();
+    }
+  });
+}
+
+tlg_status tlg_recursive_update(tlg_model* m, const double* x, const double* y, const double* z,
+                                size_t mm, size_t z_len, tlg_mem in_mem, int allow_birth,
+                                tlg_update_report* report) {
+  return guard([&] {
+    check_ptr(m, "model");
+    tlg_ctx* ctx = m->ctx;
+    tlg_update_report rep{};
+    const double* dx = as_device(ctx, S_IN_X, x, mm, in_mem);
+    const double* dy = as_device(ctx, S_IN_Y, y, mm, in_mem);
+    const double* dz = as_device(ctx, S_IN_Z, z, z_len, in_mem);
+    validate_obs_device(ctx, dx, dy, dz, mm, z_len);
+    recursive_update_device(m, dx, dy, dz, mm, allow_birth != 0, &rep);
+    if (report) *report = rep;
+  });
+}
+
+tlg_status tlg_fit_batch_ridge(tlg_ctx* ctx, const tlg_kernel_params* kernel,
+                               const tlg_center_params* centers, const double* cx,
+                               const double* cy, size_t n, const double* x, const double* y,
+                               const double* z, size_t m, size_t z_len, tlg_mem mem,
+                               tlg_model** out) {
+  tlg_model* model = nullptr;
+  tlg_status st = guard([&] {
+    check_ptr(out, "out");
+    // terrain_model.cpp:272 validates before building the model
+    const double* dx = as_device(ctx, S_IN_X, x, m, mem);
+    const double* dy = as_device(ctx, S_IN_Y, y, m, mem);
+    const double* dz = as_device(ctx, S_IN_Z, z, z_len, mem);
+    validate_obs_device(ctx, dx, dy, dz, m, z_len);
+  });
+  if (st != TLG_OK) return st;
+  st = tlg_model_create(ctx, kernel, centers, cx, cy, n, mem, &model);
+  if (st != TLG_OK) return st;
+  st = guard([&] {
+    const double* dx = as_device(ctx, S_IN_X, x, m, mem);
+    const double* dy = as_device(ctx, S_IN_Y, y, m, mem);
+    const double* dz = as_device(ctx, S_IN_Z, z, z_len, mem);
+    batch_fit_device(model, dx, dy, dz, m);
+  });
+  if (st != TLG_OK) {
+    tlg_model_destroy(model);
+    return st;
+  }
+  *out = model;
+  return TLG_OK;
+}
+
+// ---- RBFT snapshot (snapshot.cpp:7-126) ---------------------------------------
+tlg_status tlg_model_save(tlg_model* m, const char* path) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(path, "path");
+    const size_t n = m->hcx.size();
+    std::vector<double> w(n);
+    if (n) {
+      TLG_CUDA(cudaMemcpyAsync(w.data(), m->w.p, n * 8, cudaMemcpyDeviceToHost, m->ctx->stream));
+    }
+    std::vector<std::vector<double>> blocks(m->members.size());
+    for (size_t b = 0; b < m->members.size(); ++b) {
+      const size_t bn = m->members[b].size();
+      blocks[b].resize(bn * bn);
+      if (bn)
+        TLG_CUDA(cudaMemcpy2DAsync(blocks[b].data(), bn * 8, m->pool.p + m->blk_off[b],
+                                   m->blk_ld[b] * 8, bn * 8, bn, cudaMemcpyDeviceToHost,
+                                   m->ctx->stream));
+    }
+    m->ctx->sync();
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw Error(TLG_RUNTIME_ERROR, std::string("cannot open ") + path);
+    auto put32 = [&](uint32_t v) { out.write(reinterpret_cast<const char*>(&v), 4); };
+    auto putd = [&](double v) { out.write(reinterpret_cast<const char*>(&v), 8); };
+    out.write("RBFT", 4);
+    put32(1u);
+    put32(static_cast<uint32_t>(n));
+    put32(static_cast<uint32_t>(m->members.size()));
+    for (size_t i = 0; i < n; ++i) {
+      putd(m->hcx[i]);
+      putd(m->hcy[i]);
+    }
+    for (size_t i = 0; i < n; ++i) putd(w[i]);
+    for (size_t i = 0; i < n; ++i) put32(m->block_index[i]);
+    for (size_t b = 0; b < m->members.size(); ++b) {
+      const size_t bn = m->members[b].size();
+      for (size_t r = 0; r < bn; ++r)
+        for (size_t c = 0; c <= r; ++c) putd(blocks[b][c * bn + r]);  // row-major lower
+    }
+    putd(m->kernel.sigma);
+    putd(m->kernel.sigma_eps);
+    putd(m->kernel.lambda);
+    putd(m->kernel.cutoff_radius);
+    putd(m->cparams.mesh_resolution);
+    putd(m->cparams.accept_radius);
+    put32(static_cast<uint32_t>(m->cparams.accept_count));
+    putd(m->cparams.roi_min_x);
+    putd(m->cparams.roi_min_y);
+    putd(m->cparams.roi_max_x);
+    putd(m->cparams.roi_max_y);
+    if (!out) throw Error(TLG_RUNTIME_ERROR, std::string("write failed: ") + path);
+  });
+}
+
+tlg_status tlg_model_load(tlg_ctx* ctx, const char* path, tlg_model** out) {
+  tlg_model* model = nullptr;
+  tlg_status st = guard([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(path, "path");
+    check_ptr(out, "out");
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw Error(TLG_RUNTIME_ERROR, std::string("cannot open ") + path);
+    auto get32 = [&]() {
+      uint32_t v;
+      in.read(reinterpret_cast<char*>(&v), 4);
+      if (!in) throw Error(TLG_RUNTIME_ERROR, "truncated terrain snapshot");
+      return v;
+    };
+    auto getd = [&]() {
+      double v;
+      in.read(reinterpret_cast<char*>(&v), 8);
+      if (!in) throw Error(TLG_RUNTIME_ERROR, "truncated terrain snapshot");
+      return v;
+    };
+    char magic[4];
+    in.read(magic, 4);
+    if (!in || std::memcmp(magic, "RBFT", 4) != 0)
+      throw Error(TLG_RUNTIME_ERROR, std::string("not a terrain snapshot: ") + path);
+    if (get32() != 1u) throw Error(TLG_RUNTIME_ERROR, "unsupported snapshot version");
+    const uint32_t n = get32(), nb = get32();
+    std::vector<double> cx(n), cy(n), w(n);
+    for (uint32_t i = 0; i < n; ++i) {
+      cx[i] = getd();
+      cy[i] = getd();
+    }
+    for (uint32_t i = 0; i < n; ++i) w[i] = getd();
+    std::vector<uint32_t> bidx(n);
+    std::vector<std::vector<uint32_t>> mem(nb);
+    for (uint32_t i = 0; i < n; ++i) {
+      bidx[i] = get32();
+      if (bidx[i] >= nb) throw Error(TLG_RUNTIME_ERROR, "corrupt block index");
+      mem[bidx[i]].push_back(i);
+    }
+    std::vector<std::vector<double>> blocks(nb);
+    for (uint32_t b = 0; b < nb; ++b) {
+      const size_t bn = mem[b].size();
+      blocks[b].resize(bn * bn);
+      for (size_t r = 0; r < bn; ++r)
+        for (size_t c = 0; c <= r; ++c) {
+          const double v = getd();
+          blocks[b][c * bn + r] = v;
+          blocks[b][r * bn + c] = v;
+        }
+    }
+    tlg_kernel_params k;
+    k.sigma = getd();
+    k.sigma_eps = getd();
+    k.lambda = getd();
+    k.cutoff_radius = getd();
+    tlg_center_params cp{};
+    cp.mesh_resolution = getd();
+    cp.accept_radius = getd();
+    cp.accept_count = static_cast<int32_t>(get32());
+    cp.roi_min_x = getd();
+    cp.roi_min_y = getd();
+    cp.roi_max_x = getd();
+    cp.roi_max_y = getd();
+    // Build with the stored block structure: the snapshot's block ids are
+    // authoritative (snapshot.cpp:89-96,120-123).
+    model = model_create_impl(ctx, k, cp, nullptr, nullptr, 0);
+    model->members = mem;
+    model->block_index = bidx;
+    model->blk_off.assign(nb, 0);
+    model->blk_ld.assign(nb, 0);
+    model->tile_blocks.clear();
+    for (uint32_t i = 0; i < n; ++i) model->tile_blocks.emplace(tile_key(model, cx[i], cy[i]), bidx[i]);
+    model->hcx = cx;
+    model->hcy = cy;
+    for (uint32_t i = 0; i < n; ++i) model->occupancy.insert(mesh_node_key(model, cx[i], cy[i]));
+    size_t total = 0;
+    for (uint32_t b = 0; b < nb; ++b) {
+      const int ld = std::max(8, (static_cast<int>(mem[b].size()) + 7) & ~7);
+      model->blk_ld[b] = ld;
+      model->blk_off[b] = total;
+      total += static_cast<size_t>(ld) * ld;
+    }
+    model->pool.ensure(total + total / 2 + 64);
+    model->pool_used = total;
+    upload_new_centres(model, 0);
+    TLG_CUDA(cudaMemcpyAsync(model->w.p, w.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    for (uint32_t b = 0; b < nb; ++b) {
+      const size_t bn = mem[b].size();
+      if (bn)
+        TLG_CUDA(cudaMemcpy2DAsync(model->pool.p + model->blk_off[b], model->blk_ld[b] * 8,
+                                   blocks[b].data(), bn * 8, bn * 8, bn, cudaMemcpyHostToDevice,
+                                   ctx->stream));
+    }
+    ctx->sync();
+    build_center_grid(model);
+    ctx->sync();
+  });
+  if (st != TLG_OK) {
+    delete model;
+    return st;
+  }
+  *out = model;
+  return TLG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,37 @@
+// Dense FP64 building blocks for the kernel-matrix update (column-major).
+#pragma once
+
+#include "internal.cuh"
+
+namespace tlg {
+
+// C = alpha * op(A) op(B) + beta * C   (op = transpose when t* != 0)
+// uplo = 1 skips CTA tiles strictly above the diagonal (SYRK-style updates).
+struct GemmDesc {
+  int M, N, K;
+  const double* A;
+  int lda, ta;
+  const double* B;
+  int ldb, tb;
+  double* C;
+  int ldc;
+  double alpha, beta;
+  int uplo;
+};
+
+void gemm(tlg_ctx* ctx, const GemmDesc& d);
+// Grouped GEMM over `count` descriptors already resident in device memory.
+void gemm_grouped(tlg_ctx* ctx, const GemmDesc* d_descs, int count, int max_m, int max_n);
+
+// In-place lower Cholesky (A = L L^T) of the n x n matrix at A (lda).
+// `info` (device int) is set non-zero when a pivot is not positive/finite.
+void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info);
+// B <- L^-1 B (trans = 0) or B <- L^-T B (trans = 1); L lower n x n, B n x nrhs.
+void trsm_left_lower(tlg_ctx* ctx, const double* L, int n, int ldl, double* B, int nrhs,
+                     int ldb, int trans);
+// A <- 0.5 (A + A^T) for a square n x n matrix (in place).
+void symmetrize(tlg_ctx* ctx, double* A, int n, int lda);
+// A[i,i] += v
+void add_diag(tlg_ctx* ctx, double* A, int n, int lda, double v);
+
+}  // namespace tlg

@@ -1,0 +1,257 @@
+// Internal declarations of the B200 terralio library (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/terralio_gpu.h"
+
+namespace tlg {
+
+// ---------------------------------------------------------------------------
+// Errors: internal code throws tlg::Error; every ABI entry point converts it
+// into a status code + thread-local message (see guard() in abi.cu).
+struct Error : std::runtime_error {
+  tlg_status status;
+  Error(tlg_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
+
+#define TLG_CUDA(call)                                                       \
+  do {                                                                       \
+    cudaError_t _e = (call);                                                 \
+    if (_e != cudaSuccess) ::tlg::throw_cuda(_e, #call, __FILE__, __LINE__); \
+  } while (0)
+
+#define TLG_LAUNCHED(ctx)                                                    \
+  do {                                                                       \
+    cudaError_t _e = cudaPeekAtLastError();                                  \
+    if (_e != cudaSuccess) ::tlg::throw_cuda(_e, "kernel launch", __FILE__, __LINE__); \
+    ++(ctx)->launches;                                                       \
+  } while (0)
+
+struct NoSupported : Error {
+  NoSupported() : Error(TLG_NO_SUPPORTED_CENTERS, "no supported centers") {}
+};
+
+inline void require(bool ok, tlg_status s, const char* msg) {
+  if (!ok) throw Error(s, msg);
+}
+
+// ---------------------------------------------------------------------------
+// Device buffers.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;    // capacity (elements)
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  // grow-only; contents are NOT preserved
+  T* ensure(size_t count) {
+    if (count <= n && p) return p;
+    release();
+    size_t c = count ? count : 1;
+    cudaError_t e = cudaMalloc(&p, c * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw Error(e == cudaErrorMemoryAllocation ? TLG_OUT_OF_MEMORY : TLG_CUDA_ERROR,
+                  std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    n = c;
+    return p;
+  }
+  // grow preserving the first `keep` elements (stream-ordered copy)
+  T* grow_keep(size_t count, size_t keep, cudaStream_t s) {
+    if (count <= n && p) return p;
+    DBuf nb;
+    nb.ensure(count);
+    if (keep && p) {
+      cudaError_t e = cudaMemcpyAsync(nb.p, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) throw_cuda(e, "grow copy", __FILE__, __LINE__);
+      cudaStreamSynchronize(s);
+    }
+    *this = std::move(nb);
+    return p;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Scratch arena: named grow-only slots, reused across calls.
+enum Slot : int {
+  S_IN_X, S_IN_Y, S_IN_Z, S_IN_HX, S_IN_HY, S_IN_HZ,
+  S_OUT_Z, S_OUT_GX, S_OUT_GY, S_OUT_SUP, S_OUT_R, S_OUT_J, S_OUT_RAW,
+  S_FLAGS, S_PARTIALS, S_CUB, S_CUB2,
+  S_KEYS, S_KEYS2, S_VALS, S_VALS2, S_NODES_X, S_NODES_Y, S_NODE_FLAG, S_NODE_IDX,
+  S_COUNT, S_ACTIVE, S_BLOCKFLAG, S_ROWOF, S_MERGED, S_ROWPTR, S_COLIDX, S_MTVAL,
+  S_KMAT, S_SMAT, S_RESID, S_U, S_YMAT, S_HMAT, S_WORK1, S_WORK2, S_WORK3, S_BLKTAB,
+  S_MOMENT_ROW, S_TROWP, S_TKEYS,
+  S_NUM_SLOTS
+};
+
+struct tlg_ctx_impl;
+
+}  // namespace tlg
+
+// ---------------------------------------------------------------------------
+struct tlg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  uint64_t launches = 0;
+  int num_sms = 148;
+  tlg::DBuf<unsigned char> slots[tlg::S_NUM_SLOTS];
+  // pinned host staging
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+
+  template <typename T>
+  T* ws(int slot, size_t count) {
+    return reinterpret_cast<T*>(slots[slot].ensure(count * sizeof(T) + 16));
+  }
+  void* host_stage(size_t bytes);
+  void sync();
+};
+
+namespace tlg {
+
+// Copy helpers honouring tlg_mem tags.
+void copy_in(tlg_ctx* ctx, void* dst_dev, const void* src, size_t bytes, tlg_mem mem);
+void copy_out(tlg_ctx* ctx, void* dst, const void* src_dev, size_t bytes, tlg_mem mem);
+// Returns a device pointer holding `src` (no copy when already on device).
+template <typename T>
+const T* as_device(tlg_ctx* ctx, int slot, const T* src, size_t n, tlg_mem mem) {
+  if (mem == TLG_DEVICE || n == 0) return src;
+  T* d = ctx->ws<T>(slot, n);
+  copy_in(ctx, d, src, n * sizeof(T), mem);
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// Exact (no-contraction) FP64 helpers: neighbour membership, lattice node
+// coordinates and cell keys must round exactly like the reference's
+// -O3/no-FMA host build.
+__device__ __forceinline__ double sq2_exact(double dx, double dy) {
+  return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+}
+
+// Kernel parameters after KernelParams::finalize, with derived constants.
+struct KernelConst {
+  double sigma, sigma_eps, lambda, cutoff;
+  double r2;          // cutoff * cutoff (kernel.cpp:33, grid_index.hpp:36)
+  double neg_inv_2s2; // -1 / (2 sigma^2)
+  double neg_inv_2st2;// -1 / (2 sigma_tilde^2)
+  double inv_s2;      // 1 / sigma^2 (terrain_model.cpp:129)
+  double scale;       // moment_scale
+  double sigma_tilde;
+};
+KernelConst make_kernel_const(const tlg_kernel_params& k);
+void finalize_kernel(tlg_kernel_params& k);  // kernel.cpp:15-25
+
+// Dense CSR grid over centre cells (GridIndex2 with cell = min(rho, 1e6)).
+struct CenterGrid {
+  double cell = 1.0;
+  int span = 1;
+  int gx0 = 0, gy0 = 0, gnx = 0, gny = 0;
+  DBuf<int> cell_start;        // gnx*gny + 1
+  DBuf<uint32_t> sorted_id;    // centre id in cell order (ids ascending inside a cell)
+  DBuf<double> scx, scy, sw;   // centres/weights in cell order
+};
+
+struct GridView {
+  const double* cx;
+  const double* cy;
+  const double* w;
+  const uint32_t* id;
+  const int* cell_start;
+  double cell;
+  int span, gx0, gy0, gnx, gny;
+};
+
+}  // namespace tlg
+
+// ---------------------------------------------------------------------------
+struct tlg_model {
+  tlg_ctx* ctx = nullptr;
+  tlg_kernel_params kernel{};
+  tlg_center_params cparams{};
+  tlg::KernelConst kc{};
+
+  // Host mirror of the model *structure* (ids, blocks, tiles, occupancy),
+  // the reference's bookkeeping in terrain_model.cpp:26-95.
+  std::vector<double> hcx, hcy;
+  std::vector<uint32_t> block_index;
+  std::vector<std::vector<uint32_t>> members;
+  std::unordered_map<int64_t, uint32_t> tile_blocks;
+  std::unordered_set<int64_t> occupancy;
+
+  // Device numeric state.
+  tlg::DBuf<double> cx, cy, w;
+  tlg::DBuf<uint32_t> d_block_index;
+  size_t dev_cap = 0;
+  // block info_inv pool: column-major, ld = blk_ld[b]
+  tlg::DBuf<double> pool;
+  size_t pool_used = 0;
+  std::vector<size_t> blk_off;
+  std::vector<int> blk_ld;
+  tlg::CenterGrid grid;
+  bool grid_dirty = true;
+};
+
+namespace tlg {
+int64_t pack2(int64_t x, int64_t y);
+int64_t tile_key(const tlg_model* m, double cx, double cy);
+int64_t mesh_node_key(const tlg_model* m, double x, double y);
+uint32_t block_for_tile(tlg_model* m, int64_t key);
+
+void build_center_grid(tlg_model* m);      // grid.cu
+GridView grid_view(const tlg_model* m);    // grid.cu
+void ensure_grid(tlg_model* m);
+void sync_weights_to_grid(tlg_model* m);   // after weights change
+
+// blocks / pool (model.cu)
+void pool_reserve_block(tlg_model* m, uint32_t b, int new_size);
+
+// select.cu: runs the support count over the lattice window; returns node
+// count, writes nodes (device) into ctx slots S_NODES_X/Y. If occupancy_model
+// is non-null, nodes already occupied in it are dropped (birth filter).
+size_t supported_nodes_device(tlg_ctx* ctx, const double* dx, const double* dy, size_t m,
+                              const tlg_center_params& p, const double** out_x,
+                              const double** out_y);
+void validate_obs_device(tlg_ctx* ctx, const double* x, const double* y, const double* z,
+                         size_t m, size_t zn);
+
+// eval.cu
+void eval_device(tlg_model* m, const double* x, const double* y, size_t n, double* z,
+                 uint8_t* sup, double* gx, double* gy);
+void manifold_device(tlg_model* m, const double R[9], const double t[3], const double* hx,
+                     const double* hy, const double* hz, size_t n, double wheel_radius,
+                     double lambda_M, double huber, double* r, double* J, uint8_t* valid,
+                     double* raw, tlg_normal_eq* ne);
+
+// update.cu
+void recursive_update_device(tlg_model* m, const double* x, const double* y, const double* z,
+                             size_t mm, bool allow_birth, tlg_update_report* rep);
+void batch_fit_device(tlg_model* m, const double* x, const double* y, const double* z,
+                      size_t mm);
+
+}  // namespace tlg

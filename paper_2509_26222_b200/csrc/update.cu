@@ -1,0 +1,726 @@
+// K5-K8: TerrainModel::recursive_update (terrain_model.cpp:145-253) and
+// fit_batch_ridge (:269-308) on the device.
+//
+// Host side keeps only the model *structure* (births, block/tile ids — the
+// reference's integer bookkeeping); every floating-point step runs in a
+// kernel:
+//   K5  sparse moment matrix Mt as CSR over observations (ids bit-exact,
+//       values s * kappa_sigma_tilde, dropping kappa == 0 like :193);
+//   K6  Gram / Woodbury products on the sparse pattern;
+//   K7  the solve, in one of two algebraically identical forms:
+//       (W) one-shot Woodbury (m <= n): S = I + Mt^T Hinv0 Mt (m x m),
+//           w1 = w0 + K S^-1 (z - Mt^T w0), diag blocks of
+//           Hinv1 = Hinv0 - (L^-1 K^T)^T (L^-1 K^T);
+//       (I) information form (m > n): H1 = blockdiag(info_inv)^-1 + Mt Mt^T,
+//           w1 = w0 + H1^-1 Mt (z - Mt^T w0), diag blocks of H1^-1;
+//       both equal the reference's chunk-64 Woodbury composition in exact
+//       arithmetic (comment at :211-212); dense products use DMMA.
+//   Re-split keeps only the active diagonal blocks, symmetrised (:239-251).
+// A failed (non-PD) inner factorisation reports `rejected` and leaves
+// weights/blocks untouched while births persist (:222-225).
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <map>
+
+#include "dense.cuh"
+
+namespace tlg {
+
+void block_resize(tlg_model* m, uint32_t b, int old_n, int new_n);
+void upload_new_centres(tlg_model* m, size_t first);
+uint32_t add_center_host(tlg_model* m, double x, double y);
+
+// ---------------------------------------------------------------------------
+// Neighbour sweep shared by the CSR builders (same cells/test as K3).
+struct Sweep {
+  int x_lo, x_hi, y_lo, y_hi;
+};
+__device__ __forceinline__ Sweep sweep_of(const GridView& g, double px, double py) {
+  const int qx = static_cast<int>(floor(px / g.cell));
+  const int qy = static_cast<int>(floor(py / g.cell));
+  Sweep s;
+  s.y_lo = max(qy - g.span - g.gy0, 0);
+  s.y_hi = min(qy + g.span - g.gy0, g.gny - 1);
+  s.x_lo = max(qx - g.span - g.gx0, 0);
+  s.x_hi = min(qx + g.span - g.gx0, g.gnx - 1);
+  if (s.y_lo > s.y_hi) s.x_hi = s.x_lo - 1;
+  return s;
+}
+
+__global__ void k_mark_active(GridView g, const double* __restrict__ x,
+                              const double* __restrict__ y, size_t m, double r2,
+                              uint8_t* __restrict__ active) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < m;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const double px = x[i], py = y[i];
+    const Sweep s = sweep_of(g, px, py);
+    for (int gx = s.x_lo; gx <= s.x_hi; ++gx) {
+      const int b = g.cell_start[gx * g.gny + s.y_lo], e = g.cell_start[gx * g.gny + s.y_hi + 1];
+      for (int k = b; k < e; ++k)
+        if (sq2_exact(g.cx[k] - px, g.cy[k] - py) <= r2) active[g.id[k]] = 1;
+    }
+  }
+}
+
+__global__ void k_mark_blocks(const uint8_t* __restrict__ active,
+                              const uint32_t* __restrict__ bidx, size_t n,
+                              uint8_t* __restrict__ bflag) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i < n && active[i]) bflag[bidx[i]] = 1;
+}
+
+__global__ void k_scatter_rowof(const uint32_t* __restrict__ merged, int n,
+                                int* __restrict__ rowof) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) rowof[merged[r]] = r;
+}
+
+// CSR count / fill over observations: entry (col, s * exp(-d2/(2 b^2))) for
+// every candidate with d2 <= cutoff^2 and kappa != 0. col = rowof[id] or id.
+__global__ void k_csr_count(GridView g, const double* __restrict__ x, const double* __restrict__ y,
+                            size_t m, double r2, double neg_inv_2b2, uint32_t* __restrict__ cnt) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const double px = x[i], py = y[i];
+  const Sweep s = sweep_of(g, px, py);
+  uint32_t c = 0;
+  for (int gx = s.x_lo; gx <= s.x_hi; ++gx) {
+    const int b = g.cell_start[gx * g.gny + s.y_lo], e = g.cell_start[gx * g.gny + s.y_hi + 1];
+    for (int k = b; k < e; ++k) {
+      const double d2 = sq2_exact(g.cx[k] - px, g.cy[k] - py);
+      if (d2 <= r2 && exp(d2 * neg_inv_2b2) != 0.0) ++c;
+    }
+  }
+  cnt[i] = c;
+}
+
+__global__ void k_csr_fill(GridView g, const double* __restrict__ x, const double* __restrict__ y,
+                           size_t m, double r2, double neg_inv_2b2, double scale,
+                           const uint32_t* __restrict__ rowp, const int* __restrict__ rowof,
+                           uint32_t* __restrict__ col, double* __restrict__ val, int sort_ids) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const double px = x[i], py = y[i];
+  const Sweep s = sweep_of(g, px, py);
+  uint32_t o = rowp[i];
+  const uint32_t o0 = o;
+  for (int gx = s.x_lo; gx <= s.x_hi; ++gx) {
+    const int b = g.cell_start[gx * g.gny + s.y_lo], e = g.cell_start[gx * g.gny + s.y_hi + 1];
+    for (int k = b; k < e; ++k) {
+      const double d2 = sq2_exact(g.cx[k] - px, g.cy[k] - py);
+      if (d2 <= r2) {
+        const double kv = exp(d2 * neg_inv_2b2);
+        if (kv != 0.0) {
+          const uint32_t id = g.id[k];
+          col[o] = rowof ? static_cast<uint32_t>(rowof[id]) : id;
+          val[o] = scale * kv;
+          ++o;
+        }
+      }
+    }
+  }
+  if (sort_ids)
+    for (uint32_t a = o0 + 1; a < o; ++a) {
+      const uint32_t ki = col[a];
+      const double kvv = val[a];
+      uint32_t b = a;
+      while (b > o0 && col[b - 1] > ki) {
+        col[b] = col[b - 1];
+        val[b] = val[b - 1];
+        --b;
+      }
+      col[b] = ki;
+      val[b] = kvv;
+    }
+}
+
+struct Csr {
+  uint32_t* rowp = nullptr;
+  uint32_t* col = nullptr;
+  double* val = nullptr;
+  size_t nnz = 0;
+};
+
+// Builds the CSR in ctx slots (rowp may be supplied).
+static Csr build_csr(tlg_model* m, const double* x, const double* y, size_t mm, const int* rowof,
+                     double neg_inv_2b2, double scale, bool sort_ids, uint32_t* rowp_in) {
+  tlg_ctx* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  Csr c;
+  c.rowp = rowp_in ? rowp_in : ctx->ws<uint32_t>(S_ROWPTR, mm + 1);
+  const GridView g = grid_view(m);
+  const unsigned nb = static_cast<unsigned>((mm + 127) / 128);
+  k_csr_count<<<nb, 128, 0, s>>>(g, x, y, mm, m->kc.r2, neg_inv_2b2, c.rowp);
+  TLG_LAUNCHED(ctx);
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.rowp, c.rowp, (int)(mm + 1), s);
+  void* dtmp = ctx->ws<unsigned char>(S_CUB, tmp);
+  // the count array has mm entries; entry mm must be 0 before the scan
+  TLG_CUDA(cudaMemsetAsync(c.rowp + mm, 0, sizeof(uint32_t), s));
+  TLG_CUDA(cub::DeviceScan::ExclusiveSum(dtmp, tmp, c.rowp, c.rowp, (int)(mm + 1), s));
+  ++ctx->launches;
+  uint32_t hn = 0;
+  TLG_CUDA(cudaMemcpyAsync(&hn, c.rowp + mm, 4, cudaMemcpyDeviceToHost, s));
+  TLG_CUDA(cudaStreamSynchronize(s));
+  c.nnz = hn;
+  c.col = ctx->ws<uint32_t>(S_COLIDX, hn + 1);
+  c.val = ctx->ws<double>(S_MTVAL, hn + 1);
+  k_csr_fill<<<nb, 128, 0, s>>>(g, x, y, mm, m->kc.r2, neg_inv_2b2, scale, c.rowp, rowof, c.col,
+                                c.val, sort_ids ? 1 : 0);
+  TLG_LAUNCHED(ctx);
+  return c;
+}
+
+void moment_device(tlg_model* m, const double* x, const double* y, size_t n, uint32_t* rowp,
+                   uint32_t** ids, double** vals, size_t* nnz) {
+  ensure_grid(m);
+  tlg_ctx* ctx = m->ctx;
+  // domain check (terrain_model.cpp:98)
+  validate_obs_device(ctx, x, y, x, n, n);
+  const Csr c = build_csr(m, x, y, n, nullptr, m->kc.neg_inv_2st2, m->kc.scale, true, rowp);
+  *ids = c.col;
+  *vals = c.val;
+  *nnz = c.nnz;
+}
+
+// ---------------------------------------------------------------------------
+// Merged-system bookkeeping.
+struct BlockTab {  // per merged block q
+  size_t pool_off;
+  int ld;
+  int n;        // n_q
+  int off;      // first merged row
+  int pad;
+};
+
+__global__ void k_residual(const uint32_t* __restrict__ rowp, const uint32_t* __restrict__ col,
+                           const double* __restrict__ val, const double* __restrict__ z,
+                           const double* __restrict__ wm, size_t m, double* __restrict__ resid) {
+  const size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double s = 0.0;
+  for (uint32_t e = rowp[j]; e < rowp[j + 1]; ++e) s = fma(val[e], wm[col[e]], s);
+  resid[j] = z[j] - s;
+}
+
+__global__ void k_gather_w(const double* __restrict__ w, const uint32_t* __restrict__ merged, int n,
+                           double* __restrict__ wm) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) wm[r] = w[merged[r]];
+}
+
+__global__ void k_apply_dw(double* __restrict__ w, const uint32_t* __restrict__ merged, int n,
+                           const double* __restrict__ dw) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) w[merged[r]] += dw[r];
+}
+
+// Kt (m x n, ld m) = (Hinv0 Mt)^T ; one CTA per observation. Each (j, row)
+// is only touched by one thread -> deterministic, no atomics.
+__global__ void __launch_bounds__(128) k_build_Kt(
+    const uint32_t* __restrict__ rowp, const uint32_t* __restrict__ col,
+    const double* __restrict__ val, const int* __restrict__ rowblk,
+    const int* __restrict__ rowloc, const BlockTab* __restrict__ tab,
+    const double* __restrict__ pool, int m, double* __restrict__ Kt) {
+  const int j = blockIdx.x;
+  for (uint32_t e = rowp[j]; e < rowp[j + 1]; ++e) {
+    const int r = static_cast<int>(col[e]);
+    const BlockTab t = tab[rowblk[r]];
+    const double v = val[e];
+    const double* hcol = pool + t.pool_off + static_cast<size_t>(rowloc[r]) * t.ld;
+    for (int i = threadIdx.x; i < t.n; i += blockDim.x) {
+      double* p = Kt + j + static_cast<size_t>(t.off + i) * m;
+      *p = fma(hcol[i], v, *p);
+    }
+  }
+}
+
+// S = I + Mt^T K (m x m): CTA per row i, threads over columns j.
+__global__ void __launch_bounds__(256) k_build_S(const uint32_t* __restrict__ rowp,
+                                                 const uint32_t* __restrict__ col,
+                                                 const double* __restrict__ val,
+                                                 const double* __restrict__ Kt, int m,
+                                                 double* __restrict__ S) {
+  const int i = blockIdx.x;
+  const uint32_t b = rowp[i], e = rowp[i + 1];
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    double s = 0.0;
+    for (uint32_t q = b; q < e; ++q) s = fma(val[q], Kt[j + static_cast<size_t>(col[q]) * m], s);
+    S[i + static_cast<size_t>(j) * m] = s + (i == j ? 1.0 : 0.0);
+  }
+}
+
+// Symmetrise every merged block of the pool in place.
+__global__ void k_symmetrize_blocks(const BlockTab* __restrict__ tab, double* __restrict__ pool) {
+  const BlockTab t = tab[blockIdx.x];
+  double* a = pool + t.pool_off;
+  for (int e = threadIdx.x; e < t.n * t.n; e += blockDim.x) {
+    const int r = e % t.n, c = e / t.n;
+    if (r > c) {
+      const double v = 0.5 * (a[r + (size_t)c * t.ld] + a[c + (size_t)r * t.ld]);
+      a[r + (size_t)c * t.ld] = v;
+      a[c + (size_t)r * t.ld] = v;
+    }
+  }
+}
+
+// Transposed CSR (rows of Mt): bucket entries by row, j ascending.
+__global__ void k_expand_rows(const uint32_t* __restrict__ rowp, size_t m,
+                              uint32_t* __restrict__ obs_of) {
+  const size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  for (uint32_t e = rowp[j]; e < rowp[j + 1]; ++e) obs_of[e] = static_cast<uint32_t>(j);
+}
+
+__global__ void k_row_hist(const uint32_t* __restrict__ col, size_t nnz, uint32_t* __restrict__ cnt) {
+  const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (e < nnz) atomicAdd(&cnt[col[e]], 1u);
+}
+
+// Gram row r: G[r, :] = sum_{j in row r} v_rj * Mt[:, j]; shared-memory row
+// accumulator, observations in ascending order -> deterministic. Adds into
+// column r of H (H symmetric, col-major) so writes are coalesced.
+__global__ void __launch_bounds__(128) k_gram_rows(
+    const uint32_t* __restrict__ trowp, const uint32_t* __restrict__ tobs,
+    const double* __restrict__ tval, const uint32_t* __restrict__ rowp,
+    const uint32_t* __restrict__ col, const double* __restrict__ val, int n,
+    double* __restrict__ H, int ldh) {
+  extern __shared__ double acc[];
+  const int r = blockIdx.x;
+  for (int s = threadIdx.x; s < n; s += blockDim.x) acc[s] = 0.0;
+  __syncthreads();
+  for (uint32_t q = trowp[r]; q < trowp[r + 1]; ++q) {
+    const uint32_t j = tobs[q];
+    const double vr = tval[q];
+    for (uint32_t e = rowp[j] + threadIdx.x; e < rowp[j + 1]; e += blockDim.x)
+      acc[col[e]] = fma(vr, val[e], acc[col[e]]);
+    __syncthreads();
+  }
+  for (int s = threadIdx.x; s < n; s += blockDim.x) H[s + (size_t)r * ldh] += acc[s];
+}
+
+// rhs b[r] = sum_{j in row r} v_rj * c_j  (c = residual or z)
+__global__ void k_row_dot(const uint32_t* __restrict__ trowp, const uint32_t* __restrict__ tobs,
+                          const double* __restrict__ tval, const double* __restrict__ c, int n,
+                          double* __restrict__ b) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double s = 0.0;
+  for (uint32_t q = trowp[r]; q < trowp[r + 1]; ++q) s = fma(tval[q], c[tobs[q]], s);
+  b[r] = s;
+}
+
+__global__ void k_copy_to_pool_blocks(const BlockTab* __restrict__ tab, const double* __restrict__ H,
+                                      int ldh, double* __restrict__ pool) {
+  const BlockTab t = tab[blockIdx.x];
+  for (int e = threadIdx.x; e < t.n * t.n; e += blockDim.x) {
+    const int r = e % t.n, c = e / t.n;
+    pool[t.pool_off + r + (size_t)c * t.ld] = H[(t.off + r) + (size_t)(t.off + c) * ldh];
+  }
+}
+
+__global__ void k_set_identity(double* __restrict__ X, int n, int ld) {
+  const long long tot = (long long)n * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(e % n), c = static_cast<int>(e / n);
+    X[r + (size_t)c * ld] = (r == c) ? 1.0 : 0.0;
+  }
+}
+
+__global__ void k_diag_minmax(const double* __restrict__ L, int n, int ld, double* __restrict__ out) {
+  double mx = 0.0, mn = INFINITY;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double d = L[i + (size_t)i * ld];
+    const double v = d * d;
+    mx = fmax(mx, fabs(v));
+    mn = fmin(mn, fabs(v));
+  }
+  __shared__ double smx[256], smn[256];
+  smx[threadIdx.x] = mx;
+  smn[threadIdx.x] = mn;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)blockDim.x; ++i) {
+      mx = fmax(mx, smx[i]);
+      mn = fmin(mn, smn[i]);
+    }
+    out[0] = mx;
+    out[1] = mn;
+  }
+}
+
+// SPD inverse of the n x n matrix src (lds) into dst (ldd) via Cholesky.
+static bool spd_inverse(tlg_ctx* ctx, const double* src, int lds, int n, double* dst, int ldd) {
+  double* T = ctx->ws<double>(S_WORK2, static_cast<size_t>(n) * n);
+  int* info = ctx->ws<int>(S_FLAGS, 4) + 1;
+  TLG_CUDA(cudaMemsetAsync(info, 0, sizeof(int), ctx->stream));
+  TLG_CUDA(cudaMemcpy2DAsync(T, n * 8, src, lds * 8, n * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
+  potrf_lower(ctx, T, n, n, info);
+  k_set_identity<<<std::max(1, std::min(n * n / 256 + 1, 1024)), 256, 0, ctx->stream>>>(dst, n, ldd);
+  TLG_LAUNCHED(ctx);
+  trsm_left_lower(ctx, T, n, n, dst, n, ldd, 0);
+  trsm_left_lower(ctx, T, n, n, dst, n, ldd, 1);
+  int h = 0;
+  TLG_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TLG_CUDA(cudaStreamSynchronize(ctx->stream));
+  symmetrize(ctx, dst, n, ldd);
+  return h == 0;
+}
+
+__global__ void k_iota(uint32_t* __restrict__ a, size_t n) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i < n) a[i] = static_cast<uint32_t>(i);
+}
+static void iota_u32(tlg_ctx* ctx, uint32_t* a, size_t n) {
+  k_iota<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(a, n);
+  TLG_LAUNCHED(ctx);
+}
+__global__ void k_gather_tcsr(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ obs_of,
+                              const double* __restrict__ val, size_t nnz, uint32_t* __restrict__ tobs,
+                              double* __restrict__ tval) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= nnz) return;
+  const uint32_t e = perm[i];
+  tobs[i] = obs_of[e];
+  tval[i] = val[e];
+}
+static void gather_tcsr(tlg_ctx* ctx, const uint32_t* perm, const uint32_t* obs_of, const double* val,
+                 size_t nnz, uint32_t* tobs, double* tval) {
+  k_gather_tcsr<<<(unsigned)((nnz + 255) / 256), 256, 0, ctx->stream>>>(perm, obs_of, val, nnz, tobs, tval);
+  TLG_LAUNCHED(ctx);
+}
+
+// Transposed CSR of Mt (by merged row). Returns trowp (n+1), tobs, tval.
+struct TCsr {
+  uint32_t* rowp;
+  uint32_t* obs;
+  double* val;
+};
+static TCsr transpose_csr(tlg_ctx* ctx, const Csr& c, size_t m, int n) {
+  cudaStream_t s = ctx->stream;
+  TCsr t;
+  t.rowp = ctx->ws<uint32_t>(S_TROWP, n + 1);
+  uint32_t* obs_of = ctx->ws<uint32_t>(S_KEYS, c.nnz + 1);
+  uint32_t* col_sorted = ctx->ws<uint32_t>(S_KEYS2, c.nnz + 1);
+  t.obs = ctx->ws<uint32_t>(S_VALS, c.nnz + 1);
+  t.val = ctx->ws<double>(S_U, c.nnz + 1);
+  if (c.nnz) {
+    k_expand_rows<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(c.rowp, m, obs_of);
+    TLG_LAUNCHED(ctx);
+  }
+  TLG_CUDA(cudaMemsetAsync(t.rowp, 0, (n + 1) * sizeof(uint32_t), s));
+  if (c.nnz) {
+    k_row_hist<<<(unsigned)((c.nnz + 255) / 256), 256, 0, s>>>(c.col, c.nnz, t.rowp);
+    TLG_LAUNCHED(ctx);
+  }
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, t.rowp, t.rowp, n + 1, s);
+  void* dtmp = ctx->ws<unsigned char>(S_CUB, tmp);
+  TLG_CUDA(cub::DeviceScan::ExclusiveSum(dtmp, tmp, t.rowp, t.rowp, n + 1, s));
+  ++ctx->launches;
+  if (c.nnz) {
+    // stable sort of entry index by row keeps observations ascending per row
+    uint32_t* eidx = ctx->ws<uint32_t>(S_VALS2, c.nnz + 1);
+    uint32_t* eidx_sorted = ctx->ws<uint32_t>(S_NODE_IDX, c.nnz + 1);
+    TLG_CUDA(cudaMemcpyAsync(col_sorted, c.col, c.nnz * 4, cudaMemcpyDeviceToDevice, s));
+    tmp = 0;
+    int end_bit = 1;
+    while (end_bit < 32 && (1u << end_bit) < static_cast<uint32_t>(n)) ++end_bit;
+    iota_u32(ctx, eidx, c.nnz);
+    uint32_t* keys_out = ctx->ws<uint32_t>(S_TKEYS, c.nnz + 1);
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, col_sorted, keys_out, eidx, eidx_sorted,
+                                    (int)c.nnz, 0, end_bit, s);
+    dtmp = ctx->ws<unsigned char>(S_CUB2, tmp);
+    TLG_CUDA(cub::DeviceRadixSort::SortPairs(dtmp, tmp, col_sorted, keys_out, eidx, eidx_sorted,
+                                             (int)c.nnz, 0, end_bit, s));
+    ++ctx->launches;
+    gather_tcsr(ctx, eidx_sorted, obs_of, c.val, c.nnz, t.obs, t.val);
+  }
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+void recursive_update_device(tlg_model* m, const double* x, const double* y, const double* z,
+                             size_t mm, bool allow_birth, tlg_update_report* rep) {
+  tlg_ctx* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  *rep = tlg_update_report{};
+
+  // ---- births (terrain_model.cpp:150-161) --------------------------------
+  if (allow_birth) {
+    const tlg_center_params& cp = m->cparams;
+    if (!(cp.mesh_resolution > 0.0))
+      throw Error(TLG_INVALID_ARGUMENT, "mesh_resolution must be > 0");
+    if (cp.accept_count < 1) throw Error(TLG_INVALID_ARGUMENT, "accept_count must be >= 1");
+    const double *nx = nullptr, *ny = nullptr;
+    const size_t nn = supported_nodes_device(ctx, x, y, mm, cp, &nx, &ny);
+    if (nn) {
+      std::vector<double> hx(nn), hy(nn);
+      TLG_CUDA(cudaMemcpyAsync(hx.data(), nx, nn * 8, cudaMemcpyDeviceToHost, s));
+      TLG_CUDA(cudaMemcpyAsync(hy.data(), ny, nn * 8, cudaMemcpyDeviceToHost, s));
+      TLG_CUDA(cudaStreamSynchronize(s));
+      const size_t first = m->hcx.size();
+      std::map<uint32_t, int> old_size;
+      for (size_t k = 0; k < nn; ++k) {
+        if (m->occupancy.count(mesh_node_key(m, hx[k], hy[k]))) continue;
+        const uint32_t b = block_for_tile(m, tile_key(m, hx[k], hy[k]));
+        if (!old_size.count(b)) old_size[b] = static_cast<int>(m->members[b].size());
+        add_center_host(m, hx[k], hy[k]);
+        ++rep->born_centers;
+      }
+      if (rep->born_centers) {
+        upload_new_centres(m, first);
+        for (const auto& [b, old] : old_size)
+          block_resize(m, b, old, static_cast<int>(m->members[b].size()));
+      }
+    }
+  }
+  ensure_grid(m);
+  const size_t nc = m->hcx.size();
+  const size_t nb = m->members.size();
+  if (nc == 0) return;
+
+  // ---- active set (:163-172) ---------------------------------------------
+  const GridView g = grid_view(m);
+  uint8_t* active = ctx->ws<uint8_t>(S_ACTIVE, nc);
+  uint8_t* bflag = ctx->ws<uint8_t>(S_BLOCKFLAG, nb);
+  TLG_CUDA(cudaMemsetAsync(active, 0, nc, s));
+  TLG_CUDA(cudaMemsetAsync(bflag, 0, nb, s));
+  k_mark_active<<<(unsigned)std::min<size_t>((mm + 127) / 128, 8 * 148), 128, 0, s>>>(
+      g, x, y, mm, m->kc.r2, active);
+  TLG_LAUNCHED(ctx);
+  k_mark_blocks<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(active, m->d_block_index.p, nc, bflag);
+  TLG_LAUNCHED(ctx);
+  std::vector<uint8_t> hflag(nb);
+  TLG_CUDA(cudaMemcpyAsync(hflag.data(), bflag, nb, cudaMemcpyDeviceToHost, s));
+  TLG_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint32_t> ablocks;
+  for (uint32_t b = 0; b < nb; ++b)
+    if (hflag[b]) ablocks.push_back(b);  // std::set order = ascending ids
+  rep->active_blocks = ablocks.size();
+  if (ablocks.empty()) return;
+
+  // ---- merged system (:174-184) ------------------------------------------
+  std::vector<uint32_t> merged;
+  std::vector<BlockTab> tab(ablocks.size());
+  std::vector<int> rowblk, rowloc;
+  for (size_t q = 0; q < ablocks.size(); ++q) {
+    const uint32_t b = ablocks[q];
+    tab[q].pool_off = m->blk_off[b];
+    tab[q].ld = m->blk_ld[b];
+    tab[q].n = static_cast<int>(m->members[b].size());
+    tab[q].off = static_cast<int>(merged.size());
+    for (size_t i = 0; i < m->members[b].size(); ++i) {
+      merged.push_back(m->members[b][i]);
+      rowblk.push_back(static_cast<int>(q));
+      rowloc.push_back(static_cast<int>(i));
+    }
+  }
+  const int n = static_cast<int>(merged.size());
+  const int nq = static_cast<int>(ablocks.size());
+  rep->active_centers = static_cast<uint64_t>(n);
+  int maxq = 0;
+  for (const auto& t : tab) maxq = std::max(maxq, t.n);
+
+  // pinned staging for the small host->device tables
+  const size_t bytes_merged = n * 4, bytes_tab = nq * sizeof(BlockTab), bytes_rb = n * 4;
+  char* stage = static_cast<char*>(ctx->host_stage(bytes_merged + bytes_tab + 2 * bytes_rb + 64));
+  std::memcpy(stage, merged.data(), bytes_merged);
+  std::memcpy(stage + bytes_merged, tab.data(), bytes_tab);
+  std::memcpy(stage + bytes_merged + bytes_tab, rowblk.data(), bytes_rb);
+  std::memcpy(stage + bytes_merged + bytes_tab + bytes_rb, rowloc.data(), bytes_rb);
+  char* dstage = ctx->ws<char>(S_MERGED, bytes_merged + bytes_tab + 2 * bytes_rb + 64);
+  // BlockTab needs 8-byte alignment: place it first in device memory
+  BlockTab* d_tab = reinterpret_cast<BlockTab*>(dstage);
+  uint32_t* d_merged = reinterpret_cast<uint32_t*>(dstage + bytes_tab);
+  int* d_rowblk = reinterpret_cast<int*>(dstage + bytes_tab + bytes_merged);
+  int* d_rowloc = reinterpret_cast<int*>(dstage + bytes_tab + bytes_merged + bytes_rb);
+  TLG_CUDA(cudaMemcpyAsync(d_tab, stage + bytes_merged, bytes_tab, cudaMemcpyHostToDevice, s));
+  TLG_CUDA(cudaMemcpyAsync(d_merged, stage, bytes_merged, cudaMemcpyHostToDevice, s));
+  TLG_CUDA(cudaMemcpyAsync(d_rowblk, stage + bytes_merged + bytes_tab, 2 * bytes_rb,
+                           cudaMemcpyHostToDevice, s));
+
+  int* rowof = ctx->ws<int>(S_ROWOF, nc);
+  TLG_CUDA(cudaMemsetAsync(rowof, 0xff, nc * 4, s));
+  k_scatter_rowof<<<(n + 255) / 256, 256, 0, s>>>(d_merged, n, rowof);
+  TLG_LAUNCHED(ctx);
+
+  // ---- K5: Mt (CSR over observations, cols = merged rows) -----------------
+  const Csr c = build_csr(m, x, y, mm, rowof, m->kc.neg_inv_2st2, m->kc.scale, false, nullptr);
+  double* wm = ctx->ws<double>(S_WORK1, n);
+  k_gather_w<<<(n + 255) / 256, 256, 0, s>>>(m->w.p, d_merged, n, wm);
+  TLG_LAUNCHED(ctx);
+  double* resid = ctx->ws<double>(S_RESID, mm);
+  k_residual<<<(unsigned)((mm + 255) / 256), 256, 0, s>>>(c.rowp, c.col, c.val, z, wm, mm, resid);
+  TLG_LAUNCHED(ctx);
+
+  int* info = ctx->ws<int>(S_FLAGS, 4);
+  TLG_CUDA(cudaMemsetAsync(info, 0, 4 * sizeof(int), s));
+  double* dw = ctx->ws<double>(S_WORK3, n);
+  const int mi = static_cast<int>(mm);
+  std::vector<GemmDesc> descs(nq);
+
+  if (mm <= static_cast<size_t>(n)) {
+    // ---- (W) one-shot Woodbury ----------------------------------------------
+    rep->solver = 1;
+    double* Kt = ctx->ws<double>(S_KMAT, static_cast<size_t>(mi) * n);
+    TLG_CUDA(cudaMemsetAsync(Kt, 0, sizeof(double) * mi * n, s));
+    k_build_Kt<<<mi, 128, 0, s>>>(c.rowp, c.col, c.val, d_rowblk, d_rowloc, d_tab, m->pool.p, mi, Kt);
+    TLG_LAUNCHED(ctx);
+    double* S = ctx->ws<double>(S_SMAT, static_cast<size_t>(mi) * mi);
+    k_build_S<<<mi, 256, 0, s>>>(c.rowp, c.col, c.val, Kt, mi, S);
+    TLG_LAUNCHED(ctx);
+    symmetrize(ctx, S, mi, mi);
+    potrf_lower(ctx, S, mi, mi, info);
+    int h = 0;
+    TLG_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    TLG_CUDA(cudaStreamSynchronize(s));
+    if (h) {
+      rep->rejected = 1;
+      return;
+    }
+    // u = S^-1 r ; dw = K u
+    trsm_left_lower(ctx, S, mi, mi, resid, 1, mi, 0);
+    trsm_left_lower(ctx, S, mi, mi, resid, 1, mi, 1);
+    gemm(ctx, GemmDesc{n, 1, mi, Kt, mi, 1, resid, mi, 0, dw, n, 1.0, 0.0, 0});
+    // Y = L^-1 K^T (in place) ; Hinv1_q = Hinv0_q - Y_q^T Y_q
+    trsm_left_lower(ctx, S, mi, mi, Kt, n, mi, 0);
+    for (int q = 0; q < nq; ++q)
+      descs[q] = GemmDesc{tab[q].n, tab[q].n, mi, Kt + static_cast<size_t>(tab[q].off) * mi, mi, 1,
+                          Kt + static_cast<size_t>(tab[q].off) * mi, mi, 0,
+                          m->pool.p + tab[q].pool_off, tab[q].ld, -1.0, 1.0, 0};
+  } else {
+    // ---- (I) information form -----------------------------------------------
+    rep->solver = 2;
+    require(static_cast<size_t>(n) * 8 <= 200 * 1024, TLG_RUNTIME_ERROR,
+            "dense information-form update limited to 25600 active centres");
+    double* H = ctx->ws<double>(S_HMAT, static_cast<size_t>(n) * n);
+    TLG_CUDA(cudaMemsetAsync(H, 0, sizeof(double) * n * n, s));
+    // H0 = blockdiag(info_inv_q)^-1
+    for (int q = 0; q < nq; ++q) {
+      double* dst = H + tab[q].off + static_cast<size_t>(tab[q].off) * n;
+      if (!spd_inverse(ctx, m->pool.p + tab[q].pool_off, tab[q].ld, tab[q].n, dst, n)) {
+        rep->rejected = 1;
+        return;
+      }
+    }
+    const TCsr t = transpose_csr(ctx, c, mm, n);
+    const size_t smem = static_cast<size_t>(n) * 8;
+    if (smem > 48 * 1024)
+      TLG_CUDA(cudaFuncSetAttribute(k_gram_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_gram_rows<<<n, 128, smem, s>>>(t.rowp, t.obs, t.val, c.rowp, c.col, c.val, n, H, n);
+    TLG_LAUNCHED(ctx);
+    k_row_dot<<<(n + 255) / 256, 256, 0, s>>>(t.rowp, t.obs, t.val, resid, n, dw);
+    TLG_LAUNCHED(ctx);
+    potrf_lower(ctx, H, n, n, info);
+    int h = 0;
+    TLG_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    TLG_CUDA(cudaStreamSynchronize(s));
+    if (h) {
+      rep->rejected = 1;
+      return;
+    }
+    trsm_left_lower(ctx, H, n, n, dw, 1, n, 0);
+    trsm_left_lower(ctx, H, n, n, dw, 1, n, 1);
+    // X = L^-1 ; (H^-1)_qq = X[:,q]^T X[:,q]
+    double* X = ctx->ws<double>(S_YMAT, static_cast<size_t>(n) * n);
+    k_set_identity<<<std::min(n * n / 256 + 1, 4096), 256, 0, s>>>(X, n, n);
+    TLG_LAUNCHED(ctx);
+    trsm_left_lower(ctx, H, n, n, X, n, n, 0);
+    for (int q = 0; q < nq; ++q) {
+      const size_t o = tab[q].off;
+      descs[q] = GemmDesc{tab[q].n, tab[q].n, n - tab[q].off, X + o + o * n, n, 1,
+                          X + o + o * n, n, 0, m->pool.p + tab[q].pool_off, tab[q].ld, 1.0, 0.0, 0};
+    }
+  }
+  // per-block products, then symmetrise and write back the weights
+  GemmDesc* d_descs = reinterpret_cast<GemmDesc*>(ctx->ws<char>(S_BLKTAB, nq * sizeof(GemmDesc)));
+  GemmDesc* h_descs = static_cast<GemmDesc*>(ctx->host_stage(nq * sizeof(GemmDesc)));
+  std::memcpy(h_descs, descs.data(), nq * sizeof(GemmDesc));
+  TLG_CUDA(cudaMemcpyAsync(d_descs, h_descs, nq * sizeof(GemmDesc), cudaMemcpyHostToDevice, s));
+  gemm_grouped(ctx, d_descs, nq, maxq, maxq);
+  k_symmetrize_blocks<<<nq, 256, 0, s>>>(d_tab, m->pool.p);
+  TLG_LAUNCHED(ctx);
+  k_apply_dw<<<(n + 255) / 256, 256, 0, s>>>(m->w.p, d_merged, n, dw);
+  TLG_LAUNCHED(ctx);
+  sync_weights_to_grid(m);
+  TLG_CUDA(cudaStreamSynchronize(s));
+}
+
+__global__ void k_gather_sub(const double* __restrict__ H, int ldh, const uint32_t* __restrict__ idx,
+                             int bn, double* __restrict__ out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bn * bn; e += gridDim.x * blockDim.x) {
+    const int r = e % bn, c = e / bn;
+    out[e] = H[idx[r] + (size_t)idx[c] * ldh];
+  }
+}
+static void gather_sub(tlg_ctx* ctx, const double* H, int ldh, const std::vector<uint32_t>& mem,
+                double* out) {
+  const int bn = static_cast<int>(mem.size());
+  uint32_t* d = ctx->ws<uint32_t>(S_BLKTAB, bn);
+  TLG_CUDA(cudaMemcpyAsync(d, mem.data(), bn * 4, cudaMemcpyHostToDevice, ctx->stream));
+  k_gather_sub<<<std::min((bn * bn + 255) / 256, 1024), 256, 0, ctx->stream>>>(H, ldh, d, bn, out);
+  TLG_LAUNCHED(ctx);
+  TLG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// ---------------------------------------------------------------------------
+// fit_batch_ridge (terrain_model.cpp:269-308): H = lambda I + sum m m^T,
+// b = sum m z, w = H^-1 b (Cholesky), info_inv_b = (H_bb)^-1.
+void batch_fit_device(tlg_model* m, const double* x, const double* y, const double* z,
+                      size_t mm) {
+  tlg_ctx* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  ensure_grid(m);
+  const int n = static_cast<int>(m->hcx.size());
+  if (n == 0) return;
+  require(static_cast<size_t>(n) * 8 <= 200 * 1024, TLG_RUNTIME_ERROR,
+          "dense batch ridge fit limited to 25600 centres");
+  const Csr c = build_csr(m, x, y, mm, nullptr, m->kc.neg_inv_2st2, m->kc.scale, false, nullptr);
+  double* H = ctx->ws<double>(S_HMAT, static_cast<size_t>(n) * n);
+  TLG_CUDA(cudaMemsetAsync(H, 0, sizeof(double) * n * n, s));
+  add_diag(ctx, H, n, n, m->kernel.lambda);
+  const TCsr t = transpose_csr(ctx, c, mm, n);
+  const size_t smem = static_cast<size_t>(n) * 8;
+  if (smem > 48 * 1024)
+    TLG_CUDA(cudaFuncSetAttribute(k_gram_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_gram_rows<<<n, 128, smem, s>>>(t.rowp, t.obs, t.val, c.rowp, c.col, c.val, n, H, n);
+  TLG_LAUNCHED(ctx);
+  double* b = ctx->ws<double>(S_WORK3, n);
+  k_row_dot<<<(n + 255) / 256, 256, 0, s>>>(t.rowp, t.obs, t.val, z, n, b);
+  TLG_LAUNCHED(ctx);
+  // per-block H_bb (gathered by member ids) inverses (:298-306)
+  const int nb = static_cast<int>(m->members.size());
+  for (int bb = 0; bb < nb; ++bb) {
+    const auto& mem = m->members[bb];
+    const int bn = static_cast<int>(mem.size());
+    if (!bn) continue;
+    double* Hb = ctx->ws<double>(S_SMAT, static_cast<size_t>(bn) * bn);
+    gather_sub(ctx, H, n, mem, Hb);
+    if (!spd_inverse(ctx, Hb, bn, bn, m->pool.p + m->blk_off[bb], m->blk_ld[bb]))
+      throw Error(TLG_RUNTIME_ERROR, "ridge solve failed (block factorisation)");
+  }
+  int* info = ctx->ws<int>(S_FLAGS, 4);
+  TLG_CUDA(cudaMemsetAsync(info, 0, 4 * sizeof(int), s));
+  potrf_lower(ctx, H, n, n, info);
+  double* mnx = ctx->ws<double>(S_PARTIALS, 2);
+  k_diag_minmax<<<1, 256, 0, s>>>(H, n, n, mnx);
+  TLG_LAUNCHED(ctx);
+  trsm_left_lower(ctx, H, n, n, b, 1, n, 0);
+  trsm_left_lower(ctx, H, n, n, b, 1, n, 1);
+  int h = 0;
+  double cond[2];
+  TLG_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, s));
+  TLG_CUDA(cudaMemcpyAsync(cond, mnx, sizeof(cond), cudaMemcpyDeviceToHost, s));
+  TLG_CUDA(cudaStreamSynchronize(s));
+  if (h)
+    throw Error(TLG_RUNTIME_ERROR, "ridge solve failed; condition estimate " +
+                                       std::to_string(cond[0] / std::max(cond[1], 1e-300)));
+  TLG_CUDA(cudaMemcpyAsync(m->w.p, b, n * 8, cudaMemcpyDeviceToDevice, s));
+  sync_weights_to_grid(m);
+  TLG_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace tlg

@@ -1,0 +1,181 @@
+"""Wheel/ground manifold soft constraint over the C-ABI.
+
+Mirrors terralio::kin (contact.hpp:15-24, leg_model.hpp:32-60) and the
+manifold block of match::total_cost (scan_matcher.cpp:221-248). The batched
+entry point `manifold_rows` is the B200 hot path: one kernel computes every
+row's residual and 1x6 Jacobian and reduces J^T J, J^T r and the cost in the
+same pass (tlg_manifold_rows).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from ._abi import NormalEqC, check
+from .terrain import TerrainModel, _empty_like, _is_dev, _mem, _ptr
+
+try:
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+
+@dataclass
+class NormalEq:
+    """A = J^T J (6x6), g = J^T r, cost = |r|^2 (scan_matcher.cpp:296-299,253)."""
+    A: np.ndarray
+    g: np.ndarray
+    cost: float
+    valid: int
+
+    @staticmethod
+    def _from_c(c: NormalEqC) -> "NormalEq":
+        A = np.zeros((6, 6))
+        k = 0
+        for i in range(6):
+            for j in range(i, 6):
+                A[i, j] = A[j, i] = c.A[k]
+                k += 1
+        return NormalEq(A, np.array(c.g[:]), float(c.cost), int(round(c.valid)))
+
+
+def manifold_rows(terrain: TerrainModel, R, t, h, wheel_radius: float = 0.0,
+                  lambda_M: float = 1.0, huber_delta: float = 0.05,
+                  want=("r", "J", "valid"), out: dict | None = None):
+    """Rows r_i = sqrt(lambda_M) w_i (xi_z - wheel_radius - f(xi_xy)),
+    xi = R h_i + t, with their Jacobians (column-major n x 6 like
+    CostEval::jacobian) and the fused normal equations.
+
+    h: (n, 3) lever arms (numpy = host, torch CUDA = device). Returns
+    (rows: dict[str, array], NormalEq).
+    """
+    Rm = np.ascontiguousarray(np.asarray(R, dtype=np.float64).reshape(9))
+    tv = np.ascontiguousarray(np.asarray(t, dtype=np.float64).reshape(3))
+    if _is_dev(h):
+        hx, hy, hz = (h[:, j].to(torch.float64).contiguous() for j in range(3))
+    else:
+        ha = np.asarray(h, dtype=np.float64).reshape(-1, 3)
+        hx, hy, hz = (np.ascontiguousarray(ha[:, j]) for j in range(3))
+    n = len(hx)
+    rows = dict(out or {})
+    for key, dt, size in (("r", np.float64, n), ("J", np.float64, 6 * n), ("valid", np.uint8, n),
+                          ("raw", np.float64, n)):
+        if key in want and key not in rows:
+            rows[key] = _empty_like(hx, size, dt)
+    ne = NormalEqC()
+    check(_abi.load().tlg_manifold_rows(
+        terrain.handle, _ptr(Rm), _ptr(tv), _ptr(hx), _ptr(hy), _ptr(hz), n, _mem(hx),
+        float(wheel_radius), float(lambda_M), float(huber_delta), _ptr(rows.get("r")),
+        _ptr(rows.get("J")), _ptr(rows.get("valid")), _ptr(rows.get("raw")), _mem(hx),
+        C.byref(ne)))
+    return rows, NormalEq._from_c(ne)
+
+
+# ---------------------------------------------------------------------------
+# Leg model (leg_model.hpp:14-60): host-side forward kinematics that produces
+# the two wheel lever arms; scalar bookkeeping, not the data path.
+@dataclass
+class Link:
+    name: str = ""
+    parent: str = ""
+    offset: tuple = (0.0, 0.0, 0.0)
+    axis: tuple = (0.0, 1.0, 0.0)
+    revolute: bool = True
+
+
+@dataclass
+class LegChain:
+    links: list = field(default_factory=list)
+
+    def joint_count(self) -> int:
+        return sum(1 for l in self.links if l.revolute)
+
+
+@dataclass
+class LegModel:
+    left: LegChain = field(default_factory=LegChain)
+    right: LegChain = field(default_factory=LegChain)
+    wheel_radius: float = 0.1
+
+    def joint_count(self) -> int:
+        return self.left.joint_count() + self.right.joint_count()
+
+    def chain(self, side: str) -> LegChain:
+        return self.left if side == "left" else self.right
+
+    def joint_offset(self, side: str) -> int:
+        return 0 if side == "left" else self.left.joint_count()
+
+
+def _axis_angle(axis, angle):
+    a = np.asarray(axis, dtype=np.float64)
+    a = a / np.linalg.norm(a)
+    K = np.array([[0, -a[2], a[1]], [a[2], 0, -a[0]], [-a[1], a[0], 0]])
+    return np.eye(3) + math.sin(angle) * K + (1 - math.cos(angle)) * (K @ K)
+
+
+def chain_end_position(chain: LegChain, q) -> np.ndarray:
+    """leg_model.cpp:10-21: translate by each offset, then rotate revolute links."""
+    if len(q) < chain.joint_count():
+        raise _abi.InvalidArgument("too few joint angles for chain")
+    Rm, p, qi = np.eye(3), np.zeros(3), 0
+    for link in chain.links:
+        p = p + Rm @ np.asarray(link.offset, dtype=np.float64)
+        if link.revolute:
+            Rm = Rm @ _axis_angle(link.axis, q[qi])
+            qi += 1
+    return p
+
+
+def default_robot() -> LegModel:
+    """sim::default_robot (scene.cpp:12-28)."""
+    def chain(ys):
+        return LegChain([Link("hip", "base", (0.0, ys * 0.12, -0.08), (0, 1, 0), True),
+                         Link("knee", "hip", (0.0, 0.0, -0.24), (0, 1, 0), True),
+                         Link("wheel", "knee", (0.0, 0.0, -0.24), (0, 1, 0), False)])
+    return LegModel(chain(1.0), chain(-1.0), 0.08)
+
+
+def lever_arm(leg: LegModel, joints, side: str) -> np.ndarray:
+    off = leg.joint_offset(side)
+    ch = leg.chain(side)
+    if len(joints) < leg.joint_count():
+        raise _abi.InvalidArgument("joint config does not match leg model")
+    return chain_end_position(ch, list(joints)[off: off + ch.joint_count()])
+
+
+@dataclass
+class ManifoldResidual:
+    value: float = 0.0
+    valid: bool = False
+    wheel_center: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+
+def manifold_residual(R, t, joints, leg: LegModel, side: str,
+                      terrain: TerrainModel) -> ManifoldResidual:
+    """contact.cpp:7-19 (wheel row through the batched kernel, n = 1)."""
+    h = lever_arm(leg, joints, side)
+    rows, _ = manifold_rows(terrain, R, t, h.reshape(1, 3), leg.wheel_radius, 1.0, 0.0,
+                            want=("raw", "valid"))
+    wc = np.asarray(R, dtype=np.float64).reshape(3, 3) @ h + np.asarray(t, dtype=np.float64)
+    ok = bool(rows["valid"][0])
+    return ManifoldResidual(float(rows["raw"][0]) if ok else 0.0, ok, wc)
+
+
+def manifold_jacobian(R, t, joints, leg: LegModel, side: str, terrain: TerrainModel) -> np.ndarray:
+    """contact.cpp:21-39: d r / d [dtheta, dt] (right perturbation)."""
+    h = lever_arm(leg, joints, side)
+    rows, _ = manifold_rows(terrain, R, t, h.reshape(1, 3), leg.wheel_radius, 1.0, 0.0,
+                            want=("J", "valid"))
+    J = np.asarray(rows["J"]).reshape(6)
+    if not rows["valid"][0]:
+        # unsupported query: the reference's predict_gradient is 0 -> [0,0,1]*dxi
+        Rm = np.asarray(R, dtype=np.float64).reshape(3, 3)
+        dr = np.array([0.0, 0.0, 1.0])
+        u = Rm.T @ dr
+        return np.concatenate([np.cross(h, u), dr])
+    return J
