@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 RBF-terrain hot path (BASELINE.json metric:
+"RBF residual+Jacobian evals/s; kernel-matrix update ms/scan (M centers)").
+
+Headline (`value`): manifold soft-constraint rows — residual + 6-DoF
+Jacobian per LiDAR point, materialised (r, J column-major, valid) with the
+fused J^T J / J^T r / cost reduction — over the C5 workload: 10^7 points per
+GPU against a 316 x 316 = 99,856-centre RBF terrain (points/s, whole job).
+One step = one LM cost evaluation (tlg_manifold_rows) over all points.
+
+Secondary (`update`): per-scan TerrainModel::recursive_update latency at
+M = 4096 centres (C3 staircase), m = 400 (pipeline cap) and m = 20,000.
+
+`--impl reference` times the reference algorithm's CPU path: the plain-C++
+oracle restatement (the reference itself cannot be built here)
+on the host cores, same metric/config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "RBF residual+Jacobian evals/s (manifold rows + fused 6x6 normal equations)"
+UNIT = "points/s"
+
+# C5: ROI [0, 22.05]^2, 316 x 316 lattice, 10^7 points
+ROI_C5 = ((0.0, 0.0), (22.05, 22.05))
+RES, R_A, COUNT = 0.07, 0.12, 3
+POSE_W = (0.02, -0.015, 0.04)           # bench_main.cpp:116
+POSE_T = (0.1, -0.05, 0.08)             # bench_main.cpp:117
+BYTES_PER_POINT = 24 + 8 + 48 + 1       # h in; r, J[6], valid out
+
+
+def terrain_c5(x, y, xp):
+    """C4/C5 sinusoidal bumps z = 0.05 sin(2 pi x / 1.5) sin(2 pi y / 1.5)."""
+    return 0.05 * xp.sin(2 * math.pi * x / 1.5) * xp.sin(2 * math.pi * y / 1.5)
+
+
+def staircase(x):
+    """TerrainSpec::staircase(0.08, 0.5, 10, x0=0.5) (terrain_spec.cpp:72-77)."""
+    xr = x - 0.5
+    idx = np.floor(xr / 0.5)
+    return np.where(xr < 0.0, 0.0, 0.08 * np.minimum(idx, 10.0))
+
+
+def so3_exp(w):
+    w = np.asarray(w, dtype=np.float64)
+    th = np.linalg.norm(w)
+    K = np.array([[0, -w[2], w[1]], [w[2], 0, -w[0]], [-w[1], w[0], 0]])
+    return np.eye(3) + math.sin(th) / th * K + (1 - math.cos(th)) / th ** 2 * (K @ K)
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        self.f.flush()
+        rows = []
+        for line in Path(self.f.name).read_text().splitlines():
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_eval_rate(centers_xy, weights, kernel, pts_h, R, t, seconds=10.0, threads=None):
+    """Oracle (restated reference) manifold rows on a bounded sample."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as orc
+    from paper_2509_26222_b200.terrain import CenterSet, Rect
+    threads = threads or os.cpu_count() or 1
+    cs = CenterSet(centers_xy, RES, R_A, COUNT, Rect(*ROI_C5))
+    om = orc.Model(kernel, cs)
+    om.set_weights(weights)
+    n0 = min(len(pts_h), 20000)
+    t0 = time.perf_counter()
+    om.manifold_rows(R, t, pts_h[:n0], 0.0, 1.0, 0.05, threads=threads)
+    dt = time.perf_counter() - t0
+    rate0 = n0 / dt
+    n = int(min(len(pts_h), max(n0, rate0 * seconds)))
+    t0 = time.perf_counter()
+    om.manifold_rows(R, t, pts_h[:n], 0.0, 1.0, 0.05, threads=threads)
+    dt = time.perf_counter() - t0
+    return n / dt, n, threads, dt, om
+
+
+def build_c5(device, n_points, seed, torch):
+    """C5 model (select_centers on 10^6 support points) + n_points lever arms."""
+    from paper_2509_26222_b200 import terrain as T
+    g = torch.Generator(device=f"cuda:{device}").manual_seed(seed)
+    sup = torch.rand((1_000_000, 2), generator=g, device=f"cuda:{device}", dtype=torch.float64)
+    sup *= ROI_C5[1][0]
+    zs = terrain_c5(sup[:, 0], sup[:, 1], torch)
+    cs = T.select_centers(T.TerrainObservation(sup, zs), T.Rect(*ROI_C5), RES, R_A, COUNT)
+    kernel = T.KernelParams()
+    kernel.finalize()
+    model = T.TerrainModel(kernel, cs)
+    c = cs.centers
+    # interpolating weights: height * res^2 / (2 pi sigma^2)
+    w = terrain_c5(c[:, 0], c[:, 1], np) * RES * RES / (2 * math.pi * kernel.sigma ** 2)
+    model.set_weights(w)
+    R = so3_exp(POSE_W)
+    tv = np.array(POSE_T)
+    p = torch.rand((n_points, 2), generator=g, device=f"cuda:{device}", dtype=torch.float64)
+    p *= ROI_C5[1][0]
+    pz = terrain_c5(p[:, 0], p[:, 1], torch) + 0.01 * torch.randn(
+        n_points, generator=g, device=f"cuda:{device}", dtype=torch.float64)
+    P = torch.stack([p[:, 0], p[:, 1], pz], 1)
+    Rt = torch.from_numpy(R).to(P)
+    H = (P - torch.from_numpy(tv).to(P)) @ Rt  # rows: R^T (p - t)
+    h = tuple(H[:, j].contiguous() for j in range(3))
+    del P, H, p, pz, sup
+    return model, kernel, cs, w, R, tv, h
+
+
+# ---------------------------------------------------------------------------
+def run_update_bench(torch, device, steps=5):
+    """C3: per-scan recursive_update at M = 4096 (64 x 64 lattice)."""
+    from paper_2509_26222_b200 import terrain as T
+    roi = T.Rect((0.0, 0.0), (4.41, 4.41))
+    kernel = T.KernelParams()
+    kernel.finalize()
+    model = T.TerrainModel(kernel, T.CenterSet(np.zeros((0, 2)), RES, R_A, COUNT, roi))
+    rng = np.random.default_rng(3)
+
+    def scan(m):
+        clean = rng.uniform(0.0, 4.41, size=(m, 2))
+        noisy = clean + rng.normal(0.0, 0.1, size=(m, 2))
+        return T.TerrainObservation(np.ascontiguousarray(noisy), staircase(clean[:, 0]))
+
+    rep0 = model.recursive_update(scan(20000))  # births: all 4096 nodes
+    out = {"M": model.num_centers(), "born_first_scan": rep0.born_centers}
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for m in (400, 20000):
+        scans = [scan(m) for _ in range(steps + 2)]
+        for s in scans[:2]:
+            model.recursive_update(s)
+        times, reps = [], []
+        for s in scans[2:]:
+            ev0.record()
+            rep = model.recursive_update(s)
+            ev1.record()
+            ev1.synchronize()
+            times.append(ev0.elapsed_time(ev1))
+            reps.append(rep)
+        rep = reps[-1]
+        out[f"m{m}"] = {"ms_per_scan": statistics.median(times), "ms_min": min(times),
+                        "n_active": rep.active_centers, "active_blocks": rep.active_blocks,
+                        "solver": rep.solver, "rejected": rep.rejected}
+    return out, model, kernel
+
+
+def cpu_update_ms(model, kernel, m=400, seed=5):
+    """Oracle recursive_update (reference algorithm, single thread) at M=4096."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as orc
+    cs = model.centers()
+    om = orc.Model(kernel, cs)
+    om.set_weights(model.weights())
+    rng = np.random.default_rng(seed)
+    clean = rng.uniform(0.0, 4.41, size=(m, 2))
+    noisy = clean + rng.normal(0.0, 0.1, size=(m, 2))
+    t0 = time.perf_counter()
+    rep = om.recursive_update(noisy, staircase(clean[:, 0]))
+    return (time.perf_counter() - t0) * 1e3, rep
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--points", type=int, default=10_000_000)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-update", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_2509_26222_b200 import kinematics as kin
+    from paper_2509_26222_b200 import terrain as T
+
+    ctx = T.Context.default(local)
+    model, kernel, cs, w, R, tv, h = build_c5(local, args.points, 1000 + rank, torch)
+    n = args.points
+    rows = {"r": torch.empty(n, dtype=torch.float64, device="cuda"),
+            "J": torch.empty(6 * n, dtype=torch.float64, device="cuda"),
+            "valid": torch.empty(n, dtype=torch.uint8, device="cuda")}
+    ne_buf = torch.zeros(29, dtype=torch.float64, device="cuda")
+
+    def step():
+        _, ne = kin.manifold_rows(model, R, tv, h, 0.0, 1.0, 0.05, out=rows)
+        if world > 1:
+            vals = list(ne.A[np.triu_indices(6)]) + list(ne.g) + [ne.cost, ne.valid]
+            ne_buf.copy_(torch.tensor(vals, dtype=torch.float64))
+            dist.all_reduce(ne_buf)  # NCCL: the 29-double normal-equation reduce
+        return ne
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    lib = __import__("paper_2509_26222_b200._abi", fromlist=["load"]).load()
+    import ctypes as C
+    lib.tlg_ctx_set_profiling(ctx.handle, 1)
+    l0 = ctx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            ne = step()
+        ev1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    launches = ctx.launch_count() - l0
+    kms, kn = C.c_double(), C.c_uint64()
+    lib.tlg_ctx_kernel_stats(ctx.handle, 0, C.byref(kms), C.byref(kn))
+    lib.tlg_ctx_set_profiling(ctx.handle, 0)
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = world * n / (ms_step * 1e-3)
+    k_ms = kms.value / max(1, kn.value)
+
+    # ---- e2e: host (pinned) lever arms in, normal equations out ------------
+    hh = [torch.empty(n, dtype=torch.float64, pin_memory=True) for _ in range(3)]
+    for j in range(3):
+        hh[j].copy_(h[j])
+    hn = tuple(x.numpy() for x in hh)
+    for _ in range(2):
+        kin.manifold_rows(model, R, tv, hn, 0.0, 1.0, 0.05, want=())
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(3, min(args.steps, 10))
+    e0.record()
+    for _ in range(e2e_steps):
+        kin.manifold_rows(model, R, tv, hn, 0.0, 1.0, 0.05, want=())
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    del hh, hn
+
+    peaks, peak_kind = load_peaks()
+    achieved = BYTES_PER_POINT * n / (k_ms * 1e-3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "kernel_traffic.json"
+    if tf.exists():
+        try:
+            d = json.loads(tf.read_text())
+            if d.get("k_manifold", {}).get("points") == n:
+                traffic = d["k_manifold"]["dram_bytes_per_launch"]
+        except Exception:
+            traffic = None
+
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C5: 1e7 LiDAR ground points/GPU x 99,856 RBF centres "
+                               "(316x316 lattice, sigma=0.04, sigma_eps=0.1, cutoff 0.3231 m), "
+                               "manifold rows r+J[6]+valid materialised + fused J^T J/J^T r/cost",
+                   "points_per_gpu": n, "centres": len(cs.centers), "parallelism": f"dp{world}",
+                   "l2": "inputs (240 MB/GPU) larger than L2; no flush",
+                   "step": "one LM cost evaluation (tlg_manifold_rows)"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                     "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                     "kernel": "k_manifold", "kernel_ms": k_ms,
+                     "bytes_per_point": BYTES_PER_POINT, "peak_source": peak_kind},
+        "e2e": {"value": world * n / (e2e_ms * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 29 * 8 + 4,
+                "ms_per_step": e2e_ms, "api": "tlg_manifold_rows, pinned host lever arms in, "
+                                              "normal equations out"},
+        "clocks": clk.summary(),
+    }
+
+    if rank == 0 and world == 1:
+        dfma, dmma = C.c_double(), C.c_double()
+        lib.tlg_measure_fp64_peak(ctx.handle, C.byref(dfma), C.byref(dmma))
+        result["fp64_peak_tflops"] = {"dfma": dfma.value, "dmma": dmma.value}
+        # FP64 view of the same kernel (pairs/s based)
+        if not args.no_update:
+            upd, umodel, ukernel = run_update_bench(torch, local)
+            result["update"] = upd
+            if not args.no_cpu:
+                cms, crep = cpu_update_ms(umodel, ukernel, 400)
+                result["update"]["cpu_oracle_ms_per_scan_m400"] = cms
+                result["update"]["cpu_oracle_n_active"] = crep["active_centers"]
+        if not args.no_cpu:
+            pts_h = torch.stack(list(h), 1)[: 2_000_000].cpu().numpy()
+            rate, ns, threads, dt, _ = cpu_eval_rate(cs.centers, w, kernel, pts_h, R, tv,
+                                                     args.cpu_seconds)
+            result["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads,
+                                      "kind": "port",
+                                      "sample": f"{ns} of the C5 points ({dt:.1f} s), oracle "
+                                                f"restatement -O3 no-FMA, {threads} threads"}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference algorithm's CPU path (oracle port; the
+    reference itself is unbuildable here) on the host cores, same metric."""
+    if rank != 0:
+        return
+    import torch
+    from paper_2509_26222_b200 import terrain as T  # noqa: F401  (types only)
+    sys.path.insert(0, str(ROOT / "oracle"))
+    rng = np.random.default_rng(1000)
+    # C5 model: full 316 x 316 lattice (what select_centers yields at 1e6 support points)
+    nx = int(math.floor(22.05 / RES + 1e-9))
+    ii, jj = np.meshgrid(np.arange(nx + 1), np.arange(nx + 1), indexing="ij")
+    centers = np.stack([0.0 + ii.ravel() * RES, 0.0 + jj.ravel() * RES], 1)
+    kernel = T.KernelParams()
+    kernel.cutoff_radius = 3.0 * kernel.sigma_tilde()
+    w = terrain_c5(centers[:, 0], centers[:, 1], np) * RES * RES / (2 * math.pi * kernel.sigma ** 2)
+    R, tv = so3_exp(POSE_W), np.array(POSE_T)
+    m = 2_000_000
+    p = rng.uniform(0.0, 22.05, size=(m, 2))
+    pz = terrain_c5(p[:, 0], p[:, 1], np) + 0.01 * rng.normal(size=m)
+    H = (np.stack([p[:, 0], p[:, 1], pz], 1) - tv) @ R
+    threads = os.cpu_count() or 1
+    per_step = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    rate, ns, threads, dt, om = cpu_eval_rate(centers, w, kernel, H, R, tv, per_step, threads)
+    rates = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        om.manifold_rows(R, tv, H[:ns], 0.0, 1.0, 0.05, threads=threads)
+        d = time.perf_counter() - t0
+        if i >= args.warmup:
+            rates.append(ns / d)
+    value = statistics.median(rates)
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ns / value * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic",
+           "config": {"workload": "C5 (bounded sample per step)", "points_per_step": ns,
+                      "centres": len(centers)},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                            "sample": f"{ns} C5 points per step; oracle restatement of the "
+                                      "reference (reference unbuildable: Eigen absent)"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -95,6 +95,13 @@ tlg_status tlg_ctx_set_stream(tlg_ctx* ctx, void* stream);
 tlg_status tlg_ctx_synchronize(tlg_ctx* ctx);
 /* Number of kernels this context has launched (bench launch accounting). */
 uint64_t tlg_ctx_launch_count(const tlg_ctx* ctx);
+/* Per-kernel CUDA-event timing of the hot kernels (off by default).
+ * kernel: 0 = manifold rows (K4), 1 = height/gradient eval (K3). */
+tlg_status tlg_ctx_set_profiling(tlg_ctx* ctx, int enable);
+tlg_status tlg_ctx_kernel_stats(tlg_ctx* ctx, int kernel, double* total_ms, uint64_t* launches);
+/* FP64 roofline microbenchmark on the context's device: sustained DFMA and
+ * DMMA (mma.sync m8n8k4 f64) TFLOP/s. */
+tlg_status tlg_measure_fp64_peak(tlg_ctx* ctx, double* dfma_tflops, double* dmma_tflops);
 
 /* ---- kernel.cpp ------------------------------------------------------------- */
 /* KernelParams::finalize (kernel.cpp:15-25): fills the auto cutoff, validates. */

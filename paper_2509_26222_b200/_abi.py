@@ -101,6 +101,9 @@ _SIGS = {
     "tlg_ctx_set_stream": (_ST, [_P, _P]),
     "tlg_ctx_synchronize": (_ST, [_P]),
     "tlg_ctx_launch_count": (C.c_uint64, [_P]),
+    "tlg_ctx_set_profiling": (_ST, [_P, _I]),
+    "tlg_ctx_kernel_stats": (_ST, [_P, _I, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
+    "tlg_measure_fp64_peak": (_ST, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "tlg_kernel_finalize": (_ST, [C.POINTER(KernelParamsC)]),
     "tlg_supported_mesh_nodes": (_ST, [_P, _P, _P, _P, _SZ, _SZ, _I, C.POINTER(CenterParamsC),
                                        _P, _P, _SZ, C.POINTER(_SZ), _I]),

@@ -19,6 +19,7 @@ void upload_new_centres(tlg_model* m, size_t first);
 uint32_t add_center_host(tlg_model* m, double x, double y);
 void moment_device(tlg_model* m, const double* x, const double* y, size_t n, uint32_t* rowp,
                    uint32_t** ids, double** vals, size_t* nnz);
+void fp64_peak(tlg_ctx* ctx, double* dfma, double* dmma);
 }  // namespace tlg
 
 namespace {
@@ -139,6 +140,36 @@ tlg_status tlg_ctx_synchronize(tlg_ctx* ctx) {
 }
 
 uint64_t tlg_ctx_launch_count(const tlg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+tlg_status tlg_ctx_set_profiling(tlg_ctx* ctx, int enable) {
+  return guard([&] {
+    check_ptr(ctx, "ctx");
+    ctx->profiling = enable != 0;
+    for (int i = 0; i < 4; ++i) {
+      ctx->prof_ms[i] = 0.0;
+      ctx->prof_n[i] = 0;
+    }
+  });
+}
+
+tlg_status tlg_ctx_kernel_stats(tlg_ctx* ctx, int kernel, double* total_ms, uint64_t* launches) {
+  return guard([&] {
+    check_ptr(ctx, "ctx");
+    require(kernel >= 0 && kernel < 4, TLG_INVALID_ARGUMENT, "bad kernel id");
+    if (total_ms) *total_ms = ctx->prof_ms[kernel];
+    if (launches) *launches = ctx->prof_n[kernel];
+  });
+}
+
+tlg_status tlg_measure_fp64_peak(tlg_ctx* ctx, double* dfma, double* dmma) {
+  return guard([&] {
+    check_ptr(ctx, "ctx");
+    double a = 0, b = 0;
+    fp64_peak(ctx, &a, &b);
+    if (dfma) *dfma = a;
+    if (dmma) *dmma = b;
+  });
+}
 
 tlg_status tlg_kernel_finalize(tlg_kernel_params* p) {
   return guard([&] {

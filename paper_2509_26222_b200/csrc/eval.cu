@@ -95,11 +95,14 @@ void eval_device(tlg_model* m, const double* x, const double* y, size_t n, doubl
   int* err = ctx->ws<int>(S_FLAGS, 4);
   TLG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
   if (n) {
+    prof_begin(ctx, 1);
     k_eval<<<grid_for(ctx, n, 256, 8), 256, 0, ctx->stream>>>(
         grid_view(m), x, y, n, m->kc.r2, m->kc.neg_inv_2s2, m->kc.inv_s2, z, sup, gx, gy, err);
     TLG_LAUNCHED(ctx);
+    prof_mark_end(ctx);
   }
   check_err_flag(ctx, err, TLG_DOMAIN_ERROR, "non-finite query");
+  prof_collect(ctx);
 }
 
 // ---------------------------------------------------------------------------
@@ -222,16 +225,19 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
   double* out = partials + static_cast<size_t>(blocks) * kNE;
   int* err = ctx->ws<int>(S_FLAGS, 4);
   TLG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
+  prof_begin(ctx, 0);
   k_manifold<<<blocks, kManifoldThreads, 0, ctx->stream>>>(
       grid_view(m), pose, hx, hy, hz, n, m->kc.r2, m->kc.neg_inv_2s2, m->kc.inv_s2,
       wheel_radius, std::sqrt(lambda_M), huber, r, J, valid, raw, partials, err);
   TLG_LAUNCHED(ctx);
+  prof_mark_end(ctx);
   k_reduce_partials<<<kNE, 32, 0, ctx->stream>>>(partials, blocks, out);
   TLG_LAUNCHED(ctx);
   double h[kNE + 1];
   TLG_CUDA(cudaMemcpyAsync(h, out, kNE * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   TLG_CUDA(cudaMemcpyAsync(&h[kNE], err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   TLG_CUDA(cudaStreamSynchronize(ctx->stream));
+  prof_collect(ctx);
   int e = 0;
   std::memcpy(&e, &h[kNE], sizeof(int));
   if (e) throw Error(TLG_DOMAIN_ERROR, "non-finite query");

@@ -123,6 +123,12 @@ struct tlg_ctx {
   // pinned host staging
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // hot-kernel profiling (tlg_ctx_set_profiling)
+  bool profiling = false;
+  cudaEvent_t prof_ev[2] = {nullptr, nullptr};
+  double prof_ms[4] = {0, 0, 0, 0};
+  uint64_t prof_n[4] = {0, 0, 0, 0};
+  int prof_pending = -1;  // kernel id whose events await collection
 
   template <typename T>
   T* ws(int slot, size_t count) {
@@ -133,6 +139,12 @@ struct tlg_ctx {
 };
 
 namespace tlg {
+
+// Profiling brackets around one hot-kernel launch; prof_end() must be called
+// after the stream has been synchronised.
+void prof_begin(tlg_ctx* ctx, int kernel);
+void prof_mark_end(tlg_ctx* ctx);
+void prof_collect(tlg_ctx* ctx);
 
 // Copy helpers honouring tlg_mem tags.
 void copy_in(tlg_ctx* ctx, void* dst_dev, const void* src, size_t bytes, tlg_mem mem);

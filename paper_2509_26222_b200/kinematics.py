@@ -50,12 +50,15 @@ def manifold_rows(terrain: TerrainModel, R, t, h, wheel_radius: float = 0.0,
     xi = R h_i + t, with their Jacobians (column-major n x 6 like
     CostEval::jacobian) and the fused normal equations.
 
-    h: (n, 3) lever arms (numpy = host, torch CUDA = device). Returns
+    h: (n, 3) lever arms or an SoA tuple (hx, hy, hz) of contiguous float64
+    arrays (numpy = host, torch CUDA = device). Returns
     (rows: dict[str, array], NormalEq).
     """
     Rm = np.ascontiguousarray(np.asarray(R, dtype=np.float64).reshape(9))
     tv = np.ascontiguousarray(np.asarray(t, dtype=np.float64).reshape(3))
-    if _is_dev(h):
+    if isinstance(h, (tuple, list)):  # SoA (hx, hy, hz), used as-is (no copies)
+        hx, hy, hz = h
+    elif _is_dev(h):
         hx, hy, hz = (h[:, j].to(torch.float64).contiguous() for j in range(3))
     else:
         ha = np.asarray(h, dtype=np.float64).reshape(-1, 3)
