@@ -174,6 +174,26 @@ tlg_status tlg_manifold_rows(tlg_model* model, const double R[9], const double t
                              double huber_delta, double* r, double* J, uint8_t* valid,
                              double* raw, tlg_mem out_mem, tlg_normal_eq* ne);
 
+/* ---- scans: lever arms binned once per scan ------------------------------
+ * lm_solve evaluates the same scan's rows every LM iteration
+ * (scan_matcher.cpp:276,315). tlg_scan_create copies the lever arms to the
+ * device binned by the world cell of R0 h + t0, so later evaluations read
+ * the weight grid warp-coherently. tlg_scan_manifold_rows is
+ * tlg_manifold_rows over the scan; its rows come out in scan order: row k
+ * belongs to input point perm[k] (tlg_scan_permutation). Results do not
+ * depend on R0 (it only sets memory order). */
+typedef struct tlg_scan tlg_scan;
+tlg_status tlg_scan_create(tlg_model* model, const double R0[9], const double t0[3],
+                           const double* hx, const double* hy, const double* hz, size_t n,
+                           tlg_mem in_mem, tlg_scan** out);
+tlg_status tlg_scan_destroy(tlg_scan* scan);
+tlg_status tlg_scan_info(const tlg_scan* scan, size_t* n, double* bin_ms);
+tlg_status tlg_scan_permutation(tlg_scan* scan, uint32_t* perm, tlg_mem out_mem);
+tlg_status tlg_scan_manifold_rows(tlg_model* model, tlg_scan* scan, const double R[9],
+                                  const double t[3], double wheel_radius, double lambda_M,
+                                  double huber_delta, double* r, double* J, uint8_t* valid,
+                                  double* raw, tlg_mem out_mem, tlg_normal_eq* ne);
+
 /* recursive_update(obs, allow_birth) (terrain_model.cpp:145-253). */
 tlg_status tlg_recursive_update(tlg_model* model, const double* x, const double* y,
                                 const double* z, size_t m, size_t z_len, tlg_mem in_mem,

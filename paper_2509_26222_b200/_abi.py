@@ -10,7 +10,8 @@ import ctypes as C
 import os
 from pathlib import Path
 
-_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libterralio_gpu.so"
+_LIB_PATH = Path(os.environ.get("TLG_LIB_OVERRIDE") or
+                 Path(__file__).resolve().parent / "lib" / "libterralio_gpu.so")
 
 TLG_OK = 0
 TLG_INVALID_ARGUMENT = 1
@@ -127,6 +128,12 @@ _SIGS = {
     "tlg_moment_features": (_ST, [_P, _P, _P, _SZ, _I, _P, _P, _P, _SZ, C.POINTER(_SZ), _I]),
     "tlg_manifold_rows": (_ST, [_P, _P, _P, _P, _P, _P, _SZ, _I, C.c_double, C.c_double,
                                 C.c_double, _P, _P, _P, _P, _I, C.POINTER(NormalEqC)]),
+    "tlg_scan_create": (_ST, [_P, _P, _P, _P, _P, _P, _SZ, _I, C.POINTER(_P)]),
+    "tlg_scan_destroy": (_ST, [_P]),
+    "tlg_scan_info": (_ST, [_P, C.POINTER(_SZ), C.POINTER(C.c_double)]),
+    "tlg_scan_permutation": (_ST, [_P, _P, _I]),
+    "tlg_scan_manifold_rows": (_ST, [_P, _P, _P, _P, C.c_double, C.c_double, C.c_double, _P, _P,
+                                     _P, _P, _I, C.POINTER(NormalEqC)]),
     "tlg_recursive_update": (_ST, [_P, _P, _P, _P, _SZ, _SZ, _I, _I, C.POINTER(UpdateReportC)]),
     "tlg_fit_batch_ridge": (_ST, [_P, C.POINTER(KernelParamsC), C.POINTER(CenterParamsC), _P, _P,
                                   _SZ, _P, _P, _P, _SZ, _SZ, _I, C.POINTER(_P)]),

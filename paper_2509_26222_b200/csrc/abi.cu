@@ -20,6 +20,8 @@ uint32_t add_center_host(tlg_model* m, double x, double y);
 void moment_device(tlg_model* m, const double* x, const double* y, size_t n, uint32_t* rowp,
                    uint32_t** ids, double** vals, size_t* nnz);
 void fp64_peak(tlg_ctx* ctx, double* dfma, double* dmma);
+tlg_scan* scan_create(tlg_model* m, const double R0[9], const double t0[3], const double* hx,
+                      const double* hy, const double* hz, size_t n);
 }  // namespace tlg
 
 namespace {
@@ -455,6 +457,56 @@ tlg_status tlg_manifold_rows(tlg_model* m, const double R[9], const double t[3],
       ctx->sync();
     }
   });
+}
+
+tlg_status tlg_scan_create(tlg_model* m, const double R0[9], const double t0[3], const double* hx,
+                           const double* hy, const double* hz, size_t n, tlg_mem in_mem,
+                           tlg_scan** out) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(R0, "R0");
+    check_ptr(t0, "t0");
+    check_ptr(out, "out");
+    tlg_ctx* ctx = m->ctx;
+    const double* dhx = as_device(ctx, S_IN_HX, hx, n, in_mem);
+    const double* dhy = as_device(ctx, S_IN_HY, hy, n, in_mem);
+    const double* dhz = as_device(ctx, S_IN_HZ, hz, n, in_mem);
+    *out = scan_create(m, R0, t0, dhx, dhy, dhz, n);
+  });
+}
+
+tlg_status tlg_scan_destroy(tlg_scan* scan) {
+  return guard([&] {
+    if (!scan) return;
+    cudaStreamSynchronize(scan->ctx->stream);
+    delete scan;
+  });
+}
+
+tlg_status tlg_scan_info(const tlg_scan* scan, size_t* n, double* bin_ms) {
+  return guard([&] {
+    check_ptr(scan, "scan");
+    if (n) *n = scan->n;
+    if (bin_ms) *bin_ms = scan->bin_ms;
+  });
+}
+
+tlg_status tlg_scan_permutation(tlg_scan* scan, uint32_t* perm, tlg_mem out_mem) {
+  return guard([&] {
+    check_ptr(scan, "scan");
+    check_ptr(perm, "perm");
+    copy_out(scan->ctx, perm, scan->perm.p, scan->n * 4, out_mem);
+    scan->ctx->sync();
+  });
+}
+
+tlg_status tlg_scan_manifold_rows(tlg_model* m, tlg_scan* scan, const double R[9],
+                                  const double t[3], double wheel_radius, double lambda_M,
+                                  double huber_delta, double* r, double* J, uint8_t* valid,
+                                  double* raw, tlg_mem out_mem, tlg_normal_eq* ne) {
+  return tlg_manifold_rows(m, R, t, scan ? scan->hx.p : nullptr, scan ? scan->hy.p : nullptr,
+                           scan ? scan->hz.p : nullptr, scan ? scan->n : 0, TLG_DEVICE,
+                           wheel_radius, lambda_M, huber_delta, r, J, valid, raw, out_mem, ne);
 }
 
 tlg_status tlg_recursive_update(tlg_model* m, const double* x, const double* y, const double* z,

@@ -5,14 +5,32 @@
 //     (grid_index.hpp:32-48) bit-exactly: same cell coordinates
 //     floor(v / cell), same (2*span+1)^2 cell window, same no-FMA
 //     r^2 = dx*dx + dy*dy <= cutoff^2 test. Values are FP64 with FMA
-//     accumulation (parity: 1e-9 relative).
+//     accumulation (parity: 1e-9 of max(|ref|, sum|w kappa|)).
+//
+//     Two sweeps:
+//     - generic: the reference's 3x3 cell sweep over the CSR centre grid;
+//     - lattice (centres are mesh nodes, the select_centers/birth case): a
+//       fixed WIN x WIN node window of the dense weight grid W. Pairs are
+//       classified once per model (always inside the cutoff disc / boundary /
+//       always outside, with 1e-6-cell and 1e-9-radius safety margins), so
+//       only boundary pairs run the exact reference test; kappa is separable
+//       on the lattice, kappa = e_x(i) e_y(j), and e_x, e_y follow a
+//       two-multiply recurrence along the window (two exps per axis); each
+//       pair costs two FMAs:
+//         S_i = sum_j w_ij e_y(j),  T_i = sum_j w_ij e_y(j) dy_j,
+//         z = sum_i e_x(i) S_i, dz/dx = sum_i e_x(i) dx_i S_i / s^2, ...
+//       The paper's geometry (and the reference tests') is compiled in, so
+//       the class of every pair is a compile-time constant (no per-pair
+//       branches, always-outside pairs vanish); other geometries use the
+//       same window with runtime class masks.
 // K4: the manifold soft-constraint rows (contact.cpp:7-39 +
 //     scan_matcher.cpp:221-248), materialised as r / J (column-major rows x 6)
-//     / valid, with the 6x6 normal equations J^T J, J^T r and the cost reduced
-//     in the same pass: per-thread register accumulators, warp shuffles, one
-//     partial per CTA, then a fixed-order final reduction (deterministic, no
-//     FP64 atomics).
+//     / valid, with J^T J, J^T r and the cost reduced in the same pass: each
+//     warp drops its 32 rows' 29 products into a shared tile, lane L sums
+//     entry L; one partial per CTA, then a fixed-order final reduction
+//     (deterministic, no FP64 atomics).
 #include <cmath>
+#include <type_traits>
 
 #include "internal.cuh"
 
@@ -25,8 +43,8 @@ struct EvalOut {
 
 // Sweeps the reference's candidate cells of query (x, y); cells of one x
 // column are contiguous in cell order, so each column is one index range.
-__device__ __forceinline__ EvalOut eval_point(const GridView& g, double x, double y, double r2,
-                                              double neg_inv_2b2) {
+__device__ __forceinline__ EvalOut eval_generic(const GridView& g, double x, double y, double r2,
+                                                double neg_inv_2b2) {
   EvalOut o{0.0, 0.0, 0.0, false};
   const int qx = static_cast<int>(floor(x / g.cell));
   const int qy = static_cast<int>(floor(y / g.cell));
@@ -54,12 +72,170 @@ __device__ __forceinline__ EvalOut eval_point(const GridView& g, double x, doubl
   return o;
 }
 
-__global__ void __launch_bounds__(256) k_eval(GridView g, const double* __restrict__ x,
-                                              const double* __restrict__ y, size_t n, double r2,
-                                              double neg_inv_2s2, double inv_s2,
-                                              double* __restrict__ z, uint8_t* __restrict__ sup,
-                                              double* __restrict__ gx, double* __restrict__ gy,
-                                              int* __restrict__ err) {
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
+
+template <int WIN, int G>
+__device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, double y,
+                                                double r2, double neg_inv_2b2) {
+  EvalOut o{0.0, 0.0, 0.0, false};
+  const int ib = static_cast<int>(floor((x - L.org_x) * L.inv_res));
+  const int jb = static_cast<int>(floor((y - L.org_y) * L.inv_res));
+  const int i0 = ib - L.lo, j0 = jb - L.lo;
+  // the whole window lies in the zero padding (or beyond): no centre within
+  // the cutoff -> unsupported, exactly like an empty radius query
+  if (i0 < 0 || j0 < 0 || i0 + WIN > L.ni || j0 + WIN > L.nj) return o;
+  const int qx = static_cast<int>(floor(x / L.cell));
+  const int qy = static_cast<int>(floor(y / L.cell));
+
+  // Row factors. dy^2 is kept exact for the boundary tests; e_y follows the
+  // lattice recurrence e(l+1) = e(l) p(l), p(l+1) = p(l) exp(2 c res^2)
+  // (c = -1/(2 s^2)), two exps per axis instead of WIN.
+  double ey[WIN], eyd[WIN], dy2[WIN];
+  uint32_t rowok = 0;
+#pragma unroll
+  for (int l = 0; l < WIN; ++l) {
+    const double dy = __dsub_rn(__ldg(L.cyl + j0 + l), y);
+    dy2[l] = __dmul_rn(dy, dy);
+    eyd[l] = dy;
+    rowok |= static_cast<uint32_t>(abs(__ldg(L.ccy + j0 + l) - qy) <= L.span) << l;
+  }
+  if (L.rec_ok) {
+    double e = exp(dy2[0] * neg_inv_2b2);
+    double p = exp(L.c_res * fma(2.0, eyd[0], L.res));
+#pragma unroll
+    for (int l = 0; l < WIN; ++l) {
+      ey[l] = e;
+      e *= p;
+      p *= L.k2;
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < WIN; ++l) ey[l] = exp(dy2[l] * neg_inv_2b2);
+  }
+#pragma unroll
+  for (int l = 0; l < WIN; ++l) eyd[l] *= ey[l];
+  const double* wbase = L.W + static_cast<size_t>(i0) * L.nj + j0;
+  const double dx_first = __dsub_rn(__ldg(L.cxl + i0), x);
+  double ex_e = 0.0, ex_p = 0.0;
+  if (L.rec_ok) {
+    ex_e = exp(__dmul_rn(dx_first, dx_first) * neg_inv_2b2);
+    ex_p = exp(L.c_res * fma(2.0, dx_first, L.res));
+  }
+  auto column = [&](auto KC) {
+    constexpr int k = decltype(KC)::value;
+    const double dx = k == 0 ? dx_first : __dsub_rn(__ldg(L.cxl + i0 + k), x);
+    const double dx2 = __dmul_rn(dx, dx);
+    const bool colok = abs(__ldg(L.ccx + i0 + k) - qx) <= L.span;
+    const double* wc = wbase + static_cast<size_t>(k) * L.nj;
+    double S = 0.0, T = 0.0;
+    bool any;
+    if constexpr (G >= 0) {
+      // compiled geometry: always-outside pairs vanish, always-inside pairs
+      // carry no test, only boundary pairs run the exact reference test
+      constexpr uint32_t im = kGeoms[G].in[k], bm = kGeoms[G].bd[k];
+      static_for<0, WIN>([&](auto LC) {
+        constexpr int l = decltype(LC)::value;
+        if constexpr ((im >> l) & 1u) {
+          const double w = __ldg(wc + l);
+          S = fma(w, ey[l], S);
+          T = fma(w, eyd[l], T);
+        } else if constexpr ((bm >> l) & 1u) {
+          const bool in = colok && ((rowok >> l) & 1u) && __dadd_rn(dx2, dy2[l]) <= r2;
+          const double w = in ? __ldg(wc + l) : 0.0;
+          S = fma(w, ey[l], S);
+          T = fma(w, eyd[l], T);
+        }
+      });
+      any = (im | bm) != 0;
+    } else {
+      const uint32_t im = L.inmask[k], bm = L.bdmask[k];
+#pragma unroll
+      for (int l = 0; l < WIN; ++l) {
+        if ((im >> l) & 1u) {
+          const double w = __ldg(wc + l);
+          S = fma(w, ey[l], S);
+          T = fma(w, eyd[l], T);
+        } else if ((bm >> l) & 1u) {
+          const bool in = colok && ((rowok >> l) & 1u) && __dadd_rn(dx2, dy2[l]) <= r2;
+          const double w = in ? __ldg(wc + l) : 0.0;
+          S = fma(w, ey[l], S);
+          T = fma(w, eyd[l], T);
+        }
+      }
+      any = (im | bm) != 0;
+    }
+    double ex;
+    if (L.rec_ok) {
+      ex = ex_e;
+      ex_e *= ex_p;
+      ex_p *= L.k2;
+    } else {
+      ex = exp(dx2 * neg_inv_2b2);
+    }
+    if (any) {
+      o.z = fma(ex, S, o.z);
+      o.sx = fma(ex * dx, S, o.sx);
+      o.sy = fma(ex, T, o.sy);
+    }
+  };
+  static_for<0, WIN>(column);
+  // supported: some *present* centre passes the reference test. The cell's
+  // four corner nodes are always inside; otherwise scan the window (rare).
+  bool sup = false;
+  if (L.corner_ok) {
+    const int* pc = L.P + static_cast<size_t>(ib) * L.nj + jb;
+    sup = (__ldg(pc) | __ldg(pc + 1) | __ldg(pc + L.nj) | __ldg(pc + L.nj + 1)) != 0;
+  }
+  if (!sup) {
+    for (int k = 0; k < WIN && !sup; ++k) {
+      const double dx = __dsub_rn(__ldg(L.cxl + i0 + k), x);
+      const double dx2 = __dmul_rn(dx, dx);
+      const bool colok = abs(__ldg(L.ccx + i0 + k) - qx) <= L.span;
+      const int* pc = L.P + static_cast<size_t>(i0 + k) * L.nj + j0;
+      for (int l = 0; l < WIN; ++l) {
+        const double dy = __dsub_rn(__ldg(L.cyl + j0 + l), y);
+        const bool in = ((L.inmask[k] >> l) & 1u) ||
+                        (((L.bdmask[k] >> l) & 1u) && colok && ((rowok >> l) & 1u) &&
+                         __dadd_rn(dx2, __dmul_rn(dy, dy)) <= r2);
+        if (in && __ldg(pc + l)) {
+          sup = true;
+          break;
+        }
+      }
+    }
+  }
+  o.sup = sup;
+  return o;
+}
+
+// KIND: 0 = generic sweep, 1..kMaxWin = lattice window with runtime pair
+// classes, 100 + g = lattice window of compiled geometry kGeoms[g].
+template <int KIND>
+__device__ __forceinline__ EvalOut eval_any(const GridView& g, const LatticeView& L, double x,
+                                            double y, double r2, double neg_inv_2b2) {
+  if constexpr (KIND == 0)
+    return eval_generic(g, x, y, r2, neg_inv_2b2);
+  else if constexpr (KIND >= 100)
+    return eval_lattice<kGeoms[KIND - 100].win, KIND - 100>(L, x, y, r2, neg_inv_2b2);
+  else
+    return eval_lattice<KIND, -1>(L, x, y, r2, neg_inv_2b2);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(128, 4) k_eval(GridView g, LatticeView L,
+                                                 const double* __restrict__ x,
+                                                 const double* __restrict__ y, size_t n,
+                                                 double r2, double neg_inv_2s2, double inv_s2,
+                                                 double* __restrict__ z,
+                                                 uint8_t* __restrict__ sup,
+                                                 double* __restrict__ gx,
+                                                 double* __restrict__ gy, int* __restrict__ err) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x) {
     const double px = x[i], py = y[i];
@@ -67,7 +243,7 @@ __global__ void __launch_bounds__(256) k_eval(GridView g, const double* __restri
       atomicOr(err, 1);
       continue;
     }
-    const EvalOut o = eval_point(g, px, py, r2, neg_inv_2s2);
+    const EvalOut o = eval_any<KIND>(g, L, px, py, r2, neg_inv_2s2);
     if (z) z[i] = o.sup ? o.z : 0.0;
     if (sup) sup[i] = o.sup ? 1 : 0;
     if (gx) gx[i] = o.sx * inv_s2;
@@ -88,6 +264,29 @@ static void check_err_flag(tlg_ctx* ctx, int* d_err, tlg_status st, const char* 
   if (h) throw Error(st, msg);
 }
 
+int sweep_kind(const tlg_model* m) {
+  if (!m->lat.valid) return 0;
+  return m->lat.geom_id >= 0 ? 100 + m->lat.geom_id : m->lat.win;
+}
+
+#define TLG_KIND_DISPATCH(KINDV, CALL)                   \
+  switch (KINDV) {                                       \
+    case 100: { constexpr int W_ = 100; CALL; } break;   \
+    case 101: { constexpr int W_ = 101; CALL; } break;   \
+    case 4: { constexpr int W_ = 4; CALL; } break;       \
+    case 5: { constexpr int W_ = 5; CALL; } break;       \
+    case 6: { constexpr int W_ = 6; CALL; } break;       \
+    case 7: { constexpr int W_ = 7; CALL; } break;       \
+    case 8: { constexpr int W_ = 8; CALL; } break;       \
+    case 9: { constexpr int W_ = 9; CALL; } break;       \
+    case 10: { constexpr int W_ = 10; CALL; } break;     \
+    case 11: { constexpr int W_ = 11; CALL; } break;     \
+    case 12: { constexpr int W_ = 12; CALL; } break;     \
+    case 13: { constexpr int W_ = 13; CALL; } break;     \
+    case 14: { constexpr int W_ = 14; CALL; } break;     \
+    default: { constexpr int W_ = 0; CALL; } break;      \
+  }
+
 void eval_device(tlg_model* m, const double* x, const double* y, size_t n, double* z,
                  uint8_t* sup, double* gx, double* gy) {
   tlg_ctx* ctx = m->ctx;
@@ -95,9 +294,13 @@ void eval_device(tlg_model* m, const double* x, const double* y, size_t n, doubl
   int* err = ctx->ws<int>(S_FLAGS, 4);
   TLG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
   if (n) {
+    const GridView g = grid_view(m);
+    const LatticeView L = lattice_view(m);
     prof_begin(ctx, 1);
-    k_eval<<<grid_for(ctx, n, 256, 8), 256, 0, ctx->stream>>>(
-        grid_view(m), x, y, n, m->kc.r2, m->kc.neg_inv_2s2, m->kc.inv_s2, z, sup, gx, gy, err);
+    TLG_KIND_DISPATCH(sweep_kind(m),
+                      (k_eval<W_><<<grid_for(ctx, n, 128, 16), 128, 0, ctx->stream>>>(
+                          g, L, x, y, n, m->kc.r2, m->kc.neg_inv_2s2, m->kc.inv_s2, z, sup, gx,
+                          gy, err)));
     TLG_LAUNCHED(ctx);
     prof_mark_end(ctx);
   }
@@ -113,7 +316,13 @@ struct Pose {
 };
 
 constexpr int kNE = 29;  // 21 (A upper) + 6 (g) + cost + valid
-constexpr int kManifoldThreads = 256;
+#ifndef TLG_MANIFOLD_THREADS
+#define TLG_MANIFOLD_THREADS 128
+#endif
+#ifndef TLG_MANIFOLD_MINB
+#define TLG_MANIFOLD_MINB 4
+#endif
+constexpr int kManifoldThreads = TLG_MANIFOLD_THREADS;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -121,29 +330,37 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-__global__ void __launch_bounds__(kManifoldThreads) k_manifold(
-    GridView g, Pose pose, const double* __restrict__ hx, const double* __restrict__ hy,
-    const double* __restrict__ hz, size_t n, double r2, double neg_inv_2s2, double inv_s2,
-    double wheel_radius, double sl, double huber, double* __restrict__ out_r,
-    double* __restrict__ out_J, uint8_t* __restrict__ out_valid, double* __restrict__ out_raw,
-    double* __restrict__ partials, int* __restrict__ err) {
-  double acc[kNE];
-#pragma unroll
-  for (int k = 0; k < kNE; ++k) acc[k] = 0.0;
+template <int KIND>
+__global__ void __launch_bounds__(kManifoldThreads, TLG_MANIFOLD_MINB) k_manifold(
+    GridView g, LatticeView L, Pose pose, const double* __restrict__ hx,
+    const double* __restrict__ hy, const double* __restrict__ hz, size_t n, double r2,
+    double neg_inv_2s2, double inv_s2, double wheel_radius, double sl, double huber,
+    double* __restrict__ out_r, double* __restrict__ out_J, uint8_t* __restrict__ out_valid,
+    double* __restrict__ out_raw, double* __restrict__ partials, int* __restrict__ err) {
+  // Lane L accumulates normal-equation entry L: each warp iteration drops its
+  // 32 rows' 29 products into a per-warp shared tile and lane L sums row L in
+  // lane order (deterministic) -> one accumulator register per lane.
+  __shared__ double tile[kManifoldThreads / 32][kNE][33];
+  double acc = 0.0;
   const double* R = pose.R;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const double h0 = hx[i], h1 = hy[i], h2 = hz[i];
+  const int lane = threadIdx.x & 31;
+  const size_t warps = (size_t)gridDim.x * (blockDim.x >> 5);
+  for (size_t base = ((size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < n;
+       base += warps * 32) {
+    const size_t i = base + lane;
+    const bool live = i < n;
+    const double h0 = live ? hx[i] : 0.0, h1 = live ? hy[i] : 0.0, h2 = live ? hz[i] : 0.0;
     // xi = R h + t (leg_model.cpp:31, contact.cpp:183)
     const double xi0 = fma(R[2], h2, fma(R[1], h1, R[0] * h0)) + pose.t[0];
     const double xi1 = fma(R[5], h2, fma(R[4], h1, R[3] * h0)) + pose.t[1];
     const double xi2 = fma(R[8], h2, fma(R[7], h1, R[6] * h0)) + pose.t[2];
     double r = 0.0, raw = 0.0, J[6] = {0, 0, 0, 0, 0, 0};
     bool valid = false;
-    if (!isfinite(xi0) || !isfinite(xi1)) {
+    if (!live) {
+    } else if (!isfinite(xi0) || !isfinite(xi1)) {
       atomicOr(err, 1);
     } else {
-      const EvalOut o = eval_point(g, xi0, xi1, r2, neg_inv_2s2);
+      const EvalOut o = eval_any<KIND>(g, L, xi0, xi1, r2, neg_inv_2s2);
       if (o.sup) {
         valid = true;
         raw = xi2 - wheel_radius - o.z;
@@ -165,34 +382,38 @@ __global__ void __launch_bounds__(kManifoldThreads) k_manifold(
         J[5] = s;
       }
     }
-    if (out_r) out_r[i] = r;
-    if (out_raw) out_raw[i] = raw;
-    if (out_valid) out_valid[i] = valid ? 1 : 0;
-    if (out_J) {
+    if (live) {
+      if (out_r) out_r[i] = r;
+      if (out_raw) out_raw[i] = raw;
+      if (out_valid) out_valid[i] = valid ? 1 : 0;
+      if (out_J) {
 #pragma unroll
-      for (int c = 0; c < 6; ++c) out_J[c * n + i] = J[c];
+        for (int c = 0; c < 6; ++c) out_J[c * n + i] = J[c];
+      }
     }
+    double(*t)[33] = tile[threadIdx.x >> 5];
     int k = 0;
 #pragma unroll
     for (int a = 0; a < 6; ++a)
 #pragma unroll
-      for (int b = a; b < 6; ++b) {
-        acc[k] = fma(J[a], J[b], acc[k]);
-        ++k;
-      }
+      for (int b = a; b < 6; ++b) t[k++][lane] = J[a] * J[b];
 #pragma unroll
-    for (int a = 0; a < 6; ++a) acc[21 + a] = fma(J[a], r, acc[21 + a]);
-    acc[27] = fma(r, r, acc[27]);
-    acc[28] += valid ? 1.0 : 0.0;
+    for (int a = 0; a < 6; ++a) t[21 + a][lane] = J[a] * r;
+    t[27][lane] = r * r;
+    t[28][lane] = valid ? 1.0 : 0.0;
+    __syncwarp();
+    if (lane < kNE) {
+      double s = 0.0;
+#pragma unroll 8
+      for (int q = 0; q < 32; ++q) s += t[lane][q];
+      acc += s;
+    }
+    __syncwarp();
   }
-  // CTA reduction: warp shuffles, then warp partials through shared memory
-  __shared__ double sh[kManifoldThreads / 32][kNE];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < kNE; ++k) {
-    const double v = warp_sum(acc[k]);
-    if (lane == 0) sh[wid][k] = v;
-  }
+  // CTA reduction: lane L of every warp holds entry L; sum warps in order
+  __shared__ double sh[kManifoldThreads / 32][32];
+  const int wid = threadIdx.x >> 5;
+  sh[wid][lane] = acc;
   __syncthreads();
   if (threadIdx.x < kNE) {
     double v = 0.0;
@@ -220,15 +441,19 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
   Pose pose;
   for (int i = 0; i < 9; ++i) pose.R[i] = R[i];
   for (int i = 0; i < 3; ++i) pose.t[i] = t[i];
-  const unsigned blocks = grid_for(ctx, n, kManifoldThreads, 4);
+  const unsigned blocks = grid_for(ctx, n, kManifoldThreads, 4 * TLG_MANIFOLD_MINB);
   double* partials = ctx->ws<double>(S_PARTIALS, static_cast<size_t>(blocks) * kNE + kNE);
   double* out = partials + static_cast<size_t>(blocks) * kNE;
   int* err = ctx->ws<int>(S_FLAGS, 4);
   TLG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
+  const GridView g = grid_view(m);
+  const LatticeView L = lattice_view(m);
+  const double sl = std::sqrt(lambda_M);
   prof_begin(ctx, 0);
-  k_manifold<<<blocks, kManifoldThreads, 0, ctx->stream>>>(
-      grid_view(m), pose, hx, hy, hz, n, m->kc.r2, m->kc.neg_inv_2s2, m->kc.inv_s2,
-      wheel_radius, std::sqrt(lambda_M), huber, r, J, valid, raw, partials, err);
+  TLG_KIND_DISPATCH(sweep_kind(m),
+                    (k_manifold<W_><<<blocks, kManifoldThreads, 0, ctx->stream>>>(
+                        g, L, pose, hx, hy, hz, n, m->kc.r2, m->kc.neg_inv_2s2, m->kc.inv_s2,
+                        wheel_radius, sl, huber, r, J, valid, raw, partials, err)));
   TLG_LAUNCHED(ctx);
   prof_mark_end(ctx);
   k_reduce_partials<<<kNE, 32, 0, ctx->stream>>>(partials, blocks, out);
@@ -246,80 +471,6 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
     for (int k = 0; k < 6; ++k) ne->g[k] = h[21 + k];
     ne->cost = h[27];
     ne->valid = h[28];
-  }
-}
-
-// ---------------------------------------------------------------------------
-// moment_feature (terrain_model.cpp:97-107) as CSR: count, scan, fill, sort.
-__global__ void k_moment_count(GridView g, const double* __restrict__ x,
-                               const double* __restrict__ y, size_t n, double r2,
-                               double neg_inv_2b2, uint32_t* __restrict__ cnt,
-                               int* __restrict__ err) {
-  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double px = x[i], py = y[i];
-  if (!isfinite(px) || !isfinite(py)) {
-    atomicOr(err, 1);
-    cnt[i] = 0;
-    return;
-  }
-  uint32_t c = 0;
-  const int qx = static_cast<int>(floor(px / g.cell));
-  const int qy = static_cast<int>(floor(py / g.cell));
-  const int y_lo = max(qy - g.span - g.gy0, 0), y_hi = min(qy + g.span - g.gy0, g.gny - 1);
-  const int x_lo = max(qx - g.span - g.gx0, 0), x_hi = min(qx + g.span - g.gx0, g.gnx - 1);
-  if (y_lo <= y_hi)
-    for (int gx = x_lo; gx <= x_hi; ++gx) {
-      const int b = g.cell_start[gx * g.gny + y_lo], e = g.cell_start[gx * g.gny + y_hi + 1];
-      for (int k = b; k < e; ++k) {
-        const double d2 = sq2_exact(g.cx[k] - px, g.cy[k] - py);
-        if (d2 <= r2 && exp(d2 * neg_inv_2b2) != 0.0) ++c;
-      }
-    }
-  cnt[i] = c;
-}
-
-__global__ void k_moment_fill(GridView g, const double* __restrict__ x,
-                              const double* __restrict__ y, size_t n, double r2,
-                              double neg_inv_2b2, double scale, const uint32_t* __restrict__ rowp,
-                              uint32_t* __restrict__ ids, double* __restrict__ vals) {
-  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double px = x[i], py = y[i];
-  if (!isfinite(px) || !isfinite(py)) return;
-  uint32_t o = rowp[i];
-  const uint32_t o0 = o;
-  const int qx = static_cast<int>(floor(px / g.cell));
-  const int qy = static_cast<int>(floor(py / g.cell));
-  const int y_lo = max(qy - g.span - g.gy0, 0), y_hi = min(qy + g.span - g.gy0, g.gny - 1);
-  const int x_lo = max(qx - g.span - g.gx0, 0), x_hi = min(qx + g.span - g.gx0, g.gnx - 1);
-  if (y_lo <= y_hi)
-    for (int gx = x_lo; gx <= x_hi; ++gx) {
-      const int b = g.cell_start[gx * g.gny + y_lo], e = g.cell_start[gx * g.gny + y_hi + 1];
-      for (int k = b; k < e; ++k) {
-        const double d2 = sq2_exact(g.cx[k] - px, g.cy[k] - py);
-        if (d2 <= r2) {
-          const double kv = exp(d2 * neg_inv_2b2);
-          if (kv != 0.0) {
-            ids[o] = g.id[k];
-            vals[o] = scale * kv;
-            ++o;
-          }
-        }
-      }
-    }
-  // ascending ids (SparseVec contract, kernel.hpp:32-34): insertion sort
-  for (uint32_t a = o0 + 1; a < o; ++a) {
-    const uint32_t ki = ids[a];
-    const double kvv = vals[a];
-    uint32_t b = a;
-    while (b > o0 && ids[b - 1] > ki) {
-      ids[b] = ids[b - 1];
-      vals[b] = vals[b - 1];
-      --b;
-    }
-    ids[b] = ki;
-    vals[b] = kvv;
   }
 }
 

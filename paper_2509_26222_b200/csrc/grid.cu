@@ -66,6 +66,178 @@ __global__ void k_gather_sorted(const uint32_t* __restrict__ sid, size_t n,
   sw[i] = w[j];
 }
 
+// ---------------------------------------------------------------------------
+// Lattice detection: centre (cx, cy) is node (i, j) iff it equals
+// min + i * res bit-exactly (center_select.cpp:55-56), i = llround((c-min)/res).
+__global__ void k_lattice_check(const double* __restrict__ cx, const double* __restrict__ cy,
+                                size_t n, double min_x, double min_y, double res,
+                                int* __restrict__ st) {
+  for (size_t c = blockIdx.x * (size_t)blockDim.x + threadIdx.x; c < n;
+       c += (size_t)gridDim.x * blockDim.x) {
+    const double fi = (cx[c] - min_x) / res, fj = (cy[c] - min_y) / res;
+    bool ok = fabs(fi) < 1e8 && fabs(fj) < 1e8;
+    int i = 0, j = 0;
+    if (ok) {
+      i = static_cast<int>(llround(fi));
+      j = static_cast<int>(llround(fj));
+      ok = __dadd_rn(min_x, __dmul_rn(static_cast<double>(i), res)) == cx[c] &&
+           __dadd_rn(min_y, __dmul_rn(static_cast<double>(j), res)) == cy[c];
+    }
+    if (!ok) {
+      atomicOr(&st[0], 1);
+    } else {
+      atomicMin(&st[1], i);
+      atomicMin(&st[2], j);
+      atomicMax(&st[3], i);
+      atomicMax(&st[4], j);
+    }
+  }
+}
+
+__global__ void k_lattice_fill(const double* __restrict__ cx, const double* __restrict__ cy,
+                               const double* __restrict__ w, size_t n, double min_x,
+                               double min_y, double res, int i_org, int j_org, int nj,
+                               double* __restrict__ W, int* __restrict__ P,
+                               int* __restrict__ slot, int* __restrict__ dup) {
+  for (size_t c = blockIdx.x * (size_t)blockDim.x + threadIdx.x; c < n;
+       c += (size_t)gridDim.x * blockDim.x) {
+    const int i = static_cast<int>(llround((cx[c] - min_x) / res)) - i_org;
+    const int j = static_cast<int>(llround((cy[c] - min_y) / res)) - j_org;
+    const int s = i * nj + j;
+    slot[c] = s;
+    W[s] = w[c];
+    if (atomicAdd(&P[s], 1) != 0) atomicOr(dup, 1);
+  }
+}
+
+__global__ void k_lattice_axes(double min_v, double res, int org, int count, double cell,
+                               double* __restrict__ coord, int* __restrict__ cc) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const double v = __dadd_rn(min_v, __dmul_rn(static_cast<double>(k + org), res));
+  coord[k] = v;
+  cc[k] = static_cast<int>(floor(v / cell));
+}
+
+__global__ void k_lattice_refresh(const int* __restrict__ slot, const double* __restrict__ w,
+                                  size_t n, double* __restrict__ W) {
+  const size_t c = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (c < n) W[slot[c]] = w[c];
+}
+
+// Window geometry and pair classes (host: ~WIN^2 scalar parameter setup).
+static bool lattice_geometry(tlg_model* m, LatticeGrid& L) {
+  const double res = m->cparams.mesh_resolution;
+  if (!(res > 0.0)) return false;
+  const double R = m->kernel.cutoff_radius / res;  // cutoff in lattice units
+  if (!(R > 0.0) || R + 2 > kMaxWin) return false;
+  const Geom g = make_geom(R);
+  if (g.win == 0) return false;
+  L.lo = g.lo;
+  L.win = g.win;
+  L.pad = L.win + 1;
+  for (int k = 0; k < 16; ++k) {
+    L.inmask[k] = g.in[k];
+    L.bdmask[k] = g.bd[k];
+  }
+  L.geom_id = -1;
+  for (int i = 0; i < kNumGeoms; ++i)
+    if (geom_equal(g, kGeoms[i])) L.geom_id = i;
+  const int c0 = L.lo, c1 = L.lo + 1;
+  L.corner_ok = ((L.inmask[c0] >> c0) & 1) && ((L.inmask[c0] >> c1) & 1) &&
+                ((L.inmask[c1] >> c0) & 1) && ((L.inmask[c1] >> c1) & 1);
+  return true;
+}
+
+static void build_lattice(tlg_model* m) {
+  tlg_ctx* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  LatticeGrid& L = m->lat;
+  L.valid = false;
+  const size_t n = m->hcx.size();
+  if (n == 0 || !lattice_geometry(m, L)) return;
+  const double res = m->cparams.mesh_resolution;
+  const double mnx = m->cparams.roi_min_x, mny = m->cparams.roi_min_y;
+  int* st = ctx->ws<int>(S_COUNT, 8);
+  const int hs[8] = {0, INT_MAX, INT_MAX, INT_MIN, INT_MIN, 0, 0, 0};
+  TLG_CUDA(cudaMemcpyAsync(st, hs, sizeof(hs), cudaMemcpyHostToDevice, s));
+  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 4 * 148));
+  k_lattice_check<<<blocks, 256, 0, s>>>(m->cx.p, m->cy.p, n, mnx, mny, res, st);
+  TLG_LAUNCHED(ctx);
+  int h[8];
+  TLG_CUDA(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
+  TLG_CUDA(cudaStreamSynchronize(s));
+  if (h[0]) return;
+  L.i_org = h[1] - L.pad;
+  L.j_org = h[2] - L.pad;
+  const long long ni = static_cast<long long>(h[3]) - h[1] + 1 + 2 * L.pad;
+  const long long nj = static_cast<long long>(h[4]) - h[2] + 1 + 2 * L.pad;
+  if (ni * nj > (1ll << 28)) return;
+  L.ni = static_cast<int>(ni);
+  L.nj = static_cast<int>(nj);
+  const size_t nn = static_cast<size_t>(ni * nj);
+  L.W.ensure(nn);
+  L.P.ensure(nn);
+  L.slot.ensure(n);
+  TLG_CUDA(cudaMemsetAsync(L.W.p, 0, nn * sizeof(double), s));
+  TLG_CUDA(cudaMemsetAsync(L.P.p, 0, nn * sizeof(int), s));
+  int* dup = st + 5;
+  k_lattice_fill<<<blocks, 256, 0, s>>>(m->cx.p, m->cy.p, m->w.p, n, mnx, mny, res, L.i_org,
+                                        L.j_org, L.nj, L.W.p, L.P.p, L.slot.p, dup);
+  TLG_LAUNCHED(ctx);
+  L.cxl.ensure(L.ni);
+  L.cyl.ensure(L.nj);
+  L.ccx.ensure(L.ni);
+  L.ccy.ensure(L.nj);
+  const double cell = m->grid.cell;
+  k_lattice_axes<<<(L.ni + 127) / 128, 128, 0, s>>>(mnx, res, L.i_org, L.ni, cell, L.cxl.p, L.ccx.p);
+  TLG_LAUNCHED(ctx);
+  k_lattice_axes<<<(L.nj + 127) / 128, 128, 0, s>>>(mny, res, L.j_org, L.nj, cell, L.cyl.p, L.ccy.p);
+  TLG_LAUNCHED(ctx);
+  int hd = 0;
+  TLG_CUDA(cudaMemcpyAsync(&hd, dup, sizeof(int), cudaMemcpyDeviceToHost, s));
+  TLG_CUDA(cudaStreamSynchronize(s));
+  if (hd) return;  // repeated node: keep the generic sweep
+  L.org_x = mnx + static_cast<double>(L.i_org) * res;
+  L.org_y = mny + static_cast<double>(L.j_org) * res;
+  L.inv_res = 1.0 / res;
+  L.valid = true;
+}
+
+LatticeView lattice_view(const tlg_model* m) {
+  const LatticeGrid& L = m->lat;
+  LatticeView v;
+  v.W = L.W.p;
+  v.P = L.P.p;
+  v.cxl = L.cxl.p;
+  v.cyl = L.cyl.p;
+  v.ccx = L.ccx.p;
+  v.ccy = L.ccy.p;
+  v.ni = L.ni;
+  v.nj = L.nj;
+  v.lo = L.lo;
+  v.span = m->grid.span;
+  v.org_x = L.org_x;
+  v.org_y = L.org_y;
+  v.inv_res = L.inv_res;
+  v.cell = m->grid.cell;
+  for (int k = 0; k < 16; ++k) {
+    v.inmask[k] = L.inmask[k];
+    v.bdmask[k] = L.bdmask[k];
+  }
+  v.corner_ok = L.corner_ok;
+  // e_y recurrence (eval.cu): exponents stay within +-600 over the window
+  // span, so no under/overflow; otherwise evaluate exp per node.
+  const double res = m->cparams.mesh_resolution;
+  const double c = m->kc.neg_inv_2s2;
+  const double span = (L.win + 1) * res;
+  v.res = res;
+  v.c_res = c * res;
+  v.k2 = std::exp(2.0 * c * res * res);
+  v.rec_ok = (std::fabs(c) * span * span < 600.0 && std::fabs(c) * res * 2.0 * span < 600.0) ? 1 : 0;
+  return v;
+}
+
 void build_center_grid(tlg_model* m) {
   tlg_ctx* ctx = m->ctx;
   cudaStream_t s = ctx->stream;
@@ -133,6 +305,7 @@ void build_center_grid(tlg_model* m) {
   k_gather_sorted<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g.sorted_id.p, n, m->cx.p, m->cy.p,
                                                              m->w.p, g.scx.p, g.scy.p, g.sw.p);
   TLG_LAUNCHED(ctx);
+  build_lattice(m);
   m->grid_dirty = false;
 }
 
@@ -150,6 +323,11 @@ void sync_weights_to_grid(tlg_model* m) {
   k_gather_sorted<<<(unsigned)((n + 255) / 256), 256, 0, m->ctx->stream>>>(
       m->grid.sorted_id.p, n, m->cx.p, m->cy.p, m->w.p, nullptr, nullptr, m->grid.sw.p);
   TLG_LAUNCHED(m->ctx);
+  if (m->lat.valid) {
+    k_lattice_refresh<<<(unsigned)((n + 255) / 256), 256, 0, m->ctx->stream>>>(m->lat.slot.p, m->w.p,
+                                                                          n, m->lat.W.p);
+    TLG_LAUNCHED(m->ctx);
+  }
 }
 
 GridView grid_view(const tlg_model* m) {

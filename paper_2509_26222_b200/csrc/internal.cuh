@@ -199,6 +199,98 @@ struct GridView {
   int span, gx0, gy0, gnx, gny;
 };
 
+// Lattice fast path: when every centre is a mesh node roi.min + (i, j) * res
+// (bit-exact, as select_centers / births produce them) and no node repeats,
+// weights live in a dense zero-padded node grid W[i][j] and every query
+// sweeps a fixed WIN x WIN node window whose pairs are pre-classified
+// (always inside / boundary / always outside the cutoff disc).
+constexpr int kMaxWin = 14;
+
+// Window geometry for cutoff R (in lattice units): node offsets
+// [-lo, win - lo) around the base cell; pair (k, l) is always inside the
+// cutoff disc for every point of the (1e-6-expanded) base cell when
+// dmax^2 < (R (1 - 1e-9))^2, and can never be when dmin^2 > (R (1 + 1e-9))^2.
+// constexpr so the hot kernels can be specialised on it (eval.cu).
+struct Geom {
+  int win = 0, lo = 0;
+  uint32_t in[16] = {0}, bd[16] = {0};
+};
+
+constexpr double geo_clamp(double v, double a, double b) { return v < a ? a : (v > b ? b : v); }
+constexpr double geo_max(double a, double b) { return a > b ? a : b; }
+constexpr double geo_abs(double a) { return a < 0 ? -a : a; }
+
+constexpr Geom make_geom(double R) {
+  Geom g{};
+  const double mg = 1e-6;
+  g.lo = static_cast<int>(R + mg);
+  const int hi = static_cast<int>(1.0 + R + mg);
+  g.win = g.lo + hi + 1;
+  if (g.win > kMaxWin) {
+    g.win = 0;
+    return g;
+  }
+  const double rin = R * (1.0 - 1e-9), rout = R * (1.0 + 1e-9);
+  for (int k = 0; k < g.win; ++k)
+    for (int l = 0; l < g.win; ++l) {
+      const double di = k - g.lo, dj = l - g.lo;
+      const double nx = geo_clamp(di, -mg, 1.0 + mg), ny = geo_clamp(dj, -mg, 1.0 + mg);
+      const double dmin2 = (di - nx) * (di - nx) + (dj - ny) * (dj - ny);
+      const double fx = geo_max(geo_abs(di + mg), geo_abs(di - 1.0 - mg));
+      const double fy = geo_max(geo_abs(dj + mg), geo_abs(dj - 1.0 - mg));
+      const double dmax2 = fx * fx + fy * fy;
+      if (dmax2 < rin * rin) g.in[k] |= 1u << l;
+      else if (dmin2 <= rout * rout) g.bd[k] |= 1u << l;
+    }
+  return g;
+}
+
+// Geometries compiled into specialised kernels: the paper's parameters
+// (sigma 0.04, sigma_eps 0.1 -> cutoff 0.32311 m, mesh 0.07 m; R = 4.6159)
+// and the reference tests' (sigma 0.08, sigma_eps 0.05/0.02, mesh 0.12/0.1;
+// R = 2.36..2.47). Any other R runs the runtime-mask kernel.
+constexpr Geom kGeoms[] = {make_geom(4.615857142857142), make_geom(2.4)};
+constexpr int kNumGeoms = 2;
+
+inline bool geom_equal(const Geom& a, const Geom& b) {
+  if (a.win != b.win || a.lo != b.lo) return false;
+  for (int k = 0; k < 16; ++k)
+    if (a.in[k] != b.in[k] || a.bd[k] != b.bd[k]) return false;
+  return true;
+}
+
+struct LatticeGrid {
+  bool valid = false;
+  int win = 0, lo = 0, pad = 0;
+  int ni = 0, nj = 0;          // padded dims
+  int i_org = 0, j_org = 0;    // lattice index of padded (0, 0)
+  double org_x = 0, org_y = 0; // coordinate of padded node (0, 0) (for cell lookup only)
+  double inv_res = 1;
+  uint32_t inmask[16] = {0}, bdmask[16] = {0};
+  int corner_ok = 0;
+  int geom_id = -1;            // index into kGeoms when specialised, else -1
+  DBuf<double> W;
+  DBuf<int> P;                 // presence count per node
+  DBuf<double> cxl, cyl;       // exact node coordinate per padded column / row
+  DBuf<int> ccx, ccy;          // reference cell coordinate floor(c / cell)
+  DBuf<int> slot;              // centre id -> node index in W
+};
+
+struct LatticeView {
+  const double* W;
+  const int* P;
+  const double* cxl;
+  const double* cyl;
+  const int* ccx;
+  const int* ccy;
+  int ni, nj, lo, span;
+  double org_x, org_y, inv_res, cell;
+  uint32_t inmask[16], bdmask[16];
+  int corner_ok;
+  int rec_ok;             // exp recurrence numerically safe for these parameters
+  double res, c_res, k2;  // lattice spacing, c*res, exp(2 c res^2) with c = -1/(2 s^2)
+};
+
 }  // namespace tlg
 
 // ---------------------------------------------------------------------------
@@ -226,7 +318,19 @@ struct tlg_model {
   std::vector<size_t> blk_off;
   std::vector<int> blk_ld;
   tlg::CenterGrid grid;
+  tlg::LatticeGrid lat;
   bool grid_dirty = true;
+};
+
+// A scan's lever arms, binned once per scan by the world cell they fall in
+// under a reference pose, so LM cost evaluations read the weight grid with
+// warp-coherent windows (tlg_scan_* in the ABI).
+struct tlg_scan {
+  tlg_ctx* ctx = nullptr;
+  size_t n = 0;
+  tlg::DBuf<double> hx, hy, hz;
+  tlg::DBuf<uint32_t> perm;
+  double bin_ms = 0.0;
 };
 
 namespace tlg {
@@ -237,6 +341,7 @@ uint32_t block_for_tile(tlg_model* m, int64_t key);
 
 void build_center_grid(tlg_model* m);      // grid.cu
 GridView grid_view(const tlg_model* m);    // grid.cu
+LatticeView lattice_view(const tlg_model* m);
 void ensure_grid(tlg_model* m);
 void sync_weights_to_grid(tlg_model* m);   // after weights change
 

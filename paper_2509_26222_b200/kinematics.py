@@ -78,6 +78,69 @@ def manifold_rows(terrain: TerrainModel, R, t, h, wheel_radius: float = 0.0,
     return rows, NormalEq._from_c(ne)
 
 
+class Scan:
+    """A scan's lever arms binned on the device by world cell under pose
+    (R0, t0) (tlg_scan_create). manifold_rows() rows come out in scan order;
+    permutation()[k] is the input index of row k."""
+
+    def __init__(self, terrain: TerrainModel, R0, t0, h):
+        Rm = np.ascontiguousarray(np.asarray(R0, dtype=np.float64).reshape(9))
+        tv = np.ascontiguousarray(np.asarray(t0, dtype=np.float64).reshape(3))
+        if isinstance(h, (tuple, list)):
+            hx, hy, hz = h
+        elif _is_dev(h):
+            hx, hy, hz = (h[:, j].to(torch.float64).contiguous() for j in range(3))
+        else:
+            ha = np.asarray(h, dtype=np.float64).reshape(-1, 3)
+            hx, hy, hz = (np.ascontiguousarray(ha[:, j]) for j in range(3))
+        self.terrain = terrain
+        self.n = len(hx)
+        self._dev = _is_dev(hx)
+        self._ref = hx
+        hdl = C.c_void_p()
+        check(_abi.load().tlg_scan_create(terrain.handle, _ptr(Rm), _ptr(tv), _ptr(hx), _ptr(hy),
+                                          _ptr(hz), self.n, _mem(hx), C.byref(hdl)))
+        self.handle = hdl
+
+    def bin_ms(self) -> float:
+        n, ms = C.c_size_t(), C.c_double()
+        check(_abi.load().tlg_scan_info(self.handle, C.byref(n), C.byref(ms)))
+        return ms.value
+
+    def permutation(self) -> np.ndarray:
+        out = np.empty(self.n, dtype=np.uint32)
+        check(_abi.load().tlg_scan_permutation(self.handle, _ptr(out), _abi.TLG_HOST))
+        return out
+
+    def manifold_rows(self, R, t, wheel_radius=0.0, lambda_M=1.0, huber_delta=0.05,
+                      want=("r", "J", "valid"), out: dict | None = None, device_out=None):
+        Rm = np.ascontiguousarray(np.asarray(R, dtype=np.float64).reshape(9))
+        tv = np.ascontiguousarray(np.asarray(t, dtype=np.float64).reshape(3))
+        dev = self._dev if device_out is None else device_out
+        ref = self._ref if dev else np.empty(0)
+        n = self.n
+        rows = dict(out or {})
+        for key, dt, size in (("r", np.float64, n), ("J", np.float64, 6 * n),
+                              ("valid", np.uint8, n), ("raw", np.float64, n)):
+            if key in want and key not in rows:
+                rows[key] = _empty_like(ref, size, dt)
+        mem = _abi.TLG_DEVICE if dev else _abi.TLG_HOST
+        ne = NormalEqC()
+        check(_abi.load().tlg_scan_manifold_rows(
+            self.terrain.handle, self.handle, _ptr(Rm), _ptr(tv), float(wheel_radius),
+            float(lambda_M), float(huber_delta), _ptr(rows.get("r")), _ptr(rows.get("J")),
+            _ptr(rows.get("valid")), _ptr(rows.get("raw")), mem, C.byref(ne)))
+        return rows, NormalEq._from_c(ne)
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                _abi.load().tlg_scan_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
 # ---------------------------------------------------------------------------
 # Leg model (leg_model.hpp:14-60): host-side forward kinematics that produces
 # the two wheel lever arms; scalar bookkeeping, not the data path.

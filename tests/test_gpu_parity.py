@@ -231,3 +231,78 @@ def test_snapshot_byte_compatible(gpu_ctx, tmp_path):
     g3 = T.TerrainModel.load(pg)
     z3, _, _, _ = g3.predict(q)
     assert np.array_equal(z3, z1)
+
+
+# ---- lattice fast path edge cases + scans -------------------------------------
+def _lattice_model_with_holes(seed=41):
+    """C1-like lattice model with holes (absent nodes) and ragged support."""
+    xy, z = c1_inputs(6000, seed)
+    keep = ~((xy[:, 0] > 0.3) & (xy[:, 0] < 0.5) & (xy[:, 1] > 0.4) & (xy[:, 1] < 0.7))
+    xy, z = xy[keep], z[keep]
+    k = T.KernelParams()
+    k.finalize()
+    cs = T.select_centers(T.TerrainObservation(xy, z), ROI1, 0.07, 0.12, 3)
+    g, o = _models(k, cs)
+    w = np.cos(np.arange(len(cs.centers)) * 0.71)
+    g.set_weights(w)
+    o.set_weights(w)
+    return k, cs, g, o
+
+
+def test_lattice_edges_and_holes(gpu_ctx):
+    k, cs, g, o = _lattice_model_with_holes()
+    rng = orc.Rng(43)
+    q = uniform_xy(rng, 20000, -0.5, 1.6)
+    # points exactly on nodes and on the cutoff circle around nodes
+    c = cs.centers[::7]
+    ang = np.linspace(0, 2 * np.pi, len(c), endpoint=False)
+    ring = c + k.cutoff_radius * np.stack([np.cos(ang), np.sin(ang)], 1)
+    axis = c + np.stack([np.full(len(c), k.cutoff_radius), np.zeros(len(c))], 1)
+    q = np.concatenate([q, c, ring, axis])
+    z, s, gx, gy = g.predict(q)
+    zr, sr, gxr, gyr = o.predict(q)
+    assert np.array_equal(s, sr)
+    hs, gs = scales(o, q, k.sigma)
+    assert_values_close(z, zr, hs, what="height")
+    assert_values_close(gx, gxr, gs, what="gx")
+    assert_values_close(gy, gyr, gs, what="gy")
+
+
+def test_scan_rows_equal_unbinned(gpu_ctx):
+    k, cs, g, o = _lattice_model_with_holes(45)
+    R = so3_exp([0.03, -0.02, 0.5])
+    t = np.array([0.2, 0.1, 0.3])
+    pts = np.concatenate([uniform_xy(orc.Rng(46), 30000, -0.2, 1.3), np.full((30000, 1), 0.02)], 1)
+    h = (pts - t) @ R
+    rows, ne = kin.manifold_rows(g, R, t, h, 0.0, 1.0, 0.05, want=("r", "J", "valid"))
+    sc = kin.Scan(g, so3_exp([0.0, 0.0, 0.45]), t + 0.05, h)
+    perm = sc.permutation()
+    assert np.array_equal(np.sort(perm), np.arange(len(h)))
+    srows, sne = sc.manifold_rows(R, t, 0.0, 1.0, 0.05)
+    assert np.array_equal(srows["valid"], rows["valid"][perm])
+    assert np.array_equal(srows["r"], rows["r"][perm])  # same per-point arithmetic
+    Jn = rows["J"].reshape(6, -1)
+    Js = srows["J"].reshape(6, -1)
+    assert np.array_equal(Js, Jn[:, perm])
+    np.testing.assert_allclose(sne.A, ne.A, rtol=1e-12, atol=1e-12 * np.abs(ne.A).max())
+    assert sne.valid == ne.valid
+
+
+def test_generic_path_random_centres(gpu_ctx):
+    # non-lattice centres (acceptance_main.cpp:121-127 style) use the generic sweep
+    rng = orc.Rng(102)
+    c = uniform_xy(rng, 300, 0.0, 2.0)
+    k = T.KernelParams(sigma=0.08, sigma_eps=0.05)
+    k.finalize()
+    cs = T.CenterSet(c, 0.07, 0.12, 3, T.Rect((0.0, 0.0), (2.0, 2.0)))
+    g, o = _models(k, cs)
+    w = np.sin(np.arange(300) * 1.3)
+    g.set_weights(w)
+    o.set_weights(w)
+    q = uniform_xy(orc.Rng(103), 5000, -0.3, 2.3)
+    z, s, gx, gy = g.predict(q)
+    zr, sr, gxr, gyr = o.predict(q)
+    assert np.array_equal(s, sr)
+    hs, gs = scales(o, q, k.sigma)
+    assert_values_close(z, zr, hs, what="height")
+    assert_values_close(gx, gxr, gs, what="gx")
