@@ -246,6 +246,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_2509_26222_b200 import distributed as D
     from paper_2509_26222_b200 import kinematics as kin
     from paper_2509_26222_b200 import terrain as T
 
@@ -264,10 +265,8 @@ def main():
 
     def step():
         _, ne = scan.manifold_rows(R, tv, 0.0, 1.0, 0.05, out=rows)
-        if world > 1:
-            vals = list(ne.A[np.triu_indices(6)]) + list(ne.g) + [ne.cost, ne.valid]
-            ne_buf.copy_(torch.tensor(vals, dtype=torch.float64))
-            dist.all_reduce(ne_buf)  # NCCL: the 29-double normal-equation reduce
+        if world > 1:  # NCCL: the 29-double normal-equation reduce
+            ne = D.allreduce_normal_eq(ne, buf=ne_buf)
         return ne
 
     for _ in range(args.warmup):

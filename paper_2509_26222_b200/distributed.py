@@ -1,0 +1,52 @@
+"""Multi-GPU plumbing for the sharded manifold-row sweep.
+
+One process per GPU (torch.distributed, NCCL over NVLink on the B200 box;
+gloo works for the CPU tests). Points are sharded contiguously, every rank
+evaluates its shard with tlg_manifold_rows / tlg_scan_manifold_rows, and the
+only data-path exchange is the 29-double normal-equation block
+(J^T J upper 21, J^T r 6, cost, valid) summed across ranks — the one real
+reduction of the LM cost evaluation.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .kinematics import NormalEq
+
+_IU = np.triu_indices(6)
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous shard [b, e) of n points for `rank` (sizes differ by <= 1)."""
+    base, extra = divmod(n, world)
+    b = rank * base + min(rank, extra)
+    return b, b + base + (1 if rank < extra else 0)
+
+
+def pack(ne: NormalEq) -> np.ndarray:
+    return np.concatenate([ne.A[_IU], ne.g, [ne.cost, float(ne.valid)]])
+
+
+def unpack(v) -> NormalEq:
+    v = np.asarray(v, dtype=np.float64)
+    A = np.zeros((6, 6))
+    A[_IU] = v[:21]
+    A = A + A.T - np.diag(np.diag(A))
+    return NormalEq(A, v[21:27].copy(), float(v[27]), int(round(v[28])))
+
+
+def allreduce_normal_eq(ne: NormalEq, group=None, device=None, buf=None) -> NormalEq:
+    """Sums the normal equations over all ranks (torch.distributed SUM).
+
+    `buf` may be a preallocated 29-element float64 tensor on `device` (the
+    bench keeps one on the GPU so NCCL reduces device memory)."""
+    import torch
+    import torch.distributed as dist
+
+    v = torch.from_numpy(pack(ne))
+    if buf is None:
+        buf = v.to(device) if device is not None else v
+    else:
+        buf.copy_(v)
+    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    return unpack(buf.cpu().numpy())
