@@ -102,6 +102,10 @@ tlg_status tlg_ctx_kernel_stats(tlg_ctx* ctx, int kernel, double* total_ms, uint
 /* FP64 roofline microbenchmark on the context's device: sustained DFMA and
  * DMMA (mma.sync m8n8k4 f64) TFLOP/s. */
 tlg_status tlg_measure_fp64_peak(tlg_ctx* ctx, double* dfma_tflops, double* dmma_tflops);
+/* Dense-solver microbenchmark (diagnostics): op 0 = Cholesky of an n x n SPD
+ * matrix, 1 = triangular solve with nrhs right-hand sides, 2 = GEMM
+ * n x nrhs x n. Best of `reps`, milliseconds. */
+tlg_status tlg_debug_dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps, double* ms);
 
 /* ---- kernel.cpp ------------------------------------------------------------- */
 /* KernelParams::finalize (kernel.cpp:15-25): fills the auto cutoff, validates. */

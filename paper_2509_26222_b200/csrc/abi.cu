@@ -20,6 +20,7 @@ uint32_t add_center_host(tlg_model* m, double x, double y);
 void moment_device(tlg_model* m, const double* x, const double* y, size_t n, uint32_t* rowp,
                    uint32_t** ids, double** vals, size_t* nnz);
 void fp64_peak(tlg_ctx* ctx, double* dfma, double* dmma);
+double dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps);
 tlg_scan* scan_create(tlg_model* m, const double R0[9], const double t0[3], const double* hx,
                       const double* hy, const double* hz, size_t n);
 }  // namespace tlg
@@ -160,6 +161,14 @@ tlg_status tlg_ctx_kernel_stats(tlg_ctx* ctx, int kernel, double* total_ms, uint
     require(kernel >= 0 && kernel < 4, TLG_INVALID_ARGUMENT, "bad kernel id");
     if (total_ms) *total_ms = ctx->prof_ms[kernel];
     if (launches) *launches = ctx->prof_n[kernel];
+  });
+}
+
+tlg_status tlg_debug_dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps, double* ms) {
+  return guard([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(ms, "ms");
+    *ms = dense_bench(ctx, op, n, nrhs, reps);
   });
 }
 

@@ -20,7 +20,10 @@
 // weights/blocks untouched while births persist (:222-225).
 #include <cub/cub.cuh>
 
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 
 #include "dense.cuh"
@@ -442,11 +445,37 @@ static TCsr transpose_csr(tlg_ctx* ctx, const Csr& c, size_t m, int n) {
 }
 
 // ---------------------------------------------------------------------------
+// Stage timer for diagnosis (env TLG_TRACE=1): synchronises and prints the
+// wall time of each update stage to stderr. Off by default (no syncs).
+struct StageTrace {
+  tlg_ctx* ctx;
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  std::string out;
+  explicit StageTrace(tlg_ctx* c) : ctx(c), on(std::getenv("TLG_TRACE") != nullptr) {
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaStreamSynchronize(ctx->stream);
+    const auto now = std::chrono::steady_clock::now();
+    out += std::string(name) + "=" +
+           std::to_string(std::chrono::duration<double, std::micro>(now - last).count()) + "us ";
+    last = now;
+  }
+  ~StageTrace() {
+    if (on)
+      std::fprintf(stderr, "[tlg update] %s total=%.1fus\n", out.c_str(),
+                   std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+
 void recursive_update_device(tlg_model* m, const double* x, const double* y, const double* z,
                              size_t mm, bool allow_birth, tlg_update_report* rep) {
   tlg_ctx* ctx = m->ctx;
   cudaStream_t s = ctx->stream;
   *rep = tlg_update_report{};
+  StageTrace tr(ctx);
 
   // ---- births (terrain_model.cpp:150-161) --------------------------------
   if (allow_birth) {
@@ -481,6 +510,7 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   const size_t nc = m->hcx.size();
   const size_t nb = m->members.size();
   if (nc == 0) return;
+  tr.mark("births");
 
   // ---- active set (:163-172) ---------------------------------------------
   const GridView g = grid_view(m);
@@ -501,6 +531,7 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
     if (hflag[b]) ablocks.push_back(b);  // std::set order = ascending ids
   rep->active_blocks = ablocks.size();
   if (ablocks.empty()) return;
+  tr.mark("active");
 
   // ---- merged system (:174-184) ------------------------------------------
   std::vector<uint32_t> merged;
@@ -546,6 +577,7 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   TLG_CUDA(cudaMemsetAsync(rowof, 0xff, nc * 4, s));
   k_scatter_rowof<<<(n + 255) / 256, 256, 0, s>>>(d_merged, n, rowof);
   TLG_LAUNCHED(ctx);
+  tr.mark("merge");
 
   // ---- K5: Mt (CSR over observations, cols = merged rows) -----------------
   const Csr c = build_csr(m, x, y, mm, rowof, m->kc.neg_inv_2st2, m->kc.scale, false, nullptr);
@@ -555,6 +587,7 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   double* resid = ctx->ws<double>(S_RESID, mm);
   k_residual<<<(unsigned)((mm + 255) / 256), 256, 0, s>>>(c.rowp, c.col, c.val, z, wm, mm, resid);
   TLG_LAUNCHED(ctx);
+  tr.mark("csr");
 
   int* info = ctx->ws<int>(S_FLAGS, 4);
   TLG_CUDA(cudaMemsetAsync(info, 0, 4 * sizeof(int), s));
@@ -572,6 +605,7 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
     double* S = ctx->ws<double>(S_SMAT, static_cast<size_t>(mi) * mi);
     k_build_S<<<mi, 256, 0, s>>>(c.rowp, c.col, c.val, Kt, mi, S);
     TLG_LAUNCHED(ctx);
+    tr.mark("K_S");
     symmetrize(ctx, S, mi, mi);
     potrf_lower(ctx, S, mi, mi, info);
     int h = 0;
@@ -582,11 +616,13 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
       return;
     }
     // u = S^-1 r ; dw = K u
+    tr.mark("potrf");
     trsm_left_lower(ctx, S, mi, mi, resid, 1, mi, 0);
     trsm_left_lower(ctx, S, mi, mi, resid, 1, mi, 1);
     gemm(ctx, GemmDesc{n, 1, mi, Kt, mi, 1, resid, mi, 0, dw, n, 1.0, 0.0, 0});
     // Y = L^-1 K^T (in place) ; Hinv1_q = Hinv0_q - Y_q^T Y_q
     trsm_left_lower(ctx, S, mi, mi, Kt, n, mi, 0);
+    tr.mark("trsm");
     for (int q = 0; q < nq; ++q)
       descs[q] = GemmDesc{tab[q].n, tab[q].n, mi, Kt + static_cast<size_t>(tab[q].off) * mi, mi, 1,
                           Kt + static_cast<size_t>(tab[q].off) * mi, mi, 0,
@@ -641,6 +677,7 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   std::memcpy(h_descs, descs.data(), nq * sizeof(GemmDesc));
   TLG_CUDA(cudaMemcpyAsync(d_descs, h_descs, nq * sizeof(GemmDesc), cudaMemcpyHostToDevice, s));
   gemm_grouped(ctx, d_descs, nq, maxq, maxq);
+  tr.mark("blocks");
   k_symmetrize_blocks<<<nq, 256, 0, s>>>(d_tab, m->pool.p);
   TLG_LAUNCHED(ctx);
   k_apply_dw<<<(n + 255) / 256, 256, 0, s>>>(m->w.p, d_merged, n, dw);
