@@ -1,0 +1,436 @@
+// terralio_b200/terrain.hpp — the reference's C++ terrain API
+// (proj/core/include/terralio/terrain/{kernel,center_select,terrain_model}.hpp,
+// kinematics/contact.hpp) rebuilt on the C-ABI in terralio_gpu.h.
+//
+// Drop-in notes: same namespaces, class/function names, argument meaning and
+// exception types; the Eigen types are replaced by the small value types
+// below (x()/y()/z() accessors like Eigen's). TerrainModel is move-only like
+// the reference's (terrain_model.hpp:95). All numerics run on the GPU; this
+// header holds no arithmetic beyond parameter plumbing.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../terralio_gpu.h"
+
+namespace terralio {
+
+struct Vec2 {
+  double v[2] = {0.0, 0.0};
+  Vec2() = default;
+  Vec2(double x, double y) : v{x, y} {}
+  double x() const { return v[0]; }
+  double y() const { return v[1]; }
+  double& x() { return v[0]; }
+  double& y() { return v[1]; }
+  double squaredNorm() const { return v[0] * v[0] + v[1] * v[1]; }
+  bool allFinite() const { return std::isfinite(v[0]) && std::isfinite(v[1]); }
+};
+
+struct Vec3 {
+  double v[3] = {0.0, 0.0, 0.0};
+  Vec3() = default;
+  Vec3(double x, double y, double z) : v{x, y, z} {}
+  double x() const { return v[0]; }
+  double y() const { return v[1]; }
+  double z() const { return v[2]; }
+};
+
+// Row-major 3x3.
+struct Mat3 {
+  double a[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  double operator()(int r, int c) const { return a[3 * r + c]; }
+  double& operator()(int r, int c) { return a[3 * r + c]; }
+  static Mat3 Identity() { return Mat3{}; }
+};
+
+struct Rect {
+  Vec2 min, max;
+  bool contains(const Vec2& p) const {
+    return p.x() >= min.x() && p.x() <= max.x() && p.y() >= min.y() && p.y() <= max.y();
+  }
+  Rect dilated(double m) const {
+    return {{min.x() - m, min.y() - m}, {max.x() + m, max.y() + m}};
+  }
+};
+
+namespace gpu {
+
+// Maps a status code onto the reference's exception types.
+struct NoSupportedCentersError;
+[[noreturn]] void throw_status(tlg_status st);
+
+inline void check(tlg_status st) {
+  if (st != TLG_OK) throw_status(st);
+}
+
+// Process-wide default device context (device 0, private stream).
+class Context {
+ public:
+  explicit Context(int device = 0, void* stream = nullptr) {
+    check(tlg_ctx_create(device, stream, &ctx_));
+  }
+  ~Context() { tlg_ctx_destroy(ctx_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  tlg_ctx* get() const { return ctx_; }
+  static Context& instance() {
+    static Context c;
+    return c;
+  }
+
+ private:
+  tlg_ctx* ctx_ = nullptr;
+};
+
+}  // namespace gpu
+
+namespace terrain {
+
+// kernel.hpp:12-24
+struct KernelParams {
+  double sigma = 0.04;
+  double sigma_eps = 0.1;
+  double lambda = 1e-3;
+  double cutoff_radius = 0.0;
+  double sigma_tilde() const { return std::sqrt(sigma * sigma + sigma_eps * sigma_eps); }
+  double moment_scale() const {
+    const double st2 = sigma * sigma + sigma_eps * sigma_eps;
+    return sigma * sigma / st2;
+  }
+  void finalize() {
+    tlg_kernel_params p = c();
+    gpu::check(tlg_kernel_finalize(&p));
+    cutoff_radius = p.cutoff_radius;
+  }
+  tlg_kernel_params c() const { return {sigma, sigma_eps, lambda, cutoff_radius}; }
+};
+
+struct SparseVec {
+  std::vector<std::pair<std::uint32_t, double>> entries;
+};
+
+// center_select.hpp:11-32
+struct TerrainObservation {
+  std::vector<Vec2> xy;
+  std::vector<double> z;
+  std::size_t size() const { return xy.size(); }
+  void validate() const {
+    if (xy.size() != z.size()) throw std::invalid_argument("observation xy/z length mismatch");
+    if (xy.empty()) throw std::invalid_argument("empty observation");
+    for (std::size_t i = 0; i < xy.size(); ++i)
+      if (!xy[i].allFinite() || !std::isfinite(z[i]))
+        throw std::invalid_argument("non-finite observation coordinate");
+  }
+};
+
+struct CenterSet {
+  std::vector<Vec2> centers;
+  double mesh_resolution = 0.07;
+  double accept_radius = 0.07;
+  int accept_count = 3;
+  Rect roi;
+  tlg_center_params c() const {
+    return {mesh_resolution, accept_radius, accept_count, 0,
+            roi.min.x(),     roi.min.y(),   roi.max.x(), roi.max.y()};
+  }
+};
+
+struct NoSupportedCenters : std::runtime_error {
+  NoSupportedCenters() : std::runtime_error("no supported centers") {}
+};
+
+struct HeightQuery {
+  double z = 0.0;
+  bool supported = false;
+};
+
+struct UpdateReport {
+  std::size_t active_blocks = 0, active_centers = 0, born_centers = 0;
+  bool rejected = false;
+};
+
+namespace detail {
+struct Soa {
+  std::vector<double> x, y;
+};
+inline Soa split(const std::vector<Vec2>& v) {
+  Soa s;
+  s.x.resize(v.size());
+  s.y.resize(v.size());
+  for (std::size_t i = 0; i < v.size(); ++i) {
+    s.x[i] = v[i].x();
+    s.y[i] = v[i].y();
+  }
+  return s;
+}
+inline std::vector<Vec2> nodes(tlg_status (*fn)(tlg_ctx*, const double*, const double*,
+                                                const double*, size_t, size_t, tlg_mem,
+                                                const tlg_center_params*, double*, double*,
+                                                size_t, size_t*, tlg_mem),
+                               const TerrainObservation& pts, const tlg_center_params& cp) {
+  const Soa s = split(pts.xy);
+  size_t cap = std::max<size_t>(64, pts.size()), n = 0;
+  std::vector<double> ox(cap), oy(cap);
+  tlg_status st = fn(gpu::Context::instance().get(), s.x.data(), s.y.data(), pts.z.data(),
+                     pts.xy.size(), pts.z.size(), TLG_HOST, &cp, ox.data(), oy.data(), cap, &n,
+                     TLG_HOST);
+  if (st == TLG_BUFFER_TOO_SMALL) {
+    cap = n;
+    ox.resize(cap);
+    oy.resize(cap);
+    st = fn(gpu::Context::instance().get(), s.x.data(), s.y.data(), pts.z.data(), pts.xy.size(),
+            pts.z.size(), TLG_HOST, &cp, ox.data(), oy.data(), cap, &n, TLG_HOST);
+  }
+  gpu::check(st);
+  std::vector<Vec2> out(n);
+  for (size_t i = 0; i < n; ++i) out[i] = {ox[i], oy[i]};
+  return out;
+}
+}  // namespace detail
+
+// center_select.cpp:18-76
+inline std::vector<Vec2> supported_mesh_nodes(const TerrainObservation& points, const Rect& roi,
+                                              double mesh_resolution, double accept_radius,
+                                              int accept_count) {
+  CenterSet p;
+  p.roi = roi;
+  p.mesh_resolution = mesh_resolution;
+  p.accept_radius = accept_radius;
+  p.accept_count = accept_count;
+  return detail::nodes(&tlg_supported_mesh_nodes, points, p.c());
+}
+
+inline CenterSet select_centers(const TerrainObservation& points, const Rect& roi,
+                                double mesh_resolution, double accept_radius, int accept_count) {
+  CenterSet set;
+  set.roi = roi;
+  set.mesh_resolution = mesh_resolution;
+  set.accept_radius = accept_radius;
+  set.accept_count = accept_count;
+  set.centers = detail::nodes(&tlg_select_centers, points, set.c());
+  return set;
+}
+
+// terrain_model.hpp:28-97 over a device-resident model
+class TerrainModel {
+ public:
+  TerrainModel() = default;
+  TerrainModel(KernelParams kernel, CenterSet centers) {
+    const detail::Soa s = detail::split(centers.centers);
+    const tlg_kernel_params k = kernel.c();
+    const tlg_center_params cp = centers.c();
+    tlg_model* m = nullptr;
+    gpu::check(tlg_model_create(gpu::Context::instance().get(), &k, &cp, s.x.data(), s.y.data(),
+                                s.x.size(), TLG_HOST, &m));
+    m_.reset(m);
+  }
+  explicit TerrainModel(tlg_model* adopt) : m_(adopt) {}
+  TerrainModel(TerrainModel&&) = default;
+  TerrainModel& operator=(TerrainModel&&) = default;
+
+  KernelParams kernel() const {
+    tlg_kernel_params k;
+    gpu::check(tlg_model_kernel(m_.get(), &k));
+    return {k.sigma, k.sigma_eps, k.lambda, k.cutoff_radius};
+  }
+  CenterSet centers() const {
+    tlg_center_params p;
+    gpu::check(tlg_model_center_params(m_.get(), &p));
+    CenterSet s;
+    s.mesh_resolution = p.mesh_resolution;
+    s.accept_radius = p.accept_radius;
+    s.accept_count = p.accept_count;
+    s.roi = {{p.roi_min_x, p.roi_min_y}, {p.roi_max_x, p.roi_max_y}};
+    const std::size_t n = num_centers();
+    std::vector<double> x(n), y(n);
+    gpu::check(tlg_model_get_centers(m_.get(), x.data(), y.data(), TLG_HOST));
+    s.centers.resize(n);
+    for (std::size_t i = 0; i < n; ++i) s.centers[i] = {x[i], y[i]};
+    return s;
+  }
+  std::vector<double> weights() const {
+    std::vector<double> w(num_centers());
+    if (!w.empty()) gpu::check(tlg_model_get_weights(m_.get(), w.data(), TLG_HOST));
+    return w;
+  }
+  std::size_t num_centers() const {
+    size_t n = 0, b = 0;
+    gpu::check(tlg_model_counts(m_.get(), &n, &b));
+    return n;
+  }
+  std::size_t num_blocks() const {
+    size_t n = 0, b = 0;
+    gpu::check(tlg_model_counts(m_.get(), &n, &b));
+    return b;
+  }
+  std::uint32_t block_of(std::uint32_t center) const {
+    std::vector<std::uint32_t> b(num_centers());
+    gpu::check(tlg_model_get_block_index(m_.get(), b.data(), TLG_HOST));
+    return b.at(center);
+  }
+  std::vector<std::uint32_t> block_members(std::uint32_t b) const {
+    size_t n = 0;
+    gpu::check(tlg_model_block_size(m_.get(), b, &n));
+    std::vector<std::uint32_t> out(n);
+    gpu::check(tlg_model_get_block_members(m_.get(), b, out.data()));
+    return out;
+  }
+  // column-major bn x bn (Eigen::MatrixXd storage order)
+  std::vector<double> block_info_inverse(std::uint32_t b) const {
+    size_t n = 0;
+    gpu::check(tlg_model_block_size(m_.get(), b, &n));
+    std::vector<double> out(n * n);
+    if (n) gpu::check(tlg_model_get_block_info_inverse(m_.get(), b, out.data(), TLG_HOST));
+    return out;
+  }
+
+  // terrain_model.cpp:97-107
+  SparseVec moment_feature(const Vec2& x) const {
+    uint32_t rp[2];
+    std::vector<uint32_t> ids(4096);
+    std::vector<double> vals(4096);
+    size_t nnz = 0;
+    gpu::check(tlg_moment_features(m_.get(), &x.v[0], &x.v[1], 1, TLG_HOST, rp, ids.data(),
+                                   vals.data(), ids.size(), &nnz, TLG_HOST));
+    SparseVec out;
+    for (size_t i = 0; i < nnz; ++i) out.entries.emplace_back(ids[i], vals[i]);
+    return out;
+  }
+
+  // terrain_model.cpp:109-143 (a query of one point; batch with predict())
+  HeightQuery predict_height(const Vec2& x) const {
+    double z = 0.0;
+    uint8_t s = 0;
+    gpu::check(tlg_eval(m_.get(), &x.v[0], &x.v[1], 1, TLG_HOST, &z, &s, nullptr, nullptr,
+                        TLG_HOST));
+    return {z, s != 0};
+  }
+  Vec2 predict_gradient(const Vec2& x) const {
+    Vec2 g;
+    gpu::check(tlg_eval(m_.get(), &x.v[0], &x.v[1], 1, TLG_HOST, nullptr, nullptr, &g.v[0],
+                        &g.v[1], TLG_HOST));
+    return g;
+  }
+  // Batched: SoA host arrays; any output may be null.
+  void predict(const double* x, const double* y, std::size_t n, double* z, uint8_t* supported,
+               double* gx, double* gy) const {
+    gpu::check(tlg_eval(m_.get(), x, y, n, TLG_HOST, z, supported, gx, gy, TLG_HOST));
+  }
+
+  // terrain_model.cpp:145-253
+  UpdateReport recursive_update(const TerrainObservation& obs, bool allow_birth = true) {
+    const detail::Soa s = detail::split(obs.xy);
+    tlg_update_report r{};
+    gpu::check(tlg_recursive_update(m_.get(), s.x.data(), s.y.data(), obs.z.data(), obs.xy.size(),
+                                    obs.z.size(), TLG_HOST, allow_birth ? 1 : 0, &r));
+    return {static_cast<std::size_t>(r.active_blocks), static_cast<std::size_t>(r.active_centers),
+            static_cast<std::size_t>(r.born_centers), r.rejected != 0};
+  }
+
+  void save(const std::string& path) const { gpu::check(tlg_model_save(m_.get(), path.c_str())); }
+  static TerrainModel load(const std::string& path) {
+    tlg_model* m = nullptr;
+    gpu::check(tlg_model_load(gpu::Context::instance().get(), path.c_str(), &m));
+    return TerrainModel(m);
+  }
+
+  tlg_model* handle() const { return m_.get(); }
+
+ private:
+  struct Del {
+    void operator()(tlg_model* m) const { tlg_model_destroy(m); }
+  };
+  std::unique_ptr<tlg_model, Del> m_;
+};
+
+// terrain_model.cpp:269-308
+inline TerrainModel fit_batch_ridge(const KernelParams& params, const CenterSet& centers,
+                                    const TerrainObservation& obs) {
+  const detail::Soa c = detail::split(centers.centers);
+  const detail::Soa o = detail::split(obs.xy);
+  const tlg_kernel_params k = params.c();
+  const tlg_center_params cp = centers.c();
+  tlg_model* m = nullptr;
+  gpu::check(tlg_fit_batch_ridge(gpu::Context::instance().get(), &k, &cp, c.x.data(), c.y.data(),
+                                 c.x.size(), o.x.data(), o.y.data(), obs.z.data(), obs.xy.size(),
+                                 obs.z.size(), TLG_HOST, &m));
+  return TerrainModel(m);
+}
+
+}  // namespace terrain
+
+namespace kin {
+
+// Batched manifold rows (contact.cpp:7-39 + scan_matcher.cpp:221-248) and the
+// fused normal equations (scan_matcher.cpp:296-299).
+struct ManifoldRows {
+  std::vector<double> r, J;  // J column-major rows x 6 (Eigen CostEval layout)
+  std::vector<uint8_t> valid;
+  tlg_normal_eq ne{};
+};
+
+inline ManifoldRows manifold_rows(const terrain::TerrainModel& terrain, const Mat3& R,
+                                  const Vec3& t, const std::vector<Vec3>& lever,
+                                  double wheel_radius, double lambda_M, double huber_delta) {
+  const std::size_t n = lever.size();
+  std::vector<double> hx(n), hy(n), hz(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    hx[i] = lever[i].x();
+    hy[i] = lever[i].y();
+    hz[i] = lever[i].z();
+  }
+  ManifoldRows out;
+  out.r.resize(n);
+  out.J.resize(6 * n);
+  out.valid.resize(n);
+  gpu::check(tlg_manifold_rows(terrain.handle(), R.a, t.v, hx.data(), hy.data(), hz.data(), n,
+                               TLG_HOST, wheel_radius, lambda_M, huber_delta, out.r.data(),
+                               out.J.data(), out.valid.data(), nullptr, TLG_HOST, &out.ne));
+  return out;
+}
+
+struct ManifoldResidual {
+  double value = 0.0;
+  bool valid = false;
+};
+
+// contact.cpp:7-19 for one wheel with lever arm h (chain_end_position(q)).
+inline ManifoldResidual manifold_residual(const Mat3& R, const Vec3& t, const Vec3& h,
+                                          double wheel_radius,
+                                          const terrain::TerrainModel& terrain) {
+  double raw = 0.0;
+  uint8_t valid = 0;
+  gpu::check(tlg_manifold_rows(terrain.handle(), R.a, t.v, &h.v[0], &h.v[1], &h.v[2], 1,
+                               TLG_HOST, wheel_radius, 1.0, 0.0, nullptr, nullptr, &valid, &raw,
+                               TLG_HOST, nullptr));
+  return {valid ? raw : 0.0, valid != 0};
+}
+
+}  // namespace kin
+
+namespace gpu {
+[[noreturn]] inline void throw_status(tlg_status st) {
+  const std::string msg = tlg_last_error();
+  switch (st) {
+    case TLG_INVALID_ARGUMENT:
+      throw std::invalid_argument(msg);
+    case TLG_DOMAIN_ERROR:
+      throw std::domain_error(msg);
+    case TLG_NO_SUPPORTED_CENTERS:
+      throw terrain::NoSupportedCenters();
+    case TLG_OUT_OF_MEMORY:
+      throw std::bad_alloc();
+    default:
+      throw std::runtime_error(msg);
+  }
+}
+}  // namespace gpu
+
+}  // namespace terralio

@@ -1,0 +1,118 @@
+// C++ drop-in check: the reference's hot-path unit tests written against the
+// C++ shim (include/terralio_b200/terrain.hpp), i.e. the way proj/core code
+// calls the terrain model. Exit code = number of failed checks.
+// Build: g++ -std=c++20 -Iinclude tests/cpp/test_shim.cpp -Lpaper_2509_26222_b200/lib
+//        -lterralio_gpu -Wl,-rpath,...
+#include <cmath>
+#include <cstdio>
+#include <random>
+
+#include "terralio_b200/terrain.hpp"
+
+using namespace terralio;
+using namespace terralio::terrain;
+
+static int failures = 0;
+#define CHECK(c)                                                   \
+  do {                                                             \
+    if (!(c)) {                                                    \
+      std::printf("FAIL %s:%d  %s\n", __FILE__, __LINE__, #c);     \
+      ++failures;                                                  \
+    }                                                              \
+  } while (0)
+
+int main() {
+  // kernel.cpp finalize (test_kernel.cpp:50-69)
+  KernelParams k;
+  k.finalize();
+  CHECK(std::fabs(k.cutoff_radius - 3.0 * k.sigma_tilde()) < 1e-15);
+  bool threw = false;
+  try {
+    KernelParams bad;
+    bad.sigma = 0.0;
+    bad.finalize();
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
+
+  // select_centers support rule (test_center_select.cpp:21-36)
+  std::mt19937_64 rng(11);
+  std::uniform_real_distribution<double> u(0.0, 2.0);
+  TerrainObservation obs;
+  for (int i = 0; i < 400; ++i) {
+    obs.xy.push_back({u(rng), u(rng)});
+    obs.z.push_back(0.1 * std::sin(4.0 * obs.xy.back().x()));
+  }
+  const Rect roi{{0.0, 0.0}, {2.0, 2.0}};
+  const CenterSet set = select_centers(obs, roi, 0.1, 0.12, 3);
+  CHECK(!set.centers.empty());
+  for (const Vec2& c : set.centers) {
+    int n = 0;
+    for (const Vec2& p : obs.xy)
+      n += std::hypot(p.x() - c.x(), p.y() - c.y()) <= 0.12;
+    CHECK(roi.contains(c) && n >= 3);
+  }
+  threw = false;
+  try {
+    TerrainObservation far;
+    far.xy.push_back({10.0, 10.0});
+    far.z.push_back(0.0);
+    select_centers(far, {{0.0, 0.0}, {1.0, 1.0}}, 0.1, 0.1, 3);
+  } catch (const NoSupportedCenters&) {
+    threw = true;
+  }
+  CHECK(threw);
+
+  // model: recursive updates reproduce the batch fit (test_terrain_model.cpp:109-126)
+  KernelParams kk;
+  kk.sigma = 0.08;
+  kk.sigma_eps = 0.05;
+  kk.cutoff_radius = 10.0;
+  kk.finalize();
+  TerrainModel rec(kk, set);
+  for (int s = 0; s < 4; ++s) {
+    TerrainObservation part;
+    part.xy.assign(obs.xy.begin() + s * 100, obs.xy.begin() + (s + 1) * 100);
+    part.z.assign(obs.z.begin() + s * 100, obs.z.begin() + (s + 1) * 100);
+    const UpdateReport r = rec.recursive_update(part, false);
+    CHECK(!r.rejected);
+  }
+  const TerrainModel batch = fit_batch_ridge(kk, set, obs);
+  const auto wr = rec.weights(), wb = batch.weights();
+  double num = 0.0, den = 0.0;
+  for (std::size_t i = 0; i < wr.size(); ++i) {
+    num += (wr[i] - wb[i]) * (wr[i] - wb[i]);
+    den += wb[i] * wb[i];
+  }
+  CHECK(std::sqrt(num / den) < 1e-8);
+
+  // predict_height / unsupported (test_terrain_model.cpp:79-100)
+  const HeightQuery q = batch.predict_height({1.0, 1.0});
+  CHECK(q.supported);
+  const HeightQuery far = batch.predict_height({50.0, 50.0});
+  CHECK(!far.supported && far.z == 0.0);
+  threw = false;
+  try {
+    batch.predict_height({NAN, 0.0});
+  } catch (const std::domain_error&) {
+    threw = true;
+  }
+  CHECK(threw);
+
+  // snapshot round trip (test_terrain_model.cpp:226-241)
+  batch.save("/tmp/terralio_b200_shim.bin");
+  const TerrainModel loaded = TerrainModel::load("/tmp/terralio_b200_shim.bin");
+  CHECK(loaded.num_centers() == batch.num_centers());
+  CHECK(std::fabs(loaded.predict_height({1.0, 1.0}).z - q.z) <= 1e-14 * std::fabs(q.z) + 1e-300);
+
+  // manifold rows + normal equations
+  std::vector<Vec3> lever;
+  for (int i = 0; i < 1000; ++i) lever.push_back({u(rng), u(rng), 0.05});
+  const auto rows = kin::manifold_rows(batch, Mat3::Identity(), Vec3{0.0, 0.0, 0.0}, lever, 0.0,
+                                       1.0, 0.05);
+  CHECK(rows.ne.valid > 900);
+  CHECK(rows.ne.cost > 0.0);
+  std::printf("test_shim: %d failure(s)\n", failures);
+  return failures;
+}

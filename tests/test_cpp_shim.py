@@ -1,0 +1,32 @@
+"""The C++ drop-in shim (include/terralio_b200/terrain.hpp): compiles against
+the C-ABI header and links the in-tree library on CPU; on a B200 the C++
+restatement of the reference tests runs through it."""
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+LIBDIR = ROOT / "paper_2509_26222_b200" / "lib"
+OUT = ROOT / "build" / "test_shim"
+
+
+def _build():
+    OUT.parent.mkdir(parents=True, exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-I", str(ROOT / "include"),
+           str(ROOT / "tests" / "cpp" / "test_shim.cpp"), "-L", str(LIBDIR), "-lterralio_gpu",
+           f"-Wl,-rpath,{LIBDIR}", "-o", str(OUT)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return OUT
+
+
+def test_shim_compiles_and_links():
+    assert _build().exists()
+
+
+@pytest.mark.gpu
+def test_shim_reference_tests_on_gpu():
+    exe = _build()
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
