@@ -236,8 +236,12 @@ __global__ void __launch_bounds__(128, 4) k_eval(GridView g, LatticeView L,
                                                  uint8_t* __restrict__ sup,
                                                  double* __restrict__ gx,
                                                  double* __restrict__ gy, int* __restrict__ err) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x) {
+  // contiguous chunk per warp (locality of the weight window, see k_manifold)
+  const size_t warps = (size_t)gridDim.x * (blockDim.x >> 5);
+  const size_t per_warp = ((n + 31) / 32 + warps - 1) / warps;
+  const size_t wid_g = (size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const size_t b_end = std::min(n, (wid_g + 1) * per_warp * 32);
+  for (size_t i = wid_g * per_warp * 32 + (threadIdx.x & 31); i < b_end; i += 32) {
     const double px = x[i], py = y[i];
     if (!isfinite(px) || !isfinite(py)) {
       atomicOr(err, 1);
@@ -344,9 +348,15 @@ __global__ void __launch_bounds__(kManifoldThreads, TLG_MANIFOLD_MINB) k_manifol
   double acc = 0.0;
   const double* R = pose.R;
   const int lane = threadIdx.x & 31;
+  // Each warp walks a contiguous chunk of rows: with scan-binned input,
+  // consecutive iterations hit the same / neighbouring lattice cells, so the
+  // weight window stays L1-resident (a grid-stride walk jumps regions).
   const size_t warps = (size_t)gridDim.x * (blockDim.x >> 5);
-  for (size_t base = ((size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < n;
-       base += warps * 32) {
+  const size_t witer = (n + 31) / 32;
+  const size_t per_warp = (witer + warps - 1) / warps;
+  const size_t wid_g = (size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const size_t b_end = std::min(n, (wid_g + 1) * per_warp * 32);
+  for (size_t base = wid_g * per_warp * 32; base < b_end; base += 32) {
     const size_t i = base + lane;
     const bool live = i < n;
     const double h0 = live ? hx[i] : 0.0, h1 = live ? hy[i] : 0.0, h2 = live ? hz[i] : 0.0;
