@@ -129,6 +129,11 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
   }
   auto column = [&](auto KC) {
     constexpr int k = decltype(KC)::value;
+#ifdef TLG_COL_FENCE
+    // compiler-only barrier: keeps the window loads of later columns from
+    // being hoisted here (they would need ~2 registers each and spill)
+    if constexpr (k % TLG_COL_FENCE == 0) asm volatile("" ::: "memory");
+#endif
     const double dx = k == 0 ? dx_first : __dsub_rn(__ldg(L.cxl + i0 + k), x);
     const double dx2 = __dmul_rn(dx, dx);
     const bool colok = abs(__ldg(L.ccx + i0 + k) - qx) <= L.span;
