@@ -51,21 +51,6 @@ __device__ __forceinline__ Sweep sweep_of(const GridView& g, double px, double p
   return s;
 }
 
-__global__ void k_mark_active(GridView g, const double* __restrict__ x,
-                              const double* __restrict__ y, size_t m, double r2,
-                              uint8_t* __restrict__ active) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < m;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const double px = x[i], py = y[i];
-    const Sweep s = sweep_of(g, px, py);
-    for (int gx = s.x_lo; gx <= s.x_hi; ++gx) {
-      const int b = g.cell_start[gx * g.gny + s.y_lo], e = g.cell_start[gx * g.gny + s.y_hi + 1];
-      for (int k = b; k < e; ++k)
-        if (sq2_exact(g.cx[k] - px, g.cy[k] - py) <= r2) active[g.id[k]] = 1;
-    }
-  }
-}
-
 __global__ void k_mark_blocks(const uint8_t* __restrict__ active,
                               const uint32_t* __restrict__ bidx, size_t n,
                               uint8_t* __restrict__ bflag) {
@@ -81,61 +66,107 @@ __global__ void k_scatter_rowof(const uint32_t* __restrict__ merged, int n,
 
 // CSR count / fill over observations: entry (col, s * exp(-d2/(2 b^2))) for
 // every candidate with d2 <= cutoff^2 and kappa != 0. col = rowof[id] or id.
-__global__ void k_csr_count(GridView g, const double* __restrict__ x, const double* __restrict__ y,
-                            size_t m, double r2, double neg_inv_2b2, uint32_t* __restrict__ cnt) {
-  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  const double px = x[i], py = y[i];
-  const Sweep s = sweep_of(g, px, py);
-  uint32_t c = 0;
-  for (int gx = s.x_lo; gx <= s.x_hi; ++gx) {
-    const int b = g.cell_start[gx * g.gny + s.y_lo], e = g.cell_start[gx * g.gny + s.y_hi + 1];
-    for (int k = b; k < e; ++k) {
-      const double d2 = sq2_exact(g.cx[k] - px, g.cy[k] - py);
-      if (d2 <= r2 && exp(d2 * neg_inv_2b2) != 0.0) ++c;
+// Warp-per-observation variants (observation counts per scan are small, so
+// one thread per observation walking ~190 candidates serially leaves the GPU
+// idle): lanes stride over the candidate runs of the 3 cell columns; the fill
+// keeps the serial candidate order through a ballot prefix.
+__global__ void __launch_bounds__(128) k_mark_active_w(GridView g, const double* __restrict__ x,
+                                                       const double* __restrict__ y, size_t m,
+                                                       double r2, uint8_t* __restrict__ active) {
+  const int lane = threadIdx.x & 31;
+  const size_t nw = (size_t)gridDim.x * (blockDim.x >> 5);
+  for (size_t i = blockIdx.x * (size_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < m; i += nw) {
+    const double px = x[i], py = y[i];
+    const Sweep s = sweep_of(g, px, py);
+    for (int gx = s.x_lo; gx <= s.x_hi; ++gx) {
+      const int b = g.cell_start[gx * g.gny + s.y_lo], e = g.cell_start[gx * g.gny + s.y_hi + 1];
+      for (int k = b + lane; k < e; k += 32)
+        if (sq2_exact(g.cx[k] - px, g.cy[k] - py) <= r2) active[g.id[k]] = 1;
     }
   }
-  cnt[i] = c;
 }
 
-__global__ void k_csr_fill(GridView g, const double* __restrict__ x, const double* __restrict__ y,
-                           size_t m, double r2, double neg_inv_2b2, double scale,
-                           const uint32_t* __restrict__ rowp, const int* __restrict__ rowof,
-                           uint32_t* __restrict__ col, double* __restrict__ val, int sort_ids) {
-  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  const double px = x[i], py = y[i];
-  const Sweep s = sweep_of(g, px, py);
-  uint32_t o = rowp[i];
-  const uint32_t o0 = o;
-  for (int gx = s.x_lo; gx <= s.x_hi; ++gx) {
-    const int b = g.cell_start[gx * g.gny + s.y_lo], e = g.cell_start[gx * g.gny + s.y_hi + 1];
-    for (int k = b; k < e; ++k) {
-      const double d2 = sq2_exact(g.cx[k] - px, g.cy[k] - py);
-      if (d2 <= r2) {
-        const double kv = exp(d2 * neg_inv_2b2);
-        if (kv != 0.0) {
-          const uint32_t id = g.id[k];
-          col[o] = rowof ? static_cast<uint32_t>(rowof[id]) : id;
-          val[o] = scale * kv;
-          ++o;
-        }
+__global__ void __launch_bounds__(128) k_csr_count_w(GridView g, const double* __restrict__ x,
+                                                     const double* __restrict__ y, size_t m,
+                                                     double r2, double neg_inv_2b2,
+                                                     uint32_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const size_t nw = (size_t)gridDim.x * (blockDim.x >> 5);
+  for (size_t i = blockIdx.x * (size_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < m; i += nw) {
+    const double px = x[i], py = y[i];
+    const Sweep s = sweep_of(g, px, py);
+    uint32_t c = 0;
+    for (int gx = s.x_lo; gx <= s.x_hi; ++gx) {
+      const int b = g.cell_start[gx * g.gny + s.y_lo], e = g.cell_start[gx * g.gny + s.y_hi + 1];
+      for (int k = b + lane; k < e; k += 32) {
+        const double d2 = sq2_exact(g.cx[k] - px, g.cy[k] - py);
+        if (d2 <= r2 && exp(d2 * neg_inv_2b2) != 0.0) ++c;
       }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[i] = c;
   }
-  if (sort_ids)
-    for (uint32_t a = o0 + 1; a < o; ++a) {
-      const uint32_t ki = col[a];
-      const double kvv = val[a];
-      uint32_t b = a;
-      while (b > o0 && col[b - 1] > ki) {
-        col[b] = col[b - 1];
-        val[b] = val[b - 1];
-        --b;
+}
+
+__global__ void __launch_bounds__(128) k_csr_fill_w(GridView g, const double* __restrict__ x,
+                                                    const double* __restrict__ y, size_t m,
+                                                    double r2, double neg_inv_2b2, double scale,
+                                                    const uint32_t* __restrict__ rowp,
+                                                    const int* __restrict__ rowof,
+                                                    uint32_t* __restrict__ col,
+                                                    double* __restrict__ val, int sort_ids) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const size_t nw = (size_t)gridDim.x * (blockDim.x >> 5);
+  for (size_t i = blockIdx.x * (size_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < m; i += nw) {
+    const double px = x[i], py = y[i];
+    const Sweep s = sweep_of(g, px, py);
+    uint32_t o = rowp[i];
+    const uint32_t o0 = o;
+    for (int gx = s.x_lo; gx <= s.x_hi; ++gx) {
+      const int b = g.cell_start[gx * g.gny + s.y_lo], e = g.cell_start[gx * g.gny + s.y_hi + 1];
+      for (int k0 = b; k0 < e; k0 += 32) {
+        const int k = k0 + lane;
+        bool take = false;
+        double kv = 0.0;
+        if (k < e) {
+          const double d2 = sq2_exact(g.cx[k] - px, g.cy[k] - py);
+          if (d2 <= r2) {
+            kv = exp(d2 * neg_inv_2b2);
+            take = kv != 0.0;
+          }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, take);
+        if (take) {
+          const uint32_t pos = o + __popc(bal & lt);
+          const uint32_t id = g.id[k];
+          col[pos] = rowof ? static_cast<uint32_t>(rowof[id]) : id;
+          val[pos] = scale * kv;
+        }
+        o += __popc(bal);
       }
-      col[b] = ki;
-      val[b] = kvv;
     }
+    __syncwarp();
+    if (sort_ids && lane == 0)
+      for (uint32_t a = o0 + 1; a < o; ++a) {
+        const uint32_t ki = col[a];
+        const double kvv = val[a];
+        uint32_t b = a;
+        while (b > o0 && col[b - 1] > ki) {
+          col[b] = col[b - 1];
+          val[b] = val[b - 1];
+          --b;
+        }
+        col[b] = ki;
+        val[b] = kvv;
+      }
+    __syncwarp();
+  }
+}
+
+static unsigned warp_grid(size_t m) {
+  return static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>((m + 3) / 4, 64 * 148)));
 }
 
 struct Csr {
@@ -153,8 +184,7 @@ static Csr build_csr(tlg_model* m, const double* x, const double* y, size_t mm, 
   Csr c;
   c.rowp = rowp_in ? rowp_in : ctx->ws<uint32_t>(S_ROWPTR, mm + 1);
   const GridView g = grid_view(m);
-  const unsigned nb = static_cast<unsigned>((mm + 127) / 128);
-  k_csr_count<<<nb, 128, 0, s>>>(g, x, y, mm, m->kc.r2, neg_inv_2b2, c.rowp);
+  k_csr_count_w<<<warp_grid(mm), 128, 0, s>>>(g, x, y, mm, m->kc.r2, neg_inv_2b2, c.rowp);
   TLG_LAUNCHED(ctx);
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.rowp, c.rowp, (int)(mm + 1), s);
@@ -169,7 +199,7 @@ static Csr build_csr(tlg_model* m, const double* x, const double* y, size_t mm, 
   c.nnz = hn;
   c.col = ctx->ws<uint32_t>(S_COLIDX, hn + 1);
   c.val = ctx->ws<double>(S_MTVAL, hn + 1);
-  k_csr_fill<<<nb, 128, 0, s>>>(g, x, y, mm, m->kc.r2, neg_inv_2b2, scale, c.rowp, rowof, c.col,
+  k_csr_fill_w<<<warp_grid(mm), 128, 0, s>>>(g, x, y, mm, m->kc.r2, neg_inv_2b2, scale, c.rowp, rowof, c.col,
                                 c.val, sort_ids ? 1 : 0);
   TLG_LAUNCHED(ctx);
   return c;
@@ -518,8 +548,7 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   uint8_t* bflag = ctx->ws<uint8_t>(S_BLOCKFLAG, nb);
   TLG_CUDA(cudaMemsetAsync(active, 0, nc, s));
   TLG_CUDA(cudaMemsetAsync(bflag, 0, nb, s));
-  k_mark_active<<<(unsigned)std::min<size_t>((mm + 127) / 128, 8 * 148), 128, 0, s>>>(
-      g, x, y, mm, m->kc.r2, active);
+  k_mark_active_w<<<warp_grid(mm), 128, 0, s>>>(g, x, y, mm, m->kc.r2, active);
   TLG_LAUNCHED(ctx);
   k_mark_blocks<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(active, m->d_block_index.p, nc, bflag);
   TLG_LAUNCHED(ctx);
