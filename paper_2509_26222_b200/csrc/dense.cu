@@ -11,6 +11,10 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef TLG_PHASE
+#define TLG_PHASE(k)
+#endif
+
 namespace tlg {
 
 constexpr int TM = 64, TN = 64, TK = 16, SP = 68;  // smem pitch (doubles): conflict-free frags
@@ -659,7 +663,9 @@ __device__ void tile_potrf_inv_b4(double* __restrict__ A, int lda, int kb,
 #pragma unroll
         for (int k = 0; k < 8; ++k) rawX[q * 64 + c0 + k] = x[q][k];
     }
+    TLG_PHASE(0);
     __syncthreads();
+    TLG_PHASE(1);
     if (colown || rowown) {
       // 4x4 Cholesky of D (rows/cols j..j+3) and the inverse of its factor
       double D[4][4];
@@ -745,7 +751,9 @@ __device__ void tile_potrf_inv_b4(double* __restrict__ A, int lda, int kb,
         }
       }
     }
+    TLG_PHASE(2);
     __syncthreads();
+    TLG_PHASE(3);
     // rank-4 update: A -= L_J L_J^T (columns > j+3), X -= L_J X_J (rows > j+3)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -766,6 +774,7 @@ __device__ void tile_potrf_inv_b4(double* __restrict__ A, int lda, int kb,
         }
     }
   }
+  TLG_PHASE(4);
   if (bad) atomicOr(info, 1);
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -775,6 +784,243 @@ __device__ void tile_potrf_inv_b4(double* __restrict__ A, int lda, int kb,
       if (r < kb && c < kb && r >= c) A[r + (size_t)c * lda] = a[i][k];
       linv[r + (size_t)c * NB] = x[i][k];
     }
+  __syncthreads();
+}
+
+// Diagonal tile L L^T = A (64 x 64, 128 threads) and X = L^-1 with one-panel
+// lookahead. Panels are 4 columns wide. In phase J warp 0 brings panel J+1
+// up to date (rank-4 update of its 4 columns and of X rows j+4..j+7) and
+// factors it, while warps 1-3 apply the panel-J rank-4 update to the rest of
+// the trailing matrix and of X. One barrier per phase; the critical path is
+// warp 0's small panel chain instead of panel + whole trailing update.
+// Works in shared memory: A column-major (pitch kLaP), X row-major (pitch kLaP),
+// PL[2][64][4] = L rows of the current panel, PX[2][4][64] = final X rows.
+constexpr int kLaP = 68;
+constexpr int kDiagSmemDoubles = 2 * 64 * kLaP + 2 * 64 * 4 + 2 * 4 * 64;
+
+__device__ __forceinline__ void la_factor4(const double (&D)[4][4], double (&L)[4][4],
+                                           double (&Li)[4][4], bool& bad) {
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    double d = D[p][p];
+#pragma unroll
+    for (int k = 0; k < p; ++k) d = fma(-L[p][k], L[p][k], d);
+    bad |= !(d > 0.0) || !isfinite(d);
+    const double iv = rsqrt(d);
+    L[p][p] = d * iv;
+    Li[p][p] = iv;
+#pragma unroll
+    for (int r = p + 1; r < 4; ++r) {
+      double s = D[r][p];
+#pragma unroll
+      for (int k = 0; k < p; ++k) s = fma(-L[r][k], L[p][k], s);
+      L[r][p] = s * iv;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int r = c + 1; r < 4; ++r) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = c; k < r; ++k) s = fma(L[r][k], Li[k][c], s);
+      Li[r][c] = -Li[r][r] * s;
+    }
+}
+
+// Warp 0: panel jn (columns jn..jn+3) — update with the previous panel (when
+// jn > 0), factor, and publish L rows (PLn) and final X rows (PXn).
+__device__ __forceinline__ void la_panel(double* __restrict__ a, double* __restrict__ x,
+                                         const double* __restrict__ PLo,
+                                         const double* __restrict__ PXo, double* __restrict__ PLn,
+                                         double* __restrict__ PXn, int jn, bool& bad) {
+  const int l = threadIdx.x & 31;
+  const int j = jn - 4;
+  double ar[2][4], xr[2][4];
+  // rank-4 update of A(rows >= jn, cols jn..jn+3) and X(rows jn..jn+3, cols < jn)
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = jn + l + 32 * h;
+    if (r < 64) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) ar[h][p] = a[(jn + p) * kLaP + r];
+      if (jn > 0) {
+        double lr[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) lr[q] = PLo[r * 4 + q];
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) ar[h][p] = fma(-lr[q], PLo[(jn + p) * 4 + q], ar[h][p]);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) a[(jn + p) * kLaP + r] = ar[h][p];
+      }
+    }
+    const int c = l + 32 * h;
+    if (c < jn) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) xr[h][p] = x[(jn + p) * kLaP + c];
+      if (j >= 0 && c <= j + 3) {
+        double xo[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xo[q] = PXo[q * 64 + c];
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) xr[h][p] = fma(-PLo[(jn + p) * 4 + q], xo[q], xr[h][p]);
+      }
+    }
+  }
+  __syncwarp();
+  double D[4][4], L[4][4], Li[4][4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q <= p; ++q) D[p][q] = a[(jn + q) * kLaP + jn + p];
+  la_factor4(D, L, Li, bad);
+  // L rows: r in the diagonal block take L; rows below: a_r Li^T
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = jn + l + 32 * h;
+    if (r < 64) {
+      double v[4];
+      if (r >= jn + 4) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double s = 0.0;
+#pragma unroll
+          for (int p = 0; p <= q; ++p) s = fma(ar[h][p], Li[q][p], s);
+          v[q] = s;
+        }
+      } else {
+        const int pr = r - jn;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double s = 0.0;
+#pragma unroll
+          for (int p = 0; p < 4; ++p)
+            if (p == pr) s = q <= p ? L[p][q] : 0.0;
+          v[q] = s;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[(jn + q) * kLaP + r] = v[q];
+        PLn[r * 4 + q] = v[q];
+      }
+    }
+  }
+  // final X rows jn..jn+3: Li X(rows), columns < jn from the update, jn.. = I
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = l + 32 * h;
+    double xi[4];
+    if (c < jn) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) xi[p] = xr[h][p];
+    } else {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) xi[p] = (c == jn + p) ? 1.0 : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int p = 0; p <= q; ++p) s = fma(Li[q][p], xi[p], s);
+      if (c > jn + 3) s = 0.0;
+      x[(jn + q) * kLaP + c] = s;
+      PXn[q * 64 + c] = s;
+    }
+  }
+}
+
+__device__ void tile_potrf_inv_la(double* __restrict__ A, int lda, int kb,
+                                  double* __restrict__ linv, int* __restrict__ info,
+                                  double* sh) {
+  const int t = threadIdx.x;
+  double* a = sh;                      // [64 cols][kLaP]
+  double* x = sh + 64 * kLaP;          // [64 rows][kLaP]
+  double* PL = sh + 2 * 64 * kLaP;     // [2][64][4]
+  double* PX = PL + 2 * 64 * 4;        // [2][4][64]
+  for (int e = t; e < 64 * 64; e += 128) {
+    const int r = e & 63, c = e >> 6;
+    a[c * kLaP + r] = (r < kb && c < kb) ? (r >= c ? A[r + (size_t)c * lda] : 0.0)
+                                         : (r == c ? 1.0 : 0.0);
+    x[c * kLaP + r] = (r == c) ? 1.0 : 0.0;  // symmetric init, x row-major
+  }
+  __syncthreads();
+  bool bad = false;
+  if (t < 32) la_panel(a, x, PL, PX, PL, PX, 0, bad);
+  __syncthreads();
+#pragma unroll 1
+  for (int J = 0; J < 15; ++J) {
+    const int j = 4 * J;
+    const double* PLo = PL + (J & 1) * 256;
+    const double* PXo = PX + (J & 1) * 256;
+    if (t < 32) {
+      la_panel(a, x, PLo, PXo, PL + ((J + 1) & 1) * 256, PX + ((J + 1) & 1) * 256, j + 4, bad);
+    } else {
+      // trailing A blocks: cols >= j+8, rows >= col (4x4 blocks, cb <= rb)
+      const int cb0 = J + 2;
+      const int nc = 16 - cb0;
+      const int nA = nc * (nc + 1) / 2;
+      const int nX = nc * (J + 1);
+      for (int e = t - 32; e < nA + nX; e += 96) {
+        if (e < nA) {
+          int cb = 0, rem = e;
+          while (rem >= nc - cb) {
+            rem -= nc - cb;
+            ++cb;
+          }
+          const int c0 = (cb0 + cb) * 4, r0 = c0 + rem * 4;
+          double lr[4][4], lc[4][4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              lr[i][q] = PLo[(r0 + i) * 4 + q];
+              lc[i][q] = PLo[(c0 + i) * 4 + q];
+            }
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              double v = a[(c0 + k) * kLaP + r0 + i];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) v = fma(-lr[i][q], lc[k][q], v);
+              a[(c0 + k) * kLaP + r0 + i] = v;
+            }
+        } else {
+          const int f = e - nA;
+          const int r0 = (cb0 + f / (J + 1)) * 4, c0 = (f % (J + 1)) * 4;
+          double lr[4][4], xo[4][4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              lr[i][q] = PLo[(r0 + i) * 4 + q];
+              xo[q][i] = PXo[q * 64 + c0 + i];
+            }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              double v = x[(r0 + i) * kLaP + c0 + k];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) v = fma(-lr[i][q], xo[q][k], v);
+              x[(r0 + i) * kLaP + c0 + k] = v;
+            }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (t < 32 && bad && t == 0) atomicOr(info, 1);
+  for (int e = t; e < 64 * 64; e += 128) {
+    const int r = e & 63, c = e >> 6;
+    if (r < kb && c < kb && r >= c) A[r + (size_t)c * lda] = a[c * kLaP + r];
+    linv[r + (size_t)c * NB] = (r >= c) ? x[r * kLaP + c] : 0.0;
+  }
   __syncthreads();
 }
 
@@ -843,6 +1089,10 @@ __device__ void tile_potrf_inv(double* __restrict__ A, int lda, int kb, double* 
   __syncthreads();
 }
 
+#ifndef TLG_DIAG_TILE
+#define TLG_DIAG_TILE tile_potrf_inv_la
+#endif
+
 __global__ void __launch_bounds__(128) k_potrf_coop(double* __restrict__ A, int n, int lda,
                                                     double* __restrict__ linv,
                                                     int* __restrict__ info) {
@@ -854,7 +1104,7 @@ __global__ void __launch_bounds__(128) k_potrf_coop(double* __restrict__ A, int 
   for (int k = 0; k < nt; ++k) {
     const int k0 = k * NB, kb = min(NB, n - k0);
     if (blockIdx.x == 0)
-      tile_potrf_inv_b4(A + k0 + (size_t)k0 * lda, lda, kb, linv + (size_t)k * NB * NB, info, dyn);
+      TLG_DIAG_TILE(A + k0 + (size_t)k0 * lda, lda, kb, linv + (size_t)k * NB * NB, info, dyn);
     grid.sync();
     // panel: L_ik = A_ik L_kk^-T (in place; one CTA owns a tile)
     for (int i = k + 1 + blockIdx.x; i < nt; i += gridDim.x) {
@@ -922,7 +1172,7 @@ void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info) {
   const int nt = (n + NB - 1) / NB;
   double* linv = ctx->ws<double>(S_LINV, static_cast<size_t>(nt) * NB * NB);
   ctx->linv_owner = A;
-  const size_t smem = sizeof(double) * (2 * 64 * 65 + 64 + 256);
+  const size_t smem = sizeof(double) * std::max(kDiagSmemDoubles, 2 * 64 * 65 + 64 + 256);
   static bool attr = false;
   if (!attr) {
     TLG_CUDA(cudaFuncSetAttribute(k_potrf_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -942,7 +1192,7 @@ void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info) {
 __global__ void __launch_bounds__(128) k_diag_tile_only(double* A, int lda, double* linv, int* info,
                                                         int reps) {
   extern __shared__ double shd[];
-  for (int r = 0; r < reps; ++r) tile_potrf_inv_b4(A, lda, 64, linv, info, shd);
+  for (int r = 0; r < reps; ++r) TLG_DIAG_TILE(A, lda, 64, linv, info, shd);
 }
 
 __global__ void __launch_bounds__(128) k_gridsync_only(int reps) {
@@ -983,7 +1233,7 @@ double dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps) {
     else if (op == 1) trsm_left_lower(ctx, A.p, n, n, B.p, nrhs, n, 0);
     else if (op == 2) gemm(ctx, GemmDesc{n, nrhs, n, A.p, n, 0, A.p, n, 1, B.p, n, 1.0, 0.0, 0});
     else if (op == 3) {
-      const int sm = sizeof(double) * (2 * 64 * 65 + 64 + 256);
+      const int sm = sizeof(double) * std::max(kDiagSmemDoubles, 2 * 64 * 65 + 64 + 256);
       TLG_CUDA(cudaFuncSetAttribute(k_diag_tile_only, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       k_diag_tile_only<<<1, 128, sm, s>>>(A.p, n, B.p, info.p, nrhs);
     }
