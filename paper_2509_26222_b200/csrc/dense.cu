@@ -28,7 +28,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // One right-hand side (N == 1): 64 rows of y = alpha op(A) b + beta y with
 // plain FMAs (coalesced along the contiguous dimension of A). All reads of b
 // finish before y is written, so b may alias y (in-place triangular steps).
-__device__ __forceinline__ void gemv_tile(const GemmDesc& d, int m0) {
+__device__ __forceinline__ void gemv_tile(const GemmDesc& d, int m0, int K) {
   __shared__ double red[128];
   const int t = threadIdx.x;
   const int mb = min(TM, d.M - m0);
@@ -39,11 +39,11 @@ __device__ __forceinline__ void gemv_tile(const GemmDesc& d, int m0) {
     if (i < mb) {
       const double* a = d.A + m0 + i;
       int k = h;
-      for (; k + 2 < d.K; k += 4) {
+      for (; k + 2 < K; k += 4) {
         s0 = fma(a[(size_t)k * d.lda], bval(k), s0);
         s1 = fma(a[(size_t)(k + 2) * d.lda], bval(k + 2), s1);
       }
-      for (; k < d.K; k += 2) s0 = fma(a[(size_t)k * d.lda], bval(k), s0);
+      for (; k < K; k += 2) s0 = fma(a[(size_t)k * d.lda], bval(k), s0);
     }
     red[t] = s0 + s1;
   } else {
@@ -51,7 +51,7 @@ __device__ __forceinline__ void gemv_tile(const GemmDesc& d, int m0) {
     for (int i = w; i < mb; i += 4) {
       const double* a = d.A + (size_t)(m0 + i) * d.lda;
       double s = 0.0;
-      for (int k = lane; k < d.K; k += 32) s = fma(a[k], bval(k), s);
+      for (int k = lane; k < K; k += 32) s = fma(a[k], bval(k), s);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) red[i] = s;
@@ -70,8 +70,10 @@ __device__ __forceinline__ void gemm_tile(const GemmDesc& d, int tile_m, int til
   const int m0 = tile_m * TM, n0 = tile_n * TN;
   if (m0 >= d.M || n0 >= d.N) return;
   if (d.uplo == 1 && m0 + TM <= n0) return;  // strictly above the diagonal
+  // uplo 2: A lower triangular (not transposed) -> its columns >= m0 + TM are 0
+  const int K = (d.uplo == 2) ? min(d.K, m0 + TM) : d.K;
   if (d.N == 1) {
-    gemv_tile(d, m0);
+    gemv_tile(d, m0, K);
     return;
   }
   __shared__ double As[TK][SP];
@@ -93,14 +95,14 @@ __device__ __forceinline__ void gemm_tile(const GemmDesc& d, int tile_m, int til
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
         const int k = (t >> 6) + 2 * s, gi = m0 + i, gk = k0 + k;
-        pa[s] = (gi < d.M && gk < d.K) ? d.A[gi + (size_t)gk * d.lda] : 0.0;
+        pa[s] = (gi < d.M && gk < K) ? d.A[gi + (size_t)gk * d.lda] : 0.0;
       }
     } else {
       const int k = t & 15;
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
         const int i = (t >> 4) + 8 * s, gi = m0 + i, gk = k0 + k;
-        pa[s] = (gi < d.M && gk < d.K) ? d.A[gk + (size_t)gi * d.lda] : 0.0;
+        pa[s] = (gi < d.M && gk < K) ? d.A[gk + (size_t)gi * d.lda] : 0.0;
       }
     }
     if (!d.tb) {
@@ -108,19 +110,19 @@ __device__ __forceinline__ void gemm_tile(const GemmDesc& d, int tile_m, int til
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
         const int j = (t >> 4) + 8 * s, gj = n0 + j, gk = k0 + k;
-        pb[s] = (gj < d.N && gk < d.K) ? d.B[gk + (size_t)gj * d.ldb] : 0.0;
+        pb[s] = (gj < d.N && gk < K) ? d.B[gk + (size_t)gj * d.ldb] : 0.0;
       }
     } else {
       const int j = t & 63;
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
         const int k = (t >> 6) + 2 * s, gj = n0 + j, gk = k0 + k;
-        pb[s] = (gj < d.N && gk < d.K) ? d.B[gj + (size_t)gk * d.ldb] : 0.0;
+        pb[s] = (gj < d.N && gk < K) ? d.B[gj + (size_t)gk * d.ldb] : 0.0;
       }
     }
   };
-  if (d.K > 0) fetch(0);
-  for (int k0 = 0; k0 < d.K; k0 += TK) {
+  if (K > 0) fetch(0);
+  for (int k0 = 0; k0 < K; k0 += TK) {
     // stage chunk: op(A)(m0 + i, k0 + k) -> As[k][i], op(B)(k0 + k, n0 + j) -> Bs[k][j]
     if (!d.ta) {
 #pragma unroll
@@ -137,7 +139,7 @@ __device__ __forceinline__ void gemm_tile(const GemmDesc& d, int tile_m, int til
       for (int s = 0; s < 8; ++s) Bs[(t >> 6) + 2 * s][t & 63] = pb[s];
     }
     __syncthreads();
-    if (k0 + TK < d.K) fetch(k0 + TK);
+    if (k0 + TK < K) fetch(k0 + TK);
 #pragma unroll
     for (int kk = 0; kk < TK; kk += 4) {
       double a[4], b[4];
@@ -793,10 +795,20 @@ __device__ void tile_potrf_inv_b4(double* __restrict__ A, int lda, int kb,
 // factors it, while warps 1-3 apply the panel-J rank-4 update to the rest of
 // the trailing matrix and of X. One barrier per phase; the critical path is
 // warp 0's small panel chain instead of panel + whole trailing update.
-// Works in shared memory: A column-major (pitch kLaP), X row-major (pitch kLaP),
-// PL[2][64][4] = L rows of the current panel, PX[2][4][64] = final X rows.
-constexpr int kLaP = 68;
-constexpr int kDiagSmemDoubles = 2 * 64 * kLaP + 2 * 64 * 4 + 2 * 4 * 64;
+// Shared memory: A and X column-major with odd pitch kLaP (lanes may walk rows
+// or columns without bank conflicts); the published panel is kept twice —
+// PLr[q][64] (lane = row reads) and PLc[64][4] (broadcast reads) — and so are
+// the final X rows, PXr[q][64] and PXc[64][4]; each is double-buffered by phase.
+constexpr int kLaP = 65;
+constexpr int kLaPanel = 4 * 64;  // doubles per published panel copy
+constexpr int kDiagSmemDoubles = 2 * 64 * kLaP + 2 + 8 * kLaPanel;
+
+struct LaBuf {
+  const double* PLr;
+  const double* PLc;
+  const double* PXr;
+  const double* PXc;
+};
 
 __device__ __forceinline__ void la_factor4(const double (&D)[4][4], double (&L)[4][4],
                                            double (&Li)[4][4], bool& bad) {
@@ -829,15 +841,25 @@ __device__ __forceinline__ void la_factor4(const double (&D)[4][4], double (&L)[
 }
 
 // Warp 0: panel jn (columns jn..jn+3) — update with the previous panel (when
-// jn > 0), factor, and publish L rows (PLn) and final X rows (PXn).
+// jn > 0), factor, and publish L rows and final X rows into `out`.
 __device__ __forceinline__ void la_panel(double* __restrict__ a, double* __restrict__ x,
-                                         const double* __restrict__ PLo,
-                                         const double* __restrict__ PXo, double* __restrict__ PLn,
-                                         double* __restrict__ PXn, int jn, bool& bad) {
+                                         const LaBuf& o, double* __restrict__ PLr,
+                                         double* __restrict__ PLc, double* __restrict__ PXr,
+                                         double* __restrict__ PXc, int jn, bool& bad) {
   const int l = threadIdx.x & 31;
-  const int j = jn - 4;
   double ar[2][4], xr[2][4];
-  // rank-4 update of A(rows >= jn, cols jn..jn+3) and X(rows jn..jn+3, cols < jn)
+  double lp[4][4];  // L rows jn..jn+3 of the previous panel (broadcast)
+  if (jn > 0) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const double2 u = *reinterpret_cast<const double2*>(o.PLc + (jn + p) * 4);
+      const double2 v = *reinterpret_cast<const double2*>(o.PLc + (jn + p) * 4 + 2);
+      lp[p][0] = u.x;
+      lp[p][1] = u.y;
+      lp[p][2] = v.x;
+      lp[p][3] = v.y;
+    }
+  }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int r = jn + l + 32 * h;
@@ -847,37 +869,39 @@ __device__ __forceinline__ void la_panel(double* __restrict__ a, double* __restr
       if (jn > 0) {
         double lr[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) lr[q] = PLo[r * 4 + q];
+        for (int q = 0; q < 4; ++q) lr[q] = o.PLr[q * 64 + r];
 #pragma unroll
         for (int p = 0; p < 4; ++p)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) ar[h][p] = fma(-lr[q], PLo[(jn + p) * 4 + q], ar[h][p]);
+          for (int q = 0; q < 4; ++q) ar[h][p] = fma(-lr[q], lp[p][q], ar[h][p]);
+        if (r < jn + 4)
 #pragma unroll
-        for (int p = 0; p < 4; ++p) a[(jn + p) * kLaP + r] = ar[h][p];
+          for (int p = 0; p < 4; ++p) a[(jn + p) * kLaP + r] = ar[h][p];
       }
     }
     const int c = l + 32 * h;
     if (c < jn) {
 #pragma unroll
-      for (int p = 0; p < 4; ++p) xr[h][p] = x[(jn + p) * kLaP + c];
-      if (j >= 0 && c <= j + 3) {
-        double xo[4];
+      for (int p = 0; p < 4; ++p) xr[h][p] = x[c * kLaP + jn + p];
+      double xo[4];  // X_fin rows of the previous panel: nonzero in columns < jn
 #pragma unroll
-        for (int q = 0; q < 4; ++q) xo[q] = PXo[q * 64 + c];
+      for (int q = 0; q < 4; ++q) xo[q] = o.PXr[q * 64 + c];
 #pragma unroll
-        for (int p = 0; p < 4; ++p)
+      for (int p = 0; p < 4; ++p)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) xr[h][p] = fma(-PLo[(jn + p) * 4 + q], xo[q], xr[h][p]);
-      }
+        for (int q = 0; q < 4; ++q) xr[h][p] = fma(-lp[p][q], xo[q], xr[h][p]);
     }
   }
+  TLG_PHASE(1);
   __syncwarp();
   double D[4][4], L[4][4], Li[4][4];
 #pragma unroll
   for (int p = 0; p < 4; ++p)
 #pragma unroll
     for (int q = 0; q <= p; ++q) D[p][q] = a[(jn + q) * kLaP + jn + p];
+  TLG_PHASE(2);
   la_factor4(D, L, Li, bad);
+  TLG_PHASE(3);
   // L rows: r in the diagonal block take L; rows below: a_r Li^T
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -906,11 +930,14 @@ __device__ __forceinline__ void la_panel(double* __restrict__ a, double* __restr
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         a[(jn + q) * kLaP + r] = v[q];
-        PLn[r * 4 + q] = v[q];
+        PLr[q * 64 + r] = v[q];
       }
+      *reinterpret_cast<double2*>(PLc + r * 4) = make_double2(v[0], v[1]);
+      *reinterpret_cast<double2*>(PLc + r * 4 + 2) = make_double2(v[2], v[3]);
     }
   }
-  // final X rows jn..jn+3: Li X(rows), columns < jn from the update, jn.. = I
+  TLG_PHASE(4);
+  // final X rows jn..jn+3: Li X(rows); columns < jn from the update, jn.. = I
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int c = l + 32 * h;
@@ -922,15 +949,18 @@ __device__ __forceinline__ void la_panel(double* __restrict__ a, double* __restr
 #pragma unroll
       for (int p = 0; p < 4; ++p) xi[p] = (c == jn + p) ? 1.0 : 0.0;
     }
+    double v[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       double s = 0.0;
 #pragma unroll
       for (int p = 0; p <= q; ++p) s = fma(Li[q][p], xi[p], s);
-      if (c > jn + 3) s = 0.0;
-      x[(jn + q) * kLaP + c] = s;
-      PXn[q * 64 + c] = s;
+      v[q] = s;
+      if (c <= jn + 3) x[c * kLaP + jn + q] = s;
+      PXr[q * 64 + c] = s;
     }
+    *reinterpret_cast<double2*>(PXc + c * 4) = make_double2(v[0], v[1]);
+    *reinterpret_cast<double2*>(PXc + c * 4 + 2) = make_double2(v[2], v[3]);
   }
 }
 
@@ -938,88 +968,75 @@ __device__ void tile_potrf_inv_la(double* __restrict__ A, int lda, int kb,
                                   double* __restrict__ linv, int* __restrict__ info,
                                   double* sh) {
   const int t = threadIdx.x;
-  double* a = sh;                      // [64 cols][kLaP]
-  double* x = sh + 64 * kLaP;          // [64 rows][kLaP]
-  double* PL = sh + 2 * 64 * kLaP;     // [2][64][4]
-  double* PX = PL + 2 * 64 * 4;        // [2][4][64]
+  double* a = sh;                  // A, column-major [64][kLaP]
+  double* x = sh + 64 * kLaP;      // X, column-major [64][kLaP]
+  double* pb = sh + 2 * 64 * kLaP + 2;  // 16-byte aligned panel buffers
+  auto buf = [&](int which, int parity) { return pb + (which * 2 + parity) * kLaPanel; };
   for (int e = t; e < 64 * 64; e += 128) {
     const int r = e & 63, c = e >> 6;
     a[c * kLaP + r] = (r < kb && c < kb) ? (r >= c ? A[r + (size_t)c * lda] : 0.0)
                                          : (r == c ? 1.0 : 0.0);
-    x[c * kLaP + r] = (r == c) ? 1.0 : 0.0;  // symmetric init, x row-major
+    x[c * kLaP + r] = (r == c) ? 1.0 : 0.0;
   }
   __syncthreads();
   bool bad = false;
-  if (t < 32) la_panel(a, x, PL, PX, PL, PX, 0, bad);
+  if (t < 32) {
+    const LaBuf none{nullptr, nullptr, nullptr, nullptr};
+    la_panel(a, x, none, buf(0, 0), buf(1, 0), buf(2, 0), buf(3, 0), 0, bad);
+  }
   __syncthreads();
 #pragma unroll 1
   for (int J = 0; J < 15; ++J) {
-    const int j = 4 * J;
-    const double* PLo = PL + (J & 1) * 256;
-    const double* PXo = PX + (J & 1) * 256;
+    TLG_PHASE(0);
+    const int j = 4 * J, par = J & 1;
+    const LaBuf o{buf(0, par), buf(1, par), buf(2, par), buf(3, par)};
     if (t < 32) {
-      la_panel(a, x, PLo, PXo, PL + ((J + 1) & 1) * 256, PX + ((J + 1) & 1) * 256, j + 4, bad);
+      la_panel(a, x, o, buf(0, par ^ 1), buf(1, par ^ 1), buf(2, par ^ 1), buf(3, par ^ 1), j + 4,
+               bad);
+      TLG_PHASE(6);
     } else {
-      // trailing A blocks: cols >= j+8, rows >= col (4x4 blocks, cb <= rb)
-      const int cb0 = J + 2;
-      const int nc = 16 - cb0;
-      const int nA = nc * (nc + 1) / 2;
-      const int nX = nc * (J + 1);
-      for (int e = t - 32; e < nA + nX; e += 96) {
-        if (e < nA) {
-          int cb = 0, rem = e;
-          while (rem >= nc - cb) {
-            rem -= nc - cb;
-            ++cb;
-          }
-          const int c0 = (cb0 + cb) * 4, r0 = c0 + rem * 4;
-          double lr[4][4], lc[4][4];
+      // Items: 4-column groups x 32-row strips, lane = row.
+      //   A: column groups cg >= J+2 (rows >= 4cg);   X: column groups <= J (rows >= j+8).
+      const int lane = t & 31, w = (t >> 5) - 1;
+      const int cgA = J + 2;
+      const int nA = (16 - cgA) * 2;
+      const int nX = (J + 1) * 2;
+      for (int e = w; e < nA + nX; e += 3) {
+        const bool isA = e < nA;
+        const int f = isA ? e : e - nA;
+        const int cg = isA ? cgA + (f >> 1) : (f >> 1);
+        const int strip = f & 1;
+        const int r = 32 * strip + lane;
+        const int c0 = 4 * cg;
+        const int rmin = isA ? c0 : j + 8;
+        if (32 * strip + 31 < rmin) continue;  // whole strip above the region
+        if (r < rmin) continue;
+        double lr[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+        for (int q = 0; q < 4; ++q) lr[q] = o.PLr[q * 64 + r];
+        double* dst = isA ? a : x;
+        const double* src = isA ? o.PLc : o.PXc;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              lr[i][q] = PLo[(r0 + i) * 4 + q];
-              lc[i][q] = PLo[(c0 + i) * 4 + q];
-            }
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              double v = a[(c0 + k) * kLaP + r0 + i];
-#pragma unroll
-              for (int q = 0; q < 4; ++q) v = fma(-lr[i][q], lc[k][q], v);
-              a[(c0 + k) * kLaP + r0 + i] = v;
-            }
-        } else {
-          const int f = e - nA;
-          const int r0 = (cb0 + f / (J + 1)) * 4, c0 = (f % (J + 1)) * 4;
-          double lr[4][4], xo[4][4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              lr[i][q] = PLo[(r0 + i) * 4 + q];
-              xo[q][i] = PXo[q * 64 + c0 + i];
-            }
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              double v = x[(r0 + i) * kLaP + c0 + k];
-#pragma unroll
-              for (int q = 0; q < 4; ++q) v = fma(-lr[i][q], xo[q][k], v);
-              x[(r0 + i) * kLaP + c0 + k] = v;
-            }
+        for (int k = 0; k < 4; ++k) {
+          const double2 u = *reinterpret_cast<const double2*>(src + (c0 + k) * 4);
+          const double2 v = *reinterpret_cast<const double2*>(src + (c0 + k) * 4 + 2);
+          double val = dst[(c0 + k) * kLaP + r];
+          val = fma(-lr[0], u.x, val);
+          val = fma(-lr[1], u.y, val);
+          val = fma(-lr[2], v.x, val);
+          val = fma(-lr[3], v.y, val);
+          dst[(c0 + k) * kLaP + r] = val;
         }
       }
+      TLG_PHASE(6);
     }
     __syncthreads();
   }
-  if (t < 32 && bad && t == 0) atomicOr(info, 1);
+  if (t == 0 && bad) atomicOr(info, 1);
   for (int e = t; e < 64 * 64; e += 128) {
     const int r = e & 63, c = e >> 6;
     if (r < kb && c < kb && r >= c) A[r + (size_t)c * lda] = a[c * kLaP + r];
-    linv[r + (size_t)c * NB] = (r >= c) ? x[r * kLaP + c] : 0.0;
+    linv[r + (size_t)c * NB] = (r >= c) ? x[c * kLaP + r] : 0.0;
   }
   __syncthreads();
 }
@@ -1095,41 +1112,72 @@ __device__ void tile_potrf_inv(double* __restrict__ A, int lda, int kb, double* 
 
 __global__ void __launch_bounds__(128) k_potrf_coop(double* __restrict__ A, int n, int lda,
                                                     double* __restrict__ linv,
-                                                    int* __restrict__ info) {
+                                                    int* __restrict__ info, double* __restrict__ X,
+                                                    int ldx) {
   extern __shared__ double dyn[];
-  double(*a)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dyn);
-  double* dinv = dyn + NB * (NB + 1);
   cg::grid_group grid = cg::this_grid();
   const int nt = (n + NB - 1) / NB;
+  if (X) {
+    // X <- I (then X = L^-1 is built alongside the factorisation)
+    const size_t total = (size_t)n * n;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
+         e += (size_t)gridDim.x * blockDim.x) {
+      const int r = static_cast<int>(e % n), c = static_cast<int>(e / n);
+      X[r + (size_t)c * ldx] = (r == c) ? 1.0 : 0.0;
+    }
+    grid.sync();
+  }
   for (int k = 0; k < nt; ++k) {
     const int k0 = k * NB, kb = min(NB, n - k0);
+    const double* lk = linv + (size_t)k * NB * NB;
     if (blockIdx.x == 0)
       TLG_DIAG_TILE(A + k0 + (size_t)k0 * lda, lda, kb, linv + (size_t)k * NB * NB, info, dyn);
     grid.sync();
-    // panel: L_ik = A_ik L_kk^-T (in place; one CTA owns a tile)
-    for (int i = k + 1 + blockIdx.x; i < nt; i += gridDim.x) {
-      const int i0 = i * NB, ib = min(NB, n - i0);
-      double* P = A + i0 + (size_t)k0 * lda;
-      gemm_tile(GemmDesc{ib, kb, kb, P, lda, 0, linv + (size_t)k * NB * NB, NB, 1, P, lda, 1.0,
-                         0.0, 0},
-                0, 0);
+    // panel: L_ik = A_ik L_kk^-T (in place; one CTA owns a tile); with X also
+    // finalise block row k of L^-1: X_kj = Linv_kk X_kj, j <= k
+    const int npanel = nt - k - 1, nfin = X ? k + 1 : 0;
+    for (int e = blockIdx.x; e < npanel + nfin; e += gridDim.x) {
+      if (e < npanel) {
+        const int i = k + 1 + e;
+        const int i0 = i * NB, ib = min(NB, n - i0);
+        double* P = A + i0 + (size_t)k0 * lda;
+        gemm_tile(GemmDesc{ib, kb, kb, P, lda, 0, lk, NB, 1, P, lda, 1.0, 0.0, 0}, 0, 0);
+      } else {
+        const int j = e - npanel;
+        const int j0 = j * NB, jb = min(NB, n - j0);
+        double* T = X + k0 + (size_t)j0 * ldx;
+        gemm_tile(GemmDesc{kb, jb, kb, lk, NB, 0, T, ldx, 0, T, ldx, 1.0, 0.0, 0}, 0, 0);
+      }
       __syncthreads();
     }
     grid.sync();
-    // trailing update of the lower tiles: A_ij -= L_ik L_jk^T, k < j <= i
+    // trailing update of the lower tiles: A_ij -= L_ik L_jk^T, k < j <= i;
+    // with X: X_ij -= L_ik X_kj, i > k >= j
     const int nr = nt - k - 1;
     const int ntiles = nr * (nr + 1) / 2;
-    for (int e = blockIdx.x; e < ntiles; e += gridDim.x) {
-      int r = 0, rem = e;
-      while (rem > r) {
-        rem -= r + 1;
-        ++r;
+    const int nx = X ? nr * (k + 1) : 0;
+    for (int e = blockIdx.x; e < ntiles + nx; e += gridDim.x) {
+      if (e < ntiles) {
+        int r = 0, rem = e;
+        while (rem > r) {
+          rem -= r + 1;
+          ++r;
+        }
+        const int i = k + 1 + r, j = k + 1 + rem;
+        const int i0 = i * NB, j0 = j * NB, ib = min(NB, n - i0), jb = min(NB, n - j0);
+        gemm_tile(GemmDesc{ib, jb, kb, A + i0 + (size_t)k0 * lda, lda, 0,
+                           A + j0 + (size_t)k0 * lda, lda, 1, A + i0 + (size_t)j0 * lda, lda, -1.0,
+                           1.0, 0},
+                  0, 0);
+      } else {
+        const int f = e - ntiles;
+        const int i = k + 1 + f / (k + 1), j = f % (k + 1);
+        const int i0 = i * NB, j0 = j * NB, ib = min(NB, n - i0), jb = min(NB, n - j0);
+        gemm_tile(GemmDesc{ib, jb, kb, A + i0 + (size_t)k0 * lda, lda, 0,
+                           X + k0 + (size_t)j0 * ldx, ldx, 0, X + i0 + (size_t)j0 * ldx, ldx, -1.0,
+                           1.0, 0},
+                  0, 0);
       }
-      const int i = k + 1 + r, j = k + 1 + rem;
-      const int i0 = i * NB, j0 = j * NB, ib = min(NB, n - i0), jb = min(NB, n - j0);
-      gemm_tile(GemmDesc{ib, jb, kb, A + i0 + (size_t)k0 * lda, lda, 0, A + j0 + (size_t)k0 * lda,
-                         lda, 1, A + i0 + (size_t)j0 * lda, lda, -1.0, 1.0, 0},
-                0, 0);
       __syncthreads();
     }
     grid.sync();
@@ -1167,7 +1215,7 @@ __global__ void __launch_bounds__(128) k_trsm_tiles(const double* __restrict__ L
   }
 }
 
-void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info) {
+void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X, int ldx) {
   if (n <= 0) return;
   const int nt = (n + NB - 1) / NB;
   double* linv = ctx->ws<double>(S_LINV, static_cast<size_t>(nt) * NB * NB);
@@ -1181,9 +1229,14 @@ void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info) {
   }
   int per_sm = 0;
   TLG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_potrf_coop, 128, smem));
-  const int maxtiles = std::max(nt - 1, (nt - 1) * nt / 2);
+  int maxtiles = std::max(nt - 1, (nt - 1) * nt / 2);
+  if (X) {
+    for (int k = 0; k < nt; ++k)
+      maxtiles = std::max(maxtiles, (nt - k - 1) * (nt - k) / 2 + (nt - k - 1) * (k + 1));
+    maxtiles = std::max(maxtiles, nt);
+  }
   const int grid = std::max(1, std::min(maxtiles, ctx->num_sms * std::max(per_sm, 1)));
-  void* args[] = {&A, &n, &lda, &linv, &info};
+  void* args[] = {&A, &n, &lda, &linv, &info, &X, &ldx};
   TLG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_potrf_coop), dim3(grid),
                                        dim3(128), args, smem, ctx->stream));
   ++ctx->launches;

@@ -6,7 +6,8 @@
 namespace tlg {
 
 // C = alpha * op(A) op(B) + beta * C   (op = transpose when t* != 0)
-// uplo = 1 skips CTA tiles strictly above the diagonal (SYRK-style updates).
+// uplo = 1 skips CTA tiles strictly above the diagonal (SYRK-style updates);
+// uplo = 2 declares A lower triangular (ta = 0): row tile m0 reads K < m0 + 64.
 struct GemmDesc {
   int M, N, K;
   const double* A;
@@ -25,7 +26,10 @@ void gemm_grouped(tlg_ctx* ctx, const GemmDesc* d_descs, int count, int max_m, i
 
 // In-place lower Cholesky (A = L L^T) of the n x n matrix at A (lda).
 // `info` (device int) is set non-zero when a pivot is not positive/finite.
-void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info);
+// With X != nullptr the full inverse factor X = L^-1 (n x n, ldx, zero above
+// the diagonal) is built in the same launch, so later solves are GEMMs.
+void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X = nullptr,
+                 int ldx = 0);
 // B <- L^-1 B (trans = 0) or B <- L^-T B (trans = 1); L lower n x n, B n x nrhs.
 void trsm_left_lower(tlg_ctx* ctx, const double* L, int n, int ldl, double* B, int nrhs,
                      int ldb, int trans);

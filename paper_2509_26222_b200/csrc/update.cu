@@ -384,17 +384,16 @@ __global__ void k_diag_minmax(const double* __restrict__ L, int n, int ld, doubl
   }
 }
 
-// SPD inverse of the n x n matrix src (lds) into dst (ldd) via Cholesky.
+// SPD inverse of the n x n matrix src (lds) into dst (ldd) via Cholesky:
+// the factorisation also yields X = L^-1, and A^-1 = X^T X is one GEMM.
 static bool spd_inverse(tlg_ctx* ctx, const double* src, int lds, int n, double* dst, int ldd) {
   double* T = ctx->ws<double>(S_WORK2, static_cast<size_t>(n) * n);
+  double* X = ctx->ws<double>(S_XINV2, static_cast<size_t>(n) * n);
   int* info = ctx->ws<int>(S_FLAGS, 4) + 1;
   TLG_CUDA(cudaMemsetAsync(info, 0, sizeof(int), ctx->stream));
   TLG_CUDA(cudaMemcpy2DAsync(T, n * 8, src, lds * 8, n * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
-  potrf_lower(ctx, T, n, n, info);
-  k_set_identity<<<std::max(1, std::min(n * n / 256 + 1, 1024)), 256, 0, ctx->stream>>>(dst, n, ldd);
-  TLG_LAUNCHED(ctx);
-  trsm_left_lower(ctx, T, n, n, dst, n, ldd, 0);
-  trsm_left_lower(ctx, T, n, n, dst, n, ldd, 1);
+  potrf_lower(ctx, T, n, n, info, X, n);
+  gemm(ctx, GemmDesc{n, n, n, X, n, 1, X, n, 0, dst, ldd, 1.0, 0.0, 0});
   int h = 0;
   TLG_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   TLG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -636,7 +635,8 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
     TLG_LAUNCHED(ctx);
     tr.mark("K_S");
     symmetrize(ctx, S, mi, mi);
-    potrf_lower(ctx, S, mi, mi, info);
+    double* X = ctx->ws<double>(S_XINV, static_cast<size_t>(mi) * mi);
+    potrf_lower(ctx, S, mi, mi, info, X, mi);
     int h = 0;
     TLG_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, s));
     TLG_CUDA(cudaStreamSynchronize(s));
@@ -644,17 +644,19 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
       rep->rejected = 1;
       return;
     }
-    // u = S^-1 r ; dw = K u
     tr.mark("potrf");
-    trsm_left_lower(ctx, S, mi, mi, resid, 1, mi, 0);
-    trsm_left_lower(ctx, S, mi, mi, resid, 1, mi, 1);
+    // u = S^-1 r = X^T (X r) ; dw = K u
+    double* v = ctx->ws<double>(S_SOLVE, mi);
+    gemm(ctx, GemmDesc{mi, 1, mi, X, mi, 0, resid, mi, 0, v, mi, 1.0, 0.0, 2});
+    gemm(ctx, GemmDesc{mi, 1, mi, X, mi, 1, v, mi, 0, resid, mi, 1.0, 0.0, 0});
     gemm(ctx, GemmDesc{n, 1, mi, Kt, mi, 1, resid, mi, 0, dw, n, 1.0, 0.0, 0});
-    // Y = L^-1 K^T (in place) ; Hinv1_q = Hinv0_q - Y_q^T Y_q
-    trsm_left_lower(ctx, S, mi, mi, Kt, n, mi, 0);
+    // Y = X K^T ; Hinv1_q = Hinv0_q - Y_q^T Y_q
+    double* Y = ctx->ws<double>(S_YMAT, static_cast<size_t>(mi) * n);
+    gemm(ctx, GemmDesc{mi, n, mi, X, mi, 0, Kt, mi, 0, Y, mi, 1.0, 0.0, 2});
     tr.mark("trsm");
     for (int q = 0; q < nq; ++q)
-      descs[q] = GemmDesc{tab[q].n, tab[q].n, mi, Kt + static_cast<size_t>(tab[q].off) * mi, mi, 1,
-                          Kt + static_cast<size_t>(tab[q].off) * mi, mi, 0,
+      descs[q] = GemmDesc{tab[q].n, tab[q].n, mi, Y + static_cast<size_t>(tab[q].off) * mi, mi, 1,
+                          Y + static_cast<size_t>(tab[q].off) * mi, mi, 0,
                           m->pool.p + tab[q].pool_off, tab[q].ld, -1.0, 1.0, 0};
   } else {
     // ---- (I) information form -----------------------------------------------
@@ -679,7 +681,9 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
     TLG_LAUNCHED(ctx);
     k_row_dot<<<(n + 255) / 256, 256, 0, s>>>(t.rowp, t.obs, t.val, resid, n, dw);
     TLG_LAUNCHED(ctx);
-    potrf_lower(ctx, H, n, n, info);
+    // X = L^-1 from the factorisation; (H^-1)_qq = X[:,q]^T X[:,q]
+    double* X = ctx->ws<double>(S_YMAT, static_cast<size_t>(n) * n);
+    potrf_lower(ctx, H, n, n, info, X, n);
     int h = 0;
     TLG_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, s));
     TLG_CUDA(cudaStreamSynchronize(s));
@@ -687,13 +691,9 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
       rep->rejected = 1;
       return;
     }
-    trsm_left_lower(ctx, H, n, n, dw, 1, n, 0);
-    trsm_left_lower(ctx, H, n, n, dw, 1, n, 1);
-    // X = L^-1 ; (H^-1)_qq = X[:,q]^T X[:,q]
-    double* X = ctx->ws<double>(S_YMAT, static_cast<size_t>(n) * n);
-    k_set_identity<<<std::min(n * n / 256 + 1, 4096), 256, 0, s>>>(X, n, n);
-    TLG_LAUNCHED(ctx);
-    trsm_left_lower(ctx, H, n, n, X, n, n, 0);
+    double* v = ctx->ws<double>(S_SOLVE, n);
+    gemm(ctx, GemmDesc{n, 1, n, X, n, 0, dw, n, 0, v, n, 1.0, 0.0, 2});
+    gemm(ctx, GemmDesc{n, 1, n, X, n, 1, v, n, 0, dw, n, 1.0, 0.0, 0});
     for (int q = 0; q < nq; ++q) {
       const size_t o = tab[q].off;
       descs[q] = GemmDesc{tab[q].n, tab[q].n, n - tab[q].off, X + o + o * n, n, 1,
