@@ -104,8 +104,14 @@ tlg_status tlg_ctx_kernel_stats(tlg_ctx* ctx, int kernel, double* total_ms, uint
 tlg_status tlg_measure_fp64_peak(tlg_ctx* ctx, double* dfma_tflops, double* dmma_tflops);
 /* Dense-solver microbenchmark (diagnostics): op 0 = Cholesky of an n x n SPD
  * matrix, 1 = triangular solve with nrhs right-hand sides, 2 = GEMM
- * n x nrhs x n. Best of `reps`, milliseconds. */
+ * n x nrhs x n, 3 = 64-wide diagonal tile (nrhs repetitions), 4 = grid barrier,
+ * 5 = Cholesky + inverse factor, 6 = 64-wide Cholesky. Best of `reps`, ms. */
 tlg_status tlg_debug_dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps, double* ms);
+/* Dense-solver check (diagnostics): Cholesky of the host n x n SPD matrix A
+ * (column-major) on the device; L (lower, zero above) and X = L^-1 back to the
+ * host. tile = 0 picks the production tiling, 32 / 64 force one. Returns
+ * TLG_DOMAIN_ERROR when a pivot is not positive. */
+tlg_status tlg_debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X);
 
 /* ---- kernel.cpp ------------------------------------------------------------- */
 /* KernelParams::finalize (kernel.cpp:15-25): fills the auto cutoff, validates. */

@@ -14,6 +14,9 @@ namespace cg = cooperative_groups;
 #ifndef TLG_PHASE
 #define TLG_PHASE(k)
 #endif
+#ifndef TLG_COOP_MARK
+#define TLG_COOP_MARK(k, step)
+#endif
 
 namespace tlg {
 
@@ -1130,9 +1133,11 @@ __global__ void __launch_bounds__(128) k_potrf_coop(double* __restrict__ A, int 
   for (int k = 0; k < nt; ++k) {
     const int k0 = k * NB, kb = min(NB, n - k0);
     const double* lk = linv + (size_t)k * NB * NB;
+    TLG_COOP_MARK(0, k);
     if (blockIdx.x == 0)
       TLG_DIAG_TILE(A + k0 + (size_t)k0 * lda, lda, kb, linv + (size_t)k * NB * NB, info, dyn);
     grid.sync();
+    TLG_COOP_MARK(1, k);
     // panel: L_ik = A_ik L_kk^-T (in place; one CTA owns a tile); with X also
     // finalise block row k of L^-1: X_kj = Linv_kk X_kj, j <= k
     const int npanel = nt - k - 1, nfin = X ? k + 1 : 0;
@@ -1151,6 +1156,7 @@ __global__ void __launch_bounds__(128) k_potrf_coop(double* __restrict__ A, int 
       __syncthreads();
     }
     grid.sync();
+    TLG_COOP_MARK(2, k);
     // trailing update of the lower tiles: A_ij -= L_ik L_jk^T, k < j <= i;
     // with X: X_ij -= L_ik X_kj, i > k >= j
     const int nr = nt - k - 1;
@@ -1179,6 +1185,246 @@ __global__ void __launch_bounds__(128) k_potrf_coop(double* __restrict__ A, int 
                   0, 0);
       }
       __syncthreads();
+    }
+    grid.sync();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 32-wide tile path for small systems (n <= kSmallN), where every step of the
+// factorisation is latency-bound: a 32 x 32 DMMA tile spreads the GEMM work
+// over 4x more SMs, and the diagonal tile is factored by ONE warp entirely in
+// registers (lane i owns row i), so a pivot costs shfl -> rsqrt -> mul -> fma
+// instead of block barriers and shared-memory round trips.
+constexpr int NB32 = 32;
+constexpr int kSmallN = 1024;
+
+// C (<= 32 x 32 at tile (tm, tn)) = alpha op(A) op(B) + beta C, 128 threads;
+// warp w owns the 16 x 16 quadrant (w & 1, w >> 1). uplo 2 as in gemm_tile.
+__device__ __forceinline__ void gemm32_tile(const GemmDesc& d, int tm, int tn) {
+  constexpr int P = 36;
+  __shared__ double As32[32][P];
+  __shared__ double Bs32[32][P];
+  const int m0 = tm * 32, n0 = tn * 32;
+  if (m0 >= d.M || n0 >= d.N) return;
+  const int K = (d.uplo == 2) ? min(d.K, m0 + 32) : d.K;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int wm = (w & 1) * 16, wn = (w >> 1) * 16;
+  double acc[2][2][2] = {};
+  double cpre[2][2][2];
+  if (d.beta != 0.0) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = m0 + wm + i * 8 + (lane >> 2), c = n0 + wn + j * 8 + 2 * (lane & 3) + h;
+          cpre[i][j][h] = (r < d.M && c < d.N) ? d.C[r + (size_t)c * d.ldc] : 0.0;
+        }
+  }
+  double pa[8], pb[8];
+  // element e = t + 128 s of the 32 x 32 chunk: (k, i) = (e >> 5, e & 31) when
+  // the source is contiguous along i, else (e & 31, e >> 5)
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int e = t + 128 * s, lo = e & 31, hi = e >> 5;
+      if (!d.ta) {
+        const int gi = m0 + lo, gk = k0 + hi;
+        pa[s] = (gi < d.M && gk < K) ? d.A[gi + (size_t)gk * d.lda] : 0.0;
+      } else {
+        const int gk = k0 + lo, gi = m0 + hi;
+        pa[s] = (gi < d.M && gk < K) ? d.A[gk + (size_t)gi * d.lda] : 0.0;
+      }
+      if (!d.tb) {
+        const int gk = k0 + lo, gj = n0 + hi;
+        pb[s] = (gj < d.N && gk < K) ? d.B[gk + (size_t)gj * d.ldb] : 0.0;
+      } else {
+        const int gj = n0 + lo, gk = k0 + hi;
+        pb[s] = (gj < d.N && gk < K) ? d.B[gj + (size_t)gk * d.ldb] : 0.0;
+      }
+    }
+  };
+  if (K > 0) fetch(0);
+  for (int k0 = 0; k0 < K; k0 += 32) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int e = t + 128 * s, lo = e & 31, hi = e >> 5;
+      if (!d.ta) As32[hi][lo] = pa[s];
+      else As32[lo][hi] = pa[s];
+      if (!d.tb) Bs32[lo][hi] = pb[s];
+      else Bs32[hi][lo] = pb[s];
+    }
+    __syncthreads();
+    if (k0 + 32 < K) fetch(k0 + 32);
+#pragma unroll
+    for (int kk = 0; kk < 32; kk += 4) {
+      double a[2], b[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) a[i] = As32[kk + (lane & 3)][wm + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = Bs32[kk + (lane & 3)][wn + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = m0 + wm + i * 8 + (lane >> 2), c = n0 + wn + j * 8 + 2 * (lane & 3) + h;
+        if (r < d.M && c < d.N) {
+          const double v = d.alpha * acc[i][j][h];
+          d.C[r + (size_t)c * d.ldc] = (d.beta == 0.0) ? v : fma(d.beta, cpre[i][j][h], v);
+        }
+      }
+}
+
+// One warp: L L^T = A for the kb x kb (kb <= 32) lower tile at A (lda), padded
+// with the identity; writes L back into A and X = L^-1 (32 x 32, ld 32,
+// zero above the diagonal) into linv. sh: kWarpPotrfSmem doubles.
+constexpr int kWarpPotrfSmem = 2 * 32 + 32 * 33 + 32;
+__device__ void warp_potrf_inv32(double* __restrict__ A, int lda, int kb,
+                                 double* __restrict__ linv, int* __restrict__ info,
+                                 double* __restrict__ sh) {
+  const int i = threadIdx.x & 31;
+  double* col = sh;            // [2][32] broadcast of the current column of L
+  double* xs = sh + 64;        // [32][33] transpose buffer
+  double* dinv = xs + 32 * 33;  // [32] 1 / L_jj
+  double a[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k)
+    a[k] = (i < kb && k < kb) ? (k <= i ? A[i + (size_t)k * lda] : 0.0) : (i == k ? 1.0 : 0.0);
+  TLG_PHASE(1);
+  bool bad = false;
+  double d = __shfl_sync(0xffffffffu, a[0], 0);
+  // Right-looking, lane i = row i. Entries above the diagonal hold garbage
+  // that is never read (pivots and columns only read k <= i).
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    bad |= !(d > 0.0) || !isfinite(d);
+    const double rs = rsqrt(d);
+    const double l = (i == j) ? d * rs : a[j] * rs;
+    a[j] = l;
+    if (i == j) dinv[j] = rs;
+    if (j + 1 < 32) {
+      // next pivot straight from the owner's own value (l_{j+1,j} = its l)
+      const double dn = fma(-l, l, a[j + 1]);
+      double* cb = col + (j & 1) * 32;
+      cb[i] = l;
+      d = __shfl_sync(0xffffffffu, dn, j + 1);
+      __syncwarp();
+#pragma unroll
+      for (int p = 0; p < 16; ++p) {
+        if (2 * p + 1 <= j) continue;  // both columns already eliminated
+        const double2 v = *reinterpret_cast<const double2*>(cb + 2 * p);
+        if (2 * p > j) a[2 * p] = fma(-l, v.x, a[2 * p]);
+        a[2 * p + 1] = fma(-l, v.y, a[2 * p + 1]);
+      }
+    }
+  }
+  TLG_PHASE(2);
+  if (bad && i == 0) atomicOr(info, 1);
+  // L back to A (lower part only) and to the transpose buffer (row i)
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    if (k <= i && i < kb && k < kb) A[i + (size_t)k * lda] = a[k];
+    xs[i * 33 + k] = (k <= i) ? a[k] : 0.0;
+  }
+  __syncwarp();
+  // X = L^-1, lane c = column c: X[k][c] = (delta_kc - sum_{p<k} L[k][p] X[p][c]) / L[k][k]
+  // accumulated right-looking so each row is one fma + one mul after the last.
+  TLG_PHASE(3);
+  double x[32];  // running right-hand side, becomes X[:, i] in place
+#pragma unroll
+  for (int k = 0; k < 32; ++k) x[k] = (k == i) ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    x[k] *= dinv[k];
+#pragma unroll
+    for (int r = k + 1; r < 32; ++r) x[r] = fma(-xs[r * 33 + k], x[k], x[r]);
+  }
+  TLG_PHASE(4);
+  __syncwarp();
+  // transpose so that the store of linv (column-major) is coalesced
+#pragma unroll
+  for (int k = 0; k < 32; ++k) xs[k * 33 + i] = x[k];
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 32; ++c) linv[i + (size_t)c * NB32] = xs[i * 33 + c];
+  TLG_PHASE(5);
+}
+
+__global__ void __launch_bounds__(128) k_potrf_coop32(double* __restrict__ A, int n, int lda,
+                                                      double* __restrict__ linv,
+                                                      int* __restrict__ info,
+                                                      double* __restrict__ X, int ldx) {
+  __shared__ double wsh[kWarpPotrfSmem];
+  cg::grid_group grid = cg::this_grid();
+  const int nt = (n + NB32 - 1) / NB32;
+  if (X) {
+    const size_t total = (size_t)n * n;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
+         e += (size_t)gridDim.x * blockDim.x) {
+      const int r = static_cast<int>(e % n), c = static_cast<int>(e / n);
+      X[r + (size_t)c * ldx] = (r == c) ? 1.0 : 0.0;
+    }
+    grid.sync();
+  }
+  for (int k = 0; k < nt; ++k) {
+    const int k0 = k * NB32, kb = min(NB32, n - k0);
+    const double* lk = linv + (size_t)k * NB32 * NB32;
+    TLG_COOP_MARK(0, k);
+    if (blockIdx.x == 0 && threadIdx.x < 32)
+      warp_potrf_inv32(A + k0 + (size_t)k0 * lda, lda, kb, linv + (size_t)k * NB32 * NB32, info,
+                       wsh);
+    grid.sync();
+    TLG_COOP_MARK(1, k);
+    const int npanel = nt - k - 1, nfin = X ? k + 1 : 0;
+    for (int e = blockIdx.x; e < npanel + nfin; e += gridDim.x) {
+      if (e < npanel) {
+        const int i0 = (k + 1 + e) * NB32, ib = min(NB32, n - i0);
+        double* P = A + i0 + (size_t)k0 * lda;
+        gemm32_tile(GemmDesc{ib, kb, kb, P, lda, 0, lk, NB32, 1, P, lda, 1.0, 0.0, 0}, 0, 0);
+      } else {
+        const int j0 = (e - npanel) * NB32, jb = min(NB32, n - j0);
+        double* T = X + k0 + (size_t)j0 * ldx;
+        gemm32_tile(GemmDesc{kb, jb, kb, lk, NB32, 0, T, ldx, 0, T, ldx, 1.0, 0.0, 0}, 0, 0);
+      }
+    }
+    grid.sync();
+    TLG_COOP_MARK(2, k);
+    const int nr = nt - k - 1;
+    const int ntiles = nr * (nr + 1) / 2;
+    const int nx = X ? nr * (k + 1) : 0;
+    for (int e = blockIdx.x; e < ntiles + nx; e += gridDim.x) {
+      if (e < ntiles) {
+        int r = 0, rem = e;
+        while (rem > r) {
+          rem -= r + 1;
+          ++r;
+        }
+        const int i0 = (k + 1 + r) * NB32, j0 = (k + 1 + rem) * NB32;
+        const int ib = min(NB32, n - i0), jb = min(NB32, n - j0);
+        gemm32_tile(GemmDesc{ib, jb, kb, A + i0 + (size_t)k0 * lda, lda, 0,
+                             A + j0 + (size_t)k0 * lda, lda, 1, A + i0 + (size_t)j0 * lda, lda,
+                             -1.0, 1.0, 0},
+                    0, 0);
+      } else {
+        const int f = e - ntiles;
+        const int i0 = (k + 1 + f / (k + 1)) * NB32, j0 = (f % (k + 1)) * NB32;
+        const int ib = min(NB32, n - i0), jb = min(NB32, n - j0);
+        gemm32_tile(GemmDesc{ib, jb, kb, A + i0 + (size_t)k0 * lda, lda, 0,
+                             X + k0 + (size_t)j0 * ldx, ldx, 0, X + i0 + (size_t)j0 * ldx, ldx,
+                             -1.0, 1.0, 0},
+                    0, 0);
+      }
     }
     grid.sync();
   }
@@ -1215,8 +1461,29 @@ __global__ void __launch_bounds__(128) k_trsm_tiles(const double* __restrict__ L
   }
 }
 
+static void potrf_lower32(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X,
+                          int ldx) {
+  const int nt = (n + NB32 - 1) / NB32;
+  double* linv = ctx->ws<double>(S_LINV, static_cast<size_t>(nt) * NB32 * NB32);
+  ctx->linv_owner = nullptr;  // 32-wide inverse tiles: not usable by trsm_left_lower
+  int per_sm = 0;
+  TLG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_potrf_coop32, 128, 0));
+  int maxtiles = nt;
+  for (int k = 0; k < nt; ++k)
+    maxtiles = std::max(maxtiles, (nt - k - 1) * (nt - k) / 2 + (X ? (nt - k - 1) * (k + 1) : 0));
+  const int grid = std::max(1, std::min(maxtiles, ctx->num_sms * std::max(per_sm, 1)));
+  void* args[] = {&A, &n, &lda, &linv, &info, &X, &ldx};
+  TLG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_potrf_coop32), dim3(grid),
+                                       dim3(128), args, 0, ctx->stream));
+  ++ctx->launches;
+}
+
 void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X, int ldx) {
   if (n <= 0) return;
+  if (n <= kSmallN && !ctx->force_nb64) {
+    potrf_lower32(ctx, A, n, lda, info, X, ldx);
+    return;
+  }
   const int nt = (n + NB - 1) / NB;
   double* linv = ctx->ws<double>(S_LINV, static_cast<size_t>(nt) * NB * NB);
   ctx->linv_owner = A;
@@ -1253,6 +1520,12 @@ __global__ void __launch_bounds__(128) k_gridsync_only(int reps) {
   for (int r = 0; r < reps; ++r) grid.sync();
 }
 
+__global__ void k_zero_upper(double* A, int n) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)n * n;
+       e += (long long)gridDim.x * blockDim.x)
+    if (e / n > e % n) A[e] = 0.0;
+}
+
 __global__ void k_spd_fill(double* A, int n, unsigned seed) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)n * n;
        e += (long long)gridDim.x * blockDim.x) {
@@ -1269,7 +1542,7 @@ double dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps) {
   cudaStream_t s = ctx->stream;
   DBuf<double> A, B;
   A.ensure(static_cast<size_t>(n) * n);
-  B.ensure(static_cast<size_t>(n) * std::max(nrhs, 1));
+  B.ensure(static_cast<size_t>(n) * std::max(nrhs, op == 5 ? n : 1));
   DBuf<int> info;
   info.ensure(1);
   TLG_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
@@ -1279,10 +1552,12 @@ double dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps) {
   float best = 1e30f;
   for (int it = 0; it < reps; ++it) {
     k_spd_fill<<<256, 256, 0, s>>>(A.p, n, 12345u + it);
-    TLG_CUDA(cudaMemsetAsync(B.p, 0, sizeof(double) * n * std::max(nrhs, 1), s));
+    TLG_CUDA(cudaMemsetAsync(B.p, 0, sizeof(double) * n * std::max(nrhs, op == 5 ? n : 1), s));
+    ctx->force_nb64 = (op == 1 || op == 6);
     if (op == 1) potrf_lower(ctx, A.p, n, n, info.p);
     TLG_CUDA(cudaEventRecord(e0, s));
-    if (op == 0) potrf_lower(ctx, A.p, n, n, info.p);
+    if (op == 0 || op == 6) potrf_lower(ctx, A.p, n, n, info.p);
+    else if (op == 5) potrf_lower(ctx, A.p, n, n, info.p, B.p, n);
     else if (op == 1) trsm_left_lower(ctx, A.p, n, n, B.p, nrhs, n, 0);
     else if (op == 2) gemm(ctx, GemmDesc{n, nrhs, n, A.p, n, 0, A.p, n, 1, B.p, n, 1.0, 0.0, 0});
     else if (op == 3) {
@@ -1304,7 +1579,35 @@ double dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps) {
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  ctx->force_nb64 = false;
   return best;
+}
+
+bool debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X) {
+  cudaStream_t s = ctx->stream;
+  const size_t nn = static_cast<size_t>(n) * n;
+  DBuf<double> dA, dX;
+  dA.ensure(nn);
+  dX.ensure(nn);
+  DBuf<int> info;
+  info.ensure(1);
+  TLG_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
+  TLG_CUDA(cudaMemcpyAsync(dA.p, A, nn * 8, cudaMemcpyHostToDevice, s));
+  ctx->force_nb64 = (tile == 64);
+  if (tile == 32) {
+    potrf_lower32(ctx, dA.p, n, n, info.p, dX.p, n);
+  } else {
+    potrf_lower(ctx, dA.p, n, n, info.p, dX.p, n);
+  }
+  ctx->force_nb64 = false;
+  k_zero_upper<<<256, 256, 0, s>>>(dA.p, n);
+  TLG_LAUNCHED(ctx);
+  int h = 0;
+  TLG_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (L) TLG_CUDA(cudaMemcpyAsync(L, dA.p, nn * 8, cudaMemcpyDeviceToHost, s));
+  if (X) TLG_CUDA(cudaMemcpyAsync(X, dX.p, nn * 8, cudaMemcpyDeviceToHost, s));
+  TLG_CUDA(cudaStreamSynchronize(s));
+  return h == 0;
 }
 
 void trsm_left_lower(tlg_ctx* ctx, const double* L, int n, int ldl, double* B, int nrhs,

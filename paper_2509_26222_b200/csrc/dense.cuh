@@ -33,6 +33,9 @@ void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X =
 // B <- L^-1 B (trans = 0) or B <- L^-T B (trans = 1); L lower n x n, B n x nrhs.
 void trsm_left_lower(tlg_ctx* ctx, const double* L, int n, int ldl, double* B, int nrhs,
                      int ldb, int trans);
+// Diagnostics: factor a host matrix, return L and L^-1 (tile 0 / 32 / 64).
+bool debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X);
+double dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps);
 // A <- 0.5 (A + A^T) for a square n x n matrix (in place).
 void symmetrize(tlg_ctx* ctx, double* A, int n, int lda);
 // A[i,i] += v

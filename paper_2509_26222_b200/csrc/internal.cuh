@@ -132,6 +132,7 @@ struct tlg_ctx {
   // dense.cu: inverses of the 64x64 diagonal Cholesky tiles of the most
   // recent potrf_lower (slot S_LINV), keyed by the factored matrix
   const double* linv_owner = nullptr;
+  bool force_nb64 = false;  // dense_bench: force the 64-wide factorisation
 
   template <typename T>
   T* ws(int slot, size_t count) {

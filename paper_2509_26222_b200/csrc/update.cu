@@ -770,12 +770,15 @@ void batch_fit_device(tlg_model* m, const double* x, const double* y, const doub
   }
   int* info = ctx->ws<int>(S_FLAGS, 4);
   TLG_CUDA(cudaMemsetAsync(info, 0, 4 * sizeof(int), s));
-  potrf_lower(ctx, H, n, n, info);
+  double* X = ctx->ws<double>(S_YMAT, static_cast<size_t>(n) * n);
+  potrf_lower(ctx, H, n, n, info, X, n);
   double* mnx = ctx->ws<double>(S_PARTIALS, 2);
   k_diag_minmax<<<1, 256, 0, s>>>(H, n, n, mnx);
   TLG_LAUNCHED(ctx);
-  trsm_left_lower(ctx, H, n, n, b, 1, n, 0);
-  trsm_left_lower(ctx, H, n, n, b, 1, n, 1);
+  // w = H^-1 b = X^T (X b)
+  double* v = ctx->ws<double>(S_SOLVE, n);
+  gemm(ctx, GemmDesc{n, 1, n, X, n, 0, b, n, 0, v, n, 1.0, 0.0, 2});
+  gemm(ctx, GemmDesc{n, 1, n, X, n, 1, v, n, 0, b, n, 1.0, 0.0, 0});
   int h = 0;
   double cond[2];
   TLG_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, s));
