@@ -105,7 +105,11 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
     eyd[l] = dy;
     rowok |= static_cast<uint32_t>(abs(__ldg(L.ccy + j0 + l) - qy) <= L.span) << l;
   }
-  if (L.rec_ok) {
+  // compiled geometries are only dispatched when the recurrence is safe
+  // (sweep_kind), so their code carries no per-node exp fallback
+  constexpr bool kRecAlways = G >= 0;
+  const bool rec = kRecAlways || L.rec_ok;
+  if (rec) {
     double e = exp(dy2[0] * neg_inv_2b2);
     double p = exp(L.c_res * fma(2.0, eyd[0], L.res));
 #pragma unroll
@@ -114,7 +118,7 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
       e *= p;
       p *= L.k2;
     }
-  } else {
+  } else if constexpr (!kRecAlways) {
 #pragma unroll
     for (int l = 0; l < WIN; ++l) ey[l] = exp(dy2[l] * neg_inv_2b2);
   }
@@ -123,7 +127,7 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
   const double* wbase = L.W + static_cast<size_t>(i0) * L.nj + j0;
   const double dx_first = __dsub_rn(__ldg(L.cxl + i0), x);
   double ex_e = 0.0, ex_p = 0.0;
-  if (L.rec_ok) {
+  if (rec) {
     ex_e = exp(__dmul_rn(dx_first, dx_first) * neg_inv_2b2);
     ex_p = exp(L.c_res * fma(2.0, dx_first, L.res));
   }
@@ -175,12 +179,11 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
       }
       any = (im | bm) != 0;
     }
-    double ex;
-    if (L.rec_ok) {
-      ex = ex_e;
+    double ex = ex_e;
+    if (rec) {
       ex_e *= ex_p;
       ex_p *= L.k2;
-    } else {
+    } else if constexpr (!kRecAlways) {
       ex = exp(dx2 * neg_inv_2b2);
     }
     if (any) {
@@ -275,7 +278,7 @@ static void check_err_flag(tlg_ctx* ctx, int* d_err, tlg_status st, const char* 
 
 int sweep_kind(const tlg_model* m) {
   if (!m->lat.valid) return 0;
-  return m->lat.geom_id >= 0 ? 100 + m->lat.geom_id : m->lat.win;
+  return (m->lat.geom_id >= 0 && lattice_view(m).rec_ok) ? 100 + m->lat.geom_id : m->lat.win;
 }
 
 #define TLG_KIND_DISPATCH(KINDV, CALL)                   \
