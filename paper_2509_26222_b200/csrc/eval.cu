@@ -335,6 +335,10 @@ constexpr int kNE = 29;  // 21 (A upper) + 6 (g) + cost + valid
 #define TLG_MANIFOLD_MINB 4
 #endif
 constexpr int kManifoldThreads = TLG_MANIFOLD_THREADS;
+#ifndef TLG_MANIFOLD_CHUNK
+#define TLG_MANIFOLD_CHUNK 8
+#endif
+constexpr unsigned long long kManifoldChunk = TLG_MANIFOLD_CHUNK;  // warp-iterations per claim
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -356,15 +360,21 @@ __global__ void __launch_bounds__(kManifoldThreads, TLG_MANIFOLD_MINB) k_manifol
   double acc = 0.0;
   const double* R = pose.R;
   const int lane = threadIdx.x & 31;
-  // Each warp walks a contiguous chunk of rows: with scan-binned input,
-  // consecutive iterations hit the same / neighbouring lattice cells, so the
-  // weight window stays L1-resident (a grid-stride walk jumps regions).
-  const size_t warps = (size_t)gridDim.x * (blockDim.x >> 5);
+  // Warps claim contiguous chunks of kManifoldChunk rows-of-32 from a global
+  // counter: with scan-binned input consecutive iterations hit the same /
+  // neighbouring lattice cells, so the weight window stays L1-resident, and
+  // dynamic claiming keeps the warps of a CTA finishing together.
   const size_t witer = (n + 31) / 32;
-  const size_t per_warp = (witer + warps - 1) / warps;
-  const size_t wid_g = (size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const size_t b_end = std::min(n, (wid_g + 1) * per_warp * 32);
-  for (size_t base = wid_g * per_warp * 32; base < b_end; base += 32) {
+  size_t base = 0, b_end = 0;
+  for (;;) {
+    if (base >= b_end) {
+      unsigned long long c = 0;
+      if (lane == 0) c = atomicAdd(reinterpret_cast<unsigned long long*>(err + 2), kManifoldChunk);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      if (c >= witer) break;
+      base = static_cast<size_t>(c) * 32;
+      b_end = std::min(n, static_cast<size_t>((c + kManifoldChunk) * 32));
+    }
     const size_t i = base + lane;
     const bool live = i < n;
     const double h0 = live ? hx[i] : 0.0, h1 = live ? hy[i] : 0.0, h2 = live ? hz[i] : 0.0;
@@ -427,6 +437,7 @@ __global__ void __launch_bounds__(kManifoldThreads, TLG_MANIFOLD_MINB) k_manifol
       acc += s;
     }
     __syncwarp();
+    base += 32;
   }
   // CTA reduction: lane L of every warp holds entry L; sum warps in order
   __shared__ double sh[kManifoldThreads / 32][32];
@@ -462,8 +473,9 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
   const unsigned blocks = grid_for(ctx, n, kManifoldThreads, 4 * TLG_MANIFOLD_MINB);
   double* partials = ctx->ws<double>(S_PARTIALS, static_cast<size_t>(blocks) * kNE + kNE);
   double* out = partials + static_cast<size_t>(blocks) * kNE;
+  // err[0]: non-finite flag; err[2..3]: 64-bit chunk counter (8-byte aligned)
   int* err = ctx->ws<int>(S_FLAGS, 4);
-  TLG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
+  TLG_CUDA(cudaMemsetAsync(err, 0, 4 * sizeof(int), ctx->stream));
   const GridView g = grid_view(m);
   const LatticeView L = lattice_view(m);
   const double sl = std::sqrt(lambda_M);
