@@ -260,6 +260,7 @@ def main():
     # bin the scan once under a perturbed initial-guess pose (LM re-evaluates
     # the same scan every iteration; the binning is amortised over them)
     R0 = so3_exp(np.array(POSE_W) + np.array([0.004, -0.003, 0.01]))
+    kin.Scan(model, R0, tv, h)  # first binning also sizes the workspace (not timed)
     scan = kin.Scan(model, R0, tv + np.array([0.03, -0.02, 0.01]), h)
     bin_ms = scan.bin_ms()
 
