@@ -109,9 +109,11 @@ tlg_status tlg_measure_fp64_peak(tlg_ctx* ctx, double* dfma_tflops, double* dmma
 tlg_status tlg_debug_dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps, double* ms);
 /* Dense-solver check (diagnostics): Cholesky of the host n x n SPD matrix A
  * (column-major) on the device; L (lower, zero above) and X = L^-1 back to the
- * host. tile = 0 picks the production tiling, 32 / 64 force one. Returns
+ * host. tile = 0 picks the production tiling, 32 / 64 force one; band in
+ * (0, n) declares A lower-banded (A_ij = 0 for i - j > band). Returns
  * TLG_DOMAIN_ERROR when a pivot is not positive. */
-tlg_status tlg_debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X);
+tlg_status tlg_debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, int band, double* L,
+                           double* X);
 
 /* ---- kernel.cpp ------------------------------------------------------------- */
 /* KernelParams::finalize (kernel.cpp:15-25): fills the auto cutoff, validates. */

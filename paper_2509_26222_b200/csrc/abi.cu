@@ -21,7 +21,7 @@ void moment_device(tlg_model* m, const double* x, const double* y, size_t n, uin
                    uint32_t** ids, double** vals, size_t* nnz);
 void fp64_peak(tlg_ctx* ctx, double* dfma, double* dmma);
 double dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps);
-bool debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X);
+bool debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X, int band);
 tlg_scan* scan_create(tlg_model* m, const double R0[9], const double t0[3], const double* hx,
                       const double* hy, const double* hz, size_t n);
 }  // namespace tlg
@@ -173,13 +173,14 @@ tlg_status tlg_debug_dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps
   });
 }
 
-tlg_status tlg_debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X) {
+tlg_status tlg_debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, int band, double* L,
+                           double* X) {
   return guard([&] {
     check_ptr(ctx, "ctx");
     check_ptr(A, "A");
     require(n > 0, TLG_INVALID_ARGUMENT, "n must be positive");
     require(tile == 0 || tile == 32 || tile == 64, TLG_INVALID_ARGUMENT, "tile must be 0, 32 or 64");
-    if (!debug_potrf(ctx, n, A, tile, L, X))
+    if (!debug_potrf(ctx, n, A, tile, L, X, band > 0 && band < n ? band : n))
       throw Error(TLG_DOMAIN_ERROR, "matrix is not positive definite");
   });
 }

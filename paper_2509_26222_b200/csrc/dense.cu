@@ -1361,10 +1361,12 @@ __device__ void warp_potrf_inv32(double* __restrict__ A, int lda, int kb,
   TLG_PHASE(5);
 }
 
+// bwt: lower tile bandwidth (tile (i, j) is zero for i - j > bwt; fill-in of
+// a banded matrix stays inside the band), nt - 1 for a dense matrix.
 __global__ void __launch_bounds__(128) k_potrf_coop32(double* __restrict__ A, int n, int lda,
                                                       double* __restrict__ linv,
                                                       int* __restrict__ info,
-                                                      double* __restrict__ X, int ldx) {
+                                                      double* __restrict__ X, int ldx, int bwt) {
   __shared__ double wsh[kWarpPotrfSmem];
   cg::grid_group grid = cg::this_grid();
   const int nt = (n + NB32 - 1) / NB32;
@@ -1386,7 +1388,8 @@ __global__ void __launch_bounds__(128) k_potrf_coop32(double* __restrict__ A, in
                        wsh);
     grid.sync();
     TLG_COOP_MARK(1, k);
-    const int npanel = nt - k - 1, nfin = X ? k + 1 : 0;
+    const int last = min(nt - 1, k + bwt);  // last tile row inside the band
+    const int npanel = last - k, nfin = X ? k + 1 : 0;
     for (int e = blockIdx.x; e < npanel + nfin; e += gridDim.x) {
       if (e < npanel) {
         const int i0 = (k + 1 + e) * NB32, ib = min(NB32, n - i0);
@@ -1400,7 +1403,7 @@ __global__ void __launch_bounds__(128) k_potrf_coop32(double* __restrict__ A, in
     }
     grid.sync();
     TLG_COOP_MARK(2, k);
-    const int nr = nt - k - 1;
+    const int nr = last - k;
     const int ntiles = nr * (nr + 1) / 2;
     const int nx = X ? nr * (k + 1) : 0;
     for (int e = blockIdx.x; e < ntiles + nx; e += gridDim.x) {
@@ -1462,26 +1465,31 @@ __global__ void __launch_bounds__(128) k_trsm_tiles(const double* __restrict__ L
 }
 
 static void potrf_lower32(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X,
-                          int ldx) {
+                          int ldx, int band) {
   const int nt = (n + NB32 - 1) / NB32;
+  int bwt = std::min(nt - 1, (std::max(band, 0) + NB32 - 1) / NB32);
   double* linv = ctx->ws<double>(S_LINV, static_cast<size_t>(nt) * NB32 * NB32);
   ctx->linv_owner = nullptr;  // 32-wide inverse tiles: not usable by trsm_left_lower
   int per_sm = 0;
   TLG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_potrf_coop32, 128, 0));
   int maxtiles = nt;
-  for (int k = 0; k < nt; ++k)
-    maxtiles = std::max(maxtiles, (nt - k - 1) * (nt - k) / 2 + (X ? (nt - k - 1) * (k + 1) : 0));
+  for (int k = 0; k < nt; ++k) {
+    const int nr = std::min(nt - 1, k + bwt) - k;
+    maxtiles = std::max(maxtiles, nr * (nr + 1) / 2 + (X ? nr * (k + 1) : 0));
+  }
   const int grid = std::max(1, std::min(maxtiles, ctx->num_sms * std::max(per_sm, 1)));
-  void* args[] = {&A, &n, &lda, &linv, &info, &X, &ldx};
+  void* args[] = {&A, &n, &lda, &linv, &info, &X, &ldx, &bwt};
   TLG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_potrf_coop32), dim3(grid),
                                        dim3(128), args, 0, ctx->stream));
   ++ctx->launches;
 }
 
-void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X, int ldx) {
+void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X, int ldx,
+                 int band) {
   if (n <= 0) return;
-  if (n <= kSmallN && !ctx->force_nb64) {
-    potrf_lower32(ctx, A, n, lda, info, X, ldx);
+  if (band < 0 || band > n) band = n;
+  if ((n <= kSmallN || band < n) && !ctx->force_nb64) {
+    potrf_lower32(ctx, A, n, lda, info, X, ldx, band);
     return;
   }
   const int nt = (n + NB - 1) / NB;
@@ -1583,7 +1591,7 @@ double dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps) {
   return best;
 }
 
-bool debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X) {
+bool debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X, int band) {
   cudaStream_t s = ctx->stream;
   const size_t nn = static_cast<size_t>(n) * n;
   DBuf<double> dA, dX;
@@ -1595,9 +1603,9 @@ bool debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, doub
   TLG_CUDA(cudaMemcpyAsync(dA.p, A, nn * 8, cudaMemcpyHostToDevice, s));
   ctx->force_nb64 = (tile == 64);
   if (tile == 32) {
-    potrf_lower32(ctx, dA.p, n, n, info.p, dX.p, n);
+    potrf_lower32(ctx, dA.p, n, n, info.p, dX.p, n, band);
   } else {
-    potrf_lower(ctx, dA.p, n, n, info.p, dX.p, n);
+    potrf_lower(ctx, dA.p, n, n, info.p, dX.p, n, band);
   }
   ctx->force_nb64 = false;
   k_zero_upper<<<256, 256, 0, s>>>(dA.p, n);

@@ -28,13 +28,16 @@ void gemm_grouped(tlg_ctx* ctx, const GemmDesc* d_descs, int count, int max_m, i
 // `info` (device int) is set non-zero when a pivot is not positive/finite.
 // With X != nullptr the full inverse factor X = L^-1 (n x n, ldx, zero above
 // the diagonal) is built in the same launch, so later solves are GEMMs.
+// band < n declares A lower-banded (A_ij = 0 for i - j > band): the
+// factorisation then skips the tiles outside the band (32-wide tiles).
 void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X = nullptr,
-                 int ldx = 0);
+                 int ldx = 0, int band = -1);
 // B <- L^-1 B (trans = 0) or B <- L^-T B (trans = 1); L lower n x n, B n x nrhs.
 void trsm_left_lower(tlg_ctx* ctx, const double* L, int n, int ldl, double* B, int nrhs,
                      int ldb, int trans);
 // Diagnostics: factor a host matrix, return L and L^-1 (tile 0 / 32 / 64).
-bool debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X);
+bool debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X,
+                 int band = -1);
 double dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps);
 // A <- 0.5 (A + A^T) for a square n x n matrix (in place).
 void symmetrize(tlg_ctx* ctx, double* A, int n, int lda);

@@ -20,6 +20,7 @@
 // weights/blocks untouched while births persist (:222-225).
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -333,6 +334,105 @@ __global__ void __launch_bounds__(128) k_gram_rows(
   for (int s = threadIdx.x; s < n; s += blockDim.x) H[s + (size_t)r * ldh] += acc[s];
 }
 
+// Transposed CSR of Mt (by merged row).
+struct TCsr {
+  uint32_t* rowp;
+  uint32_t* obs;
+  double* val;
+};
+
+// Banded Gram: one warp per row r accumulates row r of Mt Mt^T over the
+// columns [r - band, r + band] in a per-warp shared window (observations in
+// ascending order, an observation's entries have distinct columns -> no
+// races, deterministic), then adds the window into column r of H.
+constexpr int kGramWarps = 4;
+__global__ void __launch_bounds__(32 * kGramWarps) k_gram_rows_band(
+    const uint32_t* __restrict__ trowp, const uint32_t* __restrict__ tobs,
+    const double* __restrict__ tval, const uint32_t* __restrict__ rowp,
+    const uint32_t* __restrict__ col, const double* __restrict__ val, int n, int band,
+    double* __restrict__ H, int ldh) {
+  extern __shared__ double gsm[];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int width = 2 * band + 1;
+  double* acc = gsm + wq * width;
+  for (int r = blockIdx.x * kGramWarps + wq; r < n; r += gridDim.x * kGramWarps) {
+    const int lo = r - band;
+    for (int s = lane; s < width; s += 32) acc[s] = 0.0;
+    __syncwarp();
+    const uint32_t q_end = trowp[r + 1];
+    for (uint32_t q0 = trowp[r]; q0 < q_end; q0 += 32) {
+      // lane-parallel fetch of 32 observations' metadata (one latency)
+      const uint32_t qq = q0 + lane;
+      uint32_t jb = 0, je = 0;
+      double vr = 0.0;
+      if (qq < q_end) {
+        const uint32_t j = tobs[qq];
+        vr = tval[qq];
+        jb = rowp[j];
+        je = rowp[j + 1];
+      }
+      const int cnt = static_cast<int>(min(32u, q_end - q0));
+      // software pipeline: entries of observation k + 1 load while k updates
+      constexpr int kPre = 4;  // entries per lane kept in flight (128 per obs)
+      int pc[kPre];
+      double pv[kPre];
+      auto fetch = [&](int k) {
+        const uint32_t b = __shfl_sync(0xffffffffu, jb, k), e = __shfl_sync(0xffffffffu, je, k);
+#pragma unroll
+        for (int u = 0; u < kPre; ++u) {
+          const uint32_t x = b + lane + 32 * u;
+          pc[u] = x < e ? static_cast<int>(col[x]) - lo : -1;
+          pv[u] = x < e ? val[x] : 0.0;
+        }
+      };
+      fetch(0);
+      for (int k = 0; k < cnt; ++k) {
+        int cc[kPre];
+        double cv[kPre];
+#pragma unroll
+        for (int u = 0; u < kPre; ++u) {
+          cc[u] = pc[u];
+          cv[u] = pv[u];
+        }
+        const double v = __shfl_sync(0xffffffffu, vr, k);
+        const uint32_t b = __shfl_sync(0xffffffffu, jb, k), e = __shfl_sync(0xffffffffu, je, k);
+        if (k + 1 < cnt) fetch(k + 1);
+#pragma unroll
+        for (int u = 0; u < kPre; ++u)
+          if (cc[u] >= 0) acc[cc[u]] = fma(v, cv[u], acc[cc[u]]);
+        // observations with more than 32 * kPre entries (other geometries)
+        for (uint32_t x = b + 32 * kPre + lane; x < e; x += 32) {
+          const int ci = static_cast<int>(col[x]) - lo;
+          acc[ci] = fma(v, val[x], acc[ci]);
+        }
+        __syncwarp();
+      }
+    }
+    const int c0 = max(lo, 0), c1 = min(r + band, n - 1);
+    for (int cc = c0 + lane; cc <= c1; cc += 32) H[cc + (size_t)r * ldh] += acc[cc - lo];
+    __syncwarp();
+  }
+}
+
+static void gram_band(tlg_ctx* ctx, const TCsr& t, const Csr& c, int n, int band, double* H,
+                      int ldh) {
+  const size_t smem_band = sizeof(double) * kGramWarps * (2 * static_cast<size_t>(band) + 1);
+  if (smem_band <= 200 * 1024) {
+    if (smem_band > 48 * 1024)
+      TLG_CUDA(cudaFuncSetAttribute(k_gram_rows_band, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem_band));
+    const unsigned blocks = static_cast<unsigned>((n + kGramWarps - 1) / kGramWarps);
+    k_gram_rows_band<<<blocks, 32 * kGramWarps, smem_band, ctx->stream>>>(
+        t.rowp, t.obs, t.val, c.rowp, c.col, c.val, n, band, H, ldh);
+  } else {
+    const size_t smem = static_cast<size_t>(n) * 8;
+    if (smem > 48 * 1024)
+      TLG_CUDA(cudaFuncSetAttribute(k_gram_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_gram_rows<<<n, 128, smem, ctx->stream>>>(t.rowp, t.obs, t.val, c.rowp, c.col, c.val, n, H, ldh);
+  }
+  TLG_LAUNCHED(ctx);
+}
+
 // rhs b[r] = sum_{j in row r} v_rj * c_j  (c = residual or z)
 __global__ void k_row_dot(const uint32_t* __restrict__ trowp, const uint32_t* __restrict__ tobs,
                           const double* __restrict__ tval, const double* __restrict__ c, int n,
@@ -401,6 +501,76 @@ static bool spd_inverse(tlg_ctx* ctx, const double* src, int lds, int n, double*
   return h == 0;
 }
 
+// All active blocks at once: one CTA per block q inverts info_inv_q (SPD,
+// n_q <= kBatchInvMax) in shared memory — right-looking Cholesky L, then
+// X = L^-1 by the same right-looking sweep on the identity, then
+// A^-1 = X^T X — and writes it into the diagonal block of H (ld ldh).
+// Warps walk rows, lanes walk columns. info != 0 on a non-positive pivot.
+constexpr int kBatchInvMax = 112;
+__global__ void __launch_bounds__(256) k_batched_spd_inverse(const BlockTab* __restrict__ tab,
+                                                             const double* __restrict__ pool,
+                                                             double* __restrict__ H, int ldh,
+                                                             int* __restrict__ info) {
+  extern __shared__ double sm[];
+  const BlockTab b = tab[blockIdx.x];
+  const int n = b.n, P = n + 1, t = threadIdx.x, lane = t & 31, wq = t >> 5;
+  const int nw = blockDim.x >> 5;
+  double* a = sm;          // a[r * P + c]: lower triangle -> L
+  double* x = sm + n * P;  // x[r * P + c]: X = L^-1 (lower)
+  const double* src = pool + b.pool_off;
+  for (int e = t; e < n * n; e += blockDim.x) {
+    const int r = e % n, c = e / n;
+    if (r >= c) a[r * P + c] = src[r + (size_t)c * b.ld];
+    x[r * P + c] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  __shared__ double piv;
+  for (int j = 0; j < n; ++j) {
+    if (t == 0) {
+      const double d = a[j * P + j];
+      if (!(d > 0.0) || !isfinite(d)) atomicOr(info, 1);
+      const double l = sqrt(d);
+      a[j * P + j] = l;
+      piv = 1.0 / l;
+    }
+    __syncthreads();
+    for (int i = j + 1 + t; i < n; i += blockDim.x) a[i * P + j] *= piv;
+    __syncthreads();
+    for (int r = j + 1 + wq; r < n; r += nw) {
+      const double lr = a[r * P + j];
+      for (int c = j + 1 + lane; c <= r; c += 32) a[r * P + c] = fma(-lr, a[c * P + j], a[r * P + c]);
+    }
+    __syncthreads();
+  }
+  // X = L^-1: row k final = row k / L_kk, then rows below lose L_rk * row k
+  for (int k = 0; k < n; ++k) {
+    const double inv = 1.0 / a[k * P + k];
+    for (int c = t; c <= k; c += blockDim.x) x[k * P + c] *= inv;
+    __syncthreads();
+    for (int r = k + 1 + wq; r < n; r += nw) {
+      const double lr = a[r * P + k];
+      for (int c = lane; c <= k; c += 32) x[r * P + c] = fma(-lr, x[k * P + c], x[r * P + c]);
+    }
+    __syncthreads();
+  }
+  // A^-1 = X^T X: (r, c) = sum_{p >= max(r, c)} x_pr x_pc; write both halves
+  double* dst = H + b.off + (size_t)b.off * ldh;
+  for (int r = wq; r < n; r += nw) {
+    for (int c = lane; c <= r; c += 32) {
+      double s0 = 0.0, s1 = 0.0;
+      int p = r;
+      for (; p + 1 < n; p += 2) {
+        s0 = fma(x[p * P + r], x[p * P + c], s0);
+        s1 = fma(x[(p + 1) * P + r], x[(p + 1) * P + c], s1);
+      }
+      if (p < n) s0 = fma(x[p * P + r], x[p * P + c], s0);
+      const double v = s0 + s1;
+      dst[r + (size_t)c * ldh] = v;
+      dst[c + (size_t)r * ldh] = v;
+    }
+  }
+}
+
 __global__ void k_iota(uint32_t* __restrict__ a, size_t n) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i < n) a[i] = static_cast<uint32_t>(i);
@@ -424,12 +594,7 @@ static void gather_tcsr(tlg_ctx* ctx, const uint32_t* perm, const uint32_t* obs_
   TLG_LAUNCHED(ctx);
 }
 
-// Transposed CSR of Mt (by merged row). Returns trowp (n+1), tobs, tval.
-struct TCsr {
-  uint32_t* rowp;
-  uint32_t* obs;
-  double* val;
-};
+// Transposed CSR of Mt (by merged row): trowp (n+1), tobs, tval.
 static TCsr transpose_csr(tlg_ctx* ctx, const Csr& c, size_t m, int n) {
   cudaStream_t s = ctx->stream;
   TCsr t;
@@ -560,6 +725,37 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   rep->active_blocks = ablocks.size();
   if (ablocks.empty()) return;
   tr.mark("active");
+  size_t n_total = 0;
+  for (uint32_t b : ablocks) n_total += m->members[b].size();
+  // The information form factors H1 = H0 + Mt Mt^T, which couples only
+  // blocks whose tiles touch (|dtx|, |dty| <= 1: shared observations lie within
+  // the cutoff of both centres, tile side = 2 cutoff). Ordering the merged
+  // blocks row by row over the tile grid (the shorter extent fastest) makes
+  // H1 block-banded; the band is passed to the factorisation. The Woodbury
+  // form keeps the reference's ascending block order.
+  const bool info_form = mm > n_total;
+  std::vector<std::pair<int64_t, int64_t>> btile;
+  if (info_form && m->tile_blocks.size() > 1) {
+    btile.assign(nb, {0, 0});
+    for (const auto& [key, b] : m->tile_blocks)
+      btile[b] = {static_cast<int32_t>(static_cast<uint64_t>(key) >> 32),
+                  static_cast<int32_t>(static_cast<uint64_t>(key) & 0xffffffffu)};
+    int64_t x0 = INT64_MAX, x1 = INT64_MIN, y0 = INT64_MAX, y1 = INT64_MIN;
+    for (uint32_t b : ablocks) {
+      x0 = std::min(x0, btile[b].first);
+      x1 = std::max(x1, btile[b].first);
+      y0 = std::min(y0, btile[b].second);
+      y1 = std::max(y1, btile[b].second);
+    }
+    const bool x_fast = (x1 - x0) <= (y1 - y0);
+    std::stable_sort(ablocks.begin(), ablocks.end(), [&](uint32_t a, uint32_t b) {
+      const auto ka = x_fast ? std::make_pair(btile[a].second, btile[a].first)
+                             : std::make_pair(btile[a].first, btile[a].second);
+      const auto kb = x_fast ? std::make_pair(btile[b].second, btile[b].first)
+                             : std::make_pair(btile[b].first, btile[b].second);
+      return ka < kb;
+    });
+  }
 
   // ---- merged system (:174-184) ------------------------------------------
   std::vector<uint32_t> merged;
@@ -582,6 +778,24 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   rep->active_centers = static_cast<uint64_t>(n);
   int maxq = 0;
   for (const auto& t : tab) maxq = std::max(maxq, t.n);
+  // lower bandwidth (rows) of H1 under the merged order: row r of block q is
+  // coupled to no column left of the first row of the earliest touching block
+  int band = n;
+  if (!btile.empty()) {
+    band = 0;
+    for (int q = 0; q < nq; ++q) {
+      int first = tab[q].off;
+      for (int p = 0; p < q; ++p) {
+        const auto& a = btile[ablocks[p]];
+        const auto& b = btile[ablocks[q]];
+        if (std::llabs(a.first - b.first) <= 1 && std::llabs(a.second - b.second) <= 1) {
+          first = tab[p].off;
+          break;
+        }
+      }
+      band = std::max(band, tab[q].off + tab[q].n - 1 - first);
+    }
+  }
 
   // pinned staging for the small host->device tables
   const size_t bytes_merged = n * 4, bytes_tab = nq * sizeof(BlockTab), bytes_rb = n * 4;
@@ -623,7 +837,7 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   const int mi = static_cast<int>(mm);
   std::vector<GemmDesc> descs(nq);
 
-  if (mm <= static_cast<size_t>(n)) {
+  if (!info_form) {
     // ---- (W) one-shot Woodbury ----------------------------------------------
     rep->solver = 1;
     double* Kt = ctx->ws<double>(S_KMAT, static_cast<size_t>(mi) * n);
@@ -665,32 +879,40 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
             "dense information-form update limited to 25600 active centres");
     double* H = ctx->ws<double>(S_HMAT, static_cast<size_t>(n) * n);
     TLG_CUDA(cudaMemsetAsync(H, 0, sizeof(double) * n * n, s));
-    // H0 = blockdiag(info_inv_q)^-1
-    for (int q = 0; q < nq; ++q) {
-      double* dst = H + tab[q].off + static_cast<size_t>(tab[q].off) * n;
-      if (!spd_inverse(ctx, m->pool.p + tab[q].pool_off, tab[q].ld, tab[q].n, dst, n)) {
-        rep->rejected = 1;
-        return;
+    // H0 = blockdiag(info_inv_q)^-1: all blocks in one launch when they fit
+    // in shared memory, else one factorisation per block
+    if (maxq <= kBatchInvMax) {
+      const int smem_inv = 2 * maxq * (maxq + 1) * 8;
+      TLG_CUDA(cudaFuncSetAttribute(k_batched_spd_inverse,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem_inv));
+      k_batched_spd_inverse<<<nq, 256, smem_inv, s>>>(d_tab, m->pool.p, H, n, info + 1);
+      TLG_LAUNCHED(ctx);
+    } else {
+      for (int q = 0; q < nq; ++q) {
+        double* dst = H + tab[q].off + static_cast<size_t>(tab[q].off) * n;
+        if (!spd_inverse(ctx, m->pool.p + tab[q].pool_off, tab[q].ld, tab[q].n, dst, n)) {
+          rep->rejected = 1;
+          return;
+        }
       }
     }
+    tr.mark("H0");
     const TCsr t = transpose_csr(ctx, c, mm, n);
-    const size_t smem = static_cast<size_t>(n) * 8;
-    if (smem > 48 * 1024)
-      TLG_CUDA(cudaFuncSetAttribute(k_gram_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_gram_rows<<<n, 128, smem, s>>>(t.rowp, t.obs, t.val, c.rowp, c.col, c.val, n, H, n);
-    TLG_LAUNCHED(ctx);
+    gram_band(ctx, t, c, n, band, H, n);
     k_row_dot<<<(n + 255) / 256, 256, 0, s>>>(t.rowp, t.obs, t.val, resid, n, dw);
     TLG_LAUNCHED(ctx);
     // X = L^-1 from the factorisation; (H^-1)_qq = X[:,q]^T X[:,q]
+    tr.mark("gram");
     double* X = ctx->ws<double>(S_YMAT, static_cast<size_t>(n) * n);
-    potrf_lower(ctx, H, n, n, info, X, n);
-    int h = 0;
-    TLG_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    potrf_lower(ctx, H, n, n, info, X, n, band);
+    int h[2] = {0, 0};
+    TLG_CUDA(cudaMemcpyAsync(h, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     TLG_CUDA(cudaStreamSynchronize(s));
-    if (h) {
+    if (h[0] || h[1]) {
       rep->rejected = 1;
       return;
     }
+    tr.mark("potrf");
     double* v = ctx->ws<double>(S_SOLVE, n);
     gemm(ctx, GemmDesc{n, 1, n, X, n, 0, dw, n, 0, v, n, 1.0, 0.0, 2});
     gemm(ctx, GemmDesc{n, 1, n, X, n, 1, v, n, 0, dw, n, 1.0, 0.0, 0});

@@ -10,13 +10,13 @@ from paper_2509_26222_b200 import _abi
 from paper_2509_26222_b200 import terrain as T
 
 
-def _potrf(A, tile):
+def _potrf(A, tile, band=0):
     n = A.shape[0]
     A = np.asfortranarray(A, dtype=np.float64)
     L = np.zeros((n, n), order="F")
     X = np.zeros((n, n), order="F")
     _abi.check(_abi.load().tlg_debug_potrf(T.Context.default().handle, n, A.ctypes.data, tile,
-                                           L.ctypes.data, X.ctypes.data))
+                                           band, L.ctypes.data, X.ctypes.data))
     return L, X
 
 
@@ -30,6 +30,23 @@ def test_potrf_and_inverse(gpu_ctx, n, tile):
     L, X = _potrf(A, tile)
     Lref = np.linalg.cholesky(A)
     assert np.abs(np.triu(L, 1)).max() == 0.0
+    np.testing.assert_allclose(L, Lref, rtol=0, atol=1e-12 * np.abs(Lref).max())
+    np.testing.assert_allclose(X @ L, np.eye(n), rtol=0, atol=1e-12)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,band", [(300, 40), (1500, 200), (2000, 31), (700, 699)])
+def test_potrf_banded(gpu_ctx, n, band):
+    # block-banded SPD matrix (the information-form structure): the banded
+    # factorisation must equal the dense one, and X = L^-1 stays exact
+    rng = np.random.default_rng(band)
+    G = rng.standard_normal((n, n))
+    A = G @ G.T
+    i, j = np.indices((n, n))
+    A[np.abs(i - j) > band] = 0.0
+    A += n * np.eye(n)
+    L, X = _potrf(A, 0, band)
+    Lref = np.linalg.cholesky(A)
     np.testing.assert_allclose(L, Lref, rtol=0, atol=1e-12 * np.abs(Lref).max())
     np.testing.assert_allclose(X @ L, np.eye(n), rtol=0, atol=1e-12)
 
