@@ -1363,6 +1363,9 @@ __device__ void warp_potrf_inv32(double* __restrict__ A, int lda, int kb,
 
 // bwt: lower tile bandwidth (tile (i, j) is zero for i - j > bwt; fill-in of
 // a banded matrix stays inside the band), nt - 1 for a dense matrix.
+// Lookahead schedule (two grid barriers per step): the diagonal tile k+1 is
+// updated and factored by block 0 inside the trailing phase of step k, while
+// the other blocks apply the rest of step k's trailing update (and X's).
 __global__ void __launch_bounds__(128) k_potrf_coop32(double* __restrict__ A, int n, int lda,
                                                       double* __restrict__ linv,
                                                       int* __restrict__ info,
@@ -1370,27 +1373,25 @@ __global__ void __launch_bounds__(128) k_potrf_coop32(double* __restrict__ A, in
   __shared__ double wsh[kWarpPotrfSmem];
   cg::grid_group grid = cg::this_grid();
   const int nt = (n + NB32 - 1) / NB32;
+  const int G = gridDim.x, bid = blockIdx.x;
   if (X) {
     const size_t total = (size_t)n * n;
-    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
-         e += (size_t)gridDim.x * blockDim.x) {
+    for (size_t e = bid * (size_t)blockDim.x + threadIdx.x; e < total;
+         e += (size_t)G * blockDim.x) {
       const int r = static_cast<int>(e % n), c = static_cast<int>(e / n);
       X[r + (size_t)c * ldx] = (r == c) ? 1.0 : 0.0;
     }
-    grid.sync();
   }
+  if (bid == 0 && threadIdx.x < 32) warp_potrf_inv32(A, lda, min(NB32, n), linv, info, wsh);
+  grid.sync();
   for (int k = 0; k < nt; ++k) {
     const int k0 = k * NB32, kb = min(NB32, n - k0);
     const double* lk = linv + (size_t)k * NB32 * NB32;
     TLG_COOP_MARK(0, k);
-    if (blockIdx.x == 0 && threadIdx.x < 32)
-      warp_potrf_inv32(A + k0 + (size_t)k0 * lda, lda, kb, linv + (size_t)k * NB32 * NB32, info,
-                       wsh);
-    grid.sync();
     TLG_COOP_MARK(1, k);
     const int last = min(nt - 1, k + bwt);  // last tile row inside the band
     const int npanel = last - k, nfin = X ? k + 1 : 0;
-    for (int e = blockIdx.x; e < npanel + nfin; e += gridDim.x) {
+    for (int e = bid; e < npanel + nfin; e += G) {
       if (e < npanel) {
         const int i0 = (k + 1 + e) * NB32, ib = min(NB32, n - i0);
         double* P = A + i0 + (size_t)k0 * lda;
@@ -1403,10 +1404,13 @@ __global__ void __launch_bounds__(128) k_potrf_coop32(double* __restrict__ A, in
     }
     grid.sync();
     TLG_COOP_MARK(2, k);
+    if (k + 1 == nt) break;
     const int nr = last - k;
     const int ntiles = nr * (nr + 1) / 2;
     const int nx = X ? nr * (k + 1) : 0;
-    for (int e = blockIdx.x; e < ntiles + nx; e += gridDim.x) {
+    // trailing tile e -> (i, j) = (k + 1 + r, k + 1 + rem), rem <= r; e = 0 is
+    // the next diagonal tile
+    auto trailing = [&](int e) {
       if (e < ntiles) {
         int r = 0, rem = e;
         while (rem > r) {
@@ -1428,6 +1432,19 @@ __global__ void __launch_bounds__(128) k_potrf_coop32(double* __restrict__ A, in
                              -1.0, 1.0, 0},
                     0, 0);
       }
+    };
+    if (bid == 0) {
+      if (ntiles > 0) trailing(0);
+      __syncthreads();
+      const int k1 = (k + 1) * NB32;
+      if (threadIdx.x < 32)
+        warp_potrf_inv32(A + k1 + (size_t)k1 * lda, lda, min(NB32, n - k1),
+                         linv + (size_t)(k + 1) * NB32 * NB32, info, wsh);
+      __syncthreads();
+      if (G == 1)
+        for (int e = 1; e < ntiles + nx; ++e) trailing(e);
+    } else {
+      for (int e = bid; e < ntiles + nx; e += G - 1) trailing(e);
     }
     grid.sync();
   }
