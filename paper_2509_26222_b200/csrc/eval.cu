@@ -346,32 +346,62 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Index of Gram entry (i, j) of V = [J0..J5, r, valid] in the 29-entry
+// normal-equation layout (A upper row-major, g, cost, valid), -1 if unused.
+__device__ __forceinline__ int ne_index(int i, int j) {
+  if (i <= j && j < 6) return i * 6 - i * (i - 1) / 2 + (j - i);
+  if (i < 6 && j == 6) return 21 + i;
+  if (i == 6 && j == 6) return 27;
+  if (i == 7 && j == 7) return 28;
+  return -1;
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(kManifoldThreads, TLG_MANIFOLD_MINB) k_manifold(
     GridView g, LatticeView L, Pose pose, const double* __restrict__ hx,
     const double* __restrict__ hy, const double* __restrict__ hz, size_t n, double r2,
     double neg_inv_2s2, double inv_s2, double wheel_radius, double sl, double huber,
     double* __restrict__ out_r, double* __restrict__ out_J, uint8_t* __restrict__ out_valid,
-    double* __restrict__ out_raw, double* __restrict__ partials, int* __restrict__ err) {
-  // Lane L accumulates normal-equation entry L: each warp iteration drops its
-  // 32 rows' 29 products into a per-warp shared tile and lane L sums row L in
-  // lane order (deterministic) -> one accumulator register per lane.
-  __shared__ double tile[kManifoldThreads / 32][kNE][33];
-  double acc = 0.0;
+    double* __restrict__ out_raw, double* __restrict__ partials, size_t nchunks,
+    int* __restrict__ err) {
+  // Normal equations on the FP64 tensor pipe: each point contributes the
+  // rank-1 Gram V V^T of V = [J, r, valid] (8 components); a warp stages its
+  // 32 rows' V in shared memory and 8 DMMA m8n8k4 steps add V^T V into an
+  // 8x8 accumulator held as 2 doubles per lane. Per claimed chunk the 29
+  // used entries go to partials[entry][chunk] (fixed slots -> the final
+  // reduction is order-fixed and deterministic despite dynamic claiming).
+  __shared__ __align__(16) double vt[kManifoldThreads / 32][32][8];
+  double c0 = 0.0, c1 = 0.0;
   const double* R = pose.R;
   const int lane = threadIdx.x & 31;
+  double(*V)[8] = vt[threadIdx.x >> 5];
+  const int gi = lane >> 2, gj0 = 2 * (lane & 3);
+  const int e0 = ne_index(gi, gj0), e1 = ne_index(gi, gj0 + 1);
   // Warps claim contiguous chunks of kManifoldChunk rows-of-32 from a global
   // counter: with scan-binned input consecutive iterations hit the same /
   // neighbouring lattice cells, so the weight window stays L1-resident, and
   // dynamic claiming keeps the warps of a CTA finishing together.
   const size_t witer = (n + 31) / 32;
   size_t base = 0, b_end = 0;
+  unsigned long long chunk = 0;
   for (;;) {
     if (base >= b_end) {
+      if (b_end != 0) {  // flush the finished chunk's Gram
+        if (e0 >= 0) partials[(size_t)e0 * nchunks + chunk] = c0;
+        if (e1 >= 0) partials[(size_t)e1 * nchunks + chunk] = c1;
+        c0 = c1 = 0.0;
+      }
       unsigned long long c = 0;
       if (lane == 0) c = atomicAdd(reinterpret_cast<unsigned long long*>(err + 2), kManifoldChunk);
       c = __shfl_sync(0xffffffffu, c, 0);
       if (c >= witer) break;
+      chunk = c / kManifoldChunk;
       base = static_cast<size_t>(c) * 32;
       b_end = std::min(n, static_cast<size_t>((c + kManifoldChunk) * 32));
     }
@@ -419,44 +449,50 @@ __global__ void __launch_bounds__(kManifoldThreads, TLG_MANIFOLD_MINB) k_manifol
         for (int c = 0; c < 6; ++c) out_J[c * n + i] = J[c];
       }
     }
-    double(*t)[33] = tile[threadIdx.x >> 5];
-    int k = 0;
-#pragma unroll
-    for (int a = 0; a < 6; ++a)
-#pragma unroll
-      for (int b = a; b < 6; ++b) t[k++][lane] = J[a] * J[b];
-#pragma unroll
-    for (int a = 0; a < 6; ++a) t[21 + a][lane] = J[a] * r;
-    t[27][lane] = r * r;
-    t[28][lane] = valid ? 1.0 : 0.0;
+    reinterpret_cast<double2*>(V[lane])[0] = make_double2(J[0], J[1]);
+    reinterpret_cast<double2*>(V[lane])[1] = make_double2(J[2], J[3]);
+    reinterpret_cast<double2*>(V[lane])[2] = make_double2(J[4], J[5]);
+    reinterpret_cast<double2*>(V[lane])[3] = make_double2(r, valid ? 1.0 : 0.0);
     __syncwarp();
-    if (lane < kNE) {
-      double s = 0.0;
-#pragma unroll 8
-      for (int q = 0; q < 32; ++q) s += t[lane][q];
-      acc += s;
+#pragma unroll
+    for (int st = 0; st < 8; ++st) {
+      // A[m][k] = B[k][m] = V[4 st + k][m]; lane holds m = lane >> 2, k = lane & 3
+      const double v = V[4 * st + (lane & 3)][lane >> 2];
+      dmma884(c0, c1, v, v);
     }
     __syncwarp();
     base += 32;
   }
-  // CTA reduction: lane L of every warp holds entry L; sum warps in order
-  __shared__ double sh[kManifoldThreads / 32][32];
-  const int wid = threadIdx.x >> 5;
-  sh[wid][lane] = acc;
-  __syncthreads();
-  if (threadIdx.x < kNE) {
-    double v = 0.0;
-    for (int w = 0; w < kManifoldThreads / 32; ++w) v += sh[w][threadIdx.x];
-    partials[blockIdx.x * kNE + threadIdx.x] = v;
-  }
 }
 
-__global__ void k_reduce_partials(const double* __restrict__ partials, int nblocks,
+// Order-fixed reduction of the per-chunk Gram partials: block (entry, seg)
+// sums a contiguous segment of chunks (fixed per-thread runs, fixed tree),
+// the second pass sums the segments in order.
+constexpr int kRedThreads = 256;
+__global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const double* __restrict__ partials,
+                                                               size_t nchunks, int nseg,
+                                                               double* __restrict__ seg_out) {
+  __shared__ double sh[kRedThreads];
+  const int entry = blockIdx.x, seg = blockIdx.y;
+  const size_t per_seg = (nchunks + nseg - 1) / nseg;
+  const size_t s0 = seg * per_seg, s1 = std::min(nchunks, s0 + per_seg);
+  const double* p = partials + (size_t)entry * nchunks;
+  double v = 0.0;
+  for (size_t c = s0 + threadIdx.x; c < s1; c += kRedThreads) v += p[c];
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = kRedThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) seg_out[(size_t)entry * nseg + seg] = sh[0];
+}
+
+__global__ void k_reduce_segments(const double* __restrict__ seg_out, int nseg,
                                   double* __restrict__ out) {
-  // one warp per component, fixed order -> deterministic
   const int k = blockIdx.x;
   double v = 0.0;
-  for (int b = threadIdx.x; b < nblocks; b += 32) v += partials[b * kNE + k];
+  for (int b = threadIdx.x; b < nseg; b += 32) v += seg_out[(size_t)k * nseg + b];
   v = warp_sum(v);
   if (threadIdx.x == 0) out[k] = v;
 }
@@ -471,8 +507,15 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
   for (int i = 0; i < 9; ++i) pose.R[i] = R[i];
   for (int i = 0; i < 3; ++i) pose.t[i] = t[i];
   const unsigned blocks = grid_for(ctx, n, kManifoldThreads, 4 * TLG_MANIFOLD_MINB);
-  double* partials = ctx->ws<double>(S_PARTIALS, static_cast<size_t>(blocks) * kNE + kNE);
-  double* out = partials + static_cast<size_t>(blocks) * kNE;
+  const size_t nchunks = std::max<size_t>(1, ((n + 31) / 32 + kManifoldChunk - 1) / kManifoldChunk);
+  if (n == 0) {  // no chunk is claimed: the (single) partial slot must read as zero
+    double* p0 = ctx->ws<double>(S_PARTIALS, nchunks * kNE + 2 * kNE);
+    TLG_CUDA(cudaMemsetAsync(p0, 0, nchunks * kNE * sizeof(double), ctx->stream));
+  }
+  const int nseg = static_cast<int>(std::min<size_t>(64, (nchunks + 1023) / 1024));
+  double* partials = ctx->ws<double>(S_PARTIALS, nchunks * kNE + static_cast<size_t>(nseg) * kNE + kNE);
+  double* seg_out = partials + nchunks * kNE;
+  double* out = seg_out + static_cast<size_t>(nseg) * kNE;
   // err[0]: non-finite flag; err[2..3]: 64-bit chunk counter (8-byte aligned)
   int* err = ctx->ws<int>(S_FLAGS, 4);
   TLG_CUDA(cudaMemsetAsync(err, 0, 4 * sizeof(int), ctx->stream));
@@ -483,10 +526,12 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
   TLG_KIND_DISPATCH(sweep_kind(m),
                     (k_manifold<W_><<<blocks, kManifoldThreads, 0, ctx->stream>>>(
                         g, L, pose, hx, hy, hz, n, m->kc.r2, m->kc.neg_inv_2s2, m->kc.inv_s2,
-                        wheel_radius, sl, huber, r, J, valid, raw, partials, err)));
+                        wheel_radius, sl, huber, r, J, valid, raw, partials, nchunks, err)));
   TLG_LAUNCHED(ctx);
   prof_mark_end(ctx);
-  k_reduce_partials<<<kNE, 32, 0, ctx->stream>>>(partials, blocks, out);
+  k_reduce_chunks<<<dim3(kNE, nseg), kRedThreads, 0, ctx->stream>>>(partials, nchunks, nseg, seg_out);
+  TLG_LAUNCHED(ctx);
+  k_reduce_segments<<<kNE, 32, 0, ctx->stream>>>(seg_out, nseg, out);
   TLG_LAUNCHED(ctx);
   double h[kNE + 1];
   TLG_CUDA(cudaMemcpyAsync(h, out, kNE * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
