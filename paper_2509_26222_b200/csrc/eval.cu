@@ -332,7 +332,7 @@ constexpr int kNE = 29;  // 21 (A upper) + 6 (g) + cost + valid
 #define TLG_MANIFOLD_THREADS 128
 #endif
 #ifndef TLG_MANIFOLD_MINB
-#define TLG_MANIFOLD_MINB 4
+#define TLG_MANIFOLD_MINB 3
 #endif
 constexpr int kManifoldThreads = TLG_MANIFOLD_THREADS;
 #ifndef TLG_MANIFOLD_CHUNK
@@ -387,27 +387,37 @@ __global__ void __launch_bounds__(kManifoldThreads, TLG_MANIFOLD_MINB) k_manifol
   // counter: with scan-binned input consecutive iterations hit the same /
   // neighbouring lattice cells, so the weight window stays L1-resident, and
   // dynamic claiming keeps the warps of a CTA finishing together.
+  // The lever arms stream from HBM (cold): the next row-of-32's loads are
+  // issued one iteration ahead, and the next chunk is claimed one chunk ahead
+  // so the prefetch also crosses chunk boundaries.
   const size_t witer = (n + 31) / 32;
-  size_t base = 0, b_end = 0;
-  unsigned long long chunk = 0;
+  auto claim = [&]() {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(reinterpret_cast<unsigned long long*>(err + 2), kManifoldChunk);
+    return __shfl_sync(0xffffffffu, c, 0);
+  };
+  unsigned long long chunk = claim();
+  if (chunk >= witer) return;
+  unsigned long long next = claim();
+  size_t base = static_cast<size_t>(chunk) * 32;
+  size_t b_end = std::min(n, static_cast<size_t>((chunk + kManifoldChunk) * 32));
+  double h0 = 0.0, h1 = 0.0, h2 = 0.0;
+  if (base + lane < n) {
+    h0 = hx[base + lane];
+    h1 = hy[base + lane];
+    h2 = hz[base + lane];
+  }
   for (;;) {
-    if (base >= b_end) {
-      if (b_end != 0) {  // flush the finished chunk's Gram
-        if (e0 >= 0) partials[(size_t)e0 * nchunks + chunk] = c0;
-        if (e1 >= 0) partials[(size_t)e1 * nchunks + chunk] = c1;
-        c0 = c1 = 0.0;
-      }
-      unsigned long long c = 0;
-      if (lane == 0) c = atomicAdd(reinterpret_cast<unsigned long long*>(err + 2), kManifoldChunk);
-      c = __shfl_sync(0xffffffffu, c, 0);
-      if (c >= witer) break;
-      chunk = c / kManifoldChunk;
-      base = static_cast<size_t>(c) * 32;
-      b_end = std::min(n, static_cast<size_t>((c + kManifoldChunk) * 32));
-    }
     const size_t i = base + lane;
     const bool live = i < n;
-    const double h0 = live ? hx[i] : 0.0, h1 = live ? hy[i] : 0.0, h2 = live ? hz[i] : 0.0;
+    size_t pf = base + 32 < b_end ? base + 32 : (next < witer ? static_cast<size_t>(next) * 32 : n);
+    pf += lane;
+    double nh0 = 0.0, nh1 = 0.0, nh2 = 0.0;
+    if (pf < n) {
+      nh0 = hx[pf];
+      nh1 = hy[pf];
+      nh2 = hz[pf];
+    }
     // xi = R h + t (leg_model.cpp:31, contact.cpp:183)
     const double xi0 = fma(R[2], h2, fma(R[1], h1, R[0] * h0)) + pose.t[0];
     const double xi1 = fma(R[5], h2, fma(R[4], h1, R[3] * h0)) + pose.t[1];
@@ -461,7 +471,20 @@ __global__ void __launch_bounds__(kManifoldThreads, TLG_MANIFOLD_MINB) k_manifol
       dmma884(c0, c1, v, v);
     }
     __syncwarp();
+    h0 = nh0;
+    h1 = nh1;
+    h2 = nh2;
     base += 32;
+    if (base >= b_end) {  // chunk done: flush its Gram, move to the pre-claimed one
+      if (e0 >= 0) partials[(size_t)e0 * nchunks + chunk / kManifoldChunk] = c0;
+      if (e1 >= 0) partials[(size_t)e1 * nchunks + chunk / kManifoldChunk] = c1;
+      c0 = c1 = 0.0;
+      if (next >= witer) break;
+      chunk = next;
+      next = claim();
+      base = static_cast<size_t>(chunk) * 32;
+      b_end = std::min(n, static_cast<size_t>((chunk + kManifoldChunk) * 32));
+    }
   }
 }
 
