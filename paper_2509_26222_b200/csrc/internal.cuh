@@ -136,7 +136,11 @@ struct tlg_ctx {
 
   template <typename T>
   T* ws(int slot, size_t count) {
-    return reinterpret_cast<T*>(slots[slot].ensure(count * sizeof(T) + 16));
+    // grow with 25 % headroom: per-scan sizes (n_active, m, nnz) fluctuate, and
+    // every regrowth is a synchronising cudaFree/cudaMalloc pair
+    size_t need = count * sizeof(T) + 16;
+    if (need > slots[slot].n) need += need / 4;
+    return reinterpret_cast<T*>(slots[slot].ensure(need));
   }
   void* host_stage(size_t bytes);
   void sync();
