@@ -202,7 +202,45 @@ def run_update_bench(torch, device, steps=5):
         out[f"m{m}"] = {"ms_per_scan": statistics.median(times), "ms_min": min(times),
                         "n_active": rep.active_centers, "active_blocks": rep.active_blocks,
                         "solver": rep.solver, "rejected": rep.rejected}
+    out["c4"] = run_update_c4(torch, steps)
     return out, model, kernel
+
+
+def run_update_c4(torch, steps=5):
+    """C4: M = 65,536 centres (256 x 256 lattice, bumps terrain, selected from
+    10^6 support points); per-scan update with 20k points in a 2.5 m footprint."""
+    from paper_2509_26222_b200 import terrain as T
+    rng = np.random.default_rng(4)
+    side = 17.85
+    sup = rng.uniform(0.0, side, size=(1_000_000, 2))
+    cs = T.select_centers(T.TerrainObservation(sup, terrain_c5(sup[:, 0], sup[:, 1], np)),
+                          T.Rect((0.0, 0.0), (side, side)), RES, R_A, COUNT)
+    kernel = T.KernelParams()
+    kernel.finalize()
+    model = T.TerrainModel(kernel, cs)
+
+    def scan(cx, cy, m=20000):
+        r = 2.5 * np.sqrt(rng.uniform(0, 1, m))
+        a = rng.uniform(0, 2 * np.pi, m)
+        clean = np.stack([cx + r * np.cos(a), cy + r * np.sin(a)], 1)
+        noisy = clean + rng.normal(0.0, 0.02, size=(m, 2))
+        return T.TerrainObservation(np.ascontiguousarray(noisy),
+                                    terrain_c5(clean[:, 0], clean[:, 1], np))
+
+    scans = [scan(4.0 + 0.5 * k, 8.0 + 0.3 * k) for k in range(steps + 2)]
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    for k, s in enumerate(scans):
+        ev0.record()
+        rep = model.recursive_update(s, False)
+        ev1.record()
+        ev1.synchronize()
+        if k >= 2:
+            times.append(ev0.elapsed_time(ev1))
+    return {"M": model.num_centers(), "m": 20000, "footprint_m": 2.5,
+            "ms_per_scan": statistics.median(times), "ms_min": min(times),
+            "n_active": rep.active_centers, "active_blocks": rep.active_blocks,
+            "solver": rep.solver, "rejected": rep.rejected}
 
 
 def cpu_update_ms(model, kernel, m=400, seed=5):

@@ -236,7 +236,7 @@ __device__ __forceinline__ EvalOut eval_any(const GridView& g, const LatticeView
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(128, 4) k_eval(GridView g, LatticeView L,
+__global__ void __launch_bounds__(128, 3) k_eval(GridView g, LatticeView L,
                                                  const double* __restrict__ x,
                                                  const double* __restrict__ y, size_t n,
                                                  double r2, double neg_inv_2s2, double inv_s2,
@@ -244,22 +244,56 @@ __global__ void __launch_bounds__(128, 4) k_eval(GridView g, LatticeView L,
                                                  uint8_t* __restrict__ sup,
                                                  double* __restrict__ gx,
                                                  double* __restrict__ gy, int* __restrict__ err) {
-  // contiguous chunk per warp (locality of the weight window, see k_manifold)
-  const size_t warps = (size_t)gridDim.x * (blockDim.x >> 5);
-  const size_t per_warp = ((n + 31) / 32 + warps - 1) / warps;
-  const size_t wid_g = (size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const size_t b_end = std::min(n, (wid_g + 1) * per_warp * 32);
-  for (size_t i = wid_g * per_warp * 32 + (threadIdx.x & 31); i < b_end; i += 32) {
-    const double px = x[i], py = y[i];
-    if (!isfinite(px) || !isfinite(py)) {
-      atomicOr(err, 1);
-      continue;
+  // Same schedule as k_manifold: warps claim chunks of 8 rows-of-32 (err[2..3]
+  // is the counter), the next row's query is loaded one iteration ahead.
+  constexpr unsigned long long kChunk = 8;
+  const int lane = threadIdx.x & 31;
+  const size_t witer = (n + 31) / 32;
+  auto claim = [&]() {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(reinterpret_cast<unsigned long long*>(err + 2), kChunk);
+    return __shfl_sync(0xffffffffu, c, 0);
+  };
+  unsigned long long chunk = claim();
+  if (chunk >= witer) return;
+  unsigned long long next = claim();
+  size_t base = static_cast<size_t>(chunk) * 32;
+  size_t b_end = std::min(n, static_cast<size_t>((chunk + kChunk) * 32));
+  double px = 0.0, py = 0.0;
+  if (base + lane < n) {
+    px = x[base + lane];
+    py = y[base + lane];
+  }
+  for (;;) {
+    const size_t i = base + lane;
+    size_t pf = base + 32 < b_end ? base + 32 : (next < witer ? static_cast<size_t>(next) * 32 : n);
+    pf += lane;
+    double nx = 0.0, ny = 0.0;
+    if (pf < n) {
+      nx = x[pf];
+      ny = y[pf];
     }
-    const EvalOut o = eval_any<KIND>(g, L, px, py, r2, neg_inv_2s2);
-    if (z) z[i] = o.sup ? o.z : 0.0;
-    if (sup) sup[i] = o.sup ? 1 : 0;
-    if (gx) gx[i] = o.sx * inv_s2;
-    if (gy) gy[i] = o.sy * inv_s2;
+    if (i < n) {
+      if (!isfinite(px) || !isfinite(py)) {
+        atomicOr(err, 1);
+      } else {
+        const EvalOut o = eval_any<KIND>(g, L, px, py, r2, neg_inv_2s2);
+        if (z) z[i] = o.sup ? o.z : 0.0;
+        if (sup) sup[i] = o.sup ? 1 : 0;
+        if (gx) gx[i] = o.sx * inv_s2;
+        if (gy) gy[i] = o.sy * inv_s2;
+      }
+    }
+    px = nx;
+    py = ny;
+    base += 32;
+    if (base >= b_end) {
+      if (next >= witer) break;
+      chunk = next;
+      next = claim();
+      base = static_cast<size_t>(chunk) * 32;
+      b_end = std::min(n, static_cast<size_t>((chunk + kChunk) * 32));
+    }
   }
 }
 
@@ -304,13 +338,13 @@ void eval_device(tlg_model* m, const double* x, const double* y, size_t n, doubl
   tlg_ctx* ctx = m->ctx;
   ensure_grid(m);
   int* err = ctx->ws<int>(S_FLAGS, 4);
-  TLG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
+  TLG_CUDA(cudaMemsetAsync(err, 0, 4 * sizeof(int), ctx->stream));
   if (n) {
     const GridView g = grid_view(m);
     const LatticeView L = lattice_view(m);
     prof_begin(ctx, 1);
     TLG_KIND_DISPATCH(sweep_kind(m),
-                      (k_eval<W_><<<grid_for(ctx, n, 128, 16), 128, 0, ctx->stream>>>(
+                      (k_eval<W_><<<grid_for(ctx, n, 128, 3), 128, 0, ctx->stream>>>(
                           g, L, x, y, n, m->kc.r2, m->kc.neg_inv_2s2, m->kc.inv_s2, z, sup, gx,
                           gy, err)));
     TLG_LAUNCHED(ctx);
@@ -529,7 +563,7 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
   Pose pose;
   for (int i = 0; i < 9; ++i) pose.R[i] = R[i];
   for (int i = 0; i < 3; ++i) pose.t[i] = t[i];
-  const unsigned blocks = grid_for(ctx, n, kManifoldThreads, 4 * TLG_MANIFOLD_MINB);
+  const unsigned blocks = grid_for(ctx, n, kManifoldThreads, TLG_MANIFOLD_MINB);
   const size_t nchunks = std::max<size_t>(1, ((n + 31) / 32 + kManifoldChunk - 1) / kManifoldChunk);
   if (n == 0) {  // no chunk is claimed: the (single) partial slot must read as zero
     double* p0 = ctx->ws<double>(S_PARTIALS, nchunks * kNE + 2 * kNE);

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--points", type=int, default=10_000_000)
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--unbinned", action="store_true")
+    ap.add_argument("--eval", action="store_true")
     a = ap.parse_args()
     model, kernel, cs, w, R, tv, h = bench.build_c5(0, a.points, 7, torch)
     n = a.points
@@ -49,6 +50,19 @@ def main():
     print(f"{os.environ.get('TLG_LIB_OVERRIDE', 'default')}: k_manifold {k:.4f} ms  "
           f"{n / k / 1e6:.3f} Gpts/s  {81 * n / (k * 1e-3) / 1e9:.1f} GB/s  cost={ne.cost:.6g}",
           flush=True)
+    if a.eval:
+        # K3 batch predict (height + gradient + supported) on the same points
+        # in scan order (binned) and in generation order
+        xy = torch.stack([h[0], h[1]], 1).contiguous()
+        for label, q in (("random order", xy),):
+            model.predict(q)
+            lib.tlg_ctx_set_profiling(ctx.handle, 1)
+            for _ in range(a.iters):
+                model.predict(q)
+            lib.tlg_ctx_kernel_stats(ctx.handle, 1, C.byref(ms), C.byref(cnt))
+            k = ms.value / cnt.value
+            print(f"k_eval ({label}): {k:.4f} ms  {n / k / 1e6:.3f} Gpts/s  "
+                  f"{41 * n / (k * 1e-3) / 1e9:.1f} GB/s", flush=True)
 
 
 if __name__ == "__main__":
