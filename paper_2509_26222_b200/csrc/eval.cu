@@ -522,36 +522,31 @@ __global__ void __launch_bounds__(kManifoldThreads, TLG_MANIFOLD_MINB) k_manifol
   }
 }
 
-// Order-fixed reduction of the per-chunk Gram partials: block (entry, seg)
-// sums a contiguous segment of chunks (fixed per-thread runs, fixed tree),
-// the second pass sums the segments in order.
+// Order-fixed reduction of the per-chunk Gram partials: block `entry` sums
+// all chunks (thread t a contiguous run, then a fixed tree); block 0 also
+// appends the non-finite flag, so one D2H copy returns everything.
 constexpr int kRedThreads = 256;
 __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const double* __restrict__ partials,
-                                                               size_t nchunks, int nseg,
-                                                               double* __restrict__ seg_out) {
+                                                               size_t nchunks,
+                                                               const int* __restrict__ err,
+                                                               double* __restrict__ out) {
   __shared__ double sh[kRedThreads];
-  const int entry = blockIdx.x, seg = blockIdx.y;
-  const size_t per_seg = (nchunks + nseg - 1) / nseg;
-  const size_t s0 = seg * per_seg, s1 = std::min(nchunks, s0 + per_seg);
+  const int entry = blockIdx.x;
+  const size_t per = (nchunks + kRedThreads - 1) / kRedThreads;
+  const size_t c0 = threadIdx.x * per, c1 = std::min(nchunks, c0 + per);
   const double* p = partials + (size_t)entry * nchunks;
   double v = 0.0;
-  for (size_t c = s0 + threadIdx.x; c < s1; c += kRedThreads) v += p[c];
+  for (size_t c = c0; c < c1; ++c) v += p[c];
   sh[threadIdx.x] = v;
   __syncthreads();
   for (int o = kRedThreads / 2; o > 0; o >>= 1) {
     if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) seg_out[(size_t)entry * nseg + seg] = sh[0];
-}
-
-__global__ void k_reduce_segments(const double* __restrict__ seg_out, int nseg,
-                                  double* __restrict__ out) {
-  const int k = blockIdx.x;
-  double v = 0.0;
-  for (int b = threadIdx.x; b < nseg; b += 32) v += seg_out[(size_t)k * nseg + b];
-  v = warp_sum(v);
-  if (threadIdx.x == 0) out[k] = v;
+  if (threadIdx.x == 0) {
+    out[entry] = sh[0];
+    if (entry == 0) out[kNE] = err[0] ? 1.0 : 0.0;
+  }
 }
 
 void manifold_device(tlg_model* m, const double R[9], const double t[3], const double* hx,
@@ -569,12 +564,11 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
     double* p0 = ctx->ws<double>(S_PARTIALS, nchunks * kNE + 2 * kNE);
     TLG_CUDA(cudaMemsetAsync(p0, 0, nchunks * kNE * sizeof(double), ctx->stream));
   }
-  const int nseg = static_cast<int>(std::min<size_t>(64, (nchunks + 1023) / 1024));
-  double* partials = ctx->ws<double>(S_PARTIALS, nchunks * kNE + static_cast<size_t>(nseg) * kNE + kNE);
-  double* seg_out = partials + nchunks * kNE;
-  double* out = seg_out + static_cast<size_t>(nseg) * kNE;
+  double* partials = ctx->ws<double>(S_PARTIALS, nchunks * kNE + kNE + 1);
+  double* out = partials + nchunks * kNE;
   // err[0]: non-finite flag; err[2..3]: 64-bit chunk counter (8-byte aligned)
   int* err = ctx->ws<int>(S_FLAGS, 4);
+  double* h = static_cast<double*>(ctx->host_stage((kNE + 1) * sizeof(double)));  // pinned
   TLG_CUDA(cudaMemsetAsync(err, 0, 4 * sizeof(int), ctx->stream));
   const GridView g = grid_view(m);
   const LatticeView L = lattice_view(m);
@@ -586,18 +580,12 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
                         wheel_radius, sl, huber, r, J, valid, raw, partials, nchunks, err)));
   TLG_LAUNCHED(ctx);
   prof_mark_end(ctx);
-  k_reduce_chunks<<<dim3(kNE, nseg), kRedThreads, 0, ctx->stream>>>(partials, nchunks, nseg, seg_out);
+  k_reduce_chunks<<<kNE, kRedThreads, 0, ctx->stream>>>(partials, nchunks, err, out);
   TLG_LAUNCHED(ctx);
-  k_reduce_segments<<<kNE, 32, 0, ctx->stream>>>(seg_out, nseg, out);
-  TLG_LAUNCHED(ctx);
-  double h[kNE + 1];
-  TLG_CUDA(cudaMemcpyAsync(h, out, kNE * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-  TLG_CUDA(cudaMemcpyAsync(&h[kNE], err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TLG_CUDA(cudaMemcpyAsync(h, out, (kNE + 1) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   TLG_CUDA(cudaStreamSynchronize(ctx->stream));
   prof_collect(ctx);
-  int e = 0;
-  std::memcpy(&e, &h[kNE], sizeof(int));
-  if (e) throw Error(TLG_DOMAIN_ERROR, "non-finite query");
+  if (h[kNE] != 0.0) throw Error(TLG_DOMAIN_ERROR, "non-finite query");
   if (ne) {
     for (int k = 0; k < 21; ++k) ne->A[k] = h[k];
     for (int k = 0; k < 6; ++k) ne->g[k] = h[21 + k];
