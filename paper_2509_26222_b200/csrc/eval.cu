@@ -30,6 +30,7 @@
 //     entry L; one partial per CTA, then a fixed-order final reduction
 //     (deterministic, no FP64 atomics).
 #include <cmath>
+#include <math_constants.h>
 #include <type_traits>
 
 #include "internal.cuh"
@@ -96,21 +97,23 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
   // Row factors. dy^2 is kept exact for the boundary tests; e_y follows the
   // lattice recurrence e(l+1) = e(l) p(l), p(l+1) = p(l) exp(2 c res^2)
   // (c = -1/(2 s^2)), two exps per axis instead of WIN.
+  // dy2 carries the reference's cell-window test too: a row outside the
+  // (2 span + 1)^2 cell sweep gets dy2 = +inf, so its boundary tests fail
+  // without a per-pair predicate (inside pairs never need it, by their margin).
   double ey[WIN], eyd[WIN], dy2[WIN];
-  uint32_t rowok = 0;
 #pragma unroll
   for (int l = 0; l < WIN; ++l) {
-    const double dy = __dsub_rn(__ldg(L.cyl + j0 + l), y);
-    dy2[l] = __dmul_rn(dy, dy);
+    const AxisNode a = L.ay[j0 + l];
+    const double dy = __dsub_rn(a.c, y);
+    dy2[l] = abs(a.cell - qy) <= L.span ? __dmul_rn(dy, dy) : CUDART_INF;
     eyd[l] = dy;
-    rowok |= static_cast<uint32_t>(abs(__ldg(L.ccy + j0 + l) - qy) <= L.span) << l;
   }
   // compiled geometries are only dispatched when the recurrence is safe
   // (sweep_kind), so their code carries no per-node exp fallback
   constexpr bool kRecAlways = G >= 0;
   const bool rec = kRecAlways || L.rec_ok;
   if (rec) {
-    double e = exp(dy2[0] * neg_inv_2b2);
+    double e = exp(__dmul_rn(eyd[0], eyd[0]) * neg_inv_2b2);
     double p = exp(L.c_res * fma(2.0, eyd[0], L.res));
 #pragma unroll
     for (int l = 0; l < WIN; ++l) {
@@ -120,12 +123,13 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
     }
   } else if constexpr (!kRecAlways) {
 #pragma unroll
-    for (int l = 0; l < WIN; ++l) ey[l] = exp(dy2[l] * neg_inv_2b2);
+    for (int l = 0; l < WIN; ++l) ey[l] = exp(__dmul_rn(eyd[l], eyd[l]) * neg_inv_2b2);
   }
 #pragma unroll
   for (int l = 0; l < WIN; ++l) eyd[l] *= ey[l];
   const double* wbase = L.W + static_cast<size_t>(i0) * L.nj + j0;
-  const double dx_first = __dsub_rn(__ldg(L.cxl + i0), x);
+  const AxisNode a0 = L.ax[i0];
+  const double dx_first = __dsub_rn(a0.c, x);
   double ex_e = 0.0, ex_p = 0.0;
   if (rec) {
     ex_e = exp(__dmul_rn(dx_first, dx_first) * neg_inv_2b2);
@@ -138,9 +142,10 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
     // being hoisted here (they would need ~2 registers each and spill)
     if constexpr (k % TLG_COL_FENCE == 0) asm volatile("" ::: "memory");
 #endif
-    const double dx = k == 0 ? dx_first : __dsub_rn(__ldg(L.cxl + i0 + k), x);
-    const double dx2 = __dmul_rn(dx, dx);
-    const bool colok = abs(__ldg(L.ccx + i0 + k) - qx) <= L.span;
+    const AxisNode a = k == 0 ? a0 : L.ax[i0 + k];
+    const double dx = k == 0 ? dx_first : __dsub_rn(a.c, x);
+    const double dxx = __dmul_rn(dx, dx);
+    const double dx2 = abs(a.cell - qx) <= L.span ? dxx : CUDART_INF;  // see dy2
     const double* wc = wbase + static_cast<size_t>(k) * L.nj;
     double S = 0.0, T = 0.0;
     bool any;
@@ -155,10 +160,17 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
           S = fma(w, ey[l], S);
           T = fma(w, eyd[l], T);
         } else if constexpr ((bm >> l) & 1u) {
-          const bool in = colok && ((rowok >> l) & 1u) && __dadd_rn(dx2, dy2[l]) <= r2;
-          const double w = in ? __ldg(wc + l) : 0.0;
+#ifdef TLG_BD_BRANCH
+          if (__dadd_rn(dx2, dy2[l]) <= r2) {
+            const double w = __ldg(wc + l);
+            S = fma(w, ey[l], S);
+            T = fma(w, eyd[l], T);
+          }
+#else
+          const double w = __dadd_rn(dx2, dy2[l]) <= r2 ? __ldg(wc + l) : 0.0;
           S = fma(w, ey[l], S);
           T = fma(w, eyd[l], T);
+#endif
         }
       });
       any = (im | bm) != 0;
@@ -171,10 +183,11 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
           S = fma(w, ey[l], S);
           T = fma(w, eyd[l], T);
         } else if ((bm >> l) & 1u) {
-          const bool in = colok && ((rowok >> l) & 1u) && __dadd_rn(dx2, dy2[l]) <= r2;
-          const double w = in ? __ldg(wc + l) : 0.0;
-          S = fma(w, ey[l], S);
-          T = fma(w, eyd[l], T);
+          if (__dadd_rn(dx2, dy2[l]) <= r2) {
+            const double w = __ldg(wc + l);
+            S = fma(w, ey[l], S);
+            T = fma(w, eyd[l], T);
+          }
         }
       }
       any = (im | bm) != 0;
@@ -184,7 +197,7 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
       ex_e *= ex_p;
       ex_p *= L.k2;
     } else if constexpr (!kRecAlways) {
-      ex = exp(dx2 * neg_inv_2b2);
+      ex = exp(dxx * neg_inv_2b2);
     }
     if (any) {
       o.z = fma(ex, S, o.z);
@@ -202,14 +215,16 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
   }
   if (!sup) {
     for (int k = 0; k < WIN && !sup; ++k) {
-      const double dx = __dsub_rn(__ldg(L.cxl + i0 + k), x);
+      const AxisNode ak = L.ax[i0 + k];
+      const double dx = __dsub_rn(ak.c, x);
       const double dx2 = __dmul_rn(dx, dx);
-      const bool colok = abs(__ldg(L.ccx + i0 + k) - qx) <= L.span;
+      const bool colok = abs(ak.cell - qx) <= L.span;
       const int* pc = L.P + static_cast<size_t>(i0 + k) * L.nj + j0;
       for (int l = 0; l < WIN; ++l) {
-        const double dy = __dsub_rn(__ldg(L.cyl + j0 + l), y);
+        const AxisNode al = L.ay[j0 + l];
+        const double dy = __dsub_rn(al.c, y);
         const bool in = ((L.inmask[k] >> l) & 1u) ||
-                        (((L.bdmask[k] >> l) & 1u) && colok && ((rowok >> l) & 1u) &&
+                        (((L.bdmask[k] >> l) & 1u) && colok && abs(al.cell - qy) <= L.span &&
                          __dadd_rn(dx2, __dmul_rn(dy, dy)) <= r2);
         if (in && __ldg(pc + l)) {
           sup = true;

@@ -111,12 +111,11 @@ __global__ void k_lattice_fill(const double* __restrict__ cx, const double* __re
 }
 
 __global__ void k_lattice_axes(double min_v, double res, int org, int count, double cell,
-                               double* __restrict__ coord, int* __restrict__ cc) {
+                               AxisNode* __restrict__ ax) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= count) return;
   const double v = __dadd_rn(min_v, __dmul_rn(static_cast<double>(k + org), res));
-  coord[k] = v;
-  cc[k] = static_cast<int>(floor(v / cell));
+  ax[k] = AxisNode{v, static_cast<int>(floor(v / cell)), 0};
 }
 
 __global__ void k_lattice_refresh(const int* __restrict__ slot, const double* __restrict__ w,
@@ -185,14 +184,12 @@ static void build_lattice(tlg_model* m) {
   k_lattice_fill<<<blocks, 256, 0, s>>>(m->cx.p, m->cy.p, m->w.p, n, mnx, mny, res, L.i_org,
                                         L.j_org, L.nj, L.W.p, L.P.p, L.slot.p, dup);
   TLG_LAUNCHED(ctx);
-  L.cxl.ensure(L.ni);
-  L.cyl.ensure(L.nj);
-  L.ccx.ensure(L.ni);
-  L.ccy.ensure(L.nj);
+  L.ax.ensure(L.ni);
+  L.ay.ensure(L.nj);
   const double cell = m->grid.cell;
-  k_lattice_axes<<<(L.ni + 127) / 128, 128, 0, s>>>(mnx, res, L.i_org, L.ni, cell, L.cxl.p, L.ccx.p);
+  k_lattice_axes<<<(L.ni + 127) / 128, 128, 0, s>>>(mnx, res, L.i_org, L.ni, cell, L.ax.p);
   TLG_LAUNCHED(ctx);
-  k_lattice_axes<<<(L.nj + 127) / 128, 128, 0, s>>>(mny, res, L.j_org, L.nj, cell, L.cyl.p, L.ccy.p);
+  k_lattice_axes<<<(L.nj + 127) / 128, 128, 0, s>>>(mny, res, L.j_org, L.nj, cell, L.ay.p);
   TLG_LAUNCHED(ctx);
   int hd = 0;
   TLG_CUDA(cudaMemcpyAsync(&hd, dup, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -209,10 +206,8 @@ LatticeView lattice_view(const tlg_model* m) {
   LatticeView v;
   v.W = L.W.p;
   v.P = L.P.p;
-  v.cxl = L.cxl.p;
-  v.cyl = L.cyl.p;
-  v.ccx = L.ccx.p;
-  v.ccy = L.ccy.p;
+  v.ax = L.ax.p;
+  v.ay = L.ay.p;
   v.ni = L.ni;
   v.nj = L.nj;
   v.lo = L.lo;

@@ -267,6 +267,12 @@ inline bool geom_equal(const Geom& a, const Geom& b) {
   return true;
 }
 
+struct __align__(16) AxisNode {
+  double c;  // node coordinate min + k * res (reference rounding)
+  int cell;  // floor(c / cell)
+  int pad;
+};
+
 struct LatticeGrid {
   bool valid = false;
   int win = 0, lo = 0, pad = 0;
@@ -279,18 +285,16 @@ struct LatticeGrid {
   int geom_id = -1;            // index into kGeoms when specialised, else -1
   DBuf<double> W;
   DBuf<int> P;                 // presence count per node
-  DBuf<double> cxl, cyl;       // exact node coordinate per padded column / row
-  DBuf<int> ccx, ccy;          // reference cell coordinate floor(c / cell)
+  DBuf<AxisNode> ax, ay;       // per padded column / row: exact node coordinate
+                               // and reference cell coordinate floor(c / cell)
   DBuf<int> slot;              // centre id -> node index in W
 };
 
 struct LatticeView {
   const double* W;
   const int* P;
-  const double* cxl;
-  const double* cyl;
-  const int* ccx;
-  const int* ccy;
+  const AxisNode* ax;  // one 16-byte load gives coordinate + cell
+  const AxisNode* ay;
   int ni, nj, lo, span;
   double org_x, org_y, inv_res, cell;
   uint32_t inmask[16], bdmask[16];
