@@ -144,6 +144,10 @@ tlg_status tlg_model_create(tlg_ctx* ctx, const tlg_kernel_params* kernel,
                             const double* cy, size_t n, tlg_mem mem, tlg_model** out);
 tlg_status tlg_model_destroy(tlg_model* model);
 tlg_status tlg_model_counts(const tlg_model* model, size_t* num_centers, size_t* num_blocks);
+/* Diagnostics: which evaluation sweep the model's centres select — 0 generic
+ * hash-grid sweep, 4..14 lattice window with runtime pair classes, 100 + g
+ * compiled geometry g — and whether the separable exp recurrence is used. */
+tlg_status tlg_model_sweep(tlg_model* model, int* kind, int* exp_recurrence);
 tlg_status tlg_model_kernel(const tlg_model* model, tlg_kernel_params* out);
 tlg_status tlg_model_center_params(const tlg_model* model, tlg_center_params* out);
 tlg_status tlg_model_get_centers(tlg_model* model, double* cx, double* cy, tlg_mem mem);

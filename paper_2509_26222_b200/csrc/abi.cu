@@ -292,6 +292,15 @@ tlg_status tlg_model_counts(const tlg_model* m, size_t* nc, size_t* nb) {
   });
 }
 
+tlg_status tlg_model_sweep(tlg_model* m, int* kind, int* exp_recurrence) {
+  return guard([&] {
+    check_ptr(m, "model");
+    ensure_grid(m);
+    if (kind) *kind = sweep_kind(m);
+    if (exp_recurrence) *exp_recurrence = m->lat.valid ? lattice_view(m).rec_ok : 0;
+  });
+}
+
 tlg_status tlg_model_kernel(const tlg_model* m, tlg_kernel_params* out) {
   return guard([&] {
     check_ptr(m, "model");

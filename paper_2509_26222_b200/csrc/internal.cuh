@@ -355,6 +355,7 @@ void build_center_grid(tlg_model* m);      // grid.cu
 GridView grid_view(const tlg_model* m);    // grid.cu
 LatticeView lattice_view(const tlg_model* m);
 void ensure_grid(tlg_model* m);
+int sweep_kind(const tlg_model* m);  // eval.cu
 void sync_weights_to_grid(tlg_model* m);   // after weights change
 
 // blocks / pool (model.cu)

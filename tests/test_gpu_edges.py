@@ -1,0 +1,130 @@
+"""Edge cases of the lattice sweep and the manifold-row reduction against the
+CPU oracle: queries exactly on / one ulp around the reference's hash-cell
+boundaries (the 3x3 cell window is part of the reference's membership rule,
+grid_index.hpp:32-48), a geometry that is not compiled in (runtime pair
+classes), parameters where the separable exp recurrence is disabled, row
+counts that are not multiples of a warp, empty scans and non-finite lever
+arms."""
+import numpy as np
+import pytest
+
+import oracle as orc
+from helpers import assert_values_close, scales, so3_exp, uniform_xy
+from paper_2509_26222_b200 import kinematics as kin
+from paper_2509_26222_b200 import terrain as T
+
+pytestmark = pytest.mark.gpu
+
+
+def _lattice_model(sigma=0.04, sigma_eps=0.1, mesh=0.07, side=1.05, seed=61):
+    k = T.KernelParams(sigma=sigma, sigma_eps=sigma_eps)
+    k.finalize()
+    roi = T.Rect((0.0, 0.0), (side, side))
+    n = int(round(side / mesh))
+    ii, jj = np.meshgrid(np.arange(n + 1), np.arange(n + 1), indexing="ij")
+    nodes = np.stack([0.0 + ii.ravel() * mesh, 0.0 + jj.ravel() * mesh], 1)
+    nodes = nodes[(nodes[:, 0] <= side) & (nodes[:, 1] <= side)]
+    cs = T.CenterSet(nodes, mesh, 0.12, 3, roi)
+    g, o = T.TerrainModel(k, cs), orc.Model(k, cs)
+    w = np.cos(np.arange(len(nodes)) * 0.53 + seed)
+    g.set_weights(w)
+    o.set_weights(w)
+    return k, cs, g, o
+
+
+def _sweep(g):
+    import ctypes as C
+    from paper_2509_26222_b200 import _abi
+    kind, rec = C.c_int(), C.c_int()
+    _abi.check(_abi.load().tlg_model_sweep(g.handle, C.byref(kind), C.byref(rec)))
+    return kind.value, rec.value
+
+
+def _check_predict(k, g, o, q):
+    z, s, gx, gy = g.predict(q)
+    zr, sr, gxr, gyr = o.predict(q)
+    assert np.array_equal(s, sr)
+    hs, gs = scales(o, q, k.sigma)
+    assert_values_close(z, zr, hs, what="height")
+    assert_values_close(gx, gxr, gs, what="gx")
+    assert_values_close(gy, gyr, gs, what="gy")
+
+
+def test_queries_on_hash_cell_boundaries(gpu_ctx):
+    k, cs, g, o = _lattice_model()
+    assert _sweep(g) == (100, 1)  # compiled paper geometry
+    cell = k.cutoff_radius  # GridIndex2 cell = min(cutoff, 1e6)
+    edges = np.arange(-1, int(1.05 / cell) + 2) * cell
+    vals = np.concatenate([edges, np.nextafter(edges, -np.inf), np.nextafter(edges, np.inf)])
+    rng = np.random.default_rng(5)
+    q = np.stack([rng.choice(vals, 6000), rng.uniform(-0.1, 1.15, 6000)], 1)
+    q = np.concatenate([q, q[:, ::-1], np.stack([rng.choice(vals, 3000), rng.choice(vals, 3000)], 1)])
+    _check_predict(k, g, o, q)
+
+
+def test_runtime_geometry_not_compiled(gpu_ctx):
+    # mesh 0.05 -> cutoff / res = 6.46 lattice units: runtime pair classes
+    k, cs, g, o = _lattice_model(mesh=0.05, side=1.0)
+    kind, rec = _sweep(g)
+    assert 4 <= kind <= 14 and rec == 1
+    q = uniform_xy(orc.Rng(71), 4000, -0.2, 1.2)
+    _check_predict(k, g, o, q)
+
+
+def test_exp_recurrence_disabled(gpu_ctx):
+    # sigma << sigma~ (cutoff 3 sigma~ spans ~30 sigma): the exponent range over
+    # the window is too wide for the two-multiply recurrence -> one exp per node
+    k, cs, g, o = _lattice_model(sigma=0.01, sigma_eps=0.1)
+    kind, rec = _sweep(g)
+    assert 4 <= kind <= 14 and rec == 0
+    q = uniform_xy(orc.Rng(72), 3000, -0.05, 1.1)
+    _check_predict(k, g, o, q)
+
+
+@pytest.mark.parametrize("n", [1, 31, 33, 257, 4099])
+def test_manifold_rows_ragged_sizes(gpu_ctx, n):
+    k, cs, g, o = _lattice_model(seed=n)
+    R = so3_exp([0.01, -0.02, 0.3])
+    t = np.array([0.05, 0.02, 0.1])
+    pts = np.concatenate([uniform_xy(orc.Rng(n), n, -0.05, 1.1), np.full((n, 1), 0.03)], 1)
+    h = (pts - t) @ R
+    rows, ne = kin.manifold_rows(g, R, t, h, 0.0, 1.0, 0.05, want=("r", "J", "valid"))
+    ref, ne_ref = o.manifold_rows(R, t, h, 0.0, 1.0, 0.05)
+    assert np.array_equal(rows["valid"], ref["valid"])
+    A = ne.A[np.triu_indices(6)]
+    scale = max(np.abs(ne_ref[:21]).max(), 1e-300)
+    np.testing.assert_allclose(A, ne_ref[:21], rtol=1e-9, atol=1e-9 * scale)
+    assert ne.valid == int(ne_ref[28])
+    sc = kin.Scan(g, R, t, h)
+    srows, sne = sc.manifold_rows(R, t, 0.0, 1.0, 0.05)
+    perm = sc.permutation()
+    assert np.array_equal(srows["valid"], rows["valid"][perm])
+    np.testing.assert_allclose(sne.A, ne.A, rtol=1e-12, atol=1e-12 * scale)
+
+
+def test_manifold_rows_empty_and_nonfinite(gpu_ctx):
+    k, cs, g, o = _lattice_model()
+    R = np.eye(3)
+    t = np.zeros(3)
+    rows, ne = kin.manifold_rows(g, R, t, np.zeros((0, 3)), 0.0, 1.0, 0.05)
+    assert ne.valid == 0 and ne.cost == 0.0 and np.all(ne.A == 0.0)
+    h = np.array([[0.5, 0.5, 0.0], [np.nan, 0.2, 0.0]])
+    with pytest.raises(T.DomainError):
+        kin.manifold_rows(g, R, t, h, 0.0, 1.0, 0.05)
+    # the model stays usable after the error
+    rows, ne = kin.manifold_rows(g, R, t, h[:1], 0.0, 1.0, 0.05)
+    assert ne.valid == 1
+
+
+def test_manifold_rows_deterministic(gpu_ctx):
+    # dynamic chunk claiming must not change the reduction order
+    k, cs, g, o = _lattice_model()
+    R = so3_exp([0.0, 0.0, 0.2])
+    t = np.array([0.0, 0.0, 0.1])
+    pts = np.concatenate([uniform_xy(orc.Rng(9), 200000, 0.0, 1.05), np.zeros((200000, 1))], 1)
+    h = (pts - t) @ R
+    ne0 = kin.manifold_rows(g, R, t, h, 0.0, 1.0, 0.05, want=())[1]
+    for _ in range(3):
+        ne1 = kin.manifold_rows(g, R, t, h, 0.0, 1.0, 0.05, want=())[1]
+        assert np.array_equal(ne1.A, ne0.A) and np.array_equal(ne1.g, ne0.g)
+        assert ne1.cost == ne0.cost
