@@ -115,6 +115,27 @@ tlg_status tlg_debug_dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps
 tlg_status tlg_debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, int band, double* L,
                            double* X);
 
+/* ---- Batch-predict consumers ------------------------------ */
+/* select_ground_points (pipeline.cpp:150-170): points p (sensor frame, SoA)
+ * with FeatureKind codes kind (2 = Ground), pose R (row-major) / t; keeps, in
+ * scan order, ground points whose world xy lies in [roi_min, roi_max], within
+ * ground_radius of t_xy, first in their xy voxel (ground_voxel); at most
+ * max_points. out_x/out_y/out_z need max_points capacity; *out_n = kept. */
+tlg_status tlg_select_ground_points(tlg_ctx* ctx, const double* px, const double* py,
+                                    const double* pz, const uint8_t* kind, size_t n,
+                                    tlg_mem in_mem, const double R[9], const double t[3],
+                                    const double roi_min[2], const double roi_max[2],
+                                    double ground_radius, double ground_voxel,
+                                    size_t max_points, double* out_x, double* out_y,
+                                    double* out_z, tlg_mem out_mem, size_t* out_n);
+/* terrain_error_histogram (metrics.cpp:199-232): errors |z - f(x, y)| (0.25 m
+ * where unsupported), top floor(trim_fraction n) dropped, bins over
+ * [0, 0.25]: edges[bins + 1], counts[bins], trimmed, overflow (host). */
+tlg_status tlg_terrain_error_histogram(tlg_model* model, const double* x, const double* y,
+                                       const double* z, size_t n, tlg_mem mem,
+                                       double trim_fraction, int bins, double* edges,
+                                       uint64_t* counts, uint64_t* trimmed, uint64_t* overflow);
+
 /* ---- kernel.cpp ------------------------------------------------------------- */
 /* KernelParams::finalize (kernel.cpp:15-25): fills the auto cutoff, validates. */
 tlg_status tlg_kernel_finalize(tlg_kernel_params* p);

@@ -102,6 +102,16 @@ def load():
                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
         _lib.orc_lm_step.argtypes = [C.c_void_p, C.c_double, C.c_void_p]
         _lib.orc_so3_exp.argtypes = [C.c_void_p, C.c_void_p]
+        _lib.orc_select_ground_points.argtypes = [
+            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
+            C.c_void_p, C.c_double, C.c_double, C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p,
+            C.c_void_p]
+        _lib.orc_terrain_error_histogram.argtypes = [
+            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_double, C.c_int,
+            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.orc_export_grid.restype = C.c_size_t
+        _lib.orc_export_grid.argtypes = [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_size_t]
     return _lib
 
 
@@ -317,6 +327,27 @@ class Model:
         _chk(load().orc_model_load(str(path).encode(), C.byref(h)))
         return Model(_h=h)
 
+    def error_histogram(self, xy, z, trim_fraction=0.0, bins=25):
+        """metrics.cpp:199-232 restated: dict(edges, counts, trimmed, overflow)."""
+        xy = _f64(xy)
+        z = _f64(z)
+        x, y = np.ascontiguousarray(xy[:, 0]), np.ascontiguousarray(xy[:, 1])
+        edges = np.empty(bins + 1)
+        counts = np.zeros(bins, dtype=np.uint64)
+        tr, ov = C.c_ulonglong(), C.c_ulonglong()
+        _chk(load().orc_terrain_error_histogram(self.h, _p(x), _p(y), _p(z), len(z),
+                                                float(trim_fraction), int(bins), _p(edges),
+                                                _p(counts), C.byref(tr), C.byref(ov)))
+        return {"edges": edges, "counts": counts, "trimmed": tr.value, "overflow": ov.value}
+
+    def export_grid(self, grid_step):
+        """terrain_model.cpp:255-267 restated: supported grid points and heights."""
+        cap = 1 << 22
+        x, y, z = np.empty(cap), np.empty(cap), np.empty(cap)
+        n = load().orc_export_grid(self.h, float(grid_step), _p(x), _p(y), _p(z), cap)
+        assert n <= cap
+        return x[:n].copy(), y[:n].copy(), z[:n].copy()
+
     def manifold_rows(self, R, t, h, wheel_radius=0.0, lambda_M=1.0, huber=0.05, threads=1):
         Rm, tv = _f64(R).reshape(9), _f64(t).reshape(3)
         ha = _f64(h).reshape(-1, 3)
@@ -328,6 +359,24 @@ class Model:
                                       wheel_radius, lambda_M, huber, _p(r), _p(J), _p(v), _p(raw),
                                       _p(ne), threads))
         return dict(r=r, J=J.reshape(n, 6), valid=v, raw=raw), ne
+
+
+def select_ground_points(p, kind, R, t, roi, radius, voxel, max_points):
+    """pipeline.cpp:150-170 restated (oracle)."""
+    p = np.ascontiguousarray(np.asarray(p, dtype=np.float64))
+    px, py, pz = (np.ascontiguousarray(p[:, j]) for j in range(3))
+    kind = np.ascontiguousarray(np.asarray(kind, dtype=np.uint8))
+    Rm = np.ascontiguousarray(np.asarray(R, dtype=np.float64).reshape(9))
+    tv = np.ascontiguousarray(np.asarray(t, dtype=np.float64).reshape(3))
+    r4 = np.array([roi.min[0], roi.min[1], roi.max[0], roi.max[1]], dtype=np.float64)
+    cap = max(int(max_points), 1)
+    ox, oy, oz = np.empty(cap), np.empty(cap), np.empty(cap)
+    n = C.c_size_t()
+    _chk(load().orc_select_ground_points(_p(px), _p(py), _p(pz), _p(kind), len(kind), _p(Rm),
+                                         _p(tv), _p(r4), float(radius), float(voxel),
+                                         int(max_points), _p(ox), _p(oy), _p(oz), C.byref(n)))
+    k = n.value
+    return np.stack([ox[:k], oy[:k]], 1), oz[:k].copy()
 
 
 def fit_batch_ridge(kernel, centers, xy, z):

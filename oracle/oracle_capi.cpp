@@ -349,4 +349,58 @@ void orc_so3_exp(const double* w, double* R) {
   std::memcpy(R, m.a, sizeof(m.a));
 }
 
+// pipeline.cpp:150-170 (out_* capacity >= max_points)
+int orc_select_ground_points(const double* px, const double* py, const double* pz,
+                             const unsigned char* kind, size_t n, const double* R,
+                             const double* t, const double* roi, double radius, double voxel,
+                             size_t max_points, double* ox, double* oy, double* oz,
+                             size_t* out_n) {
+  return guarded([&] {
+    std::vector<V3> p(n);
+    for (size_t i = 0; i < n; ++i) p[i] = {px[i], py[i], pz[i]};
+    std::vector<std::uint8_t> k(kind, kind + n);
+    M3 m;
+    std::memcpy(m.a, R, sizeof(m.a));
+    const Rect r{{roi[0], roi[1]}, {roi[2], roi[3]}};
+    const GroundPoints g = select_ground_points(p, k, m, {t[0], t[1], t[2]}, r, radius, voxel,
+                                                max_points);
+    for (size_t i = 0; i < g.xy.size(); ++i) {
+      ox[i] = g.xy[i].x;
+      oy[i] = g.xy[i].y;
+      oz[i] = g.z[i];
+    }
+    *out_n = g.xy.size();
+  });
+}
+
+// metrics.cpp:199-232
+int orc_terrain_error_histogram(void* m, const double* x, const double* y, const double* z,
+                                size_t n, double trim, int bins, double* edges,
+                                unsigned long long* counts, unsigned long long* trimmed,
+                                unsigned long long* overflow) {
+  auto* t = static_cast<TerrainModel*>(m);
+  return guarded([&] {
+    std::vector<V2> xy(n);
+    for (size_t i = 0; i < n; ++i) xy[i] = {x[i], y[i]};
+    const Histogram h = terrain_error_histogram(*t, xy, std::vector<double>(z, z + n), trim, bins);
+    for (int b = 0; b <= bins; ++b) edges[b] = h.edges[b];
+    for (int b = 0; b < bins; ++b) counts[b] = h.counts[b];
+    *trimmed = h.trimmed;
+    *overflow = h.overflow;
+  });
+}
+
+// terrain_model.cpp:255-267 (numbers of export_csv); returns the point count
+size_t orc_export_grid(void* m, double step, double* x, double* y, double* z, size_t cap) {
+  auto* t = static_cast<TerrainModel*>(m);
+  std::vector<double> xs, ys, zs;
+  export_grid(*t, step, xs, ys, zs);
+  for (size_t i = 0; i < xs.size() && i < cap; ++i) {
+    x[i] = xs[i];
+    y[i] = ys[i];
+    z[i] = zs[i];
+  }
+  return xs.size();
+}
+
 }  // extern "C"

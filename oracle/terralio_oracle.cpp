@@ -9,6 +9,7 @@
 #include <fstream>
 #include <limits>
 #include <set>
+#include <unordered_set>
 
 namespace oracle {
 
@@ -742,6 +743,75 @@ bool lm_step(const NormalEq& ne, double mu, double delta[6]) {
     finite = finite && std::isfinite(delta[i]);
   }
   return finite;
+}
+
+// --- pipeline.cpp:150-170 ----------------------------------------------------
+GroundPoints select_ground_points(const std::vector<V3>& p, const std::vector<std::uint8_t>& kind,
+                                  const M3& R, const V3& t, const Rect& roi, double radius,
+                                  double voxel, std::size_t max_points) {
+  GroundPoints out;
+  std::unordered_set<std::int64_t> voxels;
+  for (std::size_t i = 0; i < p.size(); ++i) {
+    if (kind[i] != 2) continue;  // FeatureKind::Ground
+    const V3 q0 = mul(R, p[i]);
+    const V3 q{q0.x + t.x, q0.y + t.y, q0.z + t.z};
+    const V2 xy{q.x, q.y};
+    if (!roi.contains(xy)) continue;
+    if (std::sqrt(sqnorm(xy.x - t.x, xy.y - t.y)) > radius) continue;
+    const auto vx = static_cast<std::int64_t>(std::floor(xy.x / voxel));
+    const auto vy = static_cast<std::int64_t>(std::floor(xy.y / voxel));
+    if (!voxels.insert((vx << 21) ^ (vy & ((1 << 21) - 1))).second) continue;
+    out.xy.push_back(xy);
+    out.z.push_back(q.z);
+    if (out.xy.size() >= max_points) break;
+  }
+  return out;
+}
+
+// --- metrics.cpp:199-232 -------------------------------------------------------
+Histogram terrain_error_histogram(const TerrainModel& model, const std::vector<V2>& xy,
+                                  const std::vector<double>& z, double trim_fraction, int bins) {
+  if (xy.empty() || xy.size() != z.size())
+    throw std::invalid_argument("histogram needs matched non-empty samples");
+  if (trim_fraction < 0.0 || trim_fraction >= 1.0)
+    throw std::invalid_argument("trim_fraction must be in [0, 1)");
+  constexpr double kRange = 0.25;
+  std::vector<double> errors(xy.size());
+  for (std::size_t i = 0; i < xy.size(); ++i) {
+    const HeightQuery q = model.predict_height(xy[i]);
+    errors[i] = q.supported ? std::abs(z[i] - q.z) : kRange;
+  }
+  std::sort(errors.begin(), errors.end());
+  const std::size_t keep =
+      xy.size() - static_cast<std::size_t>(std::floor(trim_fraction * static_cast<double>(xy.size())));
+  Histogram h;
+  h.trimmed = xy.size() - keep;
+  h.edges.resize(bins + 1);
+  h.counts.assign(bins, 0);
+  for (int b = 0; b <= bins; ++b) h.edges[b] = kRange * b / bins;
+  for (std::size_t i = 0; i < keep; ++i) {
+    const auto b = static_cast<int>(std::floor(errors[i] / kRange * bins));
+    if (b >= bins)
+      ++h.overflow;
+    else
+      ++h.counts[b];
+  }
+  return h;
+}
+
+// --- terrain_model.cpp:255-267 -------------------------------------------------
+void export_grid(const TerrainModel& model, double grid_step, std::vector<double>& xs,
+                 std::vector<double>& ys, std::vector<double>& zs) {
+  const Rect& roi = model.centers().roi;
+  for (double x = roi.min.x; x <= roi.max.x + 1e-12; x += grid_step) {
+    for (double y = roi.min.y; y <= roi.max.y + 1e-12; y += grid_step) {
+      const HeightQuery q = model.predict_height({x, y});
+      if (!q.supported) continue;
+      xs.push_back(x);
+      ys.push_back(y);
+      zs.push_back(q.z);
+    }
+  }
 }
 
 }  // namespace oracle

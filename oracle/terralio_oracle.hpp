@@ -237,4 +237,33 @@ struct Ldlt {
   std::vector<double> vectorD() const;
 };
 
+// --- Batch-predict consumers ----------------------------
+// pipeline.cpp:150-170 select_ground_points: ground-labelled points (kind 2)
+// in scan order, p = R f + t, kept when inside the ROI (types.hpp:18-21),
+// within `radius` of the base in xy, and first in their xy voxel key
+// (floor(x/voxel) << 21) ^ (floor(y/voxel) & (2^21 - 1)); stops after
+// max_points kept. Returns the kept world points.
+struct GroundPoints {
+  std::vector<V2> xy;
+  std::vector<double> z;
+};
+GroundPoints select_ground_points(const std::vector<V3>& p, const std::vector<std::uint8_t>& kind,
+                                  const M3& R, const V3& t, const Rect& roi, double radius,
+                                  double voxel, std::size_t max_points);
+
+// metrics.cpp:199-232 terrain_error_histogram (kRange = 0.25 m).
+struct Histogram {
+  std::vector<double> edges;
+  std::vector<std::size_t> counts;
+  std::size_t trimmed = 0;
+  std::size_t overflow = 0;
+};
+Histogram terrain_error_histogram(const TerrainModel& model, const std::vector<V2>& xy,
+                                  const std::vector<double>& z, double trim_fraction, int bins);
+
+// terrain_model.cpp:255-267 export_csv, numbers only: the supported grid
+// points (x outer, y inner, both accumulated by += grid_step) and heights.
+void export_grid(const TerrainModel& model, double grid_step, std::vector<double>& x,
+                 std::vector<double>& y, std::vector<double>& z);
+
 }  // namespace oracle

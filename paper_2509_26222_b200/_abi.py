@@ -106,6 +106,10 @@ _SIGS = {
     "tlg_ctx_kernel_stats": (_ST, [_P, _I, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
     "tlg_measure_fp64_peak": (_ST, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "tlg_debug_dense_bench": (_ST, [_P, _I, _I, _I, _I, C.POINTER(C.c_double)]),
+    "tlg_select_ground_points": (_ST, [_P, _P, _P, _P, _P, _SZ, _I, _P, _P, _P, _P, C.c_double,
+                                       C.c_double, _SZ, _P, _P, _P, _I, C.POINTER(_SZ)]),
+    "tlg_terrain_error_histogram": (_ST, [_P, _P, _P, _P, _SZ, _I, C.c_double, _I, _P, _P,
+                                          C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "tlg_debug_potrf": (_ST, [_P, _I, _P, _I, _I, _P, _P]),
     "tlg_kernel_finalize": (_ST, [C.POINTER(KernelParamsC)]),
     "tlg_supported_mesh_nodes": (_ST, [_P, _P, _P, _P, _SZ, _SZ, _I, C.POINTER(CenterParamsC),

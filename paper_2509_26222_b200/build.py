@@ -26,7 +26,7 @@ NVCC_FLAGS = [
     "-I", str(ROOT / "include"),
 ]
 
-SOURCES = ["model.cu", "grid.cu", "eval.cu", "select.cu", "dense.cu", "update.cu", "peak.cu", "scan.cu", "abi.cu"]
+SOURCES = ["model.cu", "grid.cu", "eval.cu", "select.cu", "dense.cu", "update.cu", "peak.cu", "scan.cu", "consumers.cu", "abi.cu"]
 
 
 def _stale(target: Path, deps: list[Path]) -> bool:

@@ -22,6 +22,13 @@ void moment_device(tlg_model* m, const double* x, const double* y, size_t n, uin
 void fp64_peak(tlg_ctx* ctx, double* dfma, double* dmma);
 double dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps);
 bool debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X, int band);
+size_t select_ground_device(tlg_ctx* ctx, const double* px, const double* py, const double* pz,
+                            const uint8_t* kind, size_t n, const double R[9], const double t[3],
+                            const double roi[4], double radius, double voxel, size_t max_points,
+                            double* ox, double* oy, double* oz);
+void error_histogram_device(tlg_model* m, const double* x, const double* y, const double* z,
+                            size_t n, double trim_fraction, int bins, double* edges,
+                            uint64_t* counts, uint64_t* trimmed, uint64_t* overflow);
 tlg_scan* scan_create(tlg_model* m, const double R0[9], const double t0[3], const double* hx,
                       const double* hy, const double* hz, size_t n);
 }  // namespace tlg
@@ -182,6 +189,64 @@ tlg_status tlg_debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, int b
     require(tile == 0 || tile == 32 || tile == 64, TLG_INVALID_ARGUMENT, "tile must be 0, 32 or 64");
     if (!debug_potrf(ctx, n, A, tile, L, X, band > 0 && band < n ? band : n))
       throw Error(TLG_DOMAIN_ERROR, "matrix is not positive definite");
+  });
+}
+
+tlg_status tlg_select_ground_points(tlg_ctx* ctx, const double* px, const double* py,
+                                    const double* pz, const uint8_t* kind, size_t n,
+                                    tlg_mem in_mem, const double R[9], const double t[3],
+                                    const double roi_min[2], const double roi_max[2],
+                                    double ground_radius, double ground_voxel,
+                                    size_t max_points, double* out_x, double* out_y,
+                                    double* out_z, tlg_mem out_mem, size_t* out_n) {
+  return guard([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(R, "R");
+    check_ptr(t, "t");
+    check_ptr(roi_min, "roi_min");
+    check_ptr(roi_max, "roi_max");
+    check_ptr(out_n, "out_n");
+    require(ground_voxel > 0.0, TLG_INVALID_ARGUMENT, "ground_voxel must be positive");
+    *out_n = 0;
+    if (n == 0 || max_points == 0) return;
+    const double* dx = as_device(ctx, S_IN_HX, px, n, in_mem);
+    const double* dy = as_device(ctx, S_IN_HY, py, n, in_mem);
+    const double* dz = as_device(ctx, S_IN_HZ, pz, n, in_mem);
+    const uint8_t* dk = as_device(ctx, S_MOMENT_ROW, kind, n, in_mem);
+    const bool dev = out_mem == TLG_DEVICE;
+    double* ox = out_x ? (dev ? out_x : ctx->ws<double>(S_OUT_R, max_points)) : nullptr;
+    double* oy = out_y ? (dev ? out_y : ctx->ws<double>(S_OUT_GX, max_points)) : nullptr;
+    double* oz = out_z ? (dev ? out_z : ctx->ws<double>(S_OUT_GY, max_points)) : nullptr;
+    const double roi[4] = {roi_min[0], roi_min[1], roi_max[0], roi_max[1]};
+    const size_t k = select_ground_device(ctx, dx, dy, dz, dk, n, R, t, roi, ground_radius,
+                                          ground_voxel, max_points, ox, oy, oz);
+    if (!dev && k) {
+      if (out_x) copy_out(ctx, out_x, ox, k * 8, TLG_HOST);
+      if (out_y) copy_out(ctx, out_y, oy, k * 8, TLG_HOST);
+      if (out_z) copy_out(ctx, out_z, oz, k * 8, TLG_HOST);
+    }
+    ctx->sync();
+    *out_n = k;
+  });
+}
+
+tlg_status tlg_terrain_error_histogram(tlg_model* m, const double* x, const double* y,
+                                       const double* z, size_t n, tlg_mem mem,
+                                       double trim_fraction, int bins, double* edges,
+                                       uint64_t* counts, uint64_t* trimmed, uint64_t* overflow) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(edges, "edges");
+    check_ptr(counts, "counts");
+    check_ptr(trimmed, "trimmed");
+    check_ptr(overflow, "overflow");
+    require(n > 0 && x && y && z, TLG_INVALID_ARGUMENT, "histogram needs matched non-empty samples");
+    tlg_ctx* ctx = m->ctx;
+    const double* dx = as_device(ctx, S_IN_X, x, n, mem);
+    const double* dy = as_device(ctx, S_IN_Y, y, n, mem);
+    const double* dz = as_device(ctx, S_IN_Z, z, n, mem);
+    error_histogram_device(m, dx, dy, dz, n, trim_fraction, bins, edges, counts, trimmed,
+                           overflow);
   });
 }
 

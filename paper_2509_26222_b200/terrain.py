@@ -357,6 +357,11 @@ class TerrainModel:
                                    _ptr(gx), _ptr(gy), _mem(xs)))
         return z, s, gx, gy
 
+    def export_csv(self, path: str, grid_step: float) -> None:
+        """TerrainModel::export_csv (terrain_model.cpp:255-267)."""
+        from .consumers import export_csv
+        export_csv(self, path, grid_step)
+
     def predict_height(self, x) -> HeightQuery:
         """terrain_model.cpp:109-125."""
         z, s, _, _ = self.predict(np.asarray(x, dtype=np.float64).reshape(1, 2), gradient=False)
