@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cmath>
+#include <fstream>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -334,6 +335,27 @@ class TerrainModel {
             static_cast<std::size_t>(r.born_centers), r.rejected != 0};
   }
 
+  // terrain_model.cpp:255-267: the reference's grid walk, one batched device
+  // evaluation, ostream default formatting
+  void export_csv(const std::string& path, double grid_step) const {
+    tlg_center_params cp{};
+    gpu::check(tlg_model_center_params(m_.get(), &cp));
+    std::vector<double> xs, ys;
+    for (double x = cp.roi_min_x; x <= cp.roi_max_x + 1e-12; x += grid_step)
+      for (double y = cp.roi_min_y; y <= cp.roi_max_y + 1e-12; y += grid_step) {
+        xs.push_back(x);
+        ys.push_back(y);
+      }
+    std::vector<double> z(xs.size());
+    std::vector<uint8_t> s(xs.size());
+    if (!xs.empty()) predict(xs.data(), ys.data(), xs.size(), z.data(), s.data(), nullptr, nullptr);
+    std::ofstream out(path);
+    if (!out) throw std::runtime_error("cannot open " + path);
+    out << "x,y,z_pred\n";
+    for (std::size_t i = 0; i < xs.size(); ++i)
+      if (s[i]) out << xs[i] << ',' << ys[i] << ',' << z[i] << '\n';
+  }
+
   void save(const std::string& path) const { gpu::check(tlg_model_save(m_.get(), path.c_str())); }
   static TerrainModel load(const std::string& path) {
     tlg_model* m = nullptr;
@@ -365,6 +387,55 @@ inline TerrainModel fit_batch_ridge(const KernelParams& params, const CenterSet&
 }
 
 }  // namespace terrain
+
+namespace eval {
+
+// metrics.hpp:42-51
+struct Histogram {
+  std::vector<double> edges;
+  std::vector<std::size_t> counts;
+  std::size_t trimmed = 0;
+  std::size_t overflow = 0;
+  std::size_t total() const {
+    std::size_t n = overflow;
+    for (const std::size_t c : counts) n += c;
+    return n;
+  }
+  double fraction_below(double threshold) const {
+    const std::size_t n = total();
+    if (n == 0) return 0.0;
+    std::size_t below = 0;
+    for (std::size_t b = 0; b < counts.size(); ++b)
+      if (edges[b + 1] <= threshold + 1e-12) below += counts[b];
+    return static_cast<double>(below) / static_cast<double>(n);
+  }
+};
+
+// metrics.cpp:199-232
+inline Histogram terrain_error_histogram(const terrain::TerrainModel& model,
+                                         const std::vector<Vec2>& xy, const std::vector<double>& z,
+                                         double trim_fraction, int bins) {
+  if (xy.empty() || xy.size() != z.size())
+    throw std::invalid_argument("histogram needs matched non-empty samples");
+  std::vector<double> x(xy.size()), y(xy.size());
+  for (std::size_t i = 0; i < xy.size(); ++i) {
+    x[i] = xy[i].x();
+    y[i] = xy[i].y();
+  }
+  Histogram h;
+  h.edges.resize(bins + 1);
+  std::vector<uint64_t> c(bins > 0 ? bins : 1);
+  uint64_t tr = 0, ov = 0;
+  gpu::check(tlg_terrain_error_histogram(model.handle(), x.data(), y.data(), z.data(), xy.size(),
+                                         TLG_HOST, trim_fraction, bins, h.edges.data(), c.data(),
+                                         &tr, &ov));
+  h.counts.assign(c.begin(), c.begin() + bins);
+  h.trimmed = tr;
+  h.overflow = ov;
+  return h;
+}
+
+}  // namespace eval
 
 namespace kin {
 

@@ -5,7 +5,7 @@
  * (terralio::terrain::TerrainModel & friends, /root/reference/proj/core) and
  * the sm_100a kernels in paper_2509_26222_b200/csrc. Plain C: opaque
  * handles, plain pointers + sizes, int status codes; no CUDA, torch or Eigen
- * types. A C++ shim (include/terralio_b200/*.hpp) and a ctypes binding
+ * types. A C++ shim (include/terralio_b200/terrain.hpp) and a ctypes binding
  * (paper_2509_26222_b200/_abi.py) rebuild the reference interface on top of
  * it; INTEGRATION.md shows the binding a proj/core maintainer adds.
  *

@@ -106,6 +106,21 @@ int main() {
   CHECK(loaded.num_centers() == batch.num_centers());
   CHECK(std::fabs(loaded.predict_height({1.0, 1.0}).z - q.z) <= 1e-14 * std::fabs(q.z) + 1e-300);
 
+  // metrics.cpp:199-232 through the shim: counts add up, edges as the reference's
+  {
+    std::vector<Vec2> qs;
+    std::vector<double> zs;
+    for (int i = 0; i < 2000; ++i) {
+      qs.push_back({u(rng), u(rng)});
+      zs.push_back(0.1 * std::sin(4.0 * qs.back().x()));
+    }
+    const eval::Histogram h = eval::terrain_error_histogram(batch, qs, zs, 0.1, 25);
+    CHECK(h.trimmed == 200);
+    CHECK(h.total() == 1800);
+    CHECK(h.edges.size() == 26 && h.edges[25] == 0.25);
+    batch.export_csv("/tmp/terralio_b200_shim.csv", 0.05);
+  }
+
   // manifold rows + normal equations
   std::vector<Vec3> lever;
   for (int i = 0; i < 1000; ++i) lever.push_back({u(rng), u(rng), 0.05});
