@@ -237,10 +237,21 @@ def run_update_c4(torch, steps=5):
         ev1.synchronize()
         if k >= 2:
             times.append(ev0.elapsed_time(ev1))
-    return {"M": model.num_centers(), "m": 20000, "footprint_m": 2.5,
-            "ms_per_scan": statistics.median(times), "ms_min": min(times),
-            "n_active": rep.active_centers, "active_blocks": rep.active_blocks,
-            "solver": rep.solver, "rejected": rep.rejected}
+    out = {"M": model.num_centers(), "m": 20000, "footprint_m": 2.5,
+           "ms_per_scan": statistics.median(times), "ms_min": min(times),
+           "n_active": rep.active_centers, "active_blocks": rep.active_blocks,
+           "solver": rep.solver, "rejected": rep.rejected}
+    # fit_batch_ridge at C4 scale (terrain_model.cpp:269-308):
+    # banded Gram / Cholesky / solve over the 10^6 support points
+    obs = T.TerrainObservation(sup, terrain_c5(sup[:, 0], sup[:, 1], np))
+    T.fit_batch_ridge(kernel, cs, obs)
+    ev0.record()
+    T.fit_batch_ridge(kernel, cs, obs)
+    ev1.record()
+    ev1.synchronize()
+    out["batch_fit_ms"] = ev0.elapsed_time(ev1)
+    out["batch_fit_points"] = len(sup)
+    return out
 
 
 def cpu_update_ms(model, kernel, m=400, seed=5):

@@ -1450,6 +1450,70 @@ __global__ void __launch_bounds__(128) k_potrf_coop32(double* __restrict__ A, in
   }
 }
 
+// Banded Cholesky solve L L^T x = b with the 32-wide factor (L in A, the
+// diagonal-tile inverses in linv): one CTA walks the tile rows forward
+// (y_k = Linv_kk (b_k - sum_j L_kj y_j), j in the band) and back
+// (x_k = Linv_kk^T (y_k - sum_i L_ik^T x_i)). Each step is a 32 x (32 bwt)
+// GEMV split over the 4 warps, then a 32 x 32 one.
+__global__ void __launch_bounds__(128) k_band_solve32(const double* __restrict__ L, int n, int ld,
+                                                      int bwt, const double* __restrict__ linv,
+                                                      double* __restrict__ b) {
+  __shared__ double part[4][32];
+  __shared__ double t[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nt = (n + NB32 - 1) / NB32;
+  for (int k = 0; k < nt; ++k) {  // forward
+    const int k0 = k * NB32, kb = min(NB32, n - k0);
+    const int j0 = max(0, k - bwt) * NB32;
+    double acc = 0.0;
+    if (lane < kb)
+      for (int c = j0 + w; c < k0; c += 4) acc = fma(L[k0 + lane + (size_t)c * ld], b[c], acc);
+    part[w][lane] = acc;
+    __syncthreads();
+    if (w == 0) t[lane] = lane < kb ? b[k0 + lane] - (part[0][lane] + part[1][lane] +
+                                                       part[2][lane] + part[3][lane]) : 0.0;
+    __syncthreads();
+    if (w == 0 && lane < kb) {
+      const double* Li = linv + (size_t)k * NB32 * NB32;
+      double y = 0.0;
+      for (int c = 0; c <= lane; ++c) y = fma(Li[lane + c * NB32], t[c], y);
+      b[k0 + lane] = y;
+    }
+    __syncthreads();
+  }
+  for (int k = nt - 1; k >= 0; --k) {  // backward
+    const int k0 = k * NB32, kb = min(NB32, n - k0);
+    const int i1 = min(nt - 1, k + bwt);
+    const int r_end = min(n, (i1 + 1) * NB32);
+    double acc = 0.0;
+    if (lane < kb)
+      for (int r = k0 + kb + w; r < r_end; r += 4)
+        acc = fma(L[r + (size_t)(k0 + lane) * ld], b[r], acc);
+    part[w][lane] = acc;
+    __syncthreads();
+    if (w == 0) t[lane] = lane < kb ? b[k0 + lane] - (part[0][lane] + part[1][lane] +
+                                                       part[2][lane] + part[3][lane]) : 0.0;
+    __syncthreads();
+    if (w == 0 && lane < kb) {
+      const double* Li = linv + (size_t)k * NB32 * NB32;
+      double x = 0.0;
+      for (int r = lane; r < kb; ++r) x = fma(Li[r + lane * NB32], t[r], x);
+      b[k0 + lane] = x;
+    }
+    __syncthreads();
+  }
+}
+
+void band_solve(tlg_ctx* ctx, const double* L, int n, int ld, int band, double* b) {
+  if (n <= 0) return;
+  require(ctx->linv32_owner == L, TLG_RUNTIME_ERROR, "band_solve: matrix was not factored last");
+  const int nt = (n + NB32 - 1) / NB32;
+  const int bwt = std::min(nt - 1, (std::max(band, 0) + NB32 - 1) / NB32);
+  const double* linv = ctx->ws<double>(S_LINV, 1);
+  k_band_solve32<<<1, 128, 0, ctx->stream>>>(L, n, ld, bwt, linv, b);
+  TLG_LAUNCHED(ctx);
+}
+
 // B <- L^-1 B (trans = 0) or L^-T B (trans = 1), one CTA per 64-column slab
 // of B walking the tile rows: B_k -= L_kj X_j (DMMA), X_k = Linv_kk B_k.
 __global__ void __launch_bounds__(128) k_trsm_tiles(const double* __restrict__ L, int n, int ldl,
@@ -1487,6 +1551,7 @@ static void potrf_lower32(tlg_ctx* ctx, double* A, int n, int lda, int* info, do
   int bwt = std::min(nt - 1, (std::max(band, 0) + NB32 - 1) / NB32);
   double* linv = ctx->ws<double>(S_LINV, static_cast<size_t>(nt) * NB32 * NB32);
   ctx->linv_owner = nullptr;  // 32-wide inverse tiles: not usable by trsm_left_lower
+  ctx->linv32_owner = A;
   int per_sm = 0;
   TLG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_potrf_coop32, 128, 0));
   int maxtiles = nt;
@@ -1512,6 +1577,7 @@ void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X, 
   const int nt = (n + NB - 1) / NB;
   double* linv = ctx->ws<double>(S_LINV, static_cast<size_t>(nt) * NB * NB);
   ctx->linv_owner = A;
+  ctx->linv32_owner = nullptr;
   const size_t smem = sizeof(double) * std::max(kDiagSmemDoubles, 2 * 64 * 65 + 64 + 256);
   static bool attr = false;
   if (!attr) {

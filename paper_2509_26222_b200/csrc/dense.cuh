@@ -39,6 +39,9 @@ void trsm_left_lower(tlg_ctx* ctx, const double* L, int n, int ldl, double* B, i
 bool debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X,
                  int band = -1);
 double dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps);
+// x = (L L^T)^-1 b in place, L the (banded) 32-wide factor from the last
+// potrf_lower (band as passed to it).
+void band_solve(tlg_ctx* ctx, const double* L, int n, int ld, int band, double* b);
 // A <- 0.5 (A + A^T) for a square n x n matrix (in place).
 void symmetrize(tlg_ctx* ctx, double* A, int n, int lda);
 // A[i,i] += v

@@ -132,6 +132,7 @@ struct tlg_ctx {
   // dense.cu: inverses of the 64x64 diagonal Cholesky tiles of the most
   // recent potrf_lower (slot S_LINV), keyed by the factored matrix
   const double* linv_owner = nullptr;
+  const double* linv32_owner = nullptr;  // factor whose 32-wide tile inverses S_LINV holds
   bool force_nb64 = false;  // dense_bench: force the 64-wide factorisation
 
   template <typename T>

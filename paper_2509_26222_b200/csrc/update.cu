@@ -507,20 +507,23 @@ static bool spd_inverse(tlg_ctx* ctx, const double* src, int lds, int n, double*
 // A^-1 = X^T X — and writes it into the diagonal block of H (ld ldh).
 // Warps walk rows, lanes walk columns. info != 0 on a non-positive pivot.
 constexpr int kBatchInvMax = 112;
-__global__ void __launch_bounds__(256) k_batched_spd_inverse(const BlockTab* __restrict__ tab,
-                                                             const double* __restrict__ pool,
-                                                             double* __restrict__ H, int ldh,
+struct InvJob {  // dst (ldd) <- src(lds)^-1, n x n SPD
+  const double* src;
+  double* dst;
+  int lds, ldd, n, pad;
+};
+__global__ void __launch_bounds__(256) k_batched_spd_inverse(const InvJob* __restrict__ jobs,
                                                              int* __restrict__ info) {
   extern __shared__ double sm[];
-  const BlockTab b = tab[blockIdx.x];
+  const InvJob b = jobs[blockIdx.x];
   const int n = b.n, P = n + 1, t = threadIdx.x, lane = t & 31, wq = t >> 5;
   const int nw = blockDim.x >> 5;
   double* a = sm;          // a[r * P + c]: lower triangle -> L
   double* x = sm + n * P;  // x[r * P + c]: X = L^-1 (lower)
-  const double* src = pool + b.pool_off;
+  const double* src = b.src;
   for (int e = t; e < n * n; e += blockDim.x) {
     const int r = e % n, c = e / n;
-    if (r >= c) a[r * P + c] = src[r + (size_t)c * b.ld];
+    if (r >= c) a[r * P + c] = src[r + (size_t)c * b.lds];
     x[r * P + c] = (r == c) ? 1.0 : 0.0;
   }
   __syncthreads();
@@ -554,7 +557,8 @@ __global__ void __launch_bounds__(256) k_batched_spd_inverse(const BlockTab* __r
     __syncthreads();
   }
   // A^-1 = X^T X: (r, c) = sum_{p >= max(r, c)} x_pr x_pc; write both halves
-  double* dst = H + b.off + (size_t)b.off * ldh;
+  double* dst = b.dst;
+  const int ldh = b.ldd;
   for (int r = wq; r < n; r += nw) {
     for (int c = lane; c <= r; c += 32) {
       double s0 = 0.0, s1 = 0.0;
@@ -569,6 +573,23 @@ __global__ void __launch_bounds__(256) k_batched_spd_inverse(const BlockTab* __r
       dst[c + (size_t)r * ldh] = v;
     }
   }
+}
+
+// Launches k_batched_spd_inverse over host-built jobs (all n <= kBatchInvMax).
+static void batched_spd_inverse(tlg_ctx* ctx, const std::vector<InvJob>& jobs, int* info) {
+  if (jobs.empty()) return;
+  int maxn = 0;
+  for (const auto& j : jobs) maxn = std::max(maxn, j.n);
+  const size_t bytes = jobs.size() * sizeof(InvJob);
+  InvJob* h = static_cast<InvJob*>(ctx->host_stage(bytes));
+  std::memcpy(h, jobs.data(), bytes);
+  InvJob* d = reinterpret_cast<InvJob*>(ctx->ws<char>(S_BLKTAB, bytes));
+  TLG_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  const int smem = 2 * maxn * (maxn + 1) * 8;
+  TLG_CUDA(cudaFuncSetAttribute(k_batched_spd_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem));
+  k_batched_spd_inverse<<<static_cast<unsigned>(jobs.size()), 256, smem, ctx->stream>>>(d, info);
+  TLG_LAUNCHED(ctx);
 }
 
 __global__ void k_iota(uint32_t* __restrict__ a, size_t n) {
@@ -664,6 +685,56 @@ struct StageTrace {
   }
 };
 
+// Row-by-row order of blocks over the tile grid (the shorter extent fastest):
+// with it, H = H0 + Mt Mt^T, which couples only blocks whose tiles touch
+// (shared observations lie within the cutoff of both centres, tile side =
+// 2 cutoff), is block-banded. Returns the tile coordinates per block id
+// (empty when the model has a single tile).
+static std::vector<std::pair<int64_t, int64_t>> spatial_block_order(
+    const tlg_model* m, std::vector<uint32_t>& blocks) {
+  std::vector<std::pair<int64_t, int64_t>> btile;
+  if (m->tile_blocks.size() <= 1) return btile;
+  btile.assign(m->members.size(), {0, 0});
+  for (const auto& [key, b] : m->tile_blocks)
+    btile[b] = {static_cast<int32_t>(static_cast<uint64_t>(key) >> 32),
+                static_cast<int32_t>(static_cast<uint64_t>(key) & 0xffffffffu)};
+  int64_t x0 = INT64_MAX, x1 = INT64_MIN, y0 = INT64_MAX, y1 = INT64_MIN;
+  for (uint32_t b : blocks) {
+    x0 = std::min(x0, btile[b].first);
+    x1 = std::max(x1, btile[b].first);
+    y0 = std::min(y0, btile[b].second);
+    y1 = std::max(y1, btile[b].second);
+  }
+  const bool x_fast = (x1 - x0) <= (y1 - y0);
+  auto key = [&](uint32_t b) {
+    return x_fast ? std::make_pair(btile[b].second, btile[b].first)
+                  : std::make_pair(btile[b].first, btile[b].second);
+  };
+  std::stable_sort(blocks.begin(), blocks.end(),
+                   [&](uint32_t a, uint32_t b) { return key(a) < key(b); });
+  return btile;
+}
+
+// Lower bandwidth (rows) of H under the merged order: a row of block q has no
+// entry left of the first row of the earliest block whose tile touches q's.
+static int block_band(const std::vector<std::pair<int64_t, int64_t>>& btile,
+                      const std::vector<uint32_t>& blocks, const std::vector<BlockTab>& tab) {
+  int band = 0;
+  for (size_t q = 0; q < blocks.size(); ++q) {
+    int first = tab[q].off;
+    const auto& b = btile[blocks[q]];
+    for (size_t p = 0; p < q; ++p) {
+      const auto& a = btile[blocks[p]];
+      if (std::llabs(a.first - b.first) <= 1 && std::llabs(a.second - b.second) <= 1) {
+        first = tab[p].off;
+        break;
+      }
+    }
+    band = std::max(band, tab[q].off + tab[q].n - 1 - first);
+  }
+  return band;
+}
+
 void recursive_update_device(tlg_model* m, const double* x, const double* y, const double* z,
                              size_t mm, bool allow_birth, tlg_update_report* rep) {
   tlg_ctx* ctx = m->ctx;
@@ -735,27 +806,7 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   // form keeps the reference's ascending block order.
   const bool info_form = mm > n_total;
   std::vector<std::pair<int64_t, int64_t>> btile;
-  if (info_form && m->tile_blocks.size() > 1) {
-    btile.assign(nb, {0, 0});
-    for (const auto& [key, b] : m->tile_blocks)
-      btile[b] = {static_cast<int32_t>(static_cast<uint64_t>(key) >> 32),
-                  static_cast<int32_t>(static_cast<uint64_t>(key) & 0xffffffffu)};
-    int64_t x0 = INT64_MAX, x1 = INT64_MIN, y0 = INT64_MAX, y1 = INT64_MIN;
-    for (uint32_t b : ablocks) {
-      x0 = std::min(x0, btile[b].first);
-      x1 = std::max(x1, btile[b].first);
-      y0 = std::min(y0, btile[b].second);
-      y1 = std::max(y1, btile[b].second);
-    }
-    const bool x_fast = (x1 - x0) <= (y1 - y0);
-    std::stable_sort(ablocks.begin(), ablocks.end(), [&](uint32_t a, uint32_t b) {
-      const auto ka = x_fast ? std::make_pair(btile[a].second, btile[a].first)
-                             : std::make_pair(btile[a].first, btile[a].second);
-      const auto kb = x_fast ? std::make_pair(btile[b].second, btile[b].first)
-                             : std::make_pair(btile[b].first, btile[b].second);
-      return ka < kb;
-    });
-  }
+  if (info_form) btile = spatial_block_order(m, ablocks);
 
   // ---- merged system (:174-184) ------------------------------------------
   std::vector<uint32_t> merged;
@@ -778,24 +829,7 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   rep->active_centers = static_cast<uint64_t>(n);
   int maxq = 0;
   for (const auto& t : tab) maxq = std::max(maxq, t.n);
-  // lower bandwidth (rows) of H1 under the merged order: row r of block q is
-  // coupled to no column left of the first row of the earliest touching block
-  int band = n;
-  if (!btile.empty()) {
-    band = 0;
-    for (int q = 0; q < nq; ++q) {
-      int first = tab[q].off;
-      for (int p = 0; p < q; ++p) {
-        const auto& a = btile[ablocks[p]];
-        const auto& b = btile[ablocks[q]];
-        if (std::llabs(a.first - b.first) <= 1 && std::llabs(a.second - b.second) <= 1) {
-          first = tab[p].off;
-          break;
-        }
-      }
-      band = std::max(band, tab[q].off + tab[q].n - 1 - first);
-    }
-  }
+  const int band = btile.empty() ? n : block_band(btile, ablocks, tab);
 
   // pinned staging for the small host->device tables
   const size_t bytes_merged = n * 4, bytes_tab = nq * sizeof(BlockTab), bytes_rb = n * 4;
@@ -882,11 +916,12 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
     // H0 = blockdiag(info_inv_q)^-1: all blocks in one launch when they fit
     // in shared memory, else one factorisation per block
     if (maxq <= kBatchInvMax) {
-      const int smem_inv = 2 * maxq * (maxq + 1) * 8;
-      TLG_CUDA(cudaFuncSetAttribute(k_batched_spd_inverse,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem_inv));
-      k_batched_spd_inverse<<<nq, 256, smem_inv, s>>>(d_tab, m->pool.p, H, n, info + 1);
-      TLG_LAUNCHED(ctx);
+      std::vector<InvJob> jobs(nq);
+      for (int q = 0; q < nq; ++q)
+        jobs[q] = InvJob{m->pool.p + tab[q].pool_off,
+                         H + tab[q].off + static_cast<size_t>(tab[q].off) * n, tab[q].ld, n,
+                         tab[q].n, 0};
+      batched_spd_inverse(ctx, jobs, info + 1);
     } else {
       for (int q = 0; q < nq; ++q) {
         double* dst = H + tab[q].off + static_cast<size_t>(tab[q].off) * n;
@@ -937,79 +972,97 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   TLG_CUDA(cudaStreamSynchronize(s));
 }
 
-__global__ void k_gather_sub(const double* __restrict__ H, int ldh, const uint32_t* __restrict__ idx,
-                             int bn, double* __restrict__ out) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bn * bn; e += gridDim.x * blockDim.x) {
-    const int r = e % bn, c = e / bn;
-    out[e] = H[idx[r] + (size_t)idx[c] * ldh];
-  }
-}
-static void gather_sub(tlg_ctx* ctx, const double* H, int ldh, const std::vector<uint32_t>& mem,
-                double* out) {
-  const int bn = static_cast<int>(mem.size());
-  uint32_t* d = ctx->ws<uint32_t>(S_BLKTAB, bn);
-  TLG_CUDA(cudaMemcpyAsync(d, mem.data(), bn * 4, cudaMemcpyHostToDevice, ctx->stream));
-  k_gather_sub<<<std::min((bn * bn + 255) / 256, 1024), 256, 0, ctx->stream>>>(H, ldh, d, bn, out);
-  TLG_LAUNCHED(ctx);
-  TLG_CUDA(cudaStreamSynchronize(ctx->stream));
-}
 
 // ---------------------------------------------------------------------------
 // fit_batch_ridge (terrain_model.cpp:269-308): H = lambda I + sum m m^T,
 // b = sum m z, w = H^-1 b (Cholesky), info_inv_b = (H_bb)^-1.
+__global__ void k_scatter_w(const uint32_t* __restrict__ merged, int n, const double* __restrict__ b,
+                            double* __restrict__ w) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) w[merged[r]] = b[r];
+}
+
+// terrain_model.cpp:269-308: w = (lambda I + Mt Mt^T)^-1 Mt z and
+// info_inv_b = (H_bb)^-1. Rows are merged block by block in the spatial
+// order (H is then block-banded: banded Gram, banded 32-wide Cholesky, one
+// banded forward/backward solve); the diagonal-block inverses run batched
+// before the factorisation overwrites H.
 void batch_fit_device(tlg_model* m, const double* x, const double* y, const double* z,
                       size_t mm) {
   tlg_ctx* ctx = m->ctx;
   cudaStream_t s = ctx->stream;
   ensure_grid(m);
-  const int n = static_cast<int>(m->hcx.size());
-  if (n == 0) return;
-  require(static_cast<size_t>(n) * 8 <= 200 * 1024, TLG_RUNTIME_ERROR,
-          "dense batch ridge fit limited to 25600 centres");
-  const Csr c = build_csr(m, x, y, mm, nullptr, m->kc.neg_inv_2st2, m->kc.scale, false, nullptr);
+  const int nc = static_cast<int>(m->hcx.size());
+  if (nc == 0) return;
+  const size_t dense_bytes = static_cast<size_t>(nc) * nc * 8;
+  require(dense_bytes <= (size_t{64} << 30), TLG_OUT_OF_MEMORY,
+          "batch ridge fit: the n x n system exceeds 64 GiB of device memory");
+  std::vector<uint32_t> blocks;
+  for (uint32_t bb = 0; bb < m->members.size(); ++bb)
+    if (!m->members[bb].empty()) blocks.push_back(bb);
+  const auto btile = spatial_block_order(m, blocks);
+  std::vector<uint32_t> merged;
+  std::vector<BlockTab> tab(blocks.size());
+  for (size_t q = 0; q < blocks.size(); ++q) {
+    const uint32_t bb = blocks[q];
+    tab[q].pool_off = m->blk_off[bb];
+    tab[q].ld = m->blk_ld[bb];
+    tab[q].n = static_cast<int>(m->members[bb].size());
+    tab[q].off = static_cast<int>(merged.size());
+    merged.insert(merged.end(), m->members[bb].begin(), m->members[bb].end());
+  }
+  const int n = static_cast<int>(merged.size());
+  const int band = btile.empty() ? n : block_band(btile, blocks, tab);
+  uint32_t* hm = static_cast<uint32_t*>(ctx->host_stage(n * sizeof(uint32_t)));
+  std::memcpy(hm, merged.data(), n * sizeof(uint32_t));
+  uint32_t* d_merged = ctx->ws<uint32_t>(S_MERGED, n);
+  TLG_CUDA(cudaMemcpyAsync(d_merged, hm, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  int* rowof = ctx->ws<int>(S_ROWOF, nc);
+  TLG_CUDA(cudaMemsetAsync(rowof, 0xff, nc * 4, s));
+  k_scatter_rowof<<<(n + 255) / 256, 256, 0, s>>>(d_merged, n, rowof);
+  TLG_LAUNCHED(ctx);
+  const Csr c = build_csr(m, x, y, mm, rowof, m->kc.neg_inv_2st2, m->kc.scale, false, nullptr);
   double* H = ctx->ws<double>(S_HMAT, static_cast<size_t>(n) * n);
   TLG_CUDA(cudaMemsetAsync(H, 0, sizeof(double) * n * n, s));
   add_diag(ctx, H, n, n, m->kernel.lambda);
   const TCsr t = transpose_csr(ctx, c, mm, n);
-  const size_t smem = static_cast<size_t>(n) * 8;
-  if (smem > 48 * 1024)
-    TLG_CUDA(cudaFuncSetAttribute(k_gram_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_gram_rows<<<n, 128, smem, s>>>(t.rowp, t.obs, t.val, c.rowp, c.col, c.val, n, H, n);
+  gram_band(ctx, t, c, n, band, H, n);
+  double* bvec = ctx->ws<double>(S_WORK3, n);
+  k_row_dot<<<(n + 255) / 256, 256, 0, s>>>(t.rowp, t.obs, t.val, z, n, bvec);
   TLG_LAUNCHED(ctx);
-  double* b = ctx->ws<double>(S_WORK3, n);
-  k_row_dot<<<(n + 255) / 256, 256, 0, s>>>(t.rowp, t.obs, t.val, z, n, b);
-  TLG_LAUNCHED(ctx);
-  // per-block H_bb (gathered by member ids) inverses (:298-306)
-  const int nb = static_cast<int>(m->members.size());
-  for (int bb = 0; bb < nb; ++bb) {
-    const auto& mem = m->members[bb];
-    const int bn = static_cast<int>(mem.size());
-    if (!bn) continue;
-    double* Hb = ctx->ws<double>(S_SMAT, static_cast<size_t>(bn) * bn);
-    gather_sub(ctx, H, n, mem, Hb);
-    if (!spd_inverse(ctx, Hb, bn, bn, m->pool.p + m->blk_off[bb], m->blk_ld[bb]))
-      throw Error(TLG_RUNTIME_ERROR, "ridge solve failed (block factorisation)");
-  }
   int* info = ctx->ws<int>(S_FLAGS, 4);
   TLG_CUDA(cudaMemsetAsync(info, 0, 4 * sizeof(int), s));
-  double* X = ctx->ws<double>(S_YMAT, static_cast<size_t>(n) * n);
-  potrf_lower(ctx, H, n, n, info, X, n);
+  // info_inv_b = (H_bb)^-1 (:298-306), from H before it is factored
+  int maxq = 0;
+  for (const auto& tq : tab) maxq = std::max(maxq, tq.n);
+  if (maxq <= kBatchInvMax) {
+    std::vector<InvJob> jobs(tab.size());
+    for (size_t q = 0; q < tab.size(); ++q)
+      jobs[q] = InvJob{H + tab[q].off + static_cast<size_t>(tab[q].off) * n,
+                       m->pool.p + tab[q].pool_off, n, tab[q].ld, tab[q].n, 0};
+    batched_spd_inverse(ctx, jobs, info + 1);
+  } else {
+    for (size_t q = 0; q < tab.size(); ++q)
+      if (!spd_inverse(ctx, H + tab[q].off + static_cast<size_t>(tab[q].off) * n, n, tab[q].n,
+                       m->pool.p + tab[q].pool_off, tab[q].ld))
+        throw Error(TLG_RUNTIME_ERROR, "ridge solve failed (block factorisation)");
+  }
+  potrf_lower(ctx, H, n, n, info, nullptr, 0, band);
   double* mnx = ctx->ws<double>(S_PARTIALS, 2);
   k_diag_minmax<<<1, 256, 0, s>>>(H, n, n, mnx);
   TLG_LAUNCHED(ctx);
-  // w = H^-1 b = X^T (X b)
-  double* v = ctx->ws<double>(S_SOLVE, n);
-  gemm(ctx, GemmDesc{n, 1, n, X, n, 0, b, n, 0, v, n, 1.0, 0.0, 2});
-  gemm(ctx, GemmDesc{n, 1, n, X, n, 1, v, n, 0, b, n, 1.0, 0.0, 0});
-  int h = 0;
+  band_solve(ctx, H, n, n, band, bvec);
+  int h[2] = {0, 0};
   double cond[2];
-  TLG_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, s));
+  TLG_CUDA(cudaMemcpyAsync(h, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
   TLG_CUDA(cudaMemcpyAsync(cond, mnx, sizeof(cond), cudaMemcpyDeviceToHost, s));
   TLG_CUDA(cudaStreamSynchronize(s));
-  if (h)
+  if (h[1]) throw Error(TLG_RUNTIME_ERROR, "ridge solve failed (block factorisation)");
+  if (h[0])
     throw Error(TLG_RUNTIME_ERROR, "ridge solve failed; condition estimate " +
                                        std::to_string(cond[0] / std::max(cond[1], 1e-300)));
-  TLG_CUDA(cudaMemcpyAsync(m->w.p, b, n * 8, cudaMemcpyDeviceToDevice, s));
+  k_scatter_w<<<(n + 255) / 256, 256, 0, s>>>(d_merged, n, bvec, m->w.p);
+  TLG_LAUNCHED(ctx);
   sync_weights_to_grid(m);
   TLG_CUDA(cudaStreamSynchronize(s));
 }
