@@ -127,7 +127,10 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
   }
 #pragma unroll
   for (int l = 0; l < WIN; ++l) eyd[l] *= ey[l];
-  const double* wbase = L.W + static_cast<size_t>(i0) * L.nj + j0;
+  const size_t bidx = static_cast<size_t>(i0) * L.nj + j0;
+  // compiled geometries read the window in 16-byte pairs: an odd base is
+  // served from the one-element-shifted copy W1 (the pitch nj is even)
+  const double* wbase = (G >= 0 && (bidx & 1)) ? L.W1 + bidx + 1 : L.W + bidx;
   const AxisNode a0 = L.ax[i0];
   const double dx_first = __dsub_rn(a0.c, x);
   double ex_e = 0.0, ex_p = 0.0;
@@ -151,29 +154,32 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
     bool any;
     if constexpr (G >= 0) {
       // compiled geometry: always-outside pairs vanish, always-inside pairs
-      // carry no test, only boundary pairs run the exact reference test
+      // carry no test, only boundary pairs run the exact reference test;
+      // weights arrive two rows per 16-byte load
       constexpr uint32_t im = kGeoms[G].in[k], bm = kGeoms[G].bd[k];
-      static_for<0, WIN>([&](auto LC) {
-        constexpr int l = decltype(LC)::value;
-        if constexpr ((im >> l) & 1u) {
-          const double w = __ldg(wc + l);
-          S = fma(w, ey[l], S);
-          T = fma(w, eyd[l], T);
-        } else if constexpr ((bm >> l) & 1u) {
-#ifdef TLG_BD_BRANCH
-          if (__dadd_rn(dx2, dy2[l]) <= r2) {
-            const double w = __ldg(wc + l);
-            S = fma(w, ey[l], S);
-            T = fma(w, eyd[l], T);
-          }
-#else
-          const double w = __dadd_rn(dx2, dy2[l]) <= r2 ? __ldg(wc + l) : 0.0;
-          S = fma(w, ey[l], S);
-          T = fma(w, eyd[l], T);
-#endif
+      constexpr uint32_t need = im | bm;
+      static_for<0, (WIN + 1) / 2>([&](auto PC) {
+        constexpr int pr = decltype(PC)::value;
+        constexpr uint32_t pm = (need >> (2 * pr)) & 3u;
+        if constexpr (pm != 0) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(wc) + pr);
+          static_for<0, 2>([&](auto HC) {
+            constexpr int l = 2 * pr + decltype(HC)::value;
+            if constexpr (l < WIN) {
+              const double wv = decltype(HC)::value ? v.y : v.x;
+              if constexpr ((im >> l) & 1u) {
+                S = fma(wv, ey[l], S);
+                T = fma(wv, eyd[l], T);
+              } else if constexpr ((bm >> l) & 1u) {
+                const double w = __dadd_rn(dx2, dy2[l]) <= r2 ? wv : 0.0;
+                S = fma(w, ey[l], S);
+                T = fma(w, eyd[l], T);
+              }
+            }
+          });
         }
       });
-      any = (im | bm) != 0;
+      any = need != 0;
     } else {
       const uint32_t im = L.inmask[k], bm = L.bdmask[k];
 #pragma unroll

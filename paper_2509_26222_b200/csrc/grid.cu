@@ -97,8 +97,9 @@ __global__ void k_lattice_check(const double* __restrict__ cx, const double* __r
 __global__ void k_lattice_fill(const double* __restrict__ cx, const double* __restrict__ cy,
                                const double* __restrict__ w, size_t n, double min_x,
                                double min_y, double res, int i_org, int j_org, int nj,
-                               double* __restrict__ W, int* __restrict__ P,
-                               int* __restrict__ slot, int* __restrict__ dup) {
+                               double* __restrict__ W, double* __restrict__ W1,
+                               int* __restrict__ P, int* __restrict__ slot,
+                               int* __restrict__ dup) {
   for (size_t c = blockIdx.x * (size_t)blockDim.x + threadIdx.x; c < n;
        c += (size_t)gridDim.x * blockDim.x) {
     const int i = static_cast<int>(llround((cx[c] - min_x) / res)) - i_org;
@@ -106,6 +107,7 @@ __global__ void k_lattice_fill(const double* __restrict__ cx, const double* __re
     const int s = i * nj + j;
     slot[c] = s;
     W[s] = w[c];
+    W1[s + 1] = w[c];
     if (atomicAdd(&P[s], 1) != 0) atomicOr(dup, 1);
   }
 }
@@ -119,9 +121,12 @@ __global__ void k_lattice_axes(double min_v, double res, int org, int count, dou
 }
 
 __global__ void k_lattice_refresh(const int* __restrict__ slot, const double* __restrict__ w,
-                                  size_t n, double* __restrict__ W) {
+                                  size_t n, double* __restrict__ W, double* __restrict__ W1) {
   const size_t c = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (c < n) W[slot[c]] = w[c];
+  if (c < n) {
+    W[slot[c]] = w[c];
+    W1[slot[c] + 1] = w[c];
+  }
 }
 
 // Window geometry and pair classes (host: ~WIN^2 scalar parameter setup).
@@ -170,19 +175,22 @@ static void build_lattice(tlg_model* m) {
   L.i_org = h[1] - L.pad;
   L.j_org = h[2] - L.pad;
   const long long ni = static_cast<long long>(h[3]) - h[1] + 1 + 2 * L.pad;
-  const long long nj = static_cast<long long>(h[4]) - h[2] + 1 + 2 * L.pad;
+  long long nj = static_cast<long long>(h[4]) - h[2] + 1 + 2 * L.pad;
+  nj += nj & 1;  // even row pitch: a column's pair alignment is that of its base
   if (ni * nj > (1ll << 28)) return;
   L.ni = static_cast<int>(ni);
   L.nj = static_cast<int>(nj);
   const size_t nn = static_cast<size_t>(ni * nj);
-  L.W.ensure(nn);
+  L.W.ensure(nn + 2);
+  L.W1.ensure(nn + 2);
   L.P.ensure(nn);
   L.slot.ensure(n);
-  TLG_CUDA(cudaMemsetAsync(L.W.p, 0, nn * sizeof(double), s));
+  TLG_CUDA(cudaMemsetAsync(L.W.p, 0, (nn + 2) * sizeof(double), s));
+  TLG_CUDA(cudaMemsetAsync(L.W1.p, 0, (nn + 2) * sizeof(double), s));
   TLG_CUDA(cudaMemsetAsync(L.P.p, 0, nn * sizeof(int), s));
   int* dup = st + 5;
   k_lattice_fill<<<blocks, 256, 0, s>>>(m->cx.p, m->cy.p, m->w.p, n, mnx, mny, res, L.i_org,
-                                        L.j_org, L.nj, L.W.p, L.P.p, L.slot.p, dup);
+                                        L.j_org, L.nj, L.W.p, L.W1.p, L.P.p, L.slot.p, dup);
   TLG_LAUNCHED(ctx);
   L.ax.ensure(L.ni);
   L.ay.ensure(L.nj);
@@ -205,6 +213,7 @@ LatticeView lattice_view(const tlg_model* m) {
   const LatticeGrid& L = m->lat;
   LatticeView v;
   v.W = L.W.p;
+  v.W1 = L.W1.p;
   v.P = L.P.p;
   v.ax = L.ax.p;
   v.ay = L.ay.p;
@@ -320,7 +329,8 @@ void sync_weights_to_grid(tlg_model* m) {
   TLG_LAUNCHED(m->ctx);
   if (m->lat.valid) {
     k_lattice_refresh<<<(unsigned)((n + 255) / 256), 256, 0, m->ctx->stream>>>(m->lat.slot.p, m->w.p,
-                                                                          n, m->lat.W.p);
+                                                                          n, m->lat.W.p,
+                                                                          m->lat.W1.p);
     TLG_LAUNCHED(m->ctx);
   }
 }

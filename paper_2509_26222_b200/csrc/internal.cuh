@@ -285,6 +285,7 @@ struct LatticeGrid {
   int corner_ok = 0;
   int geom_id = -1;            // index into kGeoms when specialised, else -1
   DBuf<double> W;
+  DBuf<double> W1;  // W shifted by one element (W1[s + 1] = W[s]): 16-byte pair loads at odd bases
   DBuf<int> P;                 // presence count per node
   DBuf<AxisNode> ax, ay;       // per padded column / row: exact node coordinate
                                // and reference cell coordinate floor(c / cell)
@@ -293,6 +294,7 @@ struct LatticeGrid {
 
 struct LatticeView {
   const double* W;
+  const double* W1;
   const int* P;
   const AxisNode* ax;  // one 16-byte load gives coordinate + cell
   const AxisNode* ay;
