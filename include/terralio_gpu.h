@@ -136,6 +136,45 @@ tlg_status tlg_terrain_error_histogram(tlg_model* model, const double* x, const 
                                        double trim_fraction, int bins, double* edges,
                                        uint64_t* counts, uint64_t* trimmed, uint64_t* overflow);
 
+/* ---- Feature correspondences -------------------------------- */
+/* LocalMap (local_map.hpp:17-50): sliding window of frames, per-kind kNN
+ * structures; build_correspondences (scan_matcher.cpp:44-183); feature rows
+ * of total_cost (:185-216). FeatureKind codes: 0 edge, 1 planar, 2 ground. */
+typedef struct tlg_map tlg_map;
+typedef struct {
+  double corr_gate, huber_delta, plane_fit_tol, plane_eig_ratio, edge_eig_ratio, edge_fit_tol,
+      edge_min_extent, trim_ratio, trim_floor, ground_corr_voxel, ground_corr_radius;
+} tlg_match_config; /* SolverConfig fields used by the association (scan_matcher.hpp:15-49) */
+tlg_status tlg_match_config_default(tlg_match_config* cfg);
+tlg_status tlg_map_create(tlg_ctx* ctx, double voxel_size, size_t window, tlg_map** out);
+tlg_status tlg_map_destroy(tlg_map* map);
+/* LocalMap::insert (local_map.cpp:19-45): sensor-frame points, kinds, labels
+ * (NULL = -1), pose R (row-major) / t. */
+tlg_status tlg_map_insert(tlg_map* map, const double* px, const double* py, const double* pz,
+                          const uint8_t* kind, const int32_t* label, size_t n, tlg_mem mem,
+                          const double R[9], const double t[3]);
+/* Map points of one kind (0 edge, 1 planar) in map-id order: xyz (3 per
+ * point) and labels on the host, up to cap; *count = total. */
+tlg_status tlg_map_points(tlg_map* map, int kind, double* xyz, int32_t* labels, size_t cap,
+                          size_t* count);
+/* build_correspondences: the result stays in the map object (feature order
+ * after the trims); *count = correspondences. */
+tlg_status tlg_build_correspondences(tlg_map* map, const double* px, const double* py,
+                                     const double* pz, const uint8_t* kind, size_t n,
+                                     tlg_mem mem, const double R[9], const double t[3],
+                                     const tlg_match_config* cfg, size_t* count);
+/* The last correspondences on the host (any pointer may be NULL): kind (0
+ * edge, 1 plane), feature index, params[7] (edge: point xyz, direction xyz;
+ * plane: normal xyz, offset), weight, majority label, distance, plane fit
+ * quality (smallest eigenvalue; 0 for edges). */
+tlg_status tlg_correspondences_get(tlg_map* map, int32_t* kind, uint32_t* feature,
+                                   double* params, double* weight, int32_t* label, double* dist,
+                                   double* fitq, size_t cap);
+/* Feature rows of total_cost at pose (R, t) for the last correspondences,
+ * reduced to the normal equations (valid = rows). */
+tlg_status tlg_feature_normal_eq(tlg_map* map, const double R[9], const double t[3],
+                                 tlg_normal_eq* ne);
+
 /* ---- kernel.cpp ------------------------------------------------------------- */
 /* KernelParams::finalize (kernel.cpp:15-25): fills the auto cutoff, validates. */
 tlg_status tlg_kernel_finalize(tlg_kernel_params* p);

@@ -109,6 +109,20 @@ def load():
         _lib.orc_terrain_error_histogram.argtypes = [
             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_double, C.c_int,
             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.orc_map_new.restype = C.c_void_p
+        _lib.orc_map_new.argtypes = [C.c_double, C.c_size_t]
+        _lib.orc_map_free.argtypes = [C.c_void_p]
+        _lib.orc_map_insert.argtypes = [C.c_void_p] + [C.c_void_p] * 5 + [C.c_size_t, C.c_void_p,
+                                                                          C.c_void_p]
+        _lib.orc_map_points.restype = C.c_size_t
+        _lib.orc_map_points.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_size_t]
+        _lib.orc_knn.restype = C.c_size_t
+        _lib.orc_knn.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
+                                 C.c_double, C.c_void_p]
+        _lib.orc_build_correspondences.restype = C.c_size_t
+        _lib.orc_build_correspondences.argtypes = [C.c_void_p] + [C.c_void_p] * 4 + [
+            C.c_size_t] + [C.c_void_p] * 10
+        _lib.orc_feature_normal_eq.argtypes = [C.c_size_t] + [C.c_void_p] * 7
         _lib.orc_export_grid.restype = C.c_size_t
         _lib.orc_export_grid.argtypes = [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_size_t]
@@ -377,6 +391,84 @@ def select_ground_points(p, kind, R, t, roi, radius, voxel, max_points):
                                          int(max_points), _p(ox), _p(oy), _p(oz), C.byref(n)))
     k = n.value
     return np.stack([ox[:k], oy[:k]], 1), oz[:k].copy()
+
+
+MATCH_DEFAULTS = dict(corr_gate=1.0, huber_delta=0.1, plane_fit_tol=0.025, plane_eig_ratio=5.0,
+                      edge_eig_ratio=3.0, edge_fit_tol=0.05, edge_min_extent=0.05,
+                      trim_ratio=5.0, trim_floor=0.003, ground_corr_voxel=0.25,
+                      ground_corr_radius=4.0)
+
+
+def _cfg_vec(cfg):
+    c = dict(MATCH_DEFAULTS)
+    c.update(cfg or {})
+    return np.array([c[k] for k in MATCH_DEFAULTS], dtype=np.float64)
+
+
+class LocalMap:
+    """local_map.cpp restated (oracle)."""
+
+    def __init__(self, voxel_size=0.1, window=20):
+        self.h = load().orc_map_new(float(voxel_size), int(window))
+
+    def __del__(self):
+        try:
+            load().orc_map_free(self.h)
+        except Exception:
+            pass
+
+    def insert(self, p, kind, label, R, t):
+        p = _f64(p)
+        cols = [np.ascontiguousarray(p[:, j]) for j in range(3)]
+        kind = np.ascontiguousarray(np.asarray(kind, dtype=np.uint8))
+        label = np.ascontiguousarray(np.asarray(label, dtype=np.int32))
+        load().orc_map_insert(self.h, _p(cols[0]), _p(cols[1]), _p(cols[2]), _p(kind), _p(label),
+                              len(kind), _p(_f64(R).reshape(9)), _p(_f64(t).reshape(3)))
+
+    def points(self, kind):
+        n = load().orc_map_points(self.h, kind, None, None, 0)
+        xyz = np.empty((n, 3))
+        lab = np.empty(n, dtype=np.int32)
+        load().orc_map_points(self.h, kind, _p(xyz), _p(lab), n)
+        return xyz, lab
+
+    def knn(self, kind, q, k, gate):
+        out = np.empty(k, dtype=np.uint32)
+        m = load().orc_knn(self.h, kind, float(q[0]), float(q[1]), float(q[2]), int(k),
+                           float(gate), _p(out))
+        return out[:m].copy()
+
+    def build_correspondences(self, p, kind, R, t, cfg=None):
+        p = _f64(p)
+        cols = [np.ascontiguousarray(p[:, j]) for j in range(3)]
+        kind = np.ascontiguousarray(np.asarray(kind, dtype=np.uint8))
+        n = len(kind)
+        ck = np.empty(n, dtype=np.int32)
+        cf = np.empty(n, dtype=np.uint32)
+        prm = np.empty((n, 7))
+        w = np.empty(n)
+        lab = np.empty(n, dtype=np.int32)
+        dist = np.empty(n)
+        fq = np.empty(n)
+        m = load().orc_build_correspondences(
+            self.h, _p(cols[0]), _p(cols[1]), _p(cols[2]), _p(kind), n, _p(_f64(R).reshape(9)),
+            _p(_f64(t).reshape(3)), _p(_cfg_vec(cfg)), _p(ck), _p(cf), _p(prm), _p(w), _p(lab),
+            _p(dist), _p(fq))
+        return {"kind": ck[:m].copy(), "feature": cf[:m].copy(), "params": prm[:m].copy(),
+                "weight": w[:m].copy(), "label": lab[:m].copy(), "dist": dist[:m].copy(),
+                "fitq": fq[:m].copy()}
+
+
+def feature_normal_eq(corr, p_sensor, R, t):
+    """Feature rows of total_cost (scan_matcher.cpp:185-216) -> ne29."""
+    ck = np.ascontiguousarray(corr["kind"], dtype=np.int32)
+    ps = _f64(np.asarray(p_sensor)[corr["feature"]])
+    prm = _f64(corr["params"])
+    w = _f64(corr["weight"])
+    out = np.empty(29)
+    load().orc_feature_normal_eq(len(ck), _p(ck), _p(ps), _p(prm), _p(w), _p(_f64(R).reshape(9)),
+                                 _p(_f64(t).reshape(3)), _p(out))
+    return out
 
 
 def fit_batch_ridge(kernel, centers, xy, z):

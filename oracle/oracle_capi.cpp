@@ -403,4 +403,128 @@ size_t orc_export_grid(void* m, double step, double* x, double* y, double* z, si
   return xs.size();
 }
 
+
+// ---- feature correspondences (scan_matcher.cpp:44-216, local_map.cpp) ------
+void* orc_map_new(double voxel, size_t window) {
+  MapConfig c;
+  c.voxel_size = voxel;
+  c.window = window;
+  return new LocalMap(c);
+}
+void orc_map_free(void* m) { delete static_cast<LocalMap*>(m); }
+static FeatureInput to_features(const double* px, const double* py, const double* pz,
+                                const unsigned char* kind, const int* label, size_t n) {
+  FeatureInput f;
+  f.p.resize(n);
+  f.kind.assign(kind, kind + n);
+  f.label.assign(n, -1);
+  for (size_t i = 0; i < n; ++i) {
+    f.p[i] = {px[i], py[i], pz[i]};
+    if (label) f.label[i] = label[i];
+  }
+  return f;
+}
+static M3 to_m3(const double* R) {
+  M3 m;
+  std::memcpy(m.a, R, sizeof(m.a));
+  return m;
+}
+void orc_map_insert(void* m, const double* px, const double* py, const double* pz,
+                    const unsigned char* kind, const int* label, size_t n, const double* R,
+                    const double* t) {
+  static_cast<LocalMap*>(m)->insert(to_features(px, py, pz, kind, label, n), to_m3(R),
+                                    {t[0], t[1], t[2]});
+}
+// kind 0 edge / 1 planar: count, and if xyz != NULL the points (cap) + labels
+size_t orc_map_points(void* m, int kind, double* xyz, int* labels, size_t cap) {
+  auto* mp = static_cast<LocalMap*>(m);
+  const auto& pts = kind == 0 ? mp->edge : mp->planar;
+  const auto& lab = kind == 0 ? mp->edge_label : mp->planar_label;
+  for (size_t i = 0; xyz && i < pts.size() && i < cap; ++i) {
+    xyz[3 * i] = pts[i].x;
+    xyz[3 * i + 1] = pts[i].y;
+    xyz[3 * i + 2] = pts[i].z;
+    if (labels) labels[i] = lab[i];
+  }
+  return pts.size();
+}
+size_t orc_knn(void* m, int kind, double qx, double qy, double qz, int k, double gate,
+               unsigned* out) {
+  auto* mp = static_cast<LocalMap*>(m);
+  const auto ids = knn(kind == 0 ? mp->edge : mp->planar, {qx, qy, qz}, k, gate);
+  for (size_t i = 0; i < ids.size(); ++i) out[i] = ids[i];
+  return ids.size();
+}
+// cfg: corr_gate, huber_delta, plane_fit_tol, plane_eig_ratio, edge_eig_ratio,
+// edge_fit_tol, edge_min_extent, trim_ratio, trim_floor, ground_corr_voxel,
+// ground_corr_radius. Outputs (capacity n): kind, feature index, params[7]
+// (edge: point xyz, dir xyz, 0; plane: normal xyz, offset, 0, 0, 0), weight,
+// label, dist, fitq.
+size_t orc_build_correspondences(void* m, const double* px, const double* py, const double* pz,
+                                 const unsigned char* kind, size_t n, const double* R,
+                                 const double* t, const double* cfg, int* ckind,
+                                 unsigned* cfeat, double* params, double* weight, int* label,
+                                 double* dist, double* fitq) {
+  SolverConfigM c;
+  c.corr_gate = cfg[0];
+  c.huber_delta = cfg[1];
+  c.plane_fit_tol = cfg[2];
+  c.plane_eig_ratio = cfg[3];
+  c.edge_eig_ratio = cfg[4];
+  c.edge_fit_tol = cfg[5];
+  c.edge_min_extent = cfg[6];
+  c.trim_ratio = cfg[7];
+  c.trim_floor = cfg[8];
+  c.ground_corr_voxel = cfg[9];
+  c.ground_corr_radius = cfg[10];
+  const auto out = build_correspondences(to_features(px, py, pz, kind, nullptr, n), to_m3(R),
+                                         {t[0], t[1], t[2]}, *static_cast<LocalMap*>(m), c);
+  for (size_t i = 0; i < out.size(); ++i) {
+    const auto& o = out[i];
+    ckind[i] = o.kind;
+    cfeat[i] = o.feature;
+    double* pr = params + 7 * i;
+    if (o.kind == 0) {
+      pr[0] = o.line_point.x; pr[1] = o.line_point.y; pr[2] = o.line_point.z;
+      pr[3] = o.line_dir.x; pr[4] = o.line_dir.y; pr[5] = o.line_dir.z; pr[6] = 0.0;
+    } else {
+      pr[0] = o.normal.x; pr[1] = o.normal.y; pr[2] = o.normal.z; pr[3] = o.offset;
+      pr[4] = pr[5] = pr[6] = 0.0;
+    }
+    weight[i] = o.weight;
+    label[i] = o.label;
+    dist[i] = o.dist;
+    fitq[i] = o.fitq;
+  }
+  return out.size();
+}
+// feature rows of total_cost at (R, t) -> ne29 (A upper 21, g 6, cost, rows)
+void orc_feature_normal_eq(size_t nc, const int* ckind, const double* ps, const double* params,
+                           const double* weight, const double* R, const double* t, double* ne29) {
+  std::vector<Correspondence> cs(nc);
+  for (size_t i = 0; i < nc; ++i) {
+    auto& c = cs[i];
+    c.kind = ckind[i];
+    c.p_sensor = {ps[3 * i], ps[3 * i + 1], ps[3 * i + 2]};
+    const double* pr = params + 7 * i;
+    if (c.kind == 0) {
+      c.line_point = {pr[0], pr[1], pr[2]};
+      c.line_dir = {pr[3], pr[4], pr[5]};
+    } else {
+      c.normal = {pr[0], pr[1], pr[2]};
+      c.offset = pr[3];
+    }
+    c.weight = weight[i];
+  }
+  NormalEq ne;
+  size_t rows = 0;
+  feature_normal_eq(cs, to_m3(R), {t[0], t[1], t[2]}, ne, &rows);
+  int k = 0;
+  for (int i = 0; i < 6; ++i)
+    for (int j = i; j < 6; ++j) ne29[k++] = ne.A[6 * i + j];
+  for (int i = 0; i < 6; ++i) ne29[21 + i] = ne.g[i];
+  ne29[27] = ne.cost;
+  ne29[28] = static_cast<double>(rows);
+}
+
 }  // extern "C"

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <fstream>
 #include <limits>
+#include <map>
 #include <set>
 #include <unordered_set>
 
@@ -812,6 +813,287 @@ void export_grid(const TerrainModel& model, double grid_step, std::vector<double
       zs.push_back(q.z);
     }
   }
+}
+
+// --- local_map.cpp:8-62 --------------------------------------------------------
+static std::int64_t map_voxel_key(const V3& p, double size) {
+  auto q = [&](double v) { return static_cast<std::int64_t>(std::floor(v / size)) & 0x1fffff; };
+  return (q(p.x) << 42) | (q(p.y) << 21) | q(p.z);
+}
+
+void LocalMap::insert(const FeatureInput& scan, const M3& R, const V3& t) {
+  Frame fr;
+  std::unordered_set<std::int64_t> edge_seen, planar_seen;
+  for (std::size_t i = 0; i < scan.p.size(); ++i) {
+    const V3 q0 = mul(R, scan.p[i]);
+    const V3 p{q0.x + t.x, q0.y + t.y, q0.z + t.z};
+    if (scan.kind[i] == 0) {
+      if (cfg_.voxel_size > 0.0 && !edge_seen.insert(map_voxel_key(p, cfg_.voxel_size)).second)
+        continue;
+      fr.edge.push_back(p);
+      fr.edge_label.push_back(scan.label[i]);
+    } else {
+      if (cfg_.voxel_size > 0.0 && !planar_seen.insert(map_voxel_key(p, cfg_.voxel_size)).second)
+        continue;
+      fr.planar.push_back(p);
+      fr.planar_label.push_back(scan.label[i]);
+    }
+  }
+  frames_.push_back(std::move(fr));
+  while (frames_.size() > cfg_.window) frames_.erase(frames_.begin());
+  edge.clear();
+  planar.clear();
+  edge_label.clear();
+  planar_label.clear();
+  for (const Frame& f : frames_) {
+    edge.insert(edge.end(), f.edge.begin(), f.edge.end());
+    planar.insert(planar.end(), f.planar.begin(), f.planar.end());
+    edge_label.insert(edge_label.end(), f.edge_label.begin(), f.edge_label.end());
+    planar_label.insert(planar_label.end(), f.planar_label.begin(), f.planar_label.end());
+  }
+}
+
+// kdtree.hpp:31-41/:79-99: the k smallest (d2, id) with d2 <= gate^2, ascending
+std::vector<std::uint32_t> knn(const std::vector<V3>& pts, const V3& q, int k, double gate) {
+  const double gate2 = gate * gate;
+  std::vector<std::pair<double, std::uint32_t>> cand;
+  for (std::uint32_t i = 0; i < pts.size(); ++i) {
+    const double dx = pts[i].x - q.x, dy = pts[i].y - q.y, dz = pts[i].z - q.z;
+    const double d2 = (dx * dx + dy * dy) + dz * dz;
+    if (d2 <= gate2) cand.emplace_back(d2, i);
+  }
+  const std::size_t m = std::min<std::size_t>(cand.size(), static_cast<std::size_t>(k));
+  std::partial_sort(cand.begin(), cand.begin() + m, cand.end());
+  std::vector<std::uint32_t> out(m);
+  for (std::size_t i = 0; i < m; ++i) out[i] = cand[i].second;
+  return out;
+}
+
+// cyclic Jacobi on a symmetric 3x3 (row-major in, column-major vectors out)
+void eigen_sym3(const double A[9], double evals[3], double evecs[9]) {
+  double a[3][3], v[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) a[i][j] = A[3 * i + j];
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    const double off = std::fabs(a[0][1]) + std::fabs(a[0][2]) + std::fabs(a[1][2]);
+    if (off == 0.0) break;
+    for (int p = 0; p < 2; ++p)
+      for (int q = p + 1; q < 3; ++q) {
+        if (a[p][q] == 0.0) continue;
+        const double theta = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
+        const double tt = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(tt * tt + 1.0), sn = tt * c;
+        for (int r = 0; r < 3; ++r) {  // A <- A G
+          const double arp = a[r][p], arq = a[r][q];
+          a[r][p] = c * arp - sn * arq;
+          a[r][q] = sn * arp + c * arq;
+        }
+        for (int r = 0; r < 3; ++r) {  // A <- G^T A
+          const double apr = a[p][r], aqr = a[q][r];
+          a[p][r] = c * apr - sn * aqr;
+          a[q][r] = sn * apr + c * aqr;
+        }
+        a[p][q] = a[q][p] = 0.0;
+        for (int r = 0; r < 3; ++r) {
+          const double vrp = v[r][p], vrq = v[r][q];
+          v[r][p] = c * vrp - sn * vrq;
+          v[r][q] = sn * vrp + c * vrq;
+        }
+      }
+  }
+  int idx[3] = {0, 1, 2};  // stable insertion sort, ascending eigenvalues
+  for (int i = 1; i < 3; ++i)
+    for (int j = i; j > 0 && a[idx[j]][idx[j]] < a[idx[j - 1]][idx[j - 1]]; --j)
+      std::swap(idx[j], idx[j - 1]);
+  for (int c = 0; c < 3; ++c) {
+    evals[c] = a[idx[c]][idx[c]];
+    for (int r = 0; r < 3; ++r) evecs[3 * c + r] = v[r][idx[c]];
+  }
+}
+
+// scan_matcher.cpp:21-33
+static std::int32_t majority_label(const std::vector<std::int32_t>& labels) {
+  std::map<std::int32_t, int> counts;
+  for (auto l : labels) ++counts[l];
+  std::int32_t best = -1;
+  int best_n = 0;
+  for (const auto& [l, n] : counts)
+    if (n > best_n) {
+      best = l;
+      best_n = n;
+    }
+  return best;
+}
+
+static V3 normalized(const V3& v) {
+  const double n = std::sqrt((v.x * v.x + v.y * v.y) + v.z * v.z);
+  return {v.x / n, v.y / n, v.z / n};
+}
+
+// residuals.cpp:7-25
+static V3 line_residual(const V3& p, const V3& q, const V3& d, double J[9]) {
+  const double dd[3] = {d.x, d.y, d.z};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) J[3 * i + j] = (i == j ? 1.0 : 0.0) - dd[i] * dd[j];
+  const double e[3] = {p.x - q.x, p.y - q.y, p.z - q.z};
+  V3 r;
+  double* rr[3] = {&r.x, &r.y, &r.z};
+  for (int i = 0; i < 3; ++i) *rr[i] = (J[3 * i] * e[0] + J[3 * i + 1] * e[1]) + J[3 * i + 2] * e[2];
+  return r;
+}
+static double plane_residual(const V3& p, const V3& n, double offset) {
+  return ((n.x * p.x + n.y * p.y) + n.z * p.z) + offset;
+}
+static double norm3(const V3& v) { return std::sqrt((v.x * v.x + v.y * v.y) + v.z * v.z); }
+
+// scan_matcher.cpp:44-183
+std::vector<Correspondence> build_correspondences(const FeatureInput& f, const M3& R, const V3& t,
+                                                  const LocalMap& map, const SolverConfigM& cfg) {
+  std::vector<Correspondence> out;
+  if (map.edge.empty() && map.planar.empty()) return out;
+  std::set<std::pair<std::int64_t, std::int64_t>> ground_cells;
+  for (std::uint32_t i = 0; i < f.p.size(); ++i) {
+    const V3 q0 = mul(R, f.p[i]);
+    const V3 pw{q0.x + t.x, q0.y + t.y, q0.z + t.z};
+    if (f.kind[i] == 2) {
+      if (cfg.ground_corr_radius > 0.0 &&
+          std::sqrt(sqnorm(pw.x - t.x, pw.y - t.y)) > cfg.ground_corr_radius)
+        continue;
+      if (cfg.ground_corr_voxel > 0.0) {
+        const double v = cfg.ground_corr_voxel;
+        const auto cell = std::make_pair(static_cast<std::int64_t>(std::floor(pw.x / v)),
+                                         static_cast<std::int64_t>(std::floor(pw.y / v)));
+        if (!ground_cells.insert(cell).second) continue;
+      }
+    }
+    const bool edge = f.kind[i] == 0;
+    const std::vector<V3>& pts = edge ? map.edge : map.planar;
+    const std::vector<std::int32_t>& lab = edge ? map.edge_label : map.planar_label;
+    const int k = edge ? 5 : 8;
+    if (pts.empty()) continue;
+    const auto nn = knn(pts, pw, k, cfg.corr_gate);
+    if (static_cast<int>(nn.size()) < k) continue;
+    V3 cen{0.0, 0.0, 0.0};
+    for (auto id : nn) {
+      cen.x += pts[id].x;
+      cen.y += pts[id].y;
+      cen.z += pts[id].z;
+    }
+    cen = {cen.x / nn.size(), cen.y / nn.size(), cen.z / nn.size()};
+    double S[9] = {0};
+    std::vector<std::int32_t> labels;
+    for (auto id : nn) {
+      const double d[3] = {pts[id].x - cen.x, pts[id].y - cen.y, pts[id].z - cen.z};
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) S[3 * a + b] += d[a] * d[b];
+      labels.push_back(lab[id]);
+    }
+    double ev[3], evec[9];
+    eigen_sym3(S, ev, evec);
+    Correspondence c;
+    c.feature = i;
+    c.p_sensor = f.p[i];
+    c.label = majority_label(labels);
+    if (edge) {
+      if (ev[2] < cfg.edge_eig_ratio * std::max(ev[1], 1e-12)) continue;
+      if (ev[2] < cfg.edge_min_extent * cfg.edge_min_extent) continue;
+      c.kind = 0;
+      c.line_point = cen;
+      c.line_dir = normalized({evec[6], evec[7], evec[8]});
+      bool on_line = true;
+      double J[9];
+      for (auto id : nn)
+        if (norm3(line_residual(pts[id], c.line_point, c.line_dir, J)) > cfg.edge_fit_tol) {
+          on_line = false;
+          break;
+        }
+      if (!on_line) continue;
+      const double dist = norm3(line_residual(pw, c.line_point, c.line_dir, J));
+      if (dist > cfg.corr_gate) continue;
+      if (cfg.huber_delta > 0.0 && dist > cfg.huber_delta) c.weight = cfg.huber_delta / dist;
+      c.dist = dist;
+      c.fitq = 0.0;
+    } else {
+      if (ev[1] < cfg.plane_eig_ratio * ev[0] || ev[1] < 1e-3) continue;
+      if (ev[2] > 50.0 * ev[1]) continue;
+      c.kind = 1;
+      c.normal = normalized({evec[0], evec[1], evec[2]});
+      c.offset = -((c.normal.x * cen.x + c.normal.y * cen.y) + c.normal.z * cen.z);
+      bool flat = true;
+      for (auto id : nn)
+        if (std::fabs(plane_residual(pts[id], c.normal, c.offset)) > cfg.plane_fit_tol) {
+          flat = false;
+          break;
+        }
+      if (!flat) continue;
+      const double dist = std::fabs(plane_residual(pw, c.normal, c.offset));
+      if (dist > cfg.corr_gate) continue;
+      if (cfg.huber_delta > 0.0 && dist > cfg.huber_delta) c.weight = cfg.huber_delta / dist;
+      c.dist = dist;
+      c.fitq = ev[0];
+    }
+    out.push_back(c);
+  }
+  if (cfg.trim_ratio > 0.0 && !out.empty()) {
+    std::vector<double> d;
+    for (const auto& c : out) d.push_back(c.dist);
+    std::nth_element(d.begin(), d.begin() + d.size() / 2, d.end());
+    const double cut = std::max(cfg.trim_ratio * d[d.size() / 2], cfg.trim_floor);
+    double qcut = std::numeric_limits<double>::infinity();
+    std::vector<double> pq;
+    for (const auto& c : out)
+      if (c.kind == 1) pq.push_back(c.fitq);
+    if (!pq.empty()) {
+      std::nth_element(pq.begin(), pq.begin() + pq.size() / 2, pq.end());
+      qcut = std::max(10.0 * pq[pq.size() / 2], 1e-7);
+    }
+    std::vector<Correspondence> kept;
+    for (const auto& c : out)
+      if (c.dist <= cut && c.fitq <= qcut) kept.push_back(c);
+    out = std::move(kept);
+  }
+  return out;
+}
+
+// scan_matcher.cpp:185-216 feature rows: p = R p_s + t, dp = [-R hat(p_s), I]
+void feature_normal_eq(const std::vector<Correspondence>& cs, const M3& R, const V3& t,
+                       NormalEq& ne, std::size_t* rows) {
+  std::size_t nr = 0;
+  for (const auto& c : cs) {
+    const V3 q0 = mul(R, c.p_sensor);
+    const V3 pw{q0.x + t.x, q0.y + t.y, q0.z + t.z};
+    const M3 H = hat(c.p_sensor);
+    double dp[3][6];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        dp[i][j] = (-R(i, 0) * H(0, j) + -R(i, 1) * H(1, j)) + -R(i, 2) * H(2, j);
+        dp[i][3 + j] = (i == j) ? 1.0 : 0.0;
+      }
+    const double sw = std::sqrt(c.weight);
+    if (c.kind == 0) {
+      double J[9];
+      const V3 r = line_residual(pw, c.line_point, c.line_dir, J);
+      const double rv[3] = {r.x, r.y, r.z};
+      for (int i = 0; i < 3; ++i) {
+        ManifoldRow row;
+        row.valid = true;
+        row.r = sw * rv[i];
+        for (int j = 0; j < 6; ++j)
+          row.J[j] = sw * ((J[3 * i] * dp[0][j] + J[3 * i + 1] * dp[1][j]) + J[3 * i + 2] * dp[2][j]);
+        accumulate(ne, row);
+        ++nr;
+      }
+    } else {
+      ManifoldRow row;
+      row.valid = true;
+      row.r = sw * plane_residual(pw, c.normal, c.offset);
+      for (int j = 0; j < 6; ++j)
+        row.J[j] = sw * ((c.normal.x * dp[0][j] + c.normal.y * dp[1][j]) + c.normal.z * dp[2][j]);
+      accumulate(ne, row);
+      ++nr;
+    }
+  }
+  if (rows) *rows = nr;
 }
 
 }  // namespace oracle

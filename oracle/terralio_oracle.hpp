@@ -266,4 +266,59 @@ Histogram terrain_error_histogram(const TerrainModel& model, const std::vector<V
 void export_grid(const TerrainModel& model, double grid_step, std::vector<double>& x,
                  std::vector<double>& y, std::vector<double>& z);
 
+
+// --- Feature correspondences ------------------------------
+// local_map.cpp:8-62 (sliding window of frames, per-frame voxel dedupe,
+// ground hits kept as planar), kdtree.hpp:13-101 (exact k nearest within a
+// gate, closest first, ties by smaller id — restated as an exhaustive search
+// with the same ordering), scan_matcher.cpp:44-183 (build_correspondences),
+// residuals.cpp:7-25 and scan_matcher.cpp:185-216 (feature rows of
+// total_cost). Eigen's SelfAdjointEigenSolver is replaced by cyclic Jacobi
+// (eigenvalues ascending, eigenvectors to ~1e-15): parity unpinned there.
+struct MapConfig {
+  double voxel_size = 0.1;
+  std::size_t window = 20;
+};
+struct FeatureInput {  // one scan: sensor-frame points, kinds (0 edge, 1 planar, 2 ground), labels
+  std::vector<V3> p;
+  std::vector<std::uint8_t> kind;
+  std::vector<std::int32_t> label;
+};
+class LocalMap {
+ public:
+  explicit LocalMap(MapConfig c = {}) : cfg_(c) {}
+  void insert(const FeatureInput& scan, const M3& R, const V3& t);
+  std::vector<V3> edge, planar;
+  std::vector<std::int32_t> edge_label, planar_label;
+
+ private:
+  struct Frame {
+    std::vector<V3> edge, planar;
+    std::vector<std::int32_t> edge_label, planar_label;
+  };
+  MapConfig cfg_;
+  std::vector<Frame> frames_;
+};
+std::vector<std::uint32_t> knn(const std::vector<V3>& pts, const V3& q, int k, double gate);
+void eigen_sym3(const double A[9], double evals[3], double evecs[9]);  // evecs column-major
+
+struct SolverConfigM {
+  double corr_gate = 1.0, huber_delta = 0.1, plane_fit_tol = 0.025, plane_eig_ratio = 5.0;
+  double edge_eig_ratio = 3.0, edge_fit_tol = 0.05, edge_min_extent = 0.05;
+  double trim_ratio = 5.0, trim_floor = 0.003, ground_corr_voxel = 0.25, ground_corr_radius = 4.0;
+};
+struct Correspondence {
+  int kind = 0;             // 0 edge, 1 planar
+  std::uint32_t feature = 0;  // index into the scan
+  V3 p_sensor, line_point, line_dir{1.0, 0.0, 0.0}, normal{0.0, 0.0, 1.0};
+  double offset = 0.0, weight = 1.0;
+  std::int32_t label = -1;
+  double dist = 0.0, fitq = 0.0;
+};
+std::vector<Correspondence> build_correspondences(const FeatureInput& f, const M3& R, const V3& t,
+                                                  const LocalMap& map, const SolverConfigM& cfg);
+// feature rows of total_cost at pose (R, t), accumulated into ne in row order
+void feature_normal_eq(const std::vector<Correspondence>& c, const M3& R, const V3& t,
+                       NormalEq& ne, std::size_t* rows);
+
 }  // namespace oracle

@@ -106,6 +106,14 @@ _SIGS = {
     "tlg_ctx_kernel_stats": (_ST, [_P, _I, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
     "tlg_measure_fp64_peak": (_ST, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "tlg_debug_dense_bench": (_ST, [_P, _I, _I, _I, _I, C.POINTER(C.c_double)]),
+    "tlg_match_config_default": (_ST, [_P]),
+    "tlg_map_create": (_ST, [_P, C.c_double, _SZ, _P]),
+    "tlg_map_destroy": (_ST, [_P]),
+    "tlg_map_insert": (_ST, [_P, _P, _P, _P, _P, _P, _SZ, _I, _P, _P]),
+    "tlg_map_points": (_ST, [_P, _I, _P, _P, _SZ, C.POINTER(_SZ)]),
+    "tlg_build_correspondences": (_ST, [_P, _P, _P, _P, _P, _SZ, _I, _P, _P, _P, C.POINTER(_SZ)]),
+    "tlg_correspondences_get": (_ST, [_P, _P, _P, _P, _P, _P, _P, _P, _SZ]),
+    "tlg_feature_normal_eq": (_ST, [_P, _P, _P, _P]),
     "tlg_select_ground_points": (_ST, [_P, _P, _P, _P, _P, _SZ, _I, _P, _P, _P, _P, C.c_double,
                                        C.c_double, _SZ, _P, _P, _P, _I, C.POINTER(_SZ)]),
     "tlg_terrain_error_histogram": (_ST, [_P, _P, _P, _P, _SZ, _I, C.c_double, _I, _P, _P,

@@ -26,7 +26,11 @@ NVCC_FLAGS = [
     "-I", str(ROOT / "include"),
 ]
 
-SOURCES = ["model.cu", "grid.cu", "eval.cu", "select.cu", "dense.cu", "update.cu", "peak.cu", "scan.cu", "consumers.cu", "abi.cu"]
+SOURCES = ["model.cu", "grid.cu", "eval.cu", "select.cu", "dense.cu", "update.cu", "peak.cu",
+           "scan.cu", "consumers.cu", "match.cu", "abi.cu"]
+# match.cu restates the matcher's scalar geometry (centroids, scatter, 3x3
+# eigen sweeps, residuals) with the reference's unfused rounding
+EXTRA_FLAGS = {"match.cu": ["-fmad=false"]}
 
 
 def _stale(target: Path, deps: list[Path]) -> bool:
@@ -56,7 +60,7 @@ def build_gpu(force: bool = False, verbose: bool = False) -> Path:
         o = OBJ_DIR / (src + ".o")
         objs.append(o)
         if force or _stale(o, [s, *headers]):
-            cmd = [NVCC, *NVCC_FLAGS, "-c", str(s), "-o", str(o)]
+            cmd = [NVCC, *NVCC_FLAGS, *EXTRA_FLAGS.get(src, []), "-c", str(s), "-o", str(o)]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             jobs.append(cmd)

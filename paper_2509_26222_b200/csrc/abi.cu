@@ -26,6 +26,20 @@ size_t select_ground_device(tlg_ctx* ctx, const double* px, const double* py, co
                             const uint8_t* kind, size_t n, const double R[9], const double t[3],
                             const double roi[4], double radius, double voxel, size_t max_points,
                             double* ox, double* oy, double* oz);
+void map_insert(tlg_map* m, const double* px, const double* py, const double* pz,
+                const uint8_t* kind, const int* label, size_t n, const double R[9],
+                const double t[3]);
+size_t build_correspondences_device(tlg_map* m, const double* px, const double* py,
+                                    const double* pz, const uint8_t* kind, size_t n,
+                                    const double R[9], const double t[3], const double cfgv[11]);
+void feature_normal_eq_device(tlg_map* m, const double R[9], const double t[3], double ne29[29]);
+tlg_map* map_new(tlg_ctx* ctx, double voxel, size_t window);
+void map_free(tlg_map* m);
+size_t map_points_host(tlg_map* m, int kind, double* xyz, int32_t* labels, size_t cap);
+tlg_ctx* map_ctx(tlg_map* m);
+size_t correspondences_host(tlg_map* m, int32_t* kind, uint32_t* feature, double* params,
+                            double* weight, int32_t* label, double* dist, double* fitq,
+                            size_t cap);
 void error_histogram_device(tlg_model* m, const double* x, const double* y, const double* z,
                             size_t n, double trim_fraction, int bins, double* edges,
                             uint64_t* counts, uint64_t* trimmed, uint64_t* overflow);
@@ -247,6 +261,102 @@ tlg_status tlg_terrain_error_histogram(tlg_model* m, const double* x, const doub
     const double* dz = as_device(ctx, S_IN_Z, z, n, mem);
     error_histogram_device(m, dx, dy, dz, n, trim_fraction, bins, edges, counts, trimmed,
                            overflow);
+  });
+}
+
+tlg_status tlg_match_config_default(tlg_match_config* c) {
+  return guard([&] {
+    check_ptr(c, "cfg");
+    *c = tlg_match_config{1.0, 0.1, 0.025, 5.0, 3.0, 0.05, 0.05, 5.0, 0.003, 0.25, 4.0};
+  });
+}
+
+tlg_status tlg_map_create(tlg_ctx* ctx, double voxel_size, size_t window, tlg_map** out) {
+  return guard([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(out, "out");
+    require(window > 0, TLG_INVALID_ARGUMENT, "window must be positive");
+    *out = map_new(ctx, voxel_size, window);
+  });
+}
+
+tlg_status tlg_map_destroy(tlg_map* m) {
+  return guard([&] { map_free(m); });
+}
+
+tlg_status tlg_map_insert(tlg_map* m, const double* px, const double* py, const double* pz,
+                          const uint8_t* kind, const int32_t* label, size_t n, tlg_mem mem,
+                          const double R[9], const double t[3]) {
+  return guard([&] {
+    check_ptr(m, "map");
+    check_ptr(R, "R");
+    check_ptr(t, "t");
+    tlg_ctx* ctx = map_ctx(m);
+    const double* dx = as_device(ctx, S_IN_HX, px, n, mem);
+    const double* dy = as_device(ctx, S_IN_HY, py, n, mem);
+    const double* dz = as_device(ctx, S_IN_HZ, pz, n, mem);
+    const uint8_t* dk = as_device(ctx, S_MOMENT_ROW, kind, n, mem);
+    const int32_t* dl = label ? as_device(ctx, S_IN_X, label, n, mem) : nullptr;
+    map_insert(m, dx, dy, dz, dk, dl, n, R, t);
+  });
+}
+
+tlg_status tlg_map_points(tlg_map* m, int kind, double* xyz, int32_t* labels, size_t cap,
+                          size_t* count) {
+  return guard([&] {
+    check_ptr(m, "map");
+    require(kind == 0 || kind == 1, TLG_INVALID_ARGUMENT, "kind must be 0 (edge) or 1 (planar)");
+    const size_t c = map_points_host(m, kind, xyz, labels, cap);
+    if (count) *count = c;
+  });
+}
+
+tlg_status tlg_build_correspondences(tlg_map* m, const double* px, const double* py,
+                                     const double* pz, const uint8_t* kind, size_t n,
+                                     tlg_mem mem, const double R[9], const double t[3],
+                                     const tlg_match_config* cfg, size_t* count) {
+  return guard([&] {
+    check_ptr(m, "map");
+    check_ptr(R, "R");
+    check_ptr(t, "t");
+    check_ptr(cfg, "cfg");
+    require(cfg->corr_gate > 0.0, TLG_INVALID_ARGUMENT, "corr_gate must be positive");
+    tlg_ctx* ctx = map_ctx(m);
+    const double* dx = as_device(ctx, S_IN_HX, px, n, mem);
+    const double* dy = as_device(ctx, S_IN_HY, py, n, mem);
+    const double* dz = as_device(ctx, S_IN_HZ, pz, n, mem);
+    const uint8_t* dk = as_device(ctx, S_MOMENT_ROW, kind, n, mem);
+    const double v[11] = {cfg->corr_gate,      cfg->huber_delta,   cfg->plane_fit_tol,
+                          cfg->plane_eig_ratio, cfg->edge_eig_ratio, cfg->edge_fit_tol,
+                          cfg->edge_min_extent, cfg->trim_ratio,    cfg->trim_floor,
+                          cfg->ground_corr_voxel, cfg->ground_corr_radius};
+    const size_t c = build_correspondences_device(m, dx, dy, dz, dk, n, R, t, v);
+    if (count) *count = c;
+  });
+}
+
+tlg_status tlg_correspondences_get(tlg_map* m, int32_t* kind, uint32_t* feature, double* params,
+                                   double* weight, int32_t* label, double* dist, double* fitq,
+                                   size_t cap) {
+  return guard([&] {
+    check_ptr(m, "map");
+    correspondences_host(m, kind, feature, params, weight, label, dist, fitq, cap);
+  });
+}
+
+tlg_status tlg_feature_normal_eq(tlg_map* m, const double R[9], const double t[3],
+                                 tlg_normal_eq* ne) {
+  return guard([&] {
+    check_ptr(m, "map");
+    check_ptr(R, "R");
+    check_ptr(t, "t");
+    check_ptr(ne, "ne");
+    double h[29];
+    feature_normal_eq_device(m, R, t, h);
+    for (int k = 0; k < 21; ++k) ne->A[k] = h[k];
+    for (int k = 0; k < 6; ++k) ne->g[k] = h[21 + k];
+    ne->cost = h[27];
+    ne->valid = h[28];
   });
 }
 
