@@ -140,6 +140,10 @@ tlg_status tlg_terrain_error_histogram(tlg_model* model, const double* x, const 
 /* LocalMap (local_map.hpp:17-50): sliding window of frames, per-kind kNN
  * structures; build_correspondences (scan_matcher.cpp:44-183); feature rows
  * of total_cost (:185-216). FeatureKind codes: 0 edge, 1 planar, 2 ground. */
+/* LM damped step (scan_matcher.cpp:300-305): delta = -(A + mu diag(A)^+ +
+ * 1e-3 I)^-1 g by a pivoted LDL^T; ne may be the sum of the feature and
+ * manifold normal equations. TLG_RUNTIME_ERROR when the step is not finite. */
+tlg_status tlg_lm_step(tlg_ctx* ctx, const tlg_normal_eq* ne, double mu, double delta[6]);
 typedef struct tlg_map tlg_map;
 typedef struct {
   double corr_gate, huber_delta, plane_fit_tol, plane_eig_ratio, edge_eig_ratio, edge_fit_tol,

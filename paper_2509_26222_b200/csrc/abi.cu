@@ -37,6 +37,7 @@ tlg_map* map_new(tlg_ctx* ctx, double voxel, size_t window);
 void map_free(tlg_map* m);
 size_t map_points_host(tlg_map* m, int kind, double* xyz, int32_t* labels, size_t cap);
 tlg_ctx* map_ctx(tlg_map* m);
+bool lm_step_device(tlg_ctx* ctx, const double ne29[29], double mu, double delta[6]);
 size_t correspondences_host(tlg_map* m, int32_t* kind, uint32_t* feature, double* params,
                             double* weight, int32_t* label, double* dist, double* fitq,
                             size_t cap);
@@ -261,6 +262,20 @@ tlg_status tlg_terrain_error_histogram(tlg_model* m, const double* x, const doub
     const double* dz = as_device(ctx, S_IN_Z, z, n, mem);
     error_histogram_device(m, dx, dy, dz, n, trim_fraction, bins, edges, counts, trimmed,
                            overflow);
+  });
+}
+
+tlg_status tlg_lm_step(tlg_ctx* ctx, const tlg_normal_eq* ne, double mu, double delta[6]) {
+  return guard([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(ne, "ne");
+    check_ptr(delta, "delta");
+    double v[29];
+    for (int k = 0; k < 21; ++k) v[k] = ne->A[k];
+    for (int k = 0; k < 6; ++k) v[21 + k] = ne->g[k];
+    v[27] = ne->cost;
+    v[28] = ne->valid;
+    if (!lm_step_device(ctx, v, mu, delta)) throw Error(TLG_RUNTIME_ERROR, "non-finite LM step");
   });
 }
 

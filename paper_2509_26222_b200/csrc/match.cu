@@ -845,4 +845,92 @@ void feature_normal_eq_device(tlg_map* m, const double R[9], const double t[3], 
   TLG_CUDA(cudaStreamSynchronize(s));
 }
 
+namespace {
+// scan_matcher.cpp:300-305: delta = -(A + mu diag(A)^+ + 1e-3 I)^-1 g with a
+// diagonally pivoted LDL^T (Eigen::LDLT's algorithm, as restated in the
+// oracle). One thread: 6 x 6.
+__global__ void k_lm_step(const double* __restrict__ ne29, double mu, double* __restrict__ out) {
+  double a[6][6];
+  int k = 0;
+  for (int i = 0; i < 6; ++i)
+    for (int j = i; j < 6; ++j) {
+      a[i][j] = ne29[k];
+      a[j][i] = ne29[k];
+      ++k;
+    }
+  for (int i = 0; i < 6; ++i) a[i][i] += mu * fmax(a[i][i], 1e-12);
+  for (int i = 0; i < 6; ++i) a[i][i] += 1e-3;
+  int perm[6];
+  double tmp[6];
+  for (int kk = 0; kk < 6; ++kk) {
+    int big = kk;
+    double bv = fabs(a[kk][kk]);
+    for (int i = kk + 1; i < 6; ++i)
+      if (fabs(a[i][i]) > bv) {
+        bv = fabs(a[i][i]);
+        big = i;
+      }
+    perm[kk] = big;
+    if (big != kk) {
+      for (int c = 0; c < kk; ++c) { const double t = a[kk][c]; a[kk][c] = a[big][c]; a[big][c] = t; }
+      for (int r = big + 1; r < 6; ++r) { const double t = a[r][kk]; a[r][kk] = a[r][big]; a[r][big] = t; }
+      { const double t = a[kk][kk]; a[kk][kk] = a[big][big]; a[big][big] = t; }
+      for (int i = kk + 1; i < big; ++i) { const double t = a[i][kk]; a[i][kk] = a[big][i]; a[big][i] = t; }
+    }
+    if (kk > 0) {
+      for (int c = 0; c < kk; ++c) tmp[c] = a[c][c] * a[kk][c];
+      double sacc = 0.0;
+      for (int c = 0; c < kk; ++c) sacc += a[kk][c] * tmp[c];
+      a[kk][kk] -= sacc;
+      for (int r = kk + 1; r < 6; ++r) {
+        double acc = 0.0;
+        for (int c = 0; c < kk; ++c) acc += a[r][c] * tmp[c];
+        a[r][kk] -= acc;
+      }
+    }
+    const double akk = a[kk][kk];
+    if (kk == 0 && !(fabs(akk) > 0.0)) {
+      for (int j = 0; j < 6; ++j) perm[j] = j;
+      break;
+    }
+    if (kk + 1 < 6 && fabs(akk) > 0.0)
+      for (int r = kk + 1; r < 6; ++r) a[r][kk] /= akk;
+  }
+  double v[6];
+  for (int i = 0; i < 6; ++i) v[i] = ne29[21 + i];
+  for (int kk = 0; kk < 6; ++kk) { const double t = v[kk]; v[kk] = v[perm[kk]]; v[perm[kk]] = t; }
+  for (int kk = 0; kk < 6; ++kk)
+    for (int r = kk + 1; r < 6; ++r) v[r] -= a[r][kk] * v[kk];
+  for (int kk = 0; kk < 6; ++kk) {
+    const double d = a[kk][kk];
+    v[kk] = (fabs(d) > 2.2250738585072014e-308) ? v[kk] / d : 0.0;
+  }
+  for (int kk = 5; kk >= 0; --kk) {
+    double sacc = v[kk];
+    for (int r = kk + 1; r < 6; ++r) sacc -= a[r][kk] * v[r];
+    v[kk] = sacc;
+  }
+  for (int kk = 5; kk >= 0; --kk) { const double t = v[kk]; v[kk] = v[perm[kk]]; v[perm[kk]] = t; }
+  bool finite = true;
+  for (int i = 0; i < 6; ++i) {
+    out[i] = -v[i];
+    finite = finite && isfinite(out[i]);
+  }
+  out[6] = finite ? 1.0 : 0.0;
+}
+}  // namespace
+
+bool lm_step_device(tlg_ctx* ctx, const double ne29[29], double mu, double delta[6]) {
+  cudaStream_t s = ctx->stream;
+  double* d = ctx->ws<double>(S_SOLVE, 40);
+  TLG_CUDA(cudaMemcpyAsync(d, ne29, 29 * 8, cudaMemcpyHostToDevice, s));
+  k_lm_step<<<1, 1, 0, s>>>(d, mu, d + 32);
+  TLG_LAUNCHED(ctx);
+  double h[7];
+  TLG_CUDA(cudaMemcpyAsync(h, d + 32, 7 * 8, cudaMemcpyDeviceToHost, s));
+  TLG_CUDA(cudaStreamSynchronize(s));
+  for (int i = 0; i < 6; ++i) delta[i] = h[i];
+  return h[6] != 0.0;
+}
+
 }  // namespace tlg

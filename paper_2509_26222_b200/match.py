@@ -165,3 +165,30 @@ def feature_normal_eq(local_map: LocalMap, R, t) -> NormalEq:
     ne = NormalEqC()
     check(_abi.load().tlg_feature_normal_eq(local_map.handle, _ptr(Rm), _ptr(tv), C.byref(ne)))
     return NormalEq._from_c(ne)
+
+
+def combine(*nes: NormalEq) -> NormalEq:
+    """Sum of normal equations of stacked row groups (feature + manifold rows
+    reduce into one J^T J, scan_matcher.cpp:296-299)."""
+    A = sum(n.A for n in nes)
+    g = sum(n.g for n in nes)
+    return NormalEq(A, g, float(sum(n.cost for n in nes)), int(sum(n.valid for n in nes)))
+
+
+def lm_step(ne: NormalEq, mu: float, ctx: Context | None = None) -> np.ndarray:
+    """scan_matcher.cpp:300-305 on the device: delta = -(A + mu diag(A)^+ +
+    1e-3 I)^-1 g (pivoted LDL^T)."""
+    ctx = ctx or Context.default()
+    c = NormalEqC()
+    k = 0
+    for i in range(6):
+        for j in range(i, 6):
+            c.A[k] = float(ne.A[i, j])
+            k += 1
+    for i in range(6):
+        c.g[i] = float(ne.g[i])
+    c.cost = float(ne.cost)
+    c.valid = float(ne.valid)
+    delta = np.empty(6)
+    check(_abi.load().tlg_lm_step(ctx.handle, C.byref(c), float(mu), _ptr(delta)))
+    return delta

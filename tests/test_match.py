@@ -110,3 +110,20 @@ def test_correspondences_empty_map_and_window(gpu_ctx):
         om.insert(P, K, L, np.eye(3), np.zeros(3))
     for kind in (0, 1):
         assert np.array_equal(gm.points(kind)[0], om.points(kind)[0])
+
+
+@pytest.mark.gpu
+def test_lm_step_matches_oracle(gpu_ctx):
+    gm, om = _maps(7, frames=2)
+    P, K, _ = _scene(70, 1500)
+    R = so3_exp([0.002, 0.001, 0.03])
+    t = np.array([0.05, 0.02, 0.0])
+    Ps = (P - t) @ R + np.random.default_rng(2).normal(0, 0.01, P.shape)
+    M.build_correspondences(Ps, K, R, t, gm)
+    ne = M.feature_normal_eq(gm, R, t)
+    for mu in (1e-4, 1e-2, 1.0):
+        d = M.lm_step(ne, mu)
+        ne29 = np.concatenate([ne.A[np.triu_indices(6)], ne.g, [ne.cost, ne.valid]])
+        dref, ok = orc.lm_step(ne29, mu)
+        assert ok
+        np.testing.assert_array_equal(d, dref)
