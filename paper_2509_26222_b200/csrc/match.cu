@@ -90,12 +90,13 @@ __global__ void k_map_keys(const double* __restrict__ px, const double* __restri
   idx[i] = static_cast<uint32_t>(i);
 }
 
+// run heads of sorted keys; with `sentinel`, the key ~0 marks excluded entries
 __global__ void k_first_of_run(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
-                               size_t n, uint8_t* __restrict__ first) {
+                               size_t n, int sentinel, uint8_t* __restrict__ first) {
   const size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
   const uint64_t k = keys[p];
-  if (k != ~0ull && (p == 0 || keys[p - 1] != k)) first[idx[p]] = 1;
+  if ((!sentinel || k != ~0ull) && (p == 0 || keys[p - 1] != k)) first[idx[p]] = 1;
 }
 
 __global__ void k_flag_class(const uint8_t* __restrict__ first, const uint8_t* __restrict__ kind,
@@ -264,8 +265,9 @@ __global__ void k_ground_cells(const double* __restrict__ px, const double* __re
     if (ok && cfg.ground_voxel > 0.0) {
       const int64_t cx = static_cast<int64_t>(floor(x / cfg.ground_voxel));
       const int64_t cy = static_cast<int64_t>(floor(y / cfg.ground_voxel));
-      // (cx, cy) pair order as one key: cx in the high half (offset to unsigned)
-      key = ((static_cast<uint64_t>(cx) + (1ull << 31)) << 32) |
+      // the (cx, cy) pair as one key below the ~0 sentinel: cx offset into 31
+      // bits, cy into 32 (|cell| < 2^30, far beyond any map extent)
+      key = (((static_cast<uint64_t>(cx) + (1ull << 30)) & 0x7fffffffull) << 32) |
             ((static_cast<uint64_t>(cy) + (1ull << 31)) & 0xffffffffull);
     }
   }
@@ -510,7 +512,8 @@ size_t select_flagged(tlg_ctx* ctx, const uint8_t* flags, size_t n, uint32_t* ou
 }
 
 // first element per key run (stable sort keeps scan order inside a run)
-void first_per_key(tlg_ctx* ctx, uint64_t* keys, uint32_t* idx, size_t n, uint8_t* first) {
+void first_per_key(tlg_ctx* ctx, uint64_t* keys, uint32_t* idx, size_t n, uint8_t* first,
+                   bool sentinel) {
   cudaStream_t s = ctx->stream;
   uint64_t* keys2 = ctx->ws<uint64_t>(S_KEYS2, n);
   uint32_t* idx2 = ctx->ws<uint32_t>(S_VALS2, n);
@@ -519,7 +522,8 @@ void first_per_key(tlg_ctx* ctx, uint64_t* keys, uint32_t* idx, size_t n, uint8_
   void* d = ctx->ws<char>(S_CUB, tmp);
   TLG_CUDA(cub::DeviceRadixSort::SortPairs(d, tmp, keys, keys2, idx, idx2, n, 0, 64, s));
   TLG_CUDA(cudaMemsetAsync(first, 0, n, s));
-  k_first_of_run<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(keys2, idx2, n, first);
+  k_first_of_run<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(keys2, idx2, n, sentinel ? 1 : 0,
+                                                             first);
   TLG_LAUNCHED(ctx);
 }
 
@@ -681,7 +685,7 @@ void map_insert(tlg_map* m, const double* px, const double* py, const double* pz
     k_map_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(px, py, pz, kind, n, P, m->voxel, xyz,
                                                           keys, idx);
     TLG_LAUNCHED(ctx);
-    first_per_key(ctx, keys, idx, n, first);
+    first_per_key(ctx, keys, idx, n, first, false);  // every (kind, voxel) key is valid
     for (int cls = 0; cls < 2; ++cls) {
       k_flag_class<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(first, kind, n, cls, flag);
       TLG_LAUNCHED(ctx);
@@ -743,7 +747,7 @@ size_t build_correspondences_device(tlg_map* m, const double* px, const double* 
   k_ground_cells<<<nb, 128, 0, s>>>(px, py, pz, kind, n, P, cfg, rok, keys, idx);
   TLG_LAUNCHED(ctx);
   const int use_gfirst = cfg.ground_voxel > 0.0;
-  if (use_gfirst) first_per_key(ctx, keys, idx, n, gfirst);
+  if (use_gfirst) first_per_key(ctx, keys, idx, n, gfirst, true);
   // per-feature fits
   uint8_t* pass = ctx->ws<uint8_t>(S_BLOCKFLAG, n);
   int* okind = ctx->ws<int>(S_ROWPTR, n);

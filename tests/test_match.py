@@ -127,3 +127,16 @@ def test_lm_step_matches_oracle(gpu_ctx):
         dref, ok = orc.lm_step(ne29, mu)
         assert ok
         np.testing.assert_array_equal(d, dref)
+
+
+@pytest.mark.gpu
+def test_map_voxel_key_all_ones(gpu_ctx):
+    # points with x, y, z in [-voxel, 0): every 21-bit voxel field is 0x1fffff,
+    # i.e. an all-ones key — must still be kept (regression)
+    P = np.array([[-0.05, -0.05, -0.05], [-0.02, -0.07, -0.01], [0.3, 0.3, 0.3]])
+    K = np.array([1, 1, 1], dtype=np.uint8)
+    gm, om = M.LocalMap(0.1, 20), orc.LocalMap(0.1, 20)
+    gm.insert(P, K, np.zeros(3), np.eye(3), np.zeros(3))
+    om.insert(P, K, np.zeros(3), np.eye(3), np.zeros(3))
+    assert np.array_equal(gm.points(1)[0], om.points(1)[0])
+    assert len(gm.points(1)[0]) == 2
