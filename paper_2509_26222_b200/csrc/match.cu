@@ -143,7 +143,11 @@ __global__ void k_cell_count(const uint32_t* __restrict__ keys, size_t n, int* _
 }
 
 // kdtree.hpp semantics: the k smallest (d2, id) with d2 <= gate^2,
-// d2 = (p - q).squaredNorm(); returns the count found
+// d2 = (p - q).squaredNorm(); returns the count found. Cells are visited in
+// shells of growing Chebyshev radius r around q's cell; a point first seen in
+// shell r is at least (r - 2) cells away even allowing one cell of index
+// rounding, so the search stops once ((r - 2) c)^2 exceeds the current k-th
+// distance (or the gate) — the result equals the exhaustive search's.
 template <int K>
 __device__ int knn_grid(const GridView3& g, double qx, double qy, double qz, double gate2,
                         uint32_t (&ids)[K], double (&d2s)[K]) {
@@ -151,34 +155,43 @@ __device__ int knn_grid(const GridView3& g, double qx, double qy, double qz, dou
   int c[3];
   const double q[3] = {qx, qy, qz};
   for (int a = 0; a < 3; ++a) c[a] = static_cast<int>(floor((q[a] - g.org[a]) / g.cell));
-  for (int dz = -1; dz <= 1; ++dz) {
-    const int cz = c[2] + dz;
-    if (cz < 0 || cz >= g.dim[2]) continue;
-    for (int dy = -1; dy <= 1; ++dy) {
-      const int cy = c[1] + dy;
-      if (cy < 0 || cy >= g.dim[1]) continue;
-      for (int dx = -1; dx <= 1; ++dx) {
-        const int cx = c[0] + dx;
-        if (cx < 0 || cx >= g.dim[0]) continue;
-        const int cell = (cz * g.dim[1] + cy) * g.dim[0] + cx;
-        for (int s = g.start[cell]; s < g.start[cell + 1]; ++s) {
-          const uint32_t id = g.ids[s];
-          const double ex = g.pts[3 * id] - qx, ey = g.pts[3 * id + 1] - qy,
-                       ez = g.pts[3 * id + 2] - qz;
-          const double d2 = (ex * ex + ey * ey) + ez * ez;
-          if (!(d2 <= gate2)) continue;
-          if (m == K && !(d2 < d2s[K - 1] || (d2 == d2s[K - 1] && id < ids[K - 1]))) continue;
-          int j = m < K ? m++ : K - 1;
-          while (j > 0 && (d2s[j - 1] > d2 || (d2s[j - 1] == d2 && ids[j - 1] > id))) {
-            d2s[j] = d2s[j - 1];
-            ids[j] = ids[j - 1];
-            --j;
-          }
-          d2s[j] = d2;
-          ids[j] = id;
+  auto visit = [&](int cx, int cy, int cz) {
+    if (cx < 0 || cx >= g.dim[0] || cy < 0 || cy >= g.dim[1] || cz < 0 || cz >= g.dim[2]) return;
+    const int cell = (cz * g.dim[1] + cy) * g.dim[0] + cx;
+    for (int s = g.start[cell]; s < g.start[cell + 1]; ++s) {
+      const uint32_t id = g.ids[s];
+      const double ex = g.pts[3 * id] - qx, ey = g.pts[3 * id + 1] - qy, ez = g.pts[3 * id + 2] - qz;
+      const double d2 = (ex * ex + ey * ey) + ez * ez;
+      if (!(d2 <= gate2)) continue;
+      if (m == K && !(d2 < d2s[K - 1] || (d2 == d2s[K - 1] && id < ids[K - 1]))) continue;
+      int j = m < K ? m++ : K - 1;
+      while (j > 0 && (d2s[j - 1] > d2 || (d2s[j - 1] == d2 && ids[j - 1] > id))) {
+        d2s[j] = d2s[j - 1];
+        ids[j] = ids[j - 1];
+        --j;
+      }
+      d2s[j] = d2;
+      ids[j] = id;
+    }
+  };
+  const int rmax = max(max(g.dim[0], g.dim[1]), g.dim[2]);
+  for (int r = 0; r <= rmax; ++r) {
+    if (r >= 2) {
+      const double lb = (r - 2) * g.cell;
+      const double lb2 = lb * lb;
+      if (lb2 > gate2) break;
+      if (m == K && lb2 > d2s[K - 1]) break;
+    }
+    for (int dz = -r; dz <= r; ++dz)
+      for (int dy = -r; dy <= r; ++dy) {
+        const bool face = (dz == -r || dz == r || dy == -r || dy == r);
+        if (face) {
+          for (int dx = -r; dx <= r; ++dx) visit(c[0] + dx, c[1] + dy, c[2] + dz);
+        } else {
+          visit(c[0] - r, c[1] + dy, c[2] + dz);
+          if (r > 0) visit(c[0] + r, c[1] + dy, c[2] + dz);
         }
       }
-    }
   }
   return m;
 }
@@ -580,11 +593,15 @@ void build_grid(tlg_map* m, int cls, double gate) {
   TLG_CUDA(cudaMemcpyAsync(hb, bb, sizeof(hb), cudaMemcpyDeviceToHost, s));
   TLG_CUDA(cudaStreamSynchronize(s));
   const double lo[3] = {hb[0], hb[1], hb[2]}, hi[3] = {hb[3], hb[4], hb[5]};
-  // cell slightly wider than the gate: every point within the gate of a query
-  // lies in the query's 3x3x3 cell block despite rounding of the cell index
-  double ext = 0.0;
-  for (int a = 0; a < 3; ++a) ext = std::max(ext, hi[a] - lo[a]);
-  G.cell = std::max(gate * (1.0 + 1e-6), ext / 256.0);
+  // cell edge for ~12 points per occupied cell (shell search, knn_grid), not
+  // above the gate, at most 256 cells per axis
+  double ext = 0.0, vol = 1.0;
+  for (int a = 0; a < 3; ++a) {
+    ext = std::max(ext, hi[a] - lo[a]);
+    vol *= std::max(hi[a] - lo[a], 1e-3);
+  }
+  const double c0 = std::cbrt(vol * 12.0 / static_cast<double>(n));
+  G.cell = std::max(std::min(c0, gate), ext / 256.0);
   if (!(G.cell > 0.0)) G.cell = 1.0;
   for (int a = 0; a < 3; ++a) {
     G.org[a] = lo[a];
