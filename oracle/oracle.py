@@ -118,7 +118,7 @@ def load():
         _lib.orc_map_points.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_size_t]
         _lib.orc_knn.restype = C.c_size_t
         _lib.orc_knn.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
-                                 C.c_double, C.c_void_p]
+                                 C.c_double, C.c_void_p, C.c_int]
         _lib.orc_build_correspondences.restype = C.c_size_t
         _lib.orc_build_correspondences.argtypes = [C.c_void_p] + [C.c_void_p] * 4 + [
             C.c_size_t] + [C.c_void_p] * 10
@@ -432,10 +432,10 @@ class LocalMap:
         load().orc_map_points(self.h, kind, _p(xyz), _p(lab), n)
         return xyz, lab
 
-    def knn(self, kind, q, k, gate):
+    def knn(self, kind, q, k, gate, tree=True):
         out = np.empty(k, dtype=np.uint32)
         m = load().orc_knn(self.h, kind, float(q[0]), float(q[1]), float(q[2]), int(k),
-                           float(gate), _p(out))
+                           float(gate), _p(out), int(bool(tree)))
         return out[:m].copy()
 
     def build_correspondences(self, p, kind, R, t, cfg=None):

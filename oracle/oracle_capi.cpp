@@ -448,10 +448,12 @@ size_t orc_map_points(void* m, int kind, double* xyz, int* labels, size_t cap) {
   }
   return pts.size();
 }
+// tree: 1 = the kd-tree (reference algorithm), 0 = exhaustive cross-check
 size_t orc_knn(void* m, int kind, double qx, double qy, double qz, int k, double gate,
-               unsigned* out) {
+               unsigned* out, int tree) {
   auto* mp = static_cast<LocalMap*>(m);
-  const auto ids = knn(kind == 0 ? mp->edge : mp->planar, {qx, qy, qz}, k, gate);
+  const auto ids = tree ? (kind == 0 ? mp->edge_tree : mp->planar_tree).knn({qx, qy, qz}, k, gate)
+                        : knn(kind == 0 ? mp->edge : mp->planar, {qx, qy, qz}, k, gate);
   for (size_t i = 0; i < ids.size(); ++i) out[i] = ids[i];
   return ids.size();
 }

@@ -851,6 +851,8 @@ void LocalMap::insert(const FeatureInput& scan, const M3& R, const V3& t) {
     edge_label.insert(edge_label.end(), f.edge_label.begin(), f.edge_label.end());
     planar_label.insert(planar_label.end(), f.planar_label.begin(), f.planar_label.end());
   }
+  edge_tree.build(edge);
+  planar_tree.build(planar);
 }
 
 // kdtree.hpp:31-41/:79-99: the k smallest (d2, id) with d2 <= gate^2, ascending
@@ -866,6 +868,68 @@ std::vector<std::uint32_t> knn(const std::vector<V3>& pts, const V3& q, int k, d
   std::partial_sort(cand.begin(), cand.begin() + m, cand.end());
   std::vector<std::uint32_t> out(m);
   for (std::size_t i = 0; i < m; ++i) out[i] = cand[i].second;
+  return out;
+}
+
+static double coord(const V3& p, int axis) { return axis == 0 ? p.x : (axis == 1 ? p.y : p.z); }
+
+void KdTree3::build(const std::vector<V3>& pts) {
+  pts_ = pts;
+  order_.resize(pts.size());
+  for (std::uint32_t i = 0; i < pts.size(); ++i) order_[i] = i;
+  nodes_.clear();
+  nodes_.reserve(pts.size());
+  root_ = pts.empty() ? -1 : build_range(0, static_cast<int>(pts.size()), 0);
+}
+
+int KdTree3::build_range(int b, int e, int depth) {
+  if (b >= e) return -1;
+  const int axis = depth % 3, mid = (b + e) / 2;
+  std::nth_element(order_.begin() + b, order_.begin() + mid, order_.begin() + e,
+                   [&](std::uint32_t a, std::uint32_t c) {
+                     const double va = coord(pts_[a], axis), vc = coord(pts_[c], axis);
+                     return va != vc ? va < vc : a < c;
+                   });
+  const int self = static_cast<int>(nodes_.size());
+  nodes_.push_back({order_[mid], -1, -1, axis});
+  const int l = build_range(b, mid, depth + 1);
+  const int r = build_range(mid + 1, e, depth + 1);
+  nodes_[self].left = l;
+  nodes_[self].right = r;
+  return self;
+}
+
+void KdTree3::search(int ni, const V3& q, int k, double gate2,
+                     std::vector<std::pair<double, std::uint32_t>>& heap) const {
+  const Node& n = nodes_[ni];
+  const V3& p = pts_[n.id];
+  const double dx = p.x - q.x, dy = p.y - q.y, dz = p.z - q.z;
+  const double d2 = (dx * dx + dy * dy) + dz * dz;
+  if (d2 <= gate2) {
+    const std::pair<double, std::uint32_t> c{d2, n.id};
+    if (static_cast<int>(heap.size()) < k) {
+      heap.push_back(c);
+      std::push_heap(heap.begin(), heap.end());
+    } else if (c < heap.front()) {
+      std::pop_heap(heap.begin(), heap.end());
+      heap.back() = c;
+      std::push_heap(heap.begin(), heap.end());
+    }
+  }
+  const double delta = coord(q, n.axis) - coord(p, n.axis);
+  const int near = delta < 0 ? n.left : n.right, far = delta < 0 ? n.right : n.left;
+  if (near >= 0) search(near, q, k, gate2, heap);
+  const double worst =
+      static_cast<int>(heap.size()) < k ? gate2 : std::min(gate2, heap.front().first);
+  if (far >= 0 && delta * delta <= worst) search(far, q, k, gate2, heap);
+}
+
+std::vector<std::uint32_t> KdTree3::knn(const V3& q, int k, double gate) const {
+  std::vector<std::pair<double, std::uint32_t>> heap;
+  if (root_ >= 0) search(root_, q, k, gate * gate, heap);
+  std::sort_heap(heap.begin(), heap.end());
+  std::vector<std::uint32_t> out(heap.size());
+  for (std::size_t i = 0; i < heap.size(); ++i) out[i] = heap[i].second;
   return out;
 }
 
@@ -971,7 +1035,8 @@ std::vector<Correspondence> build_correspondences(const FeatureInput& f, const M
     const std::vector<std::int32_t>& lab = edge ? map.edge_label : map.planar_label;
     const int k = edge ? 5 : 8;
     if (pts.empty()) continue;
-    const auto nn = knn(pts, pw, k, cfg.corr_gate);
+    const auto nn = map.use_tree ? (edge ? map.edge_tree : map.planar_tree).knn(pw, k, cfg.corr_gate)
+                                 : knn(pts, pw, k, cfg.corr_gate);
     if (static_cast<int>(nn.size()) < k) continue;
     V3 cen{0.0, 0.0, 0.0};
     for (auto id : nn) {

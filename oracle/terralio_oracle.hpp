@@ -284,12 +284,36 @@ struct FeatureInput {  // one scan: sensor-frame points, kinds (0 edge, 1 planar
   std::vector<std::uint8_t> kind;
   std::vector<std::int32_t> label;
 };
+// kdtree.hpp:13-101 restated (static median-split 3-d tree, same search and
+// tie rules); knn() above is its exhaustive cross-check
+class KdTree3 {
+ public:
+  void build(const std::vector<V3>& pts);
+  std::vector<std::uint32_t> knn(const V3& q, int k, double gate) const;
+
+ private:
+  struct Node {
+    std::uint32_t id;
+    int left = -1, right = -1;
+    int axis = 0;
+  };
+  int build_range(int b, int e, int depth);
+  void search(int ni, const V3& q, int k, double gate2,
+              std::vector<std::pair<double, std::uint32_t>>& heap) const;
+  std::vector<V3> pts_;
+  std::vector<std::uint32_t> order_;
+  std::vector<Node> nodes_;
+  int root_ = -1;
+};
+
 class LocalMap {
  public:
   explicit LocalMap(MapConfig c = {}) : cfg_(c) {}
   void insert(const FeatureInput& scan, const M3& R, const V3& t);
   std::vector<V3> edge, planar;
   std::vector<std::int32_t> edge_label, planar_label;
+  KdTree3 edge_tree, planar_tree;
+  bool use_tree = true;  // false: exhaustive kNN (cross-check)
 
  private:
   struct Frame {

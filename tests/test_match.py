@@ -56,6 +56,15 @@ def test_oracle_knn_and_fits_sane():
     assert len(ids) == 8 and np.all(np.diff(d) >= 0)
     brute = np.argsort(np.sum((pts - q) ** 2, 1), kind="stable")[:8]
     assert set(ids) == set(brute)
+    # the restated kd-tree (reference algorithm) equals the exhaustive search
+    rng = np.random.default_rng(3)
+    for kind in (0, 1):
+        p, _ = om.points(kind)
+        for _ in range(200):
+            qq = p[rng.integers(len(p))] + rng.normal(0, 0.05, 3)
+            for k in (5, 8):
+                assert np.array_equal(om.knn(kind, qq, k, 0.3, tree=True),
+                                      om.knn(kind, qq, k, 0.3, tree=False))
 
 
 @pytest.mark.gpu
