@@ -175,12 +175,25 @@ __device__ int knn_grid(const GridView3& g, double qx, double qy, double qz, dou
     }
   };
   const int rmax = max(max(g.dim[0], g.dim[1]), g.dim[2]);
+  // binning rounds floor((p - org) / cell) within an ulp or so: eps keeps the
+  // bound conservative
+  const double eps = 1e-9 * (fabs(g.org[0]) + fabs(g.org[1]) + fabs(g.org[2]) + g.cell * rmax);
   for (int r = 0; r <= rmax; ++r) {
-    if (r >= 2) {
-      const double lb = (r - 2) * g.cell;
-      const double lb2 = lb * lb;
-      if (lb2 > gate2) break;
-      if (m == K && lb2 > d2s[K - 1]) break;
+    if (r >= 1) {
+      // every unvisited point lies in a cell r or more away on some axis:
+      // lower bound on its distance from the actual cell faces
+      double lb = INFINITY;
+      for (int a = 0; a < 3; ++a) {
+        const double hi_face = g.org[a] + (c[a] + r) * g.cell - q[a];
+        const double lo_face = q[a] - (g.org[a] + (c[a] - r + 1) * g.cell);
+        lb = fmin(lb, fmin(hi_face, lo_face));
+      }
+      lb -= eps;
+      if (lb > 0.0) {
+        const double lb2 = lb * lb;
+        if (lb2 > gate2) break;
+        if (m == K && lb2 > d2s[K - 1]) break;
+      }
     }
     for (int dz = -r; dz <= r; ++dz)
       for (int dy = -r; dy <= r; ++dy) {
@@ -294,12 +307,14 @@ __global__ void k_correspond(const double* __restrict__ px, const double* __rest
                              const int* __restrict__ lab_e, const int* __restrict__ lab_p,
                              size_t ne, size_t np, const uint8_t* __restrict__ radius_ok,
                              const uint8_t* __restrict__ gfirst, int use_gfirst,
+                             const uint32_t* __restrict__ order,
                              uint8_t* __restrict__ pass, int* __restrict__ okind,
                              double* __restrict__ par, double* __restrict__ weight,
                              int* __restrict__ label, double* __restrict__ dist,
                              double* __restrict__ fitq) {
-  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const size_t jj = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (jj >= n) return;
+  const size_t i = order[jj];
   pass[i] = 0;
   const uint8_t kd = kind[i];
   if (kd == 2 && (!radius_ok[i] || (use_gfirst && !gfirst[i]))) return;
@@ -391,6 +406,27 @@ __global__ void k_correspond(const double* __restrict__ px, const double* __rest
   label[i] = best;
   dist[i] = dd;
   pass[i] = 1;
+}
+
+__global__ void k_query_keys(const double* __restrict__ px, const double* __restrict__ py,
+                             const double* __restrict__ pz, const uint8_t* __restrict__ kind,
+                             size_t n, Pose P, GridView3 ge, GridView3 gp,
+                             uint64_t* __restrict__ keys, uint32_t* __restrict__ idx) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double q[3];
+  xform(P, px[i], py[i], pz[i], q[0], q[1], q[2]);
+  const bool edge = kind[i] == 0;
+  const GridView3& g = edge ? ge : gp;
+  uint64_t cell = 0;
+  if (g.dim[0] > 0) {
+    int c[3];
+    for (int a = 0; a < 3; ++a)
+      c[a] = min(max(static_cast<int>(floor((q[a] - g.org[a]) / g.cell)), 0), g.dim[a] - 1);
+    cell = static_cast<uint64_t>((c[2] * g.dim[1] + c[1]) * g.dim[0] + c[0]);
+  }
+  keys[i] = (static_cast<uint64_t>(edge ? 0 : 1) << 40) | cell;
+  idx[i] = static_cast<uint32_t>(i);
 }
 
 // order-preserving signed double -> unsigned key (radix sort of fitq)
@@ -600,8 +636,13 @@ void build_grid(tlg_map* m, int cls, double gate) {
     ext = std::max(ext, hi[a] - lo[a]);
     vol *= std::max(hi[a] - lo[a], 1e-3);
   }
-  const double c0 = std::cbrt(vol * 12.0 / static_cast<double>(n));
-  G.cell = std::max(std::min(c0, gate), ext / 256.0);
+  // ~12 points per cell for a volumetric cloud, or for a surface cloud
+  // (LiDAR maps are mostly surfaces: area ~ the bounding box's face sum)
+  const double e0 = std::max(hi[0] - lo[0], 1e-3), e1 = std::max(hi[1] - lo[1], 1e-3),
+               e2 = std::max(hi[2] - lo[2], 1e-3);
+  const double c3 = std::cbrt(vol * 12.0 / static_cast<double>(n));
+  const double c2 = std::sqrt((e0 * e1 + e0 * e2 + e1 * e2) * 12.0 / static_cast<double>(n));
+  G.cell = std::max(std::min(std::min(c3, c2), gate), ext / 256.0);
   if (!(G.cell > 0.0)) G.cell = 1.0;
   for (int a = 0; a < 3; ++a) {
     G.org[a] = lo[a];
@@ -773,9 +814,22 @@ size_t build_correspondences_device(tlg_map* m, const double* px, const double* 
   int* lab = ctx->ws<int>(S_COLIDX, n);
   double* dist = ctx->ws<double>(S_OUT_GX, n);
   double* fq = ctx->ws<double>(S_OUT_GY, n);
+  // process features in (kind, map cell) order: neighbouring threads share
+  // cells and loop trip counts (results are still indexed by feature)
+  uint64_t* qk = ctx->ws<uint64_t>(S_KEYS, n);
+  uint32_t* qi = ctx->ws<uint32_t>(S_VALS, n);
+  uint64_t* qk2 = ctx->ws<uint64_t>(S_KEYS2, n);
+  uint32_t* order = ctx->ws<uint32_t>(S_VALS2, n);
+  k_query_keys<<<nb, 128, 0, s>>>(px, py, pz, kind, n, P, grid_view3(m, 0), grid_view3(m, 1), qk,
+                                  qi);
+  TLG_LAUNCHED(ctx);
+  size_t tmpq = 0;
+  TLG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmpq, qk, qk2, qi, order, n, 0, 64, s));
+  void* dq = ctx->ws<char>(S_CUB, tmpq);
+  TLG_CUDA(cub::DeviceRadixSort::SortPairs(dq, tmpq, qk, qk2, qi, order, n, 0, 64, s));
   k_correspond<<<nb, 128, 0, s>>>(px, py, pz, kind, n, P, cfg, grid_view3(m, 0), grid_view3(m, 1),
                                   m->lab[0].p, m->lab[1].p, m->n[0], m->n[1], rok, gfirst,
-                                  use_gfirst, pass, okind, par, wgt, lab, dist, fq);
+                                  use_gfirst, order, pass, okind, par, wgt, lab, dist, fq);
   TLG_LAUNCHED(ctx);
   uint32_t* sel = ctx->ws<uint32_t>(S_MERGED, n);
   size_t cnt = select_flagged<uint32_t>(ctx, pass, n, sel);
