@@ -254,6 +254,73 @@ def run_update_c4(torch, steps=5):
     return out
 
 
+def match_scene(seed, n):
+    """Synthetic LiDAR features: ground plane, two walls, three poles (edge
+    features), labelled, in random order."""
+    rng = np.random.default_rng(seed)
+    g = np.c_[rng.uniform(-5, 5, n), rng.uniform(-5, 5, n), rng.normal(0, 0.004, n)]
+    w1 = np.c_[np.full(n // 2, 3.0) + rng.normal(0, 0.004, n // 2), rng.uniform(-5, 5, n // 2),
+               rng.uniform(0, 2.5, n // 2)]
+    w2 = np.c_[rng.uniform(-5, 3, n // 2), np.full(n // 2, 4.0) + rng.normal(0, 0.004, n // 2),
+               rng.uniform(0, 2.5, n // 2)]
+    poles = [np.c_[np.full(300, x), np.full(300, y), rng.uniform(0, 2.5, 300)] +
+             rng.normal(0, 0.002, (300, 3)) for x, y in [(1.0, 1.0), (-2.0, 0.5), (0.5, -3.0)]]
+    e = np.concatenate(poles)
+    P = np.concatenate([g, w1, w2, e])
+    K = np.concatenate([np.full(len(g), 2), np.ones(len(w1) + len(w2)), np.zeros(len(e))])
+    L = np.concatenate([np.zeros(len(g)), np.full(len(w1), 1), np.full(len(w2), 2),
+                        np.repeat([3, 4, 5], 300)])
+    perm = rng.permutation(len(P))
+    return P[perm], K[perm].astype(np.uint8), L[perm].astype(np.int32)
+
+
+def run_match_bench(torch, cpu=True, steps=10):
+    """association of a ~17k-feature scan against a 20-frame
+    LocalMap (~240k map points): build_correspondences + feature normal
+    equations per LM outer iteration; the reference algorithm (restated
+    kd-tree, one core) beside it."""
+    from paper_2509_26222_b200 import match as Mt
+    gm = Mt.LocalMap(0.1, 20)
+    om = None
+    if cpu:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle as orc
+        om = orc.LocalMap(0.1, 20)
+    for f in range(20):
+        P, K, L = match_scene(100 + f, 8000)
+        R = so3_exp(np.array([0.0, 0.0, 0.01 * f]))
+        t = np.array([0.02 * f, 0.0, 0.0])
+        Ps = (P - t) @ R
+        gm.insert(Ps, K, L, R, t)
+        if om is not None:
+            om.insert(Ps, K, L, R, t)
+    P, K, _ = match_scene(7, 8000)
+    R = so3_exp(np.array([0.002, -0.001, 0.2]))
+    t = np.array([0.4, -0.1, 0.0])
+    Ps = (P - t) @ R + np.random.default_rng(3).normal(0, 0.01, P.shape)
+    Mt.build_correspondences(Ps, K, R, t, gm)
+    Mt.feature_normal_eq(gm, R, t)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        c = Mt.build_correspondences(Ps, K, R, t, gm)
+    t1 = time.perf_counter()
+    for _ in range(steps):
+        Mt.feature_normal_eq(gm, R, t)
+    t2 = time.perf_counter()
+    out = {"map_points": gm.size(), "features": len(P), "correspondences": len(c),
+           "associate_ms": (t1 - t0) / steps * 1e3, "feature_ne_ms": (t2 - t1) / steps * 1e3,
+           "timing": "wall clock per call through the Python API (host features in, "
+                     "host correspondences out)"}
+    if om is not None:
+        t3 = time.perf_counter()
+        o = om.build_correspondences(Ps, K, R, t)
+        out["cpu_reference_associate_ms"] = (time.perf_counter() - t3) * 1e3
+        out["cpu_reference"] = "oracle restatement of scan_matcher.cpp:44-183 with the kd-tree, 1 core"
+        out["cpu_correspondences"] = len(o["kind"])
+    return out
+
+
 def cpu_update_ms(model, kernel, m=400, seed=5):
     """Oracle recursive_update (reference algorithm, single thread) at M=4096."""
     sys.path.insert(0, str(ROOT / "oracle"))
@@ -421,6 +488,8 @@ def main():
                 cms, crep = cpu_update_ms(umodel, ukernel, 400)
                 result["update"]["cpu_oracle_ms_per_scan_m400"] = cms
                 result["update"]["cpu_oracle_n_active"] = crep["active_centers"]
+        if not args.no_update:
+            result["match"] = run_match_bench(torch, not args.no_cpu)
         if not args.no_cpu:
             pts_h = torch.stack(list(h), 1)[: 2_000_000].cpu().numpy()
             rate, ns, threads, dt, _ = cpu_eval_rate(cs.centers, w, kernel, pts_h, R, tv,
