@@ -144,6 +144,9 @@ tlg_status tlg_terrain_error_histogram(tlg_model* model, const double* x, const 
  * 1e-3 I)^-1 g by a pivoted LDL^T; ne may be the sum of the feature and
  * manifold normal equations. TLG_RUNTIME_ERROR when the step is not finite. */
 tlg_status tlg_lm_step(tlg_ctx* ctx, const tlg_normal_eq* ne, double mu, double delta[6]);
+/* Smallest eigenvalue of A (the degeneracy probe of lm_solve on the
+ * feature-only normal matrix, scan_matcher.cpp:280-287). */
+tlg_status tlg_ne_min_eigenvalue(tlg_ctx* ctx, const tlg_normal_eq* ne, double* lambda_min);
 typedef struct tlg_map tlg_map;
 typedef struct {
   double corr_gate, huber_delta, plane_fit_tol, plane_eig_ratio, edge_eig_ratio, edge_fit_tol,

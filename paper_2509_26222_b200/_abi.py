@@ -107,6 +107,7 @@ _SIGS = {
     "tlg_measure_fp64_peak": (_ST, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "tlg_debug_dense_bench": (_ST, [_P, _I, _I, _I, _I, C.POINTER(C.c_double)]),
     "tlg_lm_step": (_ST, [_P, _P, C.c_double, _P]),
+    "tlg_ne_min_eigenvalue": (_ST, [_P, _P, C.POINTER(C.c_double)]),
     "tlg_match_config_default": (_ST, [_P]),
     "tlg_map_create": (_ST, [_P, C.c_double, _SZ, _P]),
     "tlg_map_destroy": (_ST, [_P]),

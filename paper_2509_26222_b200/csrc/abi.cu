@@ -38,6 +38,7 @@ void map_free(tlg_map* m);
 size_t map_points_host(tlg_map* m, int kind, double* xyz, int32_t* labels, size_t cap);
 tlg_ctx* map_ctx(tlg_map* m);
 bool lm_step_device(tlg_ctx* ctx, const double ne29[29], double mu, double delta[6]);
+double eigmin6_device(tlg_ctx* ctx, const double ne29[29]);
 size_t correspondences_host(tlg_map* m, int32_t* kind, uint32_t* feature, double* params,
                             double* weight, int32_t* label, double* dist, double* fitq,
                             size_t cap);
@@ -276,6 +277,17 @@ tlg_status tlg_lm_step(tlg_ctx* ctx, const tlg_normal_eq* ne, double mu, double 
     v[27] = ne->cost;
     v[28] = ne->valid;
     if (!lm_step_device(ctx, v, mu, delta)) throw Error(TLG_RUNTIME_ERROR, "non-finite LM step");
+  });
+}
+
+tlg_status tlg_ne_min_eigenvalue(tlg_ctx* ctx, const tlg_normal_eq* ne, double* lambda_min) {
+  return guard([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(ne, "ne");
+    check_ptr(lambda_min, "lambda_min");
+    double v[29] = {0};
+    for (int k = 0; k < 21; ++k) v[k] = ne->A[k];
+    *lambda_min = eigmin6_device(ctx, v);
   });
 }
 

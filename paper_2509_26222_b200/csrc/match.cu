@@ -1008,4 +1008,58 @@ bool lm_step_device(tlg_ctx* ctx, const double ne29[29], double mu, double delta
   return h[6] != 0.0;
 }
 
+namespace {
+// smallest eigenvalue of the symmetric 6x6 J^T J (cyclic Jacobi); the
+// degeneracy probe of lm_solve (scan_matcher.cpp:280-287)
+__global__ void k_eigmin6(const double* __restrict__ ne29, double* __restrict__ out) {
+  double a[6][6];
+  int k = 0;
+  for (int i = 0; i < 6; ++i)
+    for (int j = i; j < 6; ++j) {
+      a[i][j] = ne29[k];
+      a[j][i] = ne29[k];
+      ++k;
+    }
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < 6; ++p)
+      for (int q = p + 1; q < 6; ++q) off += fabs(a[p][q]);
+    if (off == 0.0) break;
+    for (int p = 0; p < 5; ++p)
+      for (int q = p + 1; q < 6; ++q) {
+        if (a[p][q] == 0.0) continue;
+        const double theta = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
+        const double tt = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(tt * tt + 1.0), sn = tt * c;
+        for (int r = 0; r < 6; ++r) {
+          const double arp = a[r][p], arq = a[r][q];
+          a[r][p] = c * arp - sn * arq;
+          a[r][q] = sn * arp + c * arq;
+        }
+        for (int r = 0; r < 6; ++r) {
+          const double apr = a[p][r], aqr = a[q][r];
+          a[p][r] = c * apr - sn * aqr;
+          a[q][r] = sn * apr + c * aqr;
+        }
+        a[p][q] = a[q][p] = 0.0;
+      }
+  }
+  double mn = a[0][0];
+  for (int i = 1; i < 6; ++i) mn = fmin(mn, a[i][i]);
+  out[0] = mn;
+}
+}  // namespace
+
+double eigmin6_device(tlg_ctx* ctx, const double ne29[29]) {
+  cudaStream_t s = ctx->stream;
+  double* d = ctx->ws<double>(S_SOLVE, 40);
+  TLG_CUDA(cudaMemcpyAsync(d, ne29, 29 * 8, cudaMemcpyHostToDevice, s));
+  k_eigmin6<<<1, 1, 0, s>>>(d, d + 32);
+  TLG_LAUNCHED(ctx);
+  double h = 0.0;
+  TLG_CUDA(cudaMemcpyAsync(&h, d + 32, 8, cudaMemcpyDeviceToHost, s));
+  TLG_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
 }  // namespace tlg

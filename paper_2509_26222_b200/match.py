@@ -192,3 +192,175 @@ def lm_step(ne: NormalEq, mu: float, ctx: Context | None = None) -> np.ndarray:
     delta = np.empty(6)
     check(_abi.load().tlg_lm_step(ctx.handle, C.byref(c), float(mu), _ptr(delta)))
     return delta
+
+
+# ---------------------------------------------------------------------------
+# lm_solve (scan_matcher.cpp:257-358). The LM control flow and the SO(3)
+# retraction of the 6-DoF state (so3.cpp:16-58) are O(1) host work per step;
+# every data-sized computation — association, feature rows, manifold rows,
+# their normal equations, the damped solve and the degeneracy probe — runs on
+# the device.
+@dataclass
+class SolverConfig(MatchConfig):
+    lambda_manifold: float = 1.0
+    lm_init_damping: float = 1e-4
+    lm_max_iters: int = 10
+    lm_max_inner: int = 8
+    lm_max_rejects: int = 12
+    tol_dcost: float = 1e-10
+    tol_dstate: float = 1e-10
+    min_correspondences: int = 10
+    manifold_huber_delta: float = 0.05
+    degeneracy_eig_min: float = 10.0
+
+    def _c(self) -> MatchConfigC:
+        return MatchConfigC(*[float(getattr(self, f.name)) for f in fields(MatchConfig)])
+
+
+@dataclass
+class SolveReport:
+    converged: bool = False
+    failed: bool = False
+    degenerate: bool = False
+    outer_iterations: int = 0
+    accepted_steps: int = 0
+    final_cost: float = 0.0
+    correspondence_count: int = 0
+    cost_trace: list = None
+    smallest_feature_eigenvalue: float = 0.0
+
+
+def _hat(v):
+    return np.array([[0.0, -v[2], v[1]], [v[2], 0.0, -v[0]], [-v[1], v[0], 0.0]])
+
+
+def so3_exp(w) -> np.ndarray:
+    """so3.cpp:16-27 (Rodrigues, second-order Taylor below theta^2 = 1e-16)."""
+    w = np.asarray(w, dtype=np.float64)
+    th2 = float(w @ w)
+    W = _hat(w)
+    if th2 < 1e-16:
+        return np.eye(3) + W + 0.5 * (W @ W)
+    th = np.sqrt(th2)
+    return np.eye(3) + (np.sin(th) / th) * W + ((1.0 - np.cos(th)) / th2) * (W @ W)
+
+
+def _reorthonormalize(R, tol=1e-9):
+    """so3.cpp:47-58."""
+    if np.abs(R.T @ R - np.eye(3)).max() <= tol:
+        return R
+    U, _, Vt = np.linalg.svd(R)
+    F = U @ Vt
+    if np.linalg.det(F) < 0:
+        F = U @ np.diag([1.0, 1.0, -1.0]) @ Vt
+    return F
+
+
+def _retract(R, t, d):
+    """scan_matcher.cpp:35-41: R exp(hat(d_theta)), t + d_t."""
+    return _reorthonormalize(R @ so3_exp(d[:3])), t + d[3:]
+
+
+def _ne29(ne: NormalEq) -> NormalEqC:
+    c = NormalEqC()
+    k = 0
+    for i in range(6):
+        for j in range(i, 6):
+            c.A[k] = float(ne.A[i, j])
+            k += 1
+    for i in range(6):
+        c.g[i] = float(ne.g[i])
+    c.cost = float(ne.cost)
+    c.valid = float(ne.valid)
+    return c
+
+
+def lm_solve(R0, t0, points, kinds, local_map: LocalMap, config: SolverConfig | None = None,
+             terrain=None, lever_arms=None, wheel_radius: float = 0.0,
+             ctx: Context | None = None):
+    """Levenberg-Marquardt pose refinement with re-association every outer
+    iteration (scan_matcher.cpp:257-358). With a terrain model and lever arms
+    (n, 3) the manifold soft-constraint rows join the normal equations.
+    Returns (R, t, SolveReport)."""
+    from .kinematics import manifold_rows
+    cfg = config or SolverConfig()
+    ctx = ctx or Context.default()
+    lib = _abi.load()
+    rep = SolveReport(cost_trace=[])
+    R, t = np.asarray(R0, dtype=np.float64), np.asarray(t0, dtype=np.float64)
+    use_manifold = terrain is not None and lever_arms is not None and cfg.lambda_manifold > 0.0
+
+    def total_cost(Rc, tc):
+        ne = feature_normal_eq(local_map, Rc, tc)
+        feat = ne
+        if use_manifold:
+            _, nm = manifold_rows(terrain, Rc, tc, lever_arms, wheel_radius, cfg.lambda_manifold,
+                                  cfg.manifold_huber_delta, want=())
+            ne = combine(ne, nm)
+        if ne.valid == 0:
+            raise _abi.TerralioError("nothing to optimize")
+        return ne, feat
+
+    mu = cfg.lm_init_damping
+    rejects = 0
+    for _ in range(cfg.lm_max_iters):
+        rep.outer_iterations += 1
+        corr = build_correspondences(points, kinds, R, t, local_map, cfg)
+        rep.correspondence_count = len(corr)
+        if len(corr) < cfg.min_correspondences:
+            rep.degenerate = True
+            break
+        ne, feat = total_cost(R, t)
+        rep.cost_trace.append(ne.cost)
+        rep.final_cost = ne.cost
+        lam = C.c_double()
+        check(lib.tlg_ne_min_eigenvalue(ctx.handle, C.byref(_ne29(feat)), C.byref(lam)))
+        rep.smallest_feature_eigenvalue = lam.value
+        if lam.value < cfg.degeneracy_eig_min:
+            rep.degenerate = True
+        improved = local_converged = False
+        moved = 0.0
+        for _ in range(cfg.lm_max_inner):
+            delta = np.empty(6)
+            st = lib.tlg_lm_step(ctx.handle, C.byref(_ne29(ne)), float(mu), _ptr(delta))
+            if st != _abi.TLG_OK:
+                rep.failed = True
+                return np.asarray(R0, dtype=np.float64), np.asarray(t0, dtype=np.float64), rep
+            dn = float(np.linalg.norm(delta))
+            if dn < cfg.tol_dstate:
+                local_converged = True
+                break
+            Rc, tc = _retract(R, t, delta)
+            ne_c, _ = total_cost(Rc, tc)
+            if ne_c.cost < ne.cost:
+                dcost = ne.cost - ne_c.cost
+                R, t, ne = Rc, tc, ne_c
+                rep.cost_trace.append(ne.cost)
+                rep.final_cost = ne.cost
+                mu = max(mu * 0.1, 1e-12)
+                rep.accepted_steps += 1
+                improved = True
+                rejects = 0
+                moved += dn
+                if dcost < cfg.tol_dcost or dn < cfg.tol_dstate:
+                    local_converged = True
+                    break
+            else:
+                mu *= 10.0
+                rejects += 1
+                if rejects > cfg.lm_max_rejects:
+                    if rep.accepted_steps == 0:
+                        rep.failed = True
+                        return (np.asarray(R0, dtype=np.float64), np.asarray(t0, dtype=np.float64),
+                                rep)
+                    local_converged = True
+                    break
+        if local_converged and moved < 1e-9:
+            rep.converged = True
+            break
+        if not improved and not local_converged and rep.accepted_steps > 0:
+            rep.converged = True
+            break
+        if rep.degenerate and not improved:
+            break
+    return R, t, rep

@@ -149,3 +149,25 @@ def test_map_voxel_key_all_ones(gpu_ctx):
     om.insert(P, K, np.zeros(3), np.eye(3), np.zeros(3))
     assert np.array_equal(gm.points(1)[0], om.points(1)[0])
     assert len(gm.points(1)[0]) == 2
+
+
+@pytest.mark.gpu
+def test_lm_solve_recovers_pose(gpu_ctx):
+    # map built at known poses; a new scan seen from a displaced pose is
+    # registered from a perturbed guess (scan_matcher.cpp:257-358)
+    gm = M.LocalMap(0.1, 20)
+    for f in range(4):
+        P, K, L = _scene(200 + f, 3000)
+        gm.insert(P, K, L, np.eye(3), np.zeros(3))
+    P, K, _ = _scene(300, 3000)
+    R_true = so3_exp([0.01, -0.005, 0.15])
+    t_true = np.array([0.3, -0.2, 0.02])
+    Ps = (P - t_true) @ R_true + np.random.default_rng(5).normal(0, 0.003, P.shape)
+    R0 = R_true @ so3_exp([0.004, -0.003, 0.03])
+    t0 = t_true + np.array([0.05, -0.04, 0.01])
+    R, t, rep = M.lm_solve(R0, t0, Ps, K, gm)
+    assert not rep.failed and rep.accepted_steps > 0
+    assert np.linalg.norm(t - t_true) < 5e-3
+    ang = np.arccos(np.clip((np.trace(R.T @ R_true) - 1) / 2, -1, 1))
+    assert ang < 1e-3
+    assert rep.cost_trace[-1] < rep.cost_trace[0]
