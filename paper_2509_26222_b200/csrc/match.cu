@@ -218,7 +218,10 @@ __device__ void eigen_sym3(const double A[9], double ev[3], double V[9]) {
   for (int sweep = 0; sweep < 60; ++sweep) {
     const double off = fabs(a[0][1]) + fabs(a[0][2]) + fabs(a[1][2]);
     if (off == 0.0) break;
+    // rolled p/q loops (see k_eigmin6: full unrolling is miscompiled for 6x6)
+#pragma unroll 1
     for (int p = 0; p < 2; ++p)
+#pragma unroll 1
       for (int q = p + 1; q < 3; ++q) {
         if (a[p][q] == 0.0) continue;
         const double theta = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
@@ -1025,7 +1028,11 @@ __global__ void k_eigmin6(const double* __restrict__ ne29, double* __restrict__ 
     for (int p = 0; p < 6; ++p)
       for (int q = p + 1; q < 6; ++q) off += fabs(a[p][q]);
     if (off == 0.0) break;
+    // rolled p/q loops: nvcc 12.9's full unrolling of this in-place rotation
+    // miscompiles (wrong eigenvalues; correct with -Xcicc -O0) — keep rolled
+#pragma unroll 1
     for (int p = 0; p < 5; ++p)
+#pragma unroll 1
       for (int q = p + 1; q < 6; ++q) {
         if (a[p][q] == 0.0) continue;
         const double theta = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);

@@ -171,3 +171,22 @@ def test_lm_solve_recovers_pose(gpu_ctx):
     ang = np.arccos(np.clip((np.trace(R.T @ R_true) - 1) / 2, -1, 1))
     assert ang < 1e-3
     assert rep.cost_trace[-1] < rep.cost_trace[0]
+
+
+@pytest.mark.gpu
+def test_min_eigenvalue_probe(gpu_ctx):
+    # the degeneracy probe of lm_solve against numpy on random SPD 6x6 matrices
+    import ctypes as C
+    from paper_2509_26222_b200 import _abi
+    from paper_2509_26222_b200.kinematics import NormalEq
+    from paper_2509_26222_b200.terrain import Context
+    rng = np.random.default_rng(4)
+    for _ in range(20):
+        G = rng.standard_normal((6, 6)) * rng.uniform(0.1, 100, 6)
+        A = G @ G.T
+        lam = C.c_double()
+        c = M._ne29(NormalEq(A, np.zeros(6), 0.0, 0))
+        _abi.check(_abi.load().tlg_ne_min_eigenvalue(Context.default().handle, C.byref(c),
+                                                     C.byref(lam)))
+        ref = np.linalg.eigvalsh(A)[0]
+        assert abs(lam.value - ref) <= 1e-9 * np.abs(np.linalg.eigvalsh(A)).max()
