@@ -437,6 +437,149 @@ inline Histogram terrain_error_histogram(const terrain::TerrainModel& model,
 
 }  // namespace eval
 
+namespace match {
+
+// types.hpp:36-42 / FeatureCloud
+enum class FeatureKind : uint8_t { Edge = 0, Planar = 1, Ground = 2 };
+struct FeaturePoint {
+  Vec3 p;
+  FeatureKind kind = FeatureKind::Planar;
+  int32_t label = -1;
+};
+struct FeatureCloud {
+  double timestamp = 0.0;
+  std::vector<FeaturePoint> points;
+};
+
+// The association fields of SolverConfig (scan_matcher.hpp:15-49) + LM knobs.
+struct SolverConfig {
+  double lambda_manifold = 1.0, lm_init_damping = 1e-4;
+  int lm_max_iters = 10, lm_max_inner = 8, lm_max_rejects = 12;
+  double tol_dcost = 1e-10, tol_dstate = 1e-10, corr_gate = 1.0;
+  int min_correspondences = 10;
+  double huber_delta = 0.1, manifold_huber_delta = 0.05, plane_fit_tol = 0.025,
+         plane_eig_ratio = 5.0, edge_eig_ratio = 3.0, edge_fit_tol = 0.05, edge_min_extent = 0.05,
+         degeneracy_eig_min = 10.0, trim_ratio = 5.0, trim_floor = 0.003,
+         ground_corr_voxel = 0.25, ground_corr_radius = 4.0;
+  tlg_match_config c() const {
+    return {corr_gate,      huber_delta, plane_fit_tol, plane_eig_ratio,   edge_eig_ratio,
+            edge_fit_tol,   edge_min_extent, trim_ratio, trim_floor, ground_corr_voxel,
+            ground_corr_radius};
+  }
+};
+
+struct MapConfig {
+  double voxel_size = 0.1;
+  std::size_t window = 20;
+};
+
+namespace detail {
+struct Soa3 {
+  std::vector<double> x, y, z;
+  std::vector<uint8_t> kind;
+  std::vector<int32_t> label;
+};
+inline Soa3 split(const FeatureCloud& f) {
+  Soa3 s;
+  for (const auto& p : f.points) {
+    s.x.push_back(p.p.x());
+    s.y.push_back(p.p.y());
+    s.z.push_back(p.p.z());
+    s.kind.push_back(static_cast<uint8_t>(p.kind));
+    s.label.push_back(p.label);
+  }
+  return s;
+}
+}  // namespace detail
+
+// local_map.hpp:17-50 (the kd-trees are device-side uniform grids)
+class LocalMap {
+ public:
+  explicit LocalMap(MapConfig config = {}) {
+    tlg_map* m = nullptr;
+    gpu::check(tlg_map_create(gpu::Context::instance().get(), config.voxel_size, config.window,
+                              &m));
+    m_.reset(m);
+  }
+  void insert(const FeatureCloud& scan, const Mat3& rotation, const Vec3& translation) {
+    const detail::Soa3 s = detail::split(scan);
+    gpu::check(tlg_map_insert(m_.get(), s.x.data(), s.y.data(), s.z.data(), s.kind.data(),
+                              s.label.data(), s.x.size(), TLG_HOST, rotation.a, translation.v));
+  }
+  std::size_t size() const { return count(0) + count(1); }
+  bool empty() const { return size() == 0; }
+  tlg_map* handle() const { return m_.get(); }
+
+ private:
+  std::size_t count(int kind) const {
+    std::size_t n = 0;
+    gpu::check(tlg_map_points(m_.get(), kind, nullptr, nullptr, 0, &n));
+    return n;
+  }
+  struct Del {
+    void operator()(tlg_map* m) const { tlg_map_destroy(m); }
+  };
+  std::unique_ptr<tlg_map, Del> m_;
+};
+
+struct Correspondence {  // scan_matcher.hpp:51-58
+  FeatureKind kind = FeatureKind::Edge;
+  Vec3 p_sensor;
+  Vec3 line_point, line_direction{1.0, 0.0, 0.0}, plane_normal{0.0, 0.0, 1.0};
+  double plane_offset = 0.0, weight = 1.0;
+  int32_t map_label = -1;
+};
+
+// scan_matcher.cpp:44-183 at the pose (R, t); the device keeps the result for
+// feature_normal_eq
+inline std::vector<Correspondence> build_correspondences(const FeatureCloud& features,
+                                                         const Mat3& R, const Vec3& t,
+                                                         const LocalMap& map,
+                                                         const SolverConfig& config) {
+  const detail::Soa3 s = detail::split(features);
+  const tlg_match_config c = config.c();
+  std::size_t n = 0;
+  gpu::check(tlg_build_correspondences(map.handle(), s.x.data(), s.y.data(), s.z.data(),
+                                       s.kind.data(), s.x.size(), TLG_HOST, R.a, t.v, &c, &n));
+  std::vector<int32_t> kind(n), label(n);
+  std::vector<uint32_t> feat(n);
+  std::vector<double> par(7 * n), w(n);
+  gpu::check(tlg_correspondences_get(map.handle(), kind.data(), feat.data(), par.data(), w.data(),
+                                     label.data(), nullptr, nullptr, n));
+  std::vector<Correspondence> out(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    auto& o = out[i];
+    const double* p = &par[7 * i];
+    o.kind = kind[i] == 0 ? FeatureKind::Edge : FeatureKind::Planar;
+    o.p_sensor = features.points[feat[i]].p;
+    if (kind[i] == 0) {
+      o.line_point = {p[0], p[1], p[2]};
+      o.line_direction = {p[3], p[4], p[5]};
+    } else {
+      o.plane_normal = {p[0], p[1], p[2]};
+      o.plane_offset = p[3];
+    }
+    o.weight = w[i];
+    o.map_label = label[i];
+  }
+  return out;
+}
+
+// feature rows of total_cost (scan_matcher.cpp:185-216) for the map's last
+// correspondences, reduced to the normal equations
+inline tlg_normal_eq feature_normal_eq(const LocalMap& map, const Mat3& R, const Vec3& t) {
+  tlg_normal_eq ne{};
+  gpu::check(tlg_feature_normal_eq(map.handle(), R.a, t.v, &ne));
+  return ne;
+}
+
+// scan_matcher.cpp:300-305
+inline bool lm_step(const tlg_normal_eq& ne, double mu, double delta[6]) {
+  return tlg_lm_step(gpu::Context::instance().get(), &ne, mu, delta) == TLG_OK;
+}
+
+}  // namespace match
+
 namespace kin {
 
 // Batched manifold rows (contact.cpp:7-39 + scan_matcher.cpp:221-248) and the

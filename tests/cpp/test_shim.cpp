@@ -121,6 +121,33 @@ int main() {
     batch.export_csv("/tmp/terralio_b200_shim.csv", 0.05);
   }
 
+  // match: map, correspondences, feature normal equations, LM step
+  {
+    match::LocalMap lmap;
+    match::FeatureCloud cloud;
+    std::uniform_real_distribution<double> uu(-2.0, 2.0);
+    for (int i = 0; i < 6000; ++i) {
+      match::FeaturePoint f;
+      if (i % 3 == 0)
+        f = {{uu(rng), uu(rng), 0.0}, match::FeatureKind::Ground, 0};
+      else if (i % 3 == 1)
+        f = {{2.5, uu(rng), 1.0 + 0.5 * uu(rng)}, match::FeatureKind::Planar, 1};
+      else
+        f = {{uu(rng), 2.5, 1.0 + 0.5 * uu(rng)}, match::FeatureKind::Planar, 2};
+      cloud.points.push_back(f);
+    }
+    lmap.insert(cloud, Mat3::Identity(), Vec3{0.0, 0.0, 0.0});
+    CHECK(!lmap.empty());
+    match::SolverConfig sc;
+    const auto corr = match::build_correspondences(cloud, Mat3::Identity(), Vec3{0.01, 0.0, 0.0},
+                                                   lmap, sc);
+    CHECK(corr.size() > 100);
+    const tlg_normal_eq fne = match::feature_normal_eq(lmap, Mat3::Identity(), Vec3{0.01, 0.0, 0.0});
+    CHECK(fne.valid == static_cast<double>(corr.size()));
+    double delta[6];
+    CHECK(match::lm_step(fne, 1e-4, delta));
+  }
+
   // manifold rows + normal equations
   std::vector<Vec3> lever;
   for (int i = 0; i < 1000; ++i) lever.push_back({u(rng), u(rng), 0.05});
