@@ -81,6 +81,16 @@ __device__ __forceinline__ void static_for(F&& f) {
   }
 }
 
+// Boundary pair: the exact reference test d2 = fl(dx^2 + dy^2) <= r2 selects
+// the weight (a select measured faster than predicated inline-PTX FMAs, which
+// block ptxas scheduling: 0.68 vs 0.59 ms)
+__device__ __forceinline__ void bd_pair(double& S, double& T, double d2, double r2, double w,
+                                        double ey, double eyd) {
+  const double wm = d2 <= r2 ? w : 0.0;
+  S = fma(wm, ey, S);
+  T = fma(wm, eyd, T);
+}
+
 template <int WIN, int G>
 __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, double y,
                                                 double r2, double neg_inv_2b2) {
@@ -171,9 +181,7 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
                 S = fma(wv, ey[l], S);
                 T = fma(wv, eyd[l], T);
               } else if constexpr ((bm >> l) & 1u) {
-                const double w = __dadd_rn(dx2, dy2[l]) <= r2 ? wv : 0.0;
-                S = fma(w, ey[l], S);
-                T = fma(w, eyd[l], T);
+                bd_pair(S, T, __dadd_rn(dx2, dy2[l]), r2, wv, ey[l], eyd[l]);
               }
             }
           });
