@@ -20,6 +20,10 @@ uint32_t add_center_host(tlg_model* m, double x, double y);
 void moment_device(tlg_model* m, const double* x, const double* y, size_t n, uint32_t* rowp,
                    uint32_t** ids, double** vals, size_t* nnz);
 void fp64_peak(tlg_ctx* ctx, double* dfma, double* dmma);
+void manifold_device_streamed(tlg_model* m, const double R[9], const double t[3],
+                              const double* hx, const double* hy, const double* hz, size_t n,
+                              double wheel_radius, double lambda_M, double huber, double* r,
+                              double* J, uint8_t* valid, double* raw, tlg_normal_eq* ne);
 double dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps);
 bool debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X, int band);
 size_t select_ground_device(tlg_ctx* ctx, const double* px, const double* py, const double* pz,
@@ -144,6 +148,12 @@ tlg_status tlg_ctx_destroy(tlg_ctx* ctx) {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->stream);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->copy_stream) {
+      cudaStreamSynchronize(ctx->copy_stream);
+      for (auto& e : ctx->copy_ev)
+        if (e) cudaEventDestroy(e);
+      cudaStreamDestroy(ctx->copy_stream);
+    }
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -672,10 +682,16 @@ tlg_status tlg_manifold_rows(tlg_model* m, const double R[9], const double t[3],
       return;
     }
     tlg_ctx* ctx = m->ctx;
+    const bool dev = out_mem == TLG_DEVICE;
+    if (in_mem == TLG_HOST && n >= (size_t{1} << 20) && (dev || (!r && !J && !valid && !raw))) {
+      // large host batches: H2D slices overlap the kernel on earlier slices
+      manifold_device_streamed(m, R, t, hx, hy, hz, n, wheel_radius, lambda_M, huber_delta, r, J,
+                               valid, raw, ne);
+      return;
+    }
     const double* dhx = as_device(ctx, S_IN_HX, hx, n, in_mem);
     const double* dhy = as_device(ctx, S_IN_HY, hy, n, in_mem);
     const double* dhz = as_device(ctx, S_IN_HZ, hz, n, in_mem);
-    const bool dev = out_mem == TLG_DEVICE;
     double* dr = r ? (dev ? r : ctx->ws<double>(S_OUT_R, n)) : nullptr;
     double* dJ = J ? (dev ? J : ctx->ws<double>(S_OUT_J, 6 * n)) : nullptr;
     uint8_t* dv = valid ? (dev ? valid : ctx->ws<uint8_t>(S_OUT_SUP, n)) : nullptr;

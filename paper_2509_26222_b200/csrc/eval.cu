@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kManifoldThreads, TLG_MANIFOLD_MINB) k_manifol
     double neg_inv_2s2, double inv_s2, double wheel_radius, double sl, double huber,
     double* __restrict__ out_r, double* __restrict__ out_J, uint8_t* __restrict__ out_valid,
     double* __restrict__ out_raw, double* __restrict__ partials, size_t nchunks,
-    int* __restrict__ err) {
+    size_t chunk_base, size_t ldj, int* __restrict__ err) {
   // Normal equations on the FP64 tensor pipe: each point contributes the
   // rank-1 Gram V V^T of V = [J, r, valid] (8 components); a warp stages its
   // 32 rows' V in shared memory and 8 DMMA m8n8k4 steps add V^T V into an
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(kManifoldThreads, TLG_MANIFOLD_MINB) k_manifol
       if (out_valid) out_valid[i] = valid ? 1 : 0;
       if (out_J) {
 #pragma unroll
-        for (int c = 0; c < 6; ++c) out_J[c * n + i] = J[c];
+        for (int c = 0; c < 6; ++c) out_J[c * ldj + i] = J[c];
       }
     }
     reinterpret_cast<double2*>(V[lane])[0] = make_double2(J[0], J[1]);
@@ -539,8 +539,8 @@ __global__ void __launch_bounds__(kManifoldThreads, TLG_MANIFOLD_MINB) k_manifol
     h2 = nh2;
     base += 32;
     if (base >= b_end) {  // chunk done: flush its Gram, move to the pre-claimed one
-      if (e0 >= 0) partials[(size_t)e0 * nchunks + chunk / kManifoldChunk] = c0;
-      if (e1 >= 0) partials[(size_t)e1 * nchunks + chunk / kManifoldChunk] = c1;
+      if (e0 >= 0) partials[(size_t)e0 * nchunks + chunk_base + chunk / kManifoldChunk] = c0;
+      if (e1 >= 0) partials[(size_t)e1 * nchunks + chunk_base + chunk / kManifoldChunk] = c1;
       c0 = c1 = 0.0;
       if (next >= witer) break;
       chunk = next;
@@ -606,7 +606,8 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
   TLG_KIND_DISPATCH(sweep_kind(m),
                     (k_manifold<W_><<<blocks, kManifoldThreads, 0, ctx->stream>>>(
                         g, L, pose, hx, hy, hz, n, m->kc.r2, m->kc.neg_inv_2s2, m->kc.inv_s2,
-                        wheel_radius, sl, huber, r, J, valid, raw, partials, nchunks, err)));
+                        wheel_radius, sl, huber, r, J, valid, raw, partials, nchunks, 0, n,
+                        err)));
   TLG_LAUNCHED(ctx);
   prof_mark_end(ctx);
   k_reduce_chunks<<<kNE, kRedThreads, 0, ctx->stream>>>(partials, nchunks, err, out);
@@ -614,6 +615,74 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
   TLG_CUDA(cudaMemcpyAsync(h, out, (kNE + 1) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   TLG_CUDA(cudaStreamSynchronize(ctx->stream));
   prof_collect(ctx);
+  if (h[kNE] != 0.0) throw Error(TLG_DOMAIN_ERROR, "non-finite query");
+  if (ne) {
+    for (int k = 0; k < 21; ++k) ne->A[k] = h[k];
+    for (int k = 0; k < 6; ++k) ne->g[k] = h[21 + k];
+    ne->cost = h[27];
+    ne->valid = h[28];
+  }
+}
+
+// Host-resident lever arms: the H2D copy of slice s+1 (copy stream) overlaps
+// the kernel on slice s (compute stream); every slice is a whole number of
+// 8-iteration chunks, so the per-chunk partials of all slices form one
+// order-fixed reduction, exactly as in a single launch.
+void manifold_device_streamed(tlg_model* m, const double R[9], const double t[3],
+                              const double* hx, const double* hy, const double* hz, size_t n,
+                              double wheel_radius, double lambda_M, double huber, double* r,
+                              double* J, uint8_t* valid, double* raw, tlg_normal_eq* ne) {
+  tlg_ctx* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  ensure_grid(m);
+  if (!ctx->copy_stream) {
+    TLG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : ctx->copy_ev) TLG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  Pose pose;
+  for (int i = 0; i < 9; ++i) pose.R[i] = R[i];
+  for (int i = 0; i < 3; ++i) pose.t[i] = t[i];
+  const size_t nchunks = std::max<size_t>(1, ((n + 31) / 32 + kManifoldChunk - 1) / kManifoldChunk);
+  double* partials = ctx->ws<double>(S_PARTIALS, nchunks * kNE + kNE + 1);
+  double* out = partials + nchunks * kNE;
+  int* err = ctx->ws<int>(S_FLAGS, 4);
+  double* h = static_cast<double*>(ctx->host_stage((kNE + 1) * sizeof(double)));
+  double* dx = ctx->ws<double>(S_IN_HX, n);
+  double* dy = ctx->ws<double>(S_IN_HY, n);
+  double* dz = ctx->ws<double>(S_IN_HZ, n);
+  TLG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
+  const GridView g = grid_view(m);
+  const LatticeView L = lattice_view(m);
+  const double sl = std::sqrt(lambda_M);
+  constexpr size_t kRowsPerChunk = 32 * kManifoldChunk;
+  constexpr int kSlices = 8;
+  const size_t slice = ((n + kSlices - 1) / kSlices + kRowsPerChunk - 1) / kRowsPerChunk * kRowsPerChunk;
+  // the compute stream must not overtake earlier users of the input slots
+  TLG_CUDA(cudaEventRecord(ctx->copy_ev[kSlices], s));
+  TLG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_ev[kSlices], 0));
+  int si = 0;
+  for (size_t off = 0; off < n; off += slice, ++si) {
+    const size_t nc = std::min(slice, n - off);
+    TLG_CUDA(cudaMemcpyAsync(dx + off, hx + off, nc * 8, cudaMemcpyHostToDevice, ctx->copy_stream));
+    TLG_CUDA(cudaMemcpyAsync(dy + off, hy + off, nc * 8, cudaMemcpyHostToDevice, ctx->copy_stream));
+    TLG_CUDA(cudaMemcpyAsync(dz + off, hz + off, nc * 8, cudaMemcpyHostToDevice, ctx->copy_stream));
+    TLG_CUDA(cudaEventRecord(ctx->copy_ev[si], ctx->copy_stream));
+    TLG_CUDA(cudaStreamWaitEvent(s, ctx->copy_ev[si], 0));
+    TLG_CUDA(cudaMemsetAsync(err + 2, 0, 2 * sizeof(int), s));
+    const unsigned blocks = grid_for(ctx, nc, kManifoldThreads, TLG_MANIFOLD_MINB);
+    TLG_KIND_DISPATCH(sweep_kind(m),
+                      (k_manifold<W_><<<blocks, kManifoldThreads, 0, s>>>(
+                          g, L, pose, dx + off, dy + off, dz + off, nc, m->kc.r2,
+                          m->kc.neg_inv_2s2, m->kc.inv_s2, wheel_radius, sl, huber,
+                          r ? r + off : nullptr, J ? J + off : nullptr,
+                          valid ? valid + off : nullptr, raw ? raw + off : nullptr, partials,
+                          nchunks, off / kRowsPerChunk, n, err)));
+    TLG_LAUNCHED(ctx);
+  }
+  k_reduce_chunks<<<kNE, kRedThreads, 0, s>>>(partials, nchunks, err, out);
+  TLG_LAUNCHED(ctx);
+  TLG_CUDA(cudaMemcpyAsync(h, out, (kNE + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  TLG_CUDA(cudaStreamSynchronize(s));
   if (h[kNE] != 0.0) throw Error(TLG_DOMAIN_ERROR, "non-finite query");
   if (ne) {
     for (int k = 0; k < 21; ++k) ne->A[k] = h[k];

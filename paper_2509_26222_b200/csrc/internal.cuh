@@ -116,6 +116,8 @@ struct tlg_ctx_impl;
 struct tlg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // H2D slices overlapping compute (manifold rows)
+  cudaEvent_t copy_ev[9] = {};
   bool own_stream = false;
   uint64_t launches = 0;
   int num_sms = 148;

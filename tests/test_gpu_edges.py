@@ -128,3 +128,22 @@ def test_manifold_rows_deterministic(gpu_ctx):
         ne1 = kin.manifold_rows(g, R, t, h, 0.0, 1.0, 0.05, want=())[1]
         assert np.array_equal(ne1.A, ne0.A) and np.array_equal(ne1.g, ne0.g)
         assert ne1.cost == ne0.cost
+
+
+def test_streamed_host_batch_equals_device(gpu_ctx):
+    # >= 2^20 host lever arms take the sliced H2D/compute-overlap path; the
+    # chunk partials and rows must equal the single-launch device-input path
+    import torch
+    k, cs, g, o = _lattice_model()
+    n = (1 << 20) + 12345
+    rng = np.random.default_rng(8)
+    h = np.ascontiguousarray(np.c_[rng.uniform(-0.05, 1.1, n), rng.uniform(-0.05, 1.1, n),
+                                   np.full(n, 0.03)])
+    R = so3_exp([0.01, -0.02, 0.3])
+    t = np.array([0.05, 0.02, 0.1])
+    hs = tuple(np.ascontiguousarray(h[:, j]) for j in range(3))
+    _, ne_h = kin.manifold_rows(g, R, t, hs, 0.0, 1.0, 0.05, want=())
+    hd = tuple(torch.from_numpy(a).cuda() for a in hs)
+    rows_d, ne_d = kin.manifold_rows(g, R, t, hd, 0.0, 1.0, 0.05, want=("r", "valid"))
+    assert np.array_equal(ne_h.A, ne_d.A) and np.array_equal(ne_h.g, ne_d.g)
+    assert ne_h.cost == ne_d.cost and ne_h.valid == ne_d.valid
