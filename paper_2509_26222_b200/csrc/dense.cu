@@ -1451,56 +1451,62 @@ __global__ void __launch_bounds__(128) k_potrf_coop32(double* __restrict__ A, in
 }
 
 // Banded Cholesky solve L L^T x = b with the 32-wide factor (L in A, the
-// diagonal-tile inverses in linv): one CTA walks the tile rows forward
-// (y_k = Linv_kk (b_k - sum_j L_kj y_j), j in the band) and back
-// (x_k = Linv_kk^T (y_k - sum_i L_ik^T x_i)). Each step is a 32 x (32 bwt)
-// GEMV split over the 4 warps, then a 32 x 32 one.
-__global__ void __launch_bounds__(128) k_band_solve32(const double* __restrict__ L, int n, int ld,
-                                                      int bwt, const double* __restrict__ linv,
-                                                      double* __restrict__ b) {
-  __shared__ double part[4][32];
-  __shared__ double t[32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+// diagonal-tile inverses in linv), one cooperative launch, right-looking and
+// one grid barrier per tile step. Forward: every CTA forms y_k = Linv_kk b_k
+// (32 x 32, redundantly), then subtracts L_ik y_k from the band rows below
+// (thread per row, coalesced along the row index). Backward: x_k =
+// Linv_kk^T z_k, then z_c -= sum_r L_rc x_r for the band columns to the left
+// (thread per column, contiguous 32-row reads).
+__global__ void __launch_bounds__(128) k_band_solve_coop(const double* __restrict__ L, int n,
+                                                         int ld, int bwt,
+                                                         const double* __restrict__ linv,
+                                                         double* __restrict__ b,
+                                                         double* __restrict__ y) {
+  __shared__ double sk[NB32], sv[NB32];
+  cg::grid_group grid = cg::this_grid();
   const int nt = (n + NB32 - 1) / NB32;
-  for (int k = 0; k < nt; ++k) {  // forward
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  for (int k = 0; k < nt; ++k) {  // forward: y = L^-1 b
     const int k0 = k * NB32, kb = min(NB32, n - k0);
-    const int j0 = max(0, k - bwt) * NB32;
-    double acc = 0.0;
-    if (lane < kb)
-      for (int c = j0 + w; c < k0; c += 4) acc = fma(L[k0 + lane + (size_t)c * ld], b[c], acc);
-    part[w][lane] = acc;
+    if (threadIdx.x < NB32) sk[threadIdx.x] = threadIdx.x < kb ? b[k0 + threadIdx.x] : 0.0;
     __syncthreads();
-    if (w == 0) t[lane] = lane < kb ? b[k0 + lane] - (part[0][lane] + part[1][lane] +
-                                                       part[2][lane] + part[3][lane]) : 0.0;
-    __syncthreads();
-    if (w == 0 && lane < kb) {
+    if (threadIdx.x < kb) {
       const double* Li = linv + (size_t)k * NB32 * NB32;
-      double y = 0.0;
-      for (int c = 0; c <= lane; ++c) y = fma(Li[lane + c * NB32], t[c], y);
-      b[k0 + lane] = y;
+      double v = 0.0;
+      for (int c = 0; c <= (int)threadIdx.x; ++c) v = fma(Li[threadIdx.x + c * NB32], sk[c], v);
+      sv[threadIdx.x] = v;
+      if (blockIdx.x == 0) y[k0 + threadIdx.x] = v;
     }
     __syncthreads();
+    const int r0 = k0 + kb, r1 = min(n, (min(nt - 1, k + bwt) + 1) * NB32);
+    for (int r = r0 + tid; r < r1; r += nth) {
+      double acc = 0.0;
+      for (int c = 0; c < kb; ++c) acc = fma(L[r + (size_t)(k0 + c) * ld], sv[c], acc);
+      b[r] -= acc;
+    }
+    grid.sync();
   }
-  for (int k = nt - 1; k >= 0; --k) {  // backward
+  for (int k = nt - 1; k >= 0; --k) {  // backward: x = L^-T y (in y)
     const int k0 = k * NB32, kb = min(NB32, n - k0);
-    const int i1 = min(nt - 1, k + bwt);
-    const int r_end = min(n, (i1 + 1) * NB32);
-    double acc = 0.0;
-    if (lane < kb)
-      for (int r = k0 + kb + w; r < r_end; r += 4)
-        acc = fma(L[r + (size_t)(k0 + lane) * ld], b[r], acc);
-    part[w][lane] = acc;
+    if (threadIdx.x < NB32) sk[threadIdx.x] = threadIdx.x < kb ? y[k0 + threadIdx.x] : 0.0;
     __syncthreads();
-    if (w == 0) t[lane] = lane < kb ? b[k0 + lane] - (part[0][lane] + part[1][lane] +
-                                                       part[2][lane] + part[3][lane]) : 0.0;
-    __syncthreads();
-    if (w == 0 && lane < kb) {
+    if (threadIdx.x < kb) {
       const double* Li = linv + (size_t)k * NB32 * NB32;
-      double x = 0.0;
-      for (int r = lane; r < kb; ++r) x = fma(Li[r + lane * NB32], t[r], x);
-      b[k0 + lane] = x;
+      double v = 0.0;
+      for (int r = threadIdx.x; r < kb; ++r) v = fma(Li[r + threadIdx.x * NB32], sk[r], v);
+      sv[threadIdx.x] = v;
     }
     __syncthreads();
+    grid.sync();  // every CTA has read y_k before block 0 overwrites it
+    if (blockIdx.x == 0 && threadIdx.x < kb) y[k0 + threadIdx.x] = sv[threadIdx.x];
+    const int c0 = max(0, k - bwt) * NB32;
+    for (int c = c0 + tid; c < k0; c += nth) {
+      const double* col = L + (size_t)c * ld + k0;
+      double acc = 0.0;
+      for (int r = 0; r < kb; ++r) acc = fma(col[r], sv[r], acc);
+      y[c] -= acc;
+    }
+    grid.sync();
   }
 }
 
@@ -1508,10 +1514,18 @@ void band_solve(tlg_ctx* ctx, const double* L, int n, int ld, int band, double* 
   if (n <= 0) return;
   require(ctx->linv32_owner == L, TLG_RUNTIME_ERROR, "band_solve: matrix was not factored last");
   const int nt = (n + NB32 - 1) / NB32;
-  const int bwt = std::min(nt - 1, (std::max(band, 0) + NB32 - 1) / NB32);
+  int bwt = std::min(nt - 1, (std::max(band, 0) + NB32 - 1) / NB32);
   const double* linv = ctx->ws<double>(S_LINV, 1);
-  k_band_solve32<<<1, 128, 0, ctx->stream>>>(L, n, ld, bwt, linv, b);
-  TLG_LAUNCHED(ctx);
+  double* y = ctx->ws<double>(S_XINV2, n);
+  int per_sm = 0;
+  TLG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_band_solve_coop, 128, 0));
+  const int rows = (bwt + 1) * NB32;
+  const int grid = std::max(1, std::min((rows + 127) / 128, ctx->num_sms * std::max(per_sm, 1)));
+  void* args[] = {&L, &n, &ld, &bwt, &linv, &b, &y};
+  TLG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_band_solve_coop), dim3(grid),
+                                       dim3(128), args, 0, ctx->stream));
+  ++ctx->launches;
+  TLG_CUDA(cudaMemcpyAsync(b, y, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, ctx->stream));
 }
 
 // B <- L^-1 B (trans = 0) or L^-T B (trans = 1), one CTA per 64-column slab
