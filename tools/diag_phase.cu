@@ -1,4 +1,4 @@
-// Phase timing of tile_potrf_inv_b4 (clock64 at TLG_PHASE hooks, warp 0 lane 0
+// Phase timing of tile_potrf_inv_la (clock64 at TLG_PHASE hooks: warp 0 vs worker warps)
 // and the colown/rowown threads). nvcc ... -I paper_2509_26222_b200/csrc tools/diag_phase.cu
 __device__ long long g_ph[16];
 __shared__ long long s_ph[16];
