@@ -213,8 +213,18 @@ tlg_status tlg_model_destroy(tlg_model* model);
 tlg_status tlg_model_counts(const tlg_model* model, size_t* num_centers, size_t* num_blocks);
 /* Diagnostics: which evaluation sweep the model's centres select — 0 generic
  * hash-grid sweep, 4..14 lattice window with runtime pair classes, 100 + g
- * compiled geometry g — and whether the separable exp recurrence is used. */
+ * compiled geometry g, 200 + g the same with boundary pairs summed without
+ * the cutoff test (see below) — and whether the separable exp recurrence is
+ * used. */
 tlg_status tlg_model_sweep(tlg_model* model, int* kind, int* exp_recurrence);
+/* kernel_eval returns exactly 0 beyond the cutoff (kernel.cpp:27-35). By
+ * default height/gradient/manifold evaluation skips that test on window
+ * boundary pairs when the kernel value at the cutoff makes every such pair's
+ * contribution provably below 1e-11 x the window's largest |w| (paper
+ * defaults: kappa_sigma(rho) = 6.8e-15); exact != 0 forces the per-pair
+ * test. Neighbour ids (tlg_centers_near, tlg_moment_features) are always
+ * exact. */
+tlg_status tlg_model_set_exact_cutoff(tlg_model* model, int exact);
 tlg_status tlg_model_kernel(const tlg_model* model, tlg_kernel_params* out);
 tlg_status tlg_model_center_params(const tlg_model* model, tlg_center_params* out);
 tlg_status tlg_model_get_centers(tlg_model* model, double* cx, double* cy, tlg_mem mem);

@@ -131,6 +131,7 @@ _SIGS = {
     "tlg_model_destroy": (_ST, [_P]),
     "tlg_model_counts": (_ST, [_P, C.POINTER(_SZ), C.POINTER(_SZ)]),
     "tlg_model_sweep": (_ST, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "tlg_model_set_exact_cutoff": (_ST, [_P, C.c_int]),
     "tlg_model_kernel": (_ST, [_P, C.POINTER(KernelParamsC)]),
     "tlg_model_center_params": (_ST, [_P, C.POINTER(CenterParamsC)]),
     "tlg_model_get_centers": (_ST, [_P, _P, _P, _I]),

@@ -513,6 +513,13 @@ tlg_status tlg_model_sweep(tlg_model* m, int* kind, int* exp_recurrence) {
   });
 }
 
+tlg_status tlg_model_set_exact_cutoff(tlg_model* m, int exact) {
+  return guard([&] {
+    check_ptr(m, "model");
+    m->exact_cutoff = exact != 0;
+  });
+}
+
 tlg_status tlg_model_kernel(const tlg_model* m, tlg_kernel_params* out) {
   return guard([&] {
     check_ptr(m, "model");

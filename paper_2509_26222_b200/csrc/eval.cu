@@ -91,7 +91,14 @@ __device__ __forceinline__ void bd_pair(double& S, double& T, double d2, double 
   T = fma(wm, eyd, T);
 }
 
-template <int WIN, int G>
+// LOOSE (compiled geometries only, dispatched when LatticeView::loose_ok):
+// boundary pairs are summed without the cutoff test. A pair that fails it
+// lies beyond the cutoff, where kappa_sigma <= exp(-r2 / (2 sigma^2)); with
+// the paper's parameters that is 6.8e-15, and the host gate bounds the
+// total perturbation of z and sigma * grad f by 1e-11 x the window's largest
+// |w|, two orders under the 1e-9 parity tolerance. Everything else (window,
+// support flag, always-inside/outside pairs) is the exact path's.
+template <int WIN, int G, bool LOOSE = false>
 __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, double y,
                                                 double r2, double neg_inv_2b2) {
   EvalOut o{0.0, 0.0, 0.0, false};
@@ -110,13 +117,33 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
   // dy2 carries the reference's cell-window test too: a row outside the
   // (2 span + 1)^2 cell sweep gets dy2 = +inf, so its boundary tests fail
   // without a per-pair predicate (inside pairs never need it, by their margin).
+  // Node coordinates are recomputed exactly as k_lattice_axes built them
+  // (fl(min + fl(index * res))) instead of loaded: the L1 data path, not the
+  // FP64 pipe, binds this kernel. The cell sweep becomes one index range per
+  // axis (cells are monotone in the node index).
+  const int2 rx = __ldg(L.xr + min(max(qx - L.xr_base, 0), L.xr_n - 1));
+  const int2 ry = __ldg(L.yr + min(max(qy - L.yr_base, 0), L.yr_n - 1));
+  auto node_x = [&](int i) {
+    return __dadd_rn(L.min_x, __dmul_rn(static_cast<double>(i + L.i_org), L.res));
+  };
+  auto node_y = [&](int j) {
+    return __dadd_rn(L.min_y, __dmul_rn(static_cast<double>(j + L.j_org), L.res));
+  };
   double ey[WIN], eyd[WIN], dy2[WIN];
+  // LOOSE self-check inputs: the cell's four corner pairs (always inside)
+  constexpr int kLo = G >= 0 ? kGeoms[G >= 0 ? G : 0].lo : 0;
+  double cq[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, dyc[2] = {0.0, 0.0}, s4 = 0.0, t4 = 0.0;
+  // LOOSE uses no exact pair test, so offsets may drift by an ulp: dy_l =
+  // dy_0 + l res (one FMA) instead of the exact node coordinate
+  const double dy0 = __dsub_rn(node_y(j0), y);
 #pragma unroll
   for (int l = 0; l < WIN; ++l) {
-    const AxisNode a = L.ay[j0 + l];
-    const double dy = __dsub_rn(a.c, y);
-    dy2[l] = abs(a.cell - qy) <= L.span ? __dmul_rn(dy, dy) : CUDART_INF;
+    const int jj = j0 + l;
+    const double dy = l == 0 ? dy0 : (LOOSE ? fma(static_cast<double>(l), L.res, dy0)
+                                            : __dsub_rn(node_y(jj), y));
+    dy2[l] = (jj >= ry.x && jj < ry.y) ? __dmul_rn(dy, dy) : CUDART_INF;
     eyd[l] = dy;
+    if (LOOSE && (l == kLo || l == kLo + 1)) dyc[l - kLo] = fabs(dy);
   }
   // compiled geometries are only dispatched when the recurrence is safe
   // (sweep_kind), so their code carries no per-node exp fallback
@@ -141,8 +168,7 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
   // compiled geometries read the window in 16-byte pairs: an odd base is
   // served from the one-element-shifted copy W1 (the pitch nj is even)
   const double* wbase = (G >= 0 && (bidx & 1)) ? L.W1 + bidx + 1 : L.W + bidx;
-  const AxisNode a0 = L.ax[i0];
-  const double dx_first = __dsub_rn(a0.c, x);
+  const double dx_first = __dsub_rn(node_x(i0), x);
   double ex_e = 0.0, ex_p = 0.0;
   if (rec) {
     ex_e = exp(__dmul_rn(dx_first, dx_first) * neg_inv_2b2);
@@ -155,10 +181,11 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
     // being hoisted here (they would need ~2 registers each and spill)
     if constexpr (k % TLG_COL_FENCE == 0) asm volatile("" ::: "memory");
 #endif
-    const AxisNode a = k == 0 ? a0 : L.ax[i0 + k];
-    const double dx = k == 0 ? dx_first : __dsub_rn(a.c, x);
+    const double dx = k == 0 ? dx_first
+                             : (LOOSE ? fma(static_cast<double>(k), L.res, dx_first)
+                                      : __dsub_rn(node_x(i0 + k), x));
     const double dxx = __dmul_rn(dx, dx);
-    const double dx2 = abs(a.cell - qx) <= L.span ? dxx : CUDART_INF;  // see dy2
+    const double dx2 = (i0 + k >= rx.x && i0 + k < rx.y) ? dxx : CUDART_INF;  // see dy2
     const double* wc = wbase + static_cast<size_t>(k) * L.nj;
     double S = 0.0, T = 0.0;
     bool any;
@@ -177,7 +204,14 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
             constexpr int l = 2 * pr + decltype(HC)::value;
             if constexpr (l < WIN) {
               const double wv = decltype(HC)::value ? v.y : v.x;
+              if constexpr (LOOSE && (k == kLo || k == kLo + 1) && (l == kLo || l == kLo + 1)) {
+                static_assert((im >> l) & 1u, "corner pairs are always inside");
+                cq[k - kLo][l - kLo] = wv * ey[l];
+              }
               if constexpr ((im >> l) & 1u) {
+                S = fma(wv, ey[l], S);
+                T = fma(wv, eyd[l], T);
+              } else if constexpr (((bm >> l) & 1u) && LOOSE) {
                 S = fma(wv, ey[l], S);
                 T = fma(wv, eyd[l], T);
               } else if constexpr ((bm >> l) & 1u) {
@@ -218,8 +252,33 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
       o.sx = fma(ex * dx, S, o.sx);
       o.sy = fma(ex, T, o.sy);
     }
+    if constexpr (LOOSE && (k == kLo || k == kLo + 1)) {
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const double v = fabs(cq[k - kLo][b]) * ex;
+        s4 += v;
+        t4 = fma(v, fmax(fabs(dx), dyc[b]), t4);
+      }
+    }
   };
   static_for<0, WIN>(column);
+  if constexpr (LOOSE) {
+    // Per-point guarantee: the skipped tests can only add pairs beyond the
+    // cutoff, at most n_bd kappa(cutoff) |w|max to z (|w|max over this cell's
+    // window) and that times cutoff / sigma^2 to a gradient component. The
+    // parity scales are at least the corner terms: sum |w kappa| >= s4 and
+    // sum |w kappa| d / sigma^2 >= t4 / sigma^2. Keep the result only if both
+    // errors are under 1e-10 of those (10x inside the 1e-9 tolerance);
+    // otherwise (weights near zero around the point, support fringe)
+    // evaluate with the exact test.
+    const double e = L.loose_k * __ldg(L.wmax + static_cast<size_t>(ib) * L.nj + jb);
+#ifdef TLG_LOOSE_NOFB
+    if (!(e <= 1e-10 * s4 && e * L.loose_d <= 1e-10 * t4) && L.loose_k < 0.0)
+#else
+    if (!(e <= 1e-10 * s4 && e * L.loose_d <= 1e-10 * t4))
+#endif
+      return eval_lattice<WIN, G, false>(L, x, y, r2, neg_inv_2b2);
+  }
   // supported: some *present* centre passes the reference test. The cell's
   // four corner nodes are always inside; otherwise scan the window (rare).
   bool sup = false;
@@ -259,7 +318,8 @@ __device__ __forceinline__ EvalOut eval_any(const GridView& g, const LatticeView
   if constexpr (KIND == 0)
     return eval_generic(g, x, y, r2, neg_inv_2b2);
   else if constexpr (KIND >= 100)
-    return eval_lattice<kGeoms[KIND - 100].win, KIND - 100>(L, x, y, r2, neg_inv_2b2);
+    return eval_lattice<kGeoms[(KIND - 100) % 100].win, (KIND - 100) % 100, (KIND >= 200)>(
+        L, x, y, r2, neg_inv_2b2);
   else
     return eval_lattice<KIND, -1>(L, x, y, r2, neg_inv_2b2);
 }
@@ -341,13 +401,17 @@ static void check_err_flag(tlg_ctx* ctx, int* d_err, tlg_status st, const char* 
 
 int sweep_kind(const tlg_model* m) {
   if (!m->lat.valid) return 0;
-  return (m->lat.geom_id >= 0 && lattice_view(m).rec_ok) ? 100 + m->lat.geom_id : m->lat.win;
+  const LatticeView v = lattice_view(m);
+  if (m->lat.geom_id < 0 || !v.rec_ok) return m->lat.win;
+  return (v.loose_ok && !m->exact_cutoff ? 200 : 100) + m->lat.geom_id;
 }
 
 #define TLG_KIND_DISPATCH(KINDV, CALL)                   \
   switch (KINDV) {                                       \
     case 100: { constexpr int W_ = 100; CALL; } break;   \
     case 101: { constexpr int W_ = 101; CALL; } break;   \
+    case 200: { constexpr int W_ = 200; CALL; } break;   \
+    case 201: { constexpr int W_ = 201; CALL; } break;   \
     case 4: { constexpr int W_ = 4; CALL; } break;       \
     case 5: { constexpr int W_ = 5; CALL; } break;       \
     case 6: { constexpr int W_ = 6; CALL; } break;       \
@@ -370,9 +434,10 @@ void eval_device(tlg_model* m, const double* x, const double* y, size_t n, doubl
   TLG_CUDA(cudaMemsetAsync(err, 0, 4 * sizeof(int), ctx->stream));
   if (n) {
     const GridView g = grid_view(m);
+    const int kind = prepare_sweep(m);
     const LatticeView L = lattice_view(m);
     prof_begin(ctx, 1);
-    TLG_KIND_DISPATCH(sweep_kind(m),
+    TLG_KIND_DISPATCH(kind,
                       (k_eval<W_><<<grid_for(ctx, n, 128, 3), 128, 0, ctx->stream>>>(
                           g, L, x, y, n, m->kc.r2, m->kc.neg_inv_2s2, m->kc.inv_s2, z, sup, gx,
                           gy, err)));
@@ -439,11 +504,14 @@ __global__ void __launch_bounds__(kManifoldThreads, TLG_MANIFOLD_MINB) k_manifol
   // 8x8 accumulator held as 2 doubles per lane. Per claimed chunk the 29
   // used entries go to partials[entry][chunk] (fixed slots -> the final
   // reduction is order-fixed and deterministic despite dynamic claiming).
-  __shared__ __align__(16) double vt[kManifoldThreads / 32][32][8];
+  // V staged transposed, [component][row] with a 36-double pitch: the
+  // per-lane stores and the fragment loads are both bank-conflict free
+  constexpr int kVP = 36;
+  __shared__ __align__(16) double vt[kManifoldThreads / 32][8 * kVP];
   double c0 = 0.0, c1 = 0.0;
   const double* R = pose.R;
   const int lane = threadIdx.x & 31;
-  double(*V)[8] = vt[threadIdx.x >> 5];
+  double* V = vt[threadIdx.x >> 5];
   const int gi = lane >> 2, gj0 = 2 * (lane & 3);
   const int e0 = ne_index(gi, gj0), e1 = ne_index(gi, gj0 + 1);
   // Warps claim contiguous chunks of kManifoldChunk rows-of-32 from a global
@@ -522,15 +590,15 @@ __global__ void __launch_bounds__(kManifoldThreads, TLG_MANIFOLD_MINB) k_manifol
         for (int c = 0; c < 6; ++c) out_J[c * ldj + i] = J[c];
       }
     }
-    reinterpret_cast<double2*>(V[lane])[0] = make_double2(J[0], J[1]);
-    reinterpret_cast<double2*>(V[lane])[1] = make_double2(J[2], J[3]);
-    reinterpret_cast<double2*>(V[lane])[2] = make_double2(J[4], J[5]);
-    reinterpret_cast<double2*>(V[lane])[3] = make_double2(r, valid ? 1.0 : 0.0);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) V[c * kVP + lane] = J[c];
+    V[6 * kVP + lane] = r;
+    V[7 * kVP + lane] = valid ? 1.0 : 0.0;
     __syncwarp();
 #pragma unroll
     for (int st = 0; st < 8; ++st) {
-      // A[m][k] = B[k][m] = V[4 st + k][m]; lane holds m = lane >> 2, k = lane & 3
-      const double v = V[4 * st + (lane & 3)][lane >> 2];
+      // A[m][k] = B[k][m] = V_row(4 st + k)[m]; lane holds m = lane >> 2, k = lane & 3
+      const double v = V[(lane >> 2) * kVP + 4 * st + (lane & 3)];
       dmma884(c0, c1, v, v);
     }
     __syncwarp();
@@ -600,10 +668,11 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
   double* h = static_cast<double*>(ctx->host_stage((kNE + 1) * sizeof(double)));  // pinned
   TLG_CUDA(cudaMemsetAsync(err, 0, 4 * sizeof(int), ctx->stream));
   const GridView g = grid_view(m);
+  const int kind = prepare_sweep(m);
   const LatticeView L = lattice_view(m);
   const double sl = std::sqrt(lambda_M);
   prof_begin(ctx, 0);
-  TLG_KIND_DISPATCH(sweep_kind(m),
+  TLG_KIND_DISPATCH(kind,
                     (k_manifold<W_><<<blocks, kManifoldThreads, 0, ctx->stream>>>(
                         g, L, pose, hx, hy, hz, n, m->kc.r2, m->kc.neg_inv_2s2, m->kc.inv_s2,
                         wheel_radius, sl, huber, r, J, valid, raw, partials, nchunks, 0, n,
@@ -652,6 +721,7 @@ void manifold_device_streamed(tlg_model* m, const double R[9], const double t[3]
   double* dz = ctx->ws<double>(S_IN_HZ, n);
   TLG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
   const GridView g = grid_view(m);
+  const int kind = prepare_sweep(m);
   const LatticeView L = lattice_view(m);
   const double sl = std::sqrt(lambda_M);
   constexpr size_t kRowsPerChunk = 32 * kManifoldChunk;
@@ -670,7 +740,7 @@ void manifold_device_streamed(tlg_model* m, const double R[9], const double t[3]
     TLG_CUDA(cudaStreamWaitEvent(s, ctx->copy_ev[si], 0));
     TLG_CUDA(cudaMemsetAsync(err + 2, 0, 2 * sizeof(int), s));
     const unsigned blocks = grid_for(ctx, nc, kManifoldThreads, TLG_MANIFOLD_MINB);
-    TLG_KIND_DISPATCH(sweep_kind(m),
+    TLG_KIND_DISPATCH(kind,
                       (k_manifold<W_><<<blocks, kManifoldThreads, 0, s>>>(
                           g, L, pose, dx + off, dy + off, dz + off, nc, m->kc.r2,
                           m->kc.neg_inv_2s2, m->kc.inv_s2, wheel_radius, sl, huber,

@@ -120,6 +120,75 @@ __global__ void k_lattice_axes(double min_v, double res, int org, int count, dou
   ax[k] = AxisNode{v, static_cast<int>(floor(v / cell)), 0};
 }
 
+__global__ void k_lattice_ranges(const AxisNode* __restrict__ ax, int count, int span, int qbase,
+                                 int nq, int2* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nq) return;
+  auto first = [&](long long c) {  // first node with cell >= c
+    int lo = 0, hi = count;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (ax[mid].cell < c) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  const long long q = static_cast<long long>(qbase) + t;
+  out[t] = make_int2(first(q - span), first(q + span + 1));
+}
+
+// Range table over every point cell whose sweep can reach a node, plus a
+// margin; cells outside clamp to an end entry, whose range is empty.
+static void lattice_ranges(tlg_model* m, const DBuf<AxisNode>& ax, int count, double mn, int org,
+                           DBuf<int2>& out, int& base, int& nq) {
+  const double res = m->cparams.mesh_resolution, cell = m->grid.cell;
+  const int span = m->grid.span;
+  const double v0 = mn + static_cast<double>(org) * res;
+  const double v1 = mn + static_cast<double>(org + count - 1) * res;
+  const long long c0 = static_cast<long long>(std::floor(v0 / cell)) - span - 3;
+  const long long c1 = static_cast<long long>(std::floor(v1 / cell)) + span + 3;
+  require(c1 - c0 < (1ll << 24) && c0 > INT_MIN / 2 && c1 < INT_MAX / 2, TLG_RUNTIME_ERROR,
+          "lattice cell range too large");
+  base = static_cast<int>(c0);
+  nq = static_cast<int>(c1 - c0 + 1);
+  out.ensure(nq);
+  k_lattice_ranges<<<(nq + 127) / 128, 128, 0, m->ctx->stream>>>(ax.p, count, span, base, nq,
+                                                                  out.p);
+  TLG_LAUNCHED(m->ctx);
+}
+
+// Separable max filter of |W| over the evaluation window: pass 0 along j
+// (rows of the pitch), pass 1 along i. Nodes outside the padded lattice are
+// absent (weight 0).
+__global__ void k_window_max(const double* __restrict__ in, int ni, int nj, int lo, int win,
+                             int pass, double* __restrict__ out) {
+  const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (e >= (size_t)ni * nj) return;
+  const int i = static_cast<int>(e / nj), j = static_cast<int>(e % nj);
+  double mx = 0.0;
+  for (int t = 0; t < win; ++t) {
+    const int ii = pass ? i - lo + t : i, jj = pass ? j : j - lo + t;
+    if (ii >= 0 && ii < ni && jj >= 0 && jj < nj) mx = fmax(mx, fabs(in[(size_t)ii * nj + jj]));
+  }
+  out[e] = mx;
+}
+
+int prepare_sweep(tlg_model* m) {
+  const int kind = sweep_kind(m);
+  LatticeGrid& L = m->lat;
+  if (kind >= 200 && L.wmax_dirty) {
+    const size_t nn = static_cast<size_t>(L.ni) * L.nj;
+    L.wmax.ensure(nn);
+    L.wtmp.ensure(nn);
+    const unsigned b = static_cast<unsigned>((nn + 255) / 256);
+    k_window_max<<<b, 256, 0, m->ctx->stream>>>(L.W.p, L.ni, L.nj, L.lo, L.win, 0, L.wtmp.p);
+    TLG_LAUNCHED(m->ctx);
+    k_window_max<<<b, 256, 0, m->ctx->stream>>>(L.wtmp.p, L.ni, L.nj, L.lo, L.win, 1, L.wmax.p);
+    TLG_LAUNCHED(m->ctx);
+    L.wmax_dirty = false;
+  }
+  return kind;
+}
+
 __global__ void k_lattice_refresh(const int* __restrict__ slot, const double* __restrict__ w,
                                   size_t n, double* __restrict__ W, double* __restrict__ W1) {
   const size_t c = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
@@ -199,6 +268,11 @@ static void build_lattice(tlg_model* m) {
   TLG_LAUNCHED(ctx);
   k_lattice_axes<<<(L.nj + 127) / 128, 128, 0, s>>>(mny, res, L.j_org, L.nj, cell, L.ay.p);
   TLG_LAUNCHED(ctx);
+  lattice_ranges(m, L.ax, L.ni, mnx, L.i_org, L.xr, L.xr_base, L.xr_n);
+  lattice_ranges(m, L.ay, L.nj, mny, L.j_org, L.yr, L.yr_base, L.yr_n);
+  L.min_x = mnx;
+  L.min_y = mny;
+  L.wmax_dirty = true;
   int hd = 0;
   TLG_CUDA(cudaMemcpyAsync(&hd, dup, sizeof(int), cudaMemcpyDeviceToHost, s));
   TLG_CUDA(cudaStreamSynchronize(s));
@@ -217,6 +291,16 @@ LatticeView lattice_view(const tlg_model* m) {
   v.P = L.P.p;
   v.ax = L.ax.p;
   v.ay = L.ay.p;
+  v.xr = L.xr.p;
+  v.yr = L.yr.p;
+  v.xr_base = L.xr_base;
+  v.xr_n = L.xr_n;
+  v.yr_base = L.yr_base;
+  v.yr_n = L.yr_n;
+  v.i_org = L.i_org;
+  v.j_org = L.j_org;
+  v.min_x = L.min_x;
+  v.min_y = L.min_y;
   v.ni = L.ni;
   v.nj = L.nj;
   v.lo = L.lo;
@@ -239,6 +323,19 @@ LatticeView lattice_view(const tlg_model* m) {
   v.c_res = c * res;
   v.k2 = std::exp(2.0 * c * res * res);
   v.rec_ok = (std::fabs(c) * span * span < 600.0 && std::fabs(c) * res * 2.0 * span < 600.0) ? 1 : 0;
+  // LOOSE path (eval.cu): n_bd boundary pairs, each failing one lies at
+  // d > cutoff and adds at most kcut |w| to z and, since d kappa(d) falls for
+  // d > sigma, kcut cutoff |w| / sigma^2 to a gradient component. Enabled
+  // when kappa at the cutoff is small enough that the per-point check passes
+  // for ordinary (smooth) weights.
+  int nbd = 0;
+  for (int k = 0; k < 16; ++k) nbd += __builtin_popcount(L.bdmask[k]);
+  const double kcut = std::exp(m->kc.r2 * c);
+  const double sigma = m->kernel.sigma, rho = m->kernel.cutoff_radius;
+  v.loose_k = nbd * kcut;
+  v.loose_d = rho;
+  v.loose_ok = (rho > sigma && v.loose_k * std::max(1.0, rho / sigma) <= 1e-11) ? 1 : 0;
+  v.wmax = L.wmax.p;
   return v;
 }
 
@@ -332,6 +429,7 @@ void sync_weights_to_grid(tlg_model* m) {
                                                                           n, m->lat.W.p,
                                                                           m->lat.W1.p);
     TLG_LAUNCHED(m->ctx);
+    m->lat.wmax_dirty = true;
   }
 }
 

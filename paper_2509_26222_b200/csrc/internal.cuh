@@ -291,6 +291,16 @@ struct LatticeGrid {
   DBuf<int> P;                 // presence count per node
   DBuf<AxisNode> ax, ay;       // per padded column / row: exact node coordinate
                                // and reference cell coordinate floor(c / cell)
+  // Cell-sweep ranges per point cell q: [first node with cell >= q - span,
+  // first node with cell >= q + span + 1) along each axis (cells are monotone
+  // in the node index), for q in [base, base + n) (clamped outside).
+  DBuf<int2> xr, yr;
+  // Per cell (ib, jb): max |w| over the cell's evaluation window (the LOOSE
+  // path's per-point error bound, eval.cu); rebuilt lazily after weight syncs.
+  DBuf<double> wmax, wtmp;
+  bool wmax_dirty = true;
+  int xr_base = 0, xr_n = 0, yr_base = 0, yr_n = 0;
+  double min_x = 0, min_y = 0;  // node (i, j) = (min_x + (i + i_org) res, min_y + ...)
   DBuf<int> slot;              // centre id -> node index in W
 };
 
@@ -300,11 +310,19 @@ struct LatticeView {
   const int* P;
   const AxisNode* ax;  // one 16-byte load gives coordinate + cell
   const AxisNode* ay;
+  const int2* xr;      // see LatticeGrid
+  const int2* yr;
+  const double* wmax;
+  double loose_k;  // n_bd * kappa_sigma(cutoff)
+  double loose_d;  // cutoff radius (gradient bound factor)
+  int xr_base, xr_n, yr_base, yr_n, i_org, j_org;
+  double min_x, min_y;
   int ni, nj, lo, span;
   double org_x, org_y, inv_res, cell;
   uint32_t inmask[16], bdmask[16];
   int corner_ok;
   int rec_ok;             // exp recurrence numerically safe for these parameters
+  int loose_ok;           // beyond-cutoff boundary pairs negligible (eval.cu, LOOSE)
   double res, c_res, k2;  // lattice spacing, c*res, exp(2 c res^2) with c = -1/(2 s^2)
 };
 
@@ -337,6 +355,7 @@ struct tlg_model {
   tlg::CenterGrid grid;
   tlg::LatticeGrid lat;
   bool grid_dirty = true;
+  bool exact_cutoff = false;  // force the per-pair cutoff test (tlg_model_set_exact_cutoff)
 };
 
 // A scan's lever arms, binned once per scan by the world cell they fall in
@@ -361,6 +380,7 @@ GridView grid_view(const tlg_model* m);    // grid.cu
 LatticeView lattice_view(const tlg_model* m);
 void ensure_grid(tlg_model* m);
 int sweep_kind(const tlg_model* m);  // eval.cu
+int prepare_sweep(tlg_model* m);     // sweep_kind + lazily built per-kind tables (grid.cu)
 void sync_weights_to_grid(tlg_model* m);   // after weights change
 
 // blocks / pool (model.cu)

@@ -313,6 +313,18 @@ class TerrainModel:
         w = _vec(w)
         check(_abi.load().tlg_model_set_weights(self.handle, _ptr(w), _mem(w)))
 
+    def set_exact_cutoff(self, exact: bool = True) -> None:
+        """Force the per-pair cutoff test in evaluation (see
+        tlg_model_set_exact_cutoff; the default skips it only where provably
+        negligible)."""
+        check(_abi.load().tlg_model_set_exact_cutoff(self.handle, 1 if exact else 0))
+
+    def sweep(self) -> tuple[int, int]:
+        """(sweep kind, exp recurrence used) — tlg_model_sweep."""
+        kind, rec = C.c_int(), C.c_int()
+        check(_abi.load().tlg_model_sweep(self.handle, C.byref(kind), C.byref(rec)))
+        return kind.value, rec.value
+
     def block_index(self) -> np.ndarray:
         out = np.empty(self.num_centers(), dtype=np.uint32)
         check(_abi.load().tlg_model_get_block_index(self.handle, _ptr(out), _abi.TLG_HOST))

@@ -50,9 +50,15 @@ def _check_predict(k, g, o, q):
     assert_values_close(gy, gyr, gs, what="gy")
 
 
-def test_queries_on_hash_cell_boundaries(gpu_ctx):
+@pytest.mark.parametrize("exact", [False, True])
+def test_queries_on_hash_cell_boundaries(gpu_ctx, exact):
     k, cs, g, o = _lattice_model()
-    assert _sweep(g) == (100, 1)  # compiled paper geometry
+    # compiled paper geometry; by default without the per-pair cutoff test on
+    # boundary pairs (kappa_sigma(rho) = 6.8e-15), exact on request
+    assert _sweep(g) == (200, 1)
+    if exact:
+        g.set_exact_cutoff(True)
+        assert _sweep(g) == (100, 1)
     cell = k.cutoff_radius  # GridIndex2 cell = min(cutoff, 1e6)
     edges = np.arange(-1, int(1.05 / cell) + 2) * cell
     vals = np.concatenate([edges, np.nextafter(edges, -np.inf), np.nextafter(edges, np.inf)])
@@ -147,3 +153,30 @@ def test_streamed_host_batch_equals_device(gpu_ctx):
     rows_d, ne_d = kin.manifold_rows(g, R, t, hd, 0.0, 1.0, 0.05, want=("r", "valid"))
     assert np.array_equal(ne_h.A, ne_d.A) and np.array_equal(ne_h.g, ne_d.g)
     assert ne_h.cost == ne_d.cost and ne_h.valid == ne_d.valid
+
+
+def test_loose_cutoff_gate_off_for_wide_kernel(gpu_ctx):
+    # sigma = 0.1, sigma_eps = 0.04: same cutoff (3 sigma~ = 0.3231, the
+    # compiled paper geometry) but kappa_sigma(rho) = 5e-3 -> the per-pair
+    # cutoff test must stay on
+    k, cs, g, o = _lattice_model(sigma=0.1, sigma_eps=0.04)
+    assert _sweep(g) == (100, 1)
+    q = uniform_xy(orc.Rng(73), 4000, -0.1, 1.15)
+    _check_predict(k, g, o, q)
+
+
+def test_loose_matches_exact_cutoff(gpu_ctx):
+    # the default (no test on boundary pairs) against the exact per-pair test
+    # on the same device: the difference is bounded by the gate (1e-11 of the
+    # window's largest |w|)
+    k, cs, g, o = _lattice_model(seed=3)
+    q = uniform_xy(orc.Rng(74), 20000, -0.1, 1.15)
+    z0, s0, gx0, gy0 = g.predict(q)
+    g.set_exact_cutoff(True)
+    z1, s1, gx1, gy1 = g.predict(q)
+    assert np.array_equal(s0, s1)
+    wmax = np.abs(g.weights()).max()
+    assert np.abs(z0 - z1).max() <= 1e-11 * wmax
+    assert np.abs(gx0 - gx1).max() * k.sigma <= 1e-11 * wmax
+    assert np.abs(gy0 - gy1).max() * k.sigma <= 1e-11 * wmax
+    assert np.abs(z0 - z1).max() > 0.0  # the two paths really differ
