@@ -81,6 +81,15 @@ __device__ __forceinline__ void static_for(F&& f) {
   }
 }
 
+constexpr int ctz32(uint32_t v) {
+  int n = 0;
+  while (v && !(v & 1u)) {
+    v >>= 1;
+    ++n;
+  }
+  return n;
+}
+
 // Boundary pair: the exact reference test d2 = fl(dx^2 + dy^2) <= r2 selects
 // the weight (a select measured faster than predicated inline-PTX FMAs, which
 // block ptxas scheduling: 0.68 vs 0.59 ms)
@@ -208,10 +217,17 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
                 static_assert((im >> l) & 1u, "corner pairs are always inside");
                 cq[k - kLo][l - kLo] = wv * ey[l];
               }
-              if constexpr ((im >> l) & 1u) {
-                S = fma(wv, ey[l], S);
-                T = fma(wv, eyd[l], T);
-              } else if constexpr (((bm >> l) & 1u) && LOOSE) {
+              if constexpr (LOOSE && ((need >> l) & 1u)) {
+                // every window pair unconditional: the chain starts with a
+                // multiply (no zero-initialised accumulator)
+                if constexpr (l == ctz32(need)) {
+                  S = wv * ey[l];
+                  T = wv * eyd[l];
+                } else {
+                  S = fma(wv, ey[l], S);
+                  T = fma(wv, eyd[l], T);
+                }
+              } else if constexpr ((im >> l) & 1u) {
                 S = fma(wv, ey[l], S);
                 T = fma(wv, eyd[l], T);
               } else if constexpr ((bm >> l) & 1u) {
@@ -325,7 +341,13 @@ __device__ __forceinline__ EvalOut eval_any(const GridView& g, const LatticeView
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(128, 3) k_eval(GridView g, LatticeView L,
+#ifndef TLG_EVAL_THREADS
+#define TLG_EVAL_THREADS 256
+#endif
+#ifndef TLG_EVAL_MINB
+#define TLG_EVAL_MINB 2
+#endif
+__global__ void __launch_bounds__(TLG_EVAL_THREADS, TLG_EVAL_MINB) k_eval(GridView g, LatticeView L,
                                                  const double* __restrict__ x,
                                                  const double* __restrict__ y, size_t n,
                                                  double r2, double neg_inv_2s2, double inv_s2,
@@ -438,7 +460,8 @@ void eval_device(tlg_model* m, const double* x, const double* y, size_t n, doubl
     const LatticeView L = lattice_view(m);
     prof_begin(ctx, 1);
     TLG_KIND_DISPATCH(kind,
-                      (k_eval<W_><<<grid_for(ctx, n, 128, 3), 128, 0, ctx->stream>>>(
+                      (k_eval<W_><<<grid_for(ctx, n, TLG_EVAL_THREADS, TLG_EVAL_MINB), TLG_EVAL_THREADS, 0,
+                                 ctx->stream>>>(
                           g, L, x, y, n, m->kc.r2, m->kc.neg_inv_2s2, m->kc.inv_s2, z, sup, gx,
                           gy, err)));
     TLG_LAUNCHED(ctx);
@@ -457,10 +480,10 @@ struct Pose {
 
 constexpr int kNE = 29;  // 21 (A upper) + 6 (g) + cost + valid
 #ifndef TLG_MANIFOLD_THREADS
-#define TLG_MANIFOLD_THREADS 128
+#define TLG_MANIFOLD_THREADS 256
 #endif
 #ifndef TLG_MANIFOLD_MINB
-#define TLG_MANIFOLD_MINB 3
+#define TLG_MANIFOLD_MINB 2
 #endif
 constexpr int kManifoldThreads = TLG_MANIFOLD_THREADS;
 #ifndef TLG_MANIFOLD_CHUNK

@@ -54,15 +54,20 @@ def main():
         # K3 batch predict (height + gradient + supported) on the same points
         # in scan order (binned) and in generation order
         xy = torch.stack([h[0], h[1]], 1).contiguous()
-        for label, q in (("random order", xy),):
-            model.predict(q)
-            lib.tlg_ctx_set_profiling(ctx.handle, 1)
-            for _ in range(a.iters):
+        key = torch.floor(xy[:, 0] / 0.07) * 1e6 + torch.floor(xy[:, 1] / 0.07)
+        binned = xy[torch.argsort(key)].contiguous()
+        for exact in (False, True):
+            model.set_exact_cutoff(exact)
+            for label, q in (("random order", xy), ("binned", binned)):
                 model.predict(q)
-            lib.tlg_ctx_kernel_stats(ctx.handle, 1, C.byref(ms), C.byref(cnt))
-            k = ms.value / cnt.value
-            print(f"k_eval ({label}): {k:.4f} ms  {n / k / 1e6:.3f} Gpts/s  "
-                  f"{41 * n / (k * 1e-3) / 1e9:.1f} GB/s", flush=True)
+                lib.tlg_ctx_set_profiling(ctx.handle, 1)
+                for _ in range(a.iters):
+                    model.predict(q)
+                lib.tlg_ctx_kernel_stats(ctx.handle, 1, C.byref(ms), C.byref(cnt))
+                k = ms.value / cnt.value
+                print(f"k_eval ({label}, sweep {model.sweep()[0]}): {k:.4f} ms  "
+                      f"{n / k / 1e6:.3f} Gpts/s  {41 * n / (k * 1e-3) / 1e9:.1f} GB/s", flush=True)
+        model.set_exact_cutoff(False)
 
 
 if __name__ == "__main__":
