@@ -117,8 +117,13 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
   // the whole window lies in the zero padding (or beyond): no centre within
   // the cutoff -> unsupported, exactly like an empty radius query
   if (i0 < 0 || j0 < 0 || i0 + WIN > L.ni || j0 + WIN > L.nj) return o;
-  const int qx = static_cast<int>(floor(x / L.cell));
-  const int qy = static_cast<int>(floor(y / L.cell));
+  // reference hash cells of the point (a division each): only the exact
+  // path's boundary tests and the rare support scan below need them
+  int qx = 0, qy = 0;
+  if constexpr (!LOOSE) {
+    qx = static_cast<int>(floor(x / L.cell));
+    qy = static_cast<int>(floor(y / L.cell));
+  }
 
   // Row factors. dy^2 is kept exact for the boundary tests; e_y follows the
   // lattice recurrence e(l+1) = e(l) p(l), p(l+1) = p(l) exp(2 c res^2)
@@ -130,8 +135,11 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
   // (fl(min + fl(index * res))) instead of loaded: the L1 data path, not the
   // FP64 pipe, binds this kernel. The cell sweep becomes one index range per
   // axis (cells are monotone in the node index).
-  const int2 rx = __ldg(L.xr + min(max(qx - L.xr_base, 0), L.xr_n - 1));
-  const int2 ry = __ldg(L.yr + min(max(qy - L.yr_base, 0), L.yr_n - 1));
+  int2 rx = make_int2(0, 0), ry = make_int2(0, 0);
+  if constexpr (!LOOSE) {
+    rx = __ldg(L.xr + min(max(qx - L.xr_base, 0), L.xr_n - 1));
+    ry = __ldg(L.yr + min(max(qy - L.yr_base, 0), L.yr_n - 1));
+  }
   auto node_x = [&](int i) {
     return __dadd_rn(L.min_x, __dmul_rn(static_cast<double>(i + L.i_org), L.res));
   };
@@ -269,6 +277,7 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
       o.sy = fma(ex, T, o.sy);
     }
     if constexpr (LOOSE && (k == kLo || k == kLo + 1)) {
+      // corner terms v = |w| ey ex; d >= max(|dx|, |dy|)
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
         const double v = fabs(cq[k - kLo][b]) * ex;
@@ -303,6 +312,10 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
     sup = (__ldg(pc) | __ldg(pc + 1) | __ldg(pc + L.nj) | __ldg(pc + L.nj + 1)) != 0;
   }
   if (!sup) {
+    if constexpr (LOOSE) {
+      qx = static_cast<int>(floor(x / L.cell));
+      qy = static_cast<int>(floor(y / L.cell));
+    }
     for (int k = 0; k < WIN && !sup; ++k) {
       const AxisNode ak = L.ax[i0 + k];
       const double dx = __dsub_rn(ak.c, x);
