@@ -254,6 +254,62 @@ def run_update_c4(torch, steps=5):
     return out
 
 
+def run_batch_fit_c5(torch, device, rank, world, n_total=10_000_000, seed=11):
+    """C5 kernel-matrix assembly + batch ridge, point-sharded (SURVEY §8d C5,
+    §8e): the 316 x 316 lattice (99,856 centres) on every rank, n_total
+    points split over the ranks (strong scaling), banded partial systems
+    summed with one NCCL all-reduce each for H and b, every rank solving.
+    CUDA-event times per phase, max over ranks."""
+    import torch.distributed as dist
+    from paper_2509_26222_b200 import terrain as T
+    side = ROI_C5[1][0]
+    nodes = np.arange(int(round(side / RES)) + 1) * RES
+    gx, gy = np.meshgrid(nodes, nodes, indexing="ij")
+    cs = T.CenterSet(np.stack([gx.ravel(), gy.ravel()], 1), RES, R_A, COUNT, T.Rect(*ROI_C5))
+    kernel = T.KernelParams()
+    kernel.finalize()
+    model = T.TerrainModel(kernel, cs)
+    n, ld, elems = model.batch_system()
+    base, extra = divmod(n_total, world)
+    m = base + (1 if rank < extra else 0)
+    g = torch.Generator(device=f"cuda:{device}").manual_seed(seed + rank)
+    xy = torch.rand((m, 2), generator=g, device=f"cuda:{device}", dtype=torch.float64) * side
+    z = terrain_c5(xy[:, 0], xy[:, 1], torch)
+    H = torch.empty(elems, dtype=torch.float64, device=f"cuda:{device}")
+    b = torch.empty(n, dtype=torch.float64, device=f"cuda:{device}")
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    times = []
+    for it in range(2):  # warm-up (workspaces, NCCL channels), then timed
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev[0].record()
+        model.batch_assemble(xy, z, H, b, add_lambda=(rank == 0))
+        ev[1].record()
+        if world > 1:
+            dist.all_reduce(H)
+            dist.all_reduce(b)
+        ev[2].record()
+        model.batch_solve(H, b)
+        ev[3].record()
+        torch.cuda.synchronize()
+        times = [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]),
+                 ev[0].elapsed_time(ev[3])]
+    if world > 1:
+        t = torch.tensor(times, dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        times = t.tolist()
+    q = torch.rand((20000, 2), generator=g, device=f"cuda:{device}", dtype=torch.float64)
+    q = q * (side - 1.0) + 0.5
+    zq, s, _, _ = model.predict(q, gradient=False)
+    err = (zq - terrain_c5(q[:, 0], q[:, 1], torch)).abs()[s.bool()]
+    return {"centres": n, "points_total": n_total, "points_per_rank": m, "band_ld": ld,
+            "system_gb": elems * 8 / 1e9, "assemble_ms": times[0], "allreduce_ms": times[1],
+            "solve_ms": times[2], "total_ms": times[3], "scaling": "strong",
+            "fit_abs_err_median": float(err.median()),
+            "timing": "CUDA events per phase, max over ranks; solve replicated on every rank"}
+
+
 def match_scene(seed, n):
     """Synthetic LiDAR features: ground plane, two walls, three poles (edge
     features), labelled, in random order."""
@@ -476,6 +532,10 @@ def main():
         "clocks": clk.summary(),
     }
 
+    if not args.no_update:
+        # C5 kernel-matrix assembly + batch ridge, point-sharded over the ranks
+        # (collective: every rank runs it)
+        result["batch_fit_c5"] = run_batch_fit_c5(torch, local, rank, world)
     if rank == 0 and world == 1:
         dfma, dmma = C.c_double(), C.c_double()
         lib.tlg_measure_fp64_peak(ctx.handle, C.byref(dfma), C.byref(dmma))

@@ -299,6 +299,22 @@ tlg_status tlg_fit_batch_ridge(tlg_ctx* ctx, const tlg_kernel_params* kernel,
                                const double* z, size_t m, size_t z_len, tlg_mem mem,
                                tlg_model** out);
 
+/* Point-sharded fit_batch_ridge (the reference's single-process
+ * terrain_model.cpp:269-308 split at its one reduction): every rank creates
+ * the model from the same centres (tlg_model_create), asks for the system
+ * dimensions, assembles the partial system over its point shard into DEVICE
+ * buffers H (elems doubles, lower band storage: element (i, j), 0 <= i - j,
+ * at H[i + j * ld]) and b (n), the caller sums H and b over ranks (NCCL
+ * all-reduce), and every rank solves: weights and info_inv blocks as
+ * tlg_fit_batch_ridge computes them (within the stated tolerance; the
+ * cross-rank summation order differs). add_lambda != 0 on exactly one rank.
+ * An empty shard (m = 0) contributes zeros. */
+tlg_status tlg_batch_ridge_system(tlg_model* model, size_t* n, size_t* ld, size_t* elems);
+tlg_status tlg_batch_ridge_assemble(tlg_model* model, const double* x, const double* y,
+                                    const double* z, size_t m, tlg_mem mem, double* H, size_t ld,
+                                    double* b, int add_lambda);
+tlg_status tlg_batch_ridge_solve(tlg_model* model, double* H, size_t ld, double* b);
+
 /* RBFT v1 snapshot (snapshot.cpp:7-126), byte-identical layout. */
 tlg_status tlg_model_save(tlg_model* model, const char* path);
 tlg_status tlg_model_load(tlg_ctx* ctx, const char* path, tlg_model** out);

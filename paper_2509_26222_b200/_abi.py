@@ -153,6 +153,11 @@ _SIGS = {
     "tlg_scan_manifold_rows": (_ST, [_P, _P, _P, _P, C.c_double, C.c_double, C.c_double, _P, _P,
                                      _P, _P, _I, C.POINTER(NormalEqC)]),
     "tlg_recursive_update": (_ST, [_P, _P, _P, _P, _SZ, _SZ, _I, _I, C.POINTER(UpdateReportC)]),
+    "tlg_batch_ridge_system": (_ST, [_P, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
+                                     C.POINTER(C.c_size_t)]),
+    "tlg_batch_ridge_assemble": (_ST, [_P, _P, _P, _P, C.c_size_t, C.c_int, _P, C.c_size_t, _P,
+                                       C.c_int]),
+    "tlg_batch_ridge_solve": (_ST, [_P, _P, C.c_size_t, _P]),
     "tlg_fit_batch_ridge": (_ST, [_P, C.POINTER(KernelParamsC), C.POINTER(CenterParamsC), _P, _P,
                                   _SZ, _P, _P, _P, _SZ, _SZ, _I, C.POINTER(_P)]),
     "tlg_model_save": (_ST, [_P, C.c_char_p]),

@@ -812,6 +812,48 @@ tlg_status tlg_fit_batch_ridge(tlg_ctx* ctx, const tlg_kernel_params* kernel,
   return TLG_OK;
 }
 
+// ---- point-sharded batch ridge -------------------------------------
+tlg_status tlg_batch_ridge_system(tlg_model* m, size_t* n, size_t* ld, size_t* elems) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(n, "n");
+    check_ptr(ld, "ld");
+    check_ptr(elems, "elems");
+    ensure_grid(m);
+    batch_system_dims(m, n, ld, elems);
+  });
+}
+
+tlg_status tlg_batch_ridge_assemble(tlg_model* m, const double* x, const double* y,
+                                    const double* z, size_t mm, tlg_mem mem, double* H, size_t ld,
+                                    double* b, int add_lambda) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(H, "H");
+    check_ptr(b, "b");
+    tlg_ctx* ctx = m->ctx;
+    const double* dx = nullptr;
+    const double* dy = nullptr;
+    const double* dz = nullptr;
+    if (mm) {  // a shard may be empty
+      dx = as_device(ctx, S_IN_X, x, mm, mem);
+      dy = as_device(ctx, S_IN_Y, y, mm, mem);
+      dz = as_device(ctx, S_IN_Z, z, mm, mem);
+      validate_obs_device(ctx, dx, dy, dz, mm, mm);
+    }
+    batch_assemble_device(m, dx, dy, dz, mm, H, ld, b, add_lambda != 0);
+  });
+}
+
+tlg_status tlg_batch_ridge_solve(tlg_model* m, double* H, size_t ld, double* b) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(H, "H");
+    check_ptr(b, "b");
+    batch_solve_device(m, H, ld, b);
+  });
+}
+
 // ---- RBFT snapshot (snapshot.cpp:7-126) ---------------------------------------
 tlg_status tlg_model_save(tlg_model* m, const char* path) {
   return guard([&] {

@@ -408,5 +408,9 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
                              size_t mm, bool allow_birth, tlg_update_report* rep);
 void batch_fit_device(tlg_model* m, const double* x, const double* y, const double* z,
                       size_t mm);
+void batch_system_dims(tlg_model* m, size_t* n, size_t* ld, size_t* elems);
+void batch_assemble_device(tlg_model* m, const double* x, const double* y, const double* z,
+                           size_t mm, double* H, size_t ld, double* b, bool add_lambda);
+void batch_solve_device(tlg_model* m, double* H, size_t ld, double* b);
 
 }  // namespace tlg

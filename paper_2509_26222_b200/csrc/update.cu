@@ -350,13 +350,15 @@ __global__ void __launch_bounds__(32 * kGramWarps) k_gram_rows_band(
     const uint32_t* __restrict__ trowp, const uint32_t* __restrict__ tobs,
     const double* __restrict__ tval, const uint32_t* __restrict__ rowp,
     const uint32_t* __restrict__ col, const double* __restrict__ val, int n, int band,
-    double* __restrict__ H, int ldh) {
+    int lower_only, double* __restrict__ H, int ldh) {
   extern __shared__ double gsm[];
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-  const int width = 2 * band + 1;
+  // lower_only: row r accumulates only columns >= r (band storage of the
+  // lower triangle; the symmetric half is neither computed nor written)
+  const int width = lower_only ? band + 1 : 2 * band + 1;
   double* acc = gsm + wq * width;
   for (int r = blockIdx.x * kGramWarps + wq; r < n; r += gridDim.x * kGramWarps) {
-    const int lo = r - band;
+    const int lo = lower_only ? r : r - band;
     for (int s = lane; s < width; s += 32) acc[s] = 0.0;
     __syncwarp();
     const uint32_t q_end = trowp[r + 1];
@@ -403,28 +405,30 @@ __global__ void __launch_bounds__(32 * kGramWarps) k_gram_rows_band(
         // observations with more than 32 * kPre entries (other geometries)
         for (uint32_t x = b + 32 * kPre + lane; x < e; x += 32) {
           const int ci = static_cast<int>(col[x]) - lo;
-          acc[ci] = fma(v, val[x], acc[ci]);
+          if (ci >= 0) acc[ci] = fma(v, val[x], acc[ci]);
         }
         __syncwarp();
       }
     }
-    const int c0 = max(lo, 0), c1 = min(r + band, n - 1);
+    const int c0 = max(lo, 0), c1 = min(r + band, n - 1);  // H[c][r]: column r, c >= lo
     for (int cc = c0 + lane; cc <= c1; cc += 32) H[cc + (size_t)r * ldh] += acc[cc - lo];
     __syncwarp();
   }
 }
 
 static void gram_band(tlg_ctx* ctx, const TCsr& t, const Csr& c, int n, int band, double* H,
-                      int ldh) {
-  const size_t smem_band = sizeof(double) * kGramWarps * (2 * static_cast<size_t>(band) + 1);
+                      int ldh, bool lower_only = false) {
+  const size_t width = lower_only ? band + 1 : 2 * static_cast<size_t>(band) + 1;
+  const size_t smem_band = sizeof(double) * kGramWarps * width;
   if (smem_band <= 200 * 1024) {
     if (smem_band > 48 * 1024)
       TLG_CUDA(cudaFuncSetAttribute(k_gram_rows_band, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem_band));
     const unsigned blocks = static_cast<unsigned>((n + kGramWarps - 1) / kGramWarps);
     k_gram_rows_band<<<blocks, 32 * kGramWarps, smem_band, ctx->stream>>>(
-        t.rowp, t.obs, t.val, c.rowp, c.col, c.val, n, band, H, ldh);
+        t.rowp, t.obs, t.val, c.rowp, c.col, c.val, n, band, lower_only ? 1 : 0, H, ldh);
   } else {
+    require(!lower_only, TLG_RUNTIME_ERROR, "banded Gram: band too wide for band storage");
     const size_t smem = static_cast<size_t>(n) * 8;
     if (smem > 48 * 1024)
       TLG_CUDA(cudaFuncSetAttribute(k_gram_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -987,71 +991,125 @@ __global__ void k_scatter_w(const uint32_t* __restrict__ merged, int n, const do
 // order (H is then block-banded: banded Gram, banded 32-wide Cholesky, one
 // banded forward/backward solve); the diagonal-block inverses run batched
 // before the factorisation overwrites H.
-void batch_fit_device(tlg_model* m, const double* x, const double* y, const double* z,
-                      size_t mm) {
-  tlg_ctx* ctx = m->ctx;
-  cudaStream_t s = ctx->stream;
-  ensure_grid(m);
-  const int nc = static_cast<int>(m->hcx.size());
-  if (nc == 0) return;
-  const size_t dense_bytes = static_cast<size_t>(nc) * nc * 8;
-  require(dense_bytes <= (size_t{64} << 30), TLG_OUT_OF_MEMORY,
-          "batch ridge fit: the n x n system exceeds 64 GiB of device memory");
+//
+// H lives in lower band storage: element (i, j), 0 <= i - j <= kd, at
+// H[i + j * ld] with ld = 32 (bwt + 2) (bwt = tile bandwidth) — the dense
+// column-major addressing with a short leading dimension (column j's band
+// starts at j (ld + 1); n (ld + 1) elements in all), so the tile kernels run
+// unchanged; the upper triangles of the diagonal tiles alias only entries
+// beyond the band, which nothing reads. When the band covers the matrix,
+// ld = n (dense). The split into plan / assemble / solve is the
+// point-sharded multi-GPU form: ranks assemble partial systems
+// over their point shards, the caller sums them (NCCL all-reduce), every
+// rank solves.
+struct BatchPlan {
+  std::vector<uint32_t> merged;
+  std::vector<BlockTab> tab;
+  int n = 0, band = 0, ld = 0;
+};
+
+static BatchPlan batch_plan(tlg_model* m) {
+  BatchPlan p;
   std::vector<uint32_t> blocks;
   for (uint32_t bb = 0; bb < m->members.size(); ++bb)
     if (!m->members[bb].empty()) blocks.push_back(bb);
   const auto btile = spatial_block_order(m, blocks);
-  std::vector<uint32_t> merged;
-  std::vector<BlockTab> tab(blocks.size());
+  p.tab.resize(blocks.size());
   for (size_t q = 0; q < blocks.size(); ++q) {
     const uint32_t bb = blocks[q];
-    tab[q].pool_off = m->blk_off[bb];
-    tab[q].ld = m->blk_ld[bb];
-    tab[q].n = static_cast<int>(m->members[bb].size());
-    tab[q].off = static_cast<int>(merged.size());
-    merged.insert(merged.end(), m->members[bb].begin(), m->members[bb].end());
+    p.tab[q].pool_off = m->blk_off[bb];
+    p.tab[q].ld = m->blk_ld[bb];
+    p.tab[q].n = static_cast<int>(m->members[bb].size());
+    p.tab[q].off = static_cast<int>(p.merged.size());
+    p.merged.insert(p.merged.end(), m->members[bb].begin(), m->members[bb].end());
   }
-  const int n = static_cast<int>(merged.size());
-  const int band = btile.empty() ? n : block_band(btile, blocks, tab);
-  uint32_t* hm = static_cast<uint32_t*>(ctx->host_stage(n * sizeof(uint32_t)));
-  std::memcpy(hm, merged.data(), n * sizeof(uint32_t));
-  uint32_t* d_merged = ctx->ws<uint32_t>(S_MERGED, n);
-  TLG_CUDA(cudaMemcpyAsync(d_merged, hm, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  p.n = static_cast<int>(p.merged.size());
+  p.band = btile.empty() ? p.n : block_band(btile, blocks, p.tab);
+  constexpr int kTile = 32;  // potrf_lower's tile for banded systems (dense.cu NB32)
+  const long long bwt = (static_cast<long long>(p.band) + kTile - 1) / kTile;
+  const long long ldb = (bwt + 2) * kTile;
+  if (ldb < p.n) {
+    p.ld = static_cast<int>(ldb);
+  } else {
+    p.ld = p.n;
+    p.band = p.n;
+  }
+  return p;
+}
+
+static size_t batch_elems(const BatchPlan& p) {
+  return static_cast<size_t>(p.n) * (static_cast<size_t>(p.ld) + 1);
+}
+
+void batch_system_dims(tlg_model* m, size_t* n, size_t* ld, size_t* elems) {
+  const BatchPlan p = batch_plan(m);
+  *n = static_cast<size_t>(p.n);
+  *ld = static_cast<size_t>(p.ld);
+  *elems = batch_elems(p);
+}
+
+static uint32_t* upload_merged(tlg_ctx* ctx, const BatchPlan& p) {
+  cudaStream_t s = ctx->stream;
+  uint32_t* hm = static_cast<uint32_t*>(ctx->host_stage(p.n * sizeof(uint32_t)));
+  std::memcpy(hm, p.merged.data(), p.n * sizeof(uint32_t));
+  uint32_t* d_merged = ctx->ws<uint32_t>(S_MERGED, p.n);
+  TLG_CUDA(cudaMemcpyAsync(d_merged, hm, p.n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  return d_merged;
+}
+
+// H (band storage, ld) <- [lambda I +] Mt Mt^T over this shard, b <- Mt z.
+static void batch_assemble(tlg_model* m, const BatchPlan& p, const double* x, const double* y,
+                           const double* z, size_t mm, double* H, int ld, double* b,
+                           bool add_lambda) {
+  tlg_ctx* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  const int n = p.n;
+  const int nc = static_cast<int>(m->hcx.size());
+  TLG_CUDA(cudaMemsetAsync(H, 0, sizeof(double) * batch_elems(p), s));
+  TLG_CUDA(cudaMemsetAsync(b, 0, sizeof(double) * n, s));
+  if (add_lambda) add_diag(ctx, H, n, ld, m->kernel.lambda);
+  if (mm == 0) return;
+  const uint32_t* d_merged = upload_merged(ctx, p);
   int* rowof = ctx->ws<int>(S_ROWOF, nc);
   TLG_CUDA(cudaMemsetAsync(rowof, 0xff, nc * 4, s));
   k_scatter_rowof<<<(n + 255) / 256, 256, 0, s>>>(d_merged, n, rowof);
   TLG_LAUNCHED(ctx);
   const Csr c = build_csr(m, x, y, mm, rowof, m->kc.neg_inv_2st2, m->kc.scale, false, nullptr);
-  double* H = ctx->ws<double>(S_HMAT, static_cast<size_t>(n) * n);
-  TLG_CUDA(cudaMemsetAsync(H, 0, sizeof(double) * n * n, s));
-  add_diag(ctx, H, n, n, m->kernel.lambda);
   const TCsr t = transpose_csr(ctx, c, mm, n);
-  gram_band(ctx, t, c, n, band, H, n);
-  double* bvec = ctx->ws<double>(S_WORK3, n);
-  k_row_dot<<<(n + 255) / 256, 256, 0, s>>>(t.rowp, t.obs, t.val, z, n, bvec);
+  gram_band(ctx, t, c, n, p.band, H, ld, /*lower_only=*/true);
+  k_row_dot<<<(n + 255) / 256, 256, 0, s>>>(t.rowp, t.obs, t.val, z, n, b);
   TLG_LAUNCHED(ctx);
+}
+
+// info_inv_b = (H_bb)^-1 (:298-306) from H before it is factored, then the
+// banded Cholesky solve; w scattered back to centre order.
+static void batch_solve(tlg_model* m, const BatchPlan& p, double* H, int ld, double* b) {
+  tlg_ctx* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  const int n = p.n;
+  const uint32_t* d_merged = upload_merged(ctx, p);
   int* info = ctx->ws<int>(S_FLAGS, 4);
   TLG_CUDA(cudaMemsetAsync(info, 0, 4 * sizeof(int), s));
-  // info_inv_b = (H_bb)^-1 (:298-306), from H before it is factored
   int maxq = 0;
-  for (const auto& tq : tab) maxq = std::max(maxq, tq.n);
+  for (const auto& tq : p.tab) maxq = std::max(maxq, tq.n);
   if (maxq <= kBatchInvMax) {
-    std::vector<InvJob> jobs(tab.size());
-    for (size_t q = 0; q < tab.size(); ++q)
-      jobs[q] = InvJob{H + tab[q].off + static_cast<size_t>(tab[q].off) * n,
-                       m->pool.p + tab[q].pool_off, n, tab[q].ld, tab[q].n, 0};
+    std::vector<InvJob> jobs(p.tab.size());
+    for (size_t q = 0; q < p.tab.size(); ++q)
+      jobs[q] = InvJob{H + p.tab[q].off + static_cast<size_t>(p.tab[q].off) * ld,
+                       m->pool.p + p.tab[q].pool_off, ld, p.tab[q].ld, p.tab[q].n, 0};
     batched_spd_inverse(ctx, jobs, info + 1);
   } else {
-    for (size_t q = 0; q < tab.size(); ++q)
-      if (!spd_inverse(ctx, H + tab[q].off + static_cast<size_t>(tab[q].off) * n, n, tab[q].n,
-                       m->pool.p + tab[q].pool_off, tab[q].ld))
+    require(ld == n, TLG_RUNTIME_ERROR, "batch ridge: blocks too large for band storage");
+    for (size_t q = 0; q < p.tab.size(); ++q)
+      if (!spd_inverse(ctx, H + p.tab[q].off + static_cast<size_t>(p.tab[q].off) * ld, ld,
+                       p.tab[q].n, m->pool.p + p.tab[q].pool_off, p.tab[q].ld))
         throw Error(TLG_RUNTIME_ERROR, "ridge solve failed (block factorisation)");
   }
-  potrf_lower(ctx, H, n, n, info, nullptr, 0, band);
+  potrf_lower(ctx, H, n, ld, info, nullptr, 0, p.band);
   double* mnx = ctx->ws<double>(S_PARTIALS, 2);
-  k_diag_minmax<<<1, 256, 0, s>>>(H, n, n, mnx);
+  k_diag_minmax<<<1, 256, 0, s>>>(H, n, ld, mnx);
   TLG_LAUNCHED(ctx);
-  band_solve(ctx, H, n, n, band, bvec);
+  band_solve(ctx, H, n, ld, p.band, b);
   int h[2] = {0, 0};
   double cond[2];
   TLG_CUDA(cudaMemcpyAsync(h, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1061,10 +1119,43 @@ void batch_fit_device(tlg_model* m, const double* x, const double* y, const doub
   if (h[0])
     throw Error(TLG_RUNTIME_ERROR, "ridge solve failed; condition estimate " +
                                        std::to_string(cond[0] / std::max(cond[1], 1e-300)));
-  k_scatter_w<<<(n + 255) / 256, 256, 0, s>>>(d_merged, n, bvec, m->w.p);
+  k_scatter_w<<<(n + 255) / 256, 256, 0, s>>>(d_merged, n, b, m->w.p);
   TLG_LAUNCHED(ctx);
   sync_weights_to_grid(m);
   TLG_CUDA(cudaStreamSynchronize(s));
+}
+
+void batch_fit_device(tlg_model* m, const double* x, const double* y, const double* z,
+                      size_t mm) {
+  ensure_grid(m);
+  if (m->hcx.empty()) return;
+  const BatchPlan p = batch_plan(m);
+  require(batch_elems(p) * 8 <= (size_t{64} << 30), TLG_OUT_OF_MEMORY,
+          "batch ridge fit: the banded system exceeds 64 GiB of device memory");
+  double* H = m->ctx->ws<double>(S_HMAT, batch_elems(p));
+  double* b = m->ctx->ws<double>(S_WORK3, p.n);
+  batch_assemble(m, p, x, y, z, mm, H, p.ld, b, true);
+  batch_solve(m, p, H, p.ld, b);
+}
+
+void batch_assemble_device(tlg_model* m, const double* x, const double* y, const double* z,
+                           size_t mm, double* H, size_t ld, double* b, bool add_lambda) {
+  ensure_grid(m);
+  if (m->hcx.empty()) return;
+  const BatchPlan p = batch_plan(m);
+  require(ld == static_cast<size_t>(p.ld), TLG_INVALID_ARGUMENT,
+          "batch ridge: ld differs from tlg_batch_ridge_system");
+  batch_assemble(m, p, x, y, z, mm, H, p.ld, b, add_lambda);
+  TLG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+}
+
+void batch_solve_device(tlg_model* m, double* H, size_t ld, double* b) {
+  ensure_grid(m);
+  if (m->hcx.empty()) return;
+  const BatchPlan p = batch_plan(m);
+  require(ld == static_cast<size_t>(p.ld), TLG_INVALID_ARGUMENT,
+          "batch ridge: ld differs from tlg_batch_ridge_system");
+  batch_solve(m, p, H, p.ld, b);
 }
 
 }  // namespace tlg

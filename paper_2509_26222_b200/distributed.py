@@ -1,11 +1,17 @@
-"""Multi-GPU plumbing for the sharded manifold-row sweep.
+"""Multi-GPU plumbing for the point-sharded paths.
 
 One process per GPU (torch.distributed, NCCL over NVLink on the B200 box;
-gloo works for the CPU tests). Points are sharded contiguously, every rank
-evaluates its shard with tlg_manifold_rows / tlg_scan_manifold_rows, and the
-only data-path exchange is the 29-double normal-equation block
-(J^T J upper 21, J^T r 6, cost, valid) summed across ranks — the one real
-reduction of the LM cost evaluation.
+gloo works for the CPU tests). Points are sharded contiguously.
+
+* Manifold rows: every rank evaluates its shard with tlg_manifold_rows /
+  tlg_scan_manifold_rows; the only data-path exchange is the 29-double
+  normal-equation block (J^T J upper 21, J^T r 6, cost, valid) summed across
+  ranks — the one real reduction of the LM cost evaluation.
+* Batch ridge (kernel-matrix assembly): every rank assembles the banded
+  partial system (lambda I on rank 0) + sum m m^T, sum m z over its shard
+  (tlg_batch_ridge_assemble); the band and the rhs are summed across ranks
+  (one all-reduce each) and every rank factors and solves the same system
+  ("replicas" for the solve).
 """
 from __future__ import annotations
 
@@ -50,3 +56,25 @@ def allreduce_normal_eq(ne: NormalEq, group=None, device=None, buf=None) -> Norm
         buf.copy_(v)
     dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
     return unpack(buf.cpu().numpy())
+
+
+def fit_batch_ridge_sharded(model, xy_shard, z_shard, group=None, device=None):
+    """Point-sharded fit_batch_ridge into `model` (created from the same
+    centres on every rank). `model` needs batch_system / batch_assemble /
+    batch_solve (terrain.TerrainModel on the GPU). Returns (n, ld) of the
+    reduced system (band storage, terrain.TerrainModel.batch_system)."""
+    import torch
+    import torch.distributed as dist
+
+    on = dist.is_available() and dist.is_initialized()
+    rank = dist.get_rank(group) if on else 0
+    n, ld, elems = model.batch_system()
+    dev = device or ("cuda" if torch.cuda.is_available() else "cpu")
+    H = torch.empty(elems, dtype=torch.float64, device=dev)
+    b = torch.empty(n, dtype=torch.float64, device=dev)
+    model.batch_assemble(xy_shard, z_shard, H, b, add_lambda=(rank == 0))
+    if on:
+        dist.all_reduce(H, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(b, op=dist.ReduceOp.SUM, group=group)
+    model.batch_solve(H, b)
+    return n, ld

@@ -313,6 +313,41 @@ class TerrainModel:
         w = _vec(w)
         check(_abi.load().tlg_model_set_weights(self.handle, _ptr(w), _mem(w)))
 
+    # ---- point-sharded batch ridge -----------------------------
+    def batch_system(self) -> tuple[int, int, int]:
+        """(n, ld, elems) of the banded batch-ridge system
+        (tlg_batch_ridge_system); H holds `elems` doubles."""
+        n, ld, el = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        check(_abi.load().tlg_batch_ridge_system(self.handle, C.byref(n), C.byref(ld),
+                                                 C.byref(el)))
+        return n.value, ld.value, el.value
+
+    def batch_assemble(self, xy, z, H, b, add_lambda: bool) -> None:
+        """Partial system of this point shard into device tensors H (n * ld)
+        and b (n) (tlg_batch_ridge_assemble)."""
+        if not (_is_dev(H) and _is_dev(b)):
+            raise InvalidArgument("H and b must be CUDA tensors")
+        n, ld, el = self.batch_system()
+        if H.numel() < el or b.numel() < n:
+            raise InvalidArgument("H / b smaller than tlg_batch_ridge_system")
+        m = 0 if xy is None else len(xy)
+        if m:
+            x, y = _xy_of(xy)
+            zz = _vec(z)
+        else:
+            x = y = zz = None
+        check(_abi.load().tlg_batch_ridge_assemble(
+            self.handle, _ptr(x), _ptr(y), _ptr(zz), m, _mem(x) if m else _abi.TLG_HOST,
+            _ptr(H), ld, _ptr(b), 1 if add_lambda else 0))
+
+    def batch_solve(self, H, b) -> None:
+        """Factor and solve the (summed) system, writing weights and info_inv
+        blocks (tlg_batch_ridge_solve)."""
+        n, ld, el = self.batch_system()
+        if H.numel() < el or b.numel() < n:
+            raise InvalidArgument("H / b smaller than tlg_batch_ridge_system")
+        check(_abi.load().tlg_batch_ridge_solve(self.handle, _ptr(H), ld, _ptr(b)))
+
     def set_exact_cutoff(self, exact: bool = True) -> None:
         """Force the per-pair cutoff test in evaluation (see
         tlg_model_set_exact_cutoff; the default skips it only where provably

@@ -1,0 +1,75 @@
+"""Batch ridge in band storage and its point-sharded form:
+tlg_fit_batch_ridge on a field large enough that the banded system is
+stored in band form (ld < n) against the oracle's dense LDLT
+(terrain_model.cpp:269-308), and the assemble / sum / solve split — two
+shards emulated on one GPU, and the world-1 driver — against the single-call
+fit."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from helpers import rel_norm, uniform_xy
+from paper_2509_26222_b200 import distributed as D
+from paper_2509_26222_b200 import terrain as T
+
+pytestmark = pytest.mark.gpu
+
+
+def _field(side=2.2, n_points=6000, seed=41):
+    k = T.KernelParams(sigma=0.04, sigma_eps=0.1)
+    k.finalize()
+    xy = uniform_xy(orc.Rng(seed), n_points, 0.0, side)
+    z = 0.1 * np.sin(4.0 * xy[:, 0]) + 0.05 * xy[:, 1] ** 2
+    roi = T.Rect((0.0, 0.0), (side, side))
+    nodes = orc.supported_mesh_nodes(xy, z, roi, 0.07, 0.12, 3)
+    return k, T.CenterSet(nodes, 0.07, 0.12, 3, roi), T.TerrainObservation(xy, z)
+
+
+def test_batch_fit_band_storage_parity(gpu_ctx):
+    k, cs, obs = _field()
+    g = T.fit_batch_ridge(k, cs, obs)
+    n, ld, el = g.batch_system()
+    assert n == len(cs.centers) and ld < n and el == n * (ld + 1)  # band storage in use
+    o = orc.fit_batch_ridge(k, cs, obs.xy, obs.z)
+    assert rel_norm(g.weights(), o.weights()) < 1e-8
+    for b in range(o.num_blocks()):
+        assert rel_norm(g.block_info_inverse(b), o.block_info_inverse(b)) < 1e-8
+
+
+def test_batch_fit_two_shards_equal_single_call(gpu_ctx):
+    k, cs, obs = _field(seed=42)
+    full = T.fit_batch_ridge(k, cs, obs)
+    g = T.TerrainModel(k, cs)
+    n, ld, el = g.batch_system()
+    cut = len(obs.z) // 3
+    parts = []
+    for r, (b0, b1) in enumerate(((0, cut), (cut, len(obs.z)))):
+        H = torch.empty(el, dtype=torch.float64, device="cuda")
+        b = torch.empty(n, dtype=torch.float64, device="cuda")
+        g.batch_assemble(obs.xy[b0:b1], obs.z[b0:b1], H, b, add_lambda=(r == 0))
+        parts.append((H, b))
+    H = parts[0][0] + parts[1][0]
+    b = parts[0][1] + parts[1][1]
+    g.batch_solve(H, b)
+    assert rel_norm(g.weights(), full.weights()) < 1e-10
+    for q in range(full.num_blocks()):
+        assert rel_norm(g.block_info_inverse(q), full.block_info_inverse(q)) < 1e-10
+
+
+def test_batch_fit_sharded_world1_bit_identical(gpu_ctx):
+    k, cs, obs = _field(side=1.2, n_points=2500, seed=43)
+    full = T.fit_batch_ridge(k, cs, obs)
+    g = T.TerrainModel(k, cs)
+    D.fit_batch_ridge_sharded(g, obs.xy, obs.z)
+    assert np.array_equal(g.weights(), full.weights())
+
+
+def test_batch_assemble_empty_shard(gpu_ctx):
+    k, cs, obs = _field(side=1.2, n_points=2500, seed=44)
+    g = T.TerrainModel(k, cs)
+    n, ld, el = g.batch_system()
+    H = torch.full((el,), 7.0, dtype=torch.float64, device="cuda")
+    b = torch.full((n,), 7.0, dtype=torch.float64, device="cuda")
+    g.batch_assemble(None, None, H, b, add_lambda=False)
+    assert float(H.abs().max()) == 0.0 and float(b.abs().max()) == 0.0

@@ -61,3 +61,74 @@ def test_gloo_allreduce_matches_single_process():
         got = np.array(out[rank])
         np.testing.assert_allclose(got[:28], ne[:28], rtol=1e-12, atol=1e-12 * np.abs(ne).max())
         assert got[28] == ne[28]
+
+
+class _DenseRidge:
+    """CPU stand-in for TerrainModel's batch_system / batch_assemble /
+    batch_solve (dense numpy, Gaussian features of fixed centres): checks the
+    sharded driver's plumbing — lambda added once, partial systems summed,
+    every rank solving the same system."""
+
+    def __init__(self, lam=1e-3):
+        g = np.linspace(0.0, 1.0, 6)
+        self.c = np.array([(a, b) for a in g for b in g])
+        self.lam = lam
+        self.w = None
+
+    def batch_system(self):
+        return len(self.c), len(self.c), len(self.c) ** 2
+
+    def _feat(self, xy):
+        d2 = ((xy[:, None, :] - self.c[None, :, :]) ** 2).sum(-1)
+        return np.exp(-d2 / (2 * 0.2 ** 2))
+
+    def batch_assemble(self, xy, z, H, b, add_lambda):
+        import torch
+        n = len(self.c)
+        M = self._feat(np.asarray(xy)) if xy is not None and len(xy) else np.zeros((0, n))
+        Hn = M.T @ M + (self.lam * np.eye(n) if add_lambda else 0.0)
+        bn = M.T @ (np.asarray(z) if len(M) else np.zeros(0))
+        H.copy_(torch.from_numpy(np.ascontiguousarray(Hn.T).reshape(-1)))
+        b.copy_(torch.from_numpy(bn))
+
+    def batch_solve(self, H, b):
+        n = len(self.c)
+        self.w = np.linalg.solve(H.numpy().reshape(n, n).T, b.numpy())
+
+
+def _ridge_data():
+    rng = np.random.default_rng(3)
+    xy = rng.uniform(0.0, 1.0, (501, 2))
+    return xy, np.sin(3 * xy[:, 0]) * xy[:, 1]
+
+
+def _ridge_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
+    from paper_2509_26222_b200 import distributed as D
+    from test_distributed_gloo import _DenseRidge, _ridge_data
+    xy, z = _ridge_data()
+    b, e = D.shard_range(len(z), rank, world)
+    m = _DenseRidge()
+    D.fit_batch_ridge_sharded(m, xy[b:e], z[b:e], device="cpu")
+    out[rank] = m.w.tolist()
+    dist.destroy_process_group()
+
+
+def test_gloo_sharded_batch_ridge_matches_single_process():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_ridge_worker, args=(2, port, out), nprocs=2, join=True)
+    xy, z = _ridge_data()
+    ref = _DenseRidge()
+    from paper_2509_26222_b200 import distributed as D
+    D.fit_batch_ridge_sharded(ref, xy, z, device="cpu")
+    for rank in range(2):
+        np.testing.assert_allclose(np.array(out[rank]), ref.w, rtol=1e-9, atol=1e-12)
+    assert out[0] == out[1]
