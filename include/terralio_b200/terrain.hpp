@@ -356,6 +356,31 @@ class TerrainModel {
       if (s[i]) out << xs[i] << ',' << ys[i] << ',' << z[i] << '\n';
   }
 
+  // Point-sharded fit_batch_ridge (tlg_batch_ridge_*): H (elems
+  // doubles) and b (n) are DEVICE buffers sized from batch_system().
+  struct BatchSystem {
+    std::size_t n = 0, ld = 0, elems = 0;
+  };
+  BatchSystem batch_system() const {
+    BatchSystem s;
+    gpu::check(tlg_batch_ridge_system(m_.get(), &s.n, &s.ld, &s.elems));
+    return s;
+  }
+  void batch_assemble(const TerrainObservation& shard, double* H, double* b, bool add_lambda) {
+    const detail::Soa o = detail::split(shard.xy);
+    const BatchSystem s = batch_system();
+    gpu::check(tlg_batch_ridge_assemble(m_.get(), o.x.data(), o.y.data(), shard.z.data(),
+                                        shard.xy.size(), TLG_HOST, H, s.ld, b,
+                                        add_lambda ? 1 : 0));
+  }
+  void batch_solve(double* H, double* b) {
+    gpu::check(tlg_batch_ridge_solve(m_.get(), H, batch_system().ld, b));
+  }
+  // kernel_eval's exact per-pair cutoff test everywhere (tlg_model_set_exact_cutoff)
+  void set_exact_cutoff(bool exact) {
+    gpu::check(tlg_model_set_exact_cutoff(m_.get(), exact ? 1 : 0));
+  }
+
   void save(const std::string& path) const { gpu::check(tlg_model_save(m_.get(), path.c_str())); }
   static TerrainModel load(const std::string& path) {
     tlg_model* m = nullptr;
@@ -384,6 +409,20 @@ inline TerrainModel fit_batch_ridge(const KernelParams& params, const CenterSet&
                                  c.x.size(), o.x.data(), o.y.data(), obs.z.data(), obs.xy.size(),
                                  obs.z.size(), TLG_HOST, &m));
   return TerrainModel(m);
+}
+
+// Point-sharded fit_batch_ridge: every rank holds `model` built from the
+// same centres and its shard of the observations; allreduce_sum(ptr, count)
+// sums a device buffer over the ranks in place (e.g. ncclAllReduce + a
+// stream synchronize). Exactly one rank passes root = true (adds lambda I).
+template <class AllReduce>
+void fit_batch_ridge_sharded(TerrainModel& model, const TerrainObservation& shard, bool root,
+                             double* H, double* b, AllReduce&& allreduce_sum) {
+  const TerrainModel::BatchSystem s = model.batch_system();
+  model.batch_assemble(shard, H, b, root);
+  allreduce_sum(H, s.elems);
+  allreduce_sum(b, s.n);
+  model.batch_solve(H, b);
 }
 
 }  // namespace terrain

@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <random>
 
+#include <cuda_runtime.h>
+
 #include "terralio_b200/terrain.hpp"
 
 using namespace terralio;
@@ -86,6 +88,40 @@ int main() {
     den += wb[i] * wb[i];
   }
   CHECK(std::sqrt(num / den) < 1e-8);
+
+  // point-sharded batch ridge: two shards summed (host-side here) == one call
+  {
+    TerrainModel sh(kk, set);
+    const TerrainModel::BatchSystem bs = sh.batch_system();
+    double *H0, *H1, *b0, *b1;
+    CHECK(cudaMalloc(&H0, bs.elems * 8) == cudaSuccess && cudaMalloc(&H1, bs.elems * 8) == cudaSuccess);
+    CHECK(cudaMalloc(&b0, bs.n * 8) == cudaSuccess && cudaMalloc(&b1, bs.n * 8) == cudaSuccess);
+    TerrainObservation s0, s1;
+    s0.xy.assign(obs.xy.begin(), obs.xy.begin() + 150);
+    s0.z.assign(obs.z.begin(), obs.z.begin() + 150);
+    s1.xy.assign(obs.xy.begin() + 150, obs.xy.end());
+    s1.z.assign(obs.z.begin() + 150, obs.z.end());
+    sh.batch_assemble(s1, H1, b1, false);
+    auto add_other = [&](double* dst, std::size_t count) {  // a two-rank "all-reduce"
+      std::vector<double> a(count), c(count);
+      cudaMemcpy(a.data(), dst, count * 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(c.data(), dst == H0 ? H1 : b1, count * 8, cudaMemcpyDeviceToHost);
+      for (std::size_t i = 0; i < count; ++i) a[i] += c[i];
+      cudaMemcpy(dst, a.data(), count * 8, cudaMemcpyHostToDevice);
+    };
+    fit_batch_ridge_sharded(sh, s0, true, H0, b0, add_other);
+    const auto ws = sh.weights();
+    double n2 = 0.0, d2 = 0.0;
+    for (std::size_t i = 0; i < ws.size(); ++i) {
+      n2 += (ws[i] - wb[i]) * (ws[i] - wb[i]);
+      d2 += wb[i] * wb[i];
+    }
+    CHECK(std::sqrt(n2 / d2) < 1e-10);
+    cudaFree(H0);
+    cudaFree(H1);
+    cudaFree(b0);
+    cudaFree(b1);
+  }
 
   // predict_height / unsupported (test_terrain_model.cpp:79-100)
   const HeightQuery q = batch.predict_height({1.0, 1.0});

@@ -13,9 +13,12 @@ OUT = ROOT / "build" / "test_shim"
 
 def _build():
     OUT.parent.mkdir(parents=True, exist_ok=True)
+    cuda = Path("/usr/local/cuda")
     cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-I", str(ROOT / "include"),
+           "-I", str(cuda / "include"),
            str(ROOT / "tests" / "cpp" / "test_shim.cpp"), "-L", str(LIBDIR), "-lterralio_gpu",
-           f"-Wl,-rpath,{LIBDIR}", "-o", str(OUT)]
+           f"-Wl,-rpath,{LIBDIR}", "-L", str(cuda / "lib64"), "-lcudart",
+           f"-Wl,-rpath,{cuda / 'lib64'}", "-o", str(OUT)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     return OUT
