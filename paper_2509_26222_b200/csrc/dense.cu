@@ -797,60 +797,95 @@ __global__ void __launch_bounds__(128) k_potrf_coop32(double* __restrict__ A, in
 }
 
 // Banded Cholesky solve L L^T x = b with the 32-wide factor (L in A, the
-// diagonal-tile inverses in linv), one cooperative launch, right-looking and
-// one grid barrier per tile step. Forward: every CTA forms y_k = Linv_kk b_k
-// (32 x 32, redundantly), then subtracts L_ik y_k from the band rows below
-// (thread per row, coalesced along the row index). Backward: x_k =
-// Linv_kk^T z_k, then z_c -= sum_r L_rc x_r for the band columns to the left
-// (thread per column, contiguous 32-row reads).
+// diagonal-tile inverses in linv), one cooperative launch, right-looking
+// forward and left-looking backward, one grid barrier per tile step.
+// Forward: every CTA forms y_k = Linv_kk b_k (32 x 32, redundantly), then
+// subtracts L_ik y_k from the band rows below (thread per row, coalesced
+// along the row index). Backward: every CTA forms x_k = Linv_kk^T z_k from
+// the band columns' updates of earlier steps, then z_c -= L_kc^T x_k for the
+// band columns to the left — one warp per column, lanes over the 32 rows
+// (coalesced 256-byte column segments, shuffle reduction). x goes to its
+// own array, so no barrier guards a read-before-overwrite.
 __global__ void __launch_bounds__(128) k_band_solve_coop(const double* __restrict__ L, int n,
                                                          int ld, int bwt,
                                                          const double* __restrict__ linv,
                                                          double* __restrict__ b,
-                                                         double* __restrict__ y) {
+                                                         double* __restrict__ y,
+                                                         double* __restrict__ x) {
   __shared__ double sk[NB32], sv[NB32];
+  __shared__ double sl[NB32 * (NB32 + 1)];  // Linv_kk, padded rows
   cg::grid_group grid = cg::this_grid();
   const int nt = (n + NB32 - 1) / NB32;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const int gw = tid >> 5, nw = nth >> 5;
+  // Linv_kk -> shared memory in one round trip (all loads in flight)
+  // (lower triangle of the kb x kb tile; zero elsewhere)
+  auto stage_linv = [&](int k, int kb) {
+    const double* Li = linv + (size_t)k * NB32 * NB32;
+#pragma unroll
+    for (int e = threadIdx.x; e < NB32 * NB32; e += 128) {
+      const int i = e & 31, c = e >> 5;
+      sl[i * (NB32 + 1) + c] = (c <= i && i < kb) ? Li[e] : 0.0;
+    }
+  };
   for (int k = 0; k < nt; ++k) {  // forward: y = L^-1 b
     const int k0 = k * NB32, kb = min(NB32, n - k0);
+    stage_linv(k, kb);
     if (threadIdx.x < NB32) sk[threadIdx.x] = threadIdx.x < kb ? b[k0 + threadIdx.x] : 0.0;
     __syncthreads();
-    if (threadIdx.x < kb) {
-      const double* Li = linv + (size_t)k * NB32 * NB32;
+    if (threadIdx.x < NB32) {
+      // sl[i][c] = Linv(i, c), lower triangular (zero above; beyond kb unused)
       double v = 0.0;
-      for (int c = 0; c <= (int)threadIdx.x; ++c) v = fma(Li[threadIdx.x + c * NB32], sk[c], v);
+#pragma unroll
+      for (int c = 0; c < NB32; ++c) v = fma(sl[threadIdx.x * (NB32 + 1) + c], sk[c], v);
       sv[threadIdx.x] = v;
-      if (blockIdx.x == 0) y[k0 + threadIdx.x] = v;
+      if (blockIdx.x == 0 && threadIdx.x < kb) y[k0 + threadIdx.x] = v;
     }
     __syncthreads();
     const int r0 = k0 + kb, r1 = min(n, (min(nt - 1, k + bwt) + 1) * NB32);
     for (int r = r0 + tid; r < r1; r += nth) {
+      double lv[NB32];
+#pragma unroll
+      for (int c = 0; c < NB32; ++c) lv[c] = c < kb ? L[r + (size_t)(k0 + c) * ld] : 0.0;
       double acc = 0.0;
-      for (int c = 0; c < kb; ++c) acc = fma(L[r + (size_t)(k0 + c) * ld], sv[c], acc);
+#pragma unroll
+      for (int c = 0; c < NB32; ++c) acc = fma(lv[c], sv[c], acc);
       b[r] -= acc;
     }
     grid.sync();
   }
-  for (int k = nt - 1; k >= 0; --k) {  // backward: x = L^-T y (in y)
+  for (int k = nt - 1; k >= 0; --k) {  // backward: x = L^-T y
     const int k0 = k * NB32, kb = min(NB32, n - k0);
+    stage_linv(k, kb);
     if (threadIdx.x < NB32) sk[threadIdx.x] = threadIdx.x < kb ? y[k0 + threadIdx.x] : 0.0;
     __syncthreads();
-    if (threadIdx.x < kb) {
-      const double* Li = linv + (size_t)k * NB32 * NB32;
+    if (threadIdx.x < NB32) {
+      // x_i = sum_r Linv(r, i) z_r
       double v = 0.0;
-      for (int r = threadIdx.x; r < kb; ++r) v = fma(Li[r + threadIdx.x * NB32], sk[r], v);
+#pragma unroll
+      for (int r = 0; r < NB32; ++r) v = fma(sl[r * (NB32 + 1) + threadIdx.x], sk[r], v);
       sv[threadIdx.x] = v;
+      if (blockIdx.x == 0 && threadIdx.x < kb) x[k0 + threadIdx.x] = v;
     }
     __syncthreads();
-    grid.sync();  // every CTA has read y_k before block 0 overwrites it
-    if (blockIdx.x == 0 && threadIdx.x < kb) y[k0 + threadIdx.x] = sv[threadIdx.x];
     const int c0 = max(0, k - bwt) * NB32;
-    for (int c = c0 + tid; c < k0; c += nth) {
-      const double* col = L + (size_t)c * ld + k0;
-      double acc = 0.0;
-      for (int r = 0; r < kb; ++r) acc = fma(col[r], sv[r], acc);
-      y[c] -= acc;
+    const double xv = lane < kb ? sv[lane] : 0.0;
+    constexpr int U = 8;  // columns per warp with their loads in flight together
+    for (int cb = c0 + gw; cb < k0; cb += nw * U) {
+      double p[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = cb + u * nw;
+        p[u] = (c < k0 && lane < kb) ? L[(size_t)c * ld + k0 + lane] * xv : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) p[u] += __shfl_xor_sync(0xffffffffu, p[u], o);
+        const int c = cb + u * nw;
+        if (lane == 0 && c < k0) y[c] -= p[u];
+      }
     }
     grid.sync();
   }
@@ -863,15 +898,21 @@ void band_solve(tlg_ctx* ctx, const double* L, int n, int ld, int band, double* 
   int bwt = std::min(nt - 1, (std::max(band, 0) + NB32 - 1) / NB32);
   const double* linv = ctx->ws<double>(S_LINV, 1);
   double* y = ctx->ws<double>(S_XINV2, n);
+  double* x = ctx->ws<double>(S_BSOLVE, n);
   int per_sm = 0;
   TLG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_band_solve_coop, 128, 0));
+  // forward: a thread per band row; backward: a warp per band column
   const int rows = (bwt + 1) * NB32;
-  const int grid = std::max(1, std::min((rows + 127) / 128, ctx->num_sms * std::max(per_sm, 1)));
-  void* args[] = {&L, &n, &ld, &bwt, &linv, &b, &y};
+  const int want = std::max((rows + 127) / 128, (bwt * NB32 + 3) / 4);
+  // at most one CTA per SM: the per-step grid barrier dominates, and its
+  // cost grows with the CTA count
+  const int grid = std::max(1, std::min(std::min(want, ctx->num_sms),
+                                        ctx->num_sms * std::max(per_sm, 1)));
+  void* args[] = {&L, &n, &ld, &bwt, &linv, &b, &y, &x};
   TLG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_band_solve_coop), dim3(grid),
                                        dim3(128), args, 0, ctx->stream));
   ++ctx->launches;
-  TLG_CUDA(cudaMemcpyAsync(b, y, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  TLG_CUDA(cudaMemcpyAsync(b, x, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, ctx->stream));
 }
 
 // B <- L^-1 B (trans = 0) or L^-T B (trans = 1), one CTA per 64-column slab

@@ -104,7 +104,7 @@ enum Slot : int {
   S_KEYS, S_KEYS2, S_VALS, S_VALS2, S_NODES_X, S_NODES_Y, S_NODE_FLAG, S_NODE_IDX,
   S_COUNT, S_ACTIVE, S_BLOCKFLAG, S_ROWOF, S_MERGED, S_ROWPTR, S_COLIDX, S_MTVAL,
   S_KMAT, S_SMAT, S_RESID, S_U, S_YMAT, S_HMAT, S_WORK1, S_WORK2, S_WORK3, S_BLKTAB,
-  S_MOMENT_ROW, S_TROWP, S_TKEYS, S_LINV, S_XINV, S_XINV2, S_SOLVE,
+  S_MOMENT_ROW, S_TROWP, S_TKEYS, S_LINV, S_XINV, S_XINV2, S_SOLVE, S_BSOLVE,
   S_NUM_SLOTS
 };
 

@@ -1087,6 +1087,7 @@ static void batch_solve(tlg_model* m, const BatchPlan& p, double* H, int ld, dou
   tlg_ctx* ctx = m->ctx;
   cudaStream_t s = ctx->stream;
   const int n = p.n;
+  StageTrace tr(ctx);
   const uint32_t* d_merged = upload_merged(ctx, p);
   int* info = ctx->ws<int>(S_FLAGS, 4);
   TLG_CUDA(cudaMemsetAsync(info, 0, 4 * sizeof(int), s));
@@ -1105,11 +1106,14 @@ static void batch_solve(tlg_model* m, const BatchPlan& p, double* H, int ld, dou
                        p.tab[q].n, m->pool.p + p.tab[q].pool_off, p.tab[q].ld))
         throw Error(TLG_RUNTIME_ERROR, "ridge solve failed (block factorisation)");
   }
+  tr.mark("block_inv");
   potrf_lower(ctx, H, n, ld, info, nullptr, 0, p.band);
+  tr.mark("potrf");
   double* mnx = ctx->ws<double>(S_PARTIALS, 2);
   k_diag_minmax<<<1, 256, 0, s>>>(H, n, ld, mnx);
   TLG_LAUNCHED(ctx);
   band_solve(ctx, H, n, ld, p.band, b);
+  tr.mark("band_solve");
   int h[2] = {0, 0};
   double cond[2];
   TLG_CUDA(cudaMemcpyAsync(h, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
