@@ -193,11 +193,6 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
   }
   auto column = [&](auto KC) {
     constexpr int k = decltype(KC)::value;
-#ifdef TLG_COL_FENCE
-    // compiler-only barrier: keeps the window loads of later columns from
-    // being hoisted here (they would need ~2 registers each and spill)
-    if constexpr (k % TLG_COL_FENCE == 0) asm volatile("" ::: "memory");
-#endif
     const double dx = k == 0 ? dx_first
                              : (LOOSE ? fma(static_cast<double>(k), L.res, dx_first)
                                       : __dsub_rn(node_x(i0 + k), x));
@@ -297,11 +292,7 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
     // otherwise (weights near zero around the point, support fringe)
     // evaluate with the exact test.
     const double e = L.loose_k * __ldg(L.wmax + static_cast<size_t>(ib) * L.nj + jb);
-#ifdef TLG_LOOSE_NOFB
-    if (!(e <= 1e-10 * s4 && e * L.loose_d <= 1e-10 * t4) && L.loose_k < 0.0)
-#else
     if (!(e <= 1e-10 * s4 && e * L.loose_d <= 1e-10 * t4))
-#endif
       return eval_lattice<WIN, G, false>(L, x, y, r2, neg_inv_2b2);
   }
   // supported: some *present* centre passes the reference test. The cell's
