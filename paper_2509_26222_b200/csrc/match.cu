@@ -148,40 +148,83 @@ __global__ void k_cell_count(const uint32_t* __restrict__ keys, size_t n, int* _
 // shell r is at least (r - 2) cells away even allowing one cell of index
 // rounding, so the search stops once ((r - 2) c)^2 exceeds the current k-th
 // distance (or the gate) — the result equals the exhaustive search's.
-template <int K>
-__device__ int knn_grid(const GridView3& g, double qx, double qy, double qz, double gate2,
-                        uint32_t (&ids)[K], double (&d2s)[K]) {
-  int m = 0;
+// Run by a group of G lanes (one query per group): each lane scans a
+// stride-G share of every visited cell into its own top-K, and after each
+// shell the group merges the lanes' lists (K rounds of a lexicographic
+// (d2, id) minimum over the group; a point reaches the lists of one lane only,
+// but after a merge every lane continues from the merged list, so equal
+// entries are advanced together). The stopping test runs on the merged list
+// before each shell: the result is the sequential search's.
+template <int K, int G>
+__device__ int knn_group(const GridView3& g, double qx, double qy, double qz, double gate2,
+                         int glane, unsigned gmask, uint32_t (&ids)[K], double (&d2s)[K]) {
+  int m = 0;  // entries in this lane's list
   int c[3];
   const double q[3] = {qx, qy, qz};
   for (int a = 0; a < 3; ++a) c[a] = static_cast<int>(floor((q[a] - g.org[a]) / g.cell));
+  auto insert = [&](uint32_t id, double d2) {
+    if (!(d2 <= gate2)) return;
+    if (m == K && !(d2 < d2s[K - 1] || (d2 == d2s[K - 1] && id < ids[K - 1]))) return;
+    int j = m < K ? m++ : K - 1;
+    while (j > 0 && (d2s[j - 1] > d2 || (d2s[j - 1] == d2 && ids[j - 1] > id))) {
+      d2s[j] = d2s[j - 1];
+      ids[j] = ids[j - 1];
+      --j;
+    }
+    d2s[j] = d2;
+    ids[j] = id;
+  };
   auto visit = [&](int cx, int cy, int cz) {
     if (cx < 0 || cx >= g.dim[0] || cy < 0 || cy >= g.dim[1] || cz < 0 || cz >= g.dim[2]) return;
     const int cell = (cz * g.dim[1] + cy) * g.dim[0] + cx;
-    for (int s = g.start[cell]; s < g.start[cell + 1]; ++s) {
+    for (int s = g.start[cell] + glane; s < g.start[cell + 1]; s += G) {
       const uint32_t id = g.ids[s];
       const double ex = g.pts[3 * id] - qx, ey = g.pts[3 * id + 1] - qy, ez = g.pts[3 * id + 2] - qz;
-      const double d2 = (ex * ex + ey * ey) + ez * ez;
-      if (!(d2 <= gate2)) continue;
-      if (m == K && !(d2 < d2s[K - 1] || (d2 == d2s[K - 1] && id < ids[K - 1]))) continue;
-      int j = m < K ? m++ : K - 1;
-      while (j > 0 && (d2s[j - 1] > d2 || (d2s[j - 1] == d2 && ids[j - 1] > id))) {
-        d2s[j] = d2s[j - 1];
-        ids[j] = ids[j - 1];
-        --j;
-      }
-      d2s[j] = d2;
-      ids[j] = id;
+      insert(id, (ex * ex + ey * ey) + ez * ez);
     }
   };
+  auto merge = [&]() {
+    uint32_t mi[K];
+    double md[K];
+    int p = 0, mm = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double cd = INFINITY;
+      uint32_t ci = 0xffffffffu;
+#pragma unroll
+      for (int t = 0; t < K; ++t)
+        if (t == p && p < m) {
+          cd = d2s[t];
+          ci = ids[t];
+        }
+      double bd = cd;
+      uint32_t bi = ci;
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) {
+        const double od = __shfl_xor_sync(gmask, bd, o, G);
+        const uint32_t oi = __shfl_xor_sync(gmask, bi, o, G);
+        if (od < bd || (od == bd && oi < bi)) {
+          bd = od;
+          bi = oi;
+        }
+      }
+      md[k] = bd;
+      mi[k] = bi;
+      if (bi != 0xffffffffu) mm = k + 1;
+      if (ci == bi && cd == bd && p < m) ++p;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      d2s[k] = md[k];
+      ids[k] = mi[k];
+    }
+    m = mm;
+  };
   const int rmax = max(max(g.dim[0], g.dim[1]), g.dim[2]);
-  // binning rounds floor((p - org) / cell) within an ulp or so: eps keeps the
-  // bound conservative
   const double eps = 1e-9 * (fabs(g.org[0]) + fabs(g.org[1]) + fabs(g.org[2]) + g.cell * rmax);
   for (int r = 0; r <= rmax; ++r) {
     if (r >= 1) {
-      // every unvisited point lies in a cell r or more away on some axis:
-      // lower bound on its distance from the actual cell faces
+      merge();
       double lb = INFINITY;
       for (int a = 0; a < 3; ++a) {
         const double hi_face = g.org[a] + (c[a] + r) * g.cell - q[a];
@@ -205,6 +248,7 @@ __device__ int knn_grid(const GridView3& g, double qx, double qy, double qz, dou
           if (r > 0) visit(c[0] + r, c[1] + dy, c[2] + dz);
         }
       }
+    if (r == rmax) merge();
   }
   return m;
 }
@@ -304,6 +348,11 @@ __global__ void k_ground_cells(const double* __restrict__ px, const double* __re
   keys[i] = key;
 }
 
+#ifndef TLG_QG
+#define TLG_QG 8
+#endif
+constexpr int kQG = TLG_QG;  // lanes per query in k_correspond
+
 __global__ void k_correspond(const double* __restrict__ px, const double* __restrict__ py,
                              const double* __restrict__ pz, const uint8_t* __restrict__ kind,
                              size_t n, Pose P, MatchCfg cfg, GridView3 ge, GridView3 gp,
@@ -315,10 +364,15 @@ __global__ void k_correspond(const double* __restrict__ px, const double* __rest
                              double* __restrict__ par, double* __restrict__ weight,
                              int* __restrict__ label, double* __restrict__ dist,
                              double* __restrict__ fitq) {
-  const size_t jj = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  // one query per group of kQG lanes (knn_group); the fit runs on the
+  // group's first lane. Every exit before the search is group-uniform.
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const size_t jj = t / kQG;
+  const int glane = static_cast<int>(t % kQG);
+  const unsigned gmask = ((1u << kQG) - 1u) << (threadIdx.x & 31 & ~(kQG - 1));
   if (jj >= n) return;
   const size_t i = order[jj];
-  pass[i] = 0;
+  if (glane == 0) pass[i] = 0;
   const uint8_t kd = kind[i];
   if (kd == 2 && (!radius_ok[i] || (use_gfirst && !gfirst[i]))) return;
   double pw[3];
@@ -334,12 +388,12 @@ __global__ void k_correspond(const double* __restrict__ px, const double* __rest
   if (edge) {
     uint32_t i5[5];
     double d5[5];
-    m = knn_grid<5>(g, pw[0], pw[1], pw[2], gate2, i5, d5);
-    if (m < 5) return;
+    m = knn_group<5, kQG>(g, pw[0], pw[1], pw[2], gate2, glane, gmask, i5, d5);
+    if (m < 5 || glane != 0) return;
     for (int a = 0; a < 5; ++a) ids[a] = i5[a];
   } else {
-    m = knn_grid<8>(g, pw[0], pw[1], pw[2], gate2, ids, d2s);
-    if (m < 8) return;
+    m = knn_group<8, kQG>(g, pw[0], pw[1], pw[2], gate2, glane, gmask, ids, d2s);
+    if (m < 8 || glane != 0) return;
   }
   double cen[3] = {0.0, 0.0, 0.0};
   for (int a = 0; a < m; ++a)
@@ -413,7 +467,7 @@ __global__ void k_correspond(const double* __restrict__ px, const double* __rest
 
 __global__ void k_query_keys(const double* __restrict__ px, const double* __restrict__ py,
                              const double* __restrict__ pz, const uint8_t* __restrict__ kind,
-                             size_t n, Pose P, GridView3 ge, GridView3 gp,
+                             size_t n, Pose P, GridView3 ge, GridView3 gp, int cell_bits,
                              uint64_t* __restrict__ keys, uint32_t* __restrict__ idx) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -428,7 +482,7 @@ __global__ void k_query_keys(const double* __restrict__ px, const double* __rest
       c[a] = min(max(static_cast<int>(floor((q[a] - g.org[a]) / g.cell)), 0), g.dim[a] - 1);
     cell = static_cast<uint64_t>((c[2] * g.dim[1] + c[1]) * g.dim[0] + c[0]);
   }
-  keys[i] = (static_cast<uint64_t>(edge ? 0 : 1) << 40) | cell;
+  keys[i] = (static_cast<uint64_t>(edge ? 0 : 1) << cell_bits) | cell;
   idx[i] = static_cast<uint32_t>(i);
 }
 
@@ -823,14 +877,24 @@ size_t build_correspondences_device(tlg_map* m, const double* px, const double* 
   uint32_t* qi = ctx->ws<uint32_t>(S_VALS, n);
   uint64_t* qk2 = ctx->ws<uint64_t>(S_KEYS2, n);
   uint32_t* order = ctx->ws<uint32_t>(S_VALS2, n);
-  k_query_keys<<<nb, 128, 0, s>>>(px, py, pz, kind, n, P, grid_view3(m, 0), grid_view3(m, 1), qk,
-                                  qi);
+  // key = kind bit above the cell index: sort only the bits in use
+  int cell_bits = 1;
+  for (int cls = 0; cls < 2; ++cls) {
+    const GridView3 gv = grid_view3(m, cls);
+    const uint64_t nc = static_cast<uint64_t>(std::max(gv.dim[0], 0)) * std::max(gv.dim[1], 0) *
+                        std::max(gv.dim[2], 0);
+    while (cell_bits < 62 && (1ull << cell_bits) < nc) ++cell_bits;
+  }
+  k_query_keys<<<nb, 128, 0, s>>>(px, py, pz, kind, n, P, grid_view3(m, 0), grid_view3(m, 1),
+                                  cell_bits, qk, qi);
   TLG_LAUNCHED(ctx);
   size_t tmpq = 0;
-  TLG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmpq, qk, qk2, qi, order, n, 0, 64, s));
+  TLG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmpq, qk, qk2, qi, order, n, 0, cell_bits + 1,
+                                           s));
   void* dq = ctx->ws<char>(S_CUB, tmpq);
-  TLG_CUDA(cub::DeviceRadixSort::SortPairs(dq, tmpq, qk, qk2, qi, order, n, 0, 64, s));
-  k_correspond<<<nb, 128, 0, s>>>(px, py, pz, kind, n, P, cfg, grid_view3(m, 0), grid_view3(m, 1),
+  TLG_CUDA(cub::DeviceRadixSort::SortPairs(dq, tmpq, qk, qk2, qi, order, n, 0, cell_bits + 1, s));
+  k_correspond<<<static_cast<unsigned>((n * kQG + 127) / 128), 128, 0, s>>>(
+      px, py, pz, kind, n, P, cfg, grid_view3(m, 0), grid_view3(m, 1),
                                   m->lab[0].p, m->lab[1].p, m->n[0], m->n[1], rok, gfirst,
                                   use_gfirst, order, pass, okind, par, wgt, lab, dist, fq);
   TLG_LAUNCHED(ctx);
