@@ -498,15 +498,26 @@ def main():
 
     peaks, peak_kind = load_peaks()
     achieved = BYTES_PER_POINT * n / (k_ms * 1e-3) / 1e9
-    traffic = None
+    traffic, ncu_info = None, {}
     tf = ROOT / "profiles" / "kernel_traffic.json"
     if tf.exists():
         try:
             d = json.loads(tf.read_text())
             if d.get("k_manifold", {}).get("points") == n:
                 traffic = d["k_manifold"]["dram_bytes_per_launch"]
+                ncu_info = {"fp64_pipe_pct_ncu": d["k_manifold"].get("fp64_pipe_pct_active"),
+                            "issue_active_pct_ncu": d["k_manifold"].get("issue_active_pct"),
+                            "l1_lsu_wavefronts_pct_ncu":
+                                d["k_manifold"].get("l1_lsu_wavefronts_pct_elapsed")}
         except Exception:
             traffic = None
+    # point-centre pairs within the cutoff (the reference's centers_near), on
+    # a 200k-point sample of the workload: pairs/s beside points/s
+    ns = min(n, 200_000)
+    hs = np.stack([hh_.cpu().numpy() for hh_ in (h[0][:ns], h[1][:ns], h[2][:ns])], 1)
+    xw = hs @ np.asarray(R).T + np.asarray(tv)
+    rp, _, _ = model.moment_features(np.ascontiguousarray(xw[:, :2]))
+    pairs_per_point = float(rp[-1]) / ns
 
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -524,7 +535,11 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                      "kernel": "k_manifold", "kernel_ms": k_ms,
-                     "bytes_per_point": BYTES_PER_POINT, "peak_source": peak_kind},
+                     "bytes_per_point": BYTES_PER_POINT, "peak_source": peak_kind,
+                     "pairs_per_point": pairs_per_point,
+                     "pairs_per_s": world * n / (k_ms * 1e-3) * pairs_per_point,
+                     "binding": "FP64 issue latency and L1 window gathers (ncu), not HBM",
+                     **ncu_info},
         "e2e": {"value": world * n / (e2e_ms * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 29 * 8 + 4,
                 "ms_per_step": e2e_ms, "api": "tlg_manifold_rows, pinned host lever arms in, "
