@@ -180,3 +180,18 @@ def test_loose_matches_exact_cutoff(gpu_ctx):
     assert np.abs(gx0 - gx1).max() * k.sigma <= 1e-11 * wmax
     assert np.abs(gy0 - gy1).max() * k.sigma <= 1e-11 * wmax
     assert np.abs(z0 - z1).max() > 0.0  # the two paths really differ
+
+
+def test_loose_guard_follows_weight_changes(gpu_ctx):
+    # the per-cell max-|w| table behind the loose path's guard is rebuilt
+    # lazily after weight changes: evaluate, then make a few weights 1e6x
+    # larger (an error bound computed from the stale table would be far too
+    # small near them) and compare against the oracle again
+    k, cs, g, o = _lattice_model(seed=5)
+    q = uniform_xy(orc.Rng(75), 6000, -0.05, 1.1)
+    _check_predict(k, g, o, q)
+    w = g.weights()
+    w[::37] *= 1e6
+    g.set_weights(w)
+    o.set_weights(w)
+    _check_predict(k, g, o, q)
