@@ -374,40 +374,50 @@ __global__ void __launch_bounds__(32 * kGramWarps) k_gram_rows_band(
         je = rowp[j + 1];
       }
       const int cnt = static_cast<int>(min(32u, q_end - q0));
-      // software pipeline: entries of observation k + 1 load while k updates
-      constexpr int kPre = 4;  // entries per lane kept in flight (128 per obs)
-      int pc[kPre];
-      double pv[kPre];
-      auto fetch = [&](int k) {
-        const uint32_t b = __shfl_sync(0xffffffffu, jb, k), e = __shfl_sync(0xffffffffu, je, k);
+      // software pipeline: the entries of observations k + 1 .. k + kDepth
+      // are in flight while k updates (a register ring, statically indexed)
+      constexpr int kPre = 3;    // entries per lane and observation (96 per obs)
+      constexpr int kDepth = 4;  // observations in flight
+      int pc[kDepth][kPre];
+      double pv[kDepth][kPre];
+      auto fetch = [&](int k, int slot_c[kPre], double slot_v[kPre]) {
+        const uint32_t b = __shfl_sync(0xffffffffu, jb, k & 31), e = __shfl_sync(0xffffffffu, je, k & 31);
 #pragma unroll
         for (int u = 0; u < kPre; ++u) {
           const uint32_t x = b + lane + 32 * u;
-          pc[u] = x < e ? static_cast<int>(col[x]) - lo : -1;
-          pv[u] = x < e ? val[x] : 0.0;
+          const bool ok = k < cnt && x < e;
+          slot_c[u] = ok ? static_cast<int>(col[x]) - lo : -1;
+          slot_v[u] = ok ? val[x] : 0.0;
         }
       };
-      fetch(0);
-      for (int k = 0; k < cnt; ++k) {
-        int cc[kPre];
-        double cv[kPre];
 #pragma unroll
-        for (int u = 0; u < kPre; ++u) {
-          cc[u] = pc[u];
-          cv[u] = pv[u];
-        }
-        const double v = __shfl_sync(0xffffffffu, vr, k);
-        const uint32_t b = __shfl_sync(0xffffffffu, jb, k), e = __shfl_sync(0xffffffffu, je, k);
-        if (k + 1 < cnt) fetch(k + 1);
+      for (int d = 0; d < kDepth; ++d) fetch(d, pc[d], pv[d]);
+      for (int k0 = 0; k0 < cnt; k0 += kDepth) {
 #pragma unroll
-        for (int u = 0; u < kPre; ++u)
-          if (cc[u] >= 0) acc[cc[u]] = fma(v, cv[u], acc[cc[u]]);
-        // observations with more than 32 * kPre entries (other geometries)
-        for (uint32_t x = b + 32 * kPre + lane; x < e; x += 32) {
-          const int ci = static_cast<int>(col[x]) - lo;
-          if (ci >= 0) acc[ci] = fma(v, val[x], acc[ci]);
+        for (int d = 0; d < kDepth; ++d) {
+          const int k = k0 + d;
+          if (k < cnt) {  // warp-uniform
+            int cc[kPre];
+            double cv[kPre];
+#pragma unroll
+            for (int u = 0; u < kPre; ++u) {
+              cc[u] = pc[d][u];
+              cv[u] = pv[d][u];
+            }
+            const double v = __shfl_sync(0xffffffffu, vr, k);
+            const uint32_t b = __shfl_sync(0xffffffffu, jb, k), e = __shfl_sync(0xffffffffu, je, k);
+            fetch(k + kDepth, pc[d], pv[d]);
+#pragma unroll
+            for (int u = 0; u < kPre; ++u)
+              if (cc[u] >= 0) acc[cc[u]] = fma(v, cv[u], acc[cc[u]]);
+            // observations with more than 32 * kPre entries (other geometries)
+            for (uint32_t x = b + 32 * kPre + lane; x < e; x += 32) {
+              const int ci = static_cast<int>(col[x]) - lo;
+              if (ci >= 0) acc[ci] = fma(v, val[x], acc[ci]);
+            }
+            __syncwarp();
+          }
         }
-        __syncwarp();
       }
     }
     const int c0 = max(lo, 0), c1 = min(r + band, n - 1);  // H[c][r]: column r, c >= lo
