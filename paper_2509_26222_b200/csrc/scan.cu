@@ -18,6 +18,7 @@ struct BinParams {
   double R[9], t[3];
   double org_x, org_y, inv_cell;
   int nx, ny;
+  int sub;  // sub-cells per axis inside a cell (power of two), 1 = none
 };
 
 __global__ void k_bin_keys(BinParams p, const double* __restrict__ hx, const double* __restrict__ hy,
@@ -31,7 +32,14 @@ __global__ void k_bin_keys(BinParams p, const double* __restrict__ hx, const dou
   double fx = (x - p.org_x) * p.inv_cell, fy = (y - p.org_y) * p.inv_cell;
   fx = isfinite(fx) ? fmin(fmax(fx, 0.0), p.nx - 1.0) : 0.0;
   fy = isfinite(fy) ? fmin(fmax(fy, 0.0), p.ny - 1.0) : 0.0;
-  key[i] = static_cast<uint32_t>(fx) * static_cast<uint32_t>(p.ny) + static_cast<uint32_t>(fy);
+  // cell-major, then a sub-cell (row-major p.sub x p.sub) inside the cell:
+  // a warp's run of points stays compact, so a small pose change between
+  // binning and evaluation moves it into few distinct lattice windows
+  const uint32_t cx = static_cast<uint32_t>(fx), cy = static_cast<uint32_t>(fy);
+  const uint32_t sx = min(static_cast<uint32_t>((fx - cx) * p.sub), static_cast<uint32_t>(p.sub - 1));
+  const uint32_t sy = min(static_cast<uint32_t>((fy - cy) * p.sub), static_cast<uint32_t>(p.sub - 1));
+  key[i] = (cx * static_cast<uint32_t>(p.ny) + cy) * static_cast<uint32_t>(p.sub * p.sub) +
+           sx * static_cast<uint32_t>(p.sub) + sy;
   idx[i] = static_cast<uint32_t>(i);
 }
 
@@ -86,11 +94,13 @@ tlg_scan* scan_create(tlg_model* m, const double R0[9], const double t0[3], cons
     uint32_t* key = ctx->ws<uint32_t>(S_KEYS, n);
     uint32_t* key2 = ctx->ws<uint32_t>(S_KEYS2, n);
     uint32_t* idx = ctx->ws<uint32_t>(S_VALS, n);
+    const unsigned long long cells = static_cast<unsigned long long>(p.nx) * p.ny;
+    p.sub = cells * 16 <= (1ull << 32) ? 4 : (cells * 4 <= (1ull << 32) ? 2 : 1);
     k_bin_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, hx, hy, hz, n, key, idx);
     TLG_LAUNCHED(ctx);
     int end_bit = 1;
-    const unsigned long long cells = static_cast<unsigned long long>(p.nx) * p.ny;
-    while (end_bit < 32 && (1ull << end_bit) < cells) ++end_bit;
+    const unsigned long long keys = cells * p.sub * p.sub;
+    while (end_bit < 32 && (1ull << end_bit) < keys) ++end_bit;
     size_t tmp = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, key2, idx, sc->perm.p, (int)n, 0, end_bit, s);
     void* dtmp = ctx->ws<unsigned char>(S_CUB, tmp);
