@@ -656,11 +656,19 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const double* __r
                                                                double* __restrict__ out) {
   __shared__ double sh[kRedThreads];
   const int entry = blockIdx.x;
-  const size_t per = (nchunks + kRedThreads - 1) / kRedThreads;
-  const size_t c0 = threadIdx.x * per, c1 = std::min(nchunks, c0 + per);
   const double* p = partials + (size_t)entry * nchunks;
+  // thread t: chunks t, t + 256, ... (coalesced, 8 loads in flight; a fixed
+  // order, so the result is reproducible run to run)
   double v = 0.0;
-  for (size_t c = c0; c < c1; ++c) v += p[c];
+  size_t c = threadIdx.x;
+  for (; c + 7 * kRedThreads < nchunks; c += 8 * kRedThreads) {
+    double q[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) q[u] = p[c + u * kRedThreads];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v += q[u];
+  }
+  for (; c < nchunks; c += kRedThreads) v += p[c];
   sh[threadIdx.x] = v;
   __syncthreads();
   for (int o = kRedThreads / 2; o > 0; o >>= 1) {
