@@ -199,9 +199,12 @@ def run_update_bench(torch, device, steps=5):
             times.append(ev0.elapsed_time(ev1))
             reps.append(rep)
         rep = reps[-1]
+        gflop = statistics.median(r.flops for r in reps) / 1e9
         out[f"m{m}"] = {"ms_per_scan": statistics.median(times), "ms_min": min(times),
                         "n_active": rep.active_centers, "active_blocks": rep.active_blocks,
-                        "solver": rep.solver, "rejected": rep.rejected}
+                        "solver": rep.solver, "rejected": rep.rejected,
+                        "gflop_per_scan": gflop,
+                        "fp64_tflops": gflop / statistics.median(times)}
     out["c4"] = run_update_c4(torch, steps)
     return out, model, kernel
 
@@ -239,6 +242,8 @@ def run_update_c4(torch, steps=5):
             times.append(ev0.elapsed_time(ev1))
     out = {"M": model.num_centers(), "m": 20000, "footprint_m": 2.5,
            "ms_per_scan": statistics.median(times), "ms_min": min(times),
+           "gflop_per_scan": rep.flops / 1e9,
+           "fp64_tflops": rep.flops / 1e9 / statistics.median(times),
            "n_active": rep.active_centers, "active_blocks": rep.active_blocks,
            "solver": rep.solver, "rejected": rep.rejected}
     # fit_batch_ridge at C4 scale (terrain_model.cpp:269-308):
@@ -558,6 +563,11 @@ def main():
         # FP64 view of the same kernel (pairs/s based)
         if not args.no_update:
             upd, umodel, ukernel = run_update_bench(torch, local)
+            # F / t / P_FP64: the formulation's flops over the
+            # measured DMMA peak of this run
+            for key in ("m400", "m20000", "c4"):
+                if key in upd and "fp64_tflops" in upd[key]:
+                    upd[key]["dmma_peak_frac"] = upd[key]["fp64_tflops"] / dmma.value
             result["update"] = upd
             if not args.no_cpu:
                 cms, crep = cpu_update_ms(umodel, ukernel, 400)

@@ -71,6 +71,7 @@ typedef struct tlg_update_report {
   uint64_t born_centers;
   int32_t rejected;     /* inner solve failed; births persist, weights/blocks unchanged */
   int32_t solver;       /* 1 = one-shot Woodbury (m x m), 2 = information form (n x n) */
+  double flops;         /* FP64 flops of the formulation run (DESIGN.md §4 F_W / F_I) */
 } tlg_update_report;
 
 /* Normal-equation block of the stacked manifold rows

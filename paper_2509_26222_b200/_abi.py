@@ -79,7 +79,8 @@ class CenterParamsC(C.Structure):
 
 class UpdateReportC(C.Structure):
     _fields_ = [("active_blocks", C.c_uint64), ("active_centers", C.c_uint64),
-                ("born_centers", C.c_uint64), ("rejected", C.c_int32), ("solver", C.c_int32)]
+                ("born_centers", C.c_uint64), ("rejected", C.c_int32), ("solver", C.c_int32),
+                ("flops", C.c_double)]
 
 
 class NormalEqC(C.Structure):

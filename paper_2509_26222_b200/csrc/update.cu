@@ -871,6 +871,25 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
 
   // ---- K5: Mt (CSR over observations, cols = merged rows) -----------------
   const Csr c = build_csr(m, x, y, mm, rowof, m->kc.neg_inv_2st2, m->kc.scale, false, nullptr);
+  {
+    // algorithmic FP64 flops of the formulation about to run:
+    // F_W = 2 nnz nbar_q + 2 m^2 kbar + (2/3) m^3 (Cholesky + X) + m^2 n (Y)
+    //       + 2 m sum_q n_q^2;
+    // F_I = sum_q n_q^3 + 2 m kbar^2 + n b^2 + n^2 b (X) + 2 sum_q (n - off_q) n_q^2
+    const double md = static_cast<double>(mm), nd = n, nnz = static_cast<double>(c.nnz);
+    const double kbar = mm ? nnz / md : 0.0;
+    double s2 = 0.0, s3 = 0.0, st = 0.0;
+    for (const auto& tq : tab) {
+      const double q = tq.n;
+      s2 += q * q;
+      s3 += q * q * q;
+      st += (nd - tq.off) * q * q;
+    }
+    rep->flops = info_form ? s3 + 2.0 * md * kbar * kbar + nd * band * double(band) +
+                                 nd * nd * band + 2.0 * st
+                           : 2.0 * nnz * (nq ? nd / nq : 0.0) + 2.0 * md * md * kbar +
+                                 (2.0 / 3.0) * md * md * md + md * md * nd + 2.0 * md * s2;
+  }
   double* wm = ctx->ws<double>(S_WORK1, n);
   k_gather_w<<<(n + 255) / 256, 256, 0, s>>>(m->w.p, d_merged, n, wm);
   TLG_LAUNCHED(ctx);

@@ -106,6 +106,7 @@ class UpdateReport:
     born_centers: int = 0
     rejected: bool = False
     solver: str = ""
+    flops: float = 0.0  # FP64 flops of the formulation run (tlg_update_report.flops)
 
 
 @dataclass
@@ -458,7 +459,8 @@ class TerrainModel:
                                                len(zs), _mem(xs), 1 if allow_birth else 0,
                                                C.byref(rep)))
         return UpdateReport(rep.active_blocks, rep.active_centers, rep.born_centers,
-                            bool(rep.rejected), {0: "", 1: "woodbury", 2: "information"}[rep.solver])
+                            bool(rep.rejected), {0: "", 1: "woodbury", 2: "information"}[rep.solver],
+                            rep.flops)
 
     # ---- persistence (snapshot.cpp) ------------------------------------------
     def save(self, path: str) -> None:
