@@ -37,27 +37,40 @@ __device__ __forceinline__ void gemv_tile(const GemmDesc& d, int m0, int K) {
   const int mb = min(TM, d.M - m0);
   auto bval = [&](int k) { return d.tb ? d.B[(size_t)k * d.ldb] : d.B[k]; };
   if (!d.ta) {
+    // two threads per row (k even / odd), eight independent partial sums
+    // each: eight loads in flight per thread instead of one dependent chain
     const int i = t & 63, h = t >> 6;
-    double s0 = 0.0, s1 = 0.0;
+    double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     if (i < mb) {
       const double* a = d.A + m0 + i;
       int k = h;
-      for (; k + 2 < K; k += 4) {
-        s0 = fma(a[(size_t)k * d.lda], bval(k), s0);
-        s1 = fma(a[(size_t)(k + 2) * d.lda], bval(k + 2), s1);
-      }
-      for (; k < K; k += 2) s0 = fma(a[(size_t)k * d.lda], bval(k), s0);
-    }
-    red[t] = s0 + s1;
-  } else {
-    const int lane = t & 31, w = t >> 5;
-    for (int i = w; i < mb; i += 4) {
-      const double* a = d.A + (size_t)(m0 + i) * d.lda;
-      double s = 0.0;
-      for (int k = lane; k < K; k += 32) s = fma(a[k], bval(k), s);
+      for (; k + 14 < K; k += 16) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) red[i] = s;
+        for (int u = 0; u < 8; ++u)
+          s[u] = fma(a[(size_t)(k + 2 * u) * d.lda], bval(k + 2 * u), s[u]);
+      }
+      for (; k < K; k += 2) s[0] = fma(a[(size_t)k * d.lda], bval(k), s[0]);
+    }
+    red[t] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+  } else {
+    // a warp per row (lanes over k, coalesced), four rows in flight per warp
+    const int lane = t & 31, w = t >> 5;
+    for (int i0 = w; i0 < mb; i0 += 16) {
+      double sr[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + 4 * u;
+        if (i < mb) {
+          const double* a = d.A + (size_t)(m0 + i) * d.lda;
+          for (int k = lane; k < K; k += 32) sr[u] = fma(a[k], bval(k), sr[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sr[u] += __shfl_xor_sync(0xffffffffu, sr[u], o);
+        if (lane == 0 && i0 + 4 * u < mb) red[i0 + 4 * u] = sr[u];
+      }
     }
   }
   __syncthreads();

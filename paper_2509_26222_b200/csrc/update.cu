@@ -228,14 +228,19 @@ struct BlockTab {  // per merged block q
   int pad;
 };
 
+// r_j = z_j - m_j . w: a warp per observation (lanes over its entries,
+// fixed shuffle tree)
 __global__ void k_residual(const uint32_t* __restrict__ rowp, const uint32_t* __restrict__ col,
                            const double* __restrict__ val, const double* __restrict__ z,
                            const double* __restrict__ wm, size_t m, double* __restrict__ resid) {
-  const size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const size_t j = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (j >= m) return;
   double s = 0.0;
-  for (uint32_t e = rowp[j]; e < rowp[j + 1]; ++e) s = fma(val[e], wm[col[e]], s);
-  resid[j] = z[j] - s;
+  for (uint32_t e = rowp[j] + lane; e < rowp[j + 1]; e += 32) s = fma(val[e], wm[col[e]], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) resid[j] = z[j] - s;
 }
 
 __global__ void k_gather_w(const double* __restrict__ w, const uint32_t* __restrict__ merged, int n,
@@ -286,7 +291,11 @@ __global__ void __launch_bounds__(256) k_build_S(const uint32_t* __restrict__ ro
 }
 
 // Symmetrise every merged block of the pool in place.
-__global__ void k_symmetrize_blocks(const BlockTab* __restrict__ tab, double* __restrict__ pool) {
+// A_q <- 0.5 (A_q + A_q^T) per block. Blocks that fit are staged through
+// shared memory (one coalesced read and one coalesced write per element);
+// larger ones are symmetrised in place in global memory.
+__global__ void k_symmetrize_blocks_global(const BlockTab* __restrict__ tab,
+                                           double* __restrict__ pool) {
   const BlockTab t = tab[blockIdx.x];
   double* a = pool + t.pool_off;
   for (int e = threadIdx.x; e < t.n * t.n; e += blockDim.x) {
@@ -296,6 +305,20 @@ __global__ void k_symmetrize_blocks(const BlockTab* __restrict__ tab, double* __
       a[r + (size_t)c * t.ld] = v;
       a[c + (size_t)r * t.ld] = v;
     }
+  }
+}
+
+__global__ void k_symmetrize_blocks(const BlockTab* __restrict__ tab, double* __restrict__ pool) {
+  extern __shared__ double sb[];
+  const BlockTab t = tab[blockIdx.x];
+  double* a = pool + t.pool_off;
+  const int nn = t.n * t.n;
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) sb[e] = a[(e % t.n) + (size_t)(e / t.n) * t.ld];
+  __syncthreads();
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    const int r = e % t.n, c = e / t.n;
+    const double v = r == c ? sb[e] : 0.5 * (r > c ? sb[e] + sb[c + r * t.n] : sb[c + r * t.n] + sb[e]);
+    a[r + (size_t)c * t.ld] = v;
   }
 }
 
@@ -894,7 +917,8 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   k_gather_w<<<(n + 255) / 256, 256, 0, s>>>(m->w.p, d_merged, n, wm);
   TLG_LAUNCHED(ctx);
   double* resid = ctx->ws<double>(S_RESID, mm);
-  k_residual<<<(unsigned)((mm + 255) / 256), 256, 0, s>>>(c.rowp, c.col, c.val, z, wm, mm, resid);
+  k_residual<<<(unsigned)((mm * 32 + 255) / 256), 256, 0, s>>>(c.rowp, c.col, c.val, z, wm, mm,
+                                                                resid);
   TLG_LAUNCHED(ctx);
   tr.mark("csr");
 
@@ -997,7 +1021,17 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   TLG_CUDA(cudaMemcpyAsync(d_descs, h_descs, nq * sizeof(GemmDesc), cudaMemcpyHostToDevice, s));
   gemm_grouped(ctx, d_descs, nq, maxq, maxq);
   tr.mark("blocks");
-  k_symmetrize_blocks<<<nq, 256, 0, s>>>(d_tab, m->pool.p);
+  {
+    const size_t smem = sizeof(double) * static_cast<size_t>(maxq) * maxq;
+    if (smem <= 200 * 1024) {
+      if (smem > 48 * 1024)
+        TLG_CUDA(cudaFuncSetAttribute(k_symmetrize_blocks,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_symmetrize_blocks<<<nq, 256, smem, s>>>(d_tab, m->pool.p);
+    } else {
+      k_symmetrize_blocks_global<<<nq, 256, 0, s>>>(d_tab, m->pool.p);
+    }
+  }
   TLG_LAUNCHED(ctx);
   k_apply_dw<<<(n + 255) / 256, 256, 0, s>>>(m->w.p, d_merged, n, dw);
   TLG_LAUNCHED(ctx);
