@@ -262,16 +262,23 @@ __global__ void __launch_bounds__(128) k_build_Kt(
     const double* __restrict__ val, const int* __restrict__ rowblk,
     const int* __restrict__ rowloc, const BlockTab* __restrict__ tab,
     const double* __restrict__ pool, int m, double* __restrict__ Kt) {
+  // Runs of consecutive entries in the same block (the candidate sweep visits
+  // a block's centres together): per run each thread accumulates its rows
+  // over the run's entries in a register and updates Kt once.
   const int j = blockIdx.x;
-  for (uint32_t e = rowp[j]; e < rowp[j + 1]; ++e) {
-    const int r = static_cast<int>(col[e]);
-    const BlockTab t = tab[rowblk[r]];
-    const double v = val[e];
-    const double* hcol = pool + t.pool_off + static_cast<size_t>(rowloc[r]) * t.ld;
+  const uint32_t e_end = rowp[j + 1];
+  for (uint32_t e = rowp[j]; e < e_end;) {
+    const int b = rowblk[col[e]];
+    uint32_t f = e + 1;
+    while (f < e_end && rowblk[col[f]] == b) ++f;
+    const BlockTab t = tab[b];
     for (int i = threadIdx.x; i < t.n; i += blockDim.x) {
-      double* p = Kt + j + static_cast<size_t>(t.off + i) * m;
-      *p = fma(hcol[i], v, *p);
+      double acc = 0.0;
+      for (uint32_t q = e; q < f; ++q)
+        acc = fma(pool[t.pool_off + static_cast<size_t>(rowloc[col[q]]) * t.ld + i], val[q], acc);
+      Kt[j + static_cast<size_t>(t.off + i) * m] += acc;
     }
+    e = f;
   }
 }
 
