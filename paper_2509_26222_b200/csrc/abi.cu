@@ -83,11 +83,14 @@ void check_ptr(const void* p, const char* what) {
 void* tlg_ctx::host_stage(size_t bytes) {
   TLG_CUDA(cudaStreamSynchronize(stream));
   if (bytes > pinned_bytes) {
+    // pinned allocations cost milliseconds: grow with headroom (per-scan
+    // table sizes creep up with the active set), at least 1 MiB
+    const size_t cap = std::max(bytes + bytes / 2, size_t{1} << 20);
     if (pinned) cudaFreeHost(pinned);
     pinned = nullptr;
     pinned_bytes = 0;
-    TLG_CUDA(cudaMallocHost(&pinned, bytes));
-    pinned_bytes = bytes;
+    TLG_CUDA(cudaMallocHost(&pinned, cap));
+    pinned_bytes = cap;
   }
   return pinned;
 }

@@ -779,6 +779,82 @@ static int block_band(const std::vector<std::pair<int64_t, int64_t>>& btile,
   return band;
 }
 
+// Births pre-check (steady state): a node can be born only if it is
+// supported, and every supported node lies within r_a of a point, i.e. in
+// the node window of the scan's bounding box dilated by r_a. If every node of
+// that window already holds a centre (lattice presence > 0 implies the
+// reference's occupancy key), nothing can be born and the support count is
+// skipped. One CTA; out = 1 when some window node is unoccupied.
+__global__ void __launch_bounds__(1024) k_births_precheck(
+    const double* __restrict__ x, const double* __restrict__ y, size_t m, double min_x,
+    double min_y, double res, double r_a, int nx, int ny, const int* __restrict__ P, int ni,
+    int nj, int i_org, int j_org, int* __restrict__ out) {
+  __shared__ double red[4][32];
+  double lo_x = INFINITY, lo_y = INFINITY, hi_x = -INFINITY, hi_y = -INFINITY;
+  for (size_t k = threadIdx.x; k < m; k += blockDim.x) {
+    lo_x = fmin(lo_x, x[k]);
+    hi_x = fmax(hi_x, x[k]);
+    lo_y = fmin(lo_y, y[k]);
+    hi_y = fmax(hi_y, y[k]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo_x = fmin(lo_x, __shfl_xor_sync(0xffffffffu, lo_x, o));
+    hi_x = fmax(hi_x, __shfl_xor_sync(0xffffffffu, hi_x, o));
+    lo_y = fmin(lo_y, __shfl_xor_sync(0xffffffffu, lo_y, o));
+    hi_y = fmax(hi_y, __shfl_xor_sync(0xffffffffu, hi_y, o));
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    red[0][w] = lo_x;
+    red[1][w] = hi_x;
+    red[2][w] = lo_y;
+    red[3][w] = hi_y;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    lo_x = lane < nw ? red[0][lane] : INFINITY;
+    hi_x = lane < nw ? red[1][lane] : -INFINITY;
+    lo_y = lane < nw ? red[2][lane] : INFINITY;
+    hi_y = lane < nw ? red[3][lane] : -INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo_x = fmin(lo_x, __shfl_xor_sync(0xffffffffu, lo_x, o));
+      hi_x = fmax(hi_x, __shfl_xor_sync(0xffffffffu, hi_x, o));
+      lo_y = fmin(lo_y, __shfl_xor_sync(0xffffffffu, lo_y, o));
+      hi_y = fmax(hi_y, __shfl_xor_sync(0xffffffffu, hi_y, o));
+    }
+    if (lane == 0) {
+      red[0][0] = lo_x;
+      red[1][0] = hi_x;
+      red[2][0] = lo_y;
+      red[3][0] = hi_y;
+    }
+  }
+  __syncthreads();
+  // node window with a one-node margin, clamped to the roi lattice [0, nx] x [0, ny]
+  const double fi0 = floor((red[0][0] - r_a - min_x) / res) - 1.0;
+  const double fi1 = ceil((red[1][0] + r_a - min_x) / res) + 1.0;
+  const double fj0 = floor((red[2][0] - r_a - min_y) / res) - 1.0;
+  const double fj1 = ceil((red[3][0] + r_a - min_y) / res) + 1.0;
+  if (!(fi0 == fi0 && fi1 == fi1 && fj0 == fj0 && fj1 == fj1)) {
+    if (threadIdx.x == 0) *out = 1;
+    return;
+  }
+  const int i0 = static_cast<int>(fmax(fi0, 0.0)), i1 = static_cast<int>(fmin(fi1, double(nx)));
+  const int j0 = static_cast<int>(fmax(fj0, 0.0)), j1 = static_cast<int>(fmin(fj1, double(ny)));
+  if (i1 < i0 || j1 < j0) return;
+  const long long wj = j1 - j0 + 1, cnt = (i1 - i0 + 1) * wj;
+  for (long long e = threadIdx.x; e < cnt; e += blockDim.x) {
+    const int k = i0 + static_cast<int>(e / wj) - i_org, l = j0 + static_cast<int>(e % wj) - j_org;
+    if (k < 0 || k >= ni || l < 0 || l >= nj || P[static_cast<size_t>(k) * nj + l] == 0) {
+      *out = 1;
+      return;
+    }
+  }
+}
+
 void recursive_update_device(tlg_model* m, const double* x, const double* y, const double* z,
                              size_t mm, bool allow_birth, tlg_update_report* rep) {
   tlg_ctx* ctx = m->ctx;
@@ -792,8 +868,26 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
     if (!(cp.mesh_resolution > 0.0))
       throw Error(TLG_INVALID_ARGUMENT, "mesh_resolution must be > 0");
     if (cp.accept_count < 1) throw Error(TLG_INVALID_ARGUMENT, "accept_count must be >= 1");
+    bool maybe_births = true;
+    const double span_x = cp.roi_max_x - cp.roi_min_x, span_y = cp.roi_max_y - cp.roi_min_y;
+    if (!m->grid_dirty && m->lat.valid && mm > 0 && span_x >= 0.0 && span_y >= 0.0) {
+      const LatticeGrid& L = m->lat;
+      int* flag = ctx->ws<int>(S_COUNT, 8);
+      TLG_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+      const int rnx = static_cast<int>(std::floor(span_x / cp.mesh_resolution + 1e-9));
+      const int rny = static_cast<int>(std::floor(span_y / cp.mesh_resolution + 1e-9));
+      k_births_precheck<<<1, 1024, 0, s>>>(x, y, mm, cp.roi_min_x, cp.roi_min_y,
+                                           cp.mesh_resolution, cp.accept_radius, rnx, rny,
+                                           L.P.p, L.ni, L.nj, L.i_org, L.j_org, flag);
+      TLG_LAUNCHED(ctx);
+      int hflag = 1;
+      TLG_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+      TLG_CUDA(cudaStreamSynchronize(s));
+      maybe_births = hflag != 0;
+    }
     const double *nx = nullptr, *ny = nullptr;
-    const size_t nn = supported_nodes_device(ctx, x, y, mm, cp, &nx, &ny);
+    const size_t nn =
+        maybe_births ? supported_nodes_device(ctx, x, y, mm, cp, &nx, &ny) : 0;
     if (nn) {
       std::vector<double> hx(nn), hy(nn);
       TLG_CUDA(cudaMemcpyAsync(hx.data(), nx, nn * 8, cudaMemcpyDeviceToHost, s));
