@@ -102,10 +102,10 @@ __device__ __forceinline__ void bd_pair(double& S, double& T, double d2, double 
 
 // LOOSE (compiled geometries only, dispatched when LatticeView::loose_ok):
 // boundary pairs are summed without the cutoff test. A pair that fails it
-// lies beyond the cutoff, where kappa_sigma <= exp(-r2 / (2 sigma^2)); with
-// the paper's parameters that is 6.8e-15, and the host gate bounds the
-// total perturbation of z and sigma * grad f by 1e-11 x the window's largest
-// |w|, two orders under the 1e-9 parity tolerance. Everything else (window,
+// lies beyond the cutoff, where kappa_sigma <= exp(-r2 / (2 sigma^2)) (6.8e-15
+// with the paper's parameters). Every point checks that the resulting worst
+// case stays under 1e-10 of its own parity scale (guard at the end of the
+// sweep) and is re-evaluated exactly otherwise. Everything else (window,
 // support flag, always-inside/outside pairs) is the exact path's.
 template <int WIN, int G, bool LOOSE = false>
 __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, double y,
