@@ -505,11 +505,22 @@ __global__ void k_sel_keys(const uint32_t* __restrict__ sel, size_t cnt,
   if (plane) atomicAdd(nplane, 1);
 }
 
+__device__ __forceinline__ double undkey(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & ~(1ull << 63)) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+// scan_matcher.cpp:150-180 trims with the order statistics read on the
+// device (sorted keys kd2 / kq2, plane count): no host round trip
 __global__ void k_trim(const uint32_t* __restrict__ sel, size_t cnt, const double* __restrict__ dist,
-                       const double* __restrict__ fitq, double cut, double qcut,
-                       uint8_t* __restrict__ keep) {
+                       const double* __restrict__ fitq, const uint64_t* __restrict__ kd2,
+                       const uint64_t* __restrict__ kq2, const int* __restrict__ nplane,
+                       double trim_ratio, double trim_floor, uint8_t* __restrict__ keep) {
   const size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (j >= cnt) return;
+  const double cut = fmax(__dmul_rn(trim_ratio, undkey(kd2[cnt / 2])), trim_floor);
+  const int np = *nplane;
+  const double qcut = np > 0 ? fmax(__dmul_rn(10.0, undkey(kq2[np / 2])), 1e-7) : INFINITY;
   const uint32_t i = sel[j];
   keep[j] = dist[i] <= cut && fitq[i] <= qcut;
 }
@@ -917,26 +928,9 @@ size_t build_correspondences_device(tlg_map* m, const double* px, const double* 
     void* d = ctx->ws<char>(S_CUB, tmp);
     TLG_CUDA(cub::DeviceRadixSort::SortKeys(d, tmp, kd, kd2, cnt, 0, 64, s));
     TLG_CUDA(cub::DeviceRadixSort::SortKeys(d, tmp, kq, kq2, cnt, 0, 64, s));
-    uint64_t mk = 0, qk = 0;
-    int np = 0;
-    TLG_CUDA(cudaMemcpyAsync(&mk, kd2 + cnt / 2, 8, cudaMemcpyDeviceToHost, s));
-    TLG_CUDA(cudaMemcpyAsync(&np, nplane, sizeof(int), cudaMemcpyDeviceToHost, s));
-    TLG_CUDA(cudaStreamSynchronize(s));
-    auto undkey = [](uint64_t k) {
-      const uint64_t b = (k >> 63) ? (k & ~(1ull << 63)) : ~k;
-      double v;
-      std::memcpy(&v, &b, 8);
-      return v;
-    };
-    const double cut = std::max(cfg.trim_ratio * undkey(mk), cfg.trim_floor);
-    double qcut = INFINITY;
-    if (np > 0) {
-      TLG_CUDA(cudaMemcpyAsync(&qk, kq2 + np / 2, 8, cudaMemcpyDeviceToHost, s));
-      TLG_CUDA(cudaStreamSynchronize(s));
-      qcut = std::max(10.0 * undkey(qk), 1e-7);
-    }
     uint8_t* keep = ctx->ws<uint8_t>(S_ACTIVE, cnt);
-    k_trim<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(sel, cnt, dist, fq, cut, qcut, keep);
+    k_trim<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(sel, cnt, dist, fq, kd2, kq2, nplane,
+                                                         cfg.trim_ratio, cfg.trim_floor, keep);
     TLG_LAUNCHED(ctx);
     uint32_t* sel2 = ctx->ws<uint32_t>(S_NODE_IDX, cnt);
     const size_t c2 = select_flagged<uint32_t>(ctx, keep, cnt, sel2);
