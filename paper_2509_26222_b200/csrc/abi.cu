@@ -778,8 +778,8 @@ tlg_status tlg_recursive_update(tlg_model* m, const double* x, const double* y, 
     const double* dx = as_device(ctx, S_IN_X, x, mm, in_mem);
     const double* dy = as_device(ctx, S_IN_Y, y, mm, in_mem);
     const double* dz = as_device(ctx, S_IN_Z, z, z_len, in_mem);
-    validate_obs_device(ctx, dx, dy, dz, mm, z_len);
-    recursive_update_device(m, dx, dy, dz, mm, allow_birth != 0, &rep);
+    const int* vflag = validate_obs_launch(ctx, dx, dy, dz, mm, z_len);
+    recursive_update_device(m, dx, dy, dz, mm, allow_birth != 0, &rep, vflag);
     if (report) *report = rep;
   });
 }

@@ -104,7 +104,7 @@ enum Slot : int {
   S_KEYS, S_KEYS2, S_VALS, S_VALS2, S_NODES_X, S_NODES_Y, S_NODE_FLAG, S_NODE_IDX,
   S_COUNT, S_ACTIVE, S_BLOCKFLAG, S_ROWOF, S_MERGED, S_ROWPTR, S_COLIDX, S_MTVAL,
   S_KMAT, S_SMAT, S_RESID, S_U, S_YMAT, S_HMAT, S_WORK1, S_WORK2, S_WORK3, S_BLKTAB,
-  S_MOMENT_ROW, S_TROWP, S_TKEYS, S_LINV, S_XINV, S_XINV2, S_SOLVE, S_BSOLVE,
+  S_MOMENT_ROW, S_TROWP, S_TKEYS, S_LINV, S_XINV, S_XINV2, S_SOLVE, S_BSOLVE, S_VALIDATE,
   S_NUM_SLOTS
 };
 
@@ -394,6 +394,11 @@ size_t supported_nodes_device(tlg_ctx* ctx, const double* dx, const double* dy, 
                               const double** out_y);
 void validate_obs_device(tlg_ctx* ctx, const double* x, const double* y, const double* z,
                          size_t m, size_t zn);
+// Launch-only form: returns the device flag (read it at the next sync and
+// pass it to validate_obs_check, which throws like validate_obs_device).
+int* validate_obs_launch(tlg_ctx* ctx, const double* x, const double* y, const double* z,
+                         size_t m, size_t zn);
+void validate_obs_check(int flag);
 
 // eval.cu
 void eval_device(tlg_model* m, const double* x, const double* y, size_t n, double* z,
@@ -404,8 +409,11 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
                      double* raw, tlg_normal_eq* ne);
 
 // update.cu
+// pending_valid: flag of a validate_obs_launch not yet read; checked at the
+// first synchronisation, before any state changes
 void recursive_update_device(tlg_model* m, const double* x, const double* y, const double* z,
-                             size_t mm, bool allow_birth, tlg_update_report* rep);
+                             size_t mm, bool allow_birth, tlg_update_report* rep,
+                             const int* pending_valid = nullptr);
 void batch_fit_device(tlg_model* m, const double* x, const double* y, const double* z,
                       size_t mm);
 void batch_system_dims(tlg_model* m, size_t* n, size_t* ld, size_t* elems);

@@ -33,20 +33,30 @@ __global__ void k_validate(const double* __restrict__ x, const double* __restric
   }
 }
 
-void validate_obs_device(tlg_ctx* ctx, const double* x, const double* y, const double* z,
+int* validate_obs_launch(tlg_ctx* ctx, const double* x, const double* y, const double* z,
                          size_t m, size_t zn) {
   // TerrainObservation::validate (center_select.cpp:9-16)
   if (m != zn) throw Error(TLG_INVALID_ARGUMENT, "observation xy/z length mismatch");
   if (m == 0) throw Error(TLG_INVALID_ARGUMENT, "empty observation");
-  int* err = ctx->ws<int>(S_FLAGS, 4);
+  int* err = ctx->ws<int>(S_VALIDATE, 1);
   TLG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
   const unsigned blocks = static_cast<unsigned>(std::min<size_t>((m + 255) / 256, 8 * 148));
   k_validate<<<blocks, 256, 0, ctx->stream>>>(x, y, z, m, zn, err);
   TLG_LAUNCHED(ctx);
+  return err;
+}
+
+void validate_obs_check(int flag) {
+  if (flag) throw Error(TLG_INVALID_ARGUMENT, "non-finite observation coordinate");
+}
+
+void validate_obs_device(tlg_ctx* ctx, const double* x, const double* y, const double* z,
+                         size_t m, size_t zn) {
+  const int* err = validate_obs_launch(ctx, x, y, z, m, zn);
   int h = 0;
   TLG_CUDA(cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   TLG_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (h) throw Error(TLG_INVALID_ARGUMENT, "non-finite observation coordinate");
+  validate_obs_check(h);
 }
 
 // cell keys of the points + per-block bbox partials

@@ -856,11 +856,21 @@ __global__ void __launch_bounds__(1024) k_births_precheck(
 }
 
 void recursive_update_device(tlg_model* m, const double* x, const double* y, const double* z,
-                             size_t mm, bool allow_birth, tlg_update_report* rep) {
+                             size_t mm, bool allow_birth, tlg_update_report* rep,
+                             const int* pending_valid) {
   tlg_ctx* ctx = m->ctx;
   cudaStream_t s = ctx->stream;
   *rep = tlg_update_report{};
   StageTrace tr(ctx);
+  // the observation check's flag rides along with the first flag read below
+  auto check_valid_now = [&]() {
+    if (!pending_valid) return;
+    int h = 0;
+    TLG_CUDA(cudaMemcpyAsync(&h, pending_valid, sizeof(int), cudaMemcpyDeviceToHost, s));
+    TLG_CUDA(cudaStreamSynchronize(s));
+    pending_valid = nullptr;
+    validate_obs_check(h);
+  };
 
   // ---- births (terrain_model.cpp:150-161) --------------------------------
   if (allow_birth) {
@@ -880,11 +890,18 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
                                            cp.mesh_resolution, cp.accept_radius, rnx, rny,
                                            L.P.p, L.ni, L.nj, L.i_org, L.j_org, flag);
       TLG_LAUNCHED(ctx);
-      int hflag = 1;
+      int hflag = 1, hvalid = 0;
       TLG_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+      if (pending_valid)
+        TLG_CUDA(cudaMemcpyAsync(&hvalid, pending_valid, sizeof(int), cudaMemcpyDeviceToHost, s));
       TLG_CUDA(cudaStreamSynchronize(s));
+      if (pending_valid) {
+        pending_valid = nullptr;
+        validate_obs_check(hvalid);
+      }
       maybe_births = hflag != 0;
     }
+    check_valid_now();
     const double *nx = nullptr, *ny = nullptr;
     const size_t nn =
         maybe_births ? supported_nodes_device(ctx, x, y, mm, cp, &nx, &ny) : 0;
@@ -909,6 +926,7 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
       }
     }
   }
+  check_valid_now();
   ensure_grid(m);
   const size_t nc = m->hcx.size();
   const size_t nb = m->members.size();
