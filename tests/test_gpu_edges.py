@@ -195,3 +195,25 @@ def test_loose_guard_follows_weight_changes(gpu_ctx):
     g.set_weights(w)
     o.set_weights(w)
     _check_predict(k, g, o, q)
+
+
+@pytest.mark.parametrize("allow_birth", [True, False])
+def test_update_rejects_nonfinite_observation_without_state_change(gpu_ctx, allow_birth):
+    # TerrainObservation::validate (center_select.cpp:9-16) runs before any
+    # birth or weight change, also when its flag is read together with the
+    # births pre-check
+    k = T.KernelParams()
+    k.finalize()
+    roi = T.Rect((0.0, 0.0), (1.05, 1.05))
+    g = T.TerrainModel(k, T.CenterSet(np.zeros((0, 2)), 0.07, 0.12, 3, roi))
+    rng = np.random.default_rng(8)
+    xy = rng.uniform(0.0, 1.05, (3000, 2))
+    g.recursive_update(T.TerrainObservation(xy, np.sin(xy[:, 0])))
+    g.recursive_update(T.TerrainObservation(xy[:400], np.sin(xy[:400, 0])))
+    w0, n0 = g.weights().copy(), g.num_centers()
+    bad = rng.uniform(0.0, 1.05, (400, 2))
+    bad[17, 1] = np.nan
+    with pytest.raises(T.InvalidArgument):
+        g.recursive_update(T.TerrainObservation(bad, np.sin(bad[:, 0])), allow_birth)
+    assert g.num_centers() == n0
+    assert np.array_equal(g.weights(), w0)
