@@ -382,6 +382,52 @@ def run_match_bench(torch, cpu=True, steps=10):
     return out
 
 
+def run_consumers_bench(torch, umodel, ukernel, cpu=True, reps=10):
+    """SURVEY §8f row 4 consumers through the Python API, host arrays in and
+    out (wall clock per call): select_ground_points on a 200k-feature scan,
+    terrain_error_histogram on 10^6 samples against the C3 model; the oracle
+    restatements (one core) beside them."""
+    from paper_2509_26222_b200 import consumers as K
+    from paper_2509_26222_b200 import terrain as T
+    rng = np.random.default_rng(21)
+    n = 200_000
+    p = np.c_[rng.uniform(-4, 4, n), rng.uniform(-4, 4, n), rng.normal(0, 0.02, n)]
+    kinds = rng.choice(np.array([0, 1, 2], dtype=np.uint8), n, p=[0.1, 0.3, 0.6])
+    R = so3_exp(np.array([0.01, 0.02, 0.7]))
+    t = np.array([2.2, 2.2, 0.4])
+    roi = T.Rect((0.0, 0.0), (4.41, 4.41))
+    K.select_ground_points(p, kinds, R, t, roi, 2.5, 0.12, 20000)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        obs = K.select_ground_points(p, kinds, R, t, roi, 2.5, 0.12, 20000)
+    sel_ms = (time.perf_counter() - t0) / reps * 1e3
+    m = 1_000_000
+    xy = rng.uniform(0.0, 4.41, (m, 2))
+    z = staircase(xy[:, 0]) + rng.normal(0.0, 0.01, m)
+    K.terrain_error_histogram(umodel, xy, z, 0.05, 25)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        h = K.terrain_error_histogram(umodel, xy, z, 0.05, 25)
+    hist_ms = (time.perf_counter() - t0) / reps * 1e3
+    out = {"ground_scan_points": n, "ground_kept": len(obs.z), "select_ground_ms": sel_ms,
+           "histogram_samples": m, "histogram_ms": hist_ms, "histogram_total": h.total(),
+           "timing": "wall clock per call through the Python API (host arrays in/out)"}
+    if cpu:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle as orc
+        t0 = time.perf_counter()
+        orc.select_ground_points(p, kinds, R, t, roi, 2.5, 0.12, 20000)
+        out["cpu_reference_select_ground_ms"] = (time.perf_counter() - t0) * 1e3
+        om = orc.Model(ukernel, umodel.centers())
+        om.set_weights(umodel.weights())
+        ms = 100_000
+        t0 = time.perf_counter()
+        om.error_histogram(xy[:ms], z[:ms], 0.05, 25)
+        out["cpu_reference_histogram_ms_per_1e6"] = (time.perf_counter() - t0) * 1e3 * (m / ms)
+        out["cpu_reference"] = "oracle restatements (pipeline.cpp:150-170, metrics.cpp:199-232), 1 core"
+    return out
+
+
 def cpu_update_ms(model, kernel, m=400, seed=5):
     """Oracle recursive_update (reference algorithm, single thread) at M=4096."""
     sys.path.insert(0, str(ROOT / "oracle"))
@@ -575,6 +621,7 @@ def main():
                 result["update"]["cpu_oracle_n_active"] = crep["active_centers"]
         if not args.no_update:
             result["match"] = run_match_bench(torch, not args.no_cpu)
+            result["consumers"] = run_consumers_bench(torch, umodel, ukernel, not args.no_cpu)
         if not args.no_cpu:
             pts_h = torch.stack(list(h), 1)[: 2_000_000].cpu().numpy()
             rate, ns, threads, dt, _ = cpu_eval_rate(cs.centers, w, kernel, pts_h, R, tv,
