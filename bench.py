@@ -409,7 +409,20 @@ def run_consumers_bench(torch, umodel, ukernel, cpu=True, reps=10):
     for _ in range(reps):
         h = K.terrain_error_histogram(umodel, xy, z, 0.05, 25)
     hist_ms = (time.perf_counter() - t0) / reps * 1e3
-    out = {"ground_scan_points": n, "ground_kept": len(obs.z), "select_ground_ms": sel_ms,
+    # RBFT snapshot round trip of the C3 model (§8f row 3; byte layout of
+    # snapshot.cpp:7-126, tests/test_gpu_parity.py checks the bytes)
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        path = str(Path(td) / "c3.rbft")
+        t0 = time.perf_counter()
+        umodel.save(path)
+        save_ms = (time.perf_counter() - t0) * 1e3
+        t0 = time.perf_counter()
+        T.TerrainModel.load(path)
+        load_ms = (time.perf_counter() - t0) * 1e3
+        snap_bytes = Path(path).stat().st_size
+    out = {"snapshot_bytes": snap_bytes, "snapshot_save_ms": save_ms, "snapshot_load_ms": load_ms,
+           "ground_scan_points": n, "ground_kept": len(obs.z), "select_ground_ms": sel_ms,
            "histogram_samples": m, "histogram_ms": hist_ms, "histogram_total": h.total(),
            "timing": "wall clock per call through the Python API (host arrays in/out)"}
     if cpu:

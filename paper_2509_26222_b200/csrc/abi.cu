@@ -917,24 +917,33 @@ tlg_status tlg_model_load(tlg_ctx* ctx, const char* path, tlg_model** out) {
     check_ptr(ctx, "ctx");
     check_ptr(path, "path");
     check_ptr(out, "out");
-    std::ifstream in(path, std::ios::binary);
+    std::ifstream in(path, std::ios::binary | std::ios::ate);
     if (!in) throw Error(TLG_RUNTIME_ERROR, std::string("cannot open ") + path);
+    // one read of the whole file, then parse from memory
+    const std::streamsize fsize = in.tellg();
+    std::vector<char> buf(static_cast<size_t>(std::max<std::streamsize>(fsize, 0)));
+    in.seekg(0);
+    if (fsize > 0 && !in.read(buf.data(), fsize))
+      throw Error(TLG_RUNTIME_ERROR, std::string("cannot read ") + path);
+    size_t pos = 0;
+    auto take = [&](void* dst, size_t nbytes) {
+      if (pos + nbytes > buf.size()) throw Error(TLG_RUNTIME_ERROR, "truncated terrain snapshot");
+      std::memcpy(dst, buf.data() + pos, nbytes);
+      pos += nbytes;
+    };
     auto get32 = [&]() {
       uint32_t v;
-      in.read(reinterpret_cast<char*>(&v), 4);
-      if (!in) throw Error(TLG_RUNTIME_ERROR, "truncated terrain snapshot");
+      take(&v, 4);
       return v;
     };
     auto getd = [&]() {
       double v;
-      in.read(reinterpret_cast<char*>(&v), 8);
-      if (!in) throw Error(TLG_RUNTIME_ERROR, "truncated terrain snapshot");
+      take(&v, 8);
       return v;
     };
-    char magic[4];
-    in.read(magic, 4);
-    if (!in || std::memcmp(magic, "RBFT", 4) != 0)
+    if (buf.size() < 4 || std::memcmp(buf.data(), "RBFT", 4) != 0)
       throw Error(TLG_RUNTIME_ERROR, std::string("not a terrain snapshot: ") + path);
+    pos = 4;
     if (get32() != 1u) throw Error(TLG_RUNTIME_ERROR, "unsupported snapshot version");
     const uint32_t n = get32(), nb = get32();
     std::vector<double> cx(n), cy(n), w(n);
