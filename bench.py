@@ -637,6 +637,14 @@ def main():
         if not args.no_update:
             result["match"] = run_match_bench(torch, not args.no_cpu)
             result["consumers"] = run_consumers_bench(torch, umodel, ukernel, not args.no_cpu)
+            # C2-style odometry stream (BASELINE configs[1]): the restated
+            # pipeline.cpp:196-300 loop over synthetic staircase scans
+            sys.path.insert(0, str(ROOT / "tools"))
+            from pipeline_c2 import run_c2
+            c2 = run_c2(scans=30)
+            c2["note"] = ("synthetic staircase with walls and poles, ~20k features/scan; host "
+                          "(Python) LM loop over device association, rows and update")
+            result["pipeline_c2"] = c2
         if not args.no_cpu:
             pts_h = torch.stack(list(h), 1)[: 2_000_000].cpu().numpy()
             rate, ns, threads, dt, _ = cpu_eval_rate(cs.centers, w, kernel, pts_h, R, tv,

@@ -44,13 +44,9 @@ def make_scan(rng, R, t, n=20000, rng_m=6.0):
     return ((P[perm] - t) @ R), K[perm]
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--scans", type=int, default=100)
-    ap.add_argument("--points", type=int, default=20000)
-    ap.add_argument("--verbose", action="store_true")
-    ap.add_argument("--no-manifold", action="store_true")
-    a = ap.parse_args()
+def run_c2(scans=100, points=20000, manifold=True, verbose=False):
+    """The C2-style run; returns a summary dict (also used by bench.py)."""
+    a = argparse.Namespace(scans=scans, points=points, no_manifold=not manifold)
     rng = np.random.default_rng(11)
     dt = 0.1
     gt = []
@@ -78,7 +74,7 @@ def main():
             stages.setdefault(k, []).append(v)
     med = {k: float(np.median(v)) for k, v in stages.items()}
     mean = {k: float(np.mean(v)) for k, v in stages.items()}
-    if "--verbose" in sys.argv:
+    if verbose:
         for f, e in zip(res.frames, err):
             s = f.solve
             if s is not None:
@@ -88,12 +84,29 @@ def main():
                       f"eig {s.smallest_feature_eigenvalue:.3g} cost {s.cost_trace[0]:.4g}->{s.final_cost:.4g}")
     held = sum(f.held for f in res.frames)
     corr = np.median([f.solve.correspondence_count for f in res.frames[1:]])
-    print(f"{'features only' if a.no_manifold else 'features + wheel manifold rows'}: "
-          f"{a.scans} scans x ~{a.points} features: {wall / a.scans * 1e3:.1f} ms/scan wall "
+    return {"scans": a.scans, "features_per_scan": a.points, "manifold_rows": not a.no_manifold,
+            "ms_per_scan_wall": wall / a.scans * 1e3, "stage_median_ms": med,
+            "stage_mean_ms": mean, "median_correspondences": float(corr), "held": int(held),
+            "ate_rmse_cm": float(np.sqrt(np.mean(err ** 2)) * 100),
+            "ate_max_cm": float(err.max() * 100), "terrain_centres": res.terrain.num_centers()}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--scans", type=int, default=100)
+    ap.add_argument("--points", type=int, default=20000)
+    ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--no-manifold", action="store_true")
+    a = ap.parse_args()
+    r = run_c2(a.scans, a.points, not a.no_manifold, a.verbose)
+    med, mean = r["stage_median_ms"], r["stage_mean_ms"]
+    print(f"{'features + wheel manifold rows' if r['manifold_rows'] else 'features only'}: "
+          f"{r['scans']} scans x ~{r['features_per_scan']} features: "
+          f"{r['ms_per_scan_wall']:.1f} ms/scan wall "
           f"(median / mean stage ms: {', '.join(f'{k} {v:.2f}/{mean[k]:.2f}' for k, v in med.items())}); "
-          f"median correspondences {corr:.0f}; held {held}; "
-          f"ATE rmse {np.sqrt(np.mean(err ** 2)) * 100:.2f} cm, max {err.max() * 100:.2f} cm; "
-          f"terrain centres {res.terrain.num_centers()}", flush=True)
+          f"median correspondences {r['median_correspondences']:.0f}; held {r['held']}; "
+          f"ATE rmse {r['ate_rmse_cm']:.2f} cm, max {r['ate_max_cm']:.2f} cm; "
+          f"terrain centres {r['terrain_centres']}", flush=True)
 
 
 if __name__ == "__main__":
