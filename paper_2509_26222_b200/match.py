@@ -18,7 +18,7 @@ import numpy as np
 from . import _abi
 from ._abi import InvalidArgument, NormalEqC, check
 from .kinematics import NormalEq
-from .terrain import Context, _col, _is_dev, _mem, _ptr
+from .terrain import Context, _col, _is_dev, _mem, _ptr, torch
 
 EDGE, PLANAR, GROUND = 0, 1, 2  # FeatureKind (types.hpp:36)
 
@@ -134,21 +134,29 @@ class LocalMap:
         return self.size() == 0
 
 
-def build_correspondences(points, kinds, R, t, local_map: LocalMap,
-                          config: MatchConfig | None = None) -> Correspondences:
-    """scan_matcher.cpp:44-183 at the guess pose (R, t)."""
+def associate(points, kinds, R, t, local_map: LocalMap, config: MatchConfig | None = None) -> int:
+    """scan_matcher.cpp:44-183 at the guess pose (R, t), keeping the
+    correspondences on the device (feature_normal_eq reads them); returns
+    their count. `points` may be (n, 3) numpy or a tuple of three contiguous
+    CUDA tensors (x, y, z) that stay resident across calls."""
     cfg = (config or MatchConfig())._c()
-    px, py, pz = _soa3(points)
+    px, py, pz = points if isinstance(points, tuple) else _soa3(points)
     kd = _u8(kinds, px)
     if len(kd) != len(px):
         raise InvalidArgument("points and kinds differ in length")
     Rm, tv = _pose(R, t)
-    lib = _abi.load()
     cnt = C.c_size_t()
-    check(lib.tlg_build_correspondences(local_map.handle, _ptr(px), _ptr(py), _ptr(pz), _ptr(kd),
-                                        len(px), _mem(px), _ptr(Rm), _ptr(tv), C.byref(cfg),
-                                        C.byref(cnt)))
-    n = cnt.value
+    check(_abi.load().tlg_build_correspondences(local_map.handle, _ptr(px), _ptr(py), _ptr(pz),
+                                                _ptr(kd), len(px), _mem(px), _ptr(Rm), _ptr(tv),
+                                                C.byref(cfg), C.byref(cnt)))
+    return cnt.value
+
+
+def build_correspondences(points, kinds, R, t, local_map: LocalMap,
+                          config: MatchConfig | None = None) -> Correspondences:
+    """scan_matcher.cpp:44-183 at the guess pose (R, t)."""
+    lib = _abi.load()
+    n = associate(points, kinds, R, t, local_map, config)
     out = Correspondences(np.empty(n, dtype=np.int32), np.empty(n, dtype=np.uint32),
                           np.empty((n, 7)), np.empty(n), np.empty(n, dtype=np.int32),
                           np.empty(n), np.empty(n))
@@ -301,13 +309,19 @@ def lm_solve(R0, t0, points, kinds, local_map: LocalMap, config: SolverConfig | 
             raise _abi.TerralioError("nothing to optimize")
         return ne, feat
 
+    # the scan stays resident on the device across the re-associations
+    scan_pts, scan_kinds = points, kinds
+    if torch is not None and torch.cuda.is_available() and not _is_dev(points):
+        P = np.asarray(points, dtype=np.float64).reshape(-1, 3)
+        scan_pts = tuple(torch.from_numpy(np.ascontiguousarray(P[:, j])).cuda() for j in range(3))
+        scan_kinds = torch.from_numpy(np.ascontiguousarray(np.asarray(kinds, dtype=np.uint8))).cuda()
     mu = cfg.lm_init_damping
     rejects = 0
     for _ in range(cfg.lm_max_iters):
         rep.outer_iterations += 1
-        corr = build_correspondences(points, kinds, R, t, local_map, cfg)
-        rep.correspondence_count = len(corr)
-        if len(corr) < cfg.min_correspondences:
+        ncorr = associate(scan_pts, scan_kinds, R, t, local_map, cfg)
+        rep.correspondence_count = ncorr
+        if ncorr < cfg.min_correspondences:
             rep.degenerate = True
             break
         ne, feat = total_cost(R, t)
