@@ -57,10 +57,14 @@ def staircase(x):
 
 
 def so3_exp(w):
+    """Rodrigues (so3.cpp:8-27), first-order Taylor below theta^2 = 1e-16."""
     w = np.asarray(w, dtype=np.float64)
-    th = np.linalg.norm(w)
+    th2 = float(w @ w)
     K = np.array([[0, -w[2], w[1]], [w[2], 0, -w[0]], [-w[1], w[0], 0]])
-    return np.eye(3) + math.sin(th) / th * K + (1 - math.cos(th)) / th ** 2 * (K @ K)
+    if th2 < 1e-16:
+        return np.eye(3) + K
+    th = math.sqrt(th2)
+    return np.eye(3) + math.sin(th) / th * K + (1 - math.cos(th)) / th2 * (K @ K)
 
 
 def load_peaks():
