@@ -57,12 +57,12 @@ def staircase(x):
 
 
 def so3_exp(w):
-    """Rodrigues (so3.cpp:8-27), first-order Taylor below theta^2 = 1e-16."""
+    """Rodrigues (so3.cpp:16-27), second-order Taylor below theta^2 = 1e-16."""
     w = np.asarray(w, dtype=np.float64)
     th2 = float(w @ w)
     K = np.array([[0, -w[2], w[1]], [w[2], 0, -w[0]], [-w[1], w[0], 0]])
     if th2 < 1e-16:
-        return np.eye(3) + K
+        return np.eye(3) + K + 0.5 * (K @ K)
     th = math.sqrt(th2)
     return np.eye(3) + math.sin(th) / th * K + (1 - math.cos(th)) / th2 * (K @ K)
 
