@@ -89,7 +89,10 @@ typedef struct tlg_model tlg_model;
 /* ---- library / context ---------------------------------------------------- */
 int tlg_abi_version(void);
 const char* tlg_last_error(void);
-/* device = CUDA ordinal; stream = cudaStream_t or NULL for a private stream. */
+/* device = CUDA ordinal; stream = the cudaStream_t every call of this context
+ * is ordered on (NULL = the legacy default stream). Device inputs must be
+ * ready on that stream; results are ready on it when a call returns with
+ * host outputs, and ordered on it otherwise. */
 tlg_status tlg_ctx_create(int device, void* stream, tlg_ctx** out);
 tlg_status tlg_ctx_destroy(tlg_ctx* ctx);
 tlg_status tlg_ctx_set_stream(tlg_ctx* ctx, void* stream);

@@ -132,16 +132,10 @@ tlg_status tlg_ctx_create(int device, void* stream, tlg_ctx** out) {
     auto* c = new tlg_ctx();
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
-    if (stream) {
-      c->stream = static_cast<cudaStream_t>(stream);
-    } else {
-      cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
-      if (e != cudaSuccess) {
-        delete c;
-        throw_cuda(e, "cudaStreamCreate", __FILE__, __LINE__);
-      }
-      c->own_stream = true;
-    }
+    // NULL is the legacy default stream (torch's default stream), not a
+    // private one: device inputs written by the caller on that stream are
+    // then ordered before the library's reads without an extra event.
+    c->stream = static_cast<cudaStream_t>(stream);
     *out = c;
   });
 }
@@ -157,7 +151,6 @@ tlg_status tlg_ctx_destroy(tlg_ctx* ctx) {
         if (e) cudaEventDestroy(e);
       cudaStreamDestroy(ctx->copy_stream);
     }
-    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
 }
@@ -166,8 +159,6 @@ tlg_status tlg_ctx_set_stream(tlg_ctx* ctx, void* stream) {
   return guard([&] {
     check_ptr(ctx, "ctx");
     ctx->sync();
-    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
-    ctx->own_stream = false;
     ctx->stream = static_cast<cudaStream_t>(stream);
   });
 }

@@ -118,7 +118,6 @@ struct tlg_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // H2D slices overlapping compute (manifold rows)
   cudaEvent_t copy_ev[9] = {};
-  bool own_stream = false;
   uint64_t launches = 0;
   int num_sms = 148;
   tlg::DBuf<unsigned char> slots[tlg::S_NUM_SLOTS];

@@ -18,7 +18,7 @@ import numpy as np
 from . import _abi
 from ._abi import InvalidArgument, NormalEqC, check
 from .kinematics import NormalEq
-from .terrain import Context, _col, _is_dev, _mem, _ptr, torch
+from .terrain import Context, _CtxBound, _col, _is_dev, _mem, _ptr, torch
 
 EDGE, PLANAR, GROUND = 0, 1, 2  # FeatureKind (types.hpp:36)
 
@@ -88,7 +88,7 @@ def _pose(R, t):
             np.ascontiguousarray(np.asarray(t, dtype=np.float64).reshape(3)))
 
 
-class LocalMap:
+class LocalMap(_CtxBound):
     """local_map.hpp:17-50."""
 
     def __init__(self, voxel_size: float = 0.1, window: int = 20, ctx: Context | None = None):
@@ -100,9 +100,9 @@ class LocalMap:
 
     def __del__(self):
         try:
-            if getattr(self, "handle", None):
-                _abi.load().tlg_map_destroy(self.handle)
-                self.handle = None
+            if self._h:
+                _abi.load().tlg_map_destroy(self._h)
+                self._h = None
         except Exception:
             pass
 
@@ -140,7 +140,7 @@ def associate(points, kinds, R, t, local_map: LocalMap, config: MatchConfig | No
     their count. `points` may be (n, 3) numpy or a tuple of three contiguous
     CUDA tensors (x, y, z) that stay resident across calls."""
     cfg = (config or MatchConfig())._c()
-    px, py, pz = points if isinstance(points, tuple) else _soa3(points)
+    px, py, pz = points if isinstance(points, (tuple, list)) else _soa3(points)
     kd = _u8(kinds, px)
     if len(kd) != len(px):
         raise InvalidArgument("points and kinds differ in length")
@@ -311,10 +311,14 @@ def lm_solve(R0, t0, points, kinds, local_map: LocalMap, config: SolverConfig | 
 
     # the scan stays resident on the device across the re-associations
     scan_pts, scan_kinds = points, kinds
-    if torch is not None and torch.cuda.is_available() and not _is_dev(points):
+    on_dev = _is_dev(points) or (isinstance(points, (tuple, list)) and _is_dev(points[0]))
+    if torch is not None and torch.cuda.is_available() and not on_dev:
+        dev = f"cuda:{ctx.device}"
         P = np.asarray(points, dtype=np.float64).reshape(-1, 3)
-        scan_pts = tuple(torch.from_numpy(np.ascontiguousarray(P[:, j])).cuda() for j in range(3))
-        scan_kinds = torch.from_numpy(np.ascontiguousarray(np.asarray(kinds, dtype=np.uint8))).cuda()
+        scan_pts = tuple(torch.from_numpy(np.ascontiguousarray(P[:, j])).to(dev)
+                         for j in range(3))
+        scan_kinds = torch.from_numpy(
+            np.ascontiguousarray(np.asarray(kinds, dtype=np.uint8))).to(dev)
     mu = cfg.lm_init_damping
     rejects = 0
     for _ in range(cfg.lm_max_iters):

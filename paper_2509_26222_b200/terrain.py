@@ -123,11 +123,32 @@ class Context:
     def __init__(self, device: int = 0, stream: int | None = None):
         lib = _abi.load()
         h = C.c_void_p()
-        if stream is None and torch is not None and torch.cuda.is_available():
+        self._follow = stream is None and torch is not None and torch.cuda.is_available()
+        if self._follow:
             stream = torch.cuda.current_stream(device).cuda_stream
+        # 0 = the legacy default stream (= torch's default stream), never a
+        # private one, so inputs torch wrote are ordered before our reads
         check(lib.tlg_ctx_create(int(device), C.c_void_p(stream or 0), C.byref(h)))
-        self.handle = h
+        self._handle = h
+        self._stream = int(stream or 0)
         self.device = device
+
+    @property
+    def handle(self):
+        """The tlg_ctx, re-pointed at torch's current stream whenever that
+        changed (so calls inside `with torch.cuda.stream(s)` order on s)."""
+        if self._follow:
+            cur = torch.cuda.current_stream(self.device).cuda_stream
+            if cur != self._stream:
+                check(_abi.load().tlg_ctx_set_stream(self._handle, C.c_void_p(cur)))
+                self._stream = cur
+        return self._handle
+
+    def set_stream(self, stream: int) -> None:
+        """Pins the context to a raw cudaStream_t (stops following torch)."""
+        self._follow = False
+        check(_abi.load().tlg_ctx_set_stream(self._handle, C.c_void_p(int(stream))))
+        self._stream = int(stream)
 
     @classmethod
     def default(cls, device: int = 0) -> "Context":
@@ -143,8 +164,8 @@ class Context:
 
     def __del__(self):
         try:
-            if getattr(self, "handle", None):
-                _abi.load().tlg_ctx_destroy(self.handle)
+            if getattr(self, "_handle", None):
+                _abi.load().tlg_ctx_destroy(self._handle)
         except Exception:
             pass
 
@@ -249,7 +270,23 @@ def select_centers(obs: TerrainObservation, roi: Rect, mesh_resolution: float,
 
 
 # ---------------------------------------------------------------------------
-class TerrainModel:
+class _CtxBound:
+    """A library handle bound to a Context: reading `handle` first re-points
+    the context at torch's current stream (Context.handle)."""
+
+    _h = None
+
+    @property
+    def handle(self):
+        self.ctx.handle
+        return self._h
+
+    @handle.setter
+    def handle(self, h):
+        self._h = h
+
+
+class TerrainModel(_CtxBound):
     """terrain_model.hpp:28-97 on the device. Move-only in the reference;
     here a handle that owns the device state."""
 
@@ -271,9 +308,9 @@ class TerrainModel:
 
     def __del__(self):
         try:
-            if getattr(self, "handle", None):
-                _abi.load().tlg_model_destroy(self.handle)
-                self.handle = None
+            if self._h:
+                _abi.load().tlg_model_destroy(self._h)
+                self._h = None
         except Exception:
             pass
 
