@@ -15,8 +15,37 @@ import numpy as np
 
 ODIR = Path(__file__).resolve().parent
 LIB = ODIR / "_build" / "liboracle.so"
+# The reference itself, compiled from /root/reference by `make -C oracle ref`
+# (oracle/ref_capi.cpp exposes it through the same orc_* entry points).
+REF_LIB = ODIR / "_ref" / "libterralio_ref.so"
+REFERENCE_SRC = Path("/root/reference/proj/core/src")
+BACKEND = "port"
+_REF_MODULE = None
+
+
+def reference():
+    """This module's API bound to the compiled reference (oracle/_ref), or None
+    when it is not built here and cannot be (no /root/reference). Functions
+    the reference keeps file-local raise OracleError(UNSUPPORTED)."""
+    global _REF_MODULE
+    if _REF_MODULE is None:
+        if not REF_LIB.exists():
+            if not REFERENCE_SRC.exists():
+                return None
+            subprocess.run(["make", "-C", str(ODIR), "-j8", "ref"], check=True,
+                           capture_output=True)
+        import importlib.util
+        spec = importlib.util.spec_from_file_location("oracle_reference", __file__)
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        mod.LIB = REF_LIB
+        mod.BACKEND = "reference"
+        mod._REF_MODULE = mod
+        _REF_MODULE = mod
+    return _REF_MODULE
 
 OK, INVALID_ARGUMENT, DOMAIN_ERROR, NO_SUPPORTED_CENTERS, RUNTIME_ERROR = 0, 1, 2, 3, 4
+UNSUPPORTED = 9
 
 
 class OracleError(RuntimeError):
@@ -42,7 +71,7 @@ _lib = None
 def load():
     global _lib
     if _lib is None:
-        if not LIB.exists():
+        if not LIB.exists() and BACKEND == "port":
             subprocess.run(["make", "-C", str(ODIR)], check=True, capture_output=True)
         _lib = C.CDLL(str(LIB))
         _lib.orc_last_error.restype = C.c_char_p

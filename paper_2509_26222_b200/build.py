@@ -73,12 +73,19 @@ def build_gpu(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+REFERENCE = Path("/root/reference/proj")
+
+
 def build_oracle(force: bool = False) -> Path:
+    """The CPU checkers (test infrastructure): the plain-C++ restatement, and,
+    where /root/reference exists (the build container; the GPU box only gets
+    the prebuilt files), the reference itself compiled into oracle/_ref."""
     odir = ROOT / "oracle"
-    args = ["make", "-C", str(odir)]
     if force:
-        _run(["make", "-C", str(odir), "clean"])
-    _run(args)
+        _run(["make", "-C", str(odir), "clean", "clean-ref"])
+    _run(["make", "-C", str(odir)])
+    if REFERENCE.exists():
+        _run(["make", "-C", str(odir), f"-j{os.cpu_count() or 4}", "ref"])
     return odir / "_build" / "liboracle.so"
 
 
