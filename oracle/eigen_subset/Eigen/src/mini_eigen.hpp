@@ -31,6 +31,7 @@
 #include <initializer_list>
 #include <limits>
 #include <stdexcept>
+#include <thread>
 #include <type_traits>
 #include <utility>
 #include <vector>
@@ -770,8 +771,35 @@ auto operator/(const X& a, const Y& b) {
   return a.cwiseQuotient(b);
 }
 
-// Matrix product: entry (i, j) = sum_k a(i,k) b(k,j), k ascending (j-k-i
-// loop order, one pass over each column of a per k).
+// Matrix product: entry (i, j) = a(i,0) b(0,j) + a(i,1) b(1,j) + ..., k
+// ascending, for every shape (so the result does not depend on the layout
+// path taken or on the thread count). Column-major left operands run as
+// column axpys (vectorisable without reassociation), transposed ones as
+// contiguous dots; large products split output columns (or, for one column,
+// rows) over std::thread workers — test-infrastructure speed only.
+namespace internal {
+inline unsigned product_threads(double work) {
+  if (work < 4e6) return 1;
+  const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
+  return static_cast<unsigned>(std::min<double>(hc, std::max(1.0, work / 2e6)));
+}
+template <class F>
+void parallel_range(Index n, unsigned threads, F f) {
+  if (threads <= 1 || n < 2) {
+    f(Index(0), n);
+    return;
+  }
+  threads = static_cast<unsigned>(std::min<Index>(threads, n));
+  std::vector<std::thread> pool;
+  const Index chunk = (n + threads - 1) / threads;
+  for (unsigned w = 0; w < threads; ++w) {
+    const Index b = w * chunk, e = std::min(n, b + chunk);
+    if (b < e) pool.emplace_back(f, b, e);
+  }
+  for (auto& t : pool) t.join();
+}
+}  // namespace internal
+
 template <DenseExpr X, DenseExpr Y>
 auto operator*(const X& a, const Y& b) {
   if constexpr (X::IsArray && Y::IsArray) {
@@ -780,16 +808,46 @@ auto operator*(const X& a, const Y& b) {
     if (a.cols() != b.rows()) throw std::logic_error("mini-eigen: product size mismatch");
     internal::prod_t<X, Y> out(a.rows(), b.cols());
     const Index n = a.rows(), m = b.cols(), kk = a.cols();
-    for (Index j = 0; j < m; ++j) {
-      double* oc = &out.coeffRef(0, j);
-      for (Index k = 0; k < kk; ++k) {
-        const double bkj = b.coeff(k, j);
-        if (k == 0) {
-          for (Index i = 0; i < n; ++i) oc[i] = a.coeff(i, 0) * bkj;
-        } else {
-          for (Index i = 0; i < n; ++i) oc[i] += a.coeff(i, k) * bkj;
+    if (n == 0 || m == 0 || kk == 0) return out;
+    const double* ap = a.p();
+    const Index ars = a.rstr(), acs = a.cstr();
+    const double* bp = b.p();
+    const Index brs = b.rstr(), bcs = b.cstr();
+    double* op = out.data();  // column-major, ld = n
+    const unsigned th = internal::product_threads(double(n) * double(m) * double(kk));
+    if (ars == 1) {
+      auto cols = [&](Index j0, Index j1, Index i0, Index i1) {
+        for (Index j = j0; j < j1; ++j) {
+          double* oc = op + j * n;
+          for (Index k = 0; k < kk; ++k) {
+            const double bkj = bp[k * brs + j * bcs];
+            const double* ac = ap + k * acs;
+            if (k == 0)
+              for (Index i = i0; i < i1; ++i) oc[i] = ac[i] * bkj;
+            else
+              for (Index i = i0; i < i1; ++i) oc[i] += ac[i] * bkj;
+          }
         }
-      }
+      };
+      if (m == 1)
+        internal::parallel_range(n, th, [&](Index i0, Index i1) { cols(0, 1, i0, i1); });
+      else
+        internal::parallel_range(m, th, [&](Index j0, Index j1) { cols(j0, j1, 0, n); });
+    } else {
+      auto rows = [&](Index j0, Index j1, Index i0, Index i1) {
+        for (Index j = j0; j < j1; ++j)
+          for (Index i = i0; i < i1; ++i) {
+            const double* ar = ap + i * ars;
+            const double* bc = bp + j * bcs;
+            double s = ar[0] * bc[0];
+            for (Index k = 1; k < kk; ++k) s += ar[k * acs] * bc[k * brs];
+            op[i + j * n] = s;
+          }
+      };
+      if (m == 1)
+        internal::parallel_range(n, th, [&](Index i0, Index i1) { rows(0, 1, i0, i1); });
+      else
+        internal::parallel_range(m, th, [&](Index j0, Index j1) { rows(j0, j1, 0, n); });
     }
     return out;
   }

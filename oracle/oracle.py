@@ -325,6 +325,13 @@ class Model:
         load().orc_model_block_members(self.h, b, _p(out))
         return out
 
+    def set_block_info_inverse(self, b, a):
+        """Reference backend only (snapshot round trip)."""
+        a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+        f = load().orc_model_set_block_info_inverse
+        f.argtypes = [C.c_void_p, C.c_uint, C.c_void_p]
+        _chk(f(self.h, int(b), a.ctypes.data_as(C.c_void_p)))
+
     def block_info_inverse(self, b):
         n = load().orc_model_block_size(self.h, b)
         out = np.empty(n * n)

@@ -29,6 +29,10 @@
 #include <thread>
 #include <unistd.h>
 #include <vector>
+#include <chrono>
+#include <deque>
+#include <span>
+#include <unordered_set>
 
 #include "terralio/eval/metrics.hpp"
 #include "terralio/grid_index.hpp"
@@ -301,6 +305,34 @@ int orc_model_set_weights(void* m, const double* w) {
       std::fstream f(path, std::ios::in | std::ios::out | std::ios::binary);
       f.seekp(16 + static_cast<std::streamoff>(16 * n));
       f.write(reinterpret_cast<const char*>(w), static_cast<std::streamsize>(8 * n));
+    }
+    r->m = TerrainModel::load(path);
+    std::remove(path.c_str());
+    r->reindex();
+  });
+}
+// replace block b's info_inv (column-major bn x bn; its lower triangle is
+// what the snapshot stores, row-major, snapshot.cpp:13) by a round trip
+int orc_model_set_block_info_inverse(void* m, unsigned b, const double* a) {
+  return guarded([&] {
+    RefModel* r = M(m);
+    const size_t n = r->m.num_centers();
+    if (b >= r->m.num_blocks()) throw std::invalid_argument("block id out of range");
+    std::streamoff off = 16 + static_cast<std::streamoff>(28 * n);
+    for (unsigned q = 0; q < b; ++q) {
+      const auto bn = static_cast<std::streamoff>(r->m.block_members(q).size());
+      off += 8 * bn * (bn + 1) / 2;
+    }
+    const size_t bn = r->m.block_members(b).size();
+    std::vector<double> tri;
+    for (size_t i = 0; i < bn; ++i)
+      for (size_t j = 0; j <= i; ++j) tri.push_back(a[i + j * bn]);
+    const std::string path = temp_path("ii");
+    r->m.save(path);
+    {
+      std::fstream f(path, std::ios::in | std::ios::out | std::ios::binary);
+      f.seekp(off);
+      f.write(reinterpret_cast<const char*>(tri.data()), static_cast<std::streamsize>(8 * tri.size()));
     }
     r->m = TerrainModel::load(path);
     std::remove(path.c_str());
@@ -653,6 +685,289 @@ void orc_feature_normal_eq(size_t nc, const int* ckind, const double* ps, const 
     pack_ne(ev.jacobian, ev.residual, ev.cost, static_cast<double>(ev.feature_rows), ne29);
   } catch (const std::runtime_error&) {
   }
+}
+
+// ---- reference simulator bundles, lm_solve and the odometry loop --------------
+// (pose-level parity: scan_matcher.cpp:257-358, pipeline.cpp:196-300)
+
+// sim::simulate on a stock scene (scene.cpp:151-168) with an optional
+// ScanConfig override (azimuth x elevation rays), kept to the first scans.
+void* ref_sim_new(const char* scene, unsigned long long seed, int az, int el, long max_scans) {
+  try {
+    sim::Scene sc = sim::stock_scene(scene);
+    if (az > 0) sc.scan.azimuth_steps = az;
+    if (el > 0) sc.scan.elevation_steps = el;
+    auto* b = new sim::SequenceBundle(sim::simulate(sc, seed));
+    if (max_scans > 0 && b->scans.size() > static_cast<size_t>(max_scans)) {
+      b->scans.resize(static_cast<size_t>(max_scans));
+      b->gt_poses.resize(static_cast<size_t>(max_scans));
+    }
+    return b;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+void ref_sim_free(void* b) { delete static_cast<sim::SequenceBundle*>(b); }
+size_t ref_sim_num_scans(void* b) { return static_cast<sim::SequenceBundle*>(b)->scans.size(); }
+// returns the point count; fills up to cap
+size_t ref_sim_scan(void* b, size_t k, double* px, double* py, double* pz, unsigned char* kind, int* label,
+                    size_t cap) {
+  const auto& pts = static_cast<sim::SequenceBundle*>(b)->scans[k].points;
+  for (size_t i = 0; i < pts.size() && i < cap; ++i) {
+    px[i] = pts[i].p.x();
+    py[i] = pts[i].p.y();
+    pz[i] = pts[i].p.z();
+    kind[i] = static_cast<unsigned char>(pts[i].kind);
+    label[i] = pts[i].label;
+  }
+  return pts.size();
+}
+void ref_sim_gt(void* b, size_t k, double* R9, double* t3, double* ts) {
+  const TimedPose& p = static_cast<sim::SequenceBundle*>(b)->gt_poses[k];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) R9[3 * i + j] = p.rotation(i, j);
+  for (int i = 0; i < 3; ++i) t3[i] = p.translation(i);
+  *ts = p.timestamp;
+}
+void ref_sim_roi(void* b, double* roi4) {
+  const Rect& r = static_cast<sim::SequenceBundle*>(b)->scene.terrain_roi;
+  roi4[0] = r.min.x();
+  roi4[1] = r.min.y();
+  roi4[2] = r.max.x();
+  roi4[3] = r.max.y();
+}
+double ref_sim_wheel_radius(void* b) { return static_cast<sim::SequenceBundle*>(b)->robot.wheel_radius; }
+
+namespace {
+// pipeline.cpp:176-186 (file-local there)
+const JointConfig* nearest_joints_(const std::vector<JointConfig>& joints, double t) {
+  if (joints.empty()) return nullptr;
+  const auto it = std::lower_bound(joints.begin(), joints.end(), t,
+                                   [](const JointConfig& j, double v) { return j.timestamp < v; });
+  if (it == joints.begin()) return &*it;
+  if (it == joints.end()) return &joints.back();
+  return (it->timestamp - t < t - std::prev(it)->timestamp) ? &*it : &*std::prev(it);
+}
+// pipeline.cpp:164-174
+std::span<const ImuSample> imu_window_(const std::vector<ImuSample>& imu, double t0, double t1) {
+  const auto begin = std::lower_bound(imu.begin(), imu.end(), t0,
+                                      [](const ImuSample& s, double t) { return s.timestamp <= t; });
+  const auto end = std::upper_bound(begin, imu.end(), t1,
+                                    [](double t, const ImuSample& s) { return t < s.timestamp - 1e-9; });
+  return {&*begin, static_cast<std::size_t>(end - begin)};
+}
+// pipeline.cpp:150-170
+terrain::TerrainObservation select_ground_points_(const FeatureCloud& scan, const Mat3& R, const Vec3& t,
+                                                  const Rect& roi, const pipeline::RunConfig& cfg) {
+  terrain::TerrainObservation obs;
+  std::unordered_set<std::int64_t> voxels;
+  for (const FeaturePoint& f : scan.points) {
+    if (f.kind != FeatureKind::Ground) continue;
+    const Vec3 p = R * f.p + t;
+    const Vec2 xy = p.head<2>();
+    if (!roi.contains(xy)) continue;
+    if ((xy - t.head<2>()).norm() > cfg.ground_radius) continue;
+    const auto vx = static_cast<std::int64_t>(std::floor(xy.x() / cfg.ground_voxel));
+    const auto vy = static_cast<std::int64_t>(std::floor(xy.y() / cfg.ground_voxel));
+    if (!voxels.insert((vx << 21) ^ (vy & ((1 << 21) - 1))).second) continue;
+    obs.xy.push_back(xy);
+    obs.z.push_back(p.z());
+    if (obs.xy.size() >= cfg.ground_max_points) break;
+  }
+  return obs;
+}
+void put_pose(double* out, const Mat3& R, const Vec3& t) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) out[3 * i + j] = R(i, j);
+  for (int i = 0; i < 3; ++i) out[9 + i] = t(i);
+}
+}  // namespace
+
+// Wheel-centre lever arms (base frame, leg_model.cpp:10-21) from the joint
+// sample nearest t (pipeline.cpp:176-186); returns 0 when there is none.
+int ref_sim_wheel_arms(void* bp, double t, double* hL, double* hR) {
+  auto* b = static_cast<sim::SequenceBundle*>(bp);
+  const JointConfig* j = nearest_joints_(b->joints, t);
+  if (!j) return 0;
+  for (const kin::Side side : {kin::Side::Left, kin::Side::Right}) {
+    const kin::LegChain& chain = b->robot.chain(side);
+    const int off = b->robot.joint_offset(side);
+    const std::span<const double> q(j->angles.data() + off, static_cast<std::size_t>(chain.joint_count()));
+    const Vec3 h = kin::chain_end_position(chain, q);
+    double* o = side == kin::Side::Left ? hL : hR;
+    for (int i = 0; i < 3; ++i) o[i] = h(i);
+  }
+  return 1;
+}
+
+// The odometry loop of pipeline.cpp:196-300 with per-frame records, in one
+// of two modes: mode 1 calls pipeline::run_odometry itself (poses, wall ms
+// and the solve/terrain reports come from its RunResult); mode 0 runs the
+// same loop restated here from the reference's public pieces, additionally
+// recording the predicted pose and the lever arms each lm_solve saw (what a
+// lock-step comparison needs). `config_json` is RunConfig::from_json text.
+// Per frame k: poses[12k] = (R row-major, t) solved, preds[12k] predicted,
+// arms[7k] = hL, hR, has_joints; ints[8k] = held, inserted, converged,
+// failed, degenerate, outer_iterations, accepted_steps, correspondences;
+// terr[4k] = active_blocks, active_centers, born_centers, rejected;
+// dbl[3k] = final_cost, wall_ms, smallest_feature_eigenvalue.
+int ref_odometry(void* bp, const char* config_json, int mode, double* poses, double* preds, double* arms,
+                 int* ints, double* terr, double* dbl) {
+  return guarded([&] {
+    const auto& bundle = *static_cast<sim::SequenceBundle*>(bp);
+    const pipeline::RunConfig config = pipeline::RunConfig::from_json(config_json);
+    const size_t nscan = bundle.scans.size();
+    auto record = [&](size_t k, const pipeline::FrameDiagnostics& d, const Mat3& R, const Vec3& t) {
+      put_pose(poses + 12 * k, R, t);
+      int* o = ints + 8 * k;
+      o[0] = d.held;
+      o[1] = d.inserted;
+      o[2] = d.solve.converged;
+      o[3] = d.solve.failed;
+      o[4] = d.solve.degenerate;
+      o[5] = d.solve.outer_iterations;
+      o[6] = d.solve.accepted_steps;
+      o[7] = static_cast<int>(d.solve.correspondence_count);
+      terr[4 * k] = static_cast<double>(d.terrain.active_blocks);
+      terr[4 * k + 1] = static_cast<double>(d.terrain.active_centers);
+      terr[4 * k + 2] = static_cast<double>(d.terrain.born_centers);
+      terr[4 * k + 3] = d.terrain.rejected;
+      dbl[3 * k] = d.solve.final_cost;
+      dbl[3 * k + 1] = d.wall_ms;
+      dbl[3 * k + 2] = d.solve.smallest_feature_eigenvalue;
+    };
+    if (mode == 1) {
+      const pipeline::RunResult res = pipeline::run_odometry(bundle, config);
+      for (size_t k = 0; k < nscan; ++k)
+        record(k, res.frames[k], res.trajectory[k].rotation, res.trajectory[k].translation);
+      return;
+    }
+    set_worker_count(static_cast<std::size_t>(config.workers));
+    terrain::KernelParams kernel = config.kernel;
+    kernel.finalize();
+    terrain::CenterSet centers;
+    centers.mesh_resolution = config.mesh_resolution;
+    centers.accept_radius = config.accept_radius;
+    centers.accept_count = config.accept_count;
+    centers.roi = bundle.scene.terrain_roi;
+    terrain::TerrainModel model(kernel, centers);
+    match::LocalMap map(config.map);
+    RobotState state;
+    state.rotation = bundle.gt_poses.front().rotation;
+    state.translation = bundle.gt_poses.front().translation;
+    state.accel_bias = config.imu_biases.accel;
+    state.gyro_bias = config.imu_biases.gyro;
+    std::deque<double> cost_history;
+    for (size_t k = 0; k < nscan; ++k) {
+      const auto t_start = std::chrono::steady_clock::now();
+      const FeatureCloud& scan = bundle.scans[k];
+      const double t_k = bundle.gt_poses[k].timestamp;
+      pipeline::FrameDiagnostics diag;
+      diag.index = k;
+      diag.timestamp = t_k;
+      RobotState pred = state;
+      double* ar = arms + 7 * k;
+      std::fill(ar, ar + 7, 0.0);
+      if (k > 0) {
+        const double t_prev = bundle.gt_poses[k - 1].timestamp;
+        const double dt = t_k - t_prev;
+        if (config.use_imu) {
+          const auto window = imu_window_(bundle.imu, t_prev, t_k);
+          const auto delta = imu::preintegrate(window, t_prev, t_k, {state.accel_bias, state.gyro_bias});
+          pred = imu::predict_pose(state, delta);
+        } else {
+          pred.translation += state.velocity * dt;
+        }
+        match::ManifoldInputs manifold;
+        const JointConfig* joints = nearest_joints_(bundle.joints, t_k);
+        if (config.use_manifold && joints) {
+          manifold.joints = joints;
+          manifold.leg = &bundle.robot;
+          manifold.terrain = &model;
+          ref_sim_wheel_arms(bp, t_k, ar, ar + 3);
+          ar[6] = 1.0;
+        }
+        RobotState solved = match::lm_solve(pred, scan, map, manifold, config.solver, &diag.solve);
+        if (diag.solve.failed) {
+          solved = pred;
+          diag.held = true;
+        }
+        solved.velocity = (solved.translation - state.translation) / dt;
+        solved.accel_bias = state.accel_bias;
+        solved.gyro_bias = state.gyro_bias;
+        state = solved;
+      }
+      put_pose(preds + 12 * k, pred.rotation, pred.translation);
+      bool accept = !diag.held;
+      if (k > 0 && accept) {
+        const double rows = std::max<std::size_t>(diag.solve.correspondence_count, 1);
+        const double per_row = diag.solve.final_cost / rows;
+        if (cost_history.size() >= 5) {
+          std::vector<double> sorted(cost_history.begin(), cost_history.end());
+          std::nth_element(sorted.begin(), sorted.begin() + sorted.size() / 2, sorted.end());
+          const double med = sorted[sorted.size() / 2];
+          if (per_row > std::max(10.0 * med, 1e-6)) accept = false;
+        }
+        if (accept) {
+          cost_history.push_back(per_row);
+          if (cost_history.size() > 20) cost_history.pop_front();
+        }
+      }
+      diag.inserted = accept;
+      if (accept) {
+        map.insert(scan, state.rotation, state.translation);
+        const auto obs = select_ground_points_(scan, state.rotation, state.translation,
+                                               bundle.scene.terrain_roi, config);
+        if (!obs.xy.empty()) diag.terrain = model.recursive_update(obs);
+      }
+      diag.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+      record(k, diag, state.rotation, state.translation);
+    }
+  });
+}
+
+// One lm_solve on the reference (scan_matcher.cpp:257-358) with the wheel
+// rows of two fixed-link legs (lever arms hL, hR; nullptr = no manifold).
+// out: R9, t3; rep[8] = converged, failed, degenerate, outer, accepted,
+// correspondences, final_cost, smallest eigenvalue; trace (cap) costs.
+int ref_lm_solve(void* map, const double* px, const double* py, const double* pz, const unsigned char* kind,
+                 size_t n, const double* R0, const double* t0, void* model, const double* hL, const double* hR,
+                 double wheel_radius, const double* cfg, double lambda_M, double manifold_huber,
+                 double* Rout, double* tout, double* rep, double* trace, size_t cap, size_t* ntrace) {
+  return guarded([&] {
+    const FeatureCloud f = to_cloud(px, py, pz, kind, nullptr, n);
+    RobotState init;
+    init.rotation = to_m3(R0);
+    init.translation = Vec3(t0[0], t0[1], t0[2]);
+    match::SolverConfig sc = to_solver(cfg);
+    sc.lambda_manifold = lambda_M;
+    sc.manifold_huber_delta = manifold_huber;
+    JointConfig joints;
+    kin::LegModel leg;
+    match::ManifoldInputs mi;
+    if (model && hL && hR) {
+      leg.wheel_radius = wheel_radius;
+      leg.left = fixed_chain(hL[0], hL[1], hL[2]);
+      leg.right = fixed_chain(hR[0], hR[1], hR[2]);
+      mi = {&joints, &leg, &M(model)->m};
+    }
+    match::SolveReport r;
+    const RobotState out = match::lm_solve(init, f, *static_cast<match::LocalMap*>(map), mi, sc, &r);
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) Rout[3 * i + j] = out.rotation(i, j);
+    for (int i = 0; i < 3; ++i) tout[i] = out.translation(i);
+    rep[0] = r.converged;
+    rep[1] = r.failed;
+    rep[2] = r.degenerate;
+    rep[3] = r.outer_iterations;
+    rep[4] = r.accepted_steps;
+    rep[5] = static_cast<double>(r.correspondence_count);
+    rep[6] = r.final_cost;
+    rep[7] = r.smallest_feature_eigenvalue;
+    *ntrace = r.cost_trace.size();
+    for (size_t i = 0; i < r.cost_trace.size() && i < cap; ++i) trace[i] = r.cost_trace[i];
+  });
 }
 
 }  // extern "C"
