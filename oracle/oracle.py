@@ -529,3 +529,115 @@ def so3_exp(w):
     R = np.empty(9)
     load().orc_so3_exp(_p(_f64(w)), _p(R))
     return R.reshape(3, 3)
+
+
+# ---- reference-only: simulator bundles, lm_solve, the odometry loop ----------
+def _ref_fn(name, restype, argtypes):
+    f = getattr(load(), name)
+    f.restype = restype
+    f.argtypes = argtypes
+    return f
+
+
+class SimBundle:
+    """sim::simulate(stock_scene(scene), seed) (sensors.cpp:249-271) with an
+    optional azimuth x elevation ray override, first `max_scans` scans."""
+
+    def __init__(self, scene="staircase", seed=11, az=0, el=0, max_scans=0):
+        f = _ref_fn("ref_sim_new", C.c_void_p, [C.c_char_p, C.c_ulonglong, C.c_int, C.c_int, C.c_long])
+        self.h = f(scene.encode(), int(seed), int(az), int(el), int(max_scans))
+        if not self.h:
+            raise OracleError(RUNTIME_ERROR, load().orc_last_error().decode())
+
+    def __del__(self):
+        try:
+            _ref_fn("ref_sim_free", None, [C.c_void_p])(self.h)
+        except Exception:
+            pass
+
+    def num_scans(self):
+        return _ref_fn("ref_sim_num_scans", C.c_size_t, [C.c_void_p])(self.h)
+
+    def scan(self, k):
+        f = _ref_fn("ref_sim_scan", C.c_size_t, [C.c_void_p, C.c_size_t] + [C.c_void_p] * 5 + [C.c_size_t])
+        n = f(self.h, k, None, None, None, None, None, 0)
+        px, py, pz = np.empty(n), np.empty(n), np.empty(n)
+        kind, lab = np.empty(n, dtype=np.uint8), np.empty(n, dtype=np.int32)
+        f(self.h, k, _p(px), _p(py), _p(pz), _p(kind), _p(lab), n)
+        return np.stack([px, py, pz], 1), kind, lab
+
+    def gt(self, k):
+        R, t, ts = np.empty(9), np.empty(3), C.c_double()
+        _ref_fn("ref_sim_gt", None, [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p])(
+            self.h, k, _p(R), _p(t), C.byref(ts))
+        return R.reshape(3, 3), t, ts.value
+
+    def roi(self):
+        r = np.empty(4)
+        _ref_fn("ref_sim_roi", None, [C.c_void_p, C.c_void_p])(self.h, _p(r))
+        return r
+
+    def wheel_radius(self):
+        return _ref_fn("ref_sim_wheel_radius", C.c_double, [C.c_void_p])(self.h)
+
+    def wheel_arms(self, t):
+        hL, hR = np.empty(3), np.empty(3)
+        ok = _ref_fn("ref_sim_wheel_arms", C.c_int, [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p])(
+            self.h, float(t), _p(hL), _p(hR))
+        return (hL, hR) if ok else None
+
+
+def run_config_json(**kw):
+    """RunConfig JSON (pipeline.cpp:22-89); nested dicts for kernel/solver/map."""
+    import json
+    return json.dumps(kw)
+
+
+def odometry(bundle: SimBundle, config_json: str, mode=0):
+    """The reference odometry loop over a bundle (mode 1: pipeline::run_odometry
+    itself; mode 0: the same loop restated from its public pieces, also
+    recording predicted poses and the lever arms each lm_solve saw)."""
+    n = bundle.num_scans()
+    poses, preds, arms = np.zeros((n, 12)), np.zeros((n, 12)), np.zeros((n, 7))
+    ints, terr, dbl = np.zeros((n, 8), dtype=np.int32), np.zeros((n, 4)), np.zeros((n, 3))
+    f = _ref_fn("ref_odometry", C.c_int, [C.c_void_p, C.c_char_p, C.c_int] + [C.c_void_p] * 6)
+    _chk(f(bundle.h, config_json.encode(), int(mode), _p(poses), _p(preds), _p(arms), _p(ints), _p(terr),
+           _p(dbl)))
+    keys = ("held", "inserted", "converged", "failed", "degenerate", "outer_iterations",
+            "accepted_steps", "correspondences")
+    out = {k: ints[:, i].copy() for i, k in enumerate(keys)}
+    out.update(R=poses[:, :9].reshape(n, 3, 3), t=poses[:, 9:].copy(),
+               R_pred=preds[:, :9].reshape(n, 3, 3), t_pred=preds[:, 9:].copy(),
+               hL=arms[:, :3].copy(), hR=arms[:, 3:6].copy(), has_arms=arms[:, 6] > 0,
+               active_blocks=terr[:, 0].astype(int), active_centers=terr[:, 1].astype(int),
+               born_centers=terr[:, 2].astype(int), rejected=terr[:, 3] > 0,
+               final_cost=dbl[:, 0].copy(), wall_ms=dbl[:, 1].copy(), min_eig=dbl[:, 2].copy())
+    return out
+
+
+def lm_solve(local_map, P, kind, R0, t0, model=None, hL=None, hR=None, wheel_radius=0.0, cfg=None,
+             lambda_M=1.0, manifold_huber=0.05):
+    """match::lm_solve on the reference (scan_matcher.cpp:257-358)."""
+    P = _f64(P)
+    cols = [np.ascontiguousarray(P[:, j]) for j in range(3)]
+    kind = np.ascontiguousarray(np.asarray(kind, dtype=np.uint8))
+    R, t, rep, trace = np.empty(9), np.empty(3), np.empty(8), np.empty(256)
+    nt = C.c_size_t()
+    f = _ref_fn("ref_lm_solve", C.c_int,
+                [C.c_void_p] * 5 + [C.c_size_t] + [C.c_void_p] * 5 + [C.c_double, C.c_void_p, C.c_double,
+                                                                   C.c_double] + [C.c_void_p] * 4 +
+                [C.c_size_t, C.c_void_p])
+    _chk(f(local_map.h, _p(cols[0]), _p(cols[1]), _p(cols[2]), _p(kind), len(kind),
+           _p(_f64(R0).reshape(9)), _p(_f64(t0).reshape(3)), model.h if model is not None else None,
+           None if hL is None else _p(_f64(hL)), None if hR is None else _p(_f64(hR)), float(wheel_radius),
+           _p(_cfg_vec(cfg)), float(lambda_M), float(manifold_huber), _p(R), _p(t), _p(rep), _p(trace),
+           len(trace), C.byref(nt)))
+    keys = ("converged", "failed", "degenerate", "outer_iterations", "accepted_steps",
+            "correspondence_count", "final_cost", "smallest_feature_eigenvalue")
+    r = dict(zip(keys, rep.tolist()))
+    for k in ("converged", "failed", "degenerate"):
+        r[k] = bool(r[k])
+    for k in ("outer_iterations", "accepted_steps", "correspondence_count"):
+        r[k] = int(r[k])
+    r["cost_trace"] = trace[: min(nt.value, len(trace))].copy()
+    return R.reshape(3, 3), t, r
