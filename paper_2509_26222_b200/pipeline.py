@@ -55,12 +55,25 @@ class RunResult:
     local_map: M.LocalMap | None = None
 
 
+def _arms_at(lever_arms, k):
+    if lever_arms is None:
+        return None
+    if callable(lever_arms):
+        return lever_arms(k)
+    a = lever_arms if isinstance(lever_arms, (list, tuple)) else np.asarray(lever_arms)
+    if isinstance(a, np.ndarray) and a.ndim == 2:
+        return a
+    return None if a[k] is None else np.asarray(a[k], dtype=np.float64)
+
+
 def run_odometry(scans, kinds, timestamps, R_first, t_first, roi: T.Rect,
                  lever_arms=None, wheel_radius: float = 0.0,
                  config: RunConfig | None = None) -> RunResult:
     """scans[k]: (n_k, 3) sensor-frame feature points, kinds[k]: FeatureKind
-    codes; lever_arms: (2, 3) wheel-centre offsets in the base frame (the
-    leg_model.cpp forward kinematics result) or None."""
+    codes; lever_arms: the (2, 3) wheel-centre offsets in the base frame (the
+    leg_model.cpp forward kinematics result) — one array for every frame, a
+    per-frame sequence (entries may be None: no joint sample), or a callable
+    k -> array | None; None disables the wheel rows."""
     cfg = config or RunConfig()
     kernel = T.KernelParams(cfg.kernel.sigma, cfg.kernel.sigma_eps, cfg.kernel.lambda_,
                             cfg.kernel.cutoff_radius)
@@ -79,10 +92,11 @@ def run_odometry(scans, kinds, timestamps, R_first, t_first, roi: T.Rect,
             dt = timestamps[k] - timestamps[k - 1]
             Rp, tp = R, t + v * dt
             t0 = time.perf_counter()
-            use_m = cfg.use_manifold and lever_arms is not None and res.terrain.num_centers() > 0
+            arms = _arms_at(lever_arms, k)
+            use_m = cfg.use_manifold and arms is not None and res.terrain.num_centers() > 0
             Rs, ts, rep = M.lm_solve(Rp, tp, P, K, res.local_map, cfg.solver,
                                      terrain=res.terrain if use_m else None,
-                                     lever_arms=lever_arms if use_m else None,
+                                     lever_arms=arms if use_m else None,
                                      wheel_radius=wheel_radius)
             d.ms["solve"] = (time.perf_counter() - t0) * 1e3
             d.solve = rep
