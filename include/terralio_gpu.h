@@ -189,6 +189,14 @@ tlg_status tlg_feature_normal_eq(tlg_map* map, const double R[9], const double t
 /* ---- kernel.cpp ------------------------------------------------------------- */
 /* KernelParams::finalize (kernel.cpp:15-25): fills the auto cutoff, validates. */
 tlg_status tlg_kernel_finalize(tlg_kernel_params* p);
+/* kernel_eval (kernel.cpp:27-35) over n (x, c) pairs on the device:
+ * out[i] = exp(-|x_i - c_i|^2 / (2 b^2)), exactly 0 when |x_i - c_i|^2 >
+ * cutoff^2 (finalized params). TLG_DOMAIN_ERROR for a non-finite input or
+ * bandwidth <= 0, before anything is written (the reference throws
+ * std::domain_error). */
+tlg_status tlg_kernel_eval(tlg_ctx* ctx, const tlg_kernel_params* p, const double* x,
+                           const double* y, const double* cx, const double* cy, size_t n,
+                           tlg_mem in_mem, double bandwidth, double* out, tlg_mem out_mem);
 
 /* ---- center_select.cpp ------------------------------------------------------ */
 /* supported_mesh_nodes (center_select.cpp:18-62): lattice nodes of `roi`

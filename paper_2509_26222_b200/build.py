@@ -89,10 +89,50 @@ def build_oracle(force: bool = False) -> Path:
     return odir / "_build" / "liboracle.so"
 
 
+DROPIN_TESTS = ["test_kernel", "test_center_select", "test_terrain_model", "test_kinematics"]
+DROPIN_OUT = ROOT / "tests" / "cpp" / "_build"
+
+
+def build_dropin_tests(force: bool = False) -> Path | None:
+    """The reference's own unit-test files, compiled in place from
+    /root/reference against include/terralio_dropin (the Eigen-typed drop-in
+    on the C-ABI; Eigen and doctest from oracle/'s minimal stand-ins) and
+    linked with libterralio_gpu.so: tests/cpp/_build/ref_tests_dropin. Only
+    where /root/reference exists; the binary travels to the GPU box."""
+    if not REFERENCE.exists():
+        return None
+    DROPIN_OUT.mkdir(parents=True, exist_ok=True)
+    exe = DROPIN_OUT / "ref_tests_dropin"
+    srcs = [REFERENCE / "tests" / "unit" / f"{t}.cpp" for t in DROPIN_TESTS]
+    support = ROOT / "tests" / "cpp" / "dropin" / "support.cpp"
+    hdrs = list((ROOT / "include" / "terralio_dropin").rglob("*.hpp")) + [
+        ROOT / "include" / "terralio_gpu.h"]
+    if not force and not _stale(exe, [*srcs, support, *hdrs, LIB]):
+        return exe
+    cxx = "/usr/bin/g++" if Path("/usr/bin/g++").exists() else "g++"
+    inc = ["-I", str(ROOT / "include" / "terralio_dropin"), "-I", str(ROOT / "oracle" / "eigen_subset"),
+           "-I", str(ROOT / "oracle" / "shims"), "-I", str(ROOT / "include"),
+           "-I", str(REFERENCE / "core" / "include")]
+    objs = []
+    jobs = []
+    for src in [*srcs, support]:
+        obj = DROPIN_OUT / (src.stem + ".o")
+        objs.append(obj)
+        jobs.append([cxx, "-std=c++20", "-O2", "-w", *inc, "-c", str(src), "-o", str(obj)])
+    with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+        list(ex.map(_run, jobs))
+    cuda = Path("/usr/local/cuda")
+    _run([cxx, *map(str, objs), "-L", str(LIB_DIR), "-lterralio_gpu", f"-Wl,-rpath,{LIB_DIR}",
+          "-L", str(cuda / "lib64"), "-lcudart", f"-Wl,-rpath,{cuda / 'lib64'}", "-lpthread",
+          "-o", str(exe)])
+    return exe
+
+
 def main() -> None:
     force = "--force" in sys.argv
     print(build_oracle(force))
     print(build_gpu(force, verbose="-v" in sys.argv))
+    print(build_dropin_tests(force))
 
 
 if __name__ == "__main__":

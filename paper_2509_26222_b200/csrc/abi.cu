@@ -408,6 +408,64 @@ tlg_status tlg_kernel_finalize(tlg_kernel_params* p) {
   });
 }
 
+// kernel.cpp:27-35, elementwise: (x - c).squaredNorm() without contraction,
+// the `>` cutoff test, exp(-r2 / (2 b b)); non-finite inputs raise a flag.
+__global__ void k_kernel_eval(const double* __restrict__ x, const double* __restrict__ y,
+                              const double* __restrict__ cx, const double* __restrict__ cy,
+                              size_t n, double cut2, double denom, double* __restrict__ out,
+                              int* __restrict__ bad) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const double xi = x[i], yi = y[i], ci = cx[i], di = cy[i];
+    if (!isfinite(xi) || !isfinite(yi) || !isfinite(ci) || !isfinite(di)) {
+      atomicOr(bad, 1);
+      out[i] = 0.0;
+      continue;
+    }
+    const double dx = __dsub_rn(xi, ci), dy = __dsub_rn(yi, di);
+    const double r2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+    out[i] = (r2 > cut2) ? 0.0 : exp(__ddiv_rn(-r2, denom));
+  }
+}
+
+tlg_status tlg_kernel_eval(tlg_ctx* ctx, const tlg_kernel_params* p, const double* x,
+                           const double* y, const double* cx, const double* cy, size_t n,
+                           tlg_mem in_mem, double bandwidth, double* out, tlg_mem out_mem) {
+  return guard([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(p, "params");
+    if (!std::isfinite(bandwidth)) throw Error(TLG_DOMAIN_ERROR, "non-finite kernel input");
+    if (!(bandwidth > 0.0)) throw Error(TLG_DOMAIN_ERROR, "bandwidth must be > 0");
+    if (n == 0) return;
+    check_ptr(x, "x");
+    check_ptr(y, "y");
+    check_ptr(cx, "cx");
+    check_ptr(cy, "cy");
+    check_ptr(out, "out");
+    const double* dx = as_device(ctx, S_IN_X, x, n, in_mem);
+    const double* dy = as_device(ctx, S_IN_Y, y, n, in_mem);
+    const double* dcx = as_device(ctx, S_IN_HX, cx, n, in_mem);
+    const double* dcy = as_device(ctx, S_IN_HY, cy, n, in_mem);
+    const bool dev = out_mem == TLG_DEVICE;
+    double* dout = dev ? out : ctx->ws<double>(S_OUT_Z, n);
+    int* bad = ctx->ws<int>(S_FLAGS, 1);
+    TLG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+    const double denom = 2.0 * bandwidth * bandwidth;
+    const int grid = static_cast<int>(std::min<size_t>((n + 255) / 256, size_t(ctx->num_sms) * 8));
+    k_kernel_eval<<<grid, 256, 0, ctx->stream>>>(dx, dy, dcx, dcy, n, p->cutoff_radius * p->cutoff_radius,
+                                                denom, dout, bad);
+    TLG_LAUNCHED(ctx);
+    int hbad = 0;
+    TLG_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    if (hbad) throw Error(TLG_DOMAIN_ERROR, "non-finite kernel input");
+    if (!dev) {
+      copy_out(ctx, out, dout, n * 8, TLG_HOST);
+      ctx->sync();
+    }
+  });
+}
+
 // ---- center selection ------------------------------------------------------
 static tlg_status select_impl(tlg_ctx* ctx, const double* x, const double* y, const double* z,
                               size_t m, size_t zn, tlg_mem in_mem, const tlg_center_params* p,
