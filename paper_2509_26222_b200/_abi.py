@@ -123,6 +123,8 @@ _SIGS = {
                                           C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "tlg_debug_potrf": (_ST, [_P, _I, _P, _I, _I, _P, _P]),
     "tlg_kernel_finalize": (_ST, [C.POINTER(KernelParamsC)]),
+    "tlg_kernel_eval": (_ST, [_P, C.POINTER(KernelParamsC), _P, _P, _P, _P, _SZ, _I, C.c_double,
+                              _P, _I]),
     "tlg_supported_mesh_nodes": (_ST, [_P, _P, _P, _P, _SZ, _SZ, _I, C.POINTER(CenterParamsC),
                                        _P, _P, _SZ, C.POINTER(_SZ), _I]),
     "tlg_select_centers": (_ST, [_P, _P, _P, _P, _SZ, _SZ, _I, C.POINTER(CenterParamsC),

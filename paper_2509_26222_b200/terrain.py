@@ -228,6 +228,23 @@ def _same_space(*arrs):
 
 
 # ---------------------------------------------------------------------------
+def kernel_eval(params: KernelParams, x, c, bandwidth: float, ctx: Context | None = None):
+    """kernel_eval (kernel.cpp:27-35) on the device, elementwise over (n, 2)
+    point and centre arrays (or one pair); DomainError on non-finite input
+    or bandwidth <= 0."""
+    ctx = ctx or Context.default()
+    xs, ys = _xy_of(x)
+    cxs, cys = _xy_of(c)
+    if len(xs) != len(cxs):
+        raise InvalidArgument("x and c differ in length")
+    _same_space(xs, cxs)
+    out = _empty_like(xs, len(xs), np.float64)
+    check(_abi.load().tlg_kernel_eval(ctx.handle, C.byref(params._c()), _ptr(xs), _ptr(ys),
+                                      _ptr(cxs), _ptr(cys), len(xs), _mem(xs), float(bandwidth),
+                                      _ptr(out), _mem(out)))
+    return out
+
+
 def _nodes_impl(fn_name, obs: TerrainObservation, roi: Rect, res, r_a, count, ctx):
     ctx = ctx or Context.default()
     lib = _abi.load()

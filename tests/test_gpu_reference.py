@@ -172,3 +172,27 @@ def test_rejected_update_keeps_model_but_births_persist(gpu_ctx, tmp_path):
         gb = g.block_info_inverse(b)
         if gb.shape == a.shape:
             assert np.array_equal(gb, a), b
+
+
+def test_kernel_eval_matches_reference(gpu_ctx):
+    """tlg_kernel_eval vs the reference's kernel_eval (kernel.cpp:27-35):
+    the exact zero beyond the cutoff bit for bit, values to 1e-15 relative
+    (device exp vs glibc exp), domain errors alike."""
+    k = T.KernelParams()
+    k.finalize()
+    rng = np.random.default_rng(21)
+    x = rng.uniform(-0.5, 0.5, (4000, 2))
+    c = rng.uniform(-0.5, 0.5, (4000, 2))
+    # pairs straddling the cutoff within an ulp
+    d = np.array([k.cutoff_radius, np.nextafter(k.cutoff_radius, 0), np.nextafter(k.cutoff_radius, 1)])
+    x = np.concatenate([x, np.stack([d, np.zeros(3)], 1)])
+    c = np.concatenate([c, np.zeros((3, 2))])
+    for bw in (k.sigma, k.sigma_tilde(), 0.3):
+        got = T.kernel_eval(k, x, c, bw)
+        ref = np.array([REF.kernel_eval(k, xi, ci, bw) for xi, ci in zip(x, c)])
+        assert np.array_equal(got == 0.0, ref == 0.0)
+        np.testing.assert_allclose(got, ref, rtol=1e-15, atol=0)
+    with pytest.raises(T.DomainError):
+        T.kernel_eval(k, np.array([[np.nan, 0.0]]), np.zeros((1, 2)), 0.04)
+    with pytest.raises(T.DomainError):
+        T.kernel_eval(k, np.zeros((1, 2)), np.zeros((1, 2)), -1.0)
