@@ -103,10 +103,14 @@ __device__ __forceinline__ void bd_pair(double& S, double& T, double d2, double 
 // LOOSE (compiled geometries only, dispatched when LatticeView::loose_ok):
 // boundary pairs are summed without the cutoff test. A pair that fails it
 // lies beyond the cutoff, where kappa_sigma <= exp(-r2 / (2 sigma^2)) (6.8e-15
-// with the paper's parameters). Every point checks that the resulting worst
-// case stays under 1e-10 of its own parity scale (guard at the end of the
-// sweep) and is re-evaluated exactly otherwise. Everything else (window,
-// support flag, always-inside/outside pairs) is the exact path's.
+// with the paper's parameters), so the sum moves by at most
+// n_bd kappa(cutoff) |w|max (z) and that times cutoff / sigma^2 (gradient).
+// k_cell_flags proves, per lattice cell, that this stays under 1e-10 of a
+// lower bound of the parity scales sum |w kappa| and sum |w kappa| d / s^2
+// over every point of the cell (10x inside the 1e-9 tolerance); cells that
+// fail (weights near zero around them, support fringe) take the exact path.
+// Everything else (window, support flag, always-inside/outside pairs) is the
+// exact path's.
 template <int WIN, int G, bool LOOSE = false>
 __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, double y,
                                                 double r2, double neg_inv_2b2) {
@@ -117,6 +121,15 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
   // the whole window lies in the zero padding (or beyond): no centre within
   // the cutoff -> unsupported, exactly like an empty radius query
   if (i0 < 0 || j0 < 0 || i0 + WIN > L.ni || j0 + WIN > L.nj) return o;
+  // LOOSE: the per-cell flags (k_cell_flags, rebuilt lazily after weight
+  // changes) say whether the skipped boundary tests are provably negligible
+  // for every point of this cell (bit 1) and whether its four corner nodes
+  // are present, which makes every point of the cell supported (bit 0)
+  uint32_t cflag = 0;
+  if constexpr (LOOSE) {
+    cflag = __ldg(L.cflag + static_cast<size_t>(ib) * L.nj + jb);
+    if (!(cflag & 2u)) return eval_lattice<WIN, G, false>(L, x, y, r2, neg_inv_2b2);
+  }
   // reference hash cells of the point (a division each): only the exact
   // path's boundary tests and the rare support scan below need them
   int qx = 0, qy = 0;
@@ -147,9 +160,6 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
     return __dadd_rn(L.min_y, __dmul_rn(static_cast<double>(j + L.j_org), L.res));
   };
   double ey[WIN], eyd[WIN], dy2[WIN];
-  // LOOSE self-check inputs: the cell's four corner pairs (always inside)
-  constexpr int kLo = G >= 0 ? kGeoms[G >= 0 ? G : 0].lo : 0;
-  double cq[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, dyc[2] = {0.0, 0.0}, s4 = 0.0, t4 = 0.0;
   // LOOSE uses no exact pair test, so offsets may drift by an ulp: dy_l =
   // dy_0 + l res (one FMA) instead of the exact node coordinate
   const double dy0 = __dsub_rn(node_y(j0), y);
@@ -160,7 +170,6 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
                                             : __dsub_rn(node_y(jj), y));
     dy2[l] = (jj >= ry.x && jj < ry.y) ? __dmul_rn(dy, dy) : CUDART_INF;
     eyd[l] = dy;
-    if (LOOSE && (l == kLo || l == kLo + 1)) dyc[l - kLo] = fabs(dy);
   }
   // compiled geometries are only dispatched when the recurrence is safe
   // (sweep_kind), so their code carries no per-node exp fallback
@@ -216,10 +225,6 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
             constexpr int l = 2 * pr + decltype(HC)::value;
             if constexpr (l < WIN) {
               const double wv = decltype(HC)::value ? v.y : v.x;
-              if constexpr (LOOSE && (k == kLo || k == kLo + 1) && (l == kLo || l == kLo + 1)) {
-                static_assert((im >> l) & 1u, "corner pairs are always inside");
-                cq[k - kLo][l - kLo] = wv * ey[l];
-              }
               if constexpr (LOOSE && ((need >> l) & 1u)) {
                 // every window pair unconditional: the chain starts with a
                 // multiply (no zero-initialised accumulator)
@@ -271,34 +276,14 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
       o.sx = fma(ex * dx, S, o.sx);
       o.sy = fma(ex, T, o.sy);
     }
-    if constexpr (LOOSE && (k == kLo || k == kLo + 1)) {
-      // corner terms v = |w| ey ex; d >= max(|dx|, |dy|)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        const double v = fabs(cq[k - kLo][b]) * ex;
-        s4 += v;
-        t4 = fma(v, fmax(fabs(dx), dyc[b]), t4);
-      }
-    }
   };
   static_for<0, WIN>(column);
-  if constexpr (LOOSE) {
-    // Per-point guarantee: the skipped tests can only add pairs beyond the
-    // cutoff, at most n_bd kappa(cutoff) |w|max to z (|w|max over this cell's
-    // window) and that times cutoff / sigma^2 to a gradient component. The
-    // parity scales are at least the corner terms: sum |w kappa| >= s4 and
-    // sum |w kappa| d / sigma^2 >= t4 / sigma^2. Keep the result only if both
-    // errors are under 1e-10 of those (10x inside the 1e-9 tolerance);
-    // otherwise (weights near zero around the point, support fringe)
-    // evaluate with the exact test.
-    const double e = L.loose_k * __ldg(L.wmax + static_cast<size_t>(ib) * L.nj + jb);
-    if (!(e <= 1e-10 * s4 && e * L.loose_d <= 1e-10 * t4))
-      return eval_lattice<WIN, G, false>(L, x, y, r2, neg_inv_2b2);
-  }
   // supported: some *present* centre passes the reference test. The cell's
   // four corner nodes are always inside; otherwise scan the window (rare).
   bool sup = false;
-  if (L.corner_ok) {
+  if constexpr (LOOSE) {
+    sup = (cflag & 1u) != 0;
+  } else if (L.corner_ok) {
     const int* pc = L.P + static_cast<size_t>(ib) * L.nj + jb;
     sup = (__ldg(pc) | __ldg(pc + 1) | __ldg(pc + L.nj) | __ldg(pc + L.nj + 1)) != 0;
   }

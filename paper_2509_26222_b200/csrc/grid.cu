@@ -156,20 +156,87 @@ static void lattice_ranges(tlg_model* m, const DBuf<AxisNode>& ax, int count, do
   TLG_LAUNCHED(m->ctx);
 }
 
-// Separable max filter of |W| over the evaluation window: pass 0 along j
-// (rows of the pitch), pass 1 along i. Nodes outside the padded lattice are
-// absent (weight 0).
-__global__ void k_window_max(const double* __restrict__ in, int ni, int nj, int lo, int win,
-                             int pass, double* __restrict__ out) {
+// Per-cell LOOSE flags (eval.cu): bit 0 = the cell's four corner nodes are
+// present (every point of the cell is supported); bit 1 = for every point of
+// the cell the boundary pairs summed without the cutoff test move z by at
+// most 1e-10 of the parity scale sum |w kappa| and a gradient component by at
+// most 1e-10 of sum |w kappa| d / sigma^2. The worst case of the skipped
+// tests is n_bd kappa(cutoff) |w|max (times cutoff / sigma^2 for the
+// gradient, since d kappa(d) falls beyond sigma). The scales are bounded
+// below on each of kSub x kSub sub-cells by the window's inside pairs: |w|
+// times the minimum over the sub-cell of kappa (and of kappa d) for that pair
+// offset (pairlb, host-computed per geometry); the cell's bound is the
+// smallest sub-cell bound.
+constexpr int kSub = 4;
+__global__ void k_cell_flags(const double* __restrict__ W, const int* __restrict__ P, int ni, int nj,
+                             int lo, int win, const double* __restrict__ pairlb, double loose_k,
+                             double loose_d, uint8_t* __restrict__ out) {
   const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (e >= (size_t)ni * nj) return;
   const int i = static_cast<int>(e / nj), j = static_cast<int>(e % nj);
-  double mx = 0.0;
-  for (int t = 0; t < win; ++t) {
-    const int ii = pass ? i - lo + t : i, jj = pass ? j : j - lo + t;
-    if (ii >= 0 && ii < ni && jj >= 0 && jj < nj) mx = fmax(mx, fabs(in[(size_t)ii * nj + jj]));
+  const int i0 = i - lo, j0 = j - lo;
+  uint8_t f = 0;
+  if (i0 >= 0 && j0 >= 0 && i0 + win <= ni && j0 + win <= nj) {
+    const size_t c = static_cast<size_t>(i) * nj + j;
+    if (P[c] && P[c + 1] && P[c + nj] && P[c + nj + 1]) f |= 1;
+    double wmax = 0.0;
+    double ls[kSub * kSub], lt[kSub * kSub];
+    for (int q = 0; q < kSub * kSub; ++q) ls[q] = lt[q] = 0.0;
+    const int np = win * win;
+    for (int k = 0; k < win; ++k)
+      for (int l = 0; l < win; ++l) {
+        const double w = fabs(W[static_cast<size_t>(i0 + k) * nj + j0 + l]);
+        wmax = fmax(wmax, w);
+        const double* lb = pairlb + 2 * (k * win + l);
+        for (int q = 0; q < kSub * kSub; ++q) {
+          ls[q] = fma(w, lb[2 * q * np], ls[q]);
+          lt[q] = fma(w, lb[2 * q * np + 1], lt[q]);
+        }
+      }
+    double ms = ls[0], mt = lt[0];
+    for (int q = 1; q < kSub * kSub; ++q) {
+      ms = fmin(ms, ls[q]);
+      mt = fmin(mt, lt[q]);
+    }
+    const double err = loose_k * wmax;
+    if (err <= 1e-10 * ms && err * loose_d <= 1e-10 * mt) f |= 2;
   }
-  out[e] = mx;
+  out[e] = f;
+}
+
+// pairlb for the model's geometry: window pair (k, l) is the node at
+// (a, b) = (k - lo, l - lo) cells from the base cell's origin; a point of
+// sub-cell (u, v) lies in [u/kSub, (u+1)/kSub) x [...] cells, so its |dx| to
+// the node spans the interval of |a - x| over that range.
+static void pair_lower_bounds(const tlg_model* m, std::vector<double>& lb) {
+  const LatticeGrid& L = m->lat;
+  const double res = m->cparams.mesh_resolution, c = m->kc.neg_inv_2s2;
+  const int np = L.win * L.win;
+  lb.assign(static_cast<size_t>(2 * np * kSub * kSub), 0.0);
+  auto span = [](int a, double x0, double x1, double& lo, double& hi) {
+    // |a - x| for x in [x0, x1]
+    const double d0 = std::fabs(a - x0), d1 = std::fabs(a - x1);
+    hi = std::max(d0, d1);
+    lo = (a >= x0 && a <= x1) ? 0.0 : std::min(d0, d1);
+  };
+  for (int u = 0; u < kSub; ++u)
+    for (int v = 0; v < kSub; ++v) {
+      const int q = u * kSub + v;
+      for (int k = 0; k < L.win; ++k)
+        for (int l = 0; l < L.win; ++l) {
+          if (!((L.inmask[k] >> l) & 1u)) continue;
+          double xl, xh, yl, yh;
+          span(k - L.lo, double(u) / kSub, double(u + 1) / kSub, xl, xh);
+          span(l - L.lo, double(v) / kSub, double(v + 1) / kSub, yl, yh);
+          const double dmin = res * std::sqrt(xl * xl + yl * yl);
+          const double dmax = res * std::sqrt(xh * xh + yh * yh);
+          const double kmin = std::exp(c * dmax * dmax);
+          const double kdmin = std::min(std::exp(c * dmin * dmin) * dmin, kmin * dmax);
+          double* o = lb.data() + 2 * (q * np + k * L.win + l);
+          o[0] = kmin * (1.0 - 1e-12);
+          o[1] = kdmin * (1.0 - 1e-12);
+        }
+    }
 }
 
 int prepare_sweep(tlg_model* m) {
@@ -177,13 +244,19 @@ int prepare_sweep(tlg_model* m) {
   LatticeGrid& L = m->lat;
   if (kind >= 200 && L.wmax_dirty) {
     const size_t nn = static_cast<size_t>(L.ni) * L.nj;
-    L.wmax.ensure(nn);
-    L.wtmp.ensure(nn);
+    L.cflag.ensure(nn);
+    std::vector<double> lb;
+    pair_lower_bounds(m, lb);
+    L.pairlb.ensure(lb.size());
+    TLG_CUDA(cudaMemcpyAsync(L.pairlb.p, lb.data(), lb.size() * sizeof(double), cudaMemcpyHostToDevice,
+                             m->ctx->stream));
+    const LatticeView v = lattice_view(m);
     const unsigned b = static_cast<unsigned>((nn + 255) / 256);
-    k_window_max<<<b, 256, 0, m->ctx->stream>>>(L.W.p, L.ni, L.nj, L.lo, L.win, 0, L.wtmp.p);
+    k_cell_flags<<<b, 256, 0, m->ctx->stream>>>(L.W.p, L.P.p, L.ni, L.nj, L.lo, L.win, L.pairlb.p, v.loose_k,
+                                                v.loose_d, L.cflag.p);
     TLG_LAUNCHED(m->ctx);
-    k_window_max<<<b, 256, 0, m->ctx->stream>>>(L.wtmp.p, L.ni, L.nj, L.lo, L.win, 1, L.wmax.p);
-    TLG_LAUNCHED(m->ctx);
+    // the host vector is read by the async copy: wait before it goes out of scope
+    TLG_CUDA(cudaStreamSynchronize(m->ctx->stream));
     L.wmax_dirty = false;
   }
   return kind;
@@ -335,7 +408,7 @@ LatticeView lattice_view(const tlg_model* m) {
   v.loose_k = nbd * kcut;
   v.loose_d = rho;
   v.loose_ok = (rho > sigma && v.loose_k * std::max(1.0, rho / sigma) <= 1e-11) ? 1 : 0;
-  v.wmax = L.wmax.p;
+  v.cflag = L.cflag.p;
   return v;
 }
 

@@ -294,9 +294,12 @@ struct LatticeGrid {
   // first node with cell >= q + span + 1) along each axis (cells are monotone
   // in the node index), for q in [base, base + n) (clamped outside).
   DBuf<int2> xr, yr;
-  // Per cell (ib, jb): max |w| over the cell's evaluation window (the LOOSE
-  // path's per-point error bound, eval.cu); rebuilt lazily after weight syncs.
-  DBuf<double> wmax, wtmp;
+  // Per cell (ib, jb): LOOSE-path flags (k_cell_flags: bit 0 corner nodes
+  // present, bit 1 skipped boundary tests provably negligible); rebuilt
+  // lazily after weight syncs. pairlb: per window pair the minimum over the
+  // cell of kappa and of kappa d (inside pairs; 0 otherwise).
+  DBuf<uint8_t> cflag;
+  DBuf<double> pairlb;
   bool wmax_dirty = true;
   int xr_base = 0, xr_n = 0, yr_base = 0, yr_n = 0;
   double min_x = 0, min_y = 0;  // node (i, j) = (min_x + (i + i_org) res, min_y + ...)
@@ -311,7 +314,7 @@ struct LatticeView {
   const AxisNode* ay;
   const int2* xr;      // see LatticeGrid
   const int2* yr;
-  const double* wmax;
+  const uint8_t* cflag;
   double loose_k;  // n_bd * kappa_sigma(cutoff)
   double loose_d;  // cutoff radius (gradient bound factor)
   int xr_base, xr_n, yr_base, yr_n, i_org, j_org;
