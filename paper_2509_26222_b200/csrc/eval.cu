@@ -175,8 +175,18 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
   // (sweep_kind), so their code carries no per-node exp fallback
   constexpr bool kRecAlways = G >= 0;
   const bool rec = kRecAlways || L.rec_ok;
+  // LOOSE compiled path: the leading factors of both axes share one exp,
+  // exp(c (dx_0^2 + dy_0^2)), applied to z and the gradient sums at the end;
+  // the axis chains then start at 1 (exponents stay within ~+-80 there)
+#ifndef TLG_SHARED_EXP
+#define TLG_SHARED_EXP 1
+#endif
+  constexpr bool kShared = LOOSE && G >= 0 && TLG_SHARED_EXP;
+  const double dx_first = __dsub_rn(node_x(i0), x);
+  double common = 1.0;
+  if constexpr (kShared) common = exp(fma(dx_first, dx_first, __dmul_rn(eyd[0], eyd[0])) * neg_inv_2b2);
   if (rec) {
-    double e = exp(__dmul_rn(eyd[0], eyd[0]) * neg_inv_2b2);
+    double e = kShared ? 1.0 : exp(__dmul_rn(eyd[0], eyd[0]) * neg_inv_2b2);
     double p = exp(L.c_res * fma(2.0, eyd[0], L.res));
 #pragma unroll
     for (int l = 0; l < WIN; ++l) {
@@ -194,10 +204,9 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
   // compiled geometries read the window in 16-byte pairs: an odd base is
   // served from the one-element-shifted copy W1 (the pitch nj is even)
   const double* wbase = (G >= 0 && (bidx & 1)) ? L.W1 + bidx + 1 : L.W + bidx;
-  const double dx_first = __dsub_rn(node_x(i0), x);
   double ex_e = 0.0, ex_p = 0.0;
   if (rec) {
-    ex_e = exp(__dmul_rn(dx_first, dx_first) * neg_inv_2b2);
+    ex_e = kShared ? 1.0 : exp(__dmul_rn(dx_first, dx_first) * neg_inv_2b2);
     ex_p = exp(L.c_res * fma(2.0, dx_first, L.res));
   }
   auto column = [&](auto KC) {
@@ -278,6 +287,11 @@ __device__ __forceinline__ EvalOut eval_lattice(const LatticeView& L, double x, 
     }
   };
   static_for<0, WIN>(column);
+  if constexpr (kShared) {
+    o.z *= common;
+    o.sx *= common;
+    o.sy *= common;
+  }
   // supported: some *present* centre passes the reference test. The cell's
   // four corner nodes are always inside; otherwise scan the window (rare).
   bool sup = false;
