@@ -122,10 +122,20 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def cpu_eval_rate(centers_xy, weights, kernel, pts_h, R, t, seconds=10.0, threads=None):
-    """Oracle (restated reference) manifold rows on a bounded sample."""
+def cpu_backend():
+    """The CPU side of the bench (cpu_baseline leg / --impl reference only):
+    the reference itself compiled from its unchanged sources (oracle/_ref,
+    kind "reference") when present, else the plain-C++ restatement ("port")."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle as orc
+    ref = orc.reference()
+    return (ref, "reference") if ref is not None else (orc, "port")
+
+
+def cpu_eval_rate(centers_xy, weights, kernel, pts_h, R, t, seconds=10.0, threads=None):
+    """The reference's manifold rows (kin::manifold_residual/jacobian with the
+    total_cost weighting) on a bounded sample, all host threads."""
+    orc, _ = cpu_backend()
     from paper_2509_26222_b200.terrain import CenterSet, Rect
     threads = threads or os.cpu_count() or 1
     cs = CenterSet(centers_xy, RES, R_A, COUNT, Rect(*ROI_C5))
@@ -448,9 +458,9 @@ def run_consumers_bench(torch, umodel, ukernel, cpu=True, reps=10):
 
 
 def cpu_update_ms(model, kernel, m=400, seed=5):
-    """Oracle recursive_update (reference algorithm, single thread) at M=4096."""
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import oracle as orc
+    """The reference's recursive_update (chunk-64 Woodbury; its GEMMs on all
+    host threads) at M = 4096 from the GPU model's weights."""
+    orc, _ = cpu_backend()
     cs = model.centers()
     om = orc.Model(kernel, cs)
     om.set_weights(model.weights())
@@ -460,6 +470,185 @@ def cpu_update_ms(model, kernel, m=400, seed=5):
     t0 = time.perf_counter()
     rep = om.recursive_update(noisy, staircase(clean[:, 0]))
     return (time.perf_counter() - t0) * 1e3, rep
+
+
+def c5_parity(model, kernel, cs, w, R, tv, h, n=100_000):
+    """Self-check of the measured kernel (cpu_baseline leg): k_manifold on the
+    first n C5 lever arms vs the reference's manifold rows with the same
+    weights, at the SURVEY §8d tolerance: |d| <= 1e-9 max(|ref|, scale) with
+    the row's sum |w kappa| scale (no additive floor)."""
+    from paper_2509_26222_b200 import kinematics as kin
+    from paper_2509_26222_b200.terrain import CenterSet, Rect
+    orc, kind = cpu_backend()
+    hs = np.ascontiguousarray(np.stack([x[:n].cpu().numpy() for x in h], 1))
+    rows, _ = kin.manifold_rows(model, R, tv, tuple(np.ascontiguousarray(hs[:, j]) for j in range(3)),
+                                0.0, 1.0, 0.05, want=("r", "J", "valid"))
+    om = orc.Model(kernel, CenterSet(cs.centers, RES, R_A, COUNT, Rect(*ROI_C5)))
+    om.set_weights(w)
+    ref, _ = om.manifold_rows(R, tv, hs, 0.0, 1.0, 0.05, threads=os.cpu_count() or 1)
+    xy = (hs @ np.asarray(R).T + tv)[:, :2]
+    S0, S1 = om.scales(xy)
+    s = np.abs(ref["J"][:, 5])
+    hn = np.linalg.norm(hs, axis=1)
+    J = rows["J"].reshape(6, -1).T
+    tiny = np.finfo(np.float64).tiny
+    scale_J = [s * hn * S1, s * hn * S1, s * hn * S1, s * S1, s * S1, s]
+
+    def worst(got, want, scale):
+        return float(np.max(np.abs(got - want) / np.maximum(np.maximum(np.abs(want), scale), tiny)))
+
+    er = worst(rows["r"], ref["r"], s * S0)
+    eJ = max(worst(J[:, c], ref["J"][:, c], scale_J[c]) for c in range(6))
+    vm = int(np.sum(rows["valid"] != ref["valid"]))
+    return {"points": n, "source": kind, "kernel_kind": int(model.sweep()[0]),
+            "max_err_r": er, "max_err_J": eJ, "valid_mismatch": vm,
+            "tolerance": 1e-9, "pass": bool(er <= 1e-9 and eJ <= 1e-9 and vm == 0),
+            "scale": "1e-9 * max(|ref|, s sum|w kappa| [r], s |h| sum|w kappa| d/sigma^2 [J_rot], "
+                     "s sum|w kappa| d/sigma^2 [J_t])"}
+
+
+def c1_inputs_np(n_points=20000, seed=2509):
+    """20k points uniform on [0, 1.05]^2 with N(0, 0.1^2) xy
+    noise, z = 0.1 sin 4x + 0.05 y^2 of the clean point."""
+    rng = np.random.default_rng(seed)
+    clean = rng.uniform(0.0, 1.05, (n_points, 2))
+    noisy = clean + rng.normal(0.0, 0.1, clean.shape)
+    z = 0.1 * np.sin(4.0 * clean[:, 0]) + 0.05 * clean[:, 1] ** 2
+    return np.ascontiguousarray(noisy), z
+
+
+def run_c1(torch, cpu=True):
+    """C1 (BASELINE configs[0]): M = 256 centres on [0, 1.05]^2, one 20k-point
+    scan: select_centers, one recursive_update (n = 256, m = 20k) and the
+    height / gradient / manifold-row evaluation of the scan, each timed on
+    the GPU (CUDA events, host arrays through the public API) and on the
+    CPU with the reference (oracle/_ref, all host threads)."""
+    from paper_2509_26222_b200 import kinematics as kin
+    from paper_2509_26222_b200 import terrain as T
+    xy, z = c1_inputs_np()
+    roi = T.Rect((0.0, 0.0), (1.05, 1.05))
+    R, tv = so3_exp(POSE_W), np.array(POSE_T)
+    P = np.concatenate([xy, z[:, None]], 1)
+    H = (P - tv) @ R
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed(f, reps=5):
+        f()
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            ev0.record()
+            out = f()
+            ev1.record()
+            ev1.synchronize()
+            ts.append(ev0.elapsed_time(ev1))
+        return statistics.median(ts), out
+
+    obs = T.TerrainObservation(xy, z)
+    k = T.KernelParams()
+    k.finalize()
+    sel_ms, cs = timed(lambda: T.select_centers(obs, roi, RES, R_A, COUNT))
+
+    def upd():
+        m = T.TerrainModel(k, cs)
+        return m, m.recursive_update(obs, False)
+    upd_ms, (model, rep) = timed(upd)
+    eval_ms, _ = timed(lambda: model.predict(xy))
+    rows_ms, _ = timed(lambda: kin.manifold_rows(model, R, tv, H, 0.0, 1.0, 0.05))
+    out = {"M": len(cs.centers), "m": len(z), "n_active": rep.active_centers, "solver": rep.solver,
+           "gpu_ms": {"select_centers": sel_ms, "model_and_recursive_update": upd_ms,
+                      "predict_height_gradient": eval_ms, "manifold_rows_normal_eq": rows_ms}}
+    if cpu:
+        orc, kind = cpu_backend()
+        th = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        nodes = orc.supported_mesh_nodes(xy, z, roi, RES, R_A, COUNT, True)
+        t1 = time.perf_counter()
+        om = orc.Model(k, T.CenterSet(nodes, RES, R_A, COUNT, roi))
+        om.recursive_update(xy, z, False)
+        t2 = time.perf_counter()
+        om.predict(xy, threads=1)
+        t3 = time.perf_counter()
+        om.manifold_rows(R, tv, H, 0.0, 1.0, 0.05, threads=1)
+        t4 = time.perf_counter()
+        out["cpu_ms"] = {"select_centers": (t1 - t0) * 1e3, "model_and_recursive_update": (t2 - t1) * 1e3,
+                         "predict_height_gradient": (t3 - t2) * 1e3,
+                         "manifold_rows_normal_eq": (t4 - t3) * 1e3}
+        out["cpu"] = {"kind": kind, "cores": th,
+                      "note": "update on all host threads (GEMMs of the compiled reference); "
+                              "evaluation single-threaded like the reference's per-query path"}
+        out["nodes_bit_exact_vs_cpu"] = bool(np.array_equal(np.asarray(cs.centers).view(np.uint64),
+                                                          nodes.view(np.uint64)))
+    return out
+
+
+def cpu_reference_figures(torch):
+    """CPU figures beside the GPU's at reduced sizes the CPU reference
+    finishes in seconds (its dense chunk-64 Woodbury is 4 n^2 m flops):
+    C3-reduced (M = 400 staircase lattice, m = 20,000: the information form on
+    the GPU) and C4-reduced (97 x 97 bumps lattice, a 1 m footprint,
+    m = 2,000). Same inputs on both; ms per update and the weights' relative
+    difference."""
+    from paper_2509_26222_b200 import terrain as T
+    orc, kind = cpu_backend()
+    k = T.KernelParams()
+    k.finalize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    out = {"kind": kind, "cores": os.cpu_count() or 1}
+
+    def lattice(side, seed):
+        roi = T.Rect((0.0, 0.0), (side, side))
+        rng = np.random.default_rng(seed)
+        sup = rng.uniform(0.0, side, (int(side * side * 1500), 2))
+        return T.select_centers(T.TerrainObservation(sup, np.zeros(len(sup))), roi, RES, R_A, COUNT)
+
+    rng = np.random.default_rng(41)
+    cases = []
+    cs3 = lattice(1.33, 1)
+    clean = rng.uniform(0.0, 1.33, (20000, 2))
+    cases.append(("c3_reduced_m20000", cs3, clean + rng.normal(0.0, 0.1, clean.shape),
+                  staircase(clean[:, 0] + 0.4)))
+    cs4 = lattice(6.72, 6)
+    rr = np.sqrt(rng.uniform(0, 1, 2000))
+    a = rng.uniform(0, 2 * np.pi, 2000)
+    clean = np.stack([3.0 + rr * np.cos(a), 3.2 + rr * np.sin(a)], 1)
+    cases.append(("c4_reduced_m2000", cs4, clean + rng.normal(0.0, 0.02, clean.shape),
+                  terrain_c5(clean[:, 0], clean[:, 1], np)))
+    for name, cs, xy, z in cases:
+        g = T.TerrainModel(k, cs)
+        g.recursive_update(T.TerrainObservation(xy, z), False)  # warm
+        g = T.TerrainModel(k, cs)
+        torch.cuda.synchronize()
+        ev0.record()
+        rep = g.recursive_update(T.TerrainObservation(xy, z), False)
+        ev1.record()
+        ev1.synchronize()
+        om = orc.Model(k, cs)
+        t0 = time.perf_counter()
+        om.recursive_update(xy, z, False)
+        cpu_ms = (time.perf_counter() - t0) * 1e3
+        wr = om.weights()
+        out[name] = {"M": len(cs.centers), "m": len(z), "n_active": rep.active_centers,
+                     "solver": rep.solver, "gpu_ms": ev0.elapsed_time(ev1), "cpu_ms": cpu_ms,
+                     "weights_rel_diff": float(np.linalg.norm(g.weights() - wr) / np.linalg.norm(wr))}
+    return out
+
+
+def reference_c2(scans=20):
+    """The reference's own pipeline::run_odometry (oracle/_ref) on its stock
+    staircase simulation at 1000 x 20 rays, RunConfig
+    defaults with use_imu false (the GPU loop's prediction): per-scan wall
+    time on the host. The GPU loop on the same bundle is compared pose by pose
+    in tests/test_pose_parity.py (profiles/r2_pose_parity.jsonl)."""
+    orc, kind = cpu_backend()
+    if kind != "reference":
+        return {"unavailable": "oracle/_ref not built"}
+    b = orc.SimBundle("staircase", 11, 1000, 20, scans)
+    o = orc.odometry(b, orc.run_config_json(use_imu=False), mode=1)
+    feats = float(np.mean([len(b.scan(k)[1]) for k in range(b.num_scans())]))
+    return {"kind": kind, "scans": int(b.num_scans()), "features_per_scan": feats,
+            "ms_per_scan_median": float(np.median(o["wall_ms"][1:])),
+            "ms_per_scan_mean": float(np.mean(o["wall_ms"][1:])), "threads": 1}
 
 
 # ---------------------------------------------------------------------------
@@ -475,6 +664,21 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+
+    # one process per GPU: `--gpus N` without a torchrun environment launches
+    # N ranks itself (torch.distributed.run on 127.0.0.1); under torchrun the
+    # world size must agree with --gpus
+    if os.environ.get("WORLD_SIZE") is None and args.gpus > 1:
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}")
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -636,8 +840,9 @@ def main():
             result["update"] = upd
             if not args.no_cpu:
                 cms, crep = cpu_update_ms(umodel, ukernel, 400)
-                result["update"]["cpu_oracle_ms_per_scan_m400"] = cms
-                result["update"]["cpu_oracle_n_active"] = crep["active_centers"]
+                result["update"]["cpu_ms_per_scan_m400"] = cms
+                result["update"]["cpu_n_active"] = crep["active_centers"]
+                result["update"]["cpu_kind"] = cpu_backend()[1]
         if not args.no_update:
             result["match"] = run_match_bench(torch, not args.no_cpu)
             result["consumers"] = run_consumers_bench(torch, umodel, ukernel, not args.no_cpu)
@@ -645,18 +850,28 @@ def main():
             # pipeline.cpp:196-300 loop over synthetic staircase scans
             sys.path.insert(0, str(ROOT / "tools"))
             from pipeline_c2 import run_c2
-            c2 = run_c2(scans=30)
+            c2 = run_c2(scans=100)
             c2["note"] = ("synthetic staircase with walls and poles, ~20k features/scan; host "
                           "(Python) LM loop over device association, rows and update")
             result["pipeline_c2"] = c2
+            result["c1"] = run_c1(torch, cpu=not args.no_cpu)
         if not args.no_cpu:
+            # ---- cpu_baseline leg: the reference on the host cores, and the
+            # checks that use it (parity of the measured kernel) -------------
+            _, kind = cpu_backend()
             pts_h = torch.stack(list(h), 1)[: 2_000_000].cpu().numpy()
             rate, ns, threads, dt, _ = cpu_eval_rate(cs.centers, w, kernel, pts_h, R, tv,
                                                      args.cpu_seconds)
+            what = ("the reference compiled from its unchanged sources (oracle/_ref)"
+                    if kind == "reference" else "oracle restatement -O3 no-FMA")
             result["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads,
-                                      "kind": "port",
-                                      "sample": f"{ns} of the C5 points ({dt:.1f} s), oracle "
-                                                f"restatement -O3 no-FMA, {threads} threads"}
+                                      "kind": kind,
+                                      "sample": f"{ns} of the C5 points ({dt:.1f} s), {what}, "
+                                                f"{threads} threads over points"}
+            result["parity"] = c5_parity(model, kernel, cs, w, R, tv, h)
+            if not args.no_update:
+                result["update"]["cpu_reference"] = cpu_reference_figures(torch)
+                result["pipeline_c2"]["reference_c2"] = reference_c2(20)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -664,8 +879,9 @@ def main():
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference algorithm's CPU path (oracle port; the
-    reference itself is unbuildable here) on the host cores, same metric."""
+    """--impl reference: the reference's own CPU path (oracle/_ref, its
+    unchanged sources compiled against a minimal Eigen subset; the
+    restatement if that is absent) on the host cores, same metric."""
     if rank != 0:
         return
     import torch
@@ -686,6 +902,7 @@ def run_reference(args, world, rank):
     H = (np.stack([p[:, 0], p[:, 1], pz], 1) - tv) @ R
     threads = os.cpu_count() or 1
     per_step = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    _, kind = cpu_backend()
     rate, ns, threads, dt, om = cpu_eval_rate(centers, w, kernel, H, R, tv, per_step, threads)
     rates = []
     for i in range(args.warmup + args.steps):
@@ -701,9 +918,12 @@ def run_reference(args, world, rank):
            "data": "synthetic",
            "config": {"workload": "C5 (bounded sample per step)", "points_per_step": ns,
                       "centres": len(centers)},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                            "sample": f"{ns} C5 points per step; oracle restatement of the "
-                                      "reference (reference unbuildable: Eigen absent)"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                            "sample": f"{ns} C5 points per step; "
+                                      + ("the reference compiled from its unchanged sources "
+                                         "(oracle/_ref: minimal Eigen subset in place of Eigen3)"
+                                         if kind == "reference" else
+                                         "oracle restatement of the reference")},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)

@@ -347,6 +347,17 @@ class Model:
                                       threads))
         return z, s, gx, gy
 
+    def scales(self, xy, threads=None):
+        """Parity scales per point: (sum |w kappa|, sum |w kappa| d / s^2)."""
+        import os
+        p = _f64(xy).reshape(-1, 2)
+        x, y = _f64(p[:, 0]), _f64(p[:, 1])
+        s, g = np.empty(len(x)), np.empty(len(x))
+        f = load().orc_model_scales
+        f.argtypes = [C.c_void_p] + [C.c_void_p] * 2 + [C.c_size_t] + [C.c_void_p] * 2 + [C.c_int]
+        _chk(f(self.h, _p(x), _p(y), len(x), _p(s), _p(g), int(threads or os.cpu_count() or 1)))
+        return s, g
+
     def centers_near(self, q):
         out = np.empty(1 << 16, dtype=np.uint32)
         n = load().orc_model_centers_near(self.h, q[0], q[1], _p(out), len(out))

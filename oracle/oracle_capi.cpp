@@ -233,6 +233,41 @@ int orc_model_predict(void* m, const double* x, const double* y, size_t n, doubl
   });
 }
 
+// Parity scales of the height and gradient at each point:
+// s = sum |w_i kappa_sigma(x, c_i)|, g = sum |w_i kappa_sigma| d_i / sigma^2
+// over the reference's neighbour set (test infrastructure).
+int orc_model_scales(void* m, const double* x, const double* y, size_t n, double* s, double* g,
+                     int threads) {
+  auto* t = static_cast<TerrainModel*>(m);
+  return guarded([&] {
+    const double sig = t->kernel().sigma, cut = t->kernel().cutoff_radius;
+    const auto& w = t->weights();
+    const auto& c = t->centers().centers;
+    auto work = [&](size_t b, size_t e) {
+      for (size_t i = b; i < e; ++i) {
+        double a = 0.0, q = 0.0;
+        for (unsigned id : t->centers_near({x[i], y[i]}, cut)) {
+          const double dx = x[i] - c[id].x, dy = y[i] - c[id].y;
+          const double d2 = dx * dx + dy * dy;
+          const double v = std::abs(w[id] * std::exp(-d2 / (2.0 * sig * sig)));
+          a += v;
+          q += v * std::sqrt(d2) / (sig * sig);
+        }
+        s[i] = a;
+        g[i] = q;
+      }
+    };
+    std::vector<std::thread> pool;
+    const int nt = std::max(1, threads);
+    const size_t chunk = (n + nt - 1) / nt;
+    for (int k = 0; k < nt; ++k) {
+      const size_t b = k * chunk, e = std::min(n, b + chunk);
+      if (b < e) pool.emplace_back(work, b, e);
+    }
+    for (auto& th : pool) th.join();
+  });
+}
+
 size_t orc_model_centers_near(void* m, double qx, double qy, unsigned* out, size_t cap) {
   auto* t = static_cast<TerrainModel*>(m);
   const auto ids = t->centers_near({qx, qy}, t->kernel().cutoff_radius);

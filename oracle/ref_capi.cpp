@@ -386,6 +386,40 @@ int orc_model_predict(void* m, const double* x, const double* y, size_t n, doubl
   });
 }
 
+// Parity scales, from the reference's neighbour index and
+// weights: s = sum |w kappa_sigma|, g = sum |w kappa_sigma| d / sigma^2.
+int orc_model_scales(void* m, const double* x, const double* y, size_t n, double* s, double* g,
+                     int threads) {
+  RefModel* r = M(m);
+  return guarded([&] {
+    const double sig = r->m.kernel().sigma, cut = r->m.kernel().cutoff_radius;
+    const Eigen::VectorXd& w = r->m.weights();
+    const auto& c = r->m.centers().centers;
+    auto work = [&](size_t b, size_t e) {
+      for (size_t i = b; i < e; ++i) {
+        double a = 0.0, q = 0.0;
+        for (std::uint32_t id : r->index->radius_query(Vec2(x[i], y[i]), cut)) {
+          const double dx = x[i] - c[id].x(), dy = y[i] - c[id].y();
+          const double d2 = dx * dx + dy * dy;
+          const double v = std::abs(w(id) * std::exp(-d2 / (2.0 * sig * sig)));
+          a += v;
+          q += v * std::sqrt(d2) / (sig * sig);
+        }
+        s[i] = a;
+        g[i] = q;
+      }
+    };
+    std::vector<std::thread> pool;
+    const int nt = std::max(1, threads);
+    const size_t chunk = (n + nt - 1) / nt;
+    for (int k = 0; k < nt; ++k) {
+      const size_t b = k * chunk, e = std::min(n, b + chunk);
+      if (b < e) pool.emplace_back(work, b, e);
+    }
+    for (auto& th : pool) th.join();
+  });
+}
+
 size_t orc_model_centers_near(void* m, double qx, double qy, unsigned* out, size_t cap) {
   RefModel* r = M(m);
   const auto ids = r->index->radius_query(Vec2(qx, qy), r->m.kernel().cutoff_radius);

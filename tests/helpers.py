@@ -88,5 +88,28 @@ def scales(model_oracle, xy, sigma):
     return hs, gs
 
 
+def manifold_row_scales(model_oracle, R, t, h, ref_J):
+    """Per-row parity scales of the manifold rows (1e-9 of
+    max(|ref|, scale), scale built from sum |w kappa| of the same point):
+    r ~ s S0 and J3, J4 ~ s S1 with S0 = sum |w kappa|, S1 = sum |w kappa| d /
+    sigma^2, J0..J2 = s h x (R^T [-g, 1]) ~ s |h| S1, J5 = s exactly; s =
+    sqrt(lambda_M) w_Huber = ref J5. No additive floor."""
+    h = np.asarray(h, dtype=np.float64).reshape(-1, 3)
+    xy = (h @ np.asarray(R).T + np.asarray(t))[:, :2]
+    S0, S1 = model_oracle.scales(xy)
+    s = np.abs(np.asarray(ref_J)[:, 5])
+    hn = np.linalg.norm(h, axis=1)
+    tiny = np.finfo(np.float64).tiny
+    return {"r": s * S0 + tiny, "raw": S0 + tiny,
+            "J": [s * hn * S1 + tiny] * 3 + [s * S1 + tiny] * 2 + [s + tiny]}
+
+
+def assert_manifold_rows_close(got_r, got_J, ref_r, ref_J, sc, rtol=1e-9):
+    """got_J, ref_J: (n, 6) row-major."""
+    assert_values_close(got_r, ref_r, sc["r"], rtol, what="r")
+    for c in range(6):
+        assert_values_close(got_J[:, c], ref_J[:, c], sc["J"][c], rtol, what=f"J{c}")
+
+
 __all__ = ["uniform_xy", "make_field", "c1_inputs", "so3_exp", "assert_values_close",
-           "rel_norm", "scales", "math"]
+           "rel_norm", "scales", "math", "manifold_row_scales", "assert_manifold_rows_close"]

@@ -1,12 +1,15 @@
 """Golden fixtures (tests/golden/*.npz, made by tests/golden/make_golden.py
-from the pinned oracle). CPU: the oracle still reproduces them. GPU: the
-sm_100a path matches them with no oracle at run time."""
+from the reference itself, oracle/_ref). CPU: the plain-C++ restatement
+reproduces them (bit-exact for indexing, within the reference's own 1e-10 bar
+for Eigen arithmetic). GPU: the sm_100a path matches them with no oracle at
+run time, at the SURVEY §8d tolerances."""
 from pathlib import Path
 
 import numpy as np
 import pytest
 
 import oracle as orc
+from helpers import assert_manifold_rows_close, assert_values_close
 from paper_2509_26222_b200.terrain import CenterSet, KernelParams, Rect
 
 G = Path(__file__).resolve().parent / "golden"
@@ -32,10 +35,11 @@ def test_oracle_eval_golden():
     d = load("eval_field.npz")
     cs = CenterSet(d["centers"], *d["mesh"][:2], int(d["mesh"][2]), Rect((0.0, 0.0), (1.0, 1.0)))
     m = orc.fit_batch_ridge(_kernel(d), cs, d["obs_xy"], d["obs_z"])
-    np.testing.assert_allclose(m.weights(), d["weights"], rtol=1e-13, atol=1e-15)
+    assert np.linalg.norm(m.weights() - d["weights"]) <= 1e-10 * np.linalg.norm(d["weights"])
+    m.set_weights(d["weights"])  # then evaluation is bit-for-bit the reference's
     z, s, gx, gy = m.predict(d["q"])
     assert np.array_equal(s, d["sup"])
-    np.testing.assert_allclose(z, d["z"], rtol=1e-12, atol=1e-14)
+    assert np.array_equal(z, d["z"]) and np.array_equal(gx, d["gx"]) and np.array_equal(gy, d["gy"])
 
 
 def test_oracle_update_golden():
@@ -47,7 +51,7 @@ def test_oracle_update_golden():
                                False)
         assert [r["active_blocks"], r["active_centers"], r["born_centers"], r["rejected"]] == \
             list(d["reports"][s])
-    np.testing.assert_allclose(m.weights(), d["weights"], rtol=1e-12, atol=1e-14)
+    assert np.linalg.norm(m.weights() - d["weights"]) <= 1e-10 * np.linalg.norm(d["weights"])
 
 
 # ---- GPU: device path vs fixtures ------------------------------------------------
@@ -68,17 +72,18 @@ def test_gpu_matches_golden(gpu_ctx):
     g.set_weights(e["weights"])  # evaluate the golden weights exactly
     z, s, gx, gy = g.predict(e["q"])
     assert np.array_equal(s, e["sup"])
-    scale = np.abs(e["z"]).max()
-    np.testing.assert_allclose(z, e["z"], rtol=1e-9, atol=1e-9 * scale)
-    np.testing.assert_allclose(gx, e["gx"], rtol=1e-9, atol=1e-9 * np.abs(e["gx"]).max())
+    assert_values_close(z, e["z"], e["scale_z"], 1e-9, what="z")
+    assert_values_close(gx, e["gx"], e["scale_g"], 1e-9, what="gx")
+    assert_values_close(gy, e["gy"], e["scale_g"], 1e-9, what="gy")
 
     mf = load("manifold.npz")
     rows, ne = kin.manifold_rows(g, mf["R"], mf["t"], mf["h"], 0.0, 1.0, 0.05,
                                  want=("r", "J", "valid"))
     assert np.array_equal(rows["valid"], mf["valid"])
-    np.testing.assert_allclose(rows["r"], mf["r"], rtol=1e-9, atol=1e-9)
-    np.testing.assert_allclose(rows["J"].reshape(6, -1).T, mf["J"].reshape(-1, 6), rtol=1e-8,
-                               atol=1e-8)
+    # 1e-9 of max(|ref|, the row's sum |w kappa| scale), no floor
+    sc = {"r": mf["scale_r"], "J": list(mf["scale_J"].T)}
+    assert_manifold_rows_close(rows["r"], rows["J"].reshape(6, -1).T, mf["r"],
+                               mf["J"].reshape(-1, 6), sc, rtol=1e-9)
     np.testing.assert_allclose(ne.A[np.triu_indices(6)], mf["ne"][:21], rtol=1e-9, atol=1e-9)
 
     u = load("update.npz")

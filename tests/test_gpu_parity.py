@@ -8,7 +8,8 @@ import numpy as np
 import pytest
 
 import oracle as orc
-from helpers import assert_values_close, c1_inputs, make_field, rel_norm, scales, so3_exp, uniform_xy
+from helpers import (assert_manifold_rows_close, assert_values_close, c1_inputs, make_field,
+                     manifold_row_scales, rel_norm, scales, so3_exp, uniform_xy)
 from paper_2509_26222_b200 import kinematics as kin
 from paper_2509_26222_b200 import terrain as T
 
@@ -132,12 +133,11 @@ def test_manifold_rows_parity(gpu_ctx):
     ref, ne_ref = o.manifold_rows(R, t, h, 0.0, 1.0, 0.05)
     assert np.array_equal(rows["valid"], ref["valid"])
     J = rows["J"].reshape(6, -1).T
-    xy = (h @ R.T + t)[:, :2]
-    hs, gs = scales(o, xy, k.sigma)
-    sc = np.maximum(hs, gs) + 1.0
-    assert_values_close(rows["r"], ref["r"], sc, what="r")
-    for c in range(6):
-        assert_values_close(J[:, c], ref["J"][:, c], sc * (1 + np.abs(h).sum(1)), what=f"J{c}")
+    # SURVEY §8d scale, no additive floor: r and J within 1e-9 of
+    # max(|ref|, s sum|w kappa| (...)) per row
+    sc = manifold_row_scales(o, R, t, h, ref["J"])
+    assert_manifold_rows_close(rows["r"], J, ref["r"], ref["J"], sc, rtol=1e-9)
+    assert_values_close(rows["raw"], ref["raw"], sc["raw"], 1e-9, what="raw")
     A = ne.A[np.triu_indices(6)]
     np.testing.assert_allclose(A, ne_ref[:21], rtol=1e-9, atol=1e-9 * np.abs(ne_ref[:21]).max())
     np.testing.assert_allclose(ne.g, ne_ref[21:27], rtol=1e-9, atol=1e-9 * np.abs(ne_ref[21:27]).max())
