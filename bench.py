@@ -827,7 +827,8 @@ def main():
         result["batch_fit_c5"] = run_batch_fit_c5(torch, local, rank, world)
     if rank == 0 and world == 1:
         dfma, dmma = C.c_double(), C.c_double()
-        lib.tlg_measure_fp64_peak(ctx.handle, C.byref(dfma), C.byref(dmma))
+        __import__("paper_2509_26222_b200._abi", fromlist=["load_diag"]).load_diag().tlg_diag_fp64_peak(
+            ctx.handle, C.byref(dfma), C.byref(dmma))
         result["fp64_peak_tflops"] = {"dfma": dfma.value, "dmma": dmma.value}
         # FP64 view of the same kernel (pairs/s based)
         if not args.no_update:

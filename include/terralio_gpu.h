@@ -103,21 +103,6 @@ uint64_t tlg_ctx_launch_count(const tlg_ctx* ctx);
  * kernel: 0 = manifold rows (K4), 1 = height/gradient eval (K3). */
 tlg_status tlg_ctx_set_profiling(tlg_ctx* ctx, int enable);
 tlg_status tlg_ctx_kernel_stats(tlg_ctx* ctx, int kernel, double* total_ms, uint64_t* launches);
-/* FP64 roofline microbenchmark on the context's device: sustained DFMA and
- * DMMA (mma.sync m8n8k4 f64) TFLOP/s. */
-tlg_status tlg_measure_fp64_peak(tlg_ctx* ctx, double* dfma_tflops, double* dmma_tflops);
-/* Dense-solver microbenchmark (diagnostics): op 0 = Cholesky of an n x n SPD
- * matrix, 1 = triangular solve with nrhs right-hand sides, 2 = GEMM
- * n x nrhs x n, 3 = 64-wide diagonal tile (nrhs repetitions), 4 = grid barrier,
- * 5 = Cholesky + inverse factor, 6 = 64-wide Cholesky. Best of `reps`, ms. */
-tlg_status tlg_debug_dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps, double* ms);
-/* Dense-solver check (diagnostics): Cholesky of the host n x n SPD matrix A
- * (column-major) on the device; L (lower, zero above) and X = L^-1 back to the
- * host. tile = 0 picks the production tiling, 32 / 64 force one; band in
- * (0, n) declares A lower-banded (A_ij = 0 for i - j > band). Returns
- * TLG_DOMAIN_ERROR when a pivot is not positive. */
-tlg_status tlg_debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, int band, double* L,
-                           double* X);
 
 /* ---- Batch-predict consumers ------------------------------ */
 /* select_ground_points (pipeline.cpp:150-170): points p (sensor frame, SoA)

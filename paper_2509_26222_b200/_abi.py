@@ -105,8 +105,6 @@ _SIGS = {
     "tlg_ctx_launch_count": (C.c_uint64, [_P]),
     "tlg_ctx_set_profiling": (_ST, [_P, _I]),
     "tlg_ctx_kernel_stats": (_ST, [_P, _I, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
-    "tlg_measure_fp64_peak": (_ST, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
-    "tlg_debug_dense_bench": (_ST, [_P, _I, _I, _I, _I, C.POINTER(C.c_double)]),
     "tlg_lm_step": (_ST, [_P, _P, C.c_double, _P]),
     "tlg_ne_min_eigenvalue": (_ST, [_P, _P, C.POINTER(C.c_double)]),
     "tlg_match_config_default": (_ST, [_P]),
@@ -121,7 +119,6 @@ _SIGS = {
                                        C.c_double, _SZ, _P, _P, _P, _I, C.POINTER(_SZ)]),
     "tlg_terrain_error_histogram": (_ST, [_P, _P, _P, _P, _SZ, _I, C.c_double, _I, _P, _P,
                                           C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
-    "tlg_debug_potrf": (_ST, [_P, _I, _P, _I, _I, _P, _P]),
     "tlg_kernel_finalize": (_ST, [C.POINTER(KernelParamsC)]),
     "tlg_kernel_eval": (_ST, [_P, C.POINTER(KernelParamsC), _P, _P, _P, _P, _SZ, _I, C.c_double,
                               _P, _I]),
@@ -192,6 +189,29 @@ def load() -> C.CDLL:
         raise ImportError("terralio_gpu ABI version mismatch")
     _lib = lib
     return lib
+
+
+_diag = None
+
+
+def load_diag() -> C.CDLL:
+    """Loads libterralio_diag.so: DIAGNOSTICS, not the product ABI
+    (include/terralio_diag.h: FP64 peak microbenchmark, dense-layer hooks)."""
+    global _diag
+    if _diag is None:
+        load()
+        path = _LIB_PATH.parent / "libterralio_diag.so"
+        d = C.CDLL(str(path))
+        d.tlg_diag_fp64_peak.restype = C.c_int
+        d.tlg_diag_fp64_peak.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        d.tlg_diag_dense_bench.restype = C.c_int
+        d.tlg_diag_dense_bench.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                           C.POINTER(C.c_double)]
+        d.tlg_diag_potrf.restype = C.c_int
+        d.tlg_diag_potrf.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                                     C.c_void_p]
+        _diag = d
+    return _diag
 
 
 def exported_symbols() -> list[str]:

@@ -26,8 +26,9 @@ NVCC_FLAGS = [
     "-I", str(ROOT / "include"),
 ]
 
-SOURCES = ["model.cu", "grid.cu", "eval.cu", "select.cu", "dense.cu", "update.cu", "peak.cu",
+SOURCES = ["model.cu", "grid.cu", "eval.cu", "select.cu", "dense.cu", "update.cu", "prof.cu",
            "scan.cu", "consumers.cu", "match.cu", "abi.cu"]
+DIAG_LIB = LIB_DIR / "libterralio_diag.so"
 # match.cu restates the matcher's scalar geometry (centroids, scatter, 3x3
 # eigen sweeps, residuals) with the reference's unfused rounding
 EXTRA_FLAGS = {"match.cu": ["-fmad=false"]}
@@ -70,6 +71,15 @@ def build_gpu(force: bool = False, verbose: bool = False) -> Path:
     if force or jobs or _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart_static",
               "-lrt", "-lpthread", "-ldl"])
+    # diagnostics (not the product ABI): its own library on top of the product
+    dsrc = CSRC / "diag" / "diag.cu"
+    dobj = OBJ_DIR / "diag.cu.o"
+    if force or _stale(dobj, [dsrc, *headers, ROOT / "include" / "terralio_diag.h"]):
+        _run([NVCC, *NVCC_FLAGS, "-c", str(dsrc), "-o", str(dobj)])
+    if force or _stale(DIAG_LIB, [dobj, LIB]):
+        _run([NVCC, *ARCH, "-shared", "-o", str(DIAG_LIB), str(dobj), "-L", str(LIB_DIR),
+              "-lterralio_gpu", "-Xlinker", f"-rpath,{LIB_DIR}", "-lcudart_static", "-lrt",
+              "-lpthread", "-ldl"])
     return LIB
 
 

@@ -19,13 +19,10 @@ void upload_new_centres(tlg_model* m, size_t first);
 uint32_t add_center_host(tlg_model* m, double x, double y);
 void moment_device(tlg_model* m, const double* x, const double* y, size_t n, uint32_t* rowp,
                    uint32_t** ids, double** vals, size_t* nnz);
-void fp64_peak(tlg_ctx* ctx, double* dfma, double* dmma);
 void manifold_device_streamed(tlg_model* m, const double R[9], const double t[3],
                               const double* hx, const double* hy, const double* hz, size_t n,
                               double wheel_radius, double lambda_M, double huber, double* r,
                               double* J, uint8_t* valid, double* raw, tlg_normal_eq* ne);
-double dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps);
-bool debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X, int band);
 size_t select_ground_device(tlg_ctx* ctx, const double* px, const double* py, const double* pz,
                             const uint8_t* kind, size_t n, const double R[9], const double t[3],
                             const double roi[4], double radius, double voxel, size_t max_points,
@@ -189,26 +186,6 @@ tlg_status tlg_ctx_kernel_stats(tlg_ctx* ctx, int kernel, double* total_ms, uint
     require(kernel >= 0 && kernel < 4, TLG_INVALID_ARGUMENT, "bad kernel id");
     if (total_ms) *total_ms = ctx->prof_ms[kernel];
     if (launches) *launches = ctx->prof_n[kernel];
-  });
-}
-
-tlg_status tlg_debug_dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps, double* ms) {
-  return guard([&] {
-    check_ptr(ctx, "ctx");
-    check_ptr(ms, "ms");
-    *ms = dense_bench(ctx, op, n, nrhs, reps);
-  });
-}
-
-tlg_status tlg_debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, int band, double* L,
-                           double* X) {
-  return guard([&] {
-    check_ptr(ctx, "ctx");
-    check_ptr(A, "A");
-    require(n > 0, TLG_INVALID_ARGUMENT, "n must be positive");
-    require(tile == 0 || tile == 32 || tile == 64, TLG_INVALID_ARGUMENT, "tile must be 0, 32 or 64");
-    if (!debug_potrf(ctx, n, A, tile, L, X, band > 0 && band < n ? band : n))
-      throw Error(TLG_DOMAIN_ERROR, "matrix is not positive definite");
   });
 }
 
@@ -391,15 +368,6 @@ tlg_status tlg_feature_normal_eq(tlg_map* m, const double R[9], const double t[3
   });
 }
 
-tlg_status tlg_measure_fp64_peak(tlg_ctx* ctx, double* dfma, double* dmma) {
-  return guard([&] {
-    check_ptr(ctx, "ctx");
-    double a = 0, b = 0;
-    fp64_peak(ctx, &a, &b);
-    if (dfma) *dfma = a;
-    if (dmma) *dmma = b;
-  });
-}
 
 tlg_status tlg_kernel_finalize(tlg_kernel_params* p) {
   return guard([&] {

@@ -959,8 +959,8 @@ __global__ void __launch_bounds__(128) k_trsm_tiles(const double* __restrict__ L
   }
 }
 
-static void potrf_lower32(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X,
-                          int ldx, int band) {
+void potrf_lower32(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X, int ldx,
+                   int band) {
   const int nt = (n + NB32 - 1) / NB32;
   int bwt = std::min(nt - 1, (std::max(band, 0) + NB32 - 1) / NB32);
   double* linv = ctx->ws<double>(S_LINV, static_cast<size_t>(nt) * NB32 * NB32);
@@ -1012,107 +1012,6 @@ void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X, 
   TLG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_potrf_coop), dim3(grid),
                                        dim3(128), args, smem, ctx->stream));
   ++ctx->launches;
-}
-
-__global__ void __launch_bounds__(128) k_diag_tile_only(double* A, int lda, double* linv, int* info,
-                                                        int reps) {
-  extern __shared__ double shd[];
-  for (int r = 0; r < reps; ++r) TLG_DIAG_TILE(A, lda, 64, linv, info, shd);
-}
-
-__global__ void __launch_bounds__(128) k_gridsync_only(int reps) {
-  cg::grid_group grid = cg::this_grid();
-  for (int r = 0; r < reps; ++r) grid.sync();
-}
-
-__global__ void k_zero_upper(double* A, int n) {
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)n * n;
-       e += (long long)gridDim.x * blockDim.x)
-    if (e / n > e % n) A[e] = 0.0;
-}
-
-__global__ void k_spd_fill(double* A, int n, unsigned seed) {
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)n * n;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int r = static_cast<int>(e % n), c = static_cast<int>(e / n);
-    const int lo = min(r, c), hi = max(r, c);
-    const unsigned hsh = (lo * 2654435761u) ^ (hi * 40503u) ^ seed;
-    A[e] = (r == c ? n : 0.0) + ((hsh % 1000) / 1000.0 - 0.5);
-  }
-}
-
-// Dense-layer microbenchmark (tlg_debug_dense_bench): op 0 = potrf, 1 = trsm
-// with nrhs columns, 2 = single 64x64x64 tile GEMM per CTA over `reps` CTAs.
-double dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps) {
-  cudaStream_t s = ctx->stream;
-  DBuf<double> A, B;
-  A.ensure(static_cast<size_t>(n) * n);
-  B.ensure(static_cast<size_t>(n) * std::max(nrhs, op == 5 ? n : 1));
-  DBuf<int> info;
-  info.ensure(1);
-  TLG_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
-  cudaEvent_t e0, e1;
-  TLG_CUDA(cudaEventCreate(&e0));
-  TLG_CUDA(cudaEventCreate(&e1));
-  float best = 1e30f;
-  for (int it = 0; it < reps; ++it) {
-    k_spd_fill<<<256, 256, 0, s>>>(A.p, n, 12345u + it);
-    TLG_CUDA(cudaMemsetAsync(B.p, 0, sizeof(double) * n * std::max(nrhs, op == 5 ? n : 1), s));
-    ctx->force_nb64 = (op == 1 || op == 6);
-    if (op == 1) potrf_lower(ctx, A.p, n, n, info.p);
-    TLG_CUDA(cudaEventRecord(e0, s));
-    if (op == 0 || op == 6) potrf_lower(ctx, A.p, n, n, info.p);
-    else if (op == 5) potrf_lower(ctx, A.p, n, n, info.p, B.p, n);
-    else if (op == 1) trsm_left_lower(ctx, A.p, n, n, B.p, nrhs, n, 0);
-    else if (op == 2) gemm(ctx, GemmDesc{n, nrhs, n, A.p, n, 0, A.p, n, 1, B.p, n, 1.0, 0.0, 0});
-    else if (op == 3) {
-      const int sm = sizeof(double) * kDiagSmemDoubles;
-      TLG_CUDA(cudaFuncSetAttribute(k_diag_tile_only, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-      k_diag_tile_only<<<1, 128, sm, s>>>(A.p, n, B.p, info.p, nrhs);
-    }
-    else {
-      int reps = nrhs;
-      void* args[] = {&reps};
-      TLG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_gridsync_only), dim3(n),
-                                           dim3(128), args, 0, s));
-    }
-    TLG_CUDA(cudaEventRecord(e1, s));
-    TLG_CUDA(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    TLG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    best = std::min(best, ms);
-  }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  ctx->force_nb64 = false;
-  return best;
-}
-
-bool debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X, int band) {
-  cudaStream_t s = ctx->stream;
-  const size_t nn = static_cast<size_t>(n) * n;
-  DBuf<double> dA, dX;
-  dA.ensure(nn);
-  dX.ensure(nn);
-  DBuf<int> info;
-  info.ensure(1);
-  TLG_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), s));
-  TLG_CUDA(cudaMemcpyAsync(dA.p, A, nn * 8, cudaMemcpyHostToDevice, s));
-  ctx->force_nb64 = (tile == 64);
-  if (tile == 32) {
-    potrf_lower32(ctx, dA.p, n, n, info.p, dX.p, n, band);
-  } else {
-    potrf_lower(ctx, dA.p, n, n, info.p, dX.p, n, band);
-  }
-  ctx->force_nb64 = false;
-  k_zero_upper<<<256, 256, 0, s>>>(dA.p, n);
-  TLG_LAUNCHED(ctx);
-  int h = 0;
-  TLG_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-  if (L) TLG_CUDA(cudaMemcpyAsync(L, dA.p, nn * 8, cudaMemcpyDeviceToHost, s));
-  if (X) TLG_CUDA(cudaMemcpyAsync(X, dX.p, nn * 8, cudaMemcpyDeviceToHost, s));
-  TLG_CUDA(cudaStreamSynchronize(s));
-  return h == 0;
 }
 
 void trsm_left_lower(tlg_ctx* ctx, const double* L, int n, int ldl, double* B, int nrhs,

@@ -35,10 +35,9 @@ void potrf_lower(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X =
 // B <- L^-1 B (trans = 0) or B <- L^-T B (trans = 1); L lower n x n, B n x nrhs.
 void trsm_left_lower(tlg_ctx* ctx, const double* L, int n, int ldl, double* B, int nrhs,
                      int ldb, int trans);
-// Diagnostics: factor a host matrix, return L and L^-1 (tile 0 / 32 / 64).
-bool debug_potrf(tlg_ctx* ctx, int n, const double* A, int tile, double* L, double* X,
-                 int band = -1);
-double dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps);
+// potrf_lower with 32-wide tiles regardless of n (the banded path).
+void potrf_lower32(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X, int ldx,
+                   int band);
 // x = (L L^T)^-1 b in place, L the (banded) 32-wide factor from the last
 // potrf_lower (band as passed to it).
 void band_solve(tlg_ctx* ctx, const double* L, int n, int ld, int band, double* b);

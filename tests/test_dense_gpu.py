@@ -15,7 +15,7 @@ def _potrf(A, tile, band=0):
     A = np.asfortranarray(A, dtype=np.float64)
     L = np.zeros((n, n), order="F")
     X = np.zeros((n, n), order="F")
-    _abi.check(_abi.load().tlg_debug_potrf(T.Context.default().handle, n, A.ctypes.data, tile,
+    _abi.check(_abi.load_diag().tlg_diag_potrf(T.Context.default().handle, n, A.ctypes.data, tile,
                                            band, L.ctypes.data, X.ctypes.data))
     return L, X
 

@@ -15,7 +15,7 @@ def potrf(A, tile=0):
     A = np.asfortranarray(A, dtype=np.float64)
     L = np.zeros((n, n), order="F")
     X = np.zeros((n, n), order="F")
-    _abi.check(_abi.load().tlg_debug_potrf(T.Context.default().handle, n, A.ctypes.data, tile, 0,
+    _abi.check(_abi.load_diag().tlg_diag_potrf(T.Context.default().handle, n, A.ctypes.data, tile, 0,
                                            L.ctypes.data, X.ctypes.data))
     return L, X
 

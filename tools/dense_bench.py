@@ -10,7 +10,7 @@ from paper_2509_26222_b200 import terrain as T  # noqa: E402
 
 def run(op, n, nrhs, reps=5):
     ms = C.c_double()
-    _abi.check(_abi.load().tlg_debug_dense_bench(T.Context.default().handle, op, n, nrhs, reps,
+    _abi.check(_abi.load_diag().tlg_diag_dense_bench(T.Context.default().handle, op, n, nrhs, reps,
                                                   C.byref(ms)))
     return ms.value
 

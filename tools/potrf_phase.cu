@@ -17,6 +17,16 @@ __device__ __forceinline__ unsigned long long gtime() {
 #include <cstdlib>
 #include <vector>
 namespace tlg {
+// SPD test matrix: n on the diagonal plus symmetric noise in [-0.5, 0.5)
+__global__ void k_spd_fill(double* A, int n, unsigned seed) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)n * n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(e % n), c = static_cast<int>(e / n);
+    const int lo = min(r, c), hi = max(r, c);
+    const unsigned hsh = (lo * 2654435761u) ^ (hi * 40503u) ^ seed;
+    A[e] = (r == c ? n : 0.0) + ((hsh % 1000) / 1000.0 - 0.5);
+  }
+}
 void throw_cuda(cudaError_t e, const char* w, const char* f, int l) {
   printf("cuda error %s at %s:%d (%s)\n", cudaGetErrorString(e), f, l, w);
   abort();
