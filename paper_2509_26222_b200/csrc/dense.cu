@@ -8,6 +8,7 @@
 #include <cooperative_groups.h>
 
 #include "dense.cuh"
+#include "dense_tile.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -640,81 +641,6 @@ __device__ __forceinline__ void gemm32_tile(const GemmDesc& d, int tm, int tn) {
           d.C[r + (size_t)c * d.ldc] = (d.beta == 0.0) ? v : fma(d.beta, cpre[i][j][h], v);
         }
       }
-}
-
-// One warp: L L^T = A for the kb x kb (kb <= 32) lower tile at A (lda), padded
-// with the identity; writes L back into A and X = L^-1 (32 x 32, ld 32,
-// zero above the diagonal) into linv. sh: kWarpPotrfSmem doubles.
-constexpr int kWarpPotrfSmem = 2 * 32 + 32 * 33 + 32;
-__device__ void warp_potrf_inv32(double* __restrict__ A, int lda, int kb,
-                                 double* __restrict__ linv, int* __restrict__ info,
-                                 double* __restrict__ sh) {
-  const int i = threadIdx.x & 31;
-  double* col = sh;            // [2][32] broadcast of the current column of L
-  double* xs = sh + 64;        // [32][33] transpose buffer
-  double* dinv = xs + 32 * 33;  // [32] 1 / L_jj
-  double a[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k)
-    a[k] = (i < kb && k < kb) ? (k <= i ? A[i + (size_t)k * lda] : 0.0) : (i == k ? 1.0 : 0.0);
-  TLG_PHASE(1);
-  bool bad = false;
-  double d = __shfl_sync(0xffffffffu, a[0], 0);
-  // Right-looking, lane i = row i. Entries above the diagonal hold garbage
-  // that is never read (pivots and columns only read k <= i).
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    bad |= !(d > 0.0) || !isfinite(d);
-    const double rs = rsqrt(d);
-    const double l = (i == j) ? d * rs : a[j] * rs;
-    a[j] = l;
-    if (i == j) dinv[j] = rs;
-    if (j + 1 < 32) {
-      // next pivot straight from the owner's own value (l_{j+1,j} = its l)
-      const double dn = fma(-l, l, a[j + 1]);
-      double* cb = col + (j & 1) * 32;
-      cb[i] = l;
-      d = __shfl_sync(0xffffffffu, dn, j + 1);
-      __syncwarp();
-#pragma unroll
-      for (int p = 0; p < 16; ++p) {
-        if (2 * p + 1 <= j) continue;  // both columns already eliminated
-        const double2 v = *reinterpret_cast<const double2*>(cb + 2 * p);
-        if (2 * p > j) a[2 * p] = fma(-l, v.x, a[2 * p]);
-        a[2 * p + 1] = fma(-l, v.y, a[2 * p + 1]);
-      }
-    }
-  }
-  TLG_PHASE(2);
-  if (bad && i == 0) atomicOr(info, 1);
-  // L back to A (lower part only) and to the transpose buffer (row i)
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    if (k <= i && i < kb && k < kb) A[i + (size_t)k * lda] = a[k];
-    xs[i * 33 + k] = (k <= i) ? a[k] : 0.0;
-  }
-  __syncwarp();
-  // X = L^-1, lane c = column c: X[k][c] = (delta_kc - sum_{p<k} L[k][p] X[p][c]) / L[k][k]
-  // accumulated right-looking so each row is one fma + one mul after the last.
-  TLG_PHASE(3);
-  double x[32];  // running right-hand side, becomes X[:, i] in place
-#pragma unroll
-  for (int k = 0; k < 32; ++k) x[k] = (k == i) ? 1.0 : 0.0;
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    x[k] *= dinv[k];
-#pragma unroll
-    for (int r = k + 1; r < 32; ++r) x[r] = fma(-xs[r * 33 + k], x[k], x[r]);
-  }
-  TLG_PHASE(4);
-  __syncwarp();
-  // transpose so that the store of linv (column-major) is coalesced
-#pragma unroll
-  for (int k = 0; k < 32; ++k) xs[k * 33 + i] = x[k];
-  __syncwarp();
-#pragma unroll
-  for (int c = 0; c < 32; ++c) linv[i + (size_t)c * NB32] = xs[i * 33 + c];
-  TLG_PHASE(5);
 }
 
 // bwt: lower tile bandwidth (tile (i, j) is zero for i - j > bwt; fill-in of

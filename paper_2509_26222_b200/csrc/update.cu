@@ -28,6 +28,7 @@
 #include <map>
 
 #include "dense.cuh"
+#include "dense_tile.cuh"
 
 namespace tlg {
 
@@ -82,7 +83,10 @@ __global__ void __launch_bounds__(128) k_mark_active_w(GridView g, const double*
     for (int gx = s.x_lo; gx <= s.x_hi; ++gx) {
       const int b = g.cell_start[gx * g.gny + s.y_lo], e = g.cell_start[gx * g.gny + s.y_hi + 1];
       for (int k = b + lane; k < e; k += 32)
-        if (sq2_exact(g.cx[k] - px, g.cy[k] - py) <= r2) active[g.id[k]] = 1;
+        if (sq2_exact(g.cx[k] - px, g.cy[k] - py) <= r2) {
+          const uint32_t id = g.id[k];
+          if (!active[id]) active[id] = 1;  // most ids are hit by many points
+        }
     }
   }
 }
@@ -342,6 +346,21 @@ __global__ void k_row_hist(const uint32_t* __restrict__ col, size_t nnz, uint32_
   if (e < nnz) atomicAdd(&cnt[col[e]], 1u);
 }
 
+// Few rows, many entries (C1: 256 rows, 1.2M entries): privatised counts in
+// shared memory, then one global add per nonzero bin and block.
+__global__ void k_row_hist_smem(const uint32_t* __restrict__ col, size_t nnz, int n,
+                                uint32_t* __restrict__ cnt) {
+  extern __shared__ uint32_t hb[];
+  for (int r = threadIdx.x; r < n; r += blockDim.x) hb[r] = 0;
+  __syncthreads();
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (size_t)gridDim.x * blockDim.x)
+    atomicAdd(&hb[col[e]], 1u);
+  __syncthreads();
+  for (int r = threadIdx.x; r < n; r += blockDim.x)
+    if (hb[r]) atomicAdd(&cnt[r], hb[r]);
+}
+
 // Gram row r: G[r, :] = sum_{j in row r} v_rj * Mt[:, j]; shared-memory row
 // accumulator, observations in ascending order -> deterministic. Adds into
 // column r of H (H symmetric, col-major) so writes are coalesced.
@@ -371,28 +390,36 @@ struct TCsr {
   double* val;
 };
 
-// Banded Gram: one warp per row r accumulates row r of Mt Mt^T over the
-// columns [r - band, r + band] in a per-warp shared window (observations in
-// ascending order, an observation's entries have distinct columns -> no
-// races, deterministic), then adds the window into column r of H.
+// Banded Gram: one warp per (row r, observation chunk c) accumulates that
+// chunk's part of row r of Mt Mt^T over the columns [r - band, r + band] in a
+// per-warp shared window (observations in ascending order, an observation's
+// entries have distinct columns -> no races, deterministic). With one chunk
+// per row the window is added into column r of H; with nch > 1 (few rows,
+// many observations per row: the C1 regime) each chunk's window goes to
+// partials[c][r][:] and k_gram_chunks_reduce sums the chunks in order.
 constexpr int kGramWarps = 4;
 __global__ void __launch_bounds__(32 * kGramWarps) k_gram_rows_band(
     const uint32_t* __restrict__ trowp, const uint32_t* __restrict__ tobs,
     const double* __restrict__ tval, const uint32_t* __restrict__ rowp,
     const uint32_t* __restrict__ col, const double* __restrict__ val, int n, int band,
-    int lower_only, double* __restrict__ H, int ldh) {
+    int lower_only, double* __restrict__ H, int ldh, int nch, double* __restrict__ partials) {
   extern __shared__ double gsm[];
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
   // lower_only: row r accumulates only columns >= r (band storage of the
   // lower triangle; the symmetric half is neither computed nor written)
   const int width = lower_only ? band + 1 : 2 * band + 1;
   double* acc = gsm + wq * width;
-  for (int r = blockIdx.x * kGramWarps + wq; r < n; r += gridDim.x * kGramWarps) {
+  const long long items = static_cast<long long>(n) * nch;
+  for (long long it = blockIdx.x * (long long)kGramWarps + wq; it < items;
+       it += (long long)gridDim.x * kGramWarps) {
+    const int r = static_cast<int>(it / nch), ch = static_cast<int>(it % nch);
     const int lo = lower_only ? r : r - band;
     for (int s = lane; s < width; s += 32) acc[s] = 0.0;
     __syncwarp();
-    const uint32_t q_end = trowp[r + 1];
-    for (uint32_t q0 = trowp[r]; q0 < q_end; q0 += 32) {
+    const uint32_t rb = trowp[r], rn = trowp[r + 1] - rb;
+    const uint32_t q_end = rb + static_cast<uint32_t>((static_cast<unsigned long long>(rn) * (ch + 1)) / nch);
+    for (uint32_t q0 = rb + static_cast<uint32_t>((static_cast<unsigned long long>(rn) * ch) / nch);
+         q0 < q_end; q0 += 32) {
       // lane-parallel fetch of 32 observations' metadata (one latency)
       const uint32_t qq = q0 + lane;
       uint32_t jb = 0, je = 0;
@@ -451,8 +478,30 @@ __global__ void __launch_bounds__(32 * kGramWarps) k_gram_rows_band(
       }
     }
     const int c0 = max(lo, 0), c1 = min(r + band, n - 1);  // H[c][r]: column r, c >= lo
-    for (int cc = c0 + lane; cc <= c1; cc += 32) H[cc + (size_t)r * ldh] += acc[cc - lo];
+    if (nch == 1) {
+      for (int cc = c0 + lane; cc <= c1; cc += 32) H[cc + (size_t)r * ldh] += acc[cc - lo];
+    } else {
+      double* pr = partials + (static_cast<size_t>(ch) * n + r) * width;
+      for (int cc = c0 + lane; cc <= c1; cc += 32) pr[cc - lo] = acc[cc - lo];
+    }
     __syncwarp();
+  }
+}
+
+// Chunk partials of the banded Gram summed in chunk order into H.
+__global__ void k_gram_chunks_reduce(const double* __restrict__ partials, int n, int band,
+                                     int lower_only, int nch, double* __restrict__ H, int ldh) {
+  const int width = lower_only ? band + 1 : 2 * band + 1;
+  const long long tot = static_cast<long long>(n) * width;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(e / width), s = static_cast<int>(e % width);
+    const int lo = lower_only ? r : r - band;
+    const int cc = lo + s;
+    if (cc < 0 || cc >= n || cc > r + band) continue;
+    double v = 0.0;
+    for (int ch = 0; ch < nch; ++ch) v += partials[(static_cast<size_t>(ch) * n + r) * width + s];
+    H[cc + static_cast<size_t>(r) * ldh] += v;
   }
 }
 
@@ -464,9 +513,26 @@ static void gram_band(tlg_ctx* ctx, const TCsr& t, const Csr& c, int n, int band
     if (smem_band > 48 * 1024)
       TLG_CUDA(cudaFuncSetAttribute(k_gram_rows_band, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem_band));
-    const unsigned blocks = static_cast<unsigned>((n + kGramWarps - 1) / kGramWarps);
+    // observation chunks per row: enough warps to fill the GPU when rows are
+    // few and long (~128 observations per chunk), within a partials budget
+    const double obs_per_row = n ? static_cast<double>(c.nnz) / n : 0.0;
+    int nch = static_cast<int>(std::min(obs_per_row / 256.0,
+                                        (1.0 * ctx->num_sms * 8 * kGramWarps) / std::max(n, 1)));
+    const size_t per_chunk = static_cast<size_t>(n) * width * sizeof(double);
+    nch = std::max(1, std::min<int>(nch, static_cast<int>((256u << 20) / std::max<size_t>(per_chunk, 1))));
+    double* partials = nch > 1 ? ctx->ws<double>(S_GRAMPART, static_cast<size_t>(nch) * n * width) : nullptr;
+    const long long items = static_cast<long long>(n) * nch;
+    const unsigned blocks = static_cast<unsigned>(
+        std::min<long long>((items + kGramWarps - 1) / kGramWarps, 1ll << 20));
     k_gram_rows_band<<<blocks, 32 * kGramWarps, smem_band, ctx->stream>>>(
-        t.rowp, t.obs, t.val, c.rowp, c.col, c.val, n, band, lower_only ? 1 : 0, H, ldh);
+        t.rowp, t.obs, t.val, c.rowp, c.col, c.val, n, band, lower_only ? 1 : 0, H, ldh, nch,
+        partials);
+    if (nch > 1) {
+      TLG_LAUNCHED(ctx);
+      const long long tot = static_cast<long long>(n) * width;
+      k_gram_chunks_reduce<<<static_cast<unsigned>(std::min<long long>((tot + 255) / 256, 8 * 148)), 256, 0,
+                             ctx->stream>>>(partials, n, band, lower_only ? 1 : 0, nch, H, ldh);
+    }
   } else {
     require(!lower_only, TLG_RUNTIME_ERROR, "banded Gram: band too wide for band storage");
     const size_t smem = static_cast<size_t>(n) * 8;
@@ -478,14 +544,20 @@ static void gram_band(tlg_ctx* ctx, const TCsr& t, const Csr& c, int n, int band
 }
 
 // rhs b[r] = sum_{j in row r} v_rj * c_j  (c = residual or z)
+// One warp per row: lane l sums entries l, l + 32, ... in order, then a
+// fixed xor tree (deterministic; rows of thousands of entries in the C1
+// regime no longer run on a single thread).
 __global__ void k_row_dot(const uint32_t* __restrict__ trowp, const uint32_t* __restrict__ tobs,
                           const double* __restrict__ tval, const double* __restrict__ c, int n,
                           double* __restrict__ b) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (r >= n) return;
   double s = 0.0;
-  for (uint32_t q = trowp[r]; q < trowp[r + 1]; ++q) s = fma(tval[q], c[tobs[q]], s);
-  b[r] = s;
+  for (uint32_t q = trowp[r] + lane; q < trowp[r + 1]; q += 32) s = fma(tval[q], c[tobs[q]], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) b[r] = s;
 }
 
 __global__ void k_copy_to_pool_blocks(const BlockTab* __restrict__ tab, const double* __restrict__ H,
@@ -546,76 +618,105 @@ static bool spd_inverse(tlg_ctx* ctx, const double* src, int lds, int n, double*
 }
 
 // All active blocks at once: one CTA per block q inverts info_inv_q (SPD,
-// n_q <= kBatchInvMax) in shared memory — right-looking Cholesky L, then
-// X = L^-1 by the same right-looking sweep on the identity, then
-// A^-1 = X^T X — and writes it into the diagonal block of H (ld ldh).
-// Warps walk rows, lanes walk columns. info != 0 on a non-positive pivot.
+// n_q <= kBatchInvMax) in shared memory with 32-wide tiles — per tile column
+// k the diagonal tile is factored and inverted by one warp in registers
+// (warp_potrf_inv32, dense_tile.cuh), the panel becomes a product with that
+// inverse and the trailing triangle a rank-32 update; then X = L^-1 tile row
+// by tile row (X_ij = -Linv_ii sum_m L_im X_mj), and A^-1 = X^T X is written
+// into the diagonal block of H (ld ldd). ~6 barriers per tile instead of 5 per
+// column; info != 0 on a non-positive pivot.
 constexpr int kBatchInvMax = 112;
+constexpr int kInvThreads = 256;
 struct InvJob {  // dst (ldd) <- src(lds)^-1, n x n SPD
   const double* src;
   double* dst;
   int lds, ldd, n, pad;
 };
-__global__ void __launch_bounds__(256) k_batched_spd_inverse(const InvJob* __restrict__ jobs,
-                                                             int* __restrict__ info) {
+__global__ void __launch_bounds__(kInvThreads) k_batched_spd_inverse(const InvJob* __restrict__ jobs,
+                                                                     int* __restrict__ info) {
   extern __shared__ double sm[];
   const InvJob b = jobs[blockIdx.x];
   const int n = b.n, P = n + 1, t = threadIdx.x, lane = t & 31, wq = t >> 5;
-  const int nw = blockDim.x >> 5;
-  double* a = sm;          // a[r * P + c]: lower triangle -> L
-  double* x = sm + n * P;  // x[r * P + c]: X = L^-1 (lower)
+  constexpr int nw = kInvThreads / 32;
+  double* a = sm;                 // a[r + c P]: lower triangle -> L
+  double* x = a + n * P;          // x[r + c P]: X = L^-1 (lower)
+  double* linv = x + n * P;       // 32 x 32, ld 32
+  double* scratch = linv + 32 * 32;
   const double* src = b.src;
-  for (int e = t; e < n * n; e += blockDim.x) {
+  for (int e = t; e < n * n; e += kInvThreads) {
     const int r = e % n, c = e / n;
-    if (r >= c) a[r * P + c] = src[r + (size_t)c * b.lds];
-    x[r * P + c] = (r == c) ? 1.0 : 0.0;
+    a[r + c * P] = (r >= c) ? src[r + (size_t)c * b.lds] : 0.0;
+    x[r + c * P] = 0.0;
   }
   __syncthreads();
-  __shared__ double piv;
-  for (int j = 0; j < n; ++j) {
-    if (t == 0) {
-      const double d = a[j * P + j];
-      if (!(d > 0.0) || !isfinite(d)) atomicOr(info, 1);
-      const double l = sqrt(d);
-      a[j * P + j] = l;
-      piv = 1.0 / l;
+  const int nt = (n + 31) / 32;
+  for (int k = 0; k < nt; ++k) {
+    const int k0 = 32 * k, kb = min(32, n - k0), r0 = k0 + kb;
+    if (wq == 0) warp_potrf_inv32(a + k0 + k0 * P, P, kb, linv, info, scratch);
+    __syncthreads();
+    // X_kk = Linv_kk
+    for (int e = t; e < kb * kb; e += kInvThreads) {
+      const int r = e % kb, c = e / kb;
+      x[k0 + r + (k0 + c) * P] = linv[r + c * 32];
+    }
+    // panel rows r >= r0: L[r][k0 + c] = sum_p A[r][k0 + p] Linv[c][p]
+    for (int r = r0 + wq; r < n; r += nw) {
+      double v = 0.0;
+      if (lane < kb)
+        for (int p = 0; p <= lane; ++p) v = fma(a[r + (k0 + p) * P], linv[lane + p * 32], v);
+      __syncwarp();
+      if (lane < kb) a[r + (k0 + lane) * P] = v;
     }
     __syncthreads();
-    for (int i = j + 1 + t; i < n; i += blockDim.x) a[i * P + j] *= piv;
-    __syncthreads();
-    for (int r = j + 1 + wq; r < n; r += nw) {
-      const double lr = a[r * P + j];
-      for (int c = j + 1 + lane; c <= r; c += 32) a[r * P + c] = fma(-lr, a[c * P + j], a[r * P + c]);
+    // trailing lower triangle: A[r][c] -= sum_p L[r][k0 + p] L[c][k0 + p]
+    const int m = n - r0;
+    for (int e = t; e < m * m; e += kInvThreads) {
+      const int r = r0 + e % m, c = r0 + e / m;
+      if (r < c) continue;
+      double v = a[r + c * P];
+      for (int p = 0; p < kb; ++p) v = fma(-a[r + (k0 + p) * P], a[c + (k0 + p) * P], v);
+      a[r + c * P] = v;
     }
     __syncthreads();
   }
-  // X = L^-1: row k final = row k / L_kk, then rows below lose L_rk * row k
-  for (int k = 0; k < n; ++k) {
-    const double inv = 1.0 / a[k * P + k];
-    for (int c = t; c <= k; c += blockDim.x) x[k * P + c] *= inv;
+  // X = L^-1 below the diagonal tiles, tile row i ascending:
+  // T = sum_{m=j}^{i-1} L_im X_mj (cols of tile column j), X_ij = -Linv_ii T
+  for (int i = 1; i < nt; ++i) {
+    const int i0 = 32 * i, ib = min(32, n - i0);
+    // T into x's (i, j) tiles (currently zero), j < i
+    for (int e = t; e < ib * i0; e += kInvThreads) {
+      const int r = i0 + e % ib, c = e / ib;  // c < i0
+      double v = 0.0;
+      for (int q = c; q < i0; ++q) v = fma(a[r + q * P], x[q + c * P], v);
+      x[r + c * P] = v;
+    }
     __syncthreads();
-    for (int r = k + 1 + wq; r < n; r += nw) {
-      const double lr = a[r * P + k];
-      for (int c = lane; c <= k; c += 32) x[r * P + c] = fma(-lr, x[k * P + c], x[r * P + c]);
+    // X_ij = -Linv_ii T: Linv_ii is x's diagonal tile (i, i); column-wise in place
+    for (int c = wq; c < i0; c += nw) {
+      double v = 0.0;
+      if (lane < ib)
+        for (int q = 0; q <= lane; ++q) v = fma(x[i0 + lane + (i0 + q) * P], x[i0 + q + c * P], v);
+      __syncwarp();
+      if (lane < ib) x[i0 + lane + c * P] = -v;
     }
     __syncthreads();
   }
   // A^-1 = X^T X: (r, c) = sum_{p >= max(r, c)} x_pr x_pc; write both halves
   double* dst = b.dst;
   const int ldh = b.ldd;
-  for (int r = wq; r < n; r += nw) {
-    for (int c = lane; c <= r; c += 32) {
-      double s0 = 0.0, s1 = 0.0;
-      int p = r;
-      for (; p + 1 < n; p += 2) {
-        s0 = fma(x[p * P + r], x[p * P + c], s0);
-        s1 = fma(x[(p + 1) * P + r], x[(p + 1) * P + c], s1);
-      }
-      if (p < n) s0 = fma(x[p * P + r], x[p * P + c], s0);
-      const double v = s0 + s1;
-      dst[r + (size_t)c * ldh] = v;
-      dst[c + (size_t)r * ldh] = v;
+  for (int e = t; e < n * n; e += kInvThreads) {
+    const int r = e % n, c = e / n;
+    if (r < c) continue;
+    double s0 = 0.0, s1 = 0.0;
+    int p = r;
+    for (; p + 1 < n; p += 2) {
+      s0 = fma(x[p + r * P], x[p + c * P], s0);
+      s1 = fma(x[p + 1 + r * P], x[p + 1 + c * P], s1);
     }
+    if (p < n) s0 = fma(x[p + r * P], x[p + c * P], s0);
+    const double v = s0 + s1;
+    dst[r + (size_t)c * ldh] = v;
+    dst[c + (size_t)r * ldh] = v;
   }
 }
 
@@ -629,10 +730,10 @@ static void batched_spd_inverse(tlg_ctx* ctx, const std::vector<InvJob>& jobs, i
   std::memcpy(h, jobs.data(), bytes);
   InvJob* d = reinterpret_cast<InvJob*>(ctx->ws<char>(S_BLKTAB, bytes));
   TLG_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  const int smem = 2 * maxn * (maxn + 1) * 8;
+  const int smem = (2 * maxn * (maxn + 1) + 32 * 32 + kWarpPotrfSmem) * 8;
   TLG_CUDA(cudaFuncSetAttribute(k_batched_spd_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem));
-  k_batched_spd_inverse<<<static_cast<unsigned>(jobs.size()), 256, smem, ctx->stream>>>(d, info);
+  k_batched_spd_inverse<<<static_cast<unsigned>(jobs.size()), kInvThreads, smem, ctx->stream>>>(d, info);
   TLG_LAUNCHED(ctx);
 }
 
@@ -674,7 +775,12 @@ static TCsr transpose_csr(tlg_ctx* ctx, const Csr& c, size_t m, int n) {
   }
   TLG_CUDA(cudaMemsetAsync(t.rowp, 0, (n + 1) * sizeof(uint32_t), s));
   if (c.nnz) {
-    k_row_hist<<<(unsigned)((c.nnz + 255) / 256), 256, 0, s>>>(c.col, c.nnz, t.rowp);
+    if (n <= 12288) {
+      const unsigned b = static_cast<unsigned>(std::min<size_t>((c.nnz + 1023) / 1024, 2 * 148));
+      k_row_hist_smem<<<b, 256, n * sizeof(uint32_t), s>>>(c.col, c.nnz, n, t.rowp);
+    } else {
+      k_row_hist<<<(unsigned)((c.nnz + 255) / 256), 256, 0, s>>>(c.col, c.nnz, t.rowp);
+    }
     TLG_LAUNCHED(ctx);
   }
   size_t tmp = 0;
@@ -1110,7 +1216,7 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
     tr.mark("H0");
     const TCsr t = transpose_csr(ctx, c, mm, n);
     gram_band(ctx, t, c, n, band, H, n);
-    k_row_dot<<<(n + 255) / 256, 256, 0, s>>>(t.rowp, t.obs, t.val, resid, n, dw);
+    k_row_dot<<<(n + 7) / 8, 256, 0, s>>>(t.rowp, t.obs, t.val, resid, n, dw);
     TLG_LAUNCHED(ctx);
     // X = L^-1 from the factorisation; (H^-1)_qq = X[:,q]^T X[:,q]
     tr.mark("gram");
@@ -1259,7 +1365,7 @@ static void batch_assemble(tlg_model* m, const BatchPlan& p, const double* x, co
   const Csr c = build_csr(m, x, y, mm, rowof, m->kc.neg_inv_2st2, m->kc.scale, false, nullptr);
   const TCsr t = transpose_csr(ctx, c, mm, n);
   gram_band(ctx, t, c, n, p.band, H, ld, /*lower_only=*/true);
-  k_row_dot<<<(n + 255) / 256, 256, 0, s>>>(t.rowp, t.obs, t.val, z, n, b);
+  k_row_dot<<<(n + 7) / 8, 256, 0, s>>>(t.rowp, t.obs, t.val, z, n, b);
   TLG_LAUNCHED(ctx);
 }
 
