@@ -166,6 +166,16 @@ tlg_status tlg_build_correspondences(tlg_map* map, const double* px, const doubl
 tlg_status tlg_correspondences_get(tlg_map* map, int32_t* kind, uint32_t* feature,
                                    double* params, double* weight, int32_t* label, double* dist,
                                    double* fitq, size_t cap);
+/* total_cost's feature rows (scan_matcher.cpp:196-214) for n HOST
+ * correspondences at pose (R, t): kind (0 edge -> 3 rows, 1 plane -> 1
+ * row), p_sensor (3 per corr.), params (7 per corr., as
+ * tlg_correspondences_get), weight. Host outputs r[rows] and J (column-major
+ * rows x 6, ld = rows); *rows always set, TLG_BUFFER_TOO_SMALL when it
+ * exceeds cap_rows. */
+tlg_status tlg_feature_rows(tlg_ctx* ctx, const int32_t* kind, const double* p_sensor,
+                            const double* params, const double* weight, size_t n,
+                            const double R[9], const double t[3], double* r, double* J,
+                            size_t cap_rows, size_t* rows);
 /* Feature rows of total_cost at pose (R, t) for the last correspondences,
  * reduced to the normal equations (valid = rows). */
 tlg_status tlg_feature_normal_eq(tlg_map* map, const double R[9], const double t[3],

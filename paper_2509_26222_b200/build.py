@@ -99,7 +99,8 @@ def build_oracle(force: bool = False) -> Path:
     return odir / "_build" / "liboracle.so"
 
 
-DROPIN_TESTS = ["test_kernel", "test_center_select", "test_terrain_model", "test_kinematics"]
+DROPIN_TESTS = ["test_kernel", "test_center_select", "test_terrain_model", "test_kinematics",
+                "test_matcher"]
 DROPIN_OUT = ROOT / "tests" / "cpp" / "_build"
 
 

@@ -33,6 +33,9 @@ void map_insert(tlg_map* m, const double* px, const double* py, const double* pz
 size_t build_correspondences_device(tlg_map* m, const double* px, const double* py,
                                     const double* pz, const uint8_t* kind, size_t n,
                                     const double R[9], const double t[3], const double cfgv[11]);
+void feature_rows_device(tlg_ctx* ctx, size_t nc, const int32_t* kind, const double* ps,
+                         const double* par, const double* wgt, const double R[9], const double t[3],
+                         double* r, double* J, size_t* rows_out);
 void feature_normal_eq_device(tlg_map* m, const double R[9], const double t[3], double ne29[29]);
 tlg_map* map_new(tlg_ctx* ctx, double voxel, size_t window);
 void map_free(tlg_map* m);
@@ -349,6 +352,24 @@ tlg_status tlg_correspondences_get(tlg_map* m, int32_t* kind, uint32_t* feature,
   return guard([&] {
     check_ptr(m, "map");
     correspondences_host(m, kind, feature, params, weight, label, dist, fitq, cap);
+  });
+}
+
+tlg_status tlg_feature_rows(tlg_ctx* ctx, const int32_t* kind, const double* p_sensor,
+                            const double* params, const double* weight, size_t n,
+                            const double R[9], const double t[3], double* r, double* J,
+                            size_t cap_rows, size_t* rows) {
+  return guard([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(R, "R");
+    check_ptr(t, "t");
+    check_ptr(rows, "rows");
+    size_t need = 0;
+    for (size_t j = 0; j < n; ++j) need += kind[j] == 0 ? 3 : 1;
+    *rows = need;
+    if (need > cap_rows) throw Error(TLG_BUFFER_TOO_SMALL, "feature rows: buffer too small");
+    size_t got = 0;
+    feature_rows_device(ctx, n, kind, p_sensor, params, weight, R, t, r, J, &got);
   });
 }
 

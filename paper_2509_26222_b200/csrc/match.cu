@@ -613,6 +613,48 @@ __global__ void __launch_bounds__(kNeThreads) k_feature_ne(size_t nc, const int*
   }
 }
 
+// total_cost feature rows materialised (scan_matcher.cpp:196-214): the rows
+// of correspondence j start at row0[j] (3 for an edge, 1 for a plane); J is
+// column-major rows x 6 (Eigen's CostEval layout, ld = rows). Same
+// arithmetic as k_feature_ne, which reduces these rows.
+__global__ void k_feature_rows(size_t nc, const int* __restrict__ ck, const double* __restrict__ ps,
+                               const double* __restrict__ par, const double* __restrict__ wgt,
+                               const uint32_t* __restrict__ row0, Pose P, size_t rows,
+                               double* __restrict__ r_out, double* __restrict__ J_out) {
+  const size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (j >= nc) return;
+  const double s0 = ps[3 * j], s1 = ps[3 * j + 1], s2 = ps[3 * j + 2];
+  double pw[3];
+  xform(P, s0, s1, s2, pw[0], pw[1], pw[2]);
+  const double H[9] = {0.0, -s2, s1, s2, 0.0, -s0, -s1, s0, 0.0};
+  double dp[3][6];
+  for (int i = 0; i < 3; ++i)
+    for (int c = 0; c < 3; ++c) {
+      dp[i][c] = (-P.R[3 * i] * H[c] + -P.R[3 * i + 1] * H[3 + c]) + -P.R[3 * i + 2] * H[6 + c];
+      dp[i][3 + c] = (i == c) ? 1.0 : 0.0;
+    }
+  const double sw = sqrt(wgt[j]);
+  const double* pr = par + 7 * j;
+  const size_t o = row0[j];
+  if (ck[j] == 0) {
+    const double d[3] = {pr[3], pr[4], pr[5]};
+    double J[9];
+    for (int i = 0; i < 3; ++i)
+      for (int c = 0; c < 3; ++c) J[3 * i + c] = (i == c ? 1.0 : 0.0) - d[i] * d[c];
+    const double e[3] = {pw[0] - pr[0], pw[1] - pr[1], pw[2] - pr[2]};
+    for (int i = 0; i < 3; ++i) {
+      r_out[o + i] = sw * ((J[3 * i] * e[0] + J[3 * i + 1] * e[1]) + J[3 * i + 2] * e[2]);
+      for (int c = 0; c < 6; ++c)
+        J_out[o + i + c * rows] =
+            sw * ((J[3 * i] * dp[0][c] + J[3 * i + 1] * dp[1][c]) + J[3 * i + 2] * dp[2][c]);
+    }
+  } else {
+    r_out[o] = sw * (((pr[0] * pw[0] + pr[1] * pw[1]) + pr[2] * pw[2]) + pr[3]);
+    for (int c = 0; c < 6; ++c)
+      J_out[o + c * rows] = sw * ((pr[0] * dp[0][c] + pr[1] * dp[1][c]) + pr[2] * dp[2][c]);
+  }
+}
+
 template <typename T>
 size_t select_flagged(tlg_ctx* ctx, const uint8_t* flags, size_t n, uint32_t* out) {
   cudaStream_t s = ctx->stream;
@@ -959,6 +1001,41 @@ size_t build_correspondences_device(tlg_map* m, const double* px, const double* 
   TLG_CUDA(cudaStreamSynchronize(s));
   m->nc = cnt;
   return cnt;
+}
+
+void feature_rows_device(tlg_ctx* ctx, size_t nc, const int32_t* kind, const double* ps,
+                         const double* par, const double* wgt, const double R[9], const double t[3],
+                         double* r, double* J, size_t* rows_out) {
+  cudaStream_t s = ctx->stream;
+  std::vector<uint32_t> row0(nc);
+  size_t rows = 0;
+  for (size_t j = 0; j < nc; ++j) {
+    row0[j] = static_cast<uint32_t>(rows);
+    rows += kind[j] == 0 ? 3 : 1;
+  }
+  *rows_out = rows;
+  if (nc == 0) return;
+  int* dk = ctx->ws<int>(S_KEYS, nc);
+  double* dps = ctx->ws<double>(S_NODES_X, 3 * nc);
+  double* dpar = ctx->ws<double>(S_NODES_Y, 7 * nc);
+  double* dw = ctx->ws<double>(S_VALS, nc);
+  uint32_t* dr0 = ctx->ws<uint32_t>(S_VALS2, nc);
+  double* dr = ctx->ws<double>(S_OUT_R, rows);
+  double* dJ = ctx->ws<double>(S_OUT_J, 6 * rows);
+  TLG_CUDA(cudaMemcpyAsync(dk, kind, nc * 4, cudaMemcpyHostToDevice, s));
+  TLG_CUDA(cudaMemcpyAsync(dps, ps, 3 * nc * 8, cudaMemcpyHostToDevice, s));
+  TLG_CUDA(cudaMemcpyAsync(dpar, par, 7 * nc * 8, cudaMemcpyHostToDevice, s));
+  TLG_CUDA(cudaMemcpyAsync(dw, wgt, nc * 8, cudaMemcpyHostToDevice, s));
+  TLG_CUDA(cudaMemcpyAsync(dr0, row0.data(), nc * 4, cudaMemcpyHostToDevice, s));
+  Pose P;
+  for (int i = 0; i < 9; ++i) P.R[i] = R[i];
+  for (int i = 0; i < 3; ++i) P.t[i] = t[i];
+  k_feature_rows<<<(unsigned)((nc + 127) / 128), 128, 0, s>>>(nc, dk, dps, dpar, dw, dr0, P, rows, dr,
+                                                              dJ);
+  TLG_LAUNCHED(ctx);
+  TLG_CUDA(cudaMemcpyAsync(r, dr, rows * 8, cudaMemcpyDeviceToHost, s));
+  TLG_CUDA(cudaMemcpyAsync(J, dJ, 6 * rows * 8, cudaMemcpyDeviceToHost, s));
+  TLG_CUDA(cudaStreamSynchronize(s));
 }
 
 void feature_normal_eq_device(tlg_map* m, const double R[9], const double t[3], double ne29[29]) {

@@ -48,17 +48,18 @@ def _dropin():
 
 def test_reference_unit_tests_compile_against_dropin():
     """The reference's own test_kernel / test_center_select /
-    test_terrain_model / test_kinematics files (unchanged, compiled in place)
-    build and link against include/terralio_dropin + libterralio_gpu.so."""
+    test_terrain_model / test_kinematics / test_matcher files (unchanged,
+    compiled in place) build and link against include/terralio_dropin +
+    libterralio_gpu.so."""
     r = subprocess.run([str(_dropin()), "-ltc"], capture_output=True, text=True, timeout=60)
     assert r.returncode == 0, r.stderr
     cases = r.stdout.split("\n")
-    assert len([c for c in cases if c]) == 24
+    assert len([c for c in cases if c]) == 31
 
 
 @pytest.mark.gpu
 def test_reference_unit_tests_pass_on_gpu_dropin():
-    """...and all 24 of their cases pass with every call running on the GPU."""
+    """...and all 31 of their cases pass with every call running on the GPU."""
     r = subprocess.run([str(_dropin())], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert "24 passed | 0 failed" in r.stdout, r.stdout
+    assert "31 passed | 0 failed" in r.stdout, r.stdout
