@@ -256,10 +256,14 @@ class TerrainModel {
     for (std::size_t i = 0; i < n; ++i) s.centers[i] = {x[i], y[i]};
     return s;
   }
-  std::vector<double> weights() const {
-    std::vector<double> w(num_centers());
-    if (!w.empty()) gpu::check(tlg_model_get_weights(m_.get(), w.data(), TLG_HOST));
-    return w;
+  // host mirror, read from the device once per model change (not per call)
+  const std::vector<double>& weights() const {
+    if (w_at_ != ver_) {
+      w_.resize(num_centers());
+      if (!w_.empty()) gpu::check(tlg_model_get_weights(m_.get(), w_.data(), TLG_HOST));
+      w_at_ = ver_;
+    }
+    return w_;
   }
   std::size_t num_centers() const {
     size_t n = 0, b = 0;
@@ -272,9 +276,12 @@ class TerrainModel {
     return b;
   }
   std::uint32_t block_of(std::uint32_t center) const {
-    std::vector<std::uint32_t> b(num_centers());
-    gpu::check(tlg_model_get_block_index(m_.get(), b.data(), TLG_HOST));
-    return b.at(center);
+    if (bidx_at_ != ver_) {
+      bidx_.resize(num_centers());
+      if (!bidx_.empty()) gpu::check(tlg_model_get_block_index(m_.get(), bidx_.data(), TLG_HOST));
+      bidx_at_ = ver_;
+    }
+    return bidx_.at(center);
   }
   std::vector<std::uint32_t> block_members(std::uint32_t b) const {
     size_t n = 0;
@@ -313,6 +320,15 @@ class TerrainModel {
                         TLG_HOST));
     return {z, s != 0};
   }
+  // height, support flag and gradient of one point in one device call
+  HeightQuery predict_height_gradient(const Vec2& x, Vec2* grad) const {
+    double z = 0.0;
+    uint8_t s = 0;
+    Vec2 g;
+    gpu::check(tlg_eval(m_.get(), &x.v[0], &x.v[1], 1, TLG_HOST, &z, &s, &g.v[0], &g.v[1], TLG_HOST));
+    if (grad) *grad = g;
+    return {z, s != 0};
+  }
   Vec2 predict_gradient(const Vec2& x) const {
     Vec2 g;
     gpu::check(tlg_eval(m_.get(), &x.v[0], &x.v[1], 1, TLG_HOST, nullptr, nullptr, &g.v[0],
@@ -329,8 +345,11 @@ class TerrainModel {
   UpdateReport recursive_update(const TerrainObservation& obs, bool allow_birth = true) {
     const detail::Soa s = detail::split(obs.xy);
     tlg_update_report r{};
-    gpu::check(tlg_recursive_update(m_.get(), s.x.data(), s.y.data(), obs.z.data(), obs.xy.size(),
-                                    obs.z.size(), TLG_HOST, allow_birth ? 1 : 0, &r));
+    const tlg_status st = tlg_recursive_update(m_.get(), s.x.data(), s.y.data(), obs.z.data(),
+                                               obs.xy.size(), obs.z.size(), TLG_HOST,
+                                               allow_birth ? 1 : 0, &r);
+    ++ver_;  // births may have landed even when the call throws
+    gpu::check(st);
     return {static_cast<std::size_t>(r.active_blocks), static_cast<std::size_t>(r.active_centers),
             static_cast<std::size_t>(r.born_centers), r.rejected != 0};
   }
@@ -375,6 +394,7 @@ class TerrainModel {
   }
   void batch_solve(double* H, double* b) {
     gpu::check(tlg_batch_ridge_solve(m_.get(), H, batch_system().ld, b));
+    ++ver_;
   }
   // kernel_eval's exact per-pair cutoff test everywhere (tlg_model_set_exact_cutoff)
   void set_exact_cutoff(bool exact) {
@@ -389,12 +409,19 @@ class TerrainModel {
   }
 
   tlg_model* handle() const { return m_.get(); }
+  // the host mirrors are stale after changes made through handle()
+  void invalidate() { ++ver_; }
 
  private:
   struct Del {
     void operator()(tlg_model* m) const { tlg_model_destroy(m); }
   };
   std::unique_ptr<tlg_model, Del> m_;
+  std::uint64_t ver_ = 1;
+  mutable std::vector<double> w_;
+  mutable std::uint64_t w_at_ = 0;
+  mutable std::vector<std::uint32_t> bidx_;
+  mutable std::uint64_t bidx_at_ = 0;
 };
 
 // terrain_model.cpp:269-308
