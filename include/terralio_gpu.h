@@ -321,6 +321,15 @@ tlg_status tlg_batch_ridge_assemble(tlg_model* model, const double* x, const dou
                                     const double* z, size_t m, tlg_mem mem, double* H, size_t ld,
                                     double* b, int add_lambda);
 tlg_status tlg_batch_ridge_solve(tlg_model* model, double* H, size_t ld, double* b);
+/* Structural sparsity of that system, for the cross-rank reduction of the
+ * partial systems: entry (i, j) can be nonzero only for centres within two
+ * cutoffs (and the diagonal). *nnz = packed length (deterministic order, the
+ * same on every rank for the same centres); pack gathers those entries of a
+ * DEVICE H into a DEVICE packed[nnz]; unpack zeroes H and scatters them back.
+ * Reducing packed instead of H moves ~nnz doubles instead of elems. */
+tlg_status tlg_batch_ridge_pattern(tlg_model* model, size_t* nnz);
+tlg_status tlg_batch_ridge_pack(tlg_model* model, const double* H, double* packed);
+tlg_status tlg_batch_ridge_unpack(tlg_model* model, const double* packed, double* H);
 
 /* RBFT v1 snapshot (snapshot.cpp:7-126), byte-identical layout. */
 tlg_status tlg_model_save(tlg_model* model, const char* path);

@@ -115,6 +115,9 @@ _SIGS = {
     "tlg_build_correspondences": (_ST, [_P, _P, _P, _P, _P, _SZ, _I, _P, _P, _P, C.POINTER(_SZ)]),
     "tlg_correspondences_get": (_ST, [_P, _P, _P, _P, _P, _P, _P, _P, _SZ]),
     "tlg_feature_normal_eq": (_ST, [_P, _P, _P, _P]),
+    "tlg_batch_ridge_pattern": (_ST, [_P, C.POINTER(_SZ)]),
+    "tlg_batch_ridge_pack": (_ST, [_P, _P, _P]),
+    "tlg_batch_ridge_unpack": (_ST, [_P, _P, _P]),
     "tlg_feature_rows": (_ST, [_P, _P, _P, _P, _P, _SZ, _P, _P, _P, _P, _SZ, C.POINTER(_SZ)]),
     "tlg_select_ground_points": (_ST, [_P, _P, _P, _P, _P, _SZ, _I, _P, _P, _P, _P, C.c_double,
                                        C.c_double, _SZ, _P, _P, _P, _I, C.POINTER(_SZ)]),

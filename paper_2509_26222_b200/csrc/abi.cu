@@ -886,6 +886,32 @@ tlg_status tlg_batch_ridge_assemble(tlg_model* m, const double* x, const double*
   });
 }
 
+tlg_status tlg_batch_ridge_pattern(tlg_model* m, size_t* nnz) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(nnz, "nnz");
+    *nnz = batch_pattern_device(m);
+  });
+}
+
+tlg_status tlg_batch_ridge_pack(tlg_model* m, const double* H, double* packed) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(H, "H");
+    check_ptr(packed, "packed");
+    batch_pack_device(m, H, packed);
+  });
+}
+
+tlg_status tlg_batch_ridge_unpack(tlg_model* m, const double* packed, double* H) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(H, "H");
+    check_ptr(packed, "packed");
+    batch_unpack_device(m, packed, H);
+  });
+}
+
 tlg_status tlg_batch_ridge_solve(tlg_model* m, double* H, size_t ld, double* b) {
   return guard([&] {
     check_ptr(m, "model");

@@ -359,6 +359,12 @@ struct tlg_model {
   tlg::LatticeGrid lat;
   bool grid_dirty = true;
   bool exact_cutoff = false;  // force the per-pair cutoff test (tlg_model_set_exact_cutoff)
+  // structural nonzeros of the banded batch system (positions in band
+  // storage of centre pairs within 2 cutoffs): packs the partial systems of
+  // the point-sharded fit for the cross-rank reduction; keyed by the centre
+  // count it was built for
+  tlg::DBuf<uint64_t> bpat;
+  size_t bpat_nnz = 0, bpat_for = 0;
 };
 
 // A scan's lever arms, binned once per scan by the world cell they fall in
@@ -423,5 +429,8 @@ void batch_system_dims(tlg_model* m, size_t* n, size_t* ld, size_t* elems);
 void batch_assemble_device(tlg_model* m, const double* x, const double* y, const double* z,
                            size_t mm, double* H, size_t ld, double* b, bool add_lambda);
 void batch_solve_device(tlg_model* m, double* H, size_t ld, double* b);
+size_t batch_pattern_device(tlg_model* m);
+void batch_pack_device(tlg_model* m, const double* H, double* packed);
+void batch_unpack_device(tlg_model* m, const double* packed, double* H);
 
 }  // namespace tlg

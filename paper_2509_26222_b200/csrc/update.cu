@@ -1450,4 +1450,114 @@ void batch_solve_device(tlg_model* m, double* H, size_t ld, double* b) {
   batch_solve(m, p, H, p.ld, b);
 }
 
+// ---- structural sparsity of the batch system (point-sharded reduction) ----
+// Column j of the band storage holds rows i in [j, j + ld) at H[i + j ld];
+// entry (i, j) can be nonzero only when one observation lies within the
+// cutoff of both centres, i.e. |c_i - c_j| <= 2 cutoff (the diagonal always).
+// Counting pass then a fill pass in column order -> deterministic positions.
+__global__ void k_bpat_count(const uint32_t* __restrict__ merged, const double* __restrict__ cx,
+                             const double* __restrict__ cy, int n, int ld, double r2,
+                             uint32_t* __restrict__ cnt) {
+  const int j = blockIdx.x;
+  const double xj = cx[merged[j]], yj = cy[merged[j]];
+  const int i1 = min(n, j + ld);
+  uint32_t c = 0;
+  for (int i = j + threadIdx.x; i < i1; i += blockDim.x) {
+    const double dx = cx[merged[i]] - xj, dy = cy[merged[i]] - yj;
+    c += (i == j || dx * dx + dy * dy <= r2) ? 1u : 0u;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  __shared__ uint32_t sh[32];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    cnt[j] = t;
+  }
+}
+
+__global__ void k_bpat_fill(const uint32_t* __restrict__ merged, const double* __restrict__ cx,
+                            const double* __restrict__ cy, int n, int ld, double r2,
+                            const uint32_t* __restrict__ off, uint64_t* __restrict__ pos) {
+  const int j = blockIdx.x;
+  if (threadIdx.x != 0) return;  // one thread per column keeps row order (cheap: ld tests)
+  const double xj = cx[merged[j]], yj = cy[merged[j]];
+  const int i1 = min(n, j + ld);
+  uint32_t k = off[j];
+  for (int i = j; i < i1; ++i) {
+    const double dx = cx[merged[i]] - xj, dy = cy[merged[i]] - yj;
+    if (i == j || dx * dx + dy * dy <= r2) pos[k++] = static_cast<uint64_t>(i) + static_cast<uint64_t>(j) * ld;
+  }
+}
+
+__global__ void k_bpat_gather(const uint64_t* __restrict__ pos, size_t nnz, const double* __restrict__ H,
+                              double* __restrict__ packed) {
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < nnz; k += (size_t)gridDim.x * blockDim.x)
+    packed[k] = H[pos[k]];
+}
+
+__global__ void k_bpat_scatter(const uint64_t* __restrict__ pos, size_t nnz, const double* __restrict__ packed,
+                               double* __restrict__ H) {
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < nnz; k += (size_t)gridDim.x * blockDim.x)
+    H[pos[k]] = packed[k];
+}
+
+static size_t batch_pattern(tlg_model* m, const BatchPlan& p) {
+  if (m->bpat_for == m->hcx.size() && m->bpat_nnz) return m->bpat_nnz;
+  tlg_ctx* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  const int n = p.n;
+  const uint32_t* d_merged = upload_merged(ctx, p);
+  const double rr = 2.0 * m->kernel.cutoff_radius;
+  const double r2 = rr * rr * (1.0 + 1e-9);  // a superset of the true pattern
+  uint32_t* cnt = ctx->ws<uint32_t>(S_TROWP, n + 1);
+  k_bpat_count<<<n, 256, 0, s>>>(d_merged, m->cx.p, m->cy.p, n, p.ld, r2, cnt);
+  TLG_LAUNCHED(ctx);
+  std::vector<uint32_t> h(n + 1, 0);
+  TLG_CUDA(cudaMemcpyAsync(h.data(), cnt, n * 4, cudaMemcpyDeviceToHost, s));
+  TLG_CUDA(cudaStreamSynchronize(s));
+  size_t total = 0;
+  for (int j = 0; j < n; ++j) {
+    const uint32_t c = h[j];
+    h[j] = static_cast<uint32_t>(total);
+    total += c;
+  }
+  require(total < (size_t{1} << 32), TLG_RUNTIME_ERROR, "batch pattern too large");
+  TLG_CUDA(cudaMemcpyAsync(cnt, h.data(), n * 4, cudaMemcpyHostToDevice, s));
+  m->bpat.ensure(total + 1);
+  k_bpat_fill<<<n, 32, 0, s>>>(d_merged, m->cx.p, m->cy.p, n, p.ld, r2, cnt, m->bpat.p);
+  TLG_LAUNCHED(ctx);
+  TLG_CUDA(cudaStreamSynchronize(s));
+  m->bpat_nnz = total;
+  m->bpat_for = m->hcx.size();
+  return total;
+}
+
+size_t batch_pattern_device(tlg_model* m) {
+  ensure_grid(m);
+  if (m->hcx.empty()) return 0;
+  return batch_pattern(m, batch_plan(m));
+}
+
+void batch_pack_device(tlg_model* m, const double* H, double* packed) {
+  const size_t nnz = batch_pattern_device(m);
+  if (!nnz) return;
+  const unsigned b = static_cast<unsigned>(std::min<size_t>((nnz + 255) / 256, 8 * 148));
+  k_bpat_gather<<<b, 256, 0, m->ctx->stream>>>(m->bpat.p, nnz, H, packed);
+  TLG_LAUNCHED(m->ctx);
+  TLG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+}
+
+void batch_unpack_device(tlg_model* m, const double* packed, double* H) {
+  const size_t nnz = batch_pattern_device(m);
+  const BatchPlan p = batch_plan(m);
+  TLG_CUDA(cudaMemsetAsync(H, 0, sizeof(double) * batch_elems(p), m->ctx->stream));
+  if (!nnz) return;
+  const unsigned b = static_cast<unsigned>(std::min<size_t>((nnz + 255) / 256, 8 * 148));
+  k_bpat_scatter<<<b, 256, 0, m->ctx->stream>>>(m->bpat.p, nnz, packed, H);
+  TLG_LAUNCHED(m->ctx);
+  TLG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+}
+
 }  // namespace tlg

@@ -9,9 +9,11 @@ gloo works for the CPU tests). Points are sharded contiguously.
   ranks — the one real reduction of the LM cost evaluation.
 * Batch ridge (kernel-matrix assembly): every rank assembles the banded
   partial system (lambda I on rank 0) + sum m m^T, sum m z over its shard
-  (tlg_batch_ridge_assemble); the band and the rhs are summed across ranks
-  (one all-reduce each) and every rank factors and solves the same system
-  ("replicas" for the solve).
+  (tlg_batch_ridge_assemble); the structural nonzeros of the band
+  (tlg_batch_ridge_pack: centre pairs within two cutoffs, ~4% of the band
+  storage at C5) and the rhs are summed across ranks, unpacked, and every
+  rank factors and solves the same system ("replicas" for the solve,
+  SURVEY §8e).
 """
 from __future__ import annotations
 
@@ -58,11 +60,18 @@ def allreduce_normal_eq(ne: NormalEq, group=None, device=None, buf=None) -> Norm
     return unpack(buf.cpu().numpy())
 
 
-def fit_batch_ridge_sharded(model, xy_shard, z_shard, group=None, device=None):
+def fit_batch_ridge_sharded(model, xy_shard, z_shard, group=None, device=None, packed=True):
     """Point-sharded fit_batch_ridge into `model` (created from the same
     centres on every rank). `model` needs batch_system / batch_assemble /
-    batch_solve (terrain.TerrainModel on the GPU). Returns (n, ld) of the
-    reduced system (band storage, terrain.TerrainModel.batch_system)."""
+    batch_solve (terrain.TerrainModel on the GPU). Returns (n, ld, moved):
+    the reduced system's size (band storage, TerrainModel.batch_system) and
+    the doubles each rank contributed to the reduction.
+
+    The partial systems are reduced in PACKED form when the model offers
+    batch_pattern / batch_pack / batch_unpack: only the structural nonzeros
+    (centre pairs within two cutoffs, the same deterministic order on every
+    rank) cross NVLink — C5: ~1.3e7 doubles instead of the 3.4e8 of the band
+    storage — then every rank unpacks and solves the same system."""
     import torch
     import torch.distributed as dist
 
@@ -73,8 +82,18 @@ def fit_batch_ridge_sharded(model, xy_shard, z_shard, group=None, device=None):
     H = torch.empty(elems, dtype=torch.float64, device=dev)
     b = torch.empty(n, dtype=torch.float64, device=dev)
     model.batch_assemble(xy_shard, z_shard, H, b, add_lambda=(rank == 0))
+    moved = elems + n
     if on:
-        dist.all_reduce(H, op=dist.ReduceOp.SUM, group=group)
+        use_packed = packed and hasattr(model, "batch_pattern")
+        nnz = model.batch_pattern() if use_packed else elems
+        if use_packed and nnz < elems:
+            P = torch.empty(nnz, dtype=torch.float64, device=dev)
+            model.batch_pack(H, P)
+            dist.all_reduce(P, op=dist.ReduceOp.SUM, group=group)
+            model.batch_unpack(P, H)
+            moved = nnz + n
+        else:
+            dist.all_reduce(H, op=dist.ReduceOp.SUM, group=group)
         dist.all_reduce(b, op=dist.ReduceOp.SUM, group=group)
     model.batch_solve(H, b)
-    return n, ld
+    return n, ld, moved

@@ -377,6 +377,24 @@ class TerrainModel(_CtxBound):
                                                  C.byref(el)))
         return n.value, ld.value, el.value
 
+    def batch_pattern(self) -> int:
+        """Structural nonzeros of the batch system (tlg_batch_ridge_pattern)."""
+        nnz = C.c_size_t()
+        check(_abi.load().tlg_batch_ridge_pattern(self.handle, C.byref(nnz)))
+        return nnz.value
+
+    def batch_pack(self, H, packed) -> None:
+        """packed[:] = the structural nonzeros of device H (tlg_batch_ridge_pack)."""
+        if not (_is_dev(H) and _is_dev(packed)):
+            raise InvalidArgument("H and packed must be CUDA tensors")
+        check(_abi.load().tlg_batch_ridge_pack(self.handle, _ptr(H), _ptr(packed)))
+
+    def batch_unpack(self, packed, H) -> None:
+        """H = 0, then the packed entries scattered back (tlg_batch_ridge_unpack)."""
+        if not (_is_dev(H) and _is_dev(packed)):
+            raise InvalidArgument("H and packed must be CUDA tensors")
+        check(_abi.load().tlg_batch_ridge_unpack(self.handle, _ptr(packed), _ptr(H)))
+
     def batch_assemble(self, xy, z, H, b, add_lambda: bool) -> None:
         """Partial system of this point shard into device tensors H (n * ld)
         and b (n) (tlg_batch_ridge_assemble)."""

@@ -96,24 +96,47 @@ class _DenseRidge:
         self.w = np.linalg.solve(H.numpy().reshape(n, n).T, b.numpy())
 
 
+class _PackedRidge(_DenseRidge):
+    """+ the packed reduction hooks: entries of centre pairs farther apart
+    than 0.5 are structurally zero (a band of the dense system), packed in a
+    fixed order."""
+
+    def _pos(self):
+        d = np.linalg.norm(self.c[:, None, :] - self.c[None, :, :], axis=-1)
+        return np.flatnonzero((d <= 0.5).reshape(-1))
+
+    def batch_pattern(self):
+        return len(self._pos())
+
+    def batch_pack(self, H, P):
+        import torch
+        P.copy_(H[torch.from_numpy(self._pos())])
+
+    def batch_unpack(self, P, H):
+        import torch
+        H.zero_()
+        H[torch.from_numpy(self._pos())] = P
+
+
 def _ridge_data():
     rng = np.random.default_rng(3)
     xy = rng.uniform(0.0, 1.0, (501, 2))
     return xy, np.sin(3 * xy[:, 0]) * xy[:, 1]
 
 
-def _ridge_worker(rank, world, port, out):
+def _ridge_worker(rank, world, port, out, packed=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
     from paper_2509_26222_b200 import distributed as D
-    from test_distributed_gloo import _DenseRidge, _ridge_data
+    from test_distributed_gloo import _DenseRidge, _PackedRidge, _ridge_data
     xy, z = _ridge_data()
     b, e = D.shard_range(len(z), rank, world)
-    m = _DenseRidge()
-    D.fit_batch_ridge_sharded(m, xy[b:e], z[b:e], device="cpu")
+    m = _PackedRidge() if packed else _DenseRidge()
+    _, _, moved = D.fit_batch_ridge_sharded(m, xy[b:e], z[b:e], device="cpu")
     out[rank] = m.w.tolist()
+    out[f"moved{rank}"] = moved
     dist.destroy_process_group()
 
 
@@ -131,4 +154,32 @@ def test_gloo_sharded_batch_ridge_matches_single_process():
     D.fit_batch_ridge_sharded(ref, xy, z, device="cpu")
     for rank in range(2):
         np.testing.assert_allclose(np.array(out[rank]), ref.w, rtol=1e-9, atol=1e-12)
+    assert out[0] == out[1]
+
+
+def test_gloo_sharded_batch_ridge_packed_reduction():
+    """The packed (structural-nonzero) reduction gives the same system as the
+    dense one when the dropped entries are zero in every partial system."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_ridge_worker, args=(2, port, out, True), nprocs=2, join=True)
+    xy, z = _ridge_data()
+    ref = _PackedRidge()
+    n = len(ref.c)
+    # the single-process reference on the same pattern-restricted system
+    import torch
+    H = torch.empty(n * n, dtype=torch.float64)
+    b = torch.empty(n, dtype=torch.float64)
+    ref.batch_assemble(xy, z, H, b, True)
+    P = torch.empty(ref.batch_pattern(), dtype=torch.float64)
+    ref.batch_pack(H, P)
+    ref.batch_unpack(P, H)
+    ref.batch_solve(H, b)
+    for rank in range(2):
+        np.testing.assert_allclose(np.array(out[rank]), ref.w, rtol=1e-9, atol=1e-12)
+        assert out[f"moved{rank}"] == ref.batch_pattern() + n < n * n + n
     assert out[0] == out[1]
