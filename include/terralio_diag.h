@@ -23,6 +23,10 @@ tlg_status tlg_diag_dense_bench(tlg_ctx* ctx, int op, int n, int nrhs, int reps,
  * return L and X = L^-1 (host, may be NULL). */
 tlg_status tlg_diag_potrf(tlg_ctx* ctx, int n, const double* A, int tile, int band, double* L,
                           double* X);
+/* Batch-ridge assembly path of model m: 0 = automatic (the lattice element
+ * assembly when the centres are mesh nodes), 1 = the row-wise CSR Gram
+ * always (the A/B reference for the lattice path). */
+tlg_status tlg_diag_set_batch_gram(tlg_model* m, int csr);
 
 #ifdef __cplusplus
 }

@@ -214,6 +214,8 @@ def load_diag() -> C.CDLL:
         d.tlg_diag_potrf.restype = C.c_int
         d.tlg_diag_potrf.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
                                      C.c_void_p]
+        d.tlg_diag_set_batch_gram.restype = C.c_int
+        d.tlg_diag_set_batch_gram.argtypes = [C.c_void_p, C.c_int]
         _diag = d
     return _diag
 

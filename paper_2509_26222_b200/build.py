@@ -26,7 +26,7 @@ NVCC_FLAGS = [
     "-I", str(ROOT / "include"),
 ]
 
-SOURCES = ["model.cu", "grid.cu", "eval.cu", "select.cu", "dense.cu", "update.cu", "prof.cu",
+SOURCES = ["model.cu", "grid.cu", "eval.cu", "select.cu", "dense.cu", "update.cu", "assemble.cu", "prof.cu",
            "scan.cu", "consumers.cu", "match.cu", "abi.cu"]
 DIAG_LIB = LIB_DIR / "libterralio_diag.so"
 # match.cu restates the matcher's scalar geometry (centroids, scatter, 3x3

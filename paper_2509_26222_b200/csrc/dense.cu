@@ -736,97 +736,276 @@ __global__ void __launch_bounds__(128) k_potrf_coop32(double* __restrict__ A, in
 }
 
 // Banded Cholesky solve L L^T x = b with the 32-wide factor (L in A, the
-// diagonal-tile inverses in linv), one cooperative launch, right-looking
-// forward and left-looking backward, one grid barrier per tile step.
-// Forward: every CTA forms y_k = Linv_kk b_k (32 x 32, redundantly), then
-// subtracts L_ik y_k from the band rows below (thread per row, coalesced
-// along the row index). Backward: every CTA forms x_k = Linv_kk^T z_k from
-// the band columns' updates of earlier steps, then z_c -= L_kc^T x_k for the
-// band columns to the left — one warp per column, lanes over the 32 rows
-// (coalesced 256-byte column segments, shuffle reduction). x goes to its
-// own array, so no barrier guards a read-before-overwrite.
-__global__ void __launch_bounds__(128) k_band_solve_coop(const double* __restrict__ L, int n,
-                                                         int ld, int bwt,
-                                                         const double* __restrict__ linv,
-                                                         double* __restrict__ b,
-                                                         double* __restrict__ y,
-                                                         double* __restrict__ x) {
-  __shared__ double sk[NB32], sv[NB32];
-  __shared__ double sl[NB32 * (NB32 + 1)];  // Linv_kk, padded rows
-  cg::grid_group grid = cg::this_grid();
-  const int nt = (n + NB32 - 1) / NB32;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+// diagonal-tile inverses in linv) as a dataflow over row blocks of kFlowRB
+// rows, without grid barriers: persistent CTAs take blocks in order (forward
+// ascending, backward descending), and block i waits, tile by tile, only for
+// the published solution of the blocks it reads (an acquire flag per block).
+// The off-diagonal band tiles of a block are summed by its 8 warps while the
+// blocks ahead are still being solved, so the critical path per block is its
+// last tile product, the intra-block sequence of diagonal 32-tile steps and
+// one flag hand-off — about 2 us, against a grid barrier plus four
+// dependent round trips per 32 rows before.
+// Forward, row r of tile ti: y_ti = Linv_ti (b_ti - sum_{tj in band} L_ti,tj y_tj);
+// backward: x_ti = Linv_ti^T (y_ti - sum_{tj in band} L_tj,ti^T x_tj).
+constexpr int kFlowSub = 4;                // 32-row tiles per block
+constexpr int kFlowRB = 32 * kFlowSub;     // rows per block
+constexpr int kFlowThreads = 256;          // 8 warps: 2 per sub-tile
+constexpr int kFlowW = kFlowThreads / 32;
+constexpr int kFlowP = 33;                 // smem tile pitch
+constexpr int kFlowIntra = kFlowSub * (kFlowSub - 1) / 2;  // off-diagonal tiles inside a block
+// dynamic smem: Linv tiles + intra-block L tiles ([r][c], pitch 33), the
+// block's right-hand side, per-warp partials, per-warp staged solution tiles
+constexpr size_t kFlowSmem =
+    sizeof(double) * ((kFlowSub + kFlowIntra) * 32 * kFlowP + kFlowRB + kFlowW * 32 + kFlowW * 2 * 32);
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// lane 0 waits for block `blk`, then the warp reads what it published
+__device__ __forceinline__ void wait_block(const int* flag, int blk, int epoch) {
+  if ((threadIdx.x & 31) == 0)
+    while (ld_acquire(flag + blk) != epoch) __nanosleep(64);
+  __syncwarp();
+}
+
+// sum over lanes of v[c] for all 32 c at once (recursive halving, 31
+// shuffles): lane c returns sum_lanes v[c]
+__device__ __forceinline__ double warp_transpose_sum(double (&v)[32]) {
   const int lane = threadIdx.x & 31;
-  const int gw = tid >> 5, nw = nth >> 5;
-  // Linv_kk -> shared memory in one round trip (all loads in flight)
-  // (lower triangle of the kb x kb tile; zero elsewhere)
-  auto stage_linv = [&](int k, int kb) {
-    const double* Li = linv + (size_t)k * NB32 * NB32;
 #pragma unroll
-    for (int e = threadIdx.x; e < NB32 * NB32; e += 128) {
-      const int i = e & 31, c = e >> 5;
-      sl[i * (NB32 + 1) + c] = (c <= i && i < kb) ? Li[e] : 0.0;
+  for (int h = 16; h > 0; h >>= 1) {
+    const bool up = lane & h;
+#pragma unroll
+    for (int q = 0; q < h; ++q) {
+      const double send = up ? v[q] : v[q + h];
+      const double keep = up ? v[q + h] : v[q];
+      v[q] = keep + __shfl_xor_sync(0xffffffffu, send, h);
     }
-  };
-  for (int k = 0; k < nt; ++k) {  // forward: y = L^-1 b
-    const int k0 = k * NB32, kb = min(NB32, n - k0);
-    stage_linv(k, kb);
-    if (threadIdx.x < NB32) sk[threadIdx.x] = threadIdx.x < kb ? b[k0 + threadIdx.x] : 0.0;
-    __syncthreads();
-    if (threadIdx.x < NB32) {
-      // sl[i][c] = Linv(i, c), lower triangular (zero above; beyond kb unused)
-      double v = 0.0;
-#pragma unroll
-      for (int c = 0; c < NB32; ++c) v = fma(sl[threadIdx.x * (NB32 + 1) + c], sk[c], v);
-      sv[threadIdx.x] = v;
-      if (blockIdx.x == 0 && threadIdx.x < kb) y[k0 + threadIdx.x] = v;
-    }
-    __syncthreads();
-    const int r0 = k0 + kb, r1 = min(n, (min(nt - 1, k + bwt) + 1) * NB32);
-    for (int r = r0 + tid; r < r1; r += nth) {
-      double lv[NB32];
-#pragma unroll
-      for (int c = 0; c < NB32; ++c) lv[c] = c < kb ? L[r + (size_t)(k0 + c) * ld] : 0.0;
-      double acc = 0.0;
-#pragma unroll
-      for (int c = 0; c < NB32; ++c) acc = fma(lv[c], sv[c], acc);
-      b[r] -= acc;
-    }
-    grid.sync();
   }
-  for (int k = nt - 1; k >= 0; --k) {  // backward: x = L^-T y
-    const int k0 = k * NB32, kb = min(NB32, n - k0);
-    stage_linv(k, kb);
-    if (threadIdx.x < NB32) sk[threadIdx.x] = threadIdx.x < kb ? y[k0 + threadIdx.x] : 0.0;
-    __syncthreads();
-    if (threadIdx.x < NB32) {
-      // x_i = sum_r Linv(r, i) z_r
-      double v = 0.0;
+  return v[0];
+}
+
+// Stages block [t0, t1)'s diagonal inverses (lower kb x kb part) and its
+// off-diagonal tiles L(tr, tc), t0 <= tc < tr < t1, in the band, as [r][c].
+__device__ __forceinline__ void flow_stage(const double* __restrict__ L, int n, int ld, int bwt,
+                                           const double* __restrict__ linv, int t0, int t1,
+                                           double* sLi, double* sT) {
+  for (int e = threadIdx.x; e < kFlowSub * 1024; e += kFlowThreads) {
+    const int s = e >> 10, r = e & 31, c = (e >> 5) & 31, ti = t0 + s;
+    double v = 0.0;
+    if (ti < t1 && c <= r && ti * 32 + r < n) v = linv[(size_t)ti * 1024 + r + 32 * c];
+    sLi[(s * 32 + r) * kFlowP + c] = v;
+  }
+  for (int e = threadIdx.x; e < kFlowIntra * 1024; e += kFlowThreads) {
+    const int q = e >> 10, r = e & 31, c = (e >> 5) & 31;
+    int tr = 1, tc = 0, k = q;  // q -> (tr, tc) in (1,0), (2,0), (2,1), (3,0), ...
+    while (k >= tr) {
+      k -= tr;
+      ++tr;
+    }
+    tc = k;
+    const int gr = (t0 + tr) * 32 + r, gc = (t0 + tc) * 32 + c;
+    double v = 0.0;
+    if (t0 + tr < t1 && tr - tc <= bwt && gr < n) v = L[gr + (size_t)gc * ld];
+    sT[(q * 32 + r) * kFlowP + c] = v;
+  }
+}
+__device__ __forceinline__ int flow_intra(int tr, int tc) { return tr * (tr - 1) / 2 + tc; }
+
+__global__ void __launch_bounds__(kFlowThreads) k_band_fwd_flow(const double* __restrict__ L, int n,
+                                                                int ld, int bwt,
+                                                                const double* __restrict__ linv,
+                                                                const double* __restrict__ b,
+                                                                double* __restrict__ y,
+                                                                int* __restrict__ flag, int epoch) {
+  extern __shared__ __align__(16) double fsm[];
+  double* sLi = fsm;
+  double* sT = sLi + kFlowSub * 32 * kFlowP;
+  double* bb = sT + kFlowIntra * 32 * kFlowP;
+  double* part = bb + kFlowRB;      // [warp][32]
+  double* ys = part + kFlowW * 32;  // [warp][2][32]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = warp >> 1, half = warp & 1;  // this warp's sub-tile, and its half of the tiles
+  const int nt = (n + 31) / 32, nb = (n + kFlowRB - 1) / kFlowRB;
+  for (int i = blockIdx.x; i < nb; i += gridDim.x) {
+    const int t0 = i * kFlowSub, t1 = min(nt, t0 + kFlowSub);
+    const int ti = t0 + s, r = ti * 32 + lane;
+    const bool row_ok = ti < t1 && r < n;
+    flow_stage(L, n, ld, bwt, linv, t0, t1, sLi, sT);
+    // blocks <= i-2 (published earlier): tiles of the row's band, oldest first
+    const int tlo = max(0, ti - bwt), tcrit = max(0, t0 - kFlowSub);
+    double acc = 0.0;
+    for (int tj = tlo + half; tj < tcrit; tj += 2) {
+      wait_block(flag, tj / kFlowSub, epoch);
+      ys[(warp * 2) * 32 + lane] = __ldcg(y + tj * 32 + lane);
+      __syncwarp();
+      if (row_ok) {
+        const double* lr = L + r + (size_t)tj * 32 * ld;
+        double lv[32];
 #pragma unroll
-      for (int r = 0; r < NB32; ++r) v = fma(sl[r * (NB32 + 1) + threadIdx.x], sk[r], v);
-      sv[threadIdx.x] = v;
-      if (blockIdx.x == 0 && threadIdx.x < kb) x[k0 + threadIdx.x] = v;
+        for (int c = 0; c < 32; ++c) lv[c] = lr[(size_t)c * ld];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc = fma(lv[c], ys[(warp * 2) * 32 + c], acc);
+      }
+      __syncwarp();
+    }
+    // block i-1 (the critical hand-off): its tiles' rows are loaded before
+    // the wait, so only the products follow it
+    if (i > 0) {
+      double lv[2][32];
+      int tjs[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int tj = tcrit + half + 2 * u;
+        tjs[u] = (tj < t0 && tj >= tlo && row_ok) ? tj : -1;
+        const double* lr = L + (row_ok ? r : 0) + (size_t)max(tj, 0) * 32 * ld;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) lv[u][c] = tjs[u] >= 0 ? lr[(size_t)c * ld] : 0.0;
+      }
+      wait_block(flag, i - 1, epoch);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int tj = tcrit + half + 2 * u;
+        ys[(warp * 2 + u) * 32 + lane] = tj < t0 ? __ldcg(y + tj * 32 + lane) : 0.0;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (tjs[u] >= 0) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) acc = fma(lv[u][c], ys[(warp * 2 + u) * 32 + c], acc);
+        }
+    }
+    part[warp * 32 + lane] = acc;
+    __syncthreads();
+    if (threadIdx.x < kFlowRB) {
+      const int q = threadIdx.x >> 5, rr = t0 * 32 + threadIdx.x;
+      bb[threadIdx.x] = rr < n ? b[rr] - (part[(2 * q) * 32 + lane] + part[(2 * q + 1) * 32 + lane]) : 0.0;
     }
     __syncthreads();
-    const int c0 = max(0, k - bwt) * NB32;
-    const double xv = lane < kb ? sv[lane] : 0.0;
-    constexpr int U = 8;  // columns per warp with their loads in flight together
-    for (int cb = c0 + gw; cb < k0; cb += nw * U) {
-      double p[U];
+    // the block's own tiles, in order (all operands in shared memory)
+    for (int tk = t0; tk < t1; ++tk) {
+      const int k = tk - t0;
+      if (warp == 0) {
+        const double* li = sLi + (k * 32 + lane) * kFlowP;
+        double v = 0.0;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int c = cb + u * nw;
-        p[u] = (c < k0 && lane < kb) ? L[(size_t)c * ld + k0 + lane] * xv : 0.0;
+        for (int c = 0; c < 32; ++c) v = fma(li[c], bb[k * 32 + c], v);
+        const int rr = tk * 32 + lane;
+        if (rr < n) y[rr] = v;
+        bb[k * 32 + lane] = rr < n ? v : 0.0;
       }
+      __syncthreads();
+      const int tr = tk + 1 + warp;
+      if (tr < t1 && tr - tk <= bwt) {
+        const double* tl = sT + (flow_intra(tr - t0, k) * 32 + lane) * kFlowP;
+        double a = 0.0;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) p[u] += __shfl_xor_sync(0xffffffffu, p[u], o);
-        const int c = cb + u * nw;
-        if (lane == 0 && c < k0) y[c] -= p[u];
+        for (int c = 0; c < 32; ++c) a = fma(tl[c], bb[k * 32 + c], a);
+        bb[(tr - t0) * 32 + lane] -= a;
       }
+      __syncthreads();
     }
-    grid.sync();
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(flag + i, epoch);
+  }
+}
+
+__global__ void __launch_bounds__(kFlowThreads) k_band_bwd_flow(const double* __restrict__ L, int n,
+                                                                int ld, int bwt,
+                                                                const double* __restrict__ linv,
+                                                                const double* __restrict__ y,
+                                                                double* __restrict__ x,
+                                                                int* __restrict__ flag, int epoch) {
+  extern __shared__ __align__(16) double fsm[];
+  double* sLi = fsm;
+  double* sT = sLi + kFlowSub * 32 * kFlowP;
+  double* bb = sT + kFlowIntra * 32 * kFlowP;
+  double* part = bb + kFlowRB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = warp >> 1, half = warp & 1;
+  const int nt = (n + 31) / 32, nb = (n + kFlowRB - 1) / kFlowRB;
+  for (int q = blockIdx.x; q < nb; q += gridDim.x) {
+    const int i = nb - 1 - q;
+    const int t0 = i * kFlowSub, t1 = min(nt, t0 + kFlowSub);
+    const int ti = t0 + s;  // column tile of this warp's sub-tile
+    flow_stage(L, n, ld, bwt, linv, t0, t1, sLi, sT);
+    // v[c] accumulates sum_r L(tj r, ti c) x(tj r) over this warp's tiles
+    // (lane = r); one transpose-sum at the end
+    double v[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = 0.0;
+    const int thi = ti < t1 ? min(nt - 1, ti + bwt) : -1;  // last tile of the column's band
+    const int tcrit = t1 + kFlowSub;                        // tiles of block i+1: [t1, tcrit)
+    // blocks >= i+2, oldest (farthest) first
+    for (int tj = thi - half; tj >= tcrit; tj -= 2) {
+      wait_block(flag, nb - 1 - tj / kFlowSub, epoch);
+      const int r = tj * 32 + lane;
+      const double xr = r < n ? __ldcg(x + r) : 0.0;
+      const double* lr = L + min(r, n - 1) + (size_t)ti * 32 * ld;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) v[c] = fma(r < n ? lr[(size_t)c * ld] : 0.0, xr, v[c]);
+    }
+    if (i + 1 < nb) {
+      double lv[2][32];
+      int tjs[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int tj = t1 + half + 2 * u;
+        const int r = tj * 32 + lane;
+        tjs[u] = (tj <= thi && tj < tcrit) ? tj : -1;
+        const double* lr = L + min(max(r, 0), n - 1) + (size_t)max(ti, 0) * 32 * ld;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) lv[u][c] = (tjs[u] >= 0 && r < n) ? lr[(size_t)c * ld] : 0.0;
+      }
+      wait_block(flag, q - 1, epoch);
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (tjs[u] >= 0) {
+          const int r = tjs[u] * 32 + lane;
+          const double xr = r < n ? __ldcg(x + r) : 0.0;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) v[c] = fma(lv[u][c], xr, v[c]);
+        }
+    }
+    part[warp * 32 + lane] = warp_transpose_sum(v);
+    __syncthreads();
+    if (threadIdx.x < kFlowRB) {
+      const int qq = threadIdx.x >> 5, rr = t0 * 32 + threadIdx.x;
+      bb[threadIdx.x] = rr < n ? y[rr] - (part[(2 * qq) * 32 + lane] + part[(2 * qq + 1) * 32 + lane]) : 0.0;
+    }
+    __syncthreads();
+    for (int tk = t1 - 1; tk >= t0; --tk) {
+      const int k = tk - t0;
+      if (warp == 0) {
+        // x_tk = Linv^T z: lane c reads column c of the staged inverse
+        double a = 0.0;
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) a = fma(sLi[(k * 32 + rr) * kFlowP + lane], bb[k * 32 + rr], a);
+        const int c = tk * 32 + lane;
+        if (c < n) x[c] = a;
+        bb[k * 32 + lane] = c < n ? a : 0.0;
+      }
+      __syncthreads();
+      const int tc = tk - 1 - warp;  // z_tc -= L(tk, tc)^T x_tk
+      if (tc >= t0 && tk - tc <= bwt) {
+        const double* tl = sT + flow_intra(k, tc - t0) * 32 * kFlowP;
+        double a = 0.0;
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) a = fma(tl[rr * kFlowP + lane], bb[k * 32 + rr], a);
+        bb[(tc - t0) * 32 + lane] -= a;
+      }
+      __syncthreads();
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(flag + q, epoch);
   }
 }
 
@@ -838,18 +1017,29 @@ void band_solve(tlg_ctx* ctx, const double* L, int n, int ld, int band, double* 
   const double* linv = ctx->ws<double>(S_LINV, 1);
   double* y = ctx->ws<double>(S_XINV2, n);
   double* x = ctx->ws<double>(S_BSOLVE, n);
-  int per_sm = 0;
-  TLG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_band_solve_coop, 128, 0));
-  // forward: a thread per band row; backward: a warp per band column
-  const int rows = (bwt + 1) * NB32;
-  const int want = std::max((rows + 127) / 128, (bwt * NB32 + 3) / 4);
-  // at most one CTA per SM: the per-step grid barrier dominates, and its
-  // cost grows with the CTA count
-  const int grid = std::max(1, std::min(std::min(want, ctx->num_sms),
-                                        ctx->num_sms * std::max(per_sm, 1)));
-  void* args[] = {&L, &n, &ld, &bwt, &linv, &b, &y, &x};
-  TLG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_band_solve_coop), dim3(grid),
-                                       dim3(128), args, 0, ctx->stream));
+  const int nb = (n + kFlowRB - 1) / kFlowRB;
+  int* flags = ctx->ws<int>(S_FLOWFLAG, 2 * static_cast<size_t>(nb));
+  TLG_CUDA(cudaMemsetAsync(flags, 0, 2 * static_cast<size_t>(nb) * sizeof(int), ctx->stream));
+  int epoch = 1;
+  // every CTA co-resident (cooperative launch): a waiting block's producers
+  // are always running
+  // one CTA per SM: fewer pollers, and a CTA's next block is far behind the
+  // wavefront anyway
+  const int g1 = std::max(1, std::min(nb, ctx->num_sms));
+  const int g2 = g1;
+  int* f1 = flags;
+  int* f2 = flags + nb;
+  TLG_CUDA(cudaFuncSetAttribute(k_band_fwd_flow, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kFlowSmem)));
+  TLG_CUDA(cudaFuncSetAttribute(k_band_bwd_flow, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kFlowSmem)));
+  void* a1[] = {&L, &n, &ld, &bwt, &linv, &b, &y, &f1, &epoch};
+  TLG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_band_fwd_flow), dim3(g1),
+                                       dim3(kFlowThreads), a1, kFlowSmem, ctx->stream));
+  ++ctx->launches;
+  void* a2[] = {&L, &n, &ld, &bwt, &linv, &y, &x, &f2, &epoch};
+  TLG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_band_bwd_flow), dim3(g2),
+                                       dim3(kFlowThreads), a2, kFlowSmem, ctx->stream));
   ++ctx->launches;
   TLG_CUDA(cudaMemcpyAsync(b, x, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, ctx->stream));
 }

@@ -208,4 +208,11 @@ tlg_status tlg_diag_potrf(tlg_ctx* ctx, int n, const double* A, int tile, int ba
   });
 }
 
+tlg_status tlg_diag_set_batch_gram(tlg_model* m, int csr) {
+  return diag_guard([&] {
+    require(m != nullptr, TLG_INVALID_ARGUMENT, "null model");
+    m->batch_csr_gram = csr != 0;
+  });
+}
+
 }  // extern "C"

@@ -105,7 +105,7 @@ enum Slot : int {
   S_COUNT, S_ACTIVE, S_BLOCKFLAG, S_ROWOF, S_MERGED, S_ROWPTR, S_COLIDX, S_MTVAL,
   S_KMAT, S_SMAT, S_RESID, S_U, S_YMAT, S_HMAT, S_WORK1, S_WORK2, S_WORK3, S_BLKTAB,
   S_MOMENT_ROW, S_TROWP, S_TKEYS, S_LINV, S_XINV, S_XINV2, S_SOLVE, S_BSOLVE, S_VALIDATE,
-  S_GRAMPART,
+  S_GRAMPART, S_LATGRAM, S_LATSTART, S_LATPTS, S_LATNROW, S_FLOWFLAG,
   S_NUM_SLOTS
 };
 
@@ -359,6 +359,7 @@ struct tlg_model {
   tlg::LatticeGrid lat;
   bool grid_dirty = true;
   bool exact_cutoff = false;  // force the per-pair cutoff test (tlg_model_set_exact_cutoff)
+  bool batch_csr_gram = false;  // diagnostics: batch Gram by CSR rows even on a lattice
   // structural nonzeros of the banded batch system (positions in band
   // storage of centre pairs within 2 cutoffs): packs the partial systems of
   // the point-sharded fit for the cross-rank reduction; keyed by the centre
@@ -430,6 +431,10 @@ void batch_assemble_device(tlg_model* m, const double* x, const double* y, const
                            size_t mm, double* H, size_t ld, double* b, bool add_lambda);
 void batch_solve_device(tlg_model* m, double* H, size_t ld, double* b);
 size_t batch_pattern_device(tlg_model* m);
+// assemble.cu: lattice element assembly of the batch system (false: not a
+// lattice / window too wide; nothing done)
+bool lattice_gram_device(tlg_model* m, const double* x, const double* y, const double* z,
+                         size_t mm, const int* rowof, int band, double* H, int ld, double* b);
 void batch_pack_device(tlg_model* m, const double* H, double* packed);
 void batch_unpack_device(tlg_model* m, const double* packed, double* H);
 

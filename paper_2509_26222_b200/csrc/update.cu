@@ -1362,6 +1362,7 @@ static void batch_assemble(tlg_model* m, const BatchPlan& p, const double* x, co
   TLG_CUDA(cudaMemsetAsync(rowof, 0xff, nc * 4, s));
   k_scatter_rowof<<<(n + 255) / 256, 256, 0, s>>>(d_merged, n, rowof);
   TLG_LAUNCHED(ctx);
+  if (!m->batch_csr_gram && lattice_gram_device(m, x, y, z, mm, rowof, p.band, H, ld, b)) return;
   const Csr c = build_csr(m, x, y, mm, rowof, m->kc.neg_inv_2st2, m->kc.scale, false, nullptr);
   const TCsr t = transpose_csr(ctx, c, mm, n);
   gram_band(ctx, t, c, n, p.band, H, ld, /*lower_only=*/true);

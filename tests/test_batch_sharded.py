@@ -117,3 +117,45 @@ def test_batch_fit_two_shards_packed_equal_dense_sum(gpu_ctx):
     assert torch.equal(Hsum, Hs[0] + Hs[1])
     g.batch_solve(Hsum, bs[0] + bs[1])
     assert rel_norm(g.weights(), full.weights()) < 1e-10
+
+
+def _assemble(g, obs, csr):
+    from paper_2509_26222_b200 import _abi
+    _abi.check(_abi.load_diag().tlg_diag_set_batch_gram(g.handle, 1 if csr else 0))
+    n, ld, el = g.batch_system()
+    H = torch.empty(el, dtype=torch.float64, device="cuda")
+    b = torch.empty(n, dtype=torch.float64, device="cuda")
+    g.batch_assemble(obs.xy, obs.z, H, b, add_lambda=True)
+    return H, b
+
+
+@pytest.mark.parametrize("sigma,sigma_eps,side,holes", [(0.04, 0.1, 2.2, 0.0), (None, None, 1.6, 0.0),
+                                                       (None, None, 1.6, 0.15), (0.03, 0.05, 1.3, 0.1)])
+def test_batch_lattice_assembly_matches_csr_gram(gpu_ctx, sigma, sigma_eps, side, holes):
+    """The lattice element assembly (assemble.cu: per-cell DMMA Gram of the
+    dense feature block) gives the row-wise CSR Gram's system to rounding —
+    the same pair membership, summed in another order — on the paper's
+    geometry, other windows and lattices with holes (absent nodes)."""
+    k = T.KernelParams() if sigma is None else T.KernelParams(sigma=sigma, sigma_eps=sigma_eps)
+    k.finalize()
+    rng = np.random.default_rng(47)
+    xy = rng.uniform(0.0, side, (40_000, 2))
+    z = 0.1 * np.sin(4.0 * xy[:, 0]) + 0.05 * xy[:, 1] ** 2
+    roi = T.Rect((0.0, 0.0), (side, side))
+    nodes = orc.supported_mesh_nodes(xy, z, roi, 0.07, 0.12, 3)
+    if holes:
+        nodes = nodes[rng.uniform(size=len(nodes)) >= holes]
+    cs = T.CenterSet(nodes, 0.07, 0.12, 3, roi)
+    # observations beyond the ROI too (windows leaving the lattice)
+    oxy = np.concatenate([xy, rng.uniform(-0.5, side + 0.5, (3000, 2))])
+    obs = T.TerrainObservation(oxy, np.concatenate([z, rng.normal(0, 0.1, 3000)]))
+    g = T.TerrainModel(k, cs)
+    assert g.sweep()[0] != 0  # a lattice
+    H1, b1 = _assemble(g, obs, csr=False)
+    H0, b0 = _assemble(g, obs, csr=True)
+    assert float((H1 - H0).abs().max()) <= 1e-12 * float(H0.abs().max())
+    assert float((b1 - b0).abs().max()) <= 1e-12 * float(b0.abs().max())
+    assert torch.equal(H1 == 0, H0 == 0)  # the same structural pattern
+    # bit-reproducible run to run
+    H2, b2 = _assemble(g, obs, csr=False)
+    assert torch.equal(H1, H2) and torch.equal(b1, b2)

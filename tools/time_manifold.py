@@ -24,8 +24,18 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--unbinned", action="store_true")
     ap.add_argument("--eval", action="store_true")
+    ap.add_argument("--generic", action="store_true",
+                    help="jitter the centres off the lattice (generic sweep)")
     a = ap.parse_args()
     model, kernel, cs, w, R, tv, h = bench.build_c5(0, a.points, 7, torch)
+    if a.generic:
+        import numpy as np
+        rng = np.random.default_rng(3)
+        c = cs.centers + rng.uniform(-0.005, 0.005, cs.centers.shape)
+        cs = T.CenterSet(c, cs.mesh_resolution, cs.accept_radius, cs.accept_count, cs.roi)
+        model = T.TerrainModel(kernel, cs)
+        model.set_weights(w)
+        print("sweep kind", model.sweep(), flush=True)
     n = a.points
     rows = {"r": torch.empty(n, dtype=torch.float64, device="cuda"),
             "J": torch.empty(6 * n, dtype=torch.float64, device="cuda"),
