@@ -758,18 +758,24 @@ constexpr int kFlowIntra = kFlowSub * (kFlowSub - 1) / 2;  // off-diagonal tiles
 constexpr size_t kFlowSmem =
     sizeof(double) * ((kFlowSub + kFlowIntra) * 32 * kFlowP + kFlowRB + kFlowW * 32 + kFlowW * 2 * 32);
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
+// Flag observation: relaxed loads (an acquire load invalidates the whole L1
+// on every execution — CCTL.IVALL in the SASS), then one acquire fence once
+// the awaited flags are seen. Operand data is read through L2 (__ldcg).
+__device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 // lane 0 waits for block `blk`, then the warp reads what it published
 __device__ __forceinline__ void wait_block(const int* flag, int blk, int epoch) {
-  if ((threadIdx.x & 31) == 0)
-    while (ld_acquire(flag + blk) != epoch) __nanosleep(64);
+  if ((threadIdx.x & 31) == 0) {
+    while (ld_relaxed(flag + blk) != epoch) __nanosleep(64);
+    fence_acquire();
+  }
   __syncwarp();
 }
 
@@ -1075,6 +1081,204 @@ __global__ void __launch_bounds__(128) k_trsm_tiles(const double* __restrict__ L
   }
 }
 
+// Banded / dense 32-wide Cholesky as a task dataflow (no grid barriers).
+// Task (i, j) owns band tile (i, j): it applies its updates
+// A_ij -= L_ik L_jk^T for k = max(0, i - bwt) .. j - 1 in ascending k (so the
+// result is bit-reproducible), waiting per k for the two operand tiles'
+// "final" flags, then finalises the tile — the one-warp Cholesky + inverse
+// when i == j, L_ij = A_ij Linv_j^T (after tile (j, j)) otherwise — and
+// publishes it. Persistent CTAs claim tasks from a counter in column-major
+// order; every wait targets an earlier-claimed task and all CTAs are
+// co-resident, so the schedule cannot deadlock. Columns overlap freely: the
+// critical path per column is the diagonal chain POTRF(j-1) -> TRSM(j, j-1)
+// -> last update of (j, j) -> POTRF(j), while the bulk of the updates runs
+// ahead of it.
+#ifndef TLG_PF_MINB
+#define TLG_PF_MINB 4
+#endif
+constexpr int kPFP = 36;  // smem tile pitch (conflict-free fragments, as gemm32_tile)
+
+__global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __restrict__ A, int n, int lda, int bwt,
+                                                      double* __restrict__ linv, int* __restrict__ info,
+                                                      int* __restrict__ flag,
+                                                      unsigned long long* __restrict__ counter,
+                                                      int epoch) {
+  __shared__ __align__(16) double Xs[2][32][kPFP];  // double-buffered operand tiles
+  __shared__ __align__(16) double Ys[2][32][kPFP];
+  static_assert(2 * 32 * kPFP >= kWarpPotrfSmem, "diagonal-factor scratch aliases Xs");
+  double* wsh = &Xs[0][0][0];  // the diagonal factor's scratch (Xs is idle then)
+  __shared__ long long task_s;
+  __shared__ int s_first;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int wm = (w & 1) * 16, wn = (w >> 1) * 16;
+  const int nt = (n + 31) / 32;
+  const long long T0 = static_cast<long long>(nt - bwt) * (bwt + 1);
+  const long long total = T0 + static_cast<long long>(bwt) * (bwt + 1) / 2;
+  auto fl = [&](int i, int j) { return flag + static_cast<size_t>(j) * (bwt + 1) + (i - j); };
+  for (;;) {
+    if (t == 0) task_s = static_cast<long long>(atomicAdd(counter, 1ull));
+    __syncthreads();
+    const long long task = task_s;
+    __syncthreads();
+    if (task >= total) break;
+    int i, j;
+    if (task < T0) {
+      j = static_cast<int>(task / (bwt + 1));
+      i = j + static_cast<int>(task % (bwt + 1));
+    } else {
+      long long r = task - T0;
+      j = nt - bwt;
+      while (r >= nt - j) {
+        r -= nt - j;
+        ++j;
+      }
+      i = j + static_cast<int>(r);
+    }
+    const int i0 = i * 32, j0 = j * 32, ib = min(32, n - i0), jb = min(32, n - j0);
+    double acc[2][2][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = wm + a * 8 + (lane >> 2), c = wn + b * 8 + 2 * (lane & 3) + h;
+          acc[a][b][h] = (r < ib && c < jb) ? A[(i0 + r) + static_cast<size_t>(j0 + c) * lda] : 0.0;
+        }
+    // operand rows: element e = t + 128 s of a tile, (q, r) = (e >> 5, e & 31)
+    double pa[8], pb[8];
+    auto fetch = [&](int k) {
+      const int k0 = k * 32;
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) {
+        const int e = t + 128 * s2, r = e & 31, q = e >> 5;
+        const bool qk = k0 + q < n;
+        pa[s2] = (i0 + r < n && qk) ? __ldcg(A + (i0 + r) + static_cast<size_t>(k0 + q) * lda) : 0.0;
+        pb[s2] = (j0 + r < n && qk) ? __ldcg(A + (j0 + r) + static_cast<size_t>(k0 + q) * lda) : 0.0;
+      }
+    };
+    auto stash = [&](int buf) {
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) {
+        const int e = t + 128 * s2;
+        Xs[buf][e >> 5][e & 31] = pa[s2];
+        Ys[buf][e >> 5][e & 31] = pb[s2];
+      }
+    };
+    // Operand readiness: one parallel sweep of the flags of all remaining k
+    // (one round trip) gives the first k not yet final; k below it need no
+    // further polling.
+    auto first_unready = [&](int from) {
+      if (t == 0) s_first = j;
+      __syncthreads();
+      for (int kk = from + t; kk < j; kk += 128)
+        if (ld_relaxed(fl(i, kk)) != epoch || ld_relaxed(fl(j, kk)) != epoch) atomicMin(&s_first, kk);
+      fence_acquire();
+      __syncthreads();
+      const int f = s_first;
+      __syncthreads();
+      return f;
+    };
+    const int klo = max(0, i - bwt);
+    int ready_end = klo < j ? first_unready(klo) : j;
+    auto ensure = [&](int k) {
+      if (k < ready_end) return;
+      if (t == 0) {
+        while (ld_relaxed(fl(i, k)) != epoch) __nanosleep(64);
+        while (ld_relaxed(fl(j, k)) != epoch) __nanosleep(64);
+        fence_acquire();
+      }
+      __syncthreads();
+      ready_end = max(k + 1, first_unready(k + 1));
+    };
+    if (klo < j) {
+      ensure(klo);
+      fetch(klo);
+      stash(klo & 1);
+    }
+    __syncthreads();
+    for (int k = klo; k < j; ++k) {
+      const bool more = k + 1 < j;
+      if (more) {
+        ensure(k + 1);
+        fetch(k + 1);  // in flight during the products below
+      }
+      const int bf = k & 1;
+#pragma unroll
+      for (int kk = 0; kk < 32; kk += 4) {
+        double a[2], b[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) a[q] = -Xs[bf][kk + (lane & 3)][wm + q * 8 + (lane >> 2)];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) b[q] = Ys[bf][kk + (lane & 3)][wn + q * 8 + (lane >> 2)];
+#pragma unroll
+        for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+          for (int b2 = 0; b2 < 2; ++b2) dmma(acc[a2][b2][0], acc[a2][b2][1], a[a2], b[b2]);
+      }
+      if (more) stash(bf ^ 1);
+      __syncthreads();
+    }
+    if (i == j) {
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = wm + a * 8 + (lane >> 2), c = wn + b * 8 + 2 * (lane & 3) + h;
+            if (r < ib && c < jb && c <= r) A[(i0 + r) + static_cast<size_t>(j0 + c) * lda] = acc[a][b][h];
+          }
+      __syncthreads();
+      if (w == 0) warp_potrf_inv32(A + j0 + static_cast<size_t>(j0) * lda, lda, jb, linv + static_cast<size_t>(j) * 1024, info, wsh);
+    } else {
+      if (t == 0) {
+        while (ld_relaxed(fl(j, j)) != epoch) __nanosleep(64);
+        fence_acquire();
+      }
+      // L_ij = A_ij Linv_j^T: Xs[q][r] = A_ij(r, q), Ys[q][c] = Linv_j(c, q)
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = wm + a * 8 + (lane >> 2), c = wn + b * 8 + 2 * (lane & 3) + h;
+            Xs[0][c][r] = acc[a][b][h];
+            acc[a][b][h] = 0.0;
+          }
+      __syncthreads();
+      const double* lj = linv + static_cast<size_t>(j) * 1024;
+      for (int e = t; e < 1024; e += 128) Ys[0][e >> 5][e & 31] = __ldcg(lj + e);
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < 32; kk += 4) {
+        double a[2], b[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) a[q] = Xs[0][kk + (lane & 3)][wm + q * 8 + (lane >> 2)];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) b[q] = Ys[0][kk + (lane & 3)][wn + q * 8 + (lane >> 2)];
+#pragma unroll
+        for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+          for (int b2 = 0; b2 < 2; ++b2) dmma(acc[a2][b2][0], acc[a2][b2][1], a[a2], b[b2]);
+      }
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = wm + a * 8 + (lane >> 2), c = wn + b * 8 + 2 * (lane & 3) + h;
+            if (r < ib && c < jb) A[(i0 + r) + static_cast<size_t>(j0 + c) * lda] = acc[a][b][h];
+          }
+    }
+    __threadfence();
+    __syncthreads();
+    if (t == 0) st_release(fl(i, j), epoch);
+  }
+}
+
 void potrf_lower32(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X, int ldx,
                    int band) {
   const int nt = (n + NB32 - 1) / NB32;
@@ -1082,6 +1286,23 @@ void potrf_lower32(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X
   double* linv = ctx->ws<double>(S_LINV, static_cast<size_t>(nt) * NB32 * NB32);
   ctx->linv_owner = nullptr;  // 32-wide inverse tiles: not usable by trsm_left_lower
   ctx->linv32_owner = A;
+  if (!X && !ctx->force_coop_potrf) {
+    // the task dataflow (k_potrf_flow32)
+    const size_t nflag = static_cast<size_t>(nt) * (bwt + 1);
+    int* flags = ctx->ws<int>(S_FLOWFLAG, nflag + 4);
+    unsigned long long* counter = reinterpret_cast<unsigned long long*>(flags + nflag + (nflag & 1));
+    TLG_CUDA(cudaMemsetAsync(flags, 0, (nflag + 4) * sizeof(int), ctx->stream));
+    int per_sm = 0;
+    TLG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_potrf_flow32, 128, 0));
+    const long long tasks = static_cast<long long>(nt - bwt) * (bwt + 1) + static_cast<long long>(bwt) * (bwt + 1) / 2;
+    const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(tasks, static_cast<long long>(ctx->num_sms) * std::max(1, std::min(per_sm, TLG_PF_MINB)))));
+    int epoch = 1;
+    void* args[] = {&A, &n, &lda, &bwt, &linv, &info, &flags, &counter, &epoch};
+    TLG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_potrf_flow32), dim3(grid),
+                                         dim3(128), args, 0, ctx->stream));
+    ++ctx->launches;
+    return;
+  }
   int per_sm = 0;
   TLG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_potrf_coop32, 128, 0));
   int maxtiles = nt;

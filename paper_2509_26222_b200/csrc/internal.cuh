@@ -136,6 +136,7 @@ struct tlg_ctx {
   const double* linv_owner = nullptr;
   const double* linv32_owner = nullptr;  // factor whose 32-wide tile inverses S_LINV holds
   bool force_nb64 = false;  // dense_bench: force the 64-wide factorisation
+  bool force_coop_potrf = false;  // diagnostics: the grid-barrier 32-wide factorisation
 
   template <typename T>
   T* ws(int slot, size_t count) {
