@@ -27,6 +27,9 @@ tlg_status tlg_diag_potrf(tlg_ctx* ctx, int n, const double* A, int tile, int ba
  * assembly when the centres are mesh nodes), 1 = the row-wise CSR Gram
  * always (the A/B reference for the lattice path). */
 tlg_status tlg_diag_set_batch_gram(tlg_model* m, int csr);
+/* 1 when m's most recent Gram assembly (batch ridge, information-form
+ * update) took the lattice element path, else 0. */
+tlg_status tlg_diag_last_gram_lattice(const tlg_model* m, int* lattice);
 
 #ifdef __cplusplus
 }

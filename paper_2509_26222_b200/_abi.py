@@ -216,6 +216,8 @@ def load_diag() -> C.CDLL:
                                      C.c_void_p]
         d.tlg_diag_set_batch_gram.restype = C.c_int
         d.tlg_diag_set_batch_gram.argtypes = [C.c_void_p, C.c_int]
+        d.tlg_diag_last_gram_lattice.restype = C.c_int
+        d.tlg_diag_last_gram_lattice.argtypes = [C.c_void_p, C.POINTER(C.c_int)]
         _diag = d
     return _diag
 

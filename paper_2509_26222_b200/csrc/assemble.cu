@@ -339,10 +339,15 @@ bool lattice_gram_device(tlg_model* m, const double* x, const double* y, const d
   tlg_ctx* ctx = m->ctx;
   cudaStream_t s = ctx->stream;
   const LatticeGrid& LG = m->lat;
+  m->last_gram_lattice = 0;
   if (!LG.valid || LG.win < 4 || LG.win > 12 || mm >= (1ull << 32)) return false;
   const int win = LG.win;
   const LatticeView L = lattice_view(m);
   const size_t nn = static_cast<size_t>(LG.ni) * LG.nj;
+  // the per-cell blocks pay off from ~8 observations per lattice cell (a
+  // dense scan, C5: ~90); sparse batches (C3: ~3 per cell) keep the row-wise
+  // CSR Gram, whose cost does not carry the fixed per-cell work
+  if (mm < 8 * nn) return false;
   const int ko = win * (2 * win - 1);
   // column segments: >= 4 CTAs per SM in all, each >= WIN cells long (same-
   // parity segments of one column then never share a node window)
@@ -409,6 +414,7 @@ bool lattice_gram_device(tlg_model* m, const double* x, const double* y, const d
   TLG_CUDA(cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, s));
   TLG_CUDA(cudaStreamSynchronize(s));
   if (h) throw Error(TLG_RUNTIME_ERROR, "batch ridge: lattice Gram entry outside the band");
+  m->last_gram_lattice = 1;
   return true;
 }
 

@@ -194,17 +194,132 @@ __global__ void __launch_bounds__(128) k_gemm_grouped(const GemmDesc* __restrict
   gemm_tile(d, blockIdx.x, blockIdx.y);
 }
 
+// One right-hand side with long K and few row tiles (the update's
+// y = X v with X = L^-1, n = 4096: 64 row tiles): split K over CTAs so every
+// SM streams A, partial y per slice, then an order-fixed sum.
+__global__ void __launch_bounds__(128) k_gemv_splitk(GemmDesc d, int kslice, double* __restrict__ part) {
+  const int m0 = blockIdx.x * TM, s2 = blockIdx.y;
+  const int k_hi = (d.uplo == 2) ? min(d.K, m0 + TM) : d.K;
+  const int k_lo = s2 * kslice;
+  double* P = part + (size_t)s2 * d.M;
+  if (k_lo >= k_hi) {
+    if (threadIdx.x < TM && m0 + threadIdx.x < d.M) P[m0 + threadIdx.x] = 0.0;
+    return;
+  }
+  GemmDesc e = d;
+  e.A += e.ta ? k_lo : (size_t)k_lo * e.lda;
+  e.B += e.tb ? (size_t)k_lo * e.ldb : k_lo;
+  e.K = min(kslice, k_hi - k_lo);
+  e.C = P;
+  e.ldc = d.M;
+  e.alpha = 1.0;
+  e.beta = 0.0;
+  e.uplo = 0;
+  gemv_tile(e, m0, e.K);
+}
+
+__global__ void k_gemv_reduce(GemmDesc d, int splits, const double* __restrict__ part) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= d.M) return;
+  double v = 0.0;
+  for (int s2 = 0; s2 < splits; ++s2) v += part[(size_t)s2 * d.M + r];
+  v *= d.alpha;
+  double* p = d.C + r;
+  *p = (d.beta == 0.0) ? v : fma(d.beta, *p, v);
+}
+
 void gemm(tlg_ctx* ctx, const GemmDesc& d) {
   if (d.M <= 0 || d.N <= 0) return;
+  const int tm = (d.M + TM - 1) / TM;
+  if (d.N == 1 && d.K >= 1024 && tm < 2 * ctx->num_sms) {
+    const int splits = std::max(1, std::min((4 * ctx->num_sms + tm - 1) / tm, d.K / 256));
+    const int kslice = (d.K + splits - 1) / splits;
+    // the partial rows live in the output's workspace-free slot (b may alias C)
+    double* part = ctx->ws<double>(S_GEMVPART, static_cast<size_t>(splits) * d.M);
+    k_gemv_splitk<<<dim3(tm, splits), 128, 0, ctx->stream>>>(d, kslice, part);
+    TLG_LAUNCHED(ctx);
+    k_gemv_reduce<<<(d.M + 255) / 256, 256, 0, ctx->stream>>>(d, splits, part);
+    TLG_LAUNCHED(ctx);
+    return;
+  }
   dim3 grid((d.M + TM - 1) / TM, (d.N + TN - 1) / TN);
   k_gemm<<<grid, 128, 0, ctx->stream>>>(d);
   TLG_LAUNCHED(ctx);
 }
 
-void gemm_grouped(tlg_ctx* ctx, const GemmDesc* d_descs, int count, int max_m, int max_n) {
+// Split-K grouped GEMM: CTA (tm, tn, q * S + s) runs descriptor q over its
+// s-th K slice into a private partial tile; k_gemm_splitk_reduce sums the S
+// slices in order (deterministic) and applies alpha / beta. For few, small
+// outputs with long K (the update's per-block X_q^T X_q products: ~50 blocks
+// of 84 x 84, K up to n) the plain grouped GEMM leaves most SMs idle.
+__global__ void __launch_bounds__(128) k_gemm_grouped_splitk(const GemmDesc* __restrict__ ds, int splits,
+                                                             int kslice, double* __restrict__ part,
+                                                             int ldp, size_t pstride) {
+  const int q = blockIdx.z / splits, sidx = blockIdx.z % splits;
+  GemmDesc d = ds[q];
+  const int k_lo = sidx * kslice;
+  if (k_lo >= d.K || d.uplo != 0) {
+    if (d.uplo == 0) {  // an empty slice still owns its partial tile
+      const int m0 = blockIdx.x * TM, n0 = blockIdx.y * TN;
+      double* P = part + blockIdx.z * pstride;
+      for (int e = threadIdx.x; e < TM * TN; e += 128) {
+        const int r = m0 + (e & 63), c = n0 + (e >> 6);
+        if (r < d.M && c < d.N) P[r + (size_t)c * ldp] = 0.0;
+      }
+    }
+    return;
+  }
+  d.A += d.ta ? k_lo : (size_t)k_lo * d.lda;
+  d.B += d.tb ? (size_t)k_lo * d.ldb : k_lo;
+  d.K = min(kslice, d.K - k_lo);
+  d.C = part + blockIdx.z * pstride;
+  d.ldc = ldp;
+  d.alpha = 1.0;
+  d.beta = 0.0;
+  gemm_tile(d, blockIdx.x, blockIdx.y);
+}
+
+__global__ void k_gemm_splitk_reduce(const GemmDesc* __restrict__ ds, int splits,
+                                     const double* __restrict__ part, int ldp, size_t pstride,
+                                     int max_m, int max_n) {
+  const int q = blockIdx.y;
+  const GemmDesc d = ds[q];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < max_m * max_n; e += gridDim.x * blockDim.x) {
+    const int r = e % max_m, c = e / max_m;
+    if (r >= d.M || c >= d.N) continue;
+    double v = 0.0;
+    for (int s2 = 0; s2 < splits; ++s2) v += part[(q * splits + s2) * pstride + r + (size_t)c * ldp];
+    double* p = d.C + r + (size_t)c * d.ldc;
+    v *= d.alpha;
+    *p = (d.beta == 0.0) ? v : fma(d.beta, *p, v);
+  }
+}
+
+void gemm_grouped(tlg_ctx* ctx, const GemmDesc* d_descs, int count, int max_m, int max_n, int max_k) {
   if (count <= 0 || max_m <= 0 || max_n <= 0) return;
-  dim3 grid((max_m + TM - 1) / TM, (max_n + TN - 1) / TN, count);
-  k_gemm_grouped<<<grid, 128, 0, ctx->stream>>>(d_descs);
+  const int tm = (max_m + TM - 1) / TM, tn = (max_n + TN - 1) / TN;
+  const long long tiles = static_cast<long long>(tm) * tn * count;
+  // slices of >= 256 along K until ~4 CTAs per SM are busy
+  int splits = 1;
+  if (max_k > 512) {
+    const long long want = (4ll * ctx->num_sms + tiles - 1) / tiles;
+    splits = static_cast<int>(std::max(1ll, std::min<long long>(want, max_k / 256)));
+  }
+  if (splits == 1) {
+    dim3 grid(tm, tn, count);
+    k_gemm_grouped<<<grid, 128, 0, ctx->stream>>>(d_descs);
+    TLG_LAUNCHED(ctx);
+    return;
+  }
+  const int kslice = ((max_k + splits - 1) / splits + TK - 1) / TK * TK;
+  const int ldp = tm * TM;
+  const size_t pstride = static_cast<size_t>(ldp) * tn * TN;
+  double* part = ctx->ws<double>(S_GRAMPART, pstride * count * splits);
+  dim3 grid(tm, tn, count * splits);
+  k_gemm_grouped_splitk<<<grid, 128, 0, ctx->stream>>>(d_descs, splits, kslice, part, ldp, pstride);
+  TLG_LAUNCHED(ctx);
+  dim3 rgrid(static_cast<unsigned>(std::min(64, (max_m * max_n + 255) / 256)), count);
+  k_gemm_splitk_reduce<<<rgrid, 256, 0, ctx->stream>>>(d_descs, splits, part, ldp, pstride, max_m, max_n);
   TLG_LAUNCHED(ctx);
 }
 

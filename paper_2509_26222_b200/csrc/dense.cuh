@@ -22,7 +22,9 @@ struct GemmDesc {
 
 void gemm(tlg_ctx* ctx, const GemmDesc& d);
 // Grouped GEMM over `count` descriptors already resident in device memory.
-void gemm_grouped(tlg_ctx* ctx, const GemmDesc* d_descs, int count, int max_m, int max_n);
+// max_k > 512 lets long-K groups run split-K (uplo 0 descriptors only).
+void gemm_grouped(tlg_ctx* ctx, const GemmDesc* d_descs, int count, int max_m, int max_n,
+                  int max_k = 0);
 
 // In-place lower Cholesky (A = L L^T) of the n x n matrix at A (lda).
 // `info` (device int) is set non-zero when a pivot is not positive/finite.

@@ -215,4 +215,11 @@ tlg_status tlg_diag_set_batch_gram(tlg_model* m, int csr) {
   });
 }
 
+tlg_status tlg_diag_last_gram_lattice(const tlg_model* m, int* lattice) {
+  return diag_guard([&] {
+    require(m != nullptr && lattice != nullptr, TLG_INVALID_ARGUMENT, "null argument");
+    *lattice = m->last_gram_lattice;
+  });
+}
+
 }  // extern "C"

@@ -105,7 +105,7 @@ enum Slot : int {
   S_COUNT, S_ACTIVE, S_BLOCKFLAG, S_ROWOF, S_MERGED, S_ROWPTR, S_COLIDX, S_MTVAL,
   S_KMAT, S_SMAT, S_RESID, S_U, S_YMAT, S_HMAT, S_WORK1, S_WORK2, S_WORK3, S_BLKTAB,
   S_MOMENT_ROW, S_TROWP, S_TKEYS, S_LINV, S_XINV, S_XINV2, S_SOLVE, S_BSOLVE, S_VALIDATE,
-  S_GRAMPART, S_LATGRAM, S_LATSTART, S_LATPTS, S_LATNROW, S_FLOWFLAG,
+  S_GRAMPART, S_LATGRAM, S_LATSTART, S_LATPTS, S_LATNROW, S_FLOWFLAG, S_GEMVPART,
   S_NUM_SLOTS
 };
 
@@ -361,6 +361,7 @@ struct tlg_model {
   bool grid_dirty = true;
   bool exact_cutoff = false;  // force the per-pair cutoff test (tlg_model_set_exact_cutoff)
   bool batch_csr_gram = false;  // diagnostics: batch Gram by CSR rows even on a lattice
+  int last_gram_lattice = 0;    // diagnostics: the last Gram assembly took the lattice path
   // structural nonzeros of the banded batch system (positions in band
   // storage of centre pairs within 2 cutoffs): packs the partial systems of
   // the point-sharded fit for the cross-rank reduction; keyed by the centre

@@ -1214,10 +1214,16 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
       }
     }
     tr.mark("H0");
-    const TCsr t = transpose_csr(ctx, c, mm, n);
-    gram_band(ctx, t, c, n, band, H, n);
-    k_row_dot<<<(n + 7) / 8, 256, 0, s>>>(t.rowp, t.obs, t.val, resid, n, dw);
-    TLG_LAUNCHED(ctx);
+    // H += Mt Mt^T (lower band; the factorisation reads the lower triangle
+    // only) and dw = Mt resid: the lattice element assembly when the centres
+    // are mesh nodes, else the row-wise CSR Gram
+    TLG_CUDA(cudaMemsetAsync(dw, 0, sizeof(double) * n, s));
+    if (m->batch_csr_gram || !lattice_gram_device(m, x, y, resid, mm, rowof, band, H, n, dw)) {
+      const TCsr t = transpose_csr(ctx, c, mm, n);
+      gram_band(ctx, t, c, n, band, H, n);
+      k_row_dot<<<(n + 7) / 8, 256, 0, s>>>(t.rowp, t.obs, t.val, resid, n, dw);
+      TLG_LAUNCHED(ctx);
+    }
     // X = L^-1 from the factorisation; (H^-1)_qq = X[:,q]^T X[:,q]
     tr.mark("gram");
     double* X = ctx->ws<double>(S_YMAT, static_cast<size_t>(n) * n);
@@ -1233,6 +1239,7 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
     double* v = ctx->ws<double>(S_SOLVE, n);
     gemm(ctx, GemmDesc{n, 1, n, X, n, 0, dw, n, 0, v, n, 1.0, 0.0, 2});
     gemm(ctx, GemmDesc{n, 1, n, X, n, 1, v, n, 0, dw, n, 1.0, 0.0, 0});
+    tr.mark("solve");
     for (int q = 0; q < nq; ++q) {
       const size_t o = tab[q].off;
       descs[q] = GemmDesc{tab[q].n, tab[q].n, n - tab[q].off, X + o + o * n, n, 1,
@@ -1244,7 +1251,13 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   GemmDesc* h_descs = static_cast<GemmDesc*>(ctx->host_stage(nq * sizeof(GemmDesc)));
   std::memcpy(h_descs, descs.data(), nq * sizeof(GemmDesc));
   TLG_CUDA(cudaMemcpyAsync(d_descs, h_descs, nq * sizeof(GemmDesc), cudaMemcpyHostToDevice, s));
-  gemm_grouped(ctx, d_descs, nq, maxq, maxq);
+  int maxk = 0;
+  bool plain = true;
+  for (const auto& dq : descs) {
+    maxk = std::max(maxk, dq.K);
+    plain = plain && dq.uplo == 0;
+  }
+  gemm_grouped(ctx, d_descs, nq, maxq, maxq, plain ? maxk : 0);
   tr.mark("blocks");
   {
     const size_t smem = sizeof(double) * static_cast<size_t>(maxq) * maxq;

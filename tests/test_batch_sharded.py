@@ -4,6 +4,8 @@ stored in band form (ld < n) against the oracle's dense LDLT
 (terrain_model.cpp:269-308), and the assemble / sum / solve split — two
 shards emulated on one GPU, and the world-1 driver — against the single-call
 fit."""
+import ctypes as C
+
 import numpy as np
 import pytest
 import torch
@@ -152,6 +154,10 @@ def test_batch_lattice_assembly_matches_csr_gram(gpu_ctx, sigma, sigma_eps, side
     g = T.TerrainModel(k, cs)
     assert g.sweep()[0] != 0  # a lattice
     H1, b1 = _assemble(g, obs, csr=False)
+    from paper_2509_26222_b200 import _abi
+    used = C.c_int()
+    _abi.check(_abi.load_diag().tlg_diag_last_gram_lattice(g.handle, C.byref(used)))
+    assert used.value == 1  # the lattice path ran
     H0, b0 = _assemble(g, obs, csr=True)
     assert float((H1 - H0).abs().max()) <= 1e-12 * float(H0.abs().max())
     assert float((b1 - b0).abs().max()) <= 1e-12 * float(b0.abs().max())
