@@ -193,7 +193,7 @@ void error_histogram_device(tlg_model* m, const double* x, const double* y, cons
   unsigned long long* d_counts = ctx->ws<unsigned long long>(S_COUNT, bins + 1);
   TLG_CUDA(cudaMemsetAsync(d_counts, 0, (bins + 1) * sizeof(unsigned long long), s));
   if (keep) {
-    const unsigned hb = static_cast<unsigned>(std::min<size_t>((keep + 255) / 256, 2 * 148));
+    const unsigned hb = static_cast<unsigned>(std::min<size_t>((keep + 255) / 256, 2ull * ctx->num_sms));
     k_error_bins<<<hb, 256, (bins + 1) * sizeof(unsigned long long), s>>>(bits2, keep, bins,
                                                                          d_counts);
     TLG_LAUNCHED(ctx);

@@ -1230,6 +1230,7 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
   const long long T0 = static_cast<long long>(nt - bwt) * (bwt + 1);
   const long long total = T0 + static_cast<long long>(bwt) * (bwt + 1) / 2;
   auto fl = [&](int i, int j) { return flag + static_cast<size_t>(j) * (bwt + 1) + (i - j); };
+  const bool async_ok = (lda % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0);
   for (;;) {
     if (t == 0) task_s = static_cast<long long>(atomicAdd(counter, 1ull));
     __syncthreads();
@@ -1280,6 +1281,26 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
         Ys[buf][e >> 5][e & 31] = pb[s2];
       }
     };
+    // Asynchronous operand copy (cp.async, LDGSTS: global -> shared without
+    // registers) when rows pair into 16-byte chunks (even lda): chunk
+    // c = t + 128 s covers rows 2 (c & 15), 2 (c & 15) + 1 of column c >> 4;
+    // rows past n are zero-filled.
+    auto fetch_async = [&](int k, int buf) {
+      const int k0 = k * 32;
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) {
+        const int c = t + 128 * s2, tile = c >> 9, q = (c >> 4) & 31, r = 2 * (c & 15);
+        const int row = (tile ? j0 : i0) + r;
+        const int bytes = k0 + q < n ? 8 * max(0, min(2, n - row)) : 0;
+        const double* src = A + (bytes ? row + static_cast<size_t>(k0 + q) * lda : 0);
+        double* dst = tile ? &Ys[buf][q][r] : &Xs[buf][q][r];
+        const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(bytes)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    auto wait_async = [&]() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); };
     // Operand readiness: one parallel sweep of the flags of all remaining k
     // (one round trip) gives the first k not yet final; k below it need no
     // further polling.
@@ -1308,15 +1329,22 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
     };
     if (klo < j) {
       ensure(klo);
-      fetch(klo);
-      stash(klo & 1);
+      if (async_ok) {
+        fetch_async(klo, klo & 1);
+        wait_async();
+      } else {
+        fetch(klo);
+        stash(klo & 1);
+      }
     }
     __syncthreads();
     for (int k = klo; k < j; ++k) {
       const bool more = k + 1 < j;
       if (more) {
         ensure(k + 1);
-        fetch(k + 1);  // in flight during the products below
+        // in flight during the products below
+        if (async_ok) fetch_async(k + 1, (k + 1) & 1);
+        else fetch(k + 1);
       }
       const int bf = k & 1;
 #pragma unroll
@@ -1331,7 +1359,10 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
 #pragma unroll
           for (int b2 = 0; b2 < 2; ++b2) dmma(acc[a2][b2][0], acc[a2][b2][1], a[a2], b[b2]);
       }
-      if (more) stash(bf ^ 1);
+      if (more) {
+        if (async_ok) wait_async();
+        else stash(bf ^ 1);
+      }
       __syncthreads();
     }
     if (i == j) {
@@ -1491,7 +1522,7 @@ __global__ void k_symmetrize(double* __restrict__ A, int n, int lda) {
 void symmetrize(tlg_ctx* ctx, double* A, int n, int lda) {
   if (n <= 1) return;
   const long long tot = (long long)n * n;
-  const unsigned b = static_cast<unsigned>(std::min<long long>((tot + 255) / 256, 4 * 148));
+  const unsigned b = static_cast<unsigned>(std::min<long long>((tot + 255) / 256, 4ull * ctx->num_sms));
   k_symmetrize<<<b, 256, 0, ctx->stream>>>(A, n, lda);
   TLG_LAUNCHED(ctx);
 }

@@ -307,7 +307,7 @@ static void build_lattice(tlg_model* m) {
   int* st = ctx->ws<int>(S_COUNT, 8);
   const int hs[8] = {0, INT_MAX, INT_MAX, INT_MIN, INT_MIN, 0, 0, 0};
   TLG_CUDA(cudaMemcpyAsync(st, hs, sizeof(hs), cudaMemcpyHostToDevice, s));
-  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 4 * 148));
+  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 4ull * ctx->num_sms));
   k_lattice_check<<<blocks, 256, 0, s>>>(m->cx.p, m->cy.p, n, mnx, mny, res, st);
   TLG_LAUNCHED(ctx);
   int h[8];
@@ -432,7 +432,7 @@ void build_center_grid(tlg_model* m) {
   int* bbox = ctx->ws<int>(S_COUNT, 4);
   const int hb[4] = {INT_MAX, INT_MAX, INT_MIN, INT_MIN};
   TLG_CUDA(cudaMemcpyAsync(bbox, hb, sizeof(hb), cudaMemcpyHostToDevice, s));
-  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 4 * 148));
+  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 4ull * ctx->num_sms));
   k_cell_coords<<<blocks, 256, 0, s>>>(m->cx.p, m->cy.p, n, g.cell, ix, iy, bbox);
   TLG_LAUNCHED(ctx);
   int hbox[4];

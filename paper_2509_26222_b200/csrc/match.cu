@@ -1046,7 +1046,7 @@ void feature_normal_eq_device(tlg_map* m, const double R[9], const double t[3], 
   Pose P;
   for (int i = 0; i < 9; ++i) P.R[i] = R[i];
   for (int i = 0; i < 3; ++i) P.t[i] = t[i];
-  const int blocks = static_cast<int>(std::min<size_t>((m->nc + kNeThreads - 1) / kNeThreads, 148));
+  const int blocks = static_cast<int>(std::min<size_t>((m->nc + kNeThreads - 1) / kNeThreads, static_cast<size_t>(ctx->num_sms)));
   double* partials = ctx->ws<double>(S_PARTIALS, static_cast<size_t>(blocks) * 29);
   k_feature_ne<<<blocks, kNeThreads, 0, s>>>(m->nc, m->c_kind.p, m->c_ps.p, m->c_par.p, m->c_w.p,
                                              P, partials);

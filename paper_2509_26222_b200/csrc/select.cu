@@ -40,7 +40,7 @@ int* validate_obs_launch(tlg_ctx* ctx, const double* x, const double* y, const d
   if (m == 0) throw Error(TLG_INVALID_ARGUMENT, "empty observation");
   int* err = ctx->ws<int>(S_VALIDATE, 1);
   TLG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
-  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((m + 255) / 256, 8 * 148));
+  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((m + 255) / 256, 8ull * ctx->num_sms));
   k_validate<<<blocks, 256, 0, ctx->stream>>>(x, y, z, m, zn, err);
   TLG_LAUNCHED(ctx);
   return err;
@@ -223,7 +223,7 @@ size_t supported_nodes_device(tlg_ctx* ctx, const double* x, const double* y, si
   uint64_t* skey = ctx->ws<uint64_t>(S_KEYS2, m);
   uint32_t* idx = ctx->ws<uint32_t>(S_VALS, m);
   uint32_t* sidx = ctx->ws<uint32_t>(S_VALS2, m);
-  const unsigned kb = static_cast<unsigned>(std::min<size_t>((m + 255) / 256, 2 * 148));
+  const unsigned kb = static_cast<unsigned>(std::min<size_t>((m + 255) / 256, 2ull * ctx->num_sms));
   double* part = ctx->ws<double>(S_PARTIALS, 4 * kb);
   k_point_keys<<<kb, 256, 0, s>>>(x, y, m, p.cell, key, idx, part);
   TLG_LAUNCHED(ctx);
@@ -241,7 +241,7 @@ size_t supported_nodes_device(tlg_ctx* ctx, const double* x, const double* y, si
   TLG_LAUNCHED(ctx);
 
   uint8_t* flag = ctx->ws<uint8_t>(S_NODE_FLAG, static_cast<size_t>(total));
-  const unsigned nb = static_cast<unsigned>(std::min<long long>((total + 255) / 256, 16 * 148));
+  const unsigned nb = static_cast<unsigned>(std::min<long long>((total + 255) / 256, 16ull * ctx->num_sms));
   k_count_nodes<<<nb, 256, 0, s>>>(skey, sx, sy, mi, p, win, flag);
   TLG_LAUNCHED(ctx);
 

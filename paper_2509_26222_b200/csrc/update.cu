@@ -170,8 +170,8 @@ __global__ void __launch_bounds__(128) k_csr_fill_w(GridView g, const double* __
   }
 }
 
-static unsigned warp_grid(size_t m) {
-  return static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>((m + 3) / 4, 64 * 148)));
+static unsigned warp_grid(size_t m, int num_sms) {
+  return static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>((m + 3) / 4, 64ull * num_sms)));
 }
 
 struct Csr {
@@ -189,7 +189,7 @@ static Csr build_csr(tlg_model* m, const double* x, const double* y, size_t mm, 
   Csr c;
   c.rowp = rowp_in ? rowp_in : ctx->ws<uint32_t>(S_ROWPTR, mm + 1);
   const GridView g = grid_view(m);
-  k_csr_count_w<<<warp_grid(mm), 128, 0, s>>>(g, x, y, mm, m->kc.r2, neg_inv_2b2, c.rowp);
+  k_csr_count_w<<<warp_grid(mm, ctx->num_sms), 128, 0, s>>>(g, x, y, mm, m->kc.r2, neg_inv_2b2, c.rowp);
   TLG_LAUNCHED(ctx);
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.rowp, c.rowp, (int)(mm + 1), s);
@@ -204,7 +204,7 @@ static Csr build_csr(tlg_model* m, const double* x, const double* y, size_t mm, 
   c.nnz = hn;
   c.col = ctx->ws<uint32_t>(S_COLIDX, hn + 1);
   c.val = ctx->ws<double>(S_MTVAL, hn + 1);
-  k_csr_fill_w<<<warp_grid(mm), 128, 0, s>>>(g, x, y, mm, m->kc.r2, neg_inv_2b2, scale, c.rowp, rowof, c.col,
+  k_csr_fill_w<<<warp_grid(mm, ctx->num_sms), 128, 0, s>>>(g, x, y, mm, m->kc.r2, neg_inv_2b2, scale, c.rowp, rowof, c.col,
                                 c.val, sort_ids ? 1 : 0);
   TLG_LAUNCHED(ctx);
   return c;
@@ -530,7 +530,7 @@ static void gram_band(tlg_ctx* ctx, const TCsr& t, const Csr& c, int n, int band
     if (nch > 1) {
       TLG_LAUNCHED(ctx);
       const long long tot = static_cast<long long>(n) * width;
-      k_gram_chunks_reduce<<<static_cast<unsigned>(std::min<long long>((tot + 255) / 256, 8 * 148)), 256, 0,
+      k_gram_chunks_reduce<<<static_cast<unsigned>(std::min<long long>((tot + 255) / 256, 8ull * ctx->num_sms)), 256, 0,
                              ctx->stream>>>(partials, n, band, lower_only ? 1 : 0, nch, H, ldh);
     }
   } else {
@@ -776,7 +776,7 @@ static TCsr transpose_csr(tlg_ctx* ctx, const Csr& c, size_t m, int n) {
   TLG_CUDA(cudaMemsetAsync(t.rowp, 0, (n + 1) * sizeof(uint32_t), s));
   if (c.nnz) {
     if (n <= 12288) {
-      const unsigned b = static_cast<unsigned>(std::min<size_t>((c.nnz + 1023) / 1024, 2 * 148));
+      const unsigned b = static_cast<unsigned>(std::min<size_t>((c.nnz + 1023) / 1024, 2ull * ctx->num_sms));
       k_row_hist_smem<<<b, 256, n * sizeof(uint32_t), s>>>(c.col, c.nnz, n, t.rowp);
     } else {
       k_row_hist<<<(unsigned)((c.nnz + 255) / 256), 256, 0, s>>>(c.col, c.nnz, t.rowp);
@@ -1045,7 +1045,7 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   uint8_t* bflag = ctx->ws<uint8_t>(S_BLOCKFLAG, nb);
   TLG_CUDA(cudaMemsetAsync(active, 0, nc, s));
   TLG_CUDA(cudaMemsetAsync(bflag, 0, nb, s));
-  k_mark_active_w<<<warp_grid(mm), 128, 0, s>>>(g, x, y, mm, m->kc.r2, active);
+  k_mark_active_w<<<warp_grid(mm, ctx->num_sms), 128, 0, s>>>(g, x, y, mm, m->kc.r2, active);
   TLG_LAUNCHED(ctx);
   k_mark_blocks<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(active, m->d_block_index.p, nc, bflag);
   TLG_LAUNCHED(ctx);
@@ -1557,7 +1557,7 @@ size_t batch_pattern_device(tlg_model* m) {
 void batch_pack_device(tlg_model* m, const double* H, double* packed) {
   const size_t nnz = batch_pattern_device(m);
   if (!nnz) return;
-  const unsigned b = static_cast<unsigned>(std::min<size_t>((nnz + 255) / 256, 8 * 148));
+  const unsigned b = static_cast<unsigned>(std::min<size_t>((nnz + 255) / 256, 8ull * m->ctx->num_sms));
   k_bpat_gather<<<b, 256, 0, m->ctx->stream>>>(m->bpat.p, nnz, H, packed);
   TLG_LAUNCHED(m->ctx);
   TLG_CUDA(cudaStreamSynchronize(m->ctx->stream));
@@ -1568,7 +1568,7 @@ void batch_unpack_device(tlg_model* m, const double* packed, double* H) {
   const BatchPlan p = batch_plan(m);
   TLG_CUDA(cudaMemsetAsync(H, 0, sizeof(double) * batch_elems(p), m->ctx->stream));
   if (!nnz) return;
-  const unsigned b = static_cast<unsigned>(std::min<size_t>((nnz + 255) / 256, 8 * 148));
+  const unsigned b = static_cast<unsigned>(std::min<size_t>((nnz + 255) / 256, 8ull * m->ctx->num_sms));
   k_bpat_scatter<<<b, 256, 0, m->ctx->stream>>>(m->bpat.p, nnz, packed, H);
   TLG_LAUNCHED(m->ctx);
   TLG_CUDA(cudaStreamSynchronize(m->ctx->stream));
