@@ -46,7 +46,7 @@ struct LatGeo {
   static constexpr int kKO = WIN * (2 * WIN - 1);               // partner offsets per node
   static constexpr int kBatch = 32;                             // points per F block
   static constexpr size_t kSmem =
-      sizeof(double) * (kBatch * kFP + 4 * kBatch * WIN) + sizeof(int) * kF;
+      sizeof(double) * (kBatch * kFP + 2 * kBatch * WIN) + sizeof(uint32_t) * WIN;
 };
 
 // Cell key of each observation, the eval's window base (eval.cu
@@ -78,15 +78,38 @@ __global__ void k_lat_bounds(const uint32_t* __restrict__ key, size_t n, uint32_
   start[c] = static_cast<uint32_t>(lo);
 }
 
-__global__ void k_lat_gather(const uint32_t* __restrict__ perm, size_t n, const double* __restrict__ x,
-                             const double* __restrict__ y, const double* __restrict__ z,
-                             double* __restrict__ ox, double* __restrict__ oy, double* __restrict__ oz) {
+// Observations in cell order, with each one's reference cell-window masks
+// (GridIndex2::radius_query's (2 span + 1)^2 cells, the xr / yr ranges of the
+// lattice): bit k (x) / 16 + k (y) set when window node i0 + k / j0 + k lies
+// in a candidate cell — computed once here (a division per axis) instead of
+// per node in the assembly.
+__global__ void k_lat_gather(LatticeView L, int win, const uint32_t* __restrict__ perm,
+                             const uint32_t* __restrict__ key, uint32_t skip, size_t n,
+                             const double* __restrict__ x, const double* __restrict__ y,
+                             const double* __restrict__ z, double* __restrict__ ox,
+                             double* __restrict__ oy, double* __restrict__ oz,
+                             uint32_t* __restrict__ om) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t j = perm[i];
-  ox[i] = x[j];
-  oy[i] = y[j];
+  const double px = x[j], py = y[j];
+  ox[i] = px;
+  oy[i] = py;
   oz[i] = z[j];
+  uint32_t m = 0;
+  const uint32_t k = key[i];
+  if (k != skip) {
+    const int i0 = static_cast<int>(k / static_cast<uint32_t>(L.nj)) - L.lo;
+    const int j0 = static_cast<int>(k % static_cast<uint32_t>(L.nj)) - L.lo;
+    const int qx = static_cast<int>(floor(px / L.cell)), qy = static_cast<int>(floor(py / L.cell));
+    const int2 rx = L.xr[min(max(qx - L.xr_base, 0), L.xr_n - 1)];
+    const int2 ry = L.yr[min(max(qy - L.yr_base, 0), L.yr_n - 1)];
+    for (int a = 0; a < win; ++a) {
+      if (i0 + a >= rx.x && i0 + a < rx.y) m |= 1u << a;
+      if (j0 + a >= ry.x && j0 + a < ry.y) m |= 1u << (16 + a);
+    }
+  }
+  om[i] = m;
 }
 
 // Warp W's DMMA over one F block: tile rows R1 = W and R2 = kNT-1-W, lower
@@ -186,19 +209,17 @@ __device__ __forceinline__ void lat_flush_any(int w, double (&acc)[LatGeo<WIN>::
 template <int WIN>
 __global__ void __launch_bounds__(32 * LatGeo<WIN>::kNW, 2) k_gram_lattice(
     LatticeView L, const double* __restrict__ xs, const double* __restrict__ ys,
-    const double* __restrict__ zs, const uint32_t* __restrict__ start, int nseg, int seg_len,
-    double r2, double neg_inv_2b2, double scale, double* __restrict__ Hlat,
+    const double* __restrict__ zs, const uint32_t* __restrict__ ms, const uint32_t* __restrict__ start,
+    int nseg, int seg_len, double r2, double neg_inv_2b2, double scale, double* __restrict__ Hlat,
     double* __restrict__ blat) {
   using G = LatGeo<WIN>;
   constexpr int kB = G::kBatch;
   constexpr int kThreads = 32 * G::kNW;
   extern __shared__ __align__(16) unsigned char lat_smem[];
   double* F = reinterpret_cast<double*>(lat_smem);   // [kB][kFP]
-  double* ex = F + kB * G::kFP;                      // [kB][WIN]  scale e^{c dx^2}
-  double* ey = ex + kB * WIN;                        // [kB][WIN]  e^{c dy^2}
-  double* dx2 = ey + kB * WIN;                       // [kB][WIN]  dx^2, +inf outside the cell window
-  double* dy2 = dx2 + kB * WIN;
-  int* pres = reinterpret_cast<int*>(dy2 + kB * WIN);  // [kF] node present
+  double* sey = F + kB * G::kFP;    // [kB][WIN] e^{c dy^2}
+  double* sdy2 = sey + kB * WIN;    // [kB][WIN] dy^2, +inf outside the cell window
+  uint32_t* need = reinterpret_cast<uint32_t*>(sdy2 + kB * WIN);  // [WIN] present & not always-outside
   const int tid = threadIdx.x, w = tid >> 5;
   const int ib = blockIdx.x / nseg, seg = blockIdx.x % nseg;
   const int i0 = ib - L.lo;
@@ -215,53 +236,63 @@ __global__ void __launch_bounds__(32 * LatGeo<WIN>::kNW, 2) k_gram_lattice(
     const uint32_t p_beg = start[cell], p_end = start[cell + 1];
     if (p_beg == p_end) continue;
     const int j0 = jb - L.lo;
-    for (int u = tid; u < G::kF; u += kThreads)
-      pres[u] = L.P[(i0 + u / WIN) * static_cast<size_t>(nj) + j0 + u % WIN] != 0;
+    if (tid < WIN) {  // window column tid: nodes present, pair class not always-outside
+      uint32_t bits = 0;
+      const int* pc = L.P + (i0 + tid) * static_cast<size_t>(nj) + j0;
+      for (int l = 0; l < WIN; ++l) bits |= (pc[l] != 0 ? 1u : 0u) << l;
+      need[tid] = bits & (L.inmask[tid] | L.bdmask[tid]);
+    }
 #pragma unroll
     for (int t = 0; t <= G::kNT; ++t) acc[t][0] = acc[t][1] = 0.0;
     for (uint32_t pb = p_beg; pb < p_end; pb += kB) {
       const int cnt = static_cast<int>(min(static_cast<uint32_t>(kB), p_end - pb));
-      __syncthreads();  // the previous block's F is consumed; pres is written
-      // per-point axis factors: the exact node offsets of eval.cu's exact
-      // path and the reference's cell-window test (xr / yr ranges)
-      for (int it = tid; it < kB * 2 * WIN; it += kThreads) {
-        const int p = it / (2 * WIN), r = it % (2 * WIN);
-        if (p >= cnt) continue;
-        const int k = r % WIN;
-        if (r < WIN) {
-          const double px = xs[pb + p];
-          const int q = static_cast<int>(floor(px / L.cell));
-          const int2 rx = L.xr[min(max(q - L.xr_base, 0), L.xr_n - 1)];
-          const int node = i0 + k;
-          const double d = __dsub_rn(__dadd_rn(L.min_x, __dmul_rn(static_cast<double>(node + L.i_org), L.res)), px);
-          const double dd = __dmul_rn(d, d);
-          dx2[p * WIN + k] = (node >= rx.x && node < rx.y) ? dd : CUDART_INF;
-          ex[p * WIN + k] = scale * exp(dd * neg_inv_2b2);
-        } else {
+      __syncthreads();  // the previous block's F is consumed; need is written
+      // y factors of every (point, window row): the exact node offsets of
+      // eval.cu's exact path
+      for (int it = tid; it < kB * WIN; it += kThreads) {
+        const int p = it / WIN, r = it % WIN;
+        double e = 0.0, d2 = CUDART_INF;
+        if (p < cnt) {
           const double py = ys[pb + p];
-          const int q = static_cast<int>(floor(py / L.cell));
-          const int2 ry = L.yr[min(max(q - L.yr_base, 0), L.yr_n - 1)];
-          const int node = j0 + k;
-          const double d = __dsub_rn(__dadd_rn(L.min_y, __dmul_rn(static_cast<double>(node + L.j_org), L.res)), py);
+          const double d = __dsub_rn(__dadd_rn(L.min_y, __dmul_rn(static_cast<double>(j0 + r + L.j_org), L.res)), py);
           const double dd = __dmul_rn(d, d);
-          dy2[p * WIN + k] = (node >= ry.x && node < ry.y) ? dd : CUDART_INF;
-          ey[p * WIN + k] = exp(dd * neg_inv_2b2);
+          if ((ms[pb + p] >> (16 + r)) & 1u) d2 = dd;
+          e = exp(dd * neg_inv_2b2);
         }
+        sey[p * WIN + r] = e;
+        sdy2[p * WIN + r] = d2;
       }
       __syncthreads();
-      for (int it = tid; it < kB * G::kNT * 8; it += kThreads) {
-        const int p = it / (G::kNT * 8), u = it % (G::kNT * 8);
-        double v = 0.0;
+      // F row segment of (point p, window column r): its x factor, then the
+      // WIN pairs — always-inside pairs unconditionally, boundary pairs with
+      // the reference's no-FMA d^2 <= r^2 test (the cell window folded into
+      // dx^2 / dy^2 = +inf), always-outside and absent nodes zero
+      for (int it = tid; it < kB * WIN; it += kThreads) {
+        const int p = it / WIN, r = it % WIN;
+        double* row = F + p * G::kFP + r * WIN;
         if (p < cnt) {
-          if (u < G::kF) {
-            const int iu = u / WIN, ju = u % WIN;
-            if (pres[u] && __dadd_rn(dx2[p * WIN + iu], dy2[p * WIN + ju]) <= r2)
-              v = ex[p * WIN + iu] * ey[p * WIN + ju];
-          } else if (u == G::kF) {
-            v = zs[pb + p];
+          const double px = xs[pb + p];
+          const double d = __dsub_rn(__dadd_rn(L.min_x, __dmul_rn(static_cast<double>(i0 + r + L.i_org), L.res)), px);
+          const double dd = __dmul_rn(d, d);
+          const double dx2 = ((ms[pb + p] >> r) & 1u) ? dd : CUDART_INF;
+          const double ex = scale * exp(dd * neg_inv_2b2);
+          const uint32_t nd = need[r], inm = L.inmask[r];
+          const double* ey = sey + p * WIN;
+          const double* ey2 = sdy2 + p * WIN;
+#pragma unroll
+          for (int l = 0; l < WIN; ++l) {
+            double v = 0.0;
+            if ((nd >> l) & 1u)
+              if (((inm >> l) & 1u) || __dadd_rn(dx2, ey2[l]) <= r2) v = ex * ey[l];
+            row[l] = v;
           }
+          if (r == 0) row[G::kF] = zs[pb + p];
+        } else {
+#pragma unroll
+          for (int l = 0; l < WIN; ++l) row[l] = 0.0;
+          if (r == 0) row[G::kF] = 0.0;
         }
-        F[p * G::kFP + u] = v;
+        if (G::kF + 1 + r < G::kNT * 8) F[p * G::kFP + G::kF + 1 + r] = 0.0;
       }
       __syncthreads();
       lat_mma_any<WIN>(w, F, (cnt + 3) >> 2, acc);
@@ -319,13 +350,13 @@ __global__ void k_lat_nrow(const int* __restrict__ slot, const int* __restrict__
 
 template <int WIN>
 void launch_gram_lattice(tlg_ctx* ctx, const LatticeView& L, const double* xs, const double* ys,
-                         const double* zs, const uint32_t* start, int nseg, int seg_len,
-                         const KernelConst& kc, double* Hlat, double* blat) {
+                         const double* zs, const uint32_t* ms, const uint32_t* start, int nseg,
+                         int seg_len, const KernelConst& kc, double* Hlat, double* blat) {
   using G = LatGeo<WIN>;
   TLG_CUDA(cudaFuncSetAttribute(k_gram_lattice<WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(G::kSmem)));
   k_gram_lattice<WIN><<<static_cast<unsigned>(L.ni) * nseg, 32 * G::kNW, G::kSmem, ctx->stream>>>(
-      L, xs, ys, zs, start, nseg, seg_len, kc.r2, kc.neg_inv_2st2, kc.scale, Hlat, blat);
+      L, xs, ys, zs, ms, start, nseg, seg_len, kc.r2, kc.neg_inv_2st2, kc.scale, Hlat, blat);
 }
 
 }  // namespace
@@ -381,21 +412,22 @@ bool lattice_gram_device(tlg_model* m, const double* x, const double* y, const d
   uint32_t* start = ctx->ws<uint32_t>(S_LATSTART, nn + 1);
   k_lat_bounds<<<static_cast<unsigned>((nn + 256) / 256), 256, 0, s>>>(key2, mm, static_cast<uint32_t>(nn), start);
   TLG_LAUNCHED(ctx);
-  double* pts = ctx->ws<double>(S_LATPTS, 3 * mm);
-  k_lat_gather<<<static_cast<unsigned>((mm + 255) / 256), 256, 0, s>>>(perm, mm, x, y, z, pts, pts + mm,
-                                                                     pts + 2 * mm);
+  double* pts = ctx->ws<double>(S_LATPTS, 3 * mm + (mm + 1) / 2);
+  uint32_t* msk = reinterpret_cast<uint32_t*>(pts + 3 * mm);
+  k_lat_gather<<<static_cast<unsigned>((mm + 255) / 256), 256, 0, s>>>(
+      L, win, perm, key2, skip, mm, x, y, z, pts, pts + mm, pts + 2 * mm, msk);
   TLG_LAUNCHED(ctx);
 
   switch (win) {
-    case 4: launch_gram_lattice<4>(ctx, L, pts, pts + mm, pts + 2 * mm, start, nseg, seg_len, m->kc, Hlat, blat); break;
-    case 5: launch_gram_lattice<5>(ctx, L, pts, pts + mm, pts + 2 * mm, start, nseg, seg_len, m->kc, Hlat, blat); break;
-    case 6: launch_gram_lattice<6>(ctx, L, pts, pts + mm, pts + 2 * mm, start, nseg, seg_len, m->kc, Hlat, blat); break;
-    case 7: launch_gram_lattice<7>(ctx, L, pts, pts + mm, pts + 2 * mm, start, nseg, seg_len, m->kc, Hlat, blat); break;
-    case 8: launch_gram_lattice<8>(ctx, L, pts, pts + mm, pts + 2 * mm, start, nseg, seg_len, m->kc, Hlat, blat); break;
-    case 9: launch_gram_lattice<9>(ctx, L, pts, pts + mm, pts + 2 * mm, start, nseg, seg_len, m->kc, Hlat, blat); break;
-    case 10: launch_gram_lattice<10>(ctx, L, pts, pts + mm, pts + 2 * mm, start, nseg, seg_len, m->kc, Hlat, blat); break;
-    case 11: launch_gram_lattice<11>(ctx, L, pts, pts + mm, pts + 2 * mm, start, nseg, seg_len, m->kc, Hlat, blat); break;
-    default: launch_gram_lattice<12>(ctx, L, pts, pts + mm, pts + 2 * mm, start, nseg, seg_len, m->kc, Hlat, blat); break;
+    case 4: launch_gram_lattice<4>(ctx, L, pts, pts + mm, pts + 2 * mm, msk, start, nseg, seg_len, m->kc, Hlat, blat); break;
+    case 5: launch_gram_lattice<5>(ctx, L, pts, pts + mm, pts + 2 * mm, msk, start, nseg, seg_len, m->kc, Hlat, blat); break;
+    case 6: launch_gram_lattice<6>(ctx, L, pts, pts + mm, pts + 2 * mm, msk, start, nseg, seg_len, m->kc, Hlat, blat); break;
+    case 7: launch_gram_lattice<7>(ctx, L, pts, pts + mm, pts + 2 * mm, msk, start, nseg, seg_len, m->kc, Hlat, blat); break;
+    case 8: launch_gram_lattice<8>(ctx, L, pts, pts + mm, pts + 2 * mm, msk, start, nseg, seg_len, m->kc, Hlat, blat); break;
+    case 9: launch_gram_lattice<9>(ctx, L, pts, pts + mm, pts + 2 * mm, msk, start, nseg, seg_len, m->kc, Hlat, blat); break;
+    case 10: launch_gram_lattice<10>(ctx, L, pts, pts + mm, pts + 2 * mm, msk, start, nseg, seg_len, m->kc, Hlat, blat); break;
+    case 11: launch_gram_lattice<11>(ctx, L, pts, pts + mm, pts + 2 * mm, msk, start, nseg, seg_len, m->kc, Hlat, blat); break;
+    default: launch_gram_lattice<12>(ctx, L, pts, pts + mm, pts + 2 * mm, msk, start, nseg, seg_len, m->kc, Hlat, blat); break;
   }
   TLG_LAUNCHED(ctx);
 
