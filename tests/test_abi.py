@@ -59,3 +59,13 @@ def test_no_gpu_fails_loudly():
     assert st == _abi.TLG_CUDA_ERROR
     with pytest.raises(_abi.CudaError):
         _abi.check(st)
+
+
+def test_diag_library_exports_its_header():
+    """include/terralio_diag.h (diagnostics, not the product ABI) is served by
+    libterralio_diag.so."""
+    text = (ROOT / "include" / "terralio_diag.h").read_text()
+    names = sorted(set(re.findall(r"\b(tlg_diag_[a-z0-9_]+)\s*\(", text)))
+    assert len(names) >= 5
+    lib = C.CDLL(str(_abi.lib_path().parent / "libterralio_diag.so"))
+    assert not [n for n in names if not hasattr(lib, n)]
