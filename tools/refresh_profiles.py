@@ -2,7 +2,10 @@
 after the bench / ncu commands of DESIGN §5 wrote gpurun_out/): the bench
 line, the reference arm, the launch list + summary, the k_manifold ncu
 details + instruction mix + stalls, and profiles/kernel_traffic.json.
-Usage: python tools/refresh_profiles.py <tag>   (e.g. r1i)"""
+Usage: python tools/refresh_profiles.py <tag> [prefix]   (e.g. r2 r2)
+With gpurun_out/batch_fit_<tag>.ncu-rep present, also writes
+profiles/<prefix>_ncu_batch_fit.txt (lattice assembly, flow Cholesky, flow
+band solve)."""
 import collections
 import csv
 import json
@@ -16,15 +19,40 @@ OUT = ROOT / "gpurun_out"
 PROF = ROOT / "profiles"
 
 
-def main(tag):
-    shutil.copy(OUT / f"bench_{tag}.json", PROF / "r1_bench.json")
-    shutil.copy(OUT / f"bench_ref_{tag}.json", PROF / "r1_bench_reference_arm.json")
-    shutil.copy(OUT / f"launches_{tag}.csv", PROF / "r1_bench_launches.csv")
+def batch_fit_summary(rep, dst):
+    raw = list(csv.reader(subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"],
+                                         capture_output=True, text=True).stdout.splitlines()))
+    hdr, units = raw[0], raw[1]
+    want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+            "launch__grid_size", "lts__t_sector_hit_rate.pct"]
+    lines = ["ncu --set full --clock-control none, one launch each (C5 batch ridge: 10^7 points,",
+             "99,856 lattice centres, band ld 3424) of python tools/time_batch_c5.py", ""]
+    for row in raw[2:]:
+        d = dict(zip(hdr, row))
+        name = d.get("Kernel Name", "")[:60]
+        lines.append(name)
+        for k in want:
+            if k in d:
+                lines.append(f"  {k:64s} {d[k]:>14s} {units[hdr.index(k)]}")
+    dst.write_text("\n".join(lines) + "\n")
+
+
+def main(tag, prefix="r1"):
+    rep = OUT / f"batch_fit_{tag}.ncu-rep"
+    if rep.exists():
+        batch_fit_summary(rep, PROF / f"{prefix}_ncu_batch_fit.txt")
+    shutil.copy(OUT / f"bench_{tag}.json", PROF / f"{prefix}_bench.json")
+    shutil.copy(OUT / f"bench_ref_{tag}.json", PROF / f"{prefix}_bench_reference_arm.json")
+    shutil.copy(OUT / f"launches_{tag}.csv", PROF / f"{prefix}_bench_launches.csv")
     summ = subprocess.run([sys.executable, str(ROOT / "tools" / "summarize_launches.py"),
                            str(OUT / f"launches_{tag}.csv"),
                            "python bench.py --steps 2 --warmup 3 --no-cpu"],
                           capture_output=True, text=True, check=True).stdout
-    (PROF / "r1_bench_launches_summary.csv").write_text(summ)
+    (PROF / f"{prefix}_bench_launches_summary.csv").write_text(summ)
     rep = str(OUT / f"bench_manifold_{tag}.ncu-rep")
 
     def ncu(*args):
@@ -50,7 +78,7 @@ def main(tag):
         "registers_per_thread": f("launch__registers_per_thread"),
         "source": "ncu --set full --clock-control none, one k_manifold launch of python bench.py "
                   "--steps 2 --warmup 3 --no-cpu --no-update; details in "
-                  "profiles/r1_ncu_k_manifold_full.txt"}}
+                  f"profiles/{prefix}_ncu_k_manifold_full.txt"}}
     (PROF / "kernel_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
     src = list(csv.reader(ncu("--page", "source", "--csv", "--print-source", "sass").splitlines()))
     hdr = src[1]
@@ -73,9 +101,9 @@ def main(tag):
                      if "smsp__pcsamp_warps_issue_stalled" in h and not h.endswith("not_issued")
                      and v not in ("", "0")), reverse=True)[:8]
     lines += ["Warp stall samples (top):"] + [f"  {v:10.0f} {h}" for v, h in stalls]
-    (PROF / "r1_ncu_k_manifold_full.txt").write_text(details + "\n".join(lines) + "\n")
+    (PROF / f"{prefix}_ncu_k_manifold_full.txt").write_text(details + "\n".join(lines) + "\n")
     print(json.dumps(traffic, indent=1))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], *(sys.argv[2:3]))
