@@ -12,6 +12,7 @@
 #include <cmath>
 #include <fstream>
 #include <cstdint>
+#include <array>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -411,6 +412,7 @@ class TerrainModel {
   tlg_model* handle() const { return m_.get(); }
   // the host mirrors are stale after changes made through handle()
   void invalidate() { ++ver_; }
+  tlg_model* get() const { return m_.get(); }
 
  private:
   struct Del {
@@ -450,6 +452,41 @@ void fit_batch_ridge_sharded(TerrainModel& model, const TerrainObservation& shar
   allreduce_sum(H, s.elems);
   allreduce_sum(b, s.n);
   model.batch_solve(H, b);
+}
+
+// The library's own communicator (tlg_comm, one process per GPU): rank 0
+// makes the id (unique_id()), the job broadcasts it, every rank constructs.
+class Communicator {
+ public:
+  using Id = std::array<unsigned char, TLG_COMM_ID_BYTES>;
+  static Id unique_id() {
+    Id id{};
+    gpu::check(tlg_comm_unique_id(id.data()));
+    return id;
+  }
+  Communicator(const Id& id, int rank, int size) {
+    tlg_comm* c = nullptr;
+    gpu::check(tlg_comm_init(gpu::Context::instance().get(), id.data(), rank, size, &c));
+    c_.reset(c);
+  }
+  tlg_comm* get() const { return c_.get(); }
+
+ private:
+  struct Del {
+    void operator()(tlg_comm* c) const { tlg_comm_destroy(c); }
+  };
+  std::unique_ptr<tlg_comm, Del> c_;
+};
+
+// fit_batch_ridge over point shards through the library communicator: the
+// packed structural nonzeros of the partial systems and the rhs are reduced
+// (NCCL), every rank solves and ends with the same model.
+inline void fit_batch_ridge_sharded(TerrainModel& model, const Communicator& comm,
+                                    const TerrainObservation& shard) {
+  const detail::Soa o = detail::split(shard.xy);
+  gpu::check(tlg_fit_batch_ridge_sharded(model.get(), comm.get(), o.x.data(), o.y.data(),
+                                         shard.z.data(), shard.xy.size(), TLG_HOST));
+  model.invalidate();
 }
 
 }  // namespace terrain

@@ -331,6 +331,25 @@ tlg_status tlg_batch_ridge_pattern(tlg_model* model, size_t* nnz);
 tlg_status tlg_batch_ridge_pack(tlg_model* model, const double* H, double* packed);
 tlg_status tlg_batch_ridge_unpack(tlg_model* model, const double* packed, double* H);
 
+/* Communicator for the sharded variants (SURVEY §8b tlg_comm_init): an NCCL
+ * communicator over the ranks of one job (one process per GPU), created from
+ * a TLG_COMM_ID_BYTES unique id that rank 0 makes (tlg_comm_unique_id) and
+ * broadcasts out of band. NCCL is loaded at tlg_comm_unique_id / init time
+ * (libnccl.so.2; TLG_RUNTIME_ERROR when absent). */
+#define TLG_COMM_ID_BYTES 128
+typedef struct tlg_comm tlg_comm;
+tlg_status tlg_comm_unique_id(void* id);
+tlg_status tlg_comm_init(tlg_ctx* ctx, const void* id, int rank, int size, tlg_comm** out);
+tlg_status tlg_comm_destroy(tlg_comm* comm);
+/* In-place SUM of the 29-double normal-equation block over the ranks: the one
+ * exchange of a point-sharded LM cost evaluation (scan_matcher.cpp:296-299). */
+tlg_status tlg_comm_allreduce_normal_eq(tlg_comm* comm, tlg_normal_eq* ne);
+/* fit_batch_ridge over point shards in one call: assemble this rank's shard
+ * (lambda I on rank 0), all-reduce the packed structural nonzeros and the
+ * rhs, solve on every rank (every rank ends with the same model). */
+tlg_status tlg_fit_batch_ridge_sharded(tlg_model* model, tlg_comm* comm, const double* x,
+                                       const double* y, const double* z, size_t m, tlg_mem mem);
+
 /* RBFT v1 snapshot (snapshot.cpp:7-126), byte-identical layout. */
 tlg_status tlg_model_save(tlg_model* model, const char* path);
 tlg_status tlg_model_load(tlg_ctx* ctx, const char* path, tlg_model** out);

@@ -118,6 +118,11 @@ _SIGS = {
     "tlg_batch_ridge_pattern": (_ST, [_P, C.POINTER(_SZ)]),
     "tlg_batch_ridge_pack": (_ST, [_P, _P, _P]),
     "tlg_batch_ridge_unpack": (_ST, [_P, _P, _P]),
+    "tlg_comm_unique_id": (_ST, [_P]),
+    "tlg_comm_init": (_ST, [_P, _P, _I, _I, C.POINTER(_P)]),
+    "tlg_comm_destroy": (_ST, [_P]),
+    "tlg_comm_allreduce_normal_eq": (_ST, [_P, _P]),
+    "tlg_fit_batch_ridge_sharded": (_ST, [_P, _P, _P, _P, _P, _SZ, _I]),
     "tlg_feature_rows": (_ST, [_P, _P, _P, _P, _P, _SZ, _P, _P, _P, _P, _SZ, C.POINTER(_SZ)]),
     "tlg_select_ground_points": (_ST, [_P, _P, _P, _P, _P, _SZ, _I, _P, _P, _P, _P, C.c_double,
                                        C.c_double, _SZ, _P, _P, _P, _I, C.POINTER(_SZ)]),

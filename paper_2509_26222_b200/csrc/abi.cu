@@ -1,9 +1,12 @@
 // extern "C" entry points of include/terralio_gpu.h. Each one converts
 // internal exceptions into the status enum + a thread-local message.
 #include <cub/cub.cuh>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <fstream>
 
 #include "internal.cuh"
@@ -1090,3 +1093,150 @@ tlg_status tlg_model_load(tlg_ctx* ctx, const char* path, tlg_model** out) {
 }
 
 }  // extern "C"
+
+// ---- Communicator (SURVEY §8b tlg_comm_init) -------------------------------
+// NCCL is resolved at tlg_comm_init with dlopen("libnccl.so.2"), preferring a
+// copy the process already loaded (torch's), so the library itself never
+// links NCCL and single-GPU users never need it.
+namespace {
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) init_rank = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+};
+
+const NcclApi& nccl_api() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.init_rank = reinterpret_cast<decltype(a.init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    a.destroy = reinterpret_cast<decltype(a.destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    return a;
+  }();
+  require(api.get_unique_id && api.init_rank && api.all_reduce && api.destroy,
+          TLG_RUNTIME_ERROR, "NCCL (libnccl.so.2) is not available");
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) {
+    const char* e = nccl_api().error_string ? nccl_api().error_string(r) : "?";
+    throw Error(TLG_RUNTIME_ERROR, std::string(what) + ": " + e);
+  }
+}
+}  // namespace
+
+struct tlg_comm {
+  tlg_ctx* ctx = nullptr;
+  ncclComm_t comm = nullptr;
+  int rank = 0, size = 1;
+};
+
+extern "C" {
+
+tlg_status tlg_comm_unique_id(void* id) {
+  return guard([&] {
+    check_ptr(id, "id");
+    static_assert(sizeof(ncclUniqueId) == TLG_COMM_ID_BYTES, "NCCL unique id size");
+    ncclUniqueId u;
+    nccl_check(nccl_api().get_unique_id(&u), "ncclGetUniqueId");
+    std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+tlg_status tlg_comm_init(tlg_ctx* ctx, const void* id, int rank, int size, tlg_comm** out) {
+  return guard([&] {
+    check_ptr(ctx, "ctx");
+    check_ptr(id, "id");
+    check_ptr(out, "out");
+    require(size >= 1 && rank >= 0 && rank < size, TLG_INVALID_ARGUMENT, "bad rank / size");
+    TLG_CUDA(cudaSetDevice(ctx->device));
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    auto* c = new tlg_comm();
+    c->ctx = ctx;
+    c->rank = rank;
+    c->size = size;
+    const ncclResult_t r = nccl_api().init_rank(&c->comm, size, u, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      nccl_check(r, "ncclCommInitRank");
+    }
+    *out = c;
+  });
+}
+
+tlg_status tlg_comm_destroy(tlg_comm* c) {
+  return guard([&] {
+    if (!c) return;
+    if (c->comm) nccl_api().destroy(c->comm);
+    delete c;
+  });
+}
+
+tlg_status tlg_comm_allreduce_normal_eq(tlg_comm* c, tlg_normal_eq* ne) {
+  return guard([&] {
+    check_ptr(c, "comm");
+    check_ptr(ne, "ne");
+    if (c->size == 1) return;
+    tlg_ctx* ctx = c->ctx;
+    static_assert(sizeof(tlg_normal_eq) == 29 * sizeof(double), "29-double block");
+    double* d = ctx->ws<double>(S_PARTIALS, 29);
+    double* h = static_cast<double*>(ctx->host_stage(29 * sizeof(double)));
+    std::memcpy(h, ne, sizeof(*ne));
+    TLG_CUDA(cudaMemcpyAsync(d, h, sizeof(*ne), cudaMemcpyHostToDevice, ctx->stream));
+    nccl_check(nccl_api().all_reduce(d, d, 29, ncclFloat64, ncclSum, c->comm, ctx->stream),
+               "ncclAllReduce");
+    TLG_CUDA(cudaMemcpyAsync(h, d, sizeof(*ne), cudaMemcpyDeviceToHost, ctx->stream));
+    TLG_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(ne, h, sizeof(*ne));
+  });
+}
+
+tlg_status tlg_fit_batch_ridge_sharded(tlg_model* m, tlg_comm* c, const double* x, const double* y,
+                                       const double* z, size_t mm, tlg_mem mem) {
+  return guard([&] {
+    check_ptr(m, "model");
+    check_ptr(c, "comm");
+    require(c->ctx == m->ctx, TLG_INVALID_ARGUMENT, "model and communicator on different contexts");
+    tlg_ctx* ctx = m->ctx;
+    ensure_grid(m);
+    size_t n = 0, ld = 0, elems = 0;
+    batch_system_dims(m, &n, &ld, &elems);
+    if (n == 0) return;
+    const double* dx = nullptr;
+    const double* dy = nullptr;
+    const double* dz = nullptr;
+    if (mm) {
+      dx = as_device(ctx, S_IN_X, x, mm, mem);
+      dy = as_device(ctx, S_IN_Y, y, mm, mem);
+      dz = as_device(ctx, S_IN_Z, z, mm, mem);
+      validate_obs_device(ctx, dx, dy, dz, mm, mm);
+    }
+    double* H = ctx->ws<double>(S_HMAT, elems);
+    double* b = ctx->ws<double>(S_WORK3, n);
+    batch_assemble_device(m, dx, dy, dz, mm, H, ld, b, c->rank == 0);
+    if (c->size > 1) {
+      // the structural nonzeros only (tlg_batch_ridge_pack), then the rhs
+      const size_t nnz = batch_pattern_device(m);
+      double* P = ctx->ws<double>(S_GEMVPART, nnz);
+      batch_pack_device(m, H, P);
+      nccl_check(nccl_api().all_reduce(P, P, nnz, ncclFloat64, ncclSum, c->comm, ctx->stream),
+                 "ncclAllReduce");
+      batch_unpack_device(m, P, H);
+      nccl_check(nccl_api().all_reduce(b, b, n, ncclFloat64, ncclSum, c->comm, ctx->stream),
+                 "ncclAllReduce");
+    }
+    batch_solve_device(m, H, ld, b);
+  });
+}
+
+}  // extern "C"
+

@@ -567,6 +567,65 @@ class TerrainModel(_CtxBound):
                     f.write(f"{px:.6g},{py:.6g},{zz:.6g}\n")
 
 
+COMM_ID_BYTES = 128
+
+
+def comm_unique_id() -> bytes:
+    """tlg_comm_unique_id: rank 0 makes it and shares it out of band."""
+    buf = C.create_string_buffer(COMM_ID_BYTES)
+    check(_abi.load().tlg_comm_unique_id(buf))
+    return buf.raw
+
+
+class Communicator(_CtxBound):
+    """tlg_comm (SURVEY §8b tlg_comm_init): the library's own NCCL
+    communicator for the sharded variants, one process per GPU."""
+
+    def __init__(self, unique_id: bytes, rank: int, size: int, ctx: Context | None = None):
+        self.ctx = ctx or Context.default()
+        if len(unique_id) != COMM_ID_BYTES:
+            raise InvalidArgument("unique id must be 128 bytes")
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(unique_id), COMM_ID_BYTES)
+        check(_abi.load().tlg_comm_init(self.ctx.handle, buf, int(rank), int(size), C.byref(h)))
+        self.handle, self.rank, self.size = h, rank, size
+
+    def allreduce_normal_eq(self, ne):
+        """SUM of a kinematics.NormalEq's 29-double block over the ranks."""
+        from .kinematics import NormalEq
+        c = _abi.NormalEqC()
+        c.A[:] = [float(v) for v in np.asarray(ne.A)[np.triu_indices(6)]]
+        c.g[:] = [float(v) for v in ne.g]
+        c.cost, c.valid = float(ne.cost), float(ne.valid)
+        check(_abi.load().tlg_comm_allreduce_normal_eq(self.handle, C.byref(c)))
+        return NormalEq._from_c(c)
+
+    def fit_batch_ridge_sharded(self, model: "TerrainModel", xy, z) -> None:
+        """tlg_fit_batch_ridge_sharded: this rank's point shard in, the same
+        fitted model on every rank out."""
+        m = 0 if xy is None else len(xy)
+        if m:
+            x, y = _xy_of(xy)
+            zz = _vec(z)
+            mem = _mem(x)
+        else:
+            x = y = zz = None
+            mem = _abi.TLG_HOST
+        check(_abi.load().tlg_fit_batch_ridge_sharded(model.handle, self.handle, _ptr(x), _ptr(y),
+                                                      _ptr(zz), m, mem))
+
+    def close(self) -> None:
+        if self._h is not None:
+            _abi.load().tlg_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def fit_batch_ridge(kernel: KernelParams, centers: CenterSet, obs: TerrainObservation,
                     ctx: Context | None = None) -> TerrainModel:
     """terrain_model.cpp:269-308."""

@@ -123,6 +123,18 @@ int main() {
     cudaFree(b1);
   }
 
+  // the library's own communicator (tlg_comm, one rank here): the sharded fit
+  // of the whole set equals the single call
+  {
+    TerrainModel sh(kk, set);
+    const Communicator comm(Communicator::unique_id(), 0, 1);
+    fit_batch_ridge_sharded(sh, comm, obs);
+    const auto ws = sh.weights();
+    bool same = ws.size() == wb.size();
+    for (std::size_t i = 0; same && i < ws.size(); ++i) same = ws[i] == wb[i];
+    CHECK(same);
+  }
+
   // predict_height / unsupported (test_terrain_model.cpp:79-100)
   const HeightQuery q = batch.predict_height({1.0, 1.0});
   CHECK(q.supported);

@@ -165,3 +165,24 @@ def test_batch_lattice_assembly_matches_csr_gram(gpu_ctx, sigma, sigma_eps, side
     # bit-reproducible run to run
     H2, b2 = _assemble(g, obs, csr=False)
     assert torch.equal(H1, H2) and torch.equal(b1, b2)
+
+
+def test_comm_world1_sharded_fit_and_normal_eq(gpu_ctx):
+    """tlg_comm: a one-rank NCCL communicator from the library's
+    own entry points; the sharded fit equals tlg_fit_batch_ridge bit for bit
+    and the normal-equation reduction is the identity."""
+    from paper_2509_26222_b200 import kinematics as kin
+    k, cs, obs = _field(side=1.2, n_points=2500, seed=48)
+    full = T.fit_batch_ridge(k, cs, obs)
+    comm = T.Communicator(T.comm_unique_id(), 0, 1)
+    g = T.TerrainModel(k, cs)
+    comm.fit_batch_ridge_sharded(g, obs.xy, obs.z)
+    assert np.array_equal(g.weights(), full.weights())
+    for b in range(full.num_blocks()):
+        assert np.array_equal(g.block_info_inverse(b), full.block_info_inverse(b))
+    rng = np.random.default_rng(2)
+    A = rng.normal(size=(6, 6))
+    ne = kin.NormalEq(A @ A.T, rng.normal(size=6), 3.5, 17)
+    out = comm.allreduce_normal_eq(ne)
+    assert np.array_equal(out.A, ne.A) and np.array_equal(out.g, ne.g) and out.valid == 17
+    comm.close()
