@@ -1215,6 +1215,7 @@ constexpr int kPFP = 36;  // smem tile pitch (conflict-free fragments, as gemm32
 
 __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __restrict__ A, int n, int lda, int bwt,
                                                       double* __restrict__ linv, int* __restrict__ info,
+                                                      double* __restrict__ X, int ldx,
                                                       int* __restrict__ flag,
                                                       unsigned long long* __restrict__ counter,
                                                       int epoch) {
@@ -1230,13 +1231,163 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
   const long long T0 = static_cast<long long>(nt - bwt) * (bwt + 1);
   const long long total = T0 + static_cast<long long>(bwt) * (bwt + 1) / 2;
   auto fl = [&](int i, int j) { return flag + static_cast<size_t>(j) * (bwt + 1) + (i - j); };
+  // X = L^-1 tasks (when X != nullptr) follow all factor tasks: tile (i, j),
+  // i >= j, row-major; xfl(i, j) its flag
+  int* xflag = flag + static_cast<size_t>(nt) * (bwt + 1);
+  auto xfl = [&](int i, int j) { return xflag + static_cast<size_t>(j) * nt + i; };
+  const long long total_all = total + (X ? static_cast<long long>(nt) * (nt + 1) / 2 : 0);
   const bool async_ok = (lda % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0);
+  auto spin = [&](const int* f) {
+    while (ld_relaxed(f) != epoch) __nanosleep(64);
+  };
   for (;;) {
     if (t == 0) task_s = static_cast<long long>(atomicAdd(counter, 1ull));
     __syncthreads();
     const long long task = task_s;
     __syncthreads();
-    if (task >= total) break;
+    if (task >= total_all) break;
+    if (task >= total) {
+      // ---- X_ij = -Linv_i sum_{k = max(j, i - bwt)}^{i-1} L_ik X_kj  (X_jj = Linv_j)
+      // row-major over the lower tiles: row i's tiles depend on earlier rows
+      // only, so the rows form a wavefront with every column in flight
+      const long long r = task - total;
+      int i = static_cast<int>((sqrt(8.0 * static_cast<double>(r) + 1.0) - 1.0) * 0.5);
+      while (static_cast<long long>(i) * (i + 1) / 2 > r) --i;
+      while (static_cast<long long>(i + 1) * (i + 2) / 2 <= r) ++i;
+      const int j = static_cast<int>(r - static_cast<long long>(i) * (i + 1) / 2);
+      const int i0 = i * 32, j0 = j * 32, ib = min(32, n - i0), jb = min(32, n - j0);
+      if (i == j) {
+        if (t == 0) {
+          spin(fl(j, j));
+          fence_acquire();
+        }
+        __syncthreads();
+        const double* lj = linv + static_cast<size_t>(j) * 1024;
+        for (int e = t; e < 1024; e += 128) {
+          const int rr = e & 31, c = e >> 5;
+          if (rr < jb && c < jb) X[(j0 + rr) + static_cast<size_t>(j0 + c) * ldx] = c <= rr ? __ldcg(lj + e) : 0.0;
+        }
+      } else {
+        double acc[2][2][2] = {};
+        // operands of step k in registers (element e = t + 128 s: a = e & 31
+        // along the contiguous dimension, b = e >> 5), prefetched one step
+        // ahead; readiness from one relaxed sweep of the remaining flags
+        double xa[8], xb[8];
+        auto xfetch = [&](int k) {
+          const int k0 = k * 32;
+#pragma unroll
+          for (int s2 = 0; s2 < 8; ++s2) {
+            const int e = t + 128 * s2, a = e & 31, b = e >> 5;
+            xa[s2] = (i0 + a < n && k0 + b < n) ? __ldcg(A + (i0 + a) + static_cast<size_t>(k0 + b) * lda) : 0.0;
+            xb[s2] = (k0 + a < n && j0 + b < n) ? __ldcg(X + (k0 + a) + static_cast<size_t>(j0 + b) * ldx) : 0.0;
+          }
+        };
+        auto xstash = [&](int bf) {
+#pragma unroll
+          for (int s2 = 0; s2 < 8; ++s2) {
+            const int e = t + 128 * s2;
+            Xs[bf][e >> 5][e & 31] = xa[s2];  // Xs[q][r] = L(i0 + r, k0 + q)
+            Ys[bf][e >> 5][e & 31] = xb[s2];  // Ys[c][q] = X(k0 + q, j0 + c)
+          }
+        };
+        const int kl = max(j, i - bwt);
+        auto x_first_unready = [&](int from) {
+          if (t == 0) s_first = i;
+          __syncthreads();
+          for (int kk = from + t; kk < i; kk += 128)
+            if (ld_relaxed(fl(i, kk)) != epoch || ld_relaxed(xfl(kk, j)) != epoch) atomicMin(&s_first, kk);
+          fence_acquire();
+          __syncthreads();
+          const int f = s_first;
+          __syncthreads();
+          return f;
+        };
+        int xready = x_first_unready(kl);
+        auto xensure = [&](int k) {
+          if (k < xready) return;
+          if (t == 0) {
+            spin(fl(i, k));
+            spin(xfl(k, j));
+            fence_acquire();
+          }
+          __syncthreads();
+          xready = max(k + 1, x_first_unready(k + 1));
+        };
+        xensure(kl);
+        xfetch(kl);
+        xstash(kl & 1);
+        __syncthreads();
+        for (int k = kl; k < i; ++k) {
+          const bool more = k + 1 < i;
+          if (more) {
+            xensure(k + 1);
+            xfetch(k + 1);
+          }
+          const int bf = k & 1;
+#pragma unroll
+          for (int kk = 0; kk < 32; kk += 4) {
+            double av[2], bv[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) av[q] = Xs[bf][kk + (lane & 3)][wm + q * 8 + (lane >> 2)];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) bv[q] = Ys[bf][wn + q * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+            for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+              for (int b2 = 0; b2 < 2; ++b2) dmma(acc[a2][b2][0], acc[a2][b2][1], av[a2], bv[b2]);
+          }
+          if (more) xstash(bf ^ 1);
+          __syncthreads();
+        }
+        if (t == 0) {
+          spin(fl(i, i));
+          fence_acquire();
+        }
+        // Xs[q][r] = Linv_i(r, q), Ys[q][c] = acc(q, c)
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int rr = wm + a * 8 + (lane >> 2), c = wn + b * 8 + 2 * (lane & 3) + h;
+              Ys[0][rr][c] = acc[a][b][h];
+              acc[a][b][h] = 0.0;
+            }
+        __syncthreads();
+        const double* li = linv + static_cast<size_t>(i) * 1024;
+        for (int e = t; e < 1024; e += 128) {
+          const int rr = e & 31, q = e >> 5;
+          Xs[0][q][rr] = q <= rr ? __ldcg(li + e) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 32; kk += 4) {
+          double av[2], bv[2];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) av[q] = -Xs[0][kk + (lane & 3)][wm + q * 8 + (lane >> 2)];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) bv[q] = Ys[0][kk + (lane & 3)][wn + q * 8 + (lane >> 2)];
+#pragma unroll
+          for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+            for (int b2 = 0; b2 < 2; ++b2) dmma(acc[a2][b2][0], acc[a2][b2][1], av[a2], bv[b2]);
+        }
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int rr = wm + a * 8 + (lane >> 2), c = wn + b * 8 + 2 * (lane & 3) + h;
+              if (rr < ib && c < jb) X[(i0 + rr) + static_cast<size_t>(j0 + c) * ldx] = acc[a][b][h];
+            }
+      }
+      __threadfence();
+      __syncthreads();
+      if (t == 0) st_release(xfl(i, j), epoch);
+      continue;
+    }
     int i, j;
     if (task < T0) {
       j = static_cast<int>(task / (bwt + 1));
@@ -1432,18 +1583,21 @@ void potrf_lower32(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X
   double* linv = ctx->ws<double>(S_LINV, static_cast<size_t>(nt) * NB32 * NB32);
   ctx->linv_owner = nullptr;  // 32-wide inverse tiles: not usable by trsm_left_lower
   ctx->linv32_owner = A;
-  if (!X && !ctx->force_coop_potrf) {
-    // the task dataflow (k_potrf_flow32)
-    const size_t nflag = static_cast<size_t>(nt) * (bwt + 1);
+  if (!ctx->force_coop_potrf) {
+    // the task dataflow (k_potrf_flow32); with X, the L^-1 tiles as further
+    // tasks (the strictly upper tiles of X are zeroed here)
+    const size_t nflag = static_cast<size_t>(nt) * (bwt + 1) + (X ? static_cast<size_t>(nt) * nt : 0);
     int* flags = ctx->ws<int>(S_FLOWFLAG, nflag + 4);
     unsigned long long* counter = reinterpret_cast<unsigned long long*>(flags + nflag + (nflag & 1));
     TLG_CUDA(cudaMemsetAsync(flags, 0, (nflag + 4) * sizeof(int), ctx->stream));
+    if (X) TLG_CUDA(cudaMemset2DAsync(X, sizeof(double) * ldx, 0, sizeof(double) * n, n, ctx->stream));
     int per_sm = 0;
     TLG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_potrf_flow32, 128, 0));
-    const long long tasks = static_cast<long long>(nt - bwt) * (bwt + 1) + static_cast<long long>(bwt) * (bwt + 1) / 2;
+    long long tasks = static_cast<long long>(nt - bwt) * (bwt + 1) + static_cast<long long>(bwt) * (bwt + 1) / 2;
+    if (X) tasks += static_cast<long long>(nt) * (nt + 1) / 2;
     const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(tasks, static_cast<long long>(ctx->num_sms) * std::max(1, std::min(per_sm, TLG_PF_MINB)))));
     int epoch = 1;
-    void* args[] = {&A, &n, &lda, &bwt, &linv, &info, &flags, &counter, &epoch};
+    void* args[] = {&A, &n, &lda, &bwt, &linv, &info, &X, &ldx, &flags, &counter, &epoch};
     TLG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_potrf_flow32), dim3(grid),
                                          dim3(128), args, 0, ctx->stream));
     ++ctx->launches;
