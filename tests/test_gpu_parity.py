@@ -306,3 +306,36 @@ def test_generic_path_random_centres(gpu_ctx):
     hs, gs = scales(o, q, k.sigma)
     assert_values_close(z, zr, hs, what="height")
     assert_values_close(gx, gxr, gs, what="gx")
+
+
+def test_generic_fine_grid_binned_manifold_rows(gpu_ctx):
+    """Non-lattice centres (a jittered mesh) on a scan-binned evaluation:
+    the fine-grid generic sweep (warp-union candidate cells) against the
+    oracle's rows, bit-exact validity and the §8d scales."""
+    rng = np.random.default_rng(61)
+    side = 1.6
+    nodes = np.arange(int(side / 0.07) + 1) * 0.07
+    gx, gy = np.meshgrid(nodes, nodes, indexing="ij")
+    c = np.stack([gx.ravel(), gy.ravel()], 1) + rng.uniform(-0.004, 0.004, (gx.size, 2))
+    k = T.KernelParams()
+    k.finalize()
+    cs = T.CenterSet(c, 0.07, 0.12, 3, T.Rect((0.0, 0.0), (side, side)))
+    g, o = _models(k, cs)
+    assert g.sweep()[0] == 0  # generic
+    w = 0.05 * np.sin(3.0 * c[:, 0]) * np.cos(2.0 * c[:, 1])
+    g.set_weights(w)
+    o.set_weights(w)
+    R = so3_exp([0.01, -0.02, 0.3])
+    t = np.array([0.05, -0.03, 0.02])
+    pts = np.c_[rng.uniform(-0.1, side + 0.1, (40_000, 2)), rng.normal(0, 0.03, 40_000)]
+    h = (pts - t) @ R
+    scan = kin.Scan(g, R, t, h)
+    srows, sne = scan.manifold_rows(R, t, 0.0, 1.0, 0.05)
+    rows, ne = kin.manifold_rows(g, R, t, h, 0.0, 1.0, 0.05)
+    ref, ne_ref = o.manifold_rows(R, t, h, 0.0, 1.0, 0.05)
+    assert np.array_equal(rows["valid"], ref["valid"])
+    sc = manifold_row_scales(o, R, t, h, ref["J"])
+    assert_manifold_rows_close(rows["r"], rows["J"].reshape(6, -1).T, ref["r"], ref["J"], sc, rtol=1e-9)
+    perm = scan.permutation()
+    assert np.array_equal(srows["valid"], ref["valid"][perm])
+    np.testing.assert_allclose(sne.A, ne.A, rtol=1e-10, atol=1e-10 * np.abs(ne.A).max())
