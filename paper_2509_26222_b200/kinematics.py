@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _abi
-from ._abi import NormalEqC, check
+from ._abi import InvalidArgument, NormalEqC, check
 from .terrain import TerrainModel, _empty_like, _is_dev, _mem, _ptr
 
 try:
@@ -69,11 +69,17 @@ def manifold_rows(terrain: TerrainModel, R, t, h, wheel_radius: float = 0.0,
                           ("raw", np.float64, n)):
         if key in want and key not in rows:
             rows[key] = _empty_like(hx, size, dt)
+    # rows go where the caller's buffers live (host lever arms may feed
+    # device rows: the streamed H2D path of tlg_manifold_rows)
+    outs = [v for v in rows.values() if v is not None]
+    out_mem = _mem(outs[0]) if outs else _mem(hx)
+    if any(_mem(v) != out_mem for v in outs):
+        raise InvalidArgument("row buffers must all be host or all be device memory")
     ne = NormalEqC()
     check(_abi.load().tlg_manifold_rows(
         terrain.handle, _ptr(Rm), _ptr(tv), _ptr(hx), _ptr(hy), _ptr(hz), n, _mem(hx),
         float(wheel_radius), float(lambda_M), float(huber_delta), _ptr(rows.get("r")),
-        _ptr(rows.get("J")), _ptr(rows.get("valid")), _ptr(rows.get("raw")), _mem(hx),
+        _ptr(rows.get("J")), _ptr(rows.get("valid")), _ptr(rows.get("raw")), out_mem,
         C.byref(ne)))
     return rows, NormalEq._from_c(ne)
 
