@@ -1191,8 +1191,15 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
   } else {
     // ---- (I) information form -----------------------------------------------
     rep->solver = 2;
-    require(static_cast<size_t>(n) * 8 <= 200 * 1024, TLG_RUNTIME_ERROR,
-            "dense information-form update limited to 25600 active centres");
+    // the banded Gram keeps a (2 band + 1)-wide window per warp in shared
+    // memory; only when that does not fit does the row Gram's n-wide
+    // accumulator (n <= 25,600) take over (gram_band)
+    require((2.0 * band + 1.0) * 8.0 * kGramWarps <= 200.0 * 1024 ||
+                static_cast<size_t>(n) * 8 <= 200 * 1024,
+            TLG_RUNTIME_ERROR,
+            "information-form update: band of the active blocks too wide for the banded Gram");
+    require(static_cast<double>(n) * n * 8.0 * 2.0 <= 64.0 * (1ull << 30), TLG_OUT_OF_MEMORY,
+            "information-form update: the dense H and L^-1 workspaces exceed 64 GiB");
     double* H = ctx->ws<double>(S_HMAT, static_cast<size_t>(n) * n);
     TLG_CUDA(cudaMemsetAsync(H, 0, sizeof(double) * n * n, s));
     // H0 = blockdiag(info_inv_q)^-1: all blocks in one launch when they fit

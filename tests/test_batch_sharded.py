@@ -186,3 +186,34 @@ def test_comm_world1_sharded_fit_and_normal_eq(gpu_ctx):
     out = comm.allreduce_normal_eq(ne)
     assert np.array_equal(out.A, ne.A) and np.array_equal(out.g, ne.g) and out.valid == 17
     comm.close()
+
+
+def test_information_form_beyond_25600_centres(gpu_ctx):
+    """The information-form update on more than 25,600 active centres (the
+    banded Gram's window, not n, bounds it): one update from the prior equals
+    fit_batch_ridge on the same observations (test_terrain_model.cpp's
+    recursive == batch property) to 1e-8."""
+    k = T.KernelParams()
+    k.finalize()
+    side = 169 * 0.07
+    nodes = np.arange(170) * 0.07
+    gx, gy = np.meshgrid(nodes, nodes, indexing="ij")
+    roi = T.Rect((0.0, 0.0), (side, side))
+    cs = T.CenterSet(np.stack([gx.ravel(), gy.ravel()], 1), 0.07, 0.12, 3, roi)
+    rng = np.random.default_rng(52)
+    xy = rng.uniform(0.0, side, (60_000, 2))
+    z = 0.05 * np.sin(2.0 * xy[:, 0]) * np.cos(1.5 * xy[:, 1])
+    obs = T.TerrainObservation(xy, z)
+    g = T.TerrainModel(k, cs)
+    rep = g.recursive_update(obs, False)
+    assert rep.solver == "information" and rep.active_centers > 25_600, rep
+    full = T.fit_batch_ridge(k, cs, obs)
+    assert rel_norm(g.weights(), full.weights()) < 1e-8
+    # the updated blocks are diagonal blocks of H^-1 (the batch fit stores
+    # (H_bb)^-1 instead, so they are not compared): symmetric positive
+    # definite and below the prior lambda^-1 I
+    for b in range(0, g.num_blocks(), max(1, g.num_blocks() // 7)):
+        P = g.block_info_inverse(b)
+        assert np.array_equal(P, P.T)
+        ev = np.linalg.eigvalsh(P)
+        assert ev.min() > 0.0 and ev.max() <= 1.0 / k.lambda_ * (1 + 1e-9)
