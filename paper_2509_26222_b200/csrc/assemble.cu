@@ -41,12 +41,15 @@ template <int WIN>
 struct LatGeo {
   static constexpr int kF = WIN * WIN;                          // node features per cell
   static constexpr int kNT = (kF + 1 + 7) / 8;                  // 8-wide tiles (+ the z column)
-  static constexpr int kNW = (kNT + 1) / 2;                     // warps: tile rows w and kNT-1-w
+  static constexpr int kNW = (kNT + 1) / 2;                     // DMMA warps: tile rows w and kNT-1-w
+  static constexpr int kWarps = kNW > 8 ? kNW : 8;              // CTA warps (all build features)
   static constexpr int kFP = ((kNT * 8 - 4 + 15) / 16) * 16 + 4;  // F pitch = 4 (mod 16): no bank conflicts
   static constexpr int kKO = WIN * (2 * WIN - 1);               // partner offsets per node
-  static constexpr int kBatch = 32;                             // points per F block
-  static constexpr size_t kSmem =
-      sizeof(double) * (kBatch * kFP + 2 * kBatch * WIN) + sizeof(uint32_t) * WIN;
+  static constexpr int kPPW = 32 / WIN;                         // points per warp and batch
+  static constexpr int kBatch = kWarps * kPPW;                  // points per F block
+  static constexpr int kRows = (kBatch + 3) / 4 * 4;            // F rows (whole k-steps)
+  static constexpr size_t kSmem = sizeof(double) * (2 * kRows * kFP + 2 * kWarps * kPPW * WIN) +
+                                  sizeof(uint32_t) * WIN;
 };
 
 // Cell key of each observation, the eval's window base (eval.cu
@@ -207,20 +210,21 @@ __device__ __forceinline__ void lat_flush_any(int w, double (&acc)[LatGeo<WIN>::
 }
 
 template <int WIN>
-__global__ void __launch_bounds__(32 * LatGeo<WIN>::kNW, 2) k_gram_lattice(
+__global__ void __launch_bounds__(32 * LatGeo<WIN>::kWarps, 2) k_gram_lattice(
     LatticeView L, const double* __restrict__ xs, const double* __restrict__ ys,
     const double* __restrict__ zs, const uint32_t* __restrict__ ms, const uint32_t* __restrict__ start,
     int nseg, int seg_len, double r2, double neg_inv_2b2, double scale, double* __restrict__ Hlat,
     double* __restrict__ blat) {
   using G = LatGeo<WIN>;
   constexpr int kB = G::kBatch;
-  constexpr int kThreads = 32 * G::kNW;
   extern __shared__ __align__(16) unsigned char lat_smem[];
-  double* F = reinterpret_cast<double*>(lat_smem);   // [kB][kFP]
-  double* sey = F + kB * G::kFP;    // [kB][WIN] e^{c dy^2}
-  double* sdy2 = sey + kB * WIN;    // [kB][WIN] dy^2, +inf outside the cell window
-  uint32_t* need = reinterpret_cast<uint32_t*>(sdy2 + kB * WIN);  // [WIN] present & not always-outside
-  const int tid = threadIdx.x, w = tid >> 5;
+  double* Fbuf = reinterpret_cast<double*>(lat_smem);      // [2][kRows][kFP]
+  double* sey = Fbuf + 2 * G::kRows * G::kFP;              // [warp][kPPW][WIN] e^{c dy^2}
+  double* sdy2 = sey + G::kWarps * G::kPPW * WIN;          // dy^2, +inf outside the cell window
+  uint32_t* need = reinterpret_cast<uint32_t*>(sdy2 + G::kWarps * G::kPPW * WIN);  // [WIN]
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int pl = lane / WIN, r = lane % WIN;  // this lane's point (in the warp) and window column
+  const bool lane_on = pl < G::kPPW;
   const int ib = blockIdx.x / nseg, seg = blockIdx.x % nseg;
   const int i0 = ib - L.lo;
   if (i0 < 0 || i0 + WIN > L.ni) return;
@@ -230,12 +234,15 @@ __global__ void __launch_bounds__(32 * LatGeo<WIN>::kNW, 2) k_gram_lattice(
   double* Hc = Hlat + colour * nn * G::kKO;
   double* bc = blat + colour * nn;
   const int jb_end = min(nj, (seg + 1) * seg_len);
+  double* wey = sey + (w * G::kPPW + (lane_on ? pl : 0)) * WIN;
+  double* wdy2 = sdy2 + (w * G::kPPW + (lane_on ? pl : 0)) * WIN;
   double acc[G::kNT + 1][2];
   for (int jb = seg * seg_len; jb < jb_end; ++jb) {
     const size_t cell = static_cast<size_t>(ib) * nj + jb;
     const uint32_t p_beg = start[cell], p_end = start[cell + 1];
     if (p_beg == p_end) continue;
     const int j0 = jb - L.lo;
+    __syncthreads();  // the previous cell's last products read F / need
     if (tid < WIN) {  // window column tid: nodes present, pair class not always-outside
       uint32_t bits = 0;
       const int* pc = L.P + (i0 + tid) * static_cast<size_t>(nj) + j0;
@@ -244,62 +251,77 @@ __global__ void __launch_bounds__(32 * LatGeo<WIN>::kNW, 2) k_gram_lattice(
     }
 #pragma unroll
     for (int t = 0; t <= G::kNT; ++t) acc[t][0] = acc[t][1] = 0.0;
-    for (uint32_t pb = p_beg; pb < p_end; pb += kB) {
-      const int cnt = static_cast<int>(min(static_cast<uint32_t>(kB), p_end - pb));
-      __syncthreads();  // the previous block's F is consumed; need is written
-      // y factors of every (point, window row): the exact node offsets of
-      // eval.cu's exact path
-      for (int it = tid; it < kB * WIN; it += kThreads) {
-        const int p = it / WIN, r = it % WIN;
-        double e = 0.0, d2 = CUDART_INF;
-        if (p < cnt) {
-          const double py = ys[pb + p];
-          const double d = __dsub_rn(__dadd_rn(L.min_y, __dmul_rn(static_cast<double>(j0 + r + L.j_org), L.res)), py);
-          const double dd = __dmul_rn(d, d);
-          if ((ms[pb + p] >> (16 + r)) & 1u) d2 = dd;
-          e = exp(dd * neg_inv_2b2);
+    __syncthreads();
+    const int nb = static_cast<int>((p_end - p_beg + kB - 1) / kB);
+    // software pipeline: step b builds F block b (every warp, its own points:
+    // the y factors, a __syncwarp, the row segments) while the DMMA warps
+    // multiply F block b - 1; one barrier per block
+    for (int b = 0; b <= nb; ++b) {
+      if (b < nb) {
+        const uint32_t pb = p_beg + static_cast<uint32_t>(b) * kB;
+        const int cnt = static_cast<int>(min(static_cast<uint32_t>(kB), p_end - pb));
+        double* F = Fbuf + (b & 1) * G::kRows * G::kFP;
+        const int p = w * G::kPPW + pl;  // batch point of this lane
+        const bool live = lane_on && p < cnt;
+        double px = 0.0, py = 0.0;
+        uint32_t msk = 0;
+        if (live) {
+          px = xs[pb + p];
+          py = ys[pb + p];
+          msk = ms[pb + p];
         }
-        sey[p * WIN + r] = e;
-        sdy2[p * WIN + r] = d2;
-      }
-      __syncthreads();
-      // F row segment of (point p, window column r): its x factor, then the
-      // WIN pairs — always-inside pairs unconditionally, boundary pairs with
-      // the reference's no-FMA d^2 <= r^2 test (the cell window folded into
-      // dx^2 / dy^2 = +inf), always-outside and absent nodes zero
-      for (int it = tid; it < kB * WIN; it += kThreads) {
-        const int p = it / WIN, r = it % WIN;
-        double* row = F + p * G::kFP + r * WIN;
-        if (p < cnt) {
-          const double px = xs[pb + p];
-          const double d = __dsub_rn(__dadd_rn(L.min_x, __dmul_rn(static_cast<double>(i0 + r + L.i_org), L.res)), px);
-          const double dd = __dmul_rn(d, d);
-          const double dx2 = ((ms[pb + p] >> r) & 1u) ? dd : CUDART_INF;
-          const double ex = scale * exp(dd * neg_inv_2b2);
-          const uint32_t nd = need[r], inm = L.inmask[r];
-          const double* ey = sey + p * WIN;
-          const double* ey2 = sdy2 + p * WIN;
-#pragma unroll
-          for (int l = 0; l < WIN; ++l) {
-            double v = 0.0;
-            if ((nd >> l) & 1u)
-              if (((inm >> l) & 1u) || __dadd_rn(dx2, ey2[l]) <= r2) v = ex * ey[l];
-            row[l] = v;
+        if (lane_on) {  // y factor of window row r for this point
+          double e = 0.0, d2 = CUDART_INF;
+          if (live) {
+            const double d = __dsub_rn(__dadd_rn(L.min_y, __dmul_rn(static_cast<double>(j0 + r + L.j_org), L.res)), py);
+            const double dd = __dmul_rn(d, d);
+            if ((msk >> (16 + r)) & 1u) d2 = dd;
+            e = exp(dd * neg_inv_2b2);
           }
-          if (r == 0) row[G::kF] = zs[pb + p];
-        } else {
-#pragma unroll
-          for (int l = 0; l < WIN; ++l) row[l] = 0.0;
-          if (r == 0) row[G::kF] = 0.0;
+          wey[r] = e;
+          wdy2[r] = d2;
         }
-        if (G::kF + 1 + r < G::kNT * 8) F[p * G::kFP + G::kF + 1 + r] = 0.0;
+        __syncwarp();
+        if (lane_on && p < kB) {
+          // F row segment (point p, window column r): always-inside pairs
+          // unconditionally, boundary pairs with the reference's no-FMA
+          // d^2 <= r^2 test (cell window folded into +inf), others zero
+          double* row = F + p * G::kFP + r * WIN;
+          if (live) {
+            const double d = __dsub_rn(__dadd_rn(L.min_x, __dmul_rn(static_cast<double>(i0 + r + L.i_org), L.res)), px);
+            const double dd = __dmul_rn(d, d);
+            const double dx2 = ((msk >> r) & 1u) ? dd : CUDART_INF;
+            const double ex = scale * exp(dd * neg_inv_2b2);
+            const uint32_t nd = need[r], inm = L.inmask[r];
+#pragma unroll
+            for (int l = 0; l < WIN; ++l) {
+              double v = 0.0;
+              if ((nd >> l) & 1u)
+                if (((inm >> l) & 1u) || __dadd_rn(dx2, wdy2[l]) <= r2) v = ex * wey[l];
+              row[l] = v;
+            }
+            if (r == 0) row[G::kF] = zs[pb + p];
+          } else {
+#pragma unroll
+            for (int l = 0; l < WIN; ++l) row[l] = 0.0;
+            if (r == 0) row[G::kF] = 0.0;
+          }
+          if (G::kF + 1 + r < G::kNT * 8) F[p * G::kFP + G::kF + 1 + r] = 0.0;
+        }
+        // rows beyond the batch (k-step padding) stay zero
+        for (int q = kB * G::kFP + tid; q < G::kRows * G::kFP; q += 32 * G::kWarps) F[q] = 0.0;
+        __syncwarp();
+      }
+      if (b > 0 && w < G::kNW) {
+        const uint32_t pb = p_beg + static_cast<uint32_t>(b - 1) * kB;
+        const int cnt = static_cast<int>(min(static_cast<uint32_t>(kB), p_end - pb));
+        lat_mma_any<WIN>(w, Fbuf + ((b - 1) & 1) * G::kRows * G::kFP, (cnt + 3) >> 2, acc);
       }
       __syncthreads();
-      lat_mma_any<WIN>(w, F, (cnt + 3) >> 2, acc);
     }
     // the previous cell's adds to shared partners were ordered by the
     // barriers above (another thread may own the same entry this time)
-    lat_flush_any<WIN>(w, acc, i0, j0, nj, Hc, bc);
+    if (w < G::kNW) lat_flush_any<WIN>(w, acc, i0, j0, nj, Hc, bc);
   }
 }
 
@@ -355,7 +377,7 @@ void launch_gram_lattice(tlg_ctx* ctx, const LatticeView& L, const double* xs, c
   using G = LatGeo<WIN>;
   TLG_CUDA(cudaFuncSetAttribute(k_gram_lattice<WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(G::kSmem)));
-  k_gram_lattice<WIN><<<static_cast<unsigned>(L.ni) * nseg, 32 * G::kNW, G::kSmem, ctx->stream>>>(
+  k_gram_lattice<WIN><<<static_cast<unsigned>(L.ni) * nseg, 32 * G::kWarps, G::kSmem, ctx->stream>>>(
       L, xs, ys, zs, ms, start, nseg, seg_len, kc.r2, kc.neg_inv_2st2, kc.scale, Hlat, blat);
 }
 
