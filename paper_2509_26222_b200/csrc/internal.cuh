@@ -362,6 +362,7 @@ struct tlg_model {
   bool exact_cutoff = false;  // force the per-pair cutoff test (tlg_model_set_exact_cutoff)
   bool batch_csr_gram = false;  // diagnostics: batch Gram by CSR rows even on a lattice
   int last_gram_lattice = 0;    // diagnostics: the last Gram assembly took the lattice path
+  bool batch_block_order = false;  // diagnostics: batch-fit rows in block order even on a lattice
   // structural nonzeros of the banded batch system (positions in band
   // storage of centre pairs within 2 cutoffs): packs the partial systems of
   // the point-sharded fit for the cross-rank reduction; keyed by the centre

@@ -1310,17 +1310,114 @@ __global__ void k_scatter_w(const uint32_t* __restrict__ merged, int n, const do
 // point-sharded multi-GPU form: ranks assemble partial systems
 // over their point shards, the caller sums them (NCCL all-reduce), every
 // rank solves.
+// tmp_q (n_q x n_q, ld n_q) <- H_bb at the block's merged rows pos[off..]:
+// (max, min) of the two rows in lower band storage, zero beyond the band.
+__global__ void k_gather_blocks(const double* __restrict__ H, int ld, int band,
+                                const uint32_t* __restrict__ pos, const int* __restrict__ tab,
+                                double* __restrict__ tmp) {
+  const int q = blockIdx.x;
+  const int off = tab[3 * q], nq = tab[3 * q + 1], to = tab[3 * q + 2];
+  for (int e = threadIdx.x; e < nq * nq; e += blockDim.x) {
+    const int r = e % nq, c = e / nq;
+    const int a = static_cast<int>(pos[off + r]), b = static_cast<int>(pos[off + c]);
+    const int hi = max(a, b), lo = min(a, b);
+    tmp[to + e] = hi - lo <= band ? H[hi + static_cast<size_t>(lo) * ld] : 0.0;
+  }
+}
+
 struct BatchPlan {
   std::vector<uint32_t> merged;
   std::vector<BlockTab> tab;
   int n = 0, band = 0, ld = 0;
+  // node order (lattice models): rows follow the lattice row by row (the
+  // shorter extent fastest), blocks are not contiguous; pos lists each
+  // block's merged rows in member order (tab[q].off indexes pos)
+  bool node_order = false;
+  std::vector<uint32_t> pos;
 };
+
+// Node-ordered rows for a lattice model: the band of H is then the reach of
+// the 2 rho neighbourhood in lattice rows (C5: 2,846 rows instead of 3,424 in
+// the block order, ~30 % fewer factorisation flops). Returns false when the
+// model is not a lattice.
+static bool node_order_plan(tlg_model* m, const std::vector<uint32_t>& blocks, BatchPlan& p) {
+  const LatticeGrid& L = m->lat;
+  if (!L.valid) return false;
+  const size_t nc = m->hcx.size();
+  const double res = m->cparams.mesh_resolution;
+  const double mnx = m->cparams.roi_min_x, mny = m->cparams.roi_min_y;
+  std::vector<int> ni(nc), nj(nc);
+  int i0 = INT_MAX, i1 = INT_MIN, j0 = INT_MAX, j1 = INT_MIN;
+  for (size_t c = 0; c < nc; ++c) {  // node indices exactly as k_lattice_fill
+    ni[c] = static_cast<int>(std::llround((m->hcx[c] - mnx) / res));
+    nj[c] = static_cast<int>(std::llround((m->hcy[c] - mny) / res));
+    i0 = std::min(i0, ni[c]);
+    i1 = std::max(i1, ni[c]);
+    j0 = std::min(j0, nj[c]);
+    j1 = std::max(j1, nj[c]);
+  }
+  const long long ei = static_cast<long long>(i1) - i0 + 1, ej = static_cast<long long>(j1) - j0 + 1;
+  if (ei * ej > (1ll << 28)) return false;
+  const bool j_fast = ej <= ei;
+  const long long nf = j_fast ? ej : ei;
+  std::vector<int> byslot(static_cast<size_t>(ei * ej), -1);
+  for (size_t c = 0; c < nc; ++c) {
+    const long long sl = j_fast ? (ni[c] - i0) * ej + (nj[c] - j0) : (nj[c] - j0) * ei + (ni[c] - i0);
+    if (byslot[sl] >= 0) return false;  // repeated node (not a lattice after all)
+    byslot[sl] = static_cast<int>(c);
+  }
+  std::vector<uint8_t> inblock(nc, 0);
+  for (uint32_t bb : blocks)
+    for (uint32_t c : m->members[bb]) inblock[c] = 1;
+  std::vector<int> row(nc, -1);
+  for (int c : byslot)
+    if (c >= 0 && inblock[c]) {
+      row[c] = static_cast<int>(p.merged.size());
+      p.merged.push_back(static_cast<uint32_t>(c));
+    }
+  p.tab.resize(blocks.size());
+  for (size_t q = 0; q < blocks.size(); ++q) {
+    const uint32_t bb = blocks[q];
+    p.tab[q].pool_off = m->blk_off[bb];
+    p.tab[q].ld = m->blk_ld[bb];
+    p.tab[q].n = static_cast<int>(m->members[bb].size());
+    p.tab[q].off = static_cast<int>(p.pos.size());
+    for (uint32_t c : m->members[bb]) p.pos.push_back(static_cast<uint32_t>(row[c]));
+  }
+  p.n = static_cast<int>(p.merged.size());
+  // entries couple centres within two cutoffs: lattice offsets (di, dj) with
+  // (di^2 + dj^2) res^2 <= (2 rho)^2 (with margin); the merged distance of two
+  // present nodes is at most their slot distance di nf + dj
+  const double reach = 2.0 * m->kernel.cutoff_radius * (1.0 + 1e-9) / res;
+  const int R = static_cast<int>(std::ceil(reach)) + 1;
+  long long band = 0;
+  for (int di = 0; di <= R; ++di)
+    for (int dj = -R; dj <= R; ++dj)
+      if (static_cast<double>(di) * di + static_cast<double>(dj) * dj <= reach * reach + 1e-9 &&
+          (di > 0 || dj > 0))
+        band = std::max(band, di * nf + dj);
+  p.band = static_cast<int>(std::min<long long>(band, p.n));
+  p.node_order = true;
+  return true;
+}
 
 static BatchPlan batch_plan(tlg_model* m) {
   BatchPlan p;
   std::vector<uint32_t> blocks;
   for (uint32_t bb = 0; bb < m->members.size(); ++bb)
     if (!m->members[bb].empty()) blocks.push_back(bb);
+  if (!m->batch_block_order && node_order_plan(m, blocks, p)) {
+    constexpr int kTile = 32;
+    const long long bwt = (static_cast<long long>(p.band) + kTile - 1) / kTile;
+    const long long ldb = (bwt + 2) * kTile;
+    if (ldb < p.n) {
+      p.ld = static_cast<int>(ldb);
+    } else {
+      p.ld = p.n;
+      p.band = p.n;
+    }
+    return p;
+  }
   const auto btile = spatial_block_order(m, blocks);
   p.tab.resize(blocks.size());
   for (size_t q = 0; q < blocks.size(); ++q) {
@@ -1402,7 +1499,42 @@ static void batch_solve(tlg_model* m, const BatchPlan& p, double* H, int ld, dou
   TLG_CUDA(cudaMemsetAsync(info, 0, 4 * sizeof(int), s));
   int maxq = 0;
   for (const auto& tq : p.tab) maxq = std::max(maxq, tq.n);
-  if (maxq <= kBatchInvMax) {
+  if (p.node_order) {
+    // blocks are scattered over the node-ordered rows: gather each H_bb
+    // (entries beyond the band are structurally zero) into a dense n_q^2
+    // buffer, then invert them batched
+    std::vector<size_t> toff(p.tab.size() + 1, 0);
+    for (size_t q = 0; q < p.tab.size(); ++q)
+      toff[q + 1] = toff[q] + static_cast<size_t>(p.tab[q].n) * p.tab[q].n;
+    const size_t npos = p.pos.size();
+    uint32_t* hp = static_cast<uint32_t*>(ctx->host_stage(npos * 4 + (p.tab.size() + 1) * 16));
+    std::memcpy(hp, p.pos.data(), npos * 4);
+    int* htab = reinterpret_cast<int*>(hp + npos);
+    for (size_t q = 0; q < p.tab.size(); ++q) {
+      htab[3 * q] = p.tab[q].off;
+      htab[3 * q + 1] = p.tab[q].n;
+      htab[3 * q + 2] = static_cast<int>(toff[q]);
+    }
+    uint32_t* dpos = ctx->ws<uint32_t>(S_TKEYS, npos + 3 * p.tab.size() + 4);
+    int* dtab = reinterpret_cast<int*>(dpos + npos);
+    TLG_CUDA(cudaMemcpyAsync(dpos, hp, npos * 4 + 3 * p.tab.size() * 4, cudaMemcpyHostToDevice, s));
+    double* tmp = ctx->ws<double>(S_SOLVE, toff.back());
+    k_gather_blocks<<<static_cast<unsigned>(p.tab.size()), 256, 0, s>>>(H, ld, p.band, dpos, dtab,
+                                                                        tmp);
+    TLG_LAUNCHED(ctx);
+    if (maxq <= kBatchInvMax) {
+      std::vector<InvJob> jobs(p.tab.size());
+      for (size_t q = 0; q < p.tab.size(); ++q)
+        jobs[q] = InvJob{tmp + toff[q], m->pool.p + p.tab[q].pool_off, p.tab[q].n, p.tab[q].ld,
+                         p.tab[q].n, 0};
+      batched_spd_inverse(ctx, jobs, info + 1);
+    } else {
+      for (size_t q = 0; q < p.tab.size(); ++q)
+        if (!spd_inverse(ctx, tmp + toff[q], p.tab[q].n, p.tab[q].n, m->pool.p + p.tab[q].pool_off,
+                         p.tab[q].ld))
+          throw Error(TLG_RUNTIME_ERROR, "ridge solve failed (block factorisation)");
+    }
+  } else if (maxq <= kBatchInvMax) {
     std::vector<InvJob> jobs(p.tab.size());
     for (size_t q = 0; q < p.tab.size(); ++q)
       jobs[q] = InvJob{H + p.tab[q].off + static_cast<size_t>(p.tab[q].off) * ld,
