@@ -888,7 +888,8 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // lane 0 waits for block `blk`, then the warp reads what it published
 __device__ __forceinline__ void wait_block(const int* flag, int blk, int epoch) {
   if ((threadIdx.x & 31) == 0) {
-    while (ld_relaxed(flag + blk) != epoch) __nanosleep(64);
+    while (ld_relaxed(flag + blk) != epoch) {
+    }
     fence_acquire();
   }
   __syncwarp();
@@ -957,6 +958,9 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_fwd_flow(const double* __
     const int t0 = i * kFlowSub, t1 = min(nt, t0 + kFlowSub);
     const int ti = t0 + s, r = ti * 32 + lane;
     const bool row_ok = ti < t1 && r < n;
+    // this block's right-hand side, loaded now (off the critical path)
+    const int rb = t0 * 32 + threadIdx.x;
+    const double bv = (threadIdx.x < kFlowRB && rb < n) ? b[rb] : 0.0;
     flow_stage(L, n, ld, bwt, linv, t0, t1, sLi, sT);
     // blocks <= i-2 (published earlier): tiles of the row's band, oldest first
     const int tlo = max(0, ti - bwt), tcrit = max(0, t0 - kFlowSub);
@@ -1006,7 +1010,7 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_fwd_flow(const double* __
     __syncthreads();
     if (threadIdx.x < kFlowRB) {
       const int q = threadIdx.x >> 5, rr = t0 * 32 + threadIdx.x;
-      bb[threadIdx.x] = rr < n ? b[rr] - (part[(2 * q) * 32 + lane] + part[(2 * q + 1) * 32 + lane]) : 0.0;
+      bb[threadIdx.x] = rr < n ? bv - (part[(2 * q) * 32 + lane] + part[(2 * q + 1) * 32 + lane]) : 0.0;
     }
     __syncthreads();
     // the block's own tiles, in order (all operands in shared memory)
@@ -1056,6 +1060,8 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_bwd_flow(const double* __
     const int i = nb - 1 - q;
     const int t0 = i * kFlowSub, t1 = min(nt, t0 + kFlowSub);
     const int ti = t0 + s;  // column tile of this warp's sub-tile
+    const int rb = t0 * 32 + threadIdx.x;  // this block's y, loaded off the critical path
+    const double yv = (threadIdx.x < kFlowRB && rb < n) ? y[rb] : 0.0;
     flow_stage(L, n, ld, bwt, linv, t0, t1, sLi, sT);
     // v[c] accumulates sum_r L(tj r, ti c) x(tj r) over this warp's tiles
     // (lane = r); one transpose-sum at the end
@@ -1099,7 +1105,7 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_bwd_flow(const double* __
     __syncthreads();
     if (threadIdx.x < kFlowRB) {
       const int qq = threadIdx.x >> 5, rr = t0 * 32 + threadIdx.x;
-      bb[threadIdx.x] = rr < n ? y[rr] - (part[(2 * qq) * 32 + lane] + part[(2 * qq + 1) * 32 + lane]) : 0.0;
+      bb[threadIdx.x] = rr < n ? yv - (part[(2 * qq) * 32 + lane] + part[(2 * qq + 1) * 32 + lane]) : 0.0;
     }
     __syncthreads();
     for (int tk = t1 - 1; tk >= t0; --tk) {
