@@ -5,7 +5,7 @@ set -e
 cd "$(dirname "$0")/.."
 mkdir -p build/variants
 OBJS=""
-for s in model grid select dense update prof scan consumers match abi; do OBJS="$OBJS build/obj/$s.cu.o"; done
+for s in model grid select dense update assemble prof scan consumers match abi; do OBJS="$OBJS build/obj/$s.cu.o"; done
 while [ $# -ge 2 ]; do
   name=$1; flags=$2; shift 2
   nvcc -O3 -std=c++17 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC,-ffp-contract=off \
