@@ -1523,6 +1523,12 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
       __syncthreads();
     }
     if (i == j) {
+      // the diagonal step is the per-column critical path: the tile stays in
+      // shared memory (Ys[0]) for the one-warp factor + inverse, warp 0
+      // publishes Linv_j as soon as it is written (the consumers — the
+      // column's solves and the L^-1 tasks — read only Linv_j), and L_jj
+      // goes back to the band afterwards
+      double* T = &Ys[0][0][0];
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -1530,10 +1536,22 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int r = wm + a * 8 + (lane >> 2), c = wn + b * 8 + 2 * (lane & 3) + h;
-            if (r < ib && c < jb && c <= r) A[(i0 + r) + static_cast<size_t>(j0 + c) * lda] = acc[a][b][h];
+            if (c <= r) T[r + c * kPFP] = acc[a][b][h];
           }
       __syncthreads();
-      if (w == 0) warp_potrf_inv32(A + j0 + static_cast<size_t>(j0) * lda, lda, jb, linv + static_cast<size_t>(j) * 1024, info, wsh);
+      if (w == 0) {
+        warp_potrf_inv32(T, kPFP, jb, linv + static_cast<size_t>(j) * 1024, info, wsh);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release(fl(j, j), epoch);
+      }
+      __syncthreads();
+      for (int e = t; e < 1024; e += 128) {
+        const int r = e & 31, c = e >> 5;
+        if (r < jb && c < jb && c <= r) A[(j0 + r) + static_cast<size_t>(j0 + c) * lda] = T[r + c * kPFP];
+      }
+      __syncthreads();  // T is reused by the next task
+      continue;
     } else {
       if (t == 0) {
         while (ld_relaxed(fl(j, j)) != epoch) __nanosleep(64);
