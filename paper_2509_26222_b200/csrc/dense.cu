@@ -1217,6 +1217,25 @@ __global__ void __launch_bounds__(128) k_trsm_tiles(const double* __restrict__ L
 #ifndef TLG_PF_MINB
 #define TLG_PF_MINB 4
 #endif
+#ifdef TLG_FLOW_TRACE
+// Diagnostics build only (tools/flow_trace.py): globaltimer stamps of the
+// diagonal and first-solve tasks of columns [kTr0, kTr0 + kTrN).
+constexpr int kTr0 = 1000, kTrN = 64;
+__device__ unsigned long long tlg_flow_trace[kTrN][8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+  return v;
+}
+#define TLG_TR(col, slot) \
+  do { if (t == 0 && (col) >= kTr0 && (col) < kTr0 + kTrN) tlg_flow_trace[(col) - kTr0][slot] = gtime(); } while (0)
+__device__ unsigned long long tlg_flow_trace2[kTrN][8];
+#define TLG_TRW(col, slot) \
+  do { if ((col) >= kTr0 && (col) < kTr0 + kTrN) tlg_flow_trace2[(col) - kTr0][slot] = gtime(); } while (0)
+#else
+#define TLG_TR(col, slot)
+#define TLG_TRW(col, slot)
+#endif
 constexpr int kPFP = 36;  // smem tile pitch (conflict-free fragments, as gemm32_tile)
 
 __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __restrict__ A, int n, int lda, int bwt,
@@ -1408,6 +1427,8 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
       i = j + static_cast<int>(r);
     }
     const int i0 = i * 32, j0 = j * 32, ib = min(32, n - i0), jb = min(32, n - j0);
+    if (i == j) TLG_TR(j, 0);
+    if (i == j + 1) TLG_TR(j, 3);
     double acc[2][2][2];
 #pragma unroll
     for (int a = 0; a < 2; ++a)
@@ -1522,6 +1543,8 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
       }
       __syncthreads();
     }
+    if (i == j) TLG_TR(j, 1);
+    if (i == j + 1) TLG_TR(j, 4);
     if (i == j) {
       // the diagonal step is the per-column critical path: the tile stays in
       // shared memory (Ys[0]) for the one-warp factor + inverse, warp 0
@@ -1540,10 +1563,13 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
           }
       __syncthreads();
       if (w == 0) {
+        TLG_TR(j, 7);
         warp_potrf_inv32(T, kPFP, jb, linv + static_cast<size_t>(j) * 1024, info, wsh);
+        if (lane == 0) TLG_TRW(j, 5);
         __threadfence();
         __syncwarp();
         if (lane == 0) st_release(fl(j, j), epoch);
+        TLG_TR(j, 2);
       }
       __syncthreads();
       for (int e = t; e < 1024; e += 128) {
@@ -1557,6 +1583,7 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
         while (ld_relaxed(fl(j, j)) != epoch) __nanosleep(64);
         fence_acquire();
       }
+      if (i == j + 1) TLG_TR(j, 5);
       // L_ij = A_ij Linv_j^T: Xs[q][r] = A_ij(r, q), Ys[q][c] = Linv_j(c, q)
 #pragma unroll
       for (int a = 0; a < 2; ++a)
@@ -1597,8 +1624,16 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
     __threadfence();
     __syncthreads();
     if (t == 0) st_release(fl(i, j), epoch);
+    if (i == j + 1) TLG_TR(j, 6);
   }
 }
+
+#ifdef TLG_FLOW_TRACE
+extern "C" int tlg_debug_flow_trace(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, tlg_flow_trace, sizeof(tlg_flow_trace)) != cudaSuccess) return 1;
+  return cudaMemcpyFromSymbol(out + kTrN * 8, tlg_flow_trace2, sizeof(tlg_flow_trace2)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 void potrf_lower32(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X, int ldx,
                    int band) {
