@@ -645,29 +645,38 @@ __global__ void __launch_bounds__(kManifoldThreads, TLG_MANIFOLD_MINB) k_manifol
   }
 }
 
-// Order-fixed reduction of the per-chunk Gram partials: block `entry` sums
-// all chunks (thread t a contiguous run, then a fixed tree); block 0 also
-// appends the non-finite flag, so one D2H copy returns everything.
+// Order-fixed reduction of the per-chunk Gram partials, two levels in one
+// launch: block (entry, seg) sums a fixed contiguous range of chunks (thread t
+// a strided run, then a fixed tree) into seg_part[entry][seg]; the last of an
+// entry's kRedSeg blocks to finish (an arrival counter) adds the kRedSeg
+// segment sums in order and resets the counter. The result does not depend on
+// the arrival order, so it is reproducible run to run; kNE x kRedSeg blocks
+// spread the ~9 MB of partials (C5) over the SMs instead of kNE of them.
+// Block (0, 0) also appends the non-finite flag, so one D2H copy returns
+// everything.
 constexpr int kRedThreads = 256;
+constexpr int kRedSeg = 8;
 __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const double* __restrict__ partials,
                                                                size_t nchunks,
                                                                const int* __restrict__ err,
-                                                               double* __restrict__ out) {
+                                                               double* __restrict__ out,
+                                                               double* __restrict__ seg_part,
+                                                               unsigned* __restrict__ arrive) {
   __shared__ double sh[kRedThreads];
-  const int entry = blockIdx.x;
+  __shared__ bool last;
+  const int entry = blockIdx.x / kRedSeg, seg = blockIdx.x % kRedSeg;
   const double* p = partials + (size_t)entry * nchunks;
-  // thread t: chunks t, t + 256, ... (coalesced, 8 loads in flight; a fixed
-  // order, so the result is reproducible run to run)
+  const size_t c0 = nchunks * seg / kRedSeg, c1 = nchunks * (seg + 1) / kRedSeg;
   double v = 0.0;
-  size_t c = threadIdx.x;
-  for (; c + 7 * kRedThreads < nchunks; c += 8 * kRedThreads) {
+  size_t c = c0 + threadIdx.x;
+  for (; c + 7 * kRedThreads < c1; c += 8 * kRedThreads) {
     double q[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) q[u] = p[c + u * kRedThreads];
 #pragma unroll
     for (int u = 0; u < 8; ++u) v += q[u];
   }
-  for (; c < nchunks; c += kRedThreads) v += p[c];
+  for (; c < c1; c += kRedThreads) v += p[c];
   sh[threadIdx.x] = v;
   __syncthreads();
   for (int o = kRedThreads / 2; o > 0; o >>= 1) {
@@ -675,9 +684,19 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const double* __r
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    out[entry] = sh[0];
-    if (entry == 0) out[kNE] = err[0] ? 1.0 : 0.0;
+    seg_part[entry * kRedSeg + seg] = sh[0];
+    __threadfence();
+    last = atomicAdd(arrive + entry, 1u) == kRedSeg - 1;
   }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double s = 0.0;
+    for (int k = 0; k < kRedSeg; ++k) s += __ldcg(seg_part + entry * kRedSeg + k);
+    out[entry] = s;
+    arrive[entry] = 0u;  // ready for the next call
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[kNE] = err[0] ? 1.0 : 0.0;
 }
 
 void manifold_device(tlg_model* m, const double R[9], const double t[3], const double* hx,
@@ -697,10 +716,13 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
   }
   double* partials = ctx->ws<double>(S_PARTIALS, nchunks * kNE + kNE + 1);
   double* out = partials + nchunks * kNE;
-  // err[0]: non-finite flag; err[2..3]: 64-bit chunk counter (8-byte aligned)
-  int* err = ctx->ws<int>(S_FLAGS, 4);
+  double* seg_part = ctx->ws<double>(S_REDSEG, kNE * kRedSeg);
+  // err[0]: non-finite flag; err[2..3]: 64-bit chunk counter (8-byte aligned);
+  // err[4..]: the reduction's arrival counters (one memset clears all)
+  int* err = ctx->ws<int>(S_FLAGS, 4 + kNE);
+  unsigned* arrive = reinterpret_cast<unsigned*>(err + 4);
   double* h = static_cast<double*>(ctx->host_stage((kNE + 1) * sizeof(double)));  // pinned
-  TLG_CUDA(cudaMemsetAsync(err, 0, 4 * sizeof(int), ctx->stream));
+  TLG_CUDA(cudaMemsetAsync(err, 0, (4 + kNE) * sizeof(int), ctx->stream));
   const GridView g = grid_view(m);
   const int kind = prepare_sweep(m);
   const LatticeView L = lattice_view(m);
@@ -713,7 +735,8 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
                         err)));
   TLG_LAUNCHED(ctx);
   prof_mark_end(ctx);
-  k_reduce_chunks<<<kNE, kRedThreads, 0, ctx->stream>>>(partials, nchunks, err, out);
+  k_reduce_chunks<<<kNE * kRedSeg, kRedThreads, 0, ctx->stream>>>(partials, nchunks, err, out,
+                                                                   seg_part, arrive);
   TLG_LAUNCHED(ctx);
   TLG_CUDA(cudaMemcpyAsync(h, out, (kNE + 1) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   TLG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -748,12 +771,14 @@ void manifold_device_streamed(tlg_model* m, const double R[9], const double t[3]
   const size_t nchunks = std::max<size_t>(1, ((n + 31) / 32 + kManifoldChunk - 1) / kManifoldChunk);
   double* partials = ctx->ws<double>(S_PARTIALS, nchunks * kNE + kNE + 1);
   double* out = partials + nchunks * kNE;
-  int* err = ctx->ws<int>(S_FLAGS, 4);
+  double* seg_part = ctx->ws<double>(S_REDSEG, kNE * kRedSeg);
+  int* err = ctx->ws<int>(S_FLAGS, 4 + kNE);
+  unsigned* arrive = reinterpret_cast<unsigned*>(err + 4);
   double* h = static_cast<double*>(ctx->host_stage((kNE + 1) * sizeof(double)));
   double* dx = ctx->ws<double>(S_IN_HX, n);
   double* dy = ctx->ws<double>(S_IN_HY, n);
   double* dz = ctx->ws<double>(S_IN_HZ, n);
-  TLG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
+  TLG_CUDA(cudaMemsetAsync(err, 0, (4 + kNE) * sizeof(int), s));
   const GridView g = grid_view(m);
   const int kind = prepare_sweep(m);
   const LatticeView L = lattice_view(m);
@@ -783,7 +808,8 @@ void manifold_device_streamed(tlg_model* m, const double R[9], const double t[3]
                           nchunks, off / kRowsPerChunk, n, err)));
     TLG_LAUNCHED(ctx);
   }
-  k_reduce_chunks<<<kNE, kRedThreads, 0, s>>>(partials, nchunks, err, out);
+  k_reduce_chunks<<<kNE * kRedSeg, kRedThreads, 0, s>>>(partials, nchunks, err, out, seg_part,
+                                                         arrive);
   TLG_LAUNCHED(ctx);
   TLG_CUDA(cudaMemcpyAsync(h, out, (kNE + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
   TLG_CUDA(cudaStreamSynchronize(s));

@@ -34,13 +34,14 @@ class NormalEq:
 
     @staticmethod
     def _from_c(c: NormalEqC) -> "NormalEq":
-        A = np.zeros((6, 6))
-        k = 0
-        for i in range(6):
-            for j in range(i, 6):
-                A[i, j] = A[j, i] = c.A[k]
-                k += 1
-        return NormalEq(A, np.array(c.g[:]), float(c.cost), int(round(c.valid)))
+        v = np.frombuffer(c, dtype=np.float64)  # A[21] (upper, row-major), g[6], cost, valid
+        A = np.empty((6, 6))
+        A[_IU] = v[:21]
+        A[_IU[1], _IU[0]] = v[:21]
+        return NormalEq(A, v[21:27].copy(), float(v[27]), int(round(v[28])))
+
+
+_IU = np.triu_indices(6)
 
 
 def manifold_rows(terrain: TerrainModel, R, t, h, wheel_radius: float = 0.0,
@@ -103,6 +104,10 @@ class Scan:
         self.n = len(hx)
         self._dev = _is_dev(hx)
         self._ref = hx
+        self._pose = np.zeros(12)  # R (9) then t (3), reused by every evaluation
+        self._pose_p = self._pose.ctypes.data
+        self._ne = NormalEqC()
+        self._ne_ref = C.byref(self._ne)
         hdl = C.c_void_p()
         check(_abi.load().tlg_scan_create(terrain.handle, _ptr(Rm), _ptr(tv), _ptr(hx), _ptr(hy),
                                           _ptr(hz), self.n, _mem(hx), C.byref(hdl)))
@@ -120,22 +125,29 @@ class Scan:
 
     def manifold_rows(self, R, t, wheel_radius=0.0, lambda_M=1.0, huber_delta=0.05,
                       want=("r", "J", "valid"), out: dict | None = None, device_out=None):
-        Rm = np.ascontiguousarray(np.asarray(R, dtype=np.float64).reshape(9))
-        tv = np.ascontiguousarray(np.asarray(t, dtype=np.float64).reshape(3))
+        # called once per LM cost evaluation: a lean path (pose into a
+        # reused buffer, the caller's row buffers as-is)
+        pose = self._pose
+        pose[:9] = np.asarray(R, dtype=np.float64).reshape(9)
+        pose[9:] = np.asarray(t, dtype=np.float64).reshape(3)
         dev = self._dev if device_out is None else device_out
-        ref = self._ref if dev else np.empty(0)
         n = self.n
-        rows = dict(out or {})
-        for key, dt, size in (("r", np.float64, n), ("J", np.float64, 6 * n),
-                              ("valid", np.uint8, n), ("raw", np.float64, n)):
-            if key in want and key not in rows:
-                rows[key] = _empty_like(ref, size, dt)
+        if out is not None and all(k in out for k in want):
+            rows = out
+        else:
+            ref = self._ref if dev else np.empty(0)
+            rows = dict(out or {})
+            for key, dt, size in (("r", np.float64, n), ("J", np.float64, 6 * n),
+                                  ("valid", np.uint8, n), ("raw", np.float64, n)):
+                if key in want and key not in rows:
+                    rows[key] = _empty_like(ref, size, dt)
         mem = _abi.TLG_DEVICE if dev else _abi.TLG_HOST
-        ne = NormalEqC()
+        ne = self._ne
+        get = rows.get
         check(_abi.load().tlg_scan_manifold_rows(
-            self.terrain.handle, self.handle, _ptr(Rm), _ptr(tv), float(wheel_radius),
-            float(lambda_M), float(huber_delta), _ptr(rows.get("r")), _ptr(rows.get("J")),
-            _ptr(rows.get("valid")), _ptr(rows.get("raw")), mem, C.byref(ne)))
+            self.terrain.handle, self.handle, self._pose_p, self._pose_p + 72, float(wheel_radius),
+            float(lambda_M), float(huber_delta), _ptr(get("r")), _ptr(get("J")),
+            _ptr(get("valid")), _ptr(get("raw")), mem, self._ne_ref))
         return rows, NormalEq._from_c(ne)
 
     def __del__(self):
