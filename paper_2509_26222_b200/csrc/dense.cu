@@ -1246,7 +1246,7 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
                                                       int epoch) {
   __shared__ __align__(16) double Xs[2][32][kPFP];  // double-buffered operand tiles
   __shared__ __align__(16) double Ys[2][32][kPFP];
-  static_assert(2 * 32 * kPFP >= kWarpPotrfSmem, "diagonal-factor scratch aliases Xs");
+  static_assert(2 * 32 * kPFP >= kWarp2PotrfSmem, "diagonal-factor scratch aliases Xs");
   double* wsh = &Xs[0][0][0];  // the diagonal factor's scratch (Xs is idle then)
   __shared__ long long task_s;
   __shared__ int s_first;
@@ -1561,15 +1561,19 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
             const int r = wm + a * 8 + (lane >> 2), c = wn + b * 8 + 2 * (lane & 3) + h;
             if (c <= r) T[r + c * kPFP] = acc[a][b][h];
           }
+      if (t == 0) *warp2_potrf_pub(wsh) = 0;
       __syncthreads();
-      if (w == 0) {
+      if (w < 2) {
+        // warp 0 factors, warp 1 forms Linv_j one published column behind it
         TLG_TR(j, 7);
-        warp_potrf_inv32(T, kPFP, jb, linv + static_cast<size_t>(j) * 1024, info, wsh);
-        if (lane == 0) TLG_TRW(j, 5);
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) st_release(fl(j, j), epoch);
-        TLG_TR(j, 2);
+        warp2_potrf_inv32(T, kPFP, jb, linv + static_cast<size_t>(j) * 1024, info, wsh);
+        if (w == 1) {
+          if (lane == 0) TLG_TRW(j, 5);
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) st_release(fl(j, j), epoch);
+          if (lane == 0) TLG_TRW(j, 2);  // flag released (trace2 slot 2)
+        }
       }
       __syncthreads();
       for (int e = t; e < 1024; e += 128) {

@@ -26,7 +26,7 @@ t0 = a[:, 0:1]
 rel = (a - t0) / 1e3
 print("col  diag:upd  potrf:start potrf:end diag:pub | solve:upd solve:seen solve:pub | next diag pub")
 for c in range(0, 63):
-    nxt = (a[c + 1, 2] - a[c, 2]) / 1e3
+    nxt = (b[c + 1, 2] - b[c, 2]) / 1e3  # Linv published (warp 1, trace2 slot 2)
     ps, pe = (a[c, 7] - a[c, 0]) / 1e3, (b[c, 5] - a[c, 0]) / 1e3
-    print(f"{1000 + c:5d} {rel[c, 1]:8.2f} {ps:8.2f} {pe:8.2f} {rel[c, 2]:8.2f} | {rel[c, 4]:9.2f} "
+    print(f"{1000 + c:5d} {rel[c, 1]:8.2f} {ps:8.2f} {pe:8.2f} {(b[c, 2] - a[c, 0]) / 1e3:8.2f} | {rel[c, 4]:9.2f} "
           f"{rel[c, 5]:9.2f} {rel[c, 6]:9.2f} | {nxt:8.2f}")
