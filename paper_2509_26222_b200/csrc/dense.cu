@@ -1566,7 +1566,7 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
       if (w < 2) {
         // warp 0 factors, warp 1 forms Linv_j one published column behind it
         TLG_TR(j, 7);
-        warp2_potrf_inv32(T, kPFP, jb, linv + static_cast<size_t>(j) * 1024, info, wsh);
+        warp2b_potrf_inv32(T, kPFP, jb, linv + static_cast<size_t>(j) * 1024, info, wsh);
         if (w == 1) {
           if (lane == 0) TLG_TRW(j, 5);
           __threadfence();

@@ -31,7 +31,8 @@ __global__ void kk(const double* A, double* Lout, double* linv, int* info, int r
     if (which == 0) {
       if (w == 0) tlg::warp_potrf_inv32(T, P, 32, linv, info, sh);
     } else if (w < 2) {
-      tlg::warp2_potrf_inv32(T, P, 32, linv, info, sh);
+      if (which == 1) tlg::warp2_potrf_inv32(T, P, 32, linv, info, sh);
+      else tlg::warp2b_potrf_inv32(T, P, 32, linv, info, sh);
     }
     if (t == 0) { s_w0 += clock64() - t0; s_piv[32] += clock64(); }
     if (t == 32) s_w1 += clock64() - t0;
@@ -55,15 +56,15 @@ int main() {
   double *A, *L, *X; int* info;
   cudaMalloc(&A, sizeof h); cudaMalloc(&L, sizeof h); cudaMalloc(&X, sizeof h); cudaMalloc(&info, 4);
   cudaMemcpy(A, h, sizeof h, cudaMemcpyHostToDevice);
-  double Lr[2][1024], Xr[2][1024];
-  for (int which = 0; which < 2; ++which) {
+  double Lr[3][1024], Xr[3][1024];
+  for (int which = 0; which < 3; ++which) {
     cudaMemset(info, 0, 4);
     kk<<<1, 128>>>(A, L, X, info, 50, which, 0);
     cudaDeviceSynchronize();
     long long c, c0, c1; cudaMemcpyFromSymbol(&c, g_cyc, sizeof c);
     cudaMemcpyFromSymbol(&c0, g_w0, sizeof c0); cudaMemcpyFromSymbol(&c1, g_w1, sizeof c1);
     printf("  warp 0 done %lld, warp 1 done %lld\n", c0, c1);
-    if (which) {
+    if (which == 2) {
       long long pv[33]; cudaMemcpyFromSymbol(pv, g_piv, sizeof pv);
       printf("  per pivot:");
       for (int q = 0; q < 32; ++q) printf(" %lld", (pv[q + 1] - pv[q]) / 50);
@@ -72,20 +73,22 @@ int main() {
     int inf; cudaMemcpy(&inf, info, 4, cudaMemcpyDeviceToHost);
     cudaMemcpy(Lr[which], L, sizeof h, cudaMemcpyDeviceToHost);
     cudaMemcpy(Xr[which], X, sizeof h, cudaMemcpyDeviceToHost);
-    printf("%s: %lld cycles (info %d, %s)\n", which ? "two-warp" : "one-warp", c, inf,
+    printf("%s: %lld cycles (info %d, %s)\n", which == 2 ? "two-warp blocked" : which ? "two-warp" : "one-warp", c, inf,
            cudaGetErrorString(cudaGetLastError()));
   }
+  for (int v = 1; v < 3; ++v) {
   double dl = 0, dx = 0;
-  for (int c = 0; c < 32; ++c) for (int r = c; r < 32; ++r) dl = fmax(dl, fabs(Lr[0][r + 32 * c] - Lr[1][r + 32 * c]));
-  for (int e = 0; e < 1024; ++e) dx = fmax(dx, fabs(Xr[0][e] - Xr[1][e]));
+  for (int c = 0; c < 32; ++c) for (int r = c; r < 32; ++r) dl = fmax(dl, fabs(Lr[0][r + 32 * c] - Lr[v][r + 32 * c]));
+  for (int e = 0; e < 1024; ++e) dx = fmax(dx, fabs(Xr[0][e] - Xr[v][e]));
   // L L^T = A and X L = I
   double rl = 0, rx = 0;
   for (int r = 0; r < 32; ++r) for (int c = 0; c <= r; ++c) {
     double s = 0, q = 0;
-    for (int k = 0; k <= c; ++k) s += Lr[1][r + 32 * k] * Lr[1][c + 32 * k];
+    for (int k = 0; k <= c; ++k) s += Lr[v][r + 32 * k] * Lr[v][c + 32 * k];
     rl = fmax(rl, fabs(s - h[r + 32 * c]));
-    for (int k = 0; k < 32; ++k) q += Xr[1][r + 32 * k] * (k >= c ? Lr[1][k + 32 * c] : 0.0);
+    for (int k = 0; k < 32; ++k) q += Xr[v][r + 32 * k] * (k >= c ? Lr[v][k + 32 * c] : 0.0);
     rx = fmax(rx, fabs(q - (r == c ? 1.0 : 0.0)));
   }
-  printf("max |L1 - L2| %.3g  max |X1 - X2| %.3g  |LL^T - A| %.3g  |XL - I| %.3g\n", dl, dx, rl, rx);
+  printf("variant %d: max |L - L1| %.3g  max |X - X1| %.3g  |LL^T - A| %.3g  |XL - I| %.3g\n", v, dl, dx, rl, rx);
+  }
 }
