@@ -912,6 +912,36 @@ __device__ __forceinline__ double warp_transpose_sum(double (&v)[32]) {
   return v[0];
 }
 
+#ifdef TLG_FLOW_TRACE
+// Diagnostics build only (tools/band_trace.py): globaltimer stamps of forward
+// band-solve blocks [kBt0, kBt0 + 64)
+constexpr int kBt0 = 300;
+__device__ unsigned long long tlg_band_trace[64][8];
+__device__ __forceinline__ unsigned long long gtime_b() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+  return v;
+}
+#define TLG_BT(blk, slot) \
+  do { if (threadIdx.x == 0 && (blk) >= kBt0 && (blk) < kBt0 + 64) tlg_band_trace[(blk) - kBt0][slot] = gtime_b(); } while (0)
+extern "C" int tlg_debug_band_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, tlg_band_trace, sizeof(tlg_band_trace)) == cudaSuccess ? 0 : 1;
+}
+#else
+#define TLG_BT(blk, slot)
+#endif
+
+// sum_c a[c] b[c] over 32 terms as four interleaved chains (the band
+// solve's per-block steps are latency-bound: a 32-long FMA chain is ~260
+// cycles, four chains of 8 ~70)
+template <class FA, class FB>
+__device__ __forceinline__ double dot32x4(FA a, FB b) {
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int c = 0; c < 32; ++c) s[c & 3] = fma(a(c), b(c), s[c & 3]);
+  return (s[0] + s[1]) + (s[2] + s[3]);
+}
+
 // Stages block [t0, t1)'s diagonal inverses (lower kb x kb part) and its
 // off-diagonal tiles L(tr, tc), t0 <= tc < tr < t1, in the band, as [r][c].
 __device__ __forceinline__ void flow_stage(const double* __restrict__ L, int n, int ld, int bwt,
@@ -961,6 +991,7 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_fwd_flow(const double* __
     // this block's right-hand side, loaded now (off the critical path)
     const int rb = t0 * 32 + threadIdx.x;
     const double bv = (threadIdx.x < kFlowRB && rb < n) ? b[rb] : 0.0;
+    TLG_BT(i, 0);
     flow_stage(L, n, ld, bwt, linv, t0, t1, sLi, sT);
     // blocks <= i-2 (published earlier): tiles of the row's band, oldest first
     const int tlo = max(0, ti - bwt), tcrit = max(0, t0 - kFlowSub);
@@ -974,8 +1005,8 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_fwd_flow(const double* __
         double lv[32];
 #pragma unroll
         for (int c = 0; c < 32; ++c) lv[c] = lr[(size_t)c * ld];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) acc = fma(lv[c], ys[(warp * 2) * 32 + c], acc);
+        const double* yw = ys + (warp * 2) * 32;
+        acc += dot32x4([&](int c) { return lv[c]; }, [&](int c) { return yw[c]; });
       }
       __syncwarp();
     }
@@ -992,7 +1023,9 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_fwd_flow(const double* __
 #pragma unroll
         for (int c = 0; c < 32; ++c) lv[u][c] = tjs[u] >= 0 ? lr[(size_t)c * ld] : 0.0;
       }
+      TLG_BT(i, 1);
       wait_block(flag, i - 1, epoch);
+      TLG_BT(i, 2);
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int tj = tcrit + half + 2 * u;
@@ -1002,8 +1035,8 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_fwd_flow(const double* __
 #pragma unroll
       for (int u = 0; u < 2; ++u)
         if (tjs[u] >= 0) {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) acc = fma(lv[u][c], ys[(warp * 2 + u) * 32 + c], acc);
+          const double* yw = ys + (warp * 2 + u) * 32;
+          acc += dot32x4([&](int c) { return lv[u][c]; }, [&](int c) { return yw[c]; });
         }
     }
     part[warp * 32 + lane] = acc;
@@ -1013,14 +1046,14 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_fwd_flow(const double* __
       bb[threadIdx.x] = rr < n ? bv - (part[(2 * q) * 32 + lane] + part[(2 * q + 1) * 32 + lane]) : 0.0;
     }
     __syncthreads();
+    TLG_BT(i, 3);
     // the block's own tiles, in order (all operands in shared memory)
     for (int tk = t0; tk < t1; ++tk) {
       const int k = tk - t0;
       if (warp == 0) {
         const double* li = sLi + (k * 32 + lane) * kFlowP;
-        double v = 0.0;
-#pragma unroll
-        for (int c = 0; c < 32; ++c) v = fma(li[c], bb[k * 32 + c], v);
+        const double* bk = bb + k * 32;
+        const double v = dot32x4([&](int c) { return li[c]; }, [&](int c) { return bk[c]; });
         const int rr = tk * 32 + lane;
         if (rr < n) y[rr] = v;
         bb[k * 32 + lane] = rr < n ? v : 0.0;
@@ -1029,16 +1062,17 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_fwd_flow(const double* __
       const int tr = tk + 1 + warp;
       if (tr < t1 && tr - tk <= bwt) {
         const double* tl = sT + (flow_intra(tr - t0, k) * 32 + lane) * kFlowP;
-        double a = 0.0;
-#pragma unroll
-        for (int c = 0; c < 32; ++c) a = fma(tl[c], bb[k * 32 + c], a);
+        const double* bk = bb + k * 32;
+        const double a = dot32x4([&](int c) { return tl[c]; }, [&](int c) { return bk[c]; });
         bb[(tr - t0) * 32 + lane] -= a;
       }
       __syncthreads();
     }
+    TLG_BT(i, 4);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) st_release(flag + i, epoch);
+    TLG_BT(i, 5);
   }
 }
 
@@ -1112,9 +1146,9 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_bwd_flow(const double* __
       const int k = tk - t0;
       if (warp == 0) {
         // x_tk = Linv^T z: lane c reads column c of the staged inverse
-        double a = 0.0;
-#pragma unroll
-        for (int rr = 0; rr < 32; ++rr) a = fma(sLi[(k * 32 + rr) * kFlowP + lane], bb[k * 32 + rr], a);
+        const double* lc = sLi + k * 32 * kFlowP + lane;
+        const double* bk = bb + k * 32;
+        const double a = dot32x4([&](int rr) { return lc[rr * kFlowP]; }, [&](int rr) { return bk[rr]; });
         const int c = tk * 32 + lane;
         if (c < n) x[c] = a;
         bb[k * 32 + lane] = c < n ? a : 0.0;
@@ -1122,10 +1156,9 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_bwd_flow(const double* __
       __syncthreads();
       const int tc = tk - 1 - warp;  // z_tc -= L(tk, tc)^T x_tk
       if (tc >= t0 && tk - tc <= bwt) {
-        const double* tl = sT + flow_intra(k, tc - t0) * 32 * kFlowP;
-        double a = 0.0;
-#pragma unroll
-        for (int rr = 0; rr < 32; ++rr) a = fma(tl[rr * kFlowP + lane], bb[k * 32 + rr], a);
+        const double* tl = sT + flow_intra(k, tc - t0) * 32 * kFlowP + lane;
+        const double* bk = bb + k * 32;
+        const double a = dot32x4([&](int rr) { return tl[rr * kFlowP]; }, [&](int rr) { return bk[rr]; });
         bb[(tc - t0) * 32 + lane] -= a;
       }
       __syncthreads();
