@@ -871,7 +871,8 @@ constexpr int kFlowIntra = kFlowSub * (kFlowSub - 1) / 2;  // off-diagonal tiles
 // dynamic smem: Linv tiles + intra-block L tiles ([r][c], pitch 33), the
 // block's right-hand side, per-warp partials, per-warp staged solution tiles
 constexpr size_t kFlowSmem =
-    sizeof(double) * ((kFlowSub + kFlowIntra) * 32 * kFlowP + kFlowRB + kFlowW * 32 + kFlowW * 2 * 32);
+    sizeof(double) * ((kFlowSub + kFlowIntra) * 32 * kFlowP + kFlowRB + kFlowW * 32 + kFlowW * 2 * 32 +
+                      kFlowW * 32 * kFlowP);
 
 // Flag observation: relaxed loads (an acquire load invalidates the whole L1
 // on every execution — CCTL.IVALL in the SASS), then one acquire fence once
@@ -885,12 +886,19 @@ __device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gp
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-// lane 0 waits for block `blk`, then the warp reads what it published
+// lane 0 waits for block `blk`, then the warp reads what it published. The
+// spin uses relaxed loads; the confirming load is an acquire (not a fence:
+// a fence would also wait for the lane's outstanding band-row prefetches)
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void wait_block(const int* flag, int blk, int epoch) {
   if ((threadIdx.x & 31) == 0) {
     while (ld_relaxed(flag + blk) != epoch) {
     }
-    fence_acquire();
+    (void)ld_acquire(flag + blk);
   }
   __syncwarp();
 }
@@ -917,6 +925,7 @@ __device__ __forceinline__ double warp_transpose_sum(double (&v)[32]) {
 // band-solve blocks [kBt0, kBt0 + 64)
 constexpr int kBt0 = 300;
 __device__ unsigned long long tlg_band_trace[64][8];
+__device__ unsigned long long tlg_band_trace_b[64][8];
 __device__ __forceinline__ unsigned long long gtime_b() {
   unsigned long long v;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
@@ -924,11 +933,23 @@ __device__ __forceinline__ unsigned long long gtime_b() {
 }
 #define TLG_BT(blk, slot) \
   do { if (threadIdx.x == 0 && (blk) >= kBt0 && (blk) < kBt0 + 64) tlg_band_trace[(blk) - kBt0][slot] = gtime_b(); } while (0)
+#define TLG_BTB(q, slot) \
+  do { if (threadIdx.x == 0 && (q) >= kBt0 && (q) < kBt0 + 64) tlg_band_trace_b[(q) - kBt0][slot] = gtime_b(); } while (0)
+__device__ __forceinline__ unsigned long long gtime_dep(double dep) {
+  unsigned long long v;
+  asm volatile("{\n .reg .f64 t;\n mov.f64 t, %1;\n mov.u64 %0, %globaltimer;\n}" : "=l"(v) : "d"(dep));
+  return v;
+}
+#define TLG_BTBD(q, slot, dep) \
+  do { const double _d = (dep); if (threadIdx.x == 0 && (q) >= kBt0 && (q) < kBt0 + 64) tlg_band_trace_b[(q) - kBt0][slot] = gtime_dep(_d); } while (0)
 extern "C" int tlg_debug_band_trace(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, tlg_band_trace, sizeof(tlg_band_trace)) == cudaSuccess ? 0 : 1;
+  if (cudaMemcpyFromSymbol(out, tlg_band_trace, sizeof(tlg_band_trace)) != cudaSuccess) return 1;
+  return cudaMemcpyFromSymbol(out + 64 * 8, tlg_band_trace_b, sizeof(tlg_band_trace_b)) == cudaSuccess ? 0 : 1;
 }
 #else
 #define TLG_BT(blk, slot)
+#define TLG_BTB(q, slot)
+#define TLG_BTBD(q, slot, dep)
 #endif
 
 // sum_c a[c] b[c] over 32 terms as four interleaved chains (the band
@@ -939,6 +960,21 @@ __device__ __forceinline__ double dot32x4(FA a, FB b) {
   double s[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int c = 0; c < 32; ++c) s[c & 3] = fma(a(c), b(c), s[c & 3]);
+  return (s[0] + s[1]) + (s[2] + s[3]);
+}
+
+// the same through a per-warp [32][33] shared buffer: 32 stores, 32 loads
+// (the 31-round shuffle version measured ~8 us per call inside the backward
+// band solve's critical section)
+__device__ __forceinline__ double warp_transpose_sum_smem(const double (&v)[32], double* buf) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) buf[lane * 33 + c] = v[c];
+  __syncwarp();
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int r = 0; r < 32; ++r) s[r & 3] += buf[r * 33 + lane];
+  __syncwarp();
   return (s[0] + s[1]) + (s[2] + s[3]);
 }
 
@@ -1088,6 +1124,7 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_bwd_flow(const double* __
   double* bb = sT + kFlowIntra * 32 * kFlowP;
   double* part = bb + kFlowRB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* tbuf = part + kFlowW * 32 + kFlowW * 2 * 32 + warp * 32 * kFlowP;  // transpose-sum buffer
   const int s = warp >> 1, half = warp & 1;
   const int nt = (n + 31) / 32, nb = (n + kFlowRB - 1) / kFlowRB;
   for (int q = blockIdx.x; q < nb; q += gridDim.x) {
@@ -1096,6 +1133,7 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_bwd_flow(const double* __
     const int ti = t0 + s;  // column tile of this warp's sub-tile
     const int rb = t0 * 32 + threadIdx.x;  // this block's y, loaded off the critical path
     const double yv = (threadIdx.x < kFlowRB && rb < n) ? y[rb] : 0.0;
+    TLG_BTB(q, 0);
     flow_stage(L, n, ld, bwt, linv, t0, t1, sLi, sT);
     // v[c] accumulates sum_r L(tj r, ti c) x(tj r) over this warp's tiles
     // (lane = r); one transpose-sum at the end
@@ -1125,7 +1163,9 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_bwd_flow(const double* __
 #pragma unroll
         for (int c = 0; c < 32; ++c) lv[u][c] = (tjs[u] >= 0 && r < n) ? lr[(size_t)c * ld] : 0.0;
       }
+      TLG_BTB(q, 1);
       wait_block(flag, q - 1, epoch);
+      TLG_BTB(q, 2);
 #pragma unroll
       for (int u = 0; u < 2; ++u)
         if (tjs[u] >= 0) {
@@ -1135,13 +1175,17 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_bwd_flow(const double* __
           for (int c = 0; c < 32; ++c) v[c] = fma(lv[u][c], xr, v[c]);
         }
     }
-    part[warp * 32 + lane] = warp_transpose_sum(v);
+    TLG_BTBD(q, 6, v[0] + v[31]);
+    const double vsum = warp_transpose_sum_smem(v, tbuf);
+    TLG_BTBD(q, 7, vsum);
+    part[warp * 32 + lane] = vsum;
     __syncthreads();
     if (threadIdx.x < kFlowRB) {
       const int qq = threadIdx.x >> 5, rr = t0 * 32 + threadIdx.x;
       bb[threadIdx.x] = rr < n ? yv - (part[(2 * qq) * 32 + lane] + part[(2 * qq + 1) * 32 + lane]) : 0.0;
     }
     __syncthreads();
+    TLG_BTB(q, 3);
     for (int tk = t1 - 1; tk >= t0; --tk) {
       const int k = tk - t0;
       if (warp == 0) {
@@ -1163,9 +1207,11 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_bwd_flow(const double* __
       }
       __syncthreads();
     }
+    TLG_BTB(q, 4);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) st_release(flag + q, epoch);
+    TLG_BTB(q, 5);
   }
 }
 
@@ -1317,7 +1363,7 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
       if (i == j) {
         if (t == 0) {
           spin(fl(j, j));
-          fence_acquire();
+          (void)ld_acquire(fl(j, j));
         }
         __syncthreads();
         const double* lj = linv + static_cast<size_t>(j) * 1024;
@@ -1366,7 +1412,8 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
           if (t == 0) {
             spin(fl(i, k));
             spin(xfl(k, j));
-            fence_acquire();
+            (void)ld_acquire(fl(i, k));
+            (void)ld_acquire(xfl(k, j));
           }
           __syncthreads();
           xready = max(k + 1, x_first_unready(k + 1));
@@ -1399,7 +1446,7 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
         }
         if (t == 0) {
           spin(fl(i, i));
-          fence_acquire();
+          (void)ld_acquire(fl(i, i));
         }
         // Xs[q][r] = Linv_i(r, q), Ys[q][c] = acc(q, c)
 #pragma unroll
@@ -1531,9 +1578,12 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
     auto ensure = [&](int k) {
       if (k < ready_end) return;
       if (t == 0) {
+        // acquire loads, not a fence: a fence would also wait for this
+        // thread's outstanding operand copies
         while (ld_relaxed(fl(i, k)) != epoch) __nanosleep(64);
         while (ld_relaxed(fl(j, k)) != epoch) __nanosleep(64);
-        fence_acquire();
+        (void)ld_acquire(fl(i, k));
+        (void)ld_acquire(fl(j, k));
       }
       __syncthreads();
       ready_end = max(k + 1, first_unready(k + 1));
@@ -1618,7 +1668,7 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
     } else {
       if (t == 0) {
         while (ld_relaxed(fl(j, j)) != epoch) __nanosleep(64);
-        fence_acquire();
+        (void)ld_acquire(fl(j, j));
       }
       if (i == j + 1) TLG_TR(j, 5);
       // L_ij = A_ij Linv_j^T: Xs[q][r] = A_ij(r, q), Ys[q][c] = Linv_j(c, q)
