@@ -883,6 +883,10 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
   return v;
 }
 __device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// Publication: the block's (or warp's) stores, a CTA barrier (or
+// __syncwarp), then one st.release by one thread — release is cumulative
+// over the writes ordered before it by the barrier, so no per-thread
+// __threadfence (which waited for every thread's stores to be acknowledged)
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -1105,7 +1109,6 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_fwd_flow(const double* __
       __syncthreads();
     }
     TLG_BT(i, 4);
-    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) st_release(flag + i, epoch);
     TLG_BT(i, 5);
@@ -1208,7 +1211,6 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_bwd_flow(const double* __
       __syncthreads();
     }
     TLG_BTB(q, 4);
-    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) st_release(flag + q, epoch);
     TLG_BTB(q, 5);
@@ -1488,7 +1490,6 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
               if (rr < ib && c < jb) X[(i0 + rr) + static_cast<size_t>(j0 + c) * ldx] = acc[a][b][h];
             }
       }
-      __threadfence();
       __syncthreads();
       if (t == 0) st_release(xfl(i, j), epoch);
       continue;
@@ -1652,7 +1653,6 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
         warp2b_potrf_inv32(T, kPFP, jb, linv + static_cast<size_t>(j) * 1024, info, wsh);
         if (w == 1) {
           if (lane == 0) TLG_TRW(j, 5);
-          __threadfence();
           __syncwarp();
           if (lane == 0) st_release(fl(j, j), epoch);
           if (lane == 0) TLG_TRW(j, 2);  // flag released (trace2 slot 2)
@@ -1708,7 +1708,6 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
             if (r < ib && c < jb) A[(i0 + r) + static_cast<size_t>(j0 + c) * lda] = acc[a][b][h];
           }
     }
-    __threadfence();
     __syncthreads();
     if (t == 0) st_release(fl(i, j), epoch);
     if (i == j + 1) TLG_TR(j, 6);
