@@ -1364,15 +1364,25 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
     const long long task = task_s;
     __syncthreads();
     if (task >= total_all) break;
-    if (task >= total) {
+    // with a claim-order table, entry (i, j) is factor task (i, j) and
+    // (i, -1 - j) is L^-1 task (i, j)
+    int2 oij = make_int2(0, 0);
+    if (order) oij = order[task];
+    if (order ? oij.y < 0 : task >= total) {
       // ---- X_ij = -Linv_i sum_{k = max(j, i - bwt)}^{i-1} L_ik X_kj  (X_jj = Linv_j)
       // row-major over the lower tiles: row i's tiles depend on earlier rows
       // only, so the rows form a wavefront with every column in flight
-      const long long r = task - total;
-      int i = static_cast<int>((sqrt(8.0 * static_cast<double>(r) + 1.0) - 1.0) * 0.5);
-      while (static_cast<long long>(i) * (i + 1) / 2 > r) --i;
-      while (static_cast<long long>(i + 1) * (i + 2) / 2 <= r) ++i;
-      const int j = static_cast<int>(r - static_cast<long long>(i) * (i + 1) / 2);
+      int i, j;
+      if (order) {
+        i = oij.x;
+        j = -1 - oij.y;
+      } else {
+        const long long r = task - total;
+        i = static_cast<int>((sqrt(8.0 * static_cast<double>(r) + 1.0) - 1.0) * 0.5);
+        while (static_cast<long long>(i) * (i + 1) / 2 > r) --i;
+        while (static_cast<long long>(i + 1) * (i + 2) / 2 <= r) ++i;
+        j = static_cast<int>(r - static_cast<long long>(i) * (i + 1) / 2);
+      }
       const int i0 = i * 32, j0 = j * 32, ib = min(32, n - i0), jb = min(32, n - j0);
       if (i == j) {
         if (t == 0) {
@@ -1508,9 +1518,8 @@ __global__ void __launch_bounds__(128, TLG_PF_MINB) k_potrf_flow32(double* __res
     }
     int i, j;
     if (order) {
-      const int2 ij = order[task];
-      i = ij.x;
-      j = ij.y;
+      i = oij.x;
+      j = oij.y;
     } else if (task < T0) {
       j = static_cast<int>(task / (bwt + 1));
       i = j + static_cast<int>(task % (bwt + 1));
@@ -1768,10 +1777,15 @@ void potrf_lower32(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X
     const int2* order = nullptr;
     const char* sk = std::getenv("TLG_POTRF_SKEW");
     const int skew = sk ? std::atoi(sk) : 2;
-    if (skew >= 2 && skew <= bwt) {
-      const size_t ntask = static_cast<size_t>(nt - bwt) * (bwt + 1) + static_cast<size_t>(bwt) * (bwt + 1) / 2;
+    if (skew >= 2 && skew <= std::max(bwt, 2)) {
+      // L^-1 tasks (with X) join the same order: row i's X tiles get the key
+      // just above row i's last factor task (diagonal key i S), ascending j;
+      // their dependencies (L_ik, Linv_i, X_kj for k < i) all have smaller keys
+      const size_t nfac = static_cast<size_t>(nt - bwt) * (bwt + 1) + static_cast<size_t>(bwt) * (bwt + 1) / 2;
+      const size_t ntask = nfac + (X ? static_cast<size_t>(nt) * (nt + 1) / 2 : 0);
       int2* dorder = ctx->ws<int2>(S_FLOWORDER, ntask);
-      const long long key = (static_cast<long long>(nt) << 32) ^ (static_cast<long long>(bwt) << 12) ^ skew;
+      const long long key = (static_cast<long long>(nt) << 32) ^ (static_cast<long long>(bwt) << 12) ^
+                            (skew << 1) ^ (X ? 1 : 0);
       if (ctx->flow_order_key != key) {
         std::vector<int2>& host = ctx->flow_order_host;
         host.clear();
@@ -1783,6 +1797,11 @@ void potrf_lower32(tlg_ctx* ctx, double* A, int n, int lda, int* info, double* X
           for (long long jj = jlo; jj <= jhi; ++jj) {
             const long long ii = jj + (K - jj * skew);
             if (ii < nt) host.push_back(make_int2(static_cast<int>(ii), static_cast<int>(jj)));
+          }
+          // X row i after its diagonal task (key i S)
+          if (X && K % skew == 0 && K / skew < nt) {
+            const int ii = static_cast<int>(K / skew);
+            for (int jj = 0; jj <= ii; ++jj) host.push_back(make_int2(ii, -1 - jj));
           }
         }
         require(host.size() == ntask, TLG_RUNTIME_ERROR, "potrf: task order size");
