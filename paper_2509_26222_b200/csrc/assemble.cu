@@ -25,6 +25,8 @@
 #include <cub/cub.cuh>
 #include <math_constants.h>
 
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace tlg {
@@ -397,10 +399,15 @@ bool lattice_gram_device(tlg_model* m, const double* x, const double* y, const d
   const int win = LG.win;
   const LatticeView L = lattice_view(m);
   const size_t nn = static_cast<size_t>(LG.ni) * LG.nj;
-  // the per-cell blocks pay off from ~8 observations per lattice cell (a
-  // dense scan, C5: ~90); sparse batches (C3: ~3 per cell) keep the row-wise
-  // CSR Gram, whose cost does not carry the fixed per-cell work
-  if (mm < 8 * nn) return false;
+  // the per-cell blocks carry a fixed per-cell cost (the window Gram flush);
+  // measured at C3 m = 20,000 (~5 observations per cell) they still beat the
+  // row-wise CSR Gram (0.53 vs 0.63 ms), so only batches below ~2 per cell
+  // keep the CSR path (env TLG_LAT_MIN_PER_CELL overrides)
+  static const int min_per_cell = [] {
+    const char* e = std::getenv("TLG_LAT_MIN_PER_CELL");
+    return e ? std::atoi(e) : 2;
+  }();
+  if (mm < static_cast<size_t>(min_per_cell) * nn) return false;
   const int ko = win * (2 * win - 1);
   // column segments: >= 4 CTAs per SM in all, each >= WIN cells long (same-
   // parity segments of one column then never share a node window)
