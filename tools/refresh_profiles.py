@@ -30,7 +30,7 @@ def batch_fit_summary(rep, dst):
             "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
             "launch__grid_size", "lts__t_sector_hit_rate.pct"]
     lines = ["ncu --set full --clock-control none, one launch each (C5 batch ridge: 10^7 points,",
-             "99,856 lattice centres, band ld 3424) of python tools/time_batch_c5.py", ""]
+             "99,856 lattice centres, band ld 2912) of python tools/time_batch_c5.py", ""]
     for row in raw[2:]:
         d = dict(zip(hdr, row))
         name = d.get("Kernel Name", "")[:60]
