@@ -318,7 +318,12 @@ void gemm_grouped(tlg_ctx* ctx, const GemmDesc* d_descs, int count, int max_m, i
   const int kslice = ((max_k + splits - 1) / splits + TK - 1) / TK * TK;
   const int ldp = tm * TM;
   const size_t pstride = static_cast<size_t>(ldp) * tn * TN;
-  double* part = ctx->ws<double>(S_GRAMPART, pstride * count * splits);
+  // own slot, sized for ~4 CTAs per SM of partial tiles plus one per tile
+  // (tiles x splits never exceeds that): it does not regrow when the block
+  // count shifts between scans (a regrowth is a cudaFree + cudaMalloc pair,
+  // measured at up to tens of ms mid-stream)
+  const size_t cap = static_cast<size_t>(4ll * ctx->num_sms + tiles) * TM * TN;
+  double* part = ctx->ws<double>(S_GGPART, std::max(cap, pstride * count * splits));
   dim3 grid(tm, tn, count * splits);
   k_gemm_grouped_splitk<<<grid, 128, 0, ctx->stream>>>(d_descs, splits, kslice, part, ldp, pstride);
   TLG_LAUNCHED(ctx);
@@ -1300,7 +1305,7 @@ __global__ void __launch_bounds__(128) k_trsm_tiles(const double* __restrict__ L
 // -> last update of (j, j) -> POTRF(j), while the bulk of the updates runs
 // ahead of it.
 #ifndef TLG_PF_MINB
-#define TLG_PF_MINB 4
+#define TLG_PF_MINB 3
 #endif
 #ifdef TLG_FLOW_TRACE
 // Diagnostics build only (tools/flow_trace.py): globaltimer stamps of the

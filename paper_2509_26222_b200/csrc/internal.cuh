@@ -105,7 +105,7 @@ enum Slot : int {
   S_COUNT, S_ACTIVE, S_BLOCKFLAG, S_ROWOF, S_MERGED, S_ROWPTR, S_COLIDX, S_MTVAL,
   S_KMAT, S_SMAT, S_RESID, S_U, S_YMAT, S_HMAT, S_WORK1, S_WORK2, S_WORK3, S_BLKTAB,
   S_MOMENT_ROW, S_TROWP, S_TKEYS, S_LINV, S_XINV, S_XINV2, S_SOLVE, S_BSOLVE, S_VALIDATE,
-  S_GRAMPART, S_LATGRAM, S_LATSTART, S_LATPTS, S_LATNROW, S_FLOWFLAG, S_GEMVPART, S_REDSEG, S_FLOWORDER,
+  S_GRAMPART, S_LATGRAM, S_LATSTART, S_LATPTS, S_LATNROW, S_FLOWFLAG, S_GEMVPART, S_REDSEG, S_FLOWORDER, S_GGPART,
   S_NUM_SLOTS
 };
 

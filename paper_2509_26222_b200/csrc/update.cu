@@ -1264,6 +1264,7 @@ void recursive_update_device(tlg_model* m, const double* x, const double* y, con
     maxk = std::max(maxk, dq.K);
     plain = plain && dq.uplo == 0;
   }
+  tr.mark("descs");
   gemm_grouped(ctx, d_descs, nq, maxq, maxq, plain ? maxk : 0);
   tr.mark("blocks");
   {
