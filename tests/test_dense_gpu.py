@@ -35,7 +35,10 @@ def test_potrf_and_inverse(gpu_ctx, n, tile):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,band", [(300, 40), (1500, 200), (2000, 31), (700, 699)])
+# band 0: 32-wide diagonal blocks only (bwt = 0, no claim-order table); the
+# others cover one-tile bands, ragged last tiles and the dense limit under
+# the anti-diagonal task order with the interleaved L^-1 tasks
+@pytest.mark.parametrize("n,band", [(300, 40), (1500, 200), (2000, 31), (700, 699), (200, 0), (95, 40), (1000, 5), (4100, 130)])
 def test_potrf_banded(gpu_ctx, n, band):
     # block-banded SPD matrix (the information-form structure): the banded
     # factorisation must equal the dense one, and X = L^-1 stays exact
