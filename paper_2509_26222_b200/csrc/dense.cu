@@ -1043,7 +1043,7 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_fwd_flow(const double* __
     TLG_BT(i, 0);
     flow_stage(L, n, ld, bwt, linv, t0, t1, sLi, sT);
     // blocks <= i-2 (published earlier): tiles of the row's band, oldest first
-    const int tlo = max(0, ti - bwt), tcrit = max(0, t0 - kFlowSub);
+    const int tlo = max(0, ti - bwt), tcrit = max(0, t0 - 2 * kFlowSub);
     double acc = 0.0;
     for (int tj = tlo + half; tj < tcrit; tj += 2) {
       wait_block(flag, tj / kFlowSub, epoch);
@@ -1059,26 +1059,28 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_fwd_flow(const double* __
       }
       __syncwarp();
     }
-    // block i-1 (the critical hand-off): its tiles' rows are loaded before
-    // the wait, so only the products follow it
-    if (i > 0) {
+    // blocks i-2 and i-1 (the last two hand-offs): each block's tile rows are
+    // loaded before its wait (the waits are acquire loads, which do not wait
+    // for them), so only the y loads and the products follow a flag
+    auto crit_block = [&](int blk) {
+      const int tb = blk * kFlowSub;
       double lv[2][32];
       int tjs[2];
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const int tj = tcrit + half + 2 * u;
+        const int tj = tb + half + 2 * u;
         tjs[u] = (tj < t0 && tj >= tlo && row_ok) ? tj : -1;
         const double* lr = L + (row_ok ? r : 0) + (size_t)max(tj, 0) * 32 * ld;
 #pragma unroll
         for (int c = 0; c < 32; ++c) lv[u][c] = tjs[u] >= 0 ? lr[(size_t)c * ld] : 0.0;
       }
-      TLG_BT(i, 1);
-      wait_block(flag, i - 1, epoch);
-      TLG_BT(i, 2);
+      if (blk == i - 1) TLG_BT(i, 1);
+      wait_block(flag, blk, epoch);
+      if (blk == i - 1) TLG_BT(i, 2);
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const int tj = tcrit + half + 2 * u;
-        ys[(warp * 2 + u) * 32 + lane] = tj < t0 ? __ldcg(y + tj * 32 + lane) : 0.0;
+        const int tj = tb + half + 2 * u;
+        ys[(warp * 2 + u) * 32 + lane] = (tj < t0 && tj >= tlo) ? __ldcg(y + tj * 32 + lane) : 0.0;
       }
       __syncwarp();
 #pragma unroll
@@ -1087,7 +1089,10 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_fwd_flow(const double* __
           const double* yw = ys + (warp * 2 + u) * 32;
           acc += dot32x4([&](int c) { return lv[u][c]; }, [&](int c) { return yw[c]; });
         }
-    }
+      __syncwarp();
+    };
+    if (i > 1) crit_block(i - 2);
+    if (i > 0) crit_block(i - 1);
     part[warp * 32 + lane] = acc;
     __syncthreads();
     if (threadIdx.x < kFlowRB) {
@@ -1153,8 +1158,8 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_bwd_flow(const double* __
 #pragma unroll
     for (int c = 0; c < 32; ++c) v[c] = 0.0;
     const int thi = ti < t1 ? min(nt - 1, ti + bwt) : -1;  // last tile of the column's band
-    const int tcrit = t1 + kFlowSub;                        // tiles of block i+1: [t1, tcrit)
-    // blocks >= i+2, oldest (farthest) first
+    const int tcrit = t1 + 2 * kFlowSub;                    // tiles of blocks i+1, i+2: [t1, tcrit)
+    // blocks >= i+3, oldest (farthest) first
     for (int tj = thi - half; tj >= tcrit; tj -= 2) {
       wait_block(flag, nb - 1 - tj / kFlowSub, epoch);
       const int r = tj * 32 + lane;
@@ -1163,30 +1168,37 @@ __global__ void __launch_bounds__(kFlowThreads) k_band_bwd_flow(const double* __
 #pragma unroll
       for (int c = 0; c < 32; ++c) v[c] = fma(r < n ? lr[(size_t)c * ld] : 0.0, xr, v[c]);
     }
-    if (i + 1 < nb) {
+    // blocks i+2 and i+1 (the last two hand-offs): tile rows loaded before
+    // each block's wait, then the x loads and the products
+    auto crit_block = [&](int bi) {
+      const int tb = bi * kFlowSub;
       double lv[2][32];
       int tjs[2];
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const int tj = t1 + half + 2 * u;
+        const int tj = tb + half + 2 * u;
         const int r = tj * 32 + lane;
-        tjs[u] = (tj <= thi && tj < tcrit) ? tj : -1;
+        tjs[u] = (tj <= thi && tj < tb + kFlowSub && tj < nt) ? tj : -1;
         const double* lr = L + min(max(r, 0), n - 1) + (size_t)max(ti, 0) * 32 * ld;
 #pragma unroll
         for (int c = 0; c < 32; ++c) lv[u][c] = (tjs[u] >= 0 && r < n) ? lr[(size_t)c * ld] : 0.0;
       }
-      TLG_BTB(q, 1);
-      wait_block(flag, q - 1, epoch);
-      TLG_BTB(q, 2);
+      if (bi == i + 1) TLG_BTB(q, 1);
+      wait_block(flag, nb - 1 - bi, epoch);
+      if (bi == i + 1) TLG_BTB(q, 2);
+      double xr[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int r = tjs[u] * 32 + lane;
+        xr[u] = (tjs[u] >= 0 && r < n) ? __ldcg(x + r) : 0.0;
+      }
 #pragma unroll
       for (int u = 0; u < 2; ++u)
-        if (tjs[u] >= 0) {
-          const int r = tjs[u] * 32 + lane;
-          const double xr = r < n ? __ldcg(x + r) : 0.0;
 #pragma unroll
-          for (int c = 0; c < 32; ++c) v[c] = fma(lv[u][c], xr, v[c]);
-        }
-    }
+        for (int c = 0; c < 32; ++c) v[c] = fma(lv[u][c], xr[u], v[c]);
+    };
+    if (i + 2 < nb) crit_block(i + 2);
+    if (i + 1 < nb) crit_block(i + 1);
     TLG_BTBD(q, 6, v[0] + v[31]);
     const double vsum = warp_transpose_sum_smem(v, tbuf);
     TLG_BTBD(q, 7, vsum);
