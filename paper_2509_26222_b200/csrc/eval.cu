@@ -661,7 +661,8 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const double* __r
                                                                const int* __restrict__ err,
                                                                double* __restrict__ out,
                                                                double* __restrict__ seg_part,
-                                                               unsigned* __restrict__ arrive) {
+                                                               unsigned* __restrict__ arrive,
+                                                               double* __restrict__ host_out) {
   __shared__ double sh[kRedThreads];
   __shared__ bool last;
   const int entry = blockIdx.x / kRedSeg, seg = blockIdx.x % kRedSeg;
@@ -694,9 +695,22 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_chunks(const double* __r
     double s = 0.0;
     for (int k = 0; k < kRedSeg; ++k) s += __ldcg(seg_part + entry * kRedSeg + k);
     out[entry] = s;
+    if (host_out) host_out[entry] = s;  // mapped pinned memory: no D2H copy
     arrive[entry] = 0u;  // ready for the next call
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) out[kNE] = err[0] ? 1.0 : 0.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out[kNE] = err[0] ? 1.0 : 0.0;
+    if (host_out) host_out[kNE] = out[kNE];
+  }
+}
+
+// Device view of the context's pinned staging buffer (written directly by
+// the reduction: one fewer copy-engine round trip per call)
+static double* mapped(double* h) {
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, h, 0) == cudaSuccess) return static_cast<double*>(d);
+  (void)cudaGetLastError();  // not mapped: fall back to the copy, clear the error
+  return nullptr;
 }
 
 void manifold_device(tlg_model* m, const double R[9], const double t[3], const double* hx,
@@ -735,10 +749,11 @@ void manifold_device(tlg_model* m, const double R[9], const double t[3], const d
                         err)));
   TLG_LAUNCHED(ctx);
   prof_mark_end(ctx);
+  double* hd = mapped(h);
   k_reduce_chunks<<<kNE * kRedSeg, kRedThreads, 0, ctx->stream>>>(partials, nchunks, err, out,
-                                                                   seg_part, arrive);
+                                                                   seg_part, arrive, hd);
   TLG_LAUNCHED(ctx);
-  TLG_CUDA(cudaMemcpyAsync(h, out, (kNE + 1) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  if (!hd) TLG_CUDA(cudaMemcpyAsync(h, out, (kNE + 1) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   TLG_CUDA(cudaStreamSynchronize(ctx->stream));
   prof_collect(ctx);
   if (h[kNE] != 0.0) throw Error(TLG_DOMAIN_ERROR, "non-finite query");
@@ -808,10 +823,11 @@ void manifold_device_streamed(tlg_model* m, const double R[9], const double t[3]
                           nchunks, off / kRowsPerChunk, n, err)));
     TLG_LAUNCHED(ctx);
   }
+  double* hd = mapped(h);
   k_reduce_chunks<<<kNE * kRedSeg, kRedThreads, 0, s>>>(partials, nchunks, err, out, seg_part,
-                                                         arrive);
+                                                         arrive, hd);
   TLG_LAUNCHED(ctx);
-  TLG_CUDA(cudaMemcpyAsync(h, out, (kNE + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (!hd) TLG_CUDA(cudaMemcpyAsync(h, out, (kNE + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
   TLG_CUDA(cudaStreamSynchronize(s));
   if (h[kNE] != 0.0) throw Error(TLG_DOMAIN_ERROR, "non-finite query");
   if (ne) {
