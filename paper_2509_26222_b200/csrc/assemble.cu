@@ -258,20 +258,31 @@ __global__ void __launch_bounds__(32 * LatGeo<WIN>::kWarps, 2) k_gram_lattice(
     // software pipeline: step b builds F block b (every warp, its own points:
     // the y factors, a __syncwarp, the row segments) while the DMMA warps
     // multiply F block b - 1; one barrier per block
+    // this lane's point of the next batch, loaded one batch ahead
+    const int p_lane = w * G::kPPW + pl;
+    double nx = 0.0, ny = 0.0, nz = 0.0;
+    uint32_t nm = 0;
+    auto fetch_pt = [&](int bb) {
+      const uint32_t pb = p_beg + static_cast<uint32_t>(bb) * kB;
+      const int cnt = static_cast<int>(min(static_cast<uint32_t>(kB), p_end - pb));
+      if (lane_on && p_lane < cnt) {
+        nx = xs[pb + p_lane];
+        ny = ys[pb + p_lane];
+        nm = ms[pb + p_lane];
+        if (r == 0) nz = zs[pb + p_lane];
+      }
+    };
+    fetch_pt(0);
     for (int b = 0; b <= nb; ++b) {
       if (b < nb) {
         const uint32_t pb = p_beg + static_cast<uint32_t>(b) * kB;
         const int cnt = static_cast<int>(min(static_cast<uint32_t>(kB), p_end - pb));
         double* F = Fbuf + (b & 1) * G::kRows * G::kFP;
-        const int p = w * G::kPPW + pl;  // batch point of this lane
+        const int p = p_lane;  // batch point of this lane
         const bool live = lane_on && p < cnt;
-        double px = 0.0, py = 0.0;
-        uint32_t msk = 0;
-        if (live) {
-          px = xs[pb + p];
-          py = ys[pb + p];
-          msk = ms[pb + p];
-        }
+        const double px = nx, py = ny, pz = nz;
+        const uint32_t msk = nm;
+        if (b + 1 < nb) fetch_pt(b + 1);
         if (lane_on) {  // y factor of window row r for this point
           double e = 0.0, d2 = CUDART_INF;
           if (live) {
@@ -302,7 +313,7 @@ __global__ void __launch_bounds__(32 * LatGeo<WIN>::kWarps, 2) k_gram_lattice(
                 if (((inm >> l) & 1u) || __dadd_rn(dx2, wdy2[l]) <= r2) v = ex * wey[l];
               row[l] = v;
             }
-            if (r == 0) row[G::kF] = zs[pb + p];
+            if (r == 0) row[G::kF] = pz;
           } else {
 #pragma unroll
             for (int l = 0; l < WIN; ++l) row[l] = 0.0;
